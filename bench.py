@@ -1,0 +1,341 @@
+"""bench.py — scored targets/sec of the MTFM forward (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1], "MTFM-small"): d=256, 8 Q / 2 KV heads,
+(3:1)x1 HTA stack (4 layers), 1024 users per GPU x (2 x 224 historical + 64
+realtime) context tokens + 4 scenarios x 8 targets, synthetic data, random
+weights, bf16 tensor cores. One step = one forward over the whole batch:
+planning -> tokenizer -> 4 HTA layers -> MMoE heads -> records.
+
+value : targets/s over all ranks, batch resident in HBM, CUDA events on the
+        library stream around exactly K steps, max over ranks (weak scaling:
+        every rank scores its own 1024 users; no collective on the data path).
+e2e   : the same metric through mtfm_cuda_forward with pinned host buffers:
+        H2D of the packed batch, the forward, D2H of the records, every step.
+roofline: the dominant stage of a profiled step (CUDA events around each
+        stage, same stream), algorithmic FLOPs / its duration
+        vs MEASURED_PEAKS.json.
+cpu_baseline: the reference CPU path (oracle/_ref/ref_bench, compiled from the
+        unmodified reference sources) on this host's cores, bounded sample.
+
+--impl reference runs only the reference CPU path (rank 0; other ranks exit).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+REF_BENCH = os.path.join(ROOT, "oracle", "_ref", "ref_bench")
+
+CONFIGS = {
+    # name: (datagen workload, ref_bench flags of the same shape)
+    "small": ("small", ["--d", "256", "--blocks", "1", "--K", "3", "--P", "1", "--H", "8", "--G", "2",
+                        "--dexp", "256", "--lenmin", "224", "--lenmax", "224", "--rlen", "64",
+                        "--expmin", "8", "--expmax", "8"]),
+    "large": ("large", ["--d", "1024", "--blocks", "4", "--K", "3", "--P", "1", "--H", "16", "--G", "4",
+                        "--dexp", "1024", "--lenmin", "896", "--lenmax", "896", "--rlen", "256",
+                        "--expmin", "32", "--expmax", "32"]),
+}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("hbm_gbs", 6650.0), d.get("bf16_tflops", 1590.0), d.get("bf16_tflops_sustained", 1400.0), \
+            "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and "Active" in r[3 + i]
+                          and "Not" not in r[3 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_baseline(cfg_name, threads, users, reps=2):
+    flags = CONFIGS[cfg_name][1]
+    if not os.path.exists(REF_BENCH):
+        return None
+    cmd = [REF_BENCH, *flags, "--users", str(users), "--threads", str(threads), "--reps", str(reps), "--gseed", "3"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    if out.returncode != 0:
+        return {"error": out.stderr.strip()[-200:]}
+    lines = [json.loads(x) for x in out.stdout.strip().splitlines() if x.startswith("{")]
+    best = max(lines, key=lambda r: r["targets_per_sec"])
+    best["per_rep"] = [r["targets_per_sec"] for r in lines]
+    return best
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    users = args.ref_users
+    t0 = time.time()
+    rows = []
+    for _ in range(args.warmup + args.steps):
+        r = cpu_baseline(args.config, threads, users, reps=1)
+        if r is None or "error" in (r or {}):
+            print(json.dumps({"impl": "reference", "unavailable": f"oracle/_ref/ref_bench missing or failed: {r}"}))
+            return
+        rows.append(r)
+    timed = rows[args.warmup:]
+    secs = sum(r["seconds"] for r in timed)
+    targets = sum(r["targets"] for r in timed)
+    value = targets / secs
+    line = {
+        "impl": "reference", "metric": "scored targets/sec (device-timed)", "value": value, "unit": "targets/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * secs / len(timed),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"MTFM-{args.config}", "users_per_step": users, "threads": threads,
+                   "note": "reference Model<float>::forward_sample striped over std::thread workers "
+                           "(train.hpp:157-170), compiled from the unmodified reference sources"},
+        "cpu_baseline": {"value": value, "unit": "targets/s", "cores": threads, "kind": "reference",
+                         "sample": f"{users} users x {args.steps} steps of the {args.config} shape"},
+        "e2e": {"value": value, "unit": "targets/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": time.time() - t0,
+    }
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="small", choices=sorted(CONFIGS))
+    ap.add_argument("--users", type=int, default=None, help="users per GPU (default: the config's)")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--ref-users", type=int, default=96)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-json", default=None)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2602_11235_b200 import Model, abi, datagen
+    from paper_2602_11235_b200.schema import BATCH_KEYS, batch_nbytes
+
+    wl = datagen.WORKLOADS[CONFIGS[args.config][0]]()
+    wl.seed = wl.seed + 1000 * rank  # every rank scores its own users (weak scaling)
+    batch = datagen.generate(wl, n_users=args.users)
+    model = Model(wl.schemas, wl.cfg, precision="bf16", device=local)
+    model.set_params(datagen.random_params(model.param_specs(), seed=7))
+    n_targets = int(len(batch["exp_ts"]))
+    n_tokens = int(len(batch["ev_ts"])) + n_targets
+
+    stream = torch.cuda.ExternalStream(model.stream_handle(), device=torch.device("cuda", local))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    # ---------------- device-timed headline (batch resident in HBM)
+    pb = model.prepare(batch)
+    for _ in range(args.warmup):
+        pb.run()
+    res = pb.results()
+    stats = model.last_stats()
+    launches_per_step = int(stats.kernel_launches)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            pb.run()
+        ev1.record(stream)
+        ev1.synchronize()
+        # keep the sampler alive over a short tail so a fast region still gets samples
+        t_end = time.time() + 0.3
+        while time.time() < t_end and len(clk.rows) < 3:
+            pb.run()
+            torch.cuda.synchronize()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    barrier()
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = n_targets * world / (ms / 1000.0)
+
+    # ---------------- profiled step: per-stage device times (roofline)
+    model.set_profiling(True)
+    pb.run()
+    pb.results()
+    prof = model.profile()
+    model.set_profiling(False)
+    stages = {}
+    for name, sms, fl, by in prof:
+        s = stages.setdefault(name, [0.0, 0.0, 0.0, 0])
+        s[0] += sms
+        s[1] += fl
+        s[2] += by
+        s[3] += 1
+    total_prof = sum(v[0] for v in stages.values())
+    top = max(stages.items(), key=lambda kv: kv[1][0])
+    hbm, tflops, tflops_sus, peak_kind = load_peaks()
+    tname, (tms, tfl, tby, tcnt) = top
+    if tfl > 0:
+        achieved = tfl / (tms / 1000.0) / 1e12
+        roof = {"bound": "tensor", "kernel": tname, "achieved": achieved, "peak": tflops, "unit": "TFLOP/s",
+                "frac": achieved / tflops, "traffic": None, "launches": tcnt,
+                "per_launch_ms": tms / tcnt, "algorithmic_per_launch": tfl / tcnt,
+                "share_of_step": tms / total_prof, "peak_kind": peak_kind}
+    else:
+        achieved = tby / (tms / 1000.0) / 1e9
+        roof = {"bound": "hbm", "kernel": tname, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": None, "launches": tcnt, "per_launch_ms": tms / tcnt,
+                "algorithmic_per_launch": tby / tcnt, "share_of_step": tms / total_prof, "peak_kind": peak_kind}
+    total_flops = sum(v[1] for v in stages.values())
+    step_tflops = total_flops / (ms / 1000.0) / 1e12
+    traffic_path = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(traffic_path):
+        try:
+            with open(traffic_path) as f:
+                tr = json.load(f).get(args.config, {}).get(tname)
+            if tr:
+                roof["traffic"] = tr
+        except Exception:
+            pass
+
+    # ---------------- e2e through the C ABI, pinned host buffers
+    pinned = {}
+    for k in BATCH_KEYS:
+        a = np.ascontiguousarray(batch[k])
+        t = torch.empty(a.shape, dtype={np.dtype(np.int32): torch.int32, np.dtype(np.int64): torch.int64,
+                                        np.dtype(np.uint8): torch.uint8}[a.dtype], pin_memory=True)
+        t.numpy()[...] = a
+        pinned[k] = t.numpy()
+    h2d = batch_nbytes(pinned)
+    e2e_times = []
+    for i in range(args.e2e_steps + 1):
+        barrier()
+        t0 = time.perf_counter()
+        ra = model.forward_batch(pinned)
+        t1 = time.perf_counter()
+        if i > 0:
+            e2e_times.append(t1 - t0)
+    e2e_s = float(np.median(e2e_times))
+    if dist is not None:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    d2h = len(ra) * (8 + 4 + 4 + 4 + 4 + 8)
+    e2e_value = n_targets * world / e2e_s
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        threads = os.cpu_count() or 1
+        cb = cpu_baseline(args.config, threads, args.ref_users, reps=2)
+        if cb and "error" not in cb:
+            cpu = {"value": cb["targets_per_sec"], "unit": "targets/s", "cores": threads, "kind": "reference",
+                   "sample": f"{cb['users']} users of the {args.config} shape ({cb['targets']} targets, best of 2 "
+                             f"reps), reference Model<float>::forward_sample on std::thread workers"}
+        else:
+            cpu = {"value": None, "unit": "targets/s", "cores": threads, "kind": "reference",
+                   "sample": f"unavailable: {cb}"}
+    clocks = clk.summary()
+    line = {
+        "metric": "scored targets/sec (device-timed)", "value": value, "unit": "targets/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": f"MTFM-{args.config}", "users_per_gpu": int(len(batch["user_id"])),
+                   "tokens_per_gpu": n_tokens, "targets_per_gpu": n_targets,
+                   "layers": f"({wl.cfg.hta.target_layers}:{wl.cfg.hta.full_layers})x{wl.cfg.hta.blocks}",
+                   "d_model": wl.cfg.hta.d_model, "heads": wl.cfg.hta.heads, "kv_heads": wl.cfg.hta.kv_heads,
+                   "parallelism": f"users sharded, {world} GPU(s), no data-path collective",
+                   "l2": "inputs/activations > L2 (X alone is %.0f MB)" % (n_tokens * wl.cfg.hta.d_model * 4 / 1e6)},
+        "e2e": {"value": e2e_value, "unit": "targets/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": e2e_s * 1000},
+        "gpu_launches": launches_per_step * args.steps,
+        "roofline": roof,
+        "step_tflops": step_tflops,
+        "step_frac_of_bf16_peak": step_tflops / tflops,
+        "stages_ms": {k: round(v[0], 4) for k, v in sorted(stages.items(), key=lambda kv: -kv[1][0])},
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+    }
+    print(json.dumps(line))
+    if args.profile_json:
+        with open(args.profile_json, "w") as f:
+            json.dump({"stages": stages, "prof": prof}, f, indent=1)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,208 @@
+/* mtfm_cuda.h — C ABI of the B200-native MTFM forward (libmtfm_cuda.so).
+ *
+ * Drop-in boundary for the reference's batched scoring path. Every entry point
+ * replaces one piece of the reference C++ model API (paths relative to
+ * /root/reference/proj):
+ *
+ *   mtfm_cuda_create        Model<Real>::build with the structs of
+ *                           include/mtfm/model_config.hpp:39-88 (HTAConfig,
+ *                           ModelConfig) and the SchemaSet of model.hpp:117-136.
+ *   mtfm_cuda_set_param     ParamStore<Real>::at(name).value (params.hpp:22-132):
+ *                           names and (rows, cols) exactly as registered by
+ *                           Model::register_params (model.hpp:371-463).
+ *   mtfm_cuda_forward       Model<Real>::forward_sample / forward_with /
+ *                           forward_scoped (model.hpp:244-312) applied to every
+ *                           UserSample of a packed batch; records come back in
+ *                           exactly the order of the concatenated per-sample
+ *                           forward_sample results (records.hpp:10-19).
+ *   mtfm_cuda_batch_*       the same forward split into prepare / run /
+ *                           results so callers can keep batches resident in
+ *                           HBM and time the device work alone.
+ *   mtfm_cuda_last_error    the what() of the exception the reference throws;
+ *                           the status code names its type (errors.hpp:9-40).
+ *
+ * Input: a packed jagged batch of UserSamples (schema.hpp:72-98) as flat CSR
+ * arrays (no sorting is done by the caller; token planning runs on the GPU):
+ *   users      user_id[n_users]; seq_off[n_users+1] -> sequences;
+ *              exp_off[n_users+1] -> exposures
+ *   sequences  seq_kind[s] (0 historical, 1 realtime), seq_schema[s],
+ *              ev_off[n_seqs+1] -> events. A user's sequences keep the
+ *              sample's list order (historical list, then realtime list).
+ *   events     ev_ts[e], ev_feat_off[n_events+1] -> ev_feats (item_features)
+ *   exposures  exp_scenario[x], exp_ts[x], exp_blk[3x..3x+2] = number of
+ *              user/cross/item ids, exp_feat_off[n_exposures+1] -> exp_feats
+ *              (user ids, then cross ids, then item ids)
+ * Offsets are int32 (a batch holds < 2^31 events / feature ids).
+ *
+ * Output: one record per (T token, task of its scenario) in reference order:
+ * user-major, then scenario id ascending, then task order, then the T tokens'
+ * canonical (timestamp, scenario, index) order (heads.hpp:54-97,
+ * model.hpp:284-311). probability = clamp(sigmoid(logit), 1e-12, 1-1e-12).
+ * Labels are host-side data and are not part of the device path.
+ *
+ * Threading: one model handle per device, bound to one CUDA stream, not
+ * re-entrant per handle (the reference forward is const and re-entrant; use
+ * one handle per host thread / device).
+ */
+#ifndef MTFM_CUDA_H_
+#define MTFM_CUDA_H_
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define MTFM_API __attribute__((visibility("default")))
+#else
+#define MTFM_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    MTFM_OK = 0,
+    MTFM_CONFIG_ERROR = 1,    /* config_error    errors.hpp:10 */
+    MTFM_INTEGRITY_ERROR = 2, /* integrity_error errors.hpp:15 */
+    MTFM_DIMENSION_ERROR = 3, /* dimension_error errors.hpp:20 */
+    MTFM_PARSE_ERROR = 4,     /* parse_error     errors.hpp:25 */
+    MTFM_LOOKUP_ERROR = 5,    /* lookup_error    errors.hpp:33 */
+    MTFM_CONTRACT_ERROR = 6,  /* contract_error  errors.hpp:38 */
+    MTFM_CUDA_ERROR = 7       /* device / driver failure (no reference analogue) */
+} mtfm_status;
+
+/* AttnNorm, model_config.hpp:18 */
+typedef enum { MTFM_NORM_VALID = 0, MTFM_NORM_SEQLEN = 1, MTFM_NORM_NONE = 2 } mtfm_attn_norm;
+
+typedef enum {
+    MTFM_PRECISION_BF16 = 0,      /* tcgen05 bf16 tensor cores, fp32 accumulate / residual */
+    MTFM_PRECISION_FP32_CHECK = 1 /* fp32 SIMT everywhere: the <=1e-4 parity mode */
+} mtfm_precision;
+
+/* ModelConfig + HTAConfig, model_config.hpp:39-88 */
+typedef struct {
+    int32_t d_model, blocks, target_layers, full_layers, heads, kv_heads;
+    int32_t norm; /* mtfm_attn_norm */
+    double eps;
+    int32_t d_emb, experts, d_expert;
+} mtfm_model_desc;
+
+/* SchemaSet (model.hpp:117-136) flattened: SequenceSchema / ScenarioSchema
+ * (schema.hpp:18-41) in registration order. */
+typedef struct {
+    int32_t n_hist;
+    const int32_t* hist_ids;    /* [n_hist] seq_id */
+    const int32_t* hist_nslots; /* [n_hist] */
+    const int32_t* hist_vocabs; /* concatenated feature_vocabs */
+    int32_t n_rt;
+    const int32_t* rt_ids;
+    const int32_t* rt_nslots;
+    const int32_t* rt_vocabs;
+    int32_t n_scen;
+    const int32_t* scen_ids;    /* [n_scen] scenario_id */
+    const int32_t* scen_nu;     /* user / cross / item slot counts */
+    const int32_t* scen_nc;
+    const int32_t* scen_ni;
+    const int32_t* scen_vocabs; /* per scenario: user, cross, item vocabs */
+    const int32_t* scen_ntasks; /* [n_scen] */
+    const char* const* task_names; /* concatenated task names, scenario order */
+} mtfm_schema_desc;
+
+typedef struct {
+    int32_t n_users, n_seqs, n_events, n_exposures;
+    int64_t n_ev_feats, n_exp_feats;
+    const int64_t* user_id;
+    const int32_t* seq_off;
+    const uint8_t* seq_kind;
+    const int32_t* seq_schema;
+    const int32_t* ev_off;
+    const int64_t* ev_ts;
+    const int32_t* ev_feat_off;
+    const int32_t* ev_feats;
+    const int32_t* exp_off;
+    const int32_t* exp_scenario;
+    const int64_t* exp_ts;
+    const int32_t* exp_feat_off;
+    const int32_t* exp_blk;
+    const int32_t* exp_feats;
+} mtfm_packed_batch;
+
+/* Caller-owned record buffers (capacity >= mtfm_cuda_count_records()). */
+typedef struct {
+    int64_t capacity;
+    int64_t n_records;        /* written */
+    int64_t* user_id;         /* PredictionRecord::user_id */
+    int32_t* scenario_id;     /* PredictionRecord::scenario_id */
+    int32_t* exposure_index;  /* PredictionRecord::exposure_index */
+    int32_t* task_index;      /* index into the scenario's task list */
+    float* logit;             /* pre-sigmoid head output (may be NULL) */
+    double* probability;      /* PredictionRecord::probability */
+} mtfm_records;
+
+typedef struct mtfm_cuda_model mtfm_cuda_model;
+typedef struct mtfm_cuda_batch mtfm_cuda_batch;
+
+typedef struct {
+    int64_t kernel_launches;     /* kernels enqueued by the last run */
+    double algorithmic_flops;    /* SURVEY 8(d) FLOP model of the last run */
+    double attention_flops;      /* mask-aware attention part of it */
+    int64_t tokens, targets, records;
+} mtfm_run_stats;
+
+MTFM_API const char* mtfm_cuda_last_error(void);
+MTFM_API const char* mtfm_cuda_version(void);
+
+MTFM_API mtfm_status mtfm_cuda_create(int device, const mtfm_model_desc* model, const mtfm_schema_desc* schemas,
+                             int32_t precision, mtfm_cuda_model** out);
+MTFM_API mtfm_status mtfm_cuda_destroy(mtfm_cuda_model* m);
+
+/* Unknown name -> MTFM_CONFIG_ERROR (ParamStore::index_of, params.hpp:48-52);
+ * wrong shape -> MTFM_DIMENSION_ERROR. */
+MTFM_API mtfm_status mtfm_cuda_set_param(mtfm_cuda_model* m, const char* name, const float* host_values, int64_t rows,
+                                int64_t cols);
+/* Number of parameters the model registers and their names (registration order). */
+MTFM_API int64_t mtfm_cuda_num_params(const mtfm_cuda_model* m);
+MTFM_API const char* mtfm_cuda_param_name(const mtfm_cuda_model* m, int64_t i, int64_t* rows, int64_t* cols);
+
+/* Records the batch will produce (host-side count: sum over exposures of the
+ * task count of their scenario; exposures of unknown scenarios count 0). */
+MTFM_API int64_t mtfm_cuda_count_records(const mtfm_cuda_model* m, const mtfm_packed_batch* b);
+
+/* One-call forward: host batch in, host records out (H2D + device + D2H).
+ * only_scenario >= 0 restricts binding to one scenario like forward_scoped
+ * (model.hpp:265, subgraph.hpp:47-62); -1 = all scenarios. */
+MTFM_API mtfm_status mtfm_cuda_forward(mtfm_cuda_model* m, const mtfm_packed_batch* b, int32_t only_scenario,
+                              mtfm_records* out);
+
+/* Split forward. prepare: host layout + async H2D of the batch (the host
+ * arrays may be released after the call returns). run: enqueues every
+ * kernel on the model stream, no host synchronisation. results: waits, then
+ * copies the records (and reports device-detected errors). */
+MTFM_API mtfm_status mtfm_cuda_batch_prepare(mtfm_cuda_model* m, const mtfm_packed_batch* b, int32_t only_scenario,
+                                    mtfm_cuda_batch** out);
+MTFM_API mtfm_status mtfm_cuda_batch_run(mtfm_cuda_model* m, mtfm_cuda_batch* b);
+MTFM_API mtfm_status mtfm_cuda_batch_results(mtfm_cuda_model* m, mtfm_cuda_batch* b, mtfm_records* out);
+MTFM_API mtfm_status mtfm_cuda_batch_free(mtfm_cuda_batch* b);
+
+/* The CUDA stream (cudaStream_t) the model enqueues on. */
+MTFM_API void* mtfm_cuda_stream(mtfm_cuda_model* m);
+MTFM_API mtfm_status mtfm_cuda_last_stats(const mtfm_cuda_model* m, mtfm_run_stats* out);
+
+/* Per-stage profiling: when on, batch_run brackets every kernel stage with
+ * CUDA events; after batch_results, entry i reports the stage name, its
+ * device time (ms) and its algorithmic FLOPs / bytes. */
+MTFM_API mtfm_status mtfm_cuda_set_profiling(mtfm_cuda_model* m, int32_t on);
+MTFM_API int64_t mtfm_cuda_profile_count(const mtfm_cuda_model* m);
+MTFM_API const char* mtfm_cuda_profile_entry(const mtfm_cuda_model* m, int64_t i, double* ms, double* flops,
+                                             double* bytes);
+
+/* Debug / test hooks over device buffers of the last run (row-major). which:
+ * "x" final activations [rows][d] f32, "plan" int32 [rows][4] = (source,
+ * item, prefix, self), "scale" f32 [rows]. Returns elements copied. */
+MTFM_API int64_t mtfm_cuda_debug_fetch(mtfm_cuda_model* m, mtfm_cuda_batch* b, const char* which, void* host_dst,
+                              int64_t max_bytes);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MTFM_CUDA_H_ */

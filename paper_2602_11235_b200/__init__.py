@@ -1,0 +1,9 @@
+"""B200-native (sm_100a) MTFM hot path: jagged user batches -> heterogeneous
+tokenizer -> GQA Hybrid Target Attention stack -> MMoE heads, behind the C ABI
+of include/mtfm_cuda.h (libmtfm_cuda.so). The shared library is loaded on
+first use (abi.lib()) and there is no CPU fallback."""
+from . import abi  # noqa: F401
+from .model import Model, PreparedBatch, RecordArrays, infer_request  # noqa: F401
+from .schema import (BehaviorEvent, Candidate, Exposure, HTAConfig, InferenceRequest, ModelConfig,  # noqa: F401
+                     PredictionRecord, ScenarioSchema, SchemaSet, SequenceRecord, SequenceSchema, UserSample,
+                     pack_samples, sample_view_of_request)

@@ -1,0 +1,381 @@
+// attn_tc.cuh — Hybrid Target Attention on tcgen05 (sm_100a).
+//
+// Computes, for every query row i of a tile and every head h of one KV group g
+// (hta.hpp:115-134 with the mask of mask.cpp:5-29 in closed form):
+//
+//   A_h[i] = s_i * ( sum_{j < prefix_i} silu(Q_h[i] . K_g[j]) V_g[j]
+//                    + [i is T] silu(Q_h[i] . K_g[self_i]) V_g[self_i] )
+//
+// The dense N x N mask never exists: row i sees the first prefix_i context
+// keys of its user (H tokens plus R tokens strictly older than i) and, when it
+// is a T token, itself. There is no softmax: weights are pointwise SiLU, so
+// no running max / rescale; O simply accumulates in TMEM across key tiles.
+//
+// Tile = 128 MMA rows = HS heads of one GQA group x RT query rows (HS*RT=128),
+// so every K/V tile TMA-loaded into SMEM is shared by the HS query heads that
+// read it. Per key tile j:
+//   MMA warp : S[j%2] = Q K_j^T            (TMEM, fp32, 128 x BKV)
+//              O     += P[(j-1)%2] V_{j-1}  (P from SMEM, V MN-major)
+//   8 SiLU warps: S -> regs, mask (key < prefix_i), silu, bf16, swizzled
+//              st.shared into P[j%2], fence.proxy.async, arrive.
+// Epilogue (same 8 warps): O -> regs, x s_i, + self term for T rows, bf16 out.
+#pragma once
+
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace mtfm {
+
+struct AttnTile {
+    int q_row0;    // first query row (row index of the Q matrix)
+    int n_rows;    // valid query rows in this tile (<= RT)
+    int key_base;  // KV-matrix row of the user's first context key
+    int head0;     // first query head of the tile (HS consecutive heads, one group)
+    int kmax;      // max prefix over the tile's rows (filled on device)
+    int pad[3];
+};
+
+struct AttnParams {
+    CUtensorMap tma_q;   // Q matrix, box {chunk, RT}
+    CUtensorMap tma_kv;  // KV matrix, box {chunk, BKV}
+    const AttnTile* tiles;
+    int n_tiles;
+    int q_col0, k_col0, v_col0;  // column offsets of head/group 0
+    int heads, kv_heads, hs, rt;
+    const int* q_prefix;         // per Q row
+    const float* q_scale;        // per Q row
+    const int* q_self;           // per Q row: KV row of the self key, or -1
+    const __nv_bfloat16* q_ptr;  // Q matrix (self term)
+    long long ldq;
+    const __nv_bfloat16* kv_ptr;
+    long long ldkv;
+    __nv_bfloat16* out;          // A rows indexed like Q rows
+    long long ldo;
+};
+
+namespace attn_detail {
+
+template <int D>
+struct Cfg {
+    static constexpr int BKV = D <= 128 ? 128 : 64;
+    static constexpr int CHUNK = D < 64 ? D : 64;          // elements per swizzle row
+    static constexpr int SLABS = D / CHUNK;
+    static constexpr int ROWB = CHUNK * 2;                  // bytes per swizzled row
+    static constexpr uint32_t LAYOUT = ROWB == 128 ? 2 : (ROWB == 64 ? 4 : 6);
+    static constexpr int Q_BYTES = 128 * D * 2;
+    static constexpr int KV_TILE_BYTES = BKV * D * 2;       // one of K or V
+    static constexpr int STAGE_BYTES = 2 * KV_TILE_BYTES;
+    static constexpr int P_BYTES = 128 * BKV * 2;
+    static constexpr int kStages = D <= 64 ? 3 : 2;
+    static constexpr int SMEM = Q_BYTES + kStages * STAGE_BYTES + 2 * P_BYTES + 1024 + 512;
+    static constexpr uint32_t TMEM_COLS = 512;
+    static constexpr uint32_t S_COL = 0;                    // S buffers at [0, 2*BKV)
+    static constexpr uint32_t O_COL = 2 * BKV;
+    static_assert(O_COL + D <= 512, "TMEM budget");
+    static_assert(SMEM <= 227 * 1024, "SMEM budget");
+};
+
+// Byte offset of element (row, k) of a K-major SW128 [128 x 64] slab.
+__device__ __forceinline__ uint32_t sw128_off(uint32_t row, uint32_t chunk16) {
+    return (row >> 3) * 1024 + (row & 7) * 128 + ((chunk16 ^ (row & 7)) << 4);
+}
+
+__device__ __forceinline__ float silu_fast(float x) {
+    // silu(x) = h + h*tanh(h), h = x/2 : one MUFU op per element
+    const float h = 0.5f * x;
+    float t;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(h));
+    return fmaf(h, t, h);
+}
+
+}  // namespace attn_detail
+
+template <int D>
+__global__ void __launch_bounds__(384, 1) attn_tc_kernel(const __grid_constant__ AttnParams prm) {
+    using C = attn_detail::Cfg<D>;
+    constexpr int BKV = C::BKV;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sQ = smem;
+    uint8_t* sKV = sQ + C::Q_BYTES;
+    uint8_t* sP = sKV + C::kStages * C::STAGE_BYTES;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * C::P_BYTES);
+    uint64_t* q_full = bars + 0;
+    uint64_t* q_empty = bars + 1;
+    uint64_t* o_full = bars + 2;
+    uint64_t* o_empty = bars + 3;
+    uint64_t* s_full = bars + 4;   // [2]
+    uint64_t* s_empty = bars + 6;  // [2]
+    uint64_t* p_full = bars + 8;   // [2]
+    uint64_t* p_empty = bars + 10; // [2]
+    uint64_t* kv_full = bars + 12; // [kStages]
+    uint64_t* kv_empty = kv_full + C::kStages;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kv_empty + C::kStages);
+
+    const uint32_t warp = ptx::warp_id();
+    const uint32_t lane = ptx::lane_id();
+    const int r_per_g = prm.heads / prm.kv_heads;
+
+    if (warp == 0 && lane == 0) {
+        ptx::mbar_init(q_full, 1);
+        ptx::mbar_init(q_empty, 1);
+        ptx::mbar_init(o_full, 1);
+        ptx::mbar_init(o_empty, 8);
+        for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(&s_full[i], 1);
+            ptx::mbar_init(&s_empty[i], 8);
+            ptx::mbar_init(&p_full[i], 8);
+            ptx::mbar_init(&p_empty[i], 1);
+        }
+        for (int i = 0; i < C::kStages; ++i) {
+            ptx::mbar_init(&kv_full[i], 1);
+            ptx::mbar_init(&kv_empty[i], 1);
+        }
+        ptx::fence_mbar_init();
+        ptx::tma_prefetch(&prm.tma_q);
+        ptx::tma_prefetch(&prm.tma_kv);
+    }
+    if (warp == 2) ptx::tmem_alloc<C::TMEM_COLS>(tmem_slot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------ TMA producer
+        if (ptx::elect_one()) {
+            int stage = 0;
+            uint32_t phase = 0, q_phase = 0;
+            for (int t = blockIdx.x; t < prm.n_tiles; t += gridDim.x) {
+                const AttnTile tile = prm.tiles[t];
+                const int g = tile.head0 / r_per_g;
+                const int n_kv = (tile.kmax + BKV - 1) / BKV;
+                ptx::mbar_wait(q_empty, q_phase ^ 1);
+                ptx::mbar_arrive_expect_tx(q_full, C::Q_BYTES);
+                for (int hs = 0; hs < prm.hs; ++hs)
+                    for (int sl = 0; sl < C::SLABS; ++sl)
+                        ptx::tma_load_2d(sQ + sl * (128 * C::ROWB) + hs * prm.rt * C::ROWB, &prm.tma_q, q_full,
+                                         prm.q_col0 + (tile.head0 + hs) * D + sl * C::CHUNK, tile.q_row0);
+                q_phase ^= 1;
+                for (int j = 0; j < n_kv; ++j) {
+                    ptx::mbar_wait(&kv_empty[stage], phase ^ 1);
+                    uint8_t* sk = sKV + stage * C::STAGE_BYTES;
+                    uint8_t* sv = sk + C::KV_TILE_BYTES;
+                    ptx::mbar_arrive_expect_tx(&kv_full[stage], C::STAGE_BYTES);
+                    const int row = tile.key_base + j * BKV;
+                    for (int sl = 0; sl < C::SLABS; ++sl) {
+                        ptx::tma_load_2d(sk + sl * (BKV * C::ROWB), &prm.tma_kv, &kv_full[stage],
+                                         prm.k_col0 + g * D + sl * C::CHUNK, row);
+                        ptx::tma_load_2d(sv + sl * (BKV * C::ROWB), &prm.tma_kv, &kv_full[stage],
+                                         prm.v_col0 + g * D + sl * C::CHUNK, row);
+                    }
+                    if (++stage == C::kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer
+        const uint32_t idesc_s = ptx::instr_desc_bf16(128, BKV, false, false);
+        const uint32_t idesc_o = ptx::instr_desc_bf16(128, D, false, true);
+        int stage = 0;
+        uint32_t phase = 0, q_phase = 0, o_phase = 0;
+        uint32_t s_cnt = 0;  // global key-tile counter (S/P buffer parity)
+        for (int t = blockIdx.x; t < prm.n_tiles; t += gridDim.x) {
+            const AttnTile tile = prm.tiles[t];
+            const int n_kv = (tile.kmax + BKV - 1) / BKV;
+            ptx::mbar_wait(q_full, q_phase);
+            q_phase ^= 1;
+            ptx::mbar_wait(o_empty, o_phase ^ 1);
+            o_phase ^= 1;
+            ptx::tc_fence_after();
+            const uint32_t sq = ptx::smem_u32(sQ);
+            int prev_stage = -1;
+            for (int j = 0; j <= n_kv; ++j) {
+                if (j < n_kv) {
+                    const uint32_t buf = s_cnt & 1;
+                    const uint32_t par = (s_cnt >> 1) & 1;
+                    ptx::mbar_wait(&kv_full[stage], phase);
+                    ptx::mbar_wait(&s_empty[buf], par ^ 1);
+                    ptx::tc_fence_after();
+                    if (ptx::elect_one()) {
+                        const uint32_t sk = ptx::smem_u32(sKV + stage * C::STAGE_BYTES);
+#pragma unroll
+                        for (int kk = 0; kk < D / 16; ++kk) {
+                            const uint32_t sl = (kk * 16) / C::CHUNK;
+                            const uint32_t in = ((kk * 16) % C::CHUNK) * 2;
+                            const uint64_t da = ptx::smem_desc(sq + sl * (128 * C::ROWB) + in, 16, 8 * C::ROWB, C::LAYOUT);
+                            const uint64_t db = ptx::smem_desc(sk + sl * (BKV * C::ROWB) + in, 16, 8 * C::ROWB, C::LAYOUT);
+                            ptx::umma_bf16(tmem + C::S_COL + buf * BKV, da, db, idesc_s, kk > 0);
+                        }
+                        if (j == n_kv - 1) ptx::umma_commit(q_empty);
+                        ptx::umma_commit(&s_full[buf]);
+                    }
+                    __syncwarp();
+                }
+                if (j >= 1) {
+                    const uint32_t pc = s_cnt - 1;  // P of key tile j-1
+                    const uint32_t buf = pc & 1;
+                    const uint32_t par = (pc >> 1) & 1;
+                    ptx::mbar_wait(&p_full[buf], par);
+                    ptx::tc_fence_after();
+                    if (ptx::elect_one()) {
+                        const uint32_t sp = ptx::smem_u32(sP + buf * C::P_BYTES);
+                        const uint32_t sv = ptx::smem_u32(sKV + prev_stage * C::STAGE_BYTES + C::KV_TILE_BYTES);
+#pragma unroll
+                        for (int kk = 0; kk < BKV / 16; ++kk) {
+                            const uint32_t psl = (kk * 16) / 64;
+                            const uint32_t pin = ((kk * 16) % 64) * 2;
+                            const uint64_t da = ptx::smem_desc(sp + psl * (128 * 128) + pin, 16, 1024, 2);
+                            const uint64_t db = ptx::smem_desc(sv + kk * 16 * C::ROWB, BKV * C::ROWB, 8 * C::ROWB, C::LAYOUT);
+                            ptx::umma_bf16(tmem + C::O_COL, da, db, idesc_o, (j > 1 || kk > 0));
+                        }
+                        ptx::umma_commit(&kv_empty[prev_stage]);
+                        ptx::umma_commit(&p_empty[buf]);
+                        if (j == n_kv) ptx::umma_commit(o_full);
+                    }
+                    __syncwarp();
+                }
+                if (j < n_kv) {
+                    prev_stage = stage;
+                    ++s_cnt;
+                    if (++stage == C::kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+            if (n_kv == 0) {
+                // no visible context keys: release Q, signal an all-zero O
+                if (ptx::elect_one()) {
+                    ptx::umma_commit(q_empty);
+                    ptx::umma_commit(o_full);
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp >= 4) {
+        // ------------------------------------------------ SiLU + epilogue warps
+        const uint32_t q = warp & 3;
+        const uint32_t half = (warp - 4) >> 2;
+        const uint32_t m = q * 32 + lane;  // MMA row == TMEM lane
+        const uint32_t lane_addr = (q * 32u) << 16;
+        uint32_t s_cnt = 0, o_phase = 0;
+        for (int t = blockIdx.x; t < prm.n_tiles; t += gridDim.x) {
+            const AttnTile tile = prm.tiles[t];
+            const int n_kv = (tile.kmax + BKV - 1) / BKV;
+            const int hs = m / prm.rt;
+            const int i = m - hs * prm.rt;
+            const bool valid = i < tile.n_rows;
+            const int qrow = tile.q_row0 + i;
+            const int prefix = valid ? __ldg(prm.q_prefix + qrow) : 0;
+            for (int j = 0; j < n_kv; ++j, ++s_cnt) {
+                const uint32_t buf = s_cnt & 1;
+                const uint32_t par = (s_cnt >> 1) & 1;
+                ptx::mbar_wait(&s_full[buf], par);
+                ptx::tc_fence_after();
+                uint32_t packed[BKV / 4];  // my half: BKV/2 values -> BKV/4 bf16x2
+#pragma unroll
+                for (int c = 0; c < BKV / 32; ++c) {
+                    float v[16];
+                    const int col = half * (BKV / 2) + c * 16;
+                    ptx::tmem_ld16(tmem + lane_addr + C::S_COL + buf * BKV + col, v);
+                    ptx::tmem_ld_wait();
+                    const int key0 = j * BKV + col;
+#pragma unroll
+                    for (int e = 0; e < 16; e += 2) {
+                        const float w0 = (key0 + e < prefix) ? attn_detail::silu_fast(v[e]) : 0.f;
+                        const float w1 = (key0 + e + 1 < prefix) ? attn_detail::silu_fast(v[e + 1]) : 0.f;
+                        packed[c * 8 + e / 2] = pack_bf16(w0, w1);
+                    }
+                }
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&s_empty[buf]);
+                // P buffer must have been consumed by the MMA two tiles ago
+                ptx::mbar_wait(&p_empty[buf], par ^ 1);
+                uint8_t* pb = sP + buf * C::P_BYTES;
+#pragma unroll
+                for (int c = 0; c < BKV / 32; ++c) {
+                    const int col = half * (BKV / 2) + c * 16;  // key column within tile
+                    const int slab = col / 64;
+                    const uint32_t ch = (col % 64) / 8;         // 16B chunk index (8 bf16)
+                    uint8_t* base = pb + slab * (128 * 128);
+                    *reinterpret_cast<uint4*>(base + attn_detail::sw128_off(m, ch)) =
+                        make_uint4(packed[c * 8 + 0], packed[c * 8 + 1], packed[c * 8 + 2], packed[c * 8 + 3]);
+                    *reinterpret_cast<uint4*>(base + attn_detail::sw128_off(m, ch + 1)) =
+                        make_uint4(packed[c * 8 + 4], packed[c * 8 + 5], packed[c * 8 + 6], packed[c * 8 + 7]);
+                }
+                ptx::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&p_full[buf]);
+            }
+            // ---------------- epilogue
+            ptx::mbar_wait(o_full, o_phase);
+            o_phase ^= 1;
+            ptx::tc_fence_after();
+            const int head = tile.head0 + hs;
+            const int g = tile.head0 / r_per_g;
+            float scale = 0.f, wself = 0.f;
+            int self_row = -1;
+            if (valid) {
+                scale = __ldg(prm.q_scale + qrow);
+                self_row = __ldg(prm.q_self + qrow);
+                if (self_row >= 0) {
+                    const __nv_bfloat16* qp = prm.q_ptr + (long long)qrow * prm.ldq + prm.q_col0 + head * D;
+                    const __nv_bfloat16* kp = prm.kv_ptr + (long long)self_row * prm.ldkv + prm.k_col0 + g * D;
+                    float dot = 0.f;
+                    for (int e = 0; e < D; ++e) dot += to_f32(qp[e]) * to_f32(kp[e]);
+                    wself = silu_precise(dot);
+                }
+            }
+            constexpr int DCOLS = D >= 32 ? D / 2 : D;
+            if (D >= 32 || half == 0) {
+                const int c0 = D >= 32 ? half * DCOLS : 0;
+#pragma unroll 1
+                for (int c = c0; c < c0 + DCOLS; c += 16) {
+                    float v[16];
+                    ptx::tmem_ld16(tmem + lane_addr + C::O_COL + c, v);
+                    ptx::tmem_ld_wait();
+                    if (n_kv == 0) {
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) v[e] = 0.f;
+                    }
+                    if (valid) {
+                        if (self_row >= 0) {
+                            const __nv_bfloat16* vp =
+                                prm.kv_ptr + (long long)self_row * prm.ldkv + prm.v_col0 + g * D + c;
+#pragma unroll
+                            for (int e = 0; e < 16; ++e) v[e] += wself * to_f32(vp[e]);
+                        }
+                        __nv_bfloat16* o = prm.out + (long long)qrow * prm.ldo + head * D + c;
+                        uint4 w0, w1;
+                        w0.x = pack_bf16(v[0] * scale, v[1] * scale);
+                        w0.y = pack_bf16(v[2] * scale, v[3] * scale);
+                        w0.z = pack_bf16(v[4] * scale, v[5] * scale);
+                        w0.w = pack_bf16(v[6] * scale, v[7] * scale);
+                        w1.x = pack_bf16(v[8] * scale, v[9] * scale);
+                        w1.y = pack_bf16(v[10] * scale, v[11] * scale);
+                        w1.z = pack_bf16(v[12] * scale, v[13] * scale);
+                        w1.w = pack_bf16(v[14] * scale, v[15] * scale);
+                        reinterpret_cast<uint4*>(o)[0] = w0;
+                        reinterpret_cast<uint4*>(o)[1] = w1;
+                    }
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(o_empty);
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<C::TMEM_COLS>(tmem);
+    }
+}
+
+}  // namespace mtfm

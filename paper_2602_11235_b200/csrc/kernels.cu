@@ -1,0 +1,700 @@
+// kernels.cu — planning (K0), tokenizer gather (K1 prologue), group LayerNorm,
+// gate, heads (K5 epilogue) and the fp32 SIMT check-mode GEMM / attention.
+#include <climits>
+
+#include "common.cuh"
+#include "gemm_tc.cuh"
+#include "kernels.cuh"
+
+namespace mtfm {
+
+// Error keys: atomicMin over (user, piece, stage, row, code) so the batch
+// reports the exception the reference would throw first (users in order;
+// within a user: pieces in pile order (tokenizer.hpp:244-264); within a piece
+// slot-major, dimension check of a slot before its range check
+// (tokenizer.hpp:193-207, eval_ctx.hpp:190-198)).
+__device__ __forceinline__ unsigned long long err_key(long long u, long long piece, long long stage, long long row,
+                                                      int code) {
+    u = u < (1ll << 22) - 1 ? u : (1ll << 22) - 1;
+    piece = piece < 2047 ? piece : 2047;
+    stage = stage < 2047 ? stage : 2047;
+    row = row < (1ll << 17) - 1 ? row : (1ll << 17) - 1;
+    return (static_cast<unsigned long long>(u) << 42) | (static_cast<unsigned long long>(piece) << 31) |
+           (static_cast<unsigned long long>(stage) << 20) | (static_cast<unsigned long long>(row) << 3) |
+           static_cast<unsigned long long>(code);
+}
+enum { ERR_INTEGRITY = 2, ERR_DIMENSION = 3, ERR_LOOKUP = 5, ERR_CONTRACT = 6 };
+
+__device__ __forceinline__ int find_source(const SourceInfo* src, int n_src, int kind, int id, int only_scenario) {
+    for (int s = 0; s < n_src; ++s)
+        if (src[s].kind == kind && src[s].id == id) {
+            if (kind == 2 && only_scenario >= 0 && id != only_scenario) return -1;
+            return s;
+        }
+    return -1;
+}
+
+// Sequence of global event e among the user's sequences [s0, s1).
+__device__ __forceinline__ int find_seq(const int* ev_off, int s0, int s1, int e) {
+    int lo = s0, hi = s1 - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (ev_off[mid] <= e)
+            lo = mid;
+        else
+            hi = mid - 1;
+    }
+    return lo;
+}
+
+struct CtxLess {  // (kind, ts, pile index) — std::stable_sort by ts per kind (tokenizer.hpp:117-123)
+    __device__ bool operator()(long long ta, long long sa, long long tb, long long sb) const {
+        const long long ka = sa >> 32, kb = sb >> 32;
+        if (ka != kb) return ka < kb;
+        if (ta != tb) return ta < tb;
+        return sa < sb;
+    }
+};
+struct TLess {  // (ts, scenario, index) — canonical exposure order (tokenizer.hpp:82-90)
+    __device__ bool operator()(long long ta, long long sa, long long tb, long long sb) const {
+        if (ta != tb) return ta < tb;
+        return sa < sb;
+    }
+};
+
+template <typename Less>
+__device__ void bitonic_sort(long long* ts, long long* sec, int npad, Less less) {
+    for (int k = 2; k <= npad; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < npad; i += blockDim.x) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const bool up = (i & k) == 0;
+                    const long long ta = ts[i], sa = sec[i], tb = ts[ixj], sb = sec[ixj];
+                    const bool swap = up ? less(tb, sb, ta, sa) : less(ta, sa, tb, sb);
+                    if (swap) {
+                        ts[i] = tb;
+                        sec[i] = sb;
+                        ts[ixj] = ta;
+                        sec[ixj] = sa;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// number of entries of sorted a[0, n) strictly below v
+__device__ __forceinline__ int count_below(const long long* a, int n, long long v) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (a[mid] < v)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ float row_scale_of(int norm, int c, int n_tokens) {
+    if (norm == 0) return __fdiv_rn(1.f, static_cast<float>(c > 1 ? c : 1));
+    if (norm == 1) return __fdiv_rn(1.f, static_cast<float>(n_tokens));
+    return 1.f;
+}
+
+// One CTA per user: plan_tokens (tokenizer.hpp:53-134) + make_stack_geom
+// (hta.hpp:40-71) in prefix form + record slots + input validation.
+__global__ void plan_kernel(PlanArgs a) {
+    extern __shared__ long long sm_sort[];
+    long long* s_ts = sm_sort;
+    long long* s_sec = sm_sort + a.max_sort;
+    __shared__ unsigned long long s_err;
+    __shared__ int s_lh;
+    const DevBatch& b = a.b;
+    const int u = blockIdx.x;
+    const int tid = threadIdx.x;
+    const int s0 = b.seq_off[u], s1 = b.seq_off[u + 1];
+    const int ev0 = b.ev_off[s0], ev1 = b.ev_off[s1];
+    const int n_ev = ev1 - ev0;
+    const int x0 = b.exp_off[u], x1 = b.exp_off[u + 1];
+    const int n_t = x1 - x0;
+    const int n_tok = n_ev + n_t;
+    if (tid == 0) {
+        s_err = ~0ull;
+        s_lh = 0;
+        if (n_tok == 0) s_err = err_key(u, 0, 0, 0, ERR_CONTRACT);
+    }
+    int npad = 1;
+    while (npad < n_ev) npad <<= 1;
+    int tpad = 1;
+    while (tpad < n_t) tpad <<= 1;
+    if (npad > a.max_sort || tpad + n_ev > a.max_sort) {
+        if (tid == 0) atomicMin(a.err, err_key(u, 0, 0, 0, ERR_CONTRACT) | 7ull);  // capacity
+        return;
+    }
+
+    // ---------------- context tokens: (kind, ts, pile order)
+    for (int i = tid; i < npad; i += blockDim.x) {
+        if (i < n_ev) {
+            const int e = ev0 + i;
+            const int sq = find_seq(b.ev_off, s0, s1, e);
+            s_ts[i] = b.ev_ts[e];
+            s_sec[i] = (static_cast<long long>(b.seq_kind[sq] ? 1 : 0) << 32) | i;
+        } else {
+            s_ts[i] = LLONG_MAX;
+            s_sec[i] = 3ll << 32;
+        }
+    }
+    __syncthreads();
+    if (n_ev > 1) bitonic_sort(s_ts, s_sec, npad, CtxLess{});
+    for (int i = tid; i < n_ev; i += blockDim.x)
+        if ((s_sec[i] >> 32) == 0 && (i + 1 == n_ev || (s_sec[i + 1] >> 32) != 0)) s_lh = i + 1;
+    __syncthreads();
+    const int l_h = s_lh;
+    const int l_r = n_ev - l_h;
+    const long long* r_ts = s_ts + l_h;  // sorted R timestamps
+
+    // per-row outputs for context rows + tokenizer grouping
+    for (int i = tid; i < n_ev; i += blockDim.x) {
+        const int local = static_cast<int>(s_sec[i] & 0xffffffffll);
+        const int kind = static_cast<int>(s_sec[i] >> 32);
+        const int e = ev0 + local;
+        const int sq = find_seq(b.ev_off, s0, s1, e);
+        const int src = find_source(a.src, a.n_src, kind, b.seq_schema[sq], -1);
+        const int row = e - local + i;  // == ev0 + i
+        const int prefix = l_h + count_below(r_ts, l_r, s_ts[i]);
+        a.rm.src[row] = src;
+        a.rm.item[row] = e;
+        a.rm.prefix[row] = prefix;
+        a.rm.scale[row] = row_scale_of(a.norm, prefix, n_tok);
+        a.rm.self[row] = -1;
+        a.rm.keybase[row] = ev0;
+        if (src >= 0) {
+            long long rank = e - b.ev_off[sq];
+            for (int q = s0; q < sq; ++q)
+                if (b.seq_kind[q] == b.seq_kind[sq] && b.seq_schema[q] == b.seq_schema[sq])
+                    rank += b.ev_off[q + 1] - b.ev_off[q];
+            a.rm.src_rows[a.src_base[src] + a.us_off[(long long)u * a.n_src + src] + rank] = row;
+        }
+    }
+    // validation of sequence pieces (pile order = non-empty sequences in list order)
+    for (int e = ev0 + tid; e < ev1; e += blockDim.x) {
+        const int sq = find_seq(b.ev_off, s0, s1, e);
+        int piece = 0;
+        for (int q = s0; q < sq; ++q) piece += b.ev_off[q + 1] > b.ev_off[q];
+        const int src = find_source(a.src, a.n_src, b.seq_kind[sq] ? 1 : 0, b.seq_schema[sq], -1);
+        const int r = e - b.ev_off[sq];
+        unsigned long long k = ~0ull;
+        if (src < 0) {
+            k = err_key(u, piece, 0, 0, ERR_INTEGRITY);
+        } else {
+            const SourceInfo si = a.src[src];
+            const int cnt = b.ev_feat_off[e + 1] - b.ev_feat_off[e];
+            for (int s = 0; s < si.nslot[0]; ++s) {
+                if (cnt <= s) {
+                    k = err_key(u, piece, 1 + 2 * s, r, ERR_DIMENSION);
+                    break;
+                }
+                const int id = b.ev_feats[b.ev_feat_off[e] + s];
+                if (id < 0 || id >= a.slots[si.slot0 + s].vocab) {
+                    k = err_key(u, piece, 2 + 2 * s, r, ERR_LOOKUP);
+                    break;
+                }
+            }
+        }
+        if (k != ~0ull) atomicMin(&s_err, k);
+    }
+    int n_pieces_seq = 0;
+    for (int q = s0; q < s1; ++q) n_pieces_seq += b.ev_off[q + 1] > b.ev_off[q];
+    __syncthreads();
+
+    // ---------------- target tokens: canonical (ts, scenario, index)
+    // The sorted R timestamps are needed after the T sort: stash them right
+    // behind the T sort area (the host sizes the buffer for tpad + n_ev).
+    long long* r_stash = s_ts + tpad;
+    for (int i = tid; i < l_r; i += blockDim.x) s_sec[i] = s_ts[l_h + i];
+    __syncthreads();
+    for (int i = tid; i < l_r; i += blockDim.x) r_stash[i] = s_sec[i];
+    __syncthreads();
+    for (int i = tid; i < tpad; i += blockDim.x) {
+        if (i < n_t) {
+            s_ts[i] = b.exp_ts[x0 + i];
+            s_sec[i] = (static_cast<long long>(b.exp_scenario[x0 + i]) << 32) | i;
+        } else {
+            s_ts[i] = LLONG_MAX;
+            s_sec[i] = LLONG_MAX;
+        }
+    }
+    __syncthreads();
+    if (n_t > 1) bitonic_sort(s_ts, s_sec, tpad, TLess{});
+    for (int p = tid; p < n_t; p += blockDim.x) {
+        const int local = static_cast<int>(s_sec[p] & 0xffffffffll);
+        const int scen = static_cast<int>(s_sec[p] >> 32);
+        const int x = x0 + local;
+        const long long row = static_cast<long long>(b.n_events) + x0 + p;
+        const long long t = x0 + p;
+        const int prefix = l_h + count_below(r_stash, l_r, s_ts[p]);
+        int rho = 0, n_s = 0, distinct_below = 0;
+        long long rec_before = 0;
+        for (int q = 0; q < n_t; ++q) {
+            const int sq = static_cast<int>(s_sec[q] >> 32);
+            if (sq == scen) {
+                ++n_s;
+                if (q < p) ++rho;
+            } else if (sq < scen) {
+                const int ss = find_source(a.src, a.n_src, 2, sq, a.only_scenario);
+                rec_before += ss >= 0 ? a.src[ss].ntasks : 0;
+                // first occurrence of each smaller scenario counts as a piece
+                bool first = true;
+                for (int q2 = 0; q2 < q; ++q2)
+                    if (static_cast<int>(s_sec[q2] >> 32) == sq) {
+                        first = false;
+                        break;
+                    }
+                distinct_below += first;
+            }
+        }
+        const int src = find_source(a.src, a.n_src, 2, scen, a.only_scenario);
+        a.rm.src[row] = src;
+        a.rm.item[row] = x;
+        a.rm.prefix[row] = prefix;
+        a.rm.scale[row] = row_scale_of(a.norm, prefix + 1, n_tok);
+        a.rm.self[row] = static_cast<int>(row);
+        a.rm.keybase[row] = ev0;
+        a.rm.t_user[t] = u;
+        a.rm.t_exp_ref[t] = local;
+        a.rm.t_scen[t] = scen;
+        a.rm.t_rec0[t] = a.rec_off[u] + rec_before + rho;
+        a.rm.t_rec_stride[t] = n_s;
+        const int piece = n_pieces_seq + distinct_below;
+        unsigned long long k = ~0ull;
+        if (src < 0) {
+            k = err_key(u, piece, 0, 0, ERR_INTEGRITY);
+        } else {
+            a.rm.src_rows[a.src_base[src] + a.us_off[(long long)u * a.n_src + src] + rho] = static_cast<int>(row);
+            const SourceInfo si = a.src[src];
+            int slot_base = 0;
+            int blk_off = 0;
+            for (int blk = 0; blk < 3 && k == ~0ull; ++blk) {
+                const int cnt = b.exp_blk[3 * x + blk];
+                for (int s = 0; s < si.nslot[blk]; ++s) {
+                    const int gs = slot_base + s;
+                    if (cnt <= s) {
+                        k = err_key(u, piece, 1 + 2 * gs, rho, ERR_DIMENSION);
+                        break;
+                    }
+                    const int id = b.exp_feats[b.exp_feat_off[x] + blk_off + s];
+                    if (id < 0 || id >= a.slots[si.slot0 + gs].vocab) {
+                        k = err_key(u, piece, 2 + 2 * gs, rho, ERR_LOOKUP);
+                        break;
+                    }
+                }
+                slot_base += si.nslot[blk];
+                blk_off += cnt;
+            }
+        }
+        if (k != ~0ull) atomicMin(&s_err, k);
+    }
+    __syncthreads();
+    if (tid == 0 && s_err != ~0ull) atomicMin(a.err, s_err);
+}
+
+void launch_plan(const PlanArgs& a, int smem_elems, cudaStream_t st) {
+    if (a.b.n_users == 0) return;
+    const size_t smem = static_cast<size_t>(smem_elems) * 16;
+    cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    plan_kernel<<<a.b.n_users, 256, smem, st>>>(a);
+}
+
+// ---------------------------------------------------------------- gather
+template <typename T>
+__global__ void gather_kernel(DevBatch b, const SourceInfo* __restrict__ srcs, const SlotInfo* __restrict__ slots,
+                              const int* __restrict__ src_rows, const int* __restrict__ row_item,
+                              const long long* __restrict__ src_base, const long long* __restrict__ src_cnt,
+                              const long long* __restrict__ emb_base, const T* __restrict__ tables, int d_emb,
+                              int n_src, long long total_rows, int max_slots, T* __restrict__ out) {
+    const long long n_items = total_rows * (max_slots + 1);
+    for (long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x; w < n_items;
+         w += (long long)gridDim.x * blockDim.x) {
+        const long long P = w / (max_slots + 1);
+        const int k = static_cast<int>(w - P * (max_slots + 1));
+        int s = 0;
+        while (s + 1 < n_src && P >= src_base[s + 1]) ++s;
+        const long long p = P - src_base[s];
+        if (p >= src_cnt[s]) continue;
+        const SourceInfo si = srcs[s];
+        const int nslots = si.nslot[0] + si.nslot[1] + si.nslot[2];
+        T* orow = out + emb_base[s] + p * si.k_pad;
+        if (k == nslots) {  // zero padding columns
+            for (int c = si.k_in; c < si.k_pad; ++c) orow[c] = from_f32<T>(0.f);
+            continue;
+        }
+        if (k > nslots) continue;
+        const int row = src_rows[P];
+        const int item = row_item[row];
+        int id;
+        if (si.kind < 2) {
+            id = b.ev_feats[b.ev_feat_off[item] + k];
+        } else {
+            const int nu = b.exp_blk[3 * item], nc = b.exp_blk[3 * item + 1];
+            const int off = k < si.nslot[0] ? k : (k < si.nslot[0] + si.nslot[1] ? nu + (k - si.nslot[0])
+                                                                                  : nu + nc + (k - si.nslot[0] - si.nslot[1]));
+            id = b.exp_feats[b.exp_feat_off[item] + off];
+        }
+        const SlotInfo sl = slots[si.slot0 + k];
+        id = id < 0 ? 0 : (id >= sl.vocab ? sl.vocab - 1 : id);  // invalid ids were reported by the plan
+        const T* trow = tables + sl.emb_off + static_cast<long long>(id) * d_emb;
+        T* dst = orow + k * d_emb;
+        if (sizeof(T) * d_emb % 16 == 0) {
+            const uint4* s4 = reinterpret_cast<const uint4*>(trow);
+            uint4* d4 = reinterpret_cast<uint4*>(dst);
+            for (int c = 0; c < static_cast<int>(sizeof(T) * d_emb / 16); ++c) d4[c] = __ldg(s4 + c);
+        } else {
+            for (int c = 0; c < d_emb; ++c) dst[c] = trow[c];
+        }
+    }
+}
+
+template <typename T>
+void launch_gather(const DevBatch& b, const SourceInfo* src_dev, const SlotInfo* slots_dev, const RowMeta& rm,
+                   const long long* src_base_dev, const long long* src_cnt_dev, const long long* emb_base_dev,
+                   const T* tables, int d_emb, int n_src, long long total_rows, int max_slots, T* out,
+                   cudaStream_t st) {
+    if (total_rows == 0) return;
+    const long long n = total_rows * (max_slots + 1);
+    const int blocks = static_cast<int>(std::min<long long>(cdiv(n, 256), 148ll * 16));
+    gather_kernel<T><<<blocks, 256, 0, st>>>(b, src_dev, slots_dev, rm.src_rows, rm.item, src_base_dev, src_cnt_dev,
+                                             emb_base_dev, tables, d_emb, n_src, total_rows, max_slots, out);
+}
+template void launch_gather<float>(const DevBatch&, const SourceInfo*, const SlotInfo*, const RowMeta&,
+                                   const long long*, const long long*, const long long*, const float*, int, int,
+                                   long long, int, float*, cudaStream_t);
+template void launch_gather<__nv_bfloat16>(const DevBatch&, const SourceInfo*, const SlotInfo*, const RowMeta&,
+                                           const long long*, const long long*, const long long*,
+                                           const __nv_bfloat16*, int, int, long long, int, __nv_bfloat16*,
+                                           cudaStream_t);
+
+// ---------------------------------------------------------------- GLN
+// row_normalize (kernels.hpp:132-153) + group_affine (eval_ctx.hpp:130-143).
+template <typename TIn>
+__device__ __forceinline__ void load_row(const TIn* p, int d, int lane, float (&v)[32]) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        const int c = lane + 32 * i;
+        v[i] = c < d ? to_f32(p[c]) : 0.f;
+    }
+}
+
+__device__ __forceinline__ void normalize_row(float (&v)[32], int d, int lane, float eps) {
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) s += v[i];
+    s = warp_sum(s);
+    const float mean = __fdiv_rn(s, static_cast<float>(d));
+    float q = 0.f;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        const int c = lane + 32 * i;
+        const float x = c < d ? v[i] - mean : 0.f;
+        q += x * x;
+    }
+    q = warp_sum(q);
+    const float var = __fdiv_rn(q, static_cast<float>(d));
+    const float inv = __fdiv_rn(1.f, sqrtf(var + eps));
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = (v[i] - mean) * inv;
+}
+
+template <typename T>
+__global__ void gln_kernel(const float* __restrict__ x, long long ldx, long long r0, long long n_rows, int d,
+                           const int* __restrict__ row_src, const float* __restrict__ gain,
+                           const float* __restrict__ bias, float eps, T* __restrict__ out, long long ldo) {
+    const int lane = threadIdx.x & 31;
+    const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long i = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); i < n_rows; i += warps) {
+        const long long r = r0 + i;
+        float v[32];
+        load_row(x + r * ldx, d, lane, v);
+        normalize_row(v, d, lane, eps);
+        int g = row_src[r];
+        g = g < 0 ? 0 : g;
+        const float* gg = gain + (long long)g * d;
+        const float* bb = bias + (long long)g * d;
+        T* o = out + i * ldo;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+            const int c = lane + 32 * k;
+            if (c < d) o[c] = from_f32<T>(v[k] * __ldg(gg + c) + __ldg(bb + c));
+        }
+    }
+}
+
+template <typename T>
+void launch_gln(const float* x, long long ldx, long long r0, long long n_rows, int d, const int* row_src,
+                const float* gain, const float* bias, float eps, T* out, long long ldo, cudaStream_t st) {
+    if (n_rows == 0) return;
+    const int blocks = static_cast<int>(std::min<long long>(cdiv(n_rows, 8), 148ll * 32));
+    gln_kernel<T><<<blocks, 256, 0, st>>>(x, ldx, r0, n_rows, d, row_src, gain, bias, eps, out, ldo);
+}
+template void launch_gln<float>(const float*, long long, long long, long long, int, const int*, const float*,
+                                const float*, float, float*, long long, cudaStream_t);
+template void launch_gln<__nv_bfloat16>(const float*, long long, long long, long long, int, const int*,
+                                        const float*, const float*, float, __nv_bfloat16*, long long,
+                                        cudaStream_t);
+
+template <typename T>
+__global__ void gate_kernel(const T* __restrict__ a, long long lda, const T* __restrict__ u, long long ldu,
+                            long long n_rows, int d, const int* __restrict__ row_src, const float* __restrict__ gain,
+                            const float* __restrict__ bias, float eps, T* __restrict__ out, long long ldo) {
+    const int lane = threadIdx.x & 31;
+    const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long i = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); i < n_rows; i += warps) {
+        float v[32];
+        load_row(a + i * lda, d, lane, v);
+        normalize_row(v, d, lane, eps);
+        int g = row_src[i];
+        g = g < 0 ? 0 : g;
+        const float* gg = gain + (long long)g * d;
+        const float* bb = bias + (long long)g * d;
+        const T* ur = u + i * ldu;
+        T* o = out + i * ldo;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+            const int c = lane + 32 * k;
+            if (c < d) o[c] = from_f32<T>((v[k] * __ldg(gg + c) + __ldg(bb + c)) * to_f32(ur[c]));
+        }
+    }
+}
+
+template <typename T>
+void launch_gate(const T* a, long long lda, const T* u, long long ldu, long long n_rows, int d,
+                 const int* row_src_of_rows, const float* gain, const float* bias, float eps, T* out,
+                 long long ldo, cudaStream_t st) {
+    if (n_rows == 0) return;
+    const int blocks = static_cast<int>(std::min<long long>(cdiv(n_rows, 8), 148ll * 32));
+    gate_kernel<T><<<blocks, 256, 0, st>>>(a, lda, u, ldu, n_rows, d, row_src_of_rows, gain, bias, eps, out, ldo);
+}
+template void launch_gate<float>(const float*, long long, const float*, long long, long long, int, const int*,
+                                 const float*, const float*, float, float*, long long, cudaStream_t);
+template void launch_gate<__nv_bfloat16>(const __nv_bfloat16*, long long, const __nv_bfloat16*, long long,
+                                         long long, int, const int*, const float*, const float*, float,
+                                         __nv_bfloat16*, long long, cudaStream_t);
+
+__global__ void to_bf16_kernel(const float* __restrict__ x, long long n_rows, int d, __nv_bfloat16* __restrict__ out,
+                               long long ldo) {
+    const long long n = n_rows * d;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const long long r = i / d;
+        const int c = static_cast<int>(i - r * d);
+        out[r * ldo + c] = __float2bfloat16_rn(x[i]);
+    }
+}
+void launch_to_bf16(const float* x, long long n_rows, int d, __nv_bfloat16* out, long long ldo, cudaStream_t st) {
+    if (n_rows == 0) return;
+    const int blocks = static_cast<int>(std::min<long long>(cdiv(n_rows * d, 256), 148ll * 16));
+    to_bf16_kernel<<<blocks, 256, 0, st>>>(x, n_rows, d, out, ldo);
+}
+
+// ---------------------------------------------------------------- heads
+// mmoe_forward (heads.hpp:47-99) for one T row per warp, then the record of
+// model.hpp:284-311: probability = clamp(sigmoid(z), 1e-12, 1 - 1e-12).
+__global__ void heads_kernel(HeadArgs a) {
+    const int lane = threadIdx.x & 31;
+    const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long t = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); t < a.n_t; t += warps) {
+        const int scen = a.t_scen[t];
+        int s = -1;
+        for (int i = 0; i < a.n_src; ++i)
+            if (a.src[i].kind == 2 && a.src[i].id == scen) s = i;
+        if (s < 0) continue;  // reported by the plan
+        const SourceInfo si = a.src[s];
+        const float* y = a.y + t * a.ldy;
+        for (int k = 0; k < si.ntasks; ++k) {
+            const int task = si.task0 + k;
+            // softmax over the E gate logits (kernels.hpp:155-173)
+            float g[32];
+            float mx = -INFINITY;
+            for (int e = 0; e < a.E; ++e) {
+                g[e & 31] = y[a.E * a.de + task * a.E + e] + a.gate_bias[task * a.E + e];
+                mx = fmaxf(mx, g[e & 31]);
+            }
+            float sum = 0.f;
+            for (int e = 0; e < a.E; ++e) {
+                g[e & 31] = expf(g[e & 31] - mx);
+                sum += g[e & 31];
+            }
+            const float inv = __fdiv_rn(1.f, sum);
+            for (int e = 0; e < a.E; ++e) g[e & 31] *= inv;
+            float z = 0.f;
+            for (int c = lane; c < a.de; c += 32) {
+                float m = 0.f;
+                for (int e = 0; e < a.E; ++e) {
+                    const float pre = y[e * a.de + c] + a.exp_bias[e * a.de + c];
+                    m += silu_precise(pre) * g[e & 31];
+                }
+                z += m * a.tower_w[(long long)task * a.de + c];
+            }
+            z = warp_sum(z) + a.tower_b[task];
+            if (lane == 0) {
+                const long long r = a.t_rec0[t] + (long long)k * a.t_rec_stride[t];
+                double p = static_cast<double>(sigmoid_precise(z));
+                p = p < 1e-12 ? 1e-12 : (p > 1.0 - 1e-12 ? 1.0 - 1e-12 : p);
+                a.rec_user[r] = a.user_id[a.t_user[t]];
+                a.rec_scen[r] = scen;
+                a.rec_exp[r] = a.t_exp_ref[t];
+                a.rec_task[r] = k;
+                if (a.rec_logit) a.rec_logit[r] = z;
+                a.rec_prob[r] = p;
+            }
+        }
+    }
+}
+void launch_heads(const HeadArgs& a, cudaStream_t st) {
+    if (a.n_t == 0) return;
+    const int blocks = static_cast<int>(std::min<long long>(cdiv(a.n_t, 8), 148ll * 32));
+    heads_kernel<<<blocks, 256, 0, st>>>(a);
+}
+
+// ---------------------------------------------------------------- SIMT GEMM (check mode)
+struct SimtGemmBatch {
+    SimtGemm p[kMaxProblems];
+    int n;
+};
+
+__global__ void __launch_bounds__(256) gemm_simt_kernel(const __grid_constant__ SimtGemmBatch bt) {
+    const SimtGemm& p = bt.p[blockIdx.z];
+    const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+    if (m0 >= p.M || n0 >= p.N) return;
+    __shared__ float As[16][65];
+    __shared__ float Ws[16][64];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    float acc[4][4] = {};
+    for (int k0 = 0; k0 < p.K; k0 += 16) {
+        for (int i = threadIdx.x; i < 64 * 16; i += 256) {
+            const int r = i >> 4, c = i & 15;
+            const int m = m0 + r, k = k0 + c;
+            As[c][r] = (m < p.M && k < p.K) ? p.A[(long long)m * p.lda + k] : 0.f;
+            const int kr = i >> 6, nc = i & 63;
+            const int kk = k0 + kr, n = n0 + nc;
+            Ws[kr][nc] = (kk < p.K && n < p.N) ? p.W[(long long)kk * p.N + n] : 0.f;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            float a[4], w[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = As[k][ty * 4 + i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) w[j] = Ws[k][tx * 4 + j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], w[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int m = m0 + ty * 4 + i;
+        if (m >= p.M) continue;
+        const long long orow = p.row_map ? static_cast<long long>(p.row_map[m]) : p.row_offset + m;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int n = n0 + tx * 4 + j;
+            if (n >= p.N) continue;
+            float v = acc[i][j] + (p.bias ? p.bias[n] : 0.f);
+            if (p.epi == EPI_SILU_BF16) v = silu_precise(v);
+            if (p.epi == EPI_RESID_F32) v += p.resid[orow * p.ldo + n];
+            static_cast<float*>(p.out)[orow * p.ldo + n] = v;
+        }
+    }
+}
+
+void launch_gemm_simt(const SimtGemm* probs, int n, cudaStream_t st) {
+    SimtGemmBatch bt{};
+    int gm = 0, gn = 0;
+    for (int i = 0; i < n; ++i) {
+        bt.p[i] = probs[i];
+        gm = std::max<int>(gm, static_cast<int>(cdiv(probs[i].M, 64)));
+        gn = std::max<int>(gn, static_cast<int>(cdiv(probs[i].N, 64)));
+    }
+    bt.n = n;
+    if (gm == 0 || gn == 0) return;
+    gemm_simt_kernel<<<dim3(gn, gm, n), 256, 0, st>>>(bt);
+}
+
+// ---------------------------------------------------------------- SIMT attention (check mode)
+// One warp per (query row, head); keys in order j = 0.. prefix-1 (gemm_nn
+// accumulation order of hta.hpp:128-131), then the T self key.
+__global__ void attn_simt_kernel(SimtAttn a) {
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    extern __shared__ float q_sm[];
+    float* qv = q_sm + wib * a.dh;
+    const long long total = a.n_q * a.heads;
+    const int r = a.heads / a.kv_heads;
+    const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long w = blockIdx.x * (long long)(blockDim.x >> 5) + wib; w < total; w += warps) {
+        const long long i = w / a.heads;
+        const int h = static_cast<int>(w - i * a.heads);
+        const int g = h / r;
+        const int p = a.prefix[i];
+        const long long base = a.keybase[i];
+        const int self = a.self[i];
+        const float* qrow = a.q + i * a.ldq + a.q_col0 + h * a.dh;
+        for (int c = lane; c < a.dh; c += 32) qv[c] = qrow[c];
+        __syncwarp();
+        float acc[8] = {};
+        for (int j0 = 0; j0 < p; j0 += 32) {
+            const int j = j0 + lane;
+            float wgt = 0.f;
+            if (j < p) {
+                const float* kr = a.kv + (base + j) * a.ldkv + a.k_col0 + g * a.dh;
+                float dot = 0.f;
+                for (int c = 0; c < a.dh; ++c) dot = fmaf(qv[c], kr[c], dot);
+                wgt = silu_precise(dot);
+            }
+            const int n = min(32, p - j0);
+            for (int jj = 0; jj < n; ++jj) {
+                const float wj = __shfl_sync(0xffffffffu, wgt, jj);
+                const float* vr = a.kv + (base + j0 + jj) * a.ldkv + a.v_col0 + g * a.dh;
+#pragma unroll
+                for (int m = 0; m < 8; ++m) {
+                    const int c = lane + 32 * m;
+                    if (c < a.dh) acc[m] = fmaf(wj, vr[c], acc[m]);
+                }
+            }
+        }
+        if (self >= 0) {
+            const float* kr = a.kv + (long long)self * a.ldkv + a.k_col0 + g * a.dh;
+            const float* vr = a.kv + (long long)self * a.ldkv + a.v_col0 + g * a.dh;
+            float dot = 0.f;
+            for (int c = 0; c < a.dh; ++c) dot = fmaf(qv[c], kr[c], dot);
+            const float ws = silu_precise(dot);
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                const int c = lane + 32 * m;
+                if (c < a.dh) acc[m] = fmaf(ws, vr[c], acc[m]);
+            }
+        }
+        const float s = a.scale[i];
+        float* orow = a.out + i * a.ldo + h * a.dh;
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            const int c = lane + 32 * m;
+            if (c < a.dh) orow[c] = acc[m] * s;
+        }
+        __syncwarp();
+    }
+}
+
+void launch_attn_simt(const SimtAttn& a, cudaStream_t st) {
+    if (a.n_q == 0) return;
+    const int wpb = 8;
+    const int blocks = static_cast<int>(std::min<long long>(cdiv(a.n_q * a.heads, wpb), 148ll * 64));
+    attn_simt_kernel<<<blocks, wpb * 32, wpb * a.dh * sizeof(float), st>>>(a);
+}
+
+}  // namespace mtfm

@@ -1,0 +1,1503 @@
+// model.cu — host side of libmtfm_cuda.so: the C ABI of include/mtfm_cuda.h.
+//
+// Owns the device weights (fp32 originals for the check mode, bf16 K-major
+// copies for the tensor-core path), lays out each packed batch (row space =
+// all context tokens of all users, then all T tokens; per-source tokenizer
+// regions; attention tile tables), encodes the TMA descriptors and enqueues
+// the forward (model.hpp:265-312 for every user at once):
+//
+//   plan -> gather -> tokenizer MLP (2 grouped GEMMs) -> per layer
+//   [GLN1 -> projection GEMM(s) -> attention -> gate -> f2 GEMM (+residual)]
+//   -> heads GEMM -> heads/records.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/mtfm_cuda.h"
+#include "attn_tc.cuh"
+#include "common.cuh"
+#include "gemm_tc.cuh"
+#include "kernels.cuh"
+
+namespace mtfm {
+
+// ---------------------------------------------------------------- errors
+namespace {
+thread_local std::string g_last_error;
+
+struct Error : std::runtime_error {
+    mtfm_status status;
+    Error(mtfm_status s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+[[noreturn]] void fail(mtfm_status s, const std::string& m) { throw Error(s, m); }
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(MTFM_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <typename F>
+mtfm_status guard(F&& f) {
+    try {
+        f();
+        return MTFM_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.status;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return MTFM_CONTRACT_ERROR;
+    }
+}
+
+// ---------------------------------------------------------------- TMA
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+    static EncodeFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        ck(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q), "driver entry point");
+        if (!p || q != cudaDriverEntryPointSuccess) fail(MTFM_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<EncodeFn>(p);
+    }
+    return fn;
+}
+
+// 2-D bf16 tensor map over a row-major [rows][cols] matrix with row stride ld.
+CUtensorMap tma_2d(const void* ptr, long long rows, long long cols, long long ld, int box_cols, int box_rows,
+                   int swizzle_bytes) {
+    CUtensorMap m;
+    std::memset(&m, 0, sizeof(m));
+    if (rows == 0) return m;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
+    cuuint32_t es[2] = {1, 1};
+    CUtensorMapSwizzle sw = swizzle_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                            : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                            : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                  : CU_TENSOR_MAP_SWIZZLE_NONE;
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(MTFM_CUDA_ERROR, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+    return m;
+}
+
+// ---------------------------------------------------------------- device buffers
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    void alloc(size_t n) {
+        if (n <= bytes && p) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        if (n == 0) return;
+        ck(cudaMalloc(&p, n), "cudaMalloc");
+        bytes = n;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+template <typename T>
+void upload(DevBuf& d, const std::vector<T>& h, cudaStream_t st) {
+    d.alloc(std::max<size_t>(h.size() * sizeof(T), 16));
+    if (!h.empty()) ck(cudaMemcpyAsync(d.p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, st), "H2D");
+}
+
+template <typename T>
+void upload_raw(DevBuf& d, const T* h, size_t n, cudaStream_t st) {
+    d.alloc(std::max<size_t>(n * sizeof(T), 16));
+    if (n) ck(cudaMemcpyAsync(d.p, h, n * sizeof(T), cudaMemcpyHostToDevice, st), "H2D");
+}
+
+uint16_t f2bf(float f) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    if ((u & 0x7fffffffu) > 0x7f800000u) return 0x7fc0;
+    const uint32_t lsb = (u >> 16) & 1u;
+    u += 0x7fffu + lsb;
+    return static_cast<uint16_t>(u >> 16);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- model
+struct ParamSpec {
+    std::string name;
+    long long rows, cols;
+    std::vector<float> host;
+    bool set = false;
+};
+
+struct LayerW {
+    bool target;
+    // fp32 originals ([in][out]) for check mode
+    DevBuf w1, w2, b1, b2, wkv, bkv;  // full: w1=f1, b1=f1_b ; target: w1=fuq, wkv=fkv
+    DevBuf f2, f2b;
+    DevBuf g1g, g1b, g2g, g2b;        // [n_groups][d] / [n_groups][hd]
+    // bf16 K-major ([out][in]) for the tensor-core path
+    DevBuf t1, tkv, tf2;
+};
+
+struct SourceW {
+    DevBuf w1, b1, w2, b2;  // fp32 [k_pad][2d] (zero rows past k_in), [2d][d]
+    DevBuf t1, t2;          // bf16 [2d][k_pad], [d][2d]
+};
+
+}  // namespace mtfm
+
+struct mtfm_cuda_model {
+    int device = 0;
+    int precision = 0;
+    mtfm_model_desc cfg{};
+    int d = 0, H = 0, G = 0, dh = 0, hd = 0, gd = 0, n_layers = 0;
+    std::vector<mtfm::SourceInfo> sources;
+    std::vector<mtfm::SlotInfo> slots;
+    std::vector<std::string> slot_param;  // embedding param name per slot
+    std::vector<std::vector<std::string>> tasks;  // per scenario source
+    int n_hist = 0, n_rt = 0, n_scen = 0, n_tasks_total = 0;
+    std::vector<mtfm::ParamSpec> params;
+    std::map<std::string, size_t> by_name;
+    bool finalized = false;
+    cudaStream_t stream = nullptr;
+    // device weights
+    mtfm::DevBuf d_src, d_slots;
+    mtfm::DevBuf emb_f32, emb_bf16;
+    std::vector<std::unique_ptr<mtfm::SourceW>> srcw;
+    std::vector<std::unique_ptr<mtfm::LayerW>> layers;
+    mtfm::DevBuf head_w, head_t, head_eb, head_gb, tower_w, tower_b;
+    int head_n = 0;
+    int head_ld = 0;  // head_n rounded up to 8 (16-byte rows)
+    mtfm_run_stats stats{};
+    // per-stage profiling (CUDA events around every launch) — off by default
+    bool profiling = false;
+    struct Prof {
+        std::string name;
+        cudaEvent_t a = nullptr, b = nullptr;
+        double flops = 0, bytes = 0, ms = 0;
+    };
+    std::vector<Prof> prof;
+    size_t prof_n = 0;
+    std::unique_ptr<mtfm_cuda_batch> ws;  // reusable workspace of mtfm_cuda_forward
+};
+
+struct mtfm_cuda_batch {
+    mtfm_cuda_model* m = nullptr;
+    int only_scenario = -1;
+    long long n_users = 0, n_events = 0, n_exp = 0, rows = 0, n_records = 0;
+    // batch arrays
+    mtfm::DevBuf user_id, seq_off, seq_kind, seq_schema, ev_off, ev_ts, ev_feat_off, ev_feats, exp_off, exp_scen,
+        exp_ts, exp_feat_off, exp_blk, exp_feats;
+    // layout
+    std::vector<long long> src_cnt, src_base, emb_base, hid_base;
+    mtfm::DevBuf d_us_off, d_src_base, d_src_cnt, d_emb_base, d_rec_off;
+    int sort_cap = 0;
+    // row meta
+    mtfm::DevBuf r_src, r_item, r_prefix, r_scale, r_self, r_keybase, r_src_rows, t_user, t_exp_ref, t_scen, t_rec0,
+        t_rec_stride, err;
+    // activations
+    mtfm::DevBuf X, XN, P, KV, UQ, A, Gt, E, HID, Y;
+    // attention tiles
+    std::vector<mtfm::AttnTile> h_tiles_full, h_tiles_tgt;
+    mtfm::DevBuf tiles_full, tiles_tgt;
+    // records
+    mtfm::DevBuf rec_user, rec_scen, rec_exp, rec_task, rec_logit, rec_prob;
+    mtfm::DevBuf stat_buf;
+    long long launches = 0;
+    unsigned long long sum_c_ctx = 0, sum_c_t = 0;  // sum of visible keys (stats)
+};
+
+namespace mtfm {
+namespace {
+
+void register_params(mtfm_cuda_model& m) {
+    auto add = [&](const std::string& n, long long r, long long c) {
+        if (m.by_name.count(n)) fail(MTFM_CONFIG_ERROR, "duplicate parameter name: " + n);
+        m.by_name[n] = m.params.size();
+        m.params.push_back({n, r, c, {}, false});
+    };
+    const int d = m.d, hd = m.hd, gd = m.gd, de = m.cfg.d_emb;
+    // model.hpp:377-463 registration order
+    for (const auto& s : m.sources) {
+        std::string base;
+        if (s.kind == 0) base = "tok/h" + std::to_string(s.id);
+        if (s.kind == 1) base = "tok/r" + std::to_string(s.id);
+        if (s.kind == 2) base = "tok/s" + std::to_string(s.id);
+        int slot = s.slot0;
+        if (s.kind < 2) {
+            for (int k = 0; k < s.nslot[0]; ++k, ++slot) {
+                add(base + "/emb" + std::to_string(k), m.slots[slot].vocab, de);
+                m.slot_param[slot] = base + "/emb" + std::to_string(k);
+            }
+        } else {
+            const char* pre[3] = {"/emb_u", "/emb_c", "/emb_i"};
+            for (int blk = 0; blk < 3; ++blk)
+                for (int k = 0; k < s.nslot[blk]; ++k, ++slot) {
+                    add(base + pre[blk] + std::to_string(k), m.slots[slot].vocab, de);
+                    m.slot_param[slot] = base + pre[blk] + std::to_string(k);
+                }
+        }
+        add(base + "/mlp_w1", s.k_in, 2 * d);
+        add(base + "/mlp_b1", 1, 2 * d);
+        add(base + "/mlp_w2", 2 * d, d);
+        add(base + "/mlp_b2", 1, d);
+    }
+    const int n_groups = static_cast<int>(m.sources.size());
+    for (int b = 0; b < m.cfg.blocks; ++b)
+        for (int l = 0; l < m.cfg.target_layers + m.cfg.full_layers; ++l) {
+            const bool tgt = l < m.cfg.target_layers;
+            const std::string base = "hta/b" + std::to_string(b) + "/l" + std::to_string(l);
+            if (tgt) {
+                add(base + "/fuq_w", d, 2 * hd);
+                add(base + "/fuq_b", 1, 2 * hd);
+                add(base + "/fkv_w", d, 2 * gd);
+                add(base + "/fkv_b", 1, 2 * gd);
+            } else {
+                add(base + "/f1_w", d, 2 * hd + 2 * gd);
+                add(base + "/f1_b", 1, 2 * hd + 2 * gd);
+            }
+            add(base + "/f2_w", hd, d);
+            add(base + "/f2_b", 1, d);
+            for (int g = 0; g < n_groups; ++g) {
+                const auto& s = m.sources[g];
+                const std::string key = std::string(s.kind == 0 ? "h" : (s.kind == 1 ? "r" : "t")) + std::to_string(s.id);
+                add(base + "/gln1/" + key + "/gain", 1, d);
+                add(base + "/gln1/" + key + "/bias", 1, d);
+                if (!tgt || s.kind == 2) {
+                    add(base + "/gln2/" + key + "/gain", 1, hd);
+                    add(base + "/gln2/" + key + "/bias", 1, hd);
+                }
+            }
+        }
+    for (int e = 0; e < m.cfg.experts; ++e) {
+        add("head/expert" + std::to_string(e) + "_w", d, m.cfg.d_expert);
+        add("head/expert" + std::to_string(e) + "_b", 1, m.cfg.d_expert);
+    }
+    for (const auto& s : m.sources) {
+        if (s.kind != 2) continue;
+        for (const auto& t : m.tasks[&s - m.sources.data()]) {
+            const std::string base = "head/s" + std::to_string(s.id) + "/" + t;
+            add(base + "/gate_w", d, m.cfg.experts);
+            add(base + "/gate_b", 1, m.cfg.experts);
+            add(base + "/tower_w", m.cfg.d_expert, 1);
+            add(base + "/tower_b", 1, 1);
+        }
+    }
+}
+
+const std::vector<float>& P(mtfm_cuda_model& m, const std::string& n) {
+    auto it = m.by_name.find(n);
+    if (it == m.by_name.end()) fail(MTFM_CONFIG_ERROR, "unknown parameter: " + n);
+    return m.params[it->second].host;
+}
+
+// [rows][cols] f32 -> bf16 [cols][kpad] (transposed, zero padded along k)
+std::vector<uint16_t> to_kmajor_bf16(const std::vector<float>& w, long long rows, long long cols, long long kpad) {
+    std::vector<uint16_t> t(static_cast<size_t>(cols * kpad), 0);
+    for (long long r = 0; r < rows; ++r)
+        for (long long c = 0; c < cols; ++c) t[c * kpad + r] = f2bf(w[r * cols + c]);
+    return t;
+}
+
+void finalize(mtfm_cuda_model& m) {
+    if (m.finalized) return;
+    for (const auto& p : m.params)
+        if (!p.set) fail(MTFM_CONFIG_ERROR, "parameter not set: " + p.name);
+    cudaStream_t st = m.stream;
+    const int d = m.d, hd = m.hd, gd = m.gd, de = m.cfg.d_emb;
+    // embeddings: one flat table buffer
+    std::vector<float> emb;
+    for (size_t s = 0; s < m.slots.size(); ++s) {
+        m.slots[s].emb_off = static_cast<long long>(emb.size());
+        const auto& w = P(m, m.slot_param[s]);
+        emb.insert(emb.end(), w.begin(), w.end());
+        while (emb.size() % 8) emb.push_back(0.f);
+    }
+    upload(m.emb_f32, emb, st);
+    std::vector<uint16_t> embh(emb.size());
+    for (size_t i = 0; i < emb.size(); ++i) embh[i] = f2bf(emb[i]);
+    upload(m.emb_bf16, embh, st);
+    upload(m.d_slots, m.slots, st);
+    // tokenizer MLPs
+    for (const auto& s : m.sources) {
+        auto w = std::make_unique<SourceW>();
+        std::string base = s.kind == 0 ? "tok/h" : (s.kind == 1 ? "tok/r" : "tok/s");
+        base += std::to_string(s.id);
+        std::vector<float> w1 = P(m, base + "/mlp_w1");
+        w1.resize(static_cast<size_t>(s.k_pad) * 2 * d, 0.f);  // zero rows past k_in
+        upload(w->w1, w1, st);
+        upload(w->b1, P(m, base + "/mlp_b1"), st);
+        upload(w->w2, P(m, base + "/mlp_w2"), st);
+        upload(w->b2, P(m, base + "/mlp_b2"), st);
+        upload(w->t1, to_kmajor_bf16(P(m, base + "/mlp_w1"), s.k_in, 2 * d, s.k_pad), st);
+        upload(w->t2, to_kmajor_bf16(P(m, base + "/mlp_w2"), 2 * d, d, 2 * d), st);
+        m.srcw.push_back(std::move(w));
+    }
+    // stack
+    const int n_groups = static_cast<int>(m.sources.size());
+    for (int b = 0; b < m.cfg.blocks; ++b)
+        for (int l = 0; l < m.cfg.target_layers + m.cfg.full_layers; ++l) {
+            auto L = std::make_unique<LayerW>();
+            L->target = l < m.cfg.target_layers;
+            const std::string base = "hta/b" + std::to_string(b) + "/l" + std::to_string(l);
+            if (L->target) {
+                upload(L->w1, P(m, base + "/fuq_w"), st);
+                upload(L->b1, P(m, base + "/fuq_b"), st);
+                upload(L->wkv, P(m, base + "/fkv_w"), st);
+                upload(L->bkv, P(m, base + "/fkv_b"), st);
+                upload(L->t1, to_kmajor_bf16(P(m, base + "/fuq_w"), d, 2 * hd, d), st);
+                upload(L->tkv, to_kmajor_bf16(P(m, base + "/fkv_w"), d, 2 * gd, d), st);
+            } else {
+                upload(L->w1, P(m, base + "/f1_w"), st);
+                upload(L->b1, P(m, base + "/f1_b"), st);
+                upload(L->t1, to_kmajor_bf16(P(m, base + "/f1_w"), d, 2 * hd + 2 * gd, d), st);
+            }
+            upload(L->f2, P(m, base + "/f2_w"), st);
+            upload(L->f2b, P(m, base + "/f2_b"), st);
+            upload(L->tf2, to_kmajor_bf16(P(m, base + "/f2_w"), hd, d, hd), st);
+            std::vector<float> g1g, g1b, g2g, g2b;
+            for (int g = 0; g < n_groups; ++g) {
+                const auto& s = m.sources[g];
+                const std::string key = std::string(s.kind == 0 ? "h" : (s.kind == 1 ? "r" : "t")) + std::to_string(s.id);
+                const auto& a = P(m, base + "/gln1/" + key + "/gain");
+                const auto& c = P(m, base + "/gln1/" + key + "/bias");
+                g1g.insert(g1g.end(), a.begin(), a.end());
+                g1b.insert(g1b.end(), c.begin(), c.end());
+                if (!L->target || s.kind == 2) {
+                    const auto& e = P(m, base + "/gln2/" + key + "/gain");
+                    const auto& f = P(m, base + "/gln2/" + key + "/bias");
+                    g2g.insert(g2g.end(), e.begin(), e.end());
+                    g2b.insert(g2b.end(), f.begin(), f.end());
+                } else {  // never read: target layers gate-normalise T rows only
+                    g2g.insert(g2g.end(), hd, 1.f);
+                    g2b.insert(g2b.end(), hd, 0.f);
+                }
+            }
+            upload(L->g1g, g1g, st);
+            upload(L->g1b, g1b, st);
+            upload(L->g2g, g2g, st);
+            upload(L->g2b, g2b, st);
+            m.layers.push_back(std::move(L));
+        }
+    // heads: [d][E*de | n_tasks*E]
+    const int E = m.cfg.experts, dx = m.cfg.d_expert;
+    m.head_n = E * dx + m.n_tasks_total * E;
+    m.head_ld = static_cast<int>(round_up(m.head_n, 8));
+    std::vector<float> hw(static_cast<size_t>(d) * m.head_n, 0.f), eb, gb, tw, tb;
+    for (int e = 0; e < E; ++e) {
+        const auto& w = P(m, "head/expert" + std::to_string(e) + "_w");
+        for (int r = 0; r < d; ++r)
+            for (int c = 0; c < dx; ++c) hw[static_cast<size_t>(r) * m.head_n + e * dx + c] = w[r * dx + c];
+        const auto& b = P(m, "head/expert" + std::to_string(e) + "_b");
+        eb.insert(eb.end(), b.begin(), b.end());
+    }
+    int task = 0;
+    for (size_t si = 0; si < m.sources.size(); ++si) {
+        const auto& s = m.sources[si];
+        if (s.kind != 2) continue;
+        for (const auto& t : m.tasks[si]) {
+            const std::string base = "head/s" + std::to_string(s.id) + "/" + t;
+            const auto& w = P(m, base + "/gate_w");
+            for (int r = 0; r < d; ++r)
+                for (int c = 0; c < E; ++c) hw[static_cast<size_t>(r) * m.head_n + E * dx + task * E + c] = w[r * E + c];
+            const auto& b = P(m, base + "/gate_b");
+            gb.insert(gb.end(), b.begin(), b.end());
+            const auto& tw1 = P(m, base + "/tower_w");
+            tw.insert(tw.end(), tw1.begin(), tw1.end());
+            tb.push_back(P(m, base + "/tower_b")[0]);
+            ++task;
+        }
+    }
+    upload(m.head_w, hw, st);
+    upload(m.head_t, to_kmajor_bf16(hw, d, m.head_n, d), st);
+    upload(m.head_eb, eb, st);
+    upload(m.head_gb, gb, st);
+    upload(m.tower_w, tw, st);
+    upload(m.tower_b, tb, st);
+    upload(m.d_src, m.sources, st);
+    ck(cudaStreamSynchronize(st), "weight upload");
+    m.finalized = true;
+}
+
+// ---------------------------------------------------------------- GEMM launch helpers
+template <int BN>
+void launch_gemm_tc_bn(GemmArgs& a, cudaStream_t st) {
+    using C = gemm_detail::Cfg<BN>;
+    static bool attr = false;
+    if (!attr) {
+        ck(cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM),
+           "gemm smem attr");
+        attr = true;
+    }
+    const int grid = std::min(a.n_tiles, kNumSMs);
+    gemm_tc_kernel<BN><<<grid, C::kThreads, C::SMEM, st>>>(a);
+    ck(cudaGetLastError(), "gemm_tc launch");
+}
+
+struct TcProblem {
+    const __nv_bfloat16* A;
+    long long lda;
+    const __nv_bfloat16* Bt;  // [N][K]
+    long long ldb;
+    int M, N, K;
+    int epi;
+    const float* bias;
+    void* out;
+    long long ldo;
+    const int* row_map;
+    long long row_offset;
+    const float* resid;
+};
+
+int pick_bn(const std::vector<TcProblem>& ps) {
+    int best = 256;
+    double best_eff = -1;
+    for (int bn : {256, 128, 64}) {
+        double used = 0, padded = 0;
+        for (const auto& p : ps) {
+            used += p.N;
+            padded += static_cast<double>(cdiv(p.N, bn) * bn);
+        }
+        const double eff = used / std::max(padded, 1.0);
+        if (eff > best_eff + 0.02) {
+            best_eff = eff;
+            best = bn;
+        }
+    }
+    return best;
+}
+
+void run_gemm_tc(std::vector<TcProblem> ps, cudaStream_t st, long long& launches) {
+    ps.erase(std::remove_if(ps.begin(), ps.end(), [](const TcProblem& p) { return p.M == 0 || p.N == 0; }),
+             ps.end());
+    if (ps.empty()) return;
+    const int bn = pick_bn(ps);
+    for (size_t i0 = 0; i0 < ps.size(); i0 += kMaxProblems) {
+        GemmArgs a;
+        std::memset(&a, 0, sizeof(a));
+        int tiles = 0;
+        for (size_t i = i0; i < std::min(ps.size(), i0 + kMaxProblems); ++i) {
+            const auto& s = ps[i];
+            GemmProblem& p = a.p[a.n_problems++];
+            p.tma_a = tma_2d(s.A, s.M, s.K, s.lda, 64, 128, 128);
+            p.tma_b = tma_2d(s.Bt, s.N, s.K, s.ldb, 64, bn, 128);
+            p.M = s.M;
+            p.N = s.N;
+            p.K = static_cast<int>(round_up(s.K, 64));
+            p.tile_start = tiles;
+            p.tiles_n = static_cast<int>(cdiv(s.N, bn));
+            p.epi = s.epi;
+            p.bias = s.bias;
+            p.out = s.out;
+            p.ldo = s.ldo;
+            p.row_map = s.row_map;
+            p.row_offset = s.row_offset;
+            p.resid = s.resid;
+            tiles += static_cast<int>(cdiv(s.M, 128)) * p.tiles_n;
+        }
+        a.n_tiles = tiles;
+        if (bn == 256) launch_gemm_tc_bn<256>(a, st);
+        else if (bn == 128) launch_gemm_tc_bn<128>(a, st);
+        else launch_gemm_tc_bn<64>(a, st);
+        ++launches;
+    }
+}
+
+void run_gemm_simt(std::vector<SimtGemm> ps, cudaStream_t st, long long& launches) {
+    ps.erase(std::remove_if(ps.begin(), ps.end(), [](const SimtGemm& p) { return p.M == 0 || p.N == 0; }),
+             ps.end());
+    for (size_t i0 = 0; i0 < ps.size(); i0 += kMaxProblems) {
+        launch_gemm_simt(ps.data() + i0, static_cast<int>(std::min<size_t>(kMaxProblems, ps.size() - i0)), st);
+        ck(cudaGetLastError(), "gemm_simt launch");
+        ++launches;
+    }
+}
+
+// ---------------------------------------------------------------- attention helpers
+__global__ void tile_kmax_kernel(AttnTile* tiles, int n, const int* prefix, int rt_unused) {
+    const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (t >= n) return;
+    AttnTile tl = tiles[t];
+    int mx = 0;
+    for (int i = lane; i < tl.n_rows; i += 32) mx = max(mx, prefix[tl.q_row0 + i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) tiles[t].kmax = mx;
+}
+
+struct AttnGeom {
+    int hs, rt;
+};
+AttnGeom attn_geom(const mtfm_cuda_model& m) {
+    const int r = m.H / m.G;
+    if (r <= 128 && 128 % r == 0 && 128 / r >= 8) return {r, 128 / r};
+    return {1, 128};
+}
+
+template <int D>
+void launch_attn_tc_d(const AttnParams& p, cudaStream_t st) {
+    using C = attn_detail::Cfg<D>;
+    static bool attr = false;
+    if (!attr) {
+        ck(cudaFuncSetAttribute(attn_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM),
+           "attn smem attr");
+        attr = true;
+    }
+    const int grid = std::min(p.n_tiles, kNumSMs);
+    attn_tc_kernel<D><<<grid, 384, C::SMEM, st>>>(p);
+    ck(cudaGetLastError(), "attn_tc launch");
+}
+
+void run_attn_tc(const mtfm_cuda_model& m, AttnParams p, const __nv_bfloat16* q, long long n_q, long long q_cols,
+                 long long kv_rows, long long kv_cols, cudaStream_t st) {
+    if (p.n_tiles == 0) return;
+    const int D = m.dh;
+    const int chunk = std::min(D, 64);
+    const int bkv = D <= 128 ? 128 : 64;
+    p.tma_q = tma_2d(q, n_q, q_cols, p.ldq, chunk, p.rt, chunk * 2);
+    p.tma_kv = tma_2d(p.kv_ptr, kv_rows, kv_cols, p.ldkv, chunk, bkv, chunk * 2);
+    switch (D) {
+        case 16: launch_attn_tc_d<16>(p, st); break;
+        case 32: launch_attn_tc_d<32>(p, st); break;
+        case 64: launch_attn_tc_d<64>(p, st); break;
+        case 128: launch_attn_tc_d<128>(p, st); break;
+        case 256: launch_attn_tc_d<256>(p, st); break;
+        default: fail(MTFM_CONFIG_ERROR, "bf16 attention supports head_dim in {16,32,64,128,256}");
+    }
+}
+
+// ---------------------------------------------------------------- batch layout
+long long next_pow2(long long n) {
+    long long p = 1;
+    while (p < n) p <<= 1;
+    return p;
+}
+
+int source_of(const mtfm_cuda_model& m, int kind, int id, int only_scenario) {
+    for (size_t s = 0; s < m.sources.size(); ++s)
+        if (m.sources[s].kind == kind && m.sources[s].id == id) {
+            if (kind == 2 && only_scenario >= 0 && id != only_scenario) return -1;
+            return static_cast<int>(s);
+        }
+    return -1;
+}
+
+void check_batch(const mtfm_packed_batch* b) {
+    if (!b) fail(MTFM_CONTRACT_ERROR, "null batch");
+    if (b->n_users < 0 || b->n_seqs < 0 || b->n_events < 0 || b->n_exposures < 0)
+        fail(MTFM_DIMENSION_ERROR, "negative batch sizes");
+    if (b->n_users > 0 && (!b->seq_off || !b->exp_off || !b->user_id)) fail(MTFM_CONTRACT_ERROR, "null batch arrays");
+    if (b->seq_off && b->seq_off[b->n_users] != b->n_seqs) fail(MTFM_DIMENSION_ERROR, "seq_off does not end at n_seqs");
+    if (b->exp_off && b->exp_off[b->n_users] != b->n_exposures)
+        fail(MTFM_DIMENSION_ERROR, "exp_off does not end at n_exposures");
+    if (b->n_seqs && b->ev_off[b->n_seqs] != b->n_events) fail(MTFM_DIMENSION_ERROR, "ev_off does not end at n_events");
+    for (int u = 0; u < b->n_users; ++u)
+        if (b->seq_off[u + 1] < b->seq_off[u] || b->exp_off[u + 1] < b->exp_off[u])
+            fail(MTFM_DIMENSION_ERROR, "batch offsets not monotone");
+}
+
+void prepare(mtfm_cuda_model& m, const mtfm_packed_batch* hb, int only_scenario, mtfm_cuda_batch& B) {
+    check_batch(hb);
+    finalize(m);
+    cudaStream_t st = m.stream;
+    B.m = &m;
+    B.only_scenario = only_scenario;
+    B.n_users = hb->n_users;
+    B.n_events = hb->n_events;
+    B.n_exp = hb->n_exposures;
+    B.rows = B.n_events + B.n_exp;
+    const int n_src = static_cast<int>(m.sources.size());
+    // upload the batch
+    upload_raw(B.user_id, hb->user_id, hb->n_users, st);
+    upload_raw(B.seq_off, hb->seq_off, hb->n_users + 1, st);
+    upload_raw(B.seq_kind, hb->seq_kind, hb->n_seqs, st);
+    upload_raw(B.seq_schema, hb->seq_schema, hb->n_seqs, st);
+    upload_raw(B.ev_off, hb->n_seqs ? hb->ev_off : nullptr, hb->n_seqs ? hb->n_seqs + 1 : 0, st);
+    if (!hb->n_seqs) {
+        const int zero = 0;
+        upload_raw(B.ev_off, &zero, 1, st);
+    }
+    upload_raw(B.ev_ts, hb->ev_ts, hb->n_events, st);
+    upload_raw(B.ev_feat_off, hb->ev_feat_off, hb->n_events + 1, st);
+    upload_raw(B.ev_feats, hb->ev_feats, hb->n_ev_feats, st);
+    upload_raw(B.exp_off, hb->exp_off, hb->n_users + 1, st);
+    upload_raw(B.exp_scen, hb->exp_scenario, hb->n_exposures, st);
+    upload_raw(B.exp_ts, hb->exp_ts, hb->n_exposures, st);
+    upload_raw(B.exp_feat_off, hb->exp_feat_off, hb->n_exposures + 1, st);
+    upload_raw(B.exp_blk, hb->exp_blk, 3ll * hb->n_exposures, st);
+    upload_raw(B.exp_feats, hb->exp_feats, hb->n_exp_feats, st);
+
+    // host layout: per (user, source) counts -> source regions, record offsets
+    std::vector<long long> us(static_cast<size_t>(B.n_users) * n_src, 0);
+    std::vector<long long> rec_off(B.n_users + 1, 0);
+    long long max_sort = 1;
+    for (int u = 0; u < hb->n_users; ++u) {
+        long long n_ev = 0;
+        for (int s = hb->seq_off[u]; s < hb->seq_off[u + 1]; ++s) {
+            const int src = source_of(m, hb->seq_kind[s] ? 1 : 0, hb->seq_schema[s], -1);
+            const long long len = hb->ev_off[s + 1] - hb->ev_off[s];
+            n_ev += len;
+            if (src >= 0) us[static_cast<size_t>(u) * n_src + src] += len;
+        }
+        long long recs = 0;
+        for (int x = hb->exp_off[u]; x < hb->exp_off[u + 1]; ++x) {
+            const int src = source_of(m, 2, hb->exp_scenario[x], only_scenario);
+            if (src >= 0) {
+                us[static_cast<size_t>(u) * n_src + src] += 1;
+                recs += m.sources[src].ntasks;
+            }
+        }
+        rec_off[u + 1] = rec_off[u] + recs;
+        const long long n_t = hb->exp_off[u + 1] - hb->exp_off[u];
+        max_sort = std::max({max_sort, next_pow2(n_ev), next_pow2(n_t) + n_ev});
+    }
+    B.n_records = rec_off[B.n_users];
+    if (max_sort > 12288)
+        fail(MTFM_CONTRACT_ERROR, "a user has more than 12288 tokens to plan (per-CTA sort capacity)");
+    B.sort_cap = static_cast<int>(max_sort);
+    B.src_cnt.assign(n_src, 0);
+    B.src_base.assign(n_src, 0);
+    B.emb_base.assign(n_src, 0);
+    B.hid_base.assign(n_src, 0);
+    std::vector<long long> us_off(us.size(), 0);
+    for (int s = 0; s < n_src; ++s)
+        for (int u = 0; u < hb->n_users; ++u) {
+            us_off[static_cast<size_t>(u) * n_src + s] = B.src_cnt[s];
+            B.src_cnt[s] += us[static_cast<size_t>(u) * n_src + s];
+        }
+    long long pos = 0, eb = 0, hbse = 0;
+    for (int s = 0; s < n_src; ++s) {
+        B.src_base[s] = pos;
+        B.emb_base[s] = eb;
+        B.hid_base[s] = hbse;
+        pos += B.src_cnt[s];
+        eb += B.src_cnt[s] * m.sources[s].k_pad;
+        hbse += B.src_cnt[s] * 2 * m.d;
+    }
+    upload(B.d_us_off, us_off, st);
+    upload(B.d_src_base, B.src_base, st);
+    upload(B.d_src_cnt, B.src_cnt, st);
+    upload(B.d_emb_base, B.emb_base, st);
+    upload(B.d_rec_off, rec_off, st);
+
+    // attention tiles
+    const AttnGeom ag = attn_geom(m);
+    const int r = m.H / m.G;
+    B.h_tiles_full.clear();
+    B.h_tiles_tgt.clear();
+    for (int u = 0; u < hb->n_users; ++u) {
+        const long long ev0 = hb->n_seqs ? hb->ev_off[hb->seq_off[u]] : 0;
+        const long long ev1 = hb->n_seqs ? hb->ev_off[hb->seq_off[u + 1]] : 0;
+        const long long x0 = hb->exp_off[u], x1 = hb->exp_off[u + 1];
+        for (int g = 0; g < m.G; ++g)
+            for (int hb0 = 0; hb0 < r; hb0 += ag.hs) {
+                const int head0 = g * r + hb0;
+                for (long long q = ev0; q < ev1; q += ag.rt)
+                    B.h_tiles_full.push_back({static_cast<int>(q), static_cast<int>(std::min<long long>(ag.rt, ev1 - q)),
+                                              static_cast<int>(ev0), head0, 0, {0, 0, 0}});
+                for (long long q = x0; q < x1; q += ag.rt) {
+                    const int n = static_cast<int>(std::min<long long>(ag.rt, x1 - q));
+                    B.h_tiles_full.push_back({static_cast<int>(B.n_events + q), n, static_cast<int>(ev0), head0, 0, {0, 0, 0}});
+                    B.h_tiles_tgt.push_back({static_cast<int>(q), n, static_cast<int>(ev0), head0, 0, {0, 0, 0}});
+                }
+            }
+    }
+    upload(B.tiles_full, B.h_tiles_full, st);
+    upload(B.tiles_tgt, B.h_tiles_tgt, st);
+
+    // row meta + activations
+    const long long R = B.rows, T = B.n_exp;
+    auto ia = [&](DevBuf& b, long long n, size_t el) { b.alloc(std::max<size_t>(static_cast<size_t>(n) * el, 16)); };
+    ia(B.r_src, R, 4);
+    ia(B.r_item, R, 4);
+    ia(B.r_prefix, R, 4);
+    ia(B.r_scale, R, 4);
+    ia(B.r_self, R, 4);
+    ia(B.r_keybase, R, 4);
+    ia(B.r_src_rows, R, 4);
+    ia(B.t_user, T, 4);
+    ia(B.t_exp_ref, T, 4);
+    ia(B.t_scen, T, 4);
+    ia(B.t_rec0, T, 8);
+    ia(B.t_rec_stride, T, 4);
+    ia(B.err, 1, 8);
+    const size_t el = m.precision == MTFM_PRECISION_BF16 ? 2 : 4;
+    const int pw = 2 * m.hd + 2 * m.gd;
+    ia(B.X, R * m.d, 4);
+    ia(B.XN, R * m.d, el);
+    ia(B.P, R * pw, el);
+    ia(B.KV, R * 2 * m.gd, el);
+    ia(B.UQ, T * 2 * m.hd, el);
+    ia(B.A, R * m.hd, el);
+    ia(B.Gt, R * m.hd, el);
+    ia(B.E, eb, el);
+    ia(B.HID, hbse, el);
+    ia(B.Y, T * m.head_ld, 4);
+    const long long nr = B.n_records;
+    ia(B.rec_user, nr, 8);
+    ia(B.rec_scen, nr, 4);
+    ia(B.rec_exp, nr, 4);
+    ia(B.rec_task, nr, 4);
+    ia(B.rec_logit, nr, 4);
+    ia(B.rec_prob, nr, 8);
+}
+
+DevBatch dev_batch(const mtfm_cuda_batch& B) {
+    DevBatch b;
+    b.n_users = static_cast<int>(B.n_users);
+    b.n_seqs = 0;
+    b.n_events = static_cast<int>(B.n_events);
+    b.n_exposures = static_cast<int>(B.n_exp);
+    b.user_id = B.user_id.as<long long>();
+    b.seq_off = B.seq_off.as<int>();
+    b.seq_kind = B.seq_kind.as<uint8_t>();
+    b.seq_schema = B.seq_schema.as<int>();
+    b.ev_off = B.ev_off.as<int>();
+    b.ev_ts = B.ev_ts.as<long long>();
+    b.ev_feat_off = B.ev_feat_off.as<int>();
+    b.ev_feats = B.ev_feats.as<int>();
+    b.exp_off = B.exp_off.as<int>();
+    b.exp_scenario = B.exp_scen.as<int>();
+    b.exp_ts = B.exp_ts.as<long long>();
+    b.exp_feat_off = B.exp_feat_off.as<int>();
+    b.exp_blk = B.exp_blk.as<int>();
+    b.exp_feats = B.exp_feats.as<int>();
+    return b;
+}
+
+RowMeta row_meta(const mtfm_cuda_batch& B) {
+    RowMeta r;
+    r.src = B.r_src.as<int>();
+    r.item = B.r_item.as<int>();
+    r.prefix = B.r_prefix.as<int>();
+    r.scale = B.r_scale.as<float>();
+    r.self = B.r_self.as<int>();
+    r.keybase = B.r_keybase.as<int>();
+    r.src_rows = B.r_src_rows.as<int>();
+    r.t_user = B.t_user.as<int>();
+    r.t_exp_ref = B.t_exp_ref.as<int>();
+    r.t_scen = B.t_scen.as<int>();
+    r.t_rec0 = B.t_rec0.as<long long>();
+    r.t_rec_stride = B.t_rec_stride.as<int>();
+    return r;
+}
+
+// ---------------------------------------------------------------- profiling
+struct StageScope {
+    mtfm_cuda_model& m;
+    bool on;
+    size_t idx = 0;
+    StageScope(mtfm_cuda_model& mm, const char* name, double flops, double bytes) : m(mm), on(mm.profiling) {
+        if (!on) return;
+        if (m.prof_n == m.prof.size()) {
+            m.prof.emplace_back();
+            ck(cudaEventCreate(&m.prof.back().a), "event");
+            ck(cudaEventCreate(&m.prof.back().b), "event");
+        }
+        idx = m.prof_n++;
+        auto& e = m.prof[idx];
+        e.name = name;
+        e.flops = flops;
+        e.bytes = bytes;
+        ck(cudaEventRecord(e.a, m.stream), "event record");
+    }
+    ~StageScope() {
+        if (on) cudaEventRecord(m.prof[idx].b, m.stream);
+    }
+};
+
+// ---------------------------------------------------------------- the forward
+template <typename T>
+void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
+    constexpr bool kTc = std::is_same<T, __nv_bfloat16>::value;
+    constexpr double el = sizeof(T);
+    cudaStream_t st = m.stream;
+    long long& L = B.launches;
+    L = 0;
+    m.prof_n = 0;
+    const int n_src = static_cast<int>(m.sources.size());
+    const int d = m.d, hd = m.hd, gd = m.gd, dh = m.dh;
+    const int pw = 2 * hd + 2 * gd;
+    const long long R = B.rows, NE = B.n_events, NT = B.n_exp;
+    const double Rd = static_cast<double>(R), Td = static_cast<double>(NT);
+    const float eps = static_cast<float>(m.cfg.eps);
+    if (B.n_users == 0) return;
+    RowMeta rm = row_meta(B);
+    ck(cudaMemsetAsync(B.err.p, 0xff, 8, st), "memset err");
+
+    // ---- K0: plan (tokenizer.hpp:53-134 + make_stack_geom in prefix form)
+    PlanArgs pa{};
+    pa.b = dev_batch(B);
+    pa.src = m.d_src.as<SourceInfo>();
+    pa.slots = m.d_slots.as<SlotInfo>();
+    pa.n_src = n_src;
+    pa.n_hist = m.n_hist;
+    pa.n_rt = m.n_rt;
+    pa.norm = m.cfg.norm;
+    pa.only_scenario = B.only_scenario;
+    pa.us_off = B.d_us_off.as<long long>();
+    pa.src_base = B.d_src_base.as<long long>();
+    pa.rec_off = B.d_rec_off.as<long long>();
+    pa.rm = rm;
+    pa.err = B.err.as<unsigned long long>();
+    pa.max_sort = B.sort_cap;
+    {
+        StageScope sc(m, "plan", 0, Rd * 8 * 4 + Rd * 7 * 4);
+        launch_plan(pa, B.sort_cap, st);
+        ck(cudaGetLastError(), "plan launch");
+        ++L;
+    }
+
+    // ---- K1: tokenizer (embedding gather + 2-layer SiLU MLP per source)
+    T* E = B.E.as<T>();
+    T* HID = B.HID.as<T>();
+    int max_slots = 0;
+    for (const auto& s : m.sources) max_slots = std::max(max_slots, s.nslot[0] + s.nslot[1] + s.nslot[2]);
+    long long tok_rows = 0;
+    double tok_f1 = 0, tok_f2 = 0, tok_in = 0;
+    for (int s = 0; s < n_src; ++s) {
+        tok_rows += B.src_cnt[s];
+        tok_f1 += 2.0 * B.src_cnt[s] * m.sources[s].k_in * 2 * d;
+        tok_f2 += 2.0 * B.src_cnt[s] * 2 * d * d;
+        tok_in += static_cast<double>(B.src_cnt[s]) * m.sources[s].k_pad;
+    }
+    {
+        StageScope sc(m, "gather", 0, tok_in * el * 2);
+        launch_gather<T>(pa.b, pa.src, pa.slots, rm, B.d_src_base.as<long long>(), B.d_src_cnt.as<long long>(),
+                         B.d_emb_base.as<long long>(),
+                         kTc ? static_cast<const T*>(m.emb_bf16.p) : static_cast<const T*>(m.emb_f32.p), m.cfg.d_emb,
+                         n_src, tok_rows, max_slots, E, st);
+        ck(cudaGetLastError(), "gather launch");
+        ++L;
+    }
+    float* X = B.X.as<float>();
+    if constexpr (kTc) {
+        std::vector<TcProblem> p1, p2;
+        for (int s = 0; s < n_src; ++s) {
+            const auto& si = m.sources[s];
+            const auto& w = *m.srcw[s];
+            const int M = static_cast<int>(B.src_cnt[s]);
+            p1.push_back({E + B.emb_base[s], si.k_pad, w.t1.as<__nv_bfloat16>(), si.k_pad, M, 2 * d, si.k_pad,
+                          EPI_SILU_BF16, w.b1.as<float>(), HID + B.hid_base[s], 2 * d, nullptr, 0, nullptr});
+            p2.push_back({HID + B.hid_base[s], 2 * d, w.t2.as<__nv_bfloat16>(), 2 * d, M, d, 2 * d, EPI_BIAS_F32,
+                          w.b2.as<float>(), X, d, rm.src_rows + B.src_base[s], 0, nullptr});
+        }
+        {
+            StageScope sc(m, "tok_mlp1", tok_f1, tok_in * el + Rd * 2 * d * el);
+            run_gemm_tc(p1, st, L);
+        }
+        {
+            StageScope sc(m, "tok_mlp2", tok_f2, Rd * 2 * d * el + Rd * d * 4);
+            run_gemm_tc(p2, st, L);
+        }
+    } else {
+        std::vector<SimtGemm> p1, p2;
+        for (int s = 0; s < n_src; ++s) {
+            const auto& si = m.sources[s];
+            const auto& w = *m.srcw[s];
+            const int M = static_cast<int>(B.src_cnt[s]);
+            p1.push_back({reinterpret_cast<const float*>(E) + B.emb_base[s], si.k_pad, w.w1.as<float>(), M, 2 * d,
+                          si.k_pad, w.b1.as<float>(), EPI_SILU_BF16, reinterpret_cast<float*>(HID) + B.hid_base[s],
+                          2 * d, nullptr, 0, nullptr});
+            p2.push_back({reinterpret_cast<const float*>(HID) + B.hid_base[s], 2 * d, w.w2.as<float>(), M, d, 2 * d,
+                          w.b2.as<float>(), EPI_BIAS_F32, X, d, rm.src_rows + B.src_base[s], 0, nullptr});
+        }
+        {
+            StageScope sc(m, "tok_mlp1", tok_f1, tok_in * el + Rd * 2 * d * el);
+            run_gemm_simt(p1, st, L);
+        }
+        {
+            StageScope sc(m, "tok_mlp2", tok_f2, Rd * 2 * d * el + Rd * d * 4);
+            run_gemm_simt(p2, st, L);
+        }
+    }
+
+    // ---- attention tile extents (max visible prefix per tile)
+    const AttnGeom ag = attn_geom(m);
+    const int n_full = static_cast<int>(B.h_tiles_full.size());
+    const int n_tgt = static_cast<int>(B.h_tiles_tgt.size());
+    if (kTc && (n_full || n_tgt)) {
+        StageScope sc(m, "tile_kmax", 0, (n_full + n_tgt) * 32.0);
+        if (n_full) {
+            tile_kmax_kernel<<<static_cast<int>(cdiv(n_full, 8)), 256, 0, st>>>(B.tiles_full.as<AttnTile>(), n_full,
+                                                                                rm.prefix, ag.rt);
+            ++L;
+        }
+        if (n_tgt) {
+            tile_kmax_kernel<<<static_cast<int>(cdiv(n_tgt, 8)), 256, 0, st>>>(B.tiles_tgt.as<AttnTile>(), n_tgt,
+                                                                               rm.prefix + NE, ag.rt);
+            ++L;
+        }
+    }
+
+    // ---- K2..K4: the HTA stack (hta.hpp:188-212)
+    T* XN = B.XN.as<T>();
+    T* Pm = B.P.as<T>();
+    T* KV = B.KV.as<T>();
+    T* UQ = B.UQ.as<T>();
+    T* A = B.A.as<T>();
+    T* G = B.Gt.as<T>();
+    // attention FLOPs need sum(c_i): known after the plan; use the value of
+    // the previous results() (same batch) for the profile annotation
+    const double sc_full = static_cast<double>(B.sum_c_ctx + B.sum_c_t), sc_t = static_cast<double>(B.sum_c_t);
+    for (const auto& Lw : m.layers) {
+        {
+            StageScope sc(m, "gln1", 0, Rd * d * (4 + el));
+            launch_gln<T>(X, d, 0, R, d, rm.src, Lw->g1g.as<float>(), Lw->g1b.as<float>(), eps, XN, d, st);
+            ++L;
+        }
+        if (!Lw->target) {
+            // full layer (hta.hpp:138-155)
+            {
+                StageScope sc(m, "proj_full", 2.0 * Rd * d * pw, Rd * d * el + Rd * pw * el);
+                if constexpr (kTc)
+                    run_gemm_tc({{XN, d, Lw->t1.as<__nv_bfloat16>(), d, static_cast<int>(R), pw, d, EPI_SILU_BF16,
+                                  Lw->b1.as<float>(), Pm, pw, nullptr, 0, nullptr}},
+                                st, L);
+                else
+                    run_gemm_simt({{reinterpret_cast<const float*>(XN), d, Lw->w1.as<float>(), static_cast<int>(R), pw,
+                                    d, Lw->b1.as<float>(), EPI_SILU_BF16, Pm, pw, nullptr, 0, nullptr}},
+                                  st, L);
+            }
+            {
+                StageScope sc(m, "attn_full", 4.0 * hd * sc_full, Rd * (hd + 2 * gd) * el + Rd * hd * el);
+                if constexpr (kTc) {
+                    AttnParams ap{};
+                    ap.tiles = B.tiles_full.as<AttnTile>();
+                    ap.n_tiles = n_full;
+                    ap.q_col0 = hd;
+                    ap.k_col0 = 2 * hd;
+                    ap.v_col0 = 2 * hd + gd;
+                    ap.heads = m.H;
+                    ap.kv_heads = m.G;
+                    ap.hs = ag.hs;
+                    ap.rt = ag.rt;
+                    ap.q_prefix = rm.prefix;
+                    ap.q_scale = rm.scale;
+                    ap.q_self = rm.self;
+                    ap.q_ptr = Pm;
+                    ap.ldq = pw;
+                    ap.kv_ptr = Pm;
+                    ap.ldkv = pw;
+                    ap.out = A;
+                    ap.ldo = hd;
+                    run_attn_tc(m, ap, Pm, R, pw, R, pw, st);
+                } else {
+                    SimtAttn sa{reinterpret_cast<const float*>(Pm), pw, hd, reinterpret_cast<const float*>(Pm), pw,
+                                2 * hd, 2 * hd + gd, R, rm.prefix, rm.scale, rm.self, rm.keybase, m.H, m.G, dh,
+                                reinterpret_cast<float*>(A), hd};
+                    launch_attn_simt(sa, st);
+                    ck(cudaGetLastError(), "attn_simt launch");
+                }
+                ++L;
+            }
+            {
+                StageScope sc(m, "gate", 0, Rd * hd * el * 3);
+                launch_gate<T>(A, hd, Pm, pw, R, hd, rm.src, Lw->g2g.as<float>(), Lw->g2b.as<float>(), eps, G, hd, st);
+                ++L;
+            }
+            {
+                StageScope sc(m, "f2_full", 2.0 * Rd * hd * d, Rd * hd * el + Rd * d * 8);
+                if constexpr (kTc)
+                    run_gemm_tc({{G, hd, Lw->tf2.as<__nv_bfloat16>(), hd, static_cast<int>(R), d, hd, EPI_RESID_F32,
+                                  Lw->f2b.as<float>(), X, d, nullptr, 0, X}},
+                                st, L);
+                else
+                    run_gemm_simt({{reinterpret_cast<const float*>(G), hd, Lw->f2.as<float>(), static_cast<int>(R), d,
+                                    hd, Lw->f2b.as<float>(), EPI_RESID_F32, X, d, nullptr, 0, X}},
+                                  st, L);
+            }
+        } else {
+            // target layer (hta.hpp:158-184): T rows only; H/R rows untouched
+            {
+                StageScope sc(m, "proj_target", 2.0 * (Rd * d * 2 * gd + Td * d * 2 * hd),
+                              Rd * d * el + Rd * 2 * gd * el + Td * 2 * hd * el);
+                if constexpr (kTc)
+                    run_gemm_tc({{XN, d, Lw->tkv.as<__nv_bfloat16>(), d, static_cast<int>(R), 2 * gd, d, EPI_SILU_BF16,
+                                  Lw->bkv.as<float>(), KV, 2 * gd, nullptr, 0, nullptr},
+                                 {XN + NE * d, d, Lw->t1.as<__nv_bfloat16>(), d, static_cast<int>(NT), 2 * hd, d,
+                                  EPI_SILU_BF16, Lw->b1.as<float>(), UQ, 2 * hd, nullptr, 0, nullptr}},
+                                st, L);
+                else
+                    run_gemm_simt({{reinterpret_cast<const float*>(XN), d, Lw->wkv.as<float>(), static_cast<int>(R),
+                                    2 * gd, d, Lw->bkv.as<float>(), EPI_SILU_BF16, KV, 2 * gd, nullptr, 0, nullptr},
+                                   {reinterpret_cast<const float*>(XN) + NE * d, d, Lw->w1.as<float>(),
+                                    static_cast<int>(NT), 2 * hd, d, Lw->b1.as<float>(), EPI_SILU_BF16, UQ, 2 * hd,
+                                    nullptr, 0, nullptr}},
+                                  st, L);
+            }
+            {
+                StageScope sc(m, "attn_target", 4.0 * hd * sc_t, Rd * 2 * gd * el + Td * 2 * hd * el);
+                if constexpr (kTc) {
+                    AttnParams ap{};
+                    ap.tiles = B.tiles_tgt.as<AttnTile>();
+                    ap.n_tiles = n_tgt;
+                    ap.q_col0 = hd;
+                    ap.k_col0 = 0;
+                    ap.v_col0 = gd;
+                    ap.heads = m.H;
+                    ap.kv_heads = m.G;
+                    ap.hs = ag.hs;
+                    ap.rt = ag.rt;
+                    ap.q_prefix = rm.prefix + NE;
+                    ap.q_scale = rm.scale + NE;
+                    ap.q_self = rm.self + NE;
+                    ap.q_ptr = UQ;
+                    ap.ldq = 2 * hd;
+                    ap.kv_ptr = KV;
+                    ap.ldkv = 2 * gd;
+                    ap.out = A;
+                    ap.ldo = hd;
+                    run_attn_tc(m, ap, UQ, NT, 2 * hd, R, 2 * gd, st);
+                } else {
+                    SimtAttn sa{reinterpret_cast<const float*>(UQ), 2 * hd, hd, reinterpret_cast<const float*>(KV),
+                                2 * gd, 0, gd, NT, rm.prefix + NE, rm.scale + NE, rm.self + NE, rm.keybase + NE,
+                                m.H, m.G, dh, reinterpret_cast<float*>(A), hd};
+                    launch_attn_simt(sa, st);
+                    ck(cudaGetLastError(), "attn_simt launch");
+                }
+                ++L;
+            }
+            {
+                StageScope sc(m, "gate", 0, Td * hd * el * 3);
+                launch_gate<T>(A, hd, UQ, 2 * hd, NT, hd, rm.src + NE, Lw->g2g.as<float>(), Lw->g2b.as<float>(), eps,
+                               G, hd, st);
+                ++L;
+            }
+            {
+                StageScope sc(m, "f2_target", 2.0 * Td * hd * d, Td * hd * el + Td * d * 8);
+                if constexpr (kTc)
+                    run_gemm_tc({{G, hd, Lw->tf2.as<__nv_bfloat16>(), hd, static_cast<int>(NT), d, hd, EPI_RESID_F32,
+                                  Lw->f2b.as<float>(), X, d, nullptr, NE, X}},
+                                st, L);
+                else
+                    run_gemm_simt({{reinterpret_cast<const float*>(G), hd, Lw->f2.as<float>(), static_cast<int>(NT), d,
+                                    hd, Lw->f2b.as<float>(), EPI_RESID_F32, X, d, nullptr, NE, X}},
+                                  st, L);
+            }
+        }
+    }
+
+    // ---- K5: heads (heads.hpp:47-99) + records
+    float* Y = B.Y.as<float>();
+    const double hflops = 2.0 * Td * d * m.head_n;
+    if constexpr (kTc) {
+        {
+            StageScope sc(m, "to_bf16", 0, Td * d * 6);
+            launch_to_bf16(X + NE * d, NT, d, XN, d, st);
+            ++L;
+        }
+        StageScope sc(m, "heads_gemm", hflops, Td * d * 2 + Td * m.head_n * 4);
+        run_gemm_tc({{XN, d, m.head_t.as<__nv_bfloat16>(), d, static_cast<int>(NT), m.head_n, d, EPI_BIAS_F32, nullptr,
+                      Y, m.head_ld, nullptr, 0, nullptr}},
+                    st, L);
+    } else {
+        StageScope sc(m, "heads_gemm", hflops, Td * d * 4 + Td * m.head_n * 4);
+        run_gemm_simt({{X + NE * d, d, m.head_w.as<float>(), static_cast<int>(NT), m.head_n, d, nullptr, EPI_BIAS_F32, Y,
+                        m.head_ld, nullptr, 0, nullptr}},
+                      st, L);
+    }
+    HeadArgs ha{};
+    ha.y = Y;
+    ha.ldy = m.head_ld;
+    ha.exp_bias = m.head_eb.as<float>();
+    ha.gate_bias = m.head_gb.as<float>();
+    ha.tower_w = m.tower_w.as<float>();
+    ha.tower_b = m.tower_b.as<float>();
+    ha.E = m.cfg.experts;
+    ha.de = m.cfg.d_expert;
+    ha.src = m.d_src.as<SourceInfo>();
+    ha.n_src = n_src;
+    ha.t_scen = rm.t_scen;
+    ha.t_user = rm.t_user;
+    ha.t_exp_ref = rm.t_exp_ref;
+    ha.t_rec0 = rm.t_rec0;
+    ha.t_rec_stride = rm.t_rec_stride;
+    ha.user_id = B.user_id.as<long long>();
+    ha.n_t = NT;
+    ha.precise = true;
+    ha.rec_user = B.rec_user.as<long long>();
+    ha.rec_scen = B.rec_scen.as<int>();
+    ha.rec_exp = B.rec_exp.as<int>();
+    ha.rec_task = B.rec_task.as<int>();
+    ha.rec_logit = B.rec_logit.as<float>();
+    ha.rec_prob = B.rec_prob.as<double>();
+    {
+        StageScope sc(m, "heads", 2.0 * B.n_records * m.cfg.experts * m.cfg.d_expert,
+                      Td * m.head_ld * 4 + B.n_records * 32.0);
+        launch_heads(ha, st);
+        ck(cudaGetLastError(), "heads launch");
+        ++L;
+    }
+}
+
+void results(mtfm_cuda_model& m, mtfm_cuda_batch& B, mtfm_records* out) {
+    cudaStream_t st = m.stream;
+    unsigned long long err = ~0ull;
+    if (B.n_users > 0) ck(cudaMemcpyAsync(&err, B.err.p, 8, cudaMemcpyDeviceToHost, st), "D2H err");
+    ck(cudaStreamSynchronize(st), "forward");
+    if (err != ~0ull) {
+        const int code = static_cast<int>(err & 7);
+        const long long user = static_cast<long long>(err >> 42);
+        std::string what;
+        switch (code) {
+            case 2: what = "no tokenizer for a sequence schema or scenario of the sample"; break;
+            case 3: what = "embed_rows: feature slot missing"; break;
+            case 5: what = "gather_rows: feature id out of range"; break;
+            case 6: what = "assemble_tokens: sample has no tokens"; break;
+            default: what = "planning capacity exceeded";
+        }
+        const mtfm_status s = code == 2 ? MTFM_INTEGRITY_ERROR
+                              : code == 3 ? MTFM_DIMENSION_ERROR
+                              : code == 5 ? MTFM_LOOKUP_ERROR
+                                          : MTFM_CONTRACT_ERROR;
+        fail(s, what + " (user index " + std::to_string(user) + ")");
+    }
+    if (!out) return;
+    if (out->capacity < B.n_records)
+        fail(MTFM_CONTRACT_ERROR, "record buffer too small: need " + std::to_string(B.n_records));
+    const size_t n = static_cast<size_t>(B.n_records);
+    if (n) {
+        ck(cudaMemcpyAsync(out->user_id, B.rec_user.p, n * 8, cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaMemcpyAsync(out->scenario_id, B.rec_scen.p, n * 4, cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaMemcpyAsync(out->exposure_index, B.rec_exp.p, n * 4, cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaMemcpyAsync(out->task_index, B.rec_task.p, n * 4, cudaMemcpyDeviceToHost, st), "D2H");
+        if (out->logit) ck(cudaMemcpyAsync(out->logit, B.rec_logit.p, n * 4, cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaMemcpyAsync(out->probability, B.rec_prob.p, n * 8, cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaStreamSynchronize(st), "D2H records");
+    }
+    out->n_records = B.n_records;
+}
+
+// Algorithmic FLOPs of the run: projections per complexity.hpp:54-64,
+// mask-aware attention 4*d_h*H*sum(c_i) per layer, tokenizer MLPs, heads.
+__global__ void sum_valid_kernel(const int* prefix, const int* self, long long n, unsigned long long* out) {
+    unsigned long long s = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        s += static_cast<unsigned long long>(prefix[i] + (self[i] >= 0 ? 1 : 0));
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, s);
+}
+
+}  // namespace
+}  // namespace mtfm
+
+using namespace mtfm;
+
+extern "C" {
+
+const char* mtfm_cuda_last_error(void) { return g_last_error.c_str(); }
+const char* mtfm_cuda_version(void) { return "mtfm-b200 0.1 (sm_100a)"; }
+
+mtfm_status mtfm_cuda_create(int device, const mtfm_model_desc* md, const mtfm_schema_desc* sd, int32_t precision,
+                             mtfm_cuda_model** out) {
+    return guard([&] {
+        if (!md || !sd || !out) fail(MTFM_CONTRACT_ERROR, "null argument");
+        // HTAConfig::validate / ModelConfig::validate (model_config.hpp:53-66, 82-87)
+        if (md->d_model < 1) fail(MTFM_CONFIG_ERROR, "hta: d_model must be positive");
+        if (md->blocks < 1) fail(MTFM_CONFIG_ERROR, "hta: blocks must be >= 1");
+        if (md->target_layers < 0 || md->full_layers < 0) fail(MTFM_CONFIG_ERROR, "hta: negative layer counts");
+        if (md->target_layers + md->full_layers < 1) fail(MTFM_CONFIG_ERROR, "hta: each block needs at least one layer");
+        if (md->heads < 1 || md->kv_heads < 1) fail(MTFM_CONFIG_ERROR, "hta: head counts must be >= 1");
+        if (md->heads % md->kv_heads != 0) fail(MTFM_CONFIG_ERROR, "hta: heads must be divisible by kv_heads");
+        if (md->d_model % md->heads != 0) fail(MTFM_CONFIG_ERROR, "hta: d_model must be divisible by heads");
+        if (!(md->eps > 0)) fail(MTFM_CONFIG_ERROR, "hta: eps must be positive");
+        if (md->d_emb < 1) fail(MTFM_CONFIG_ERROR, "model: d_emb must be >= 1");
+        if (md->experts < 1) fail(MTFM_CONFIG_ERROR, "model: experts must be >= 1");
+        if (md->d_expert < 1) fail(MTFM_CONFIG_ERROR, "model: d_expert must be >= 1");
+        if (md->norm < 0 || md->norm > 2) fail(MTFM_CONFIG_ERROR, "unknown attention norm");
+        if (precision != MTFM_PRECISION_BF16 && precision != MTFM_PRECISION_FP32_CHECK)
+            fail(MTFM_CONFIG_ERROR, "unknown precision");
+        // limits of this implementation (documented in DESIGN.md)
+        if (md->d_model > 1024 || md->d_model % 8) fail(MTFM_CONFIG_ERROR, "d_model must be a multiple of 8 and <= 1024");
+        if (md->experts > 32) fail(MTFM_CONFIG_ERROR, "experts must be <= 32");
+        const int dh = md->d_model / md->heads;
+        if (dh > 256) fail(MTFM_CONFIG_ERROR, "head_dim must be <= 256");
+        if (precision == MTFM_PRECISION_BF16 && (dh % 16 || (dh & (dh - 1))))
+            fail(MTFM_CONFIG_ERROR, "bf16 tensor-core path needs head_dim in {16,32,64,128,256}; use the fp32 check mode");
+        if ((md->d_emb * 2) % 16 && precision == MTFM_PRECISION_BF16)
+            fail(MTFM_CONFIG_ERROR, "bf16 path needs d_emb to be a multiple of 8");
+        int cnt = 0;
+        ck(cudaGetDeviceCount(&cnt), "cudaGetDeviceCount");
+        if (device < 0 || device >= cnt) fail(MTFM_CONFIG_ERROR, "no such CUDA device");
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        auto m = std::make_unique<mtfm_cuda_model>();
+        m->device = device;
+        m->precision = precision;
+        m->cfg = *md;
+        m->d = md->d_model;
+        m->H = md->heads;
+        m->G = md->kv_heads;
+        m->dh = dh;
+        m->hd = m->H * dh;
+        m->gd = m->G * dh;
+        m->n_layers = md->blocks * (md->target_layers + md->full_layers);
+        // sources in GroupTable order (groups.hpp:20-35)
+        auto add_seq = [&](int kind, int n, const int32_t* ids, const int32_t* ns, const int32_t* voc) {
+            int p = 0;
+            for (int i = 0; i < n; ++i) {
+                SourceInfo s{};
+                s.kind = kind;
+                s.id = ids[i];
+                s.nslot[0] = ns[i];
+                s.slot0 = static_cast<int>(m->slots.size());
+                for (int k = 0; k < ns[i]; ++k) m->slots.push_back({0, voc[p++], 0});
+                s.k_in = ns[i] * md->d_emb;
+                s.k_pad = static_cast<int>(round_up(std::max(s.k_in, 1), 8));
+                m->sources.push_back(s);
+                m->tasks.emplace_back();
+            }
+        };
+        add_seq(0, sd->n_hist, sd->hist_ids, sd->hist_nslots, sd->hist_vocabs);
+        add_seq(1, sd->n_rt, sd->rt_ids, sd->rt_nslots, sd->rt_vocabs);
+        m->n_hist = sd->n_hist;
+        m->n_rt = sd->n_rt;
+        int p = 0, tp = 0;
+        for (int i = 0; i < sd->n_scen; ++i) {
+            SourceInfo s{};
+            s.kind = 2;
+            s.id = sd->scen_ids[i];
+            s.nslot[0] = sd->scen_nu[i];
+            s.nslot[1] = sd->scen_nc[i];
+            s.nslot[2] = sd->scen_ni[i];
+            s.slot0 = static_cast<int>(m->slots.size());
+            const int ns = s.nslot[0] + s.nslot[1] + s.nslot[2];
+            for (int k = 0; k < ns; ++k) m->slots.push_back({0, sd->scen_vocabs[p++], 0});
+            s.k_in = ns * md->d_emb;
+            s.k_pad = static_cast<int>(round_up(std::max(s.k_in, 1), 8));
+            s.ntasks = sd->scen_ntasks[i];
+            s.task0 = m->n_tasks_total;
+            std::vector<std::string> names;
+            for (int t = 0; t < s.ntasks; ++t) names.push_back(sd->task_names[tp++]);
+            m->n_tasks_total += s.ntasks;
+            m->sources.push_back(s);
+            m->tasks.push_back(names);
+        }
+        m->n_scen = sd->n_scen;
+        if (m->sources.empty()) fail(MTFM_CONFIG_ERROR, "schema set is empty");
+        m->slot_param.assign(m->slots.size(), "");
+        register_params(*m);
+        ck(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking), "stream");
+        *out = m.release();
+    });
+}
+
+mtfm_status mtfm_cuda_destroy(mtfm_cuda_model* m) {
+    return guard([&] {
+        if (!m) return;
+        if (m->stream) cudaStreamSynchronize(m->stream);
+        cudaStream_t st = m->stream;
+        for (auto& e : m->prof) {
+            if (e.a) cudaEventDestroy(e.a);
+            if (e.b) cudaEventDestroy(e.b);
+        }
+        delete m;
+        if (st) cudaStreamDestroy(st);
+    });
+}
+
+mtfm_status mtfm_cuda_set_param(mtfm_cuda_model* m, const char* name, const float* v, int64_t rows, int64_t cols) {
+    return guard([&] {
+        if (!m || !name || (!v && rows * cols)) fail(MTFM_CONTRACT_ERROR, "null argument");
+        auto it = m->by_name.find(name);
+        if (it == m->by_name.end()) fail(MTFM_CONFIG_ERROR, std::string("unknown parameter: ") + name);
+        auto& p = m->params[it->second];
+        if (p.rows != rows || p.cols != cols)
+            fail(MTFM_DIMENSION_ERROR, std::string("shape mismatch for '") + name + "': expected " +
+                                           std::to_string(p.rows) + "x" + std::to_string(p.cols));
+        p.host.assign(v, v + rows * cols);
+        p.set = true;
+        m->finalized = false;
+        m->srcw.clear();
+        m->layers.clear();
+    });
+}
+
+int64_t mtfm_cuda_num_params(const mtfm_cuda_model* m) { return m ? static_cast<int64_t>(m->params.size()) : 0; }
+
+const char* mtfm_cuda_param_name(const mtfm_cuda_model* m, int64_t i, int64_t* rows, int64_t* cols) {
+    if (!m || i < 0 || i >= static_cast<int64_t>(m->params.size())) return nullptr;
+    if (rows) *rows = m->params[i].rows;
+    if (cols) *cols = m->params[i].cols;
+    return m->params[i].name.c_str();
+}
+
+int64_t mtfm_cuda_count_records(const mtfm_cuda_model* m, const mtfm_packed_batch* b) {
+    if (!m || !b) return 0;
+    int64_t n = 0;
+    for (int x = 0; x < b->n_exposures; ++x) {
+        const int s = source_of(*m, 2, b->exp_scenario[x], -1);
+        if (s >= 0) n += m->sources[s].ntasks;
+    }
+    return n;
+}
+
+mtfm_status mtfm_cuda_batch_prepare(mtfm_cuda_model* m, const mtfm_packed_batch* b, int32_t only_scenario,
+                                    mtfm_cuda_batch** out) {
+    return guard([&] {
+        if (!m || !out) fail(MTFM_CONTRACT_ERROR, "null argument");
+        ck(cudaSetDevice(m->device), "cudaSetDevice");
+        auto B = std::make_unique<mtfm_cuda_batch>();
+        prepare(*m, b, only_scenario, *B);
+        *out = B.release();
+    });
+}
+
+mtfm_status mtfm_cuda_batch_run(mtfm_cuda_model* m, mtfm_cuda_batch* b) {
+    return guard([&] {
+        if (!m || !b) fail(MTFM_CONTRACT_ERROR, "null argument");
+        if (!m->finalized) fail(MTFM_CONTRACT_ERROR, "parameters changed after prepare; prepare the batch again");
+        ck(cudaSetDevice(m->device), "cudaSetDevice");
+        if (m->precision == MTFM_PRECISION_BF16)
+            run_forward<__nv_bfloat16>(*m, *b);
+        else
+            run_forward<float>(*m, *b);
+        m->stats.kernel_launches = b->launches;
+        m->stats.tokens = b->rows;
+        m->stats.targets = b->n_exp;
+        m->stats.records = b->n_records;
+    });
+}
+
+mtfm_status mtfm_cuda_batch_results(mtfm_cuda_model* m, mtfm_cuda_batch* b, mtfm_records* out) {
+    return guard([&] {
+        if (!m || !b) fail(MTFM_CONTRACT_ERROR, "null argument");
+        results(*m, *b, out);
+        // algorithmic FLOPs
+        DevBuf acc;
+        acc.alloc(16);
+        ck(cudaMemsetAsync(acc.p, 0, 16, m->stream), "memset");
+        const auto* a = acc.as<unsigned long long>();
+        if (b->n_events)
+            sum_valid_kernel<<<64, 256, 0, m->stream>>>(b->r_prefix.as<int>(), b->r_self.as<int>(), b->n_events,
+                                                        const_cast<unsigned long long*>(a));
+        if (b->n_exp)
+            sum_valid_kernel<<<64, 256, 0, m->stream>>>(b->r_prefix.as<int>() + b->n_events,
+                                                        b->r_self.as<int>() + b->n_events, b->n_exp,
+                                                        const_cast<unsigned long long*>(a) + 1);
+        unsigned long long h[2] = {0, 0};
+        ck(cudaMemcpyAsync(h, acc.p, 16, cudaMemcpyDeviceToHost, m->stream), "D2H");
+        ck(cudaStreamSynchronize(m->stream), "stats");
+        b->sum_c_ctx = h[0];
+        b->sum_c_t = h[1];
+        if (m->profiling)
+            for (size_t i = 0; i < m->prof_n; ++i) {
+                float ms = 0;
+                ck(cudaEventElapsedTime(&ms, m->prof[i].a, m->prof[i].b), "event time");
+                m->prof[i].ms = ms;
+            }
+        const double d = m->d, hd = m->hd, gd = m->gd, R = static_cast<double>(b->rows), T = static_cast<double>(b->n_exp);
+        double proj = 0, attn = 0;
+        for (const auto& L : m->layers) {
+            if (L->target) {
+                proj += T * d * 2 * hd + R * d * 2 * gd + T * hd * d;
+                attn += 2.0 * hd * static_cast<double>(h[1]);
+            } else {
+                proj += R * d * (2 * hd + 2 * gd) + R * hd * d;
+                attn += 2.0 * hd * static_cast<double>(h[0] + h[1]);
+            }
+        }
+        double tok = 0;
+        for (size_t s = 0; s < m->sources.size(); ++s)
+            tok += static_cast<double>(b->src_cnt[s]) * (m->sources[s].k_in * 2.0 * d + 2.0 * d * d);
+        const double heads = T * (static_cast<double>(m->cfg.experts) * d * m->cfg.d_expert) +
+                             static_cast<double>(b->n_records) * (d * m->cfg.experts + m->cfg.d_expert);
+        m->stats.algorithmic_flops = 2.0 * (proj + attn + tok + heads);
+        m->stats.attention_flops = 2.0 * attn;
+    });
+}
+
+mtfm_status mtfm_cuda_batch_free(mtfm_cuda_batch* b) {
+    return guard([&] {
+        if (!b) return;
+        if (b->m && b->m->stream) cudaStreamSynchronize(b->m->stream);
+        delete b;
+    });
+}
+
+mtfm_status mtfm_cuda_forward(mtfm_cuda_model* m, const mtfm_packed_batch* b, int32_t only_scenario,
+                              mtfm_records* out) {
+    mtfm_status s = guard([&] {
+        if (!m) fail(MTFM_CONTRACT_ERROR, "null argument");
+        ck(cudaSetDevice(m->device), "cudaSetDevice");
+        if (!m->ws) m->ws = std::make_unique<mtfm_cuda_batch>();  // device buffers only grow
+        prepare(*m, b, only_scenario, *m->ws);
+    });
+    if (s == MTFM_OK) s = mtfm_cuda_batch_run(m, m->ws.get());
+    if (s == MTFM_OK) s = mtfm_cuda_batch_results(m, m->ws.get(), out);
+    return s;
+}
+
+mtfm_status mtfm_cuda_set_profiling(mtfm_cuda_model* m, int32_t on) {
+    return guard([&] {
+        if (!m) fail(MTFM_CONTRACT_ERROR, "null argument");
+        m->profiling = on != 0;
+    });
+}
+
+int64_t mtfm_cuda_profile_count(const mtfm_cuda_model* m) { return m ? static_cast<int64_t>(m->prof_n) : 0; }
+
+const char* mtfm_cuda_profile_entry(const mtfm_cuda_model* m, int64_t i, double* ms, double* flops, double* bytes) {
+    if (!m || i < 0 || i >= static_cast<int64_t>(m->prof_n)) return nullptr;
+    const auto& e = m->prof[static_cast<size_t>(i)];
+    if (ms) *ms = e.ms;
+    if (flops) *flops = e.flops;
+    if (bytes) *bytes = e.bytes;
+    return e.name.c_str();
+}
+
+void* mtfm_cuda_stream(mtfm_cuda_model* m) { return m ? static_cast<void*>(m->stream) : nullptr; }
+
+mtfm_status mtfm_cuda_last_stats(const mtfm_cuda_model* m, mtfm_run_stats* out) {
+    return guard([&] {
+        if (!m || !out) fail(MTFM_CONTRACT_ERROR, "null argument");
+        *out = m->stats;
+    });
+}
+
+int64_t mtfm_cuda_debug_fetch(mtfm_cuda_model* m, mtfm_cuda_batch* b, const char* which, void* dst, int64_t max_bytes) {
+    if (!m || !b || !which || !dst) return -1;
+    cudaStreamSynchronize(m->stream);
+    const std::string w = which;
+    auto cp = [&](const DevBuf& src, size_t bytes) -> int64_t {
+        bytes = std::min<size_t>(bytes, static_cast<size_t>(max_bytes));
+        if (cudaMemcpy(dst, src.p, bytes, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+        return static_cast<int64_t>(bytes);
+    };
+    const size_t R = static_cast<size_t>(b->rows);
+    if (w == "x") return cp(b->X, R * m->d * 4);
+    if (w == "src") return cp(b->r_src, R * 4);
+    if (w == "item") return cp(b->r_item, R * 4);
+    if (w == "prefix") return cp(b->r_prefix, R * 4);
+    if (w == "self") return cp(b->r_self, R * 4);
+    if (w == "scale") return cp(b->r_scale, R * 4);
+    if (w == "src_rows") return cp(b->r_src_rows, R * 4);
+    if (w == "t_exp_ref") return cp(b->t_exp_ref, static_cast<size_t>(b->n_exp) * 4);
+    return -1;
+}
+
+}  // extern "C"
