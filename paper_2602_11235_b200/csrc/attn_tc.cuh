@@ -14,11 +14,14 @@
 // Tile = 128 MMA rows = HS heads of one GQA group x RT query rows (HS*RT=128),
 // so every K/V tile TMA-loaded into SMEM is shared by the HS query heads that
 // read it. Per key tile j:
-//   MMA warp : S[j%2] = Q K_j^T            (TMEM, fp32, 128 x BKV)
-//              O     += P[(j-1)%2] V_{j-1}  (P from SMEM, V MN-major)
-//   8 SiLU warps: S -> regs, mask (key < prefix_i), silu, bf16, swizzled
-//              st.shared into P[j%2], fence.proxy.async, arrive.
-// Epilogue (same 8 warps): O -> regs, x s_i, + self term for T rows, bf16 out.
+//   MMA warp     : S[j%2] = Q K_j^T            (TMEM, fp32, 128 x BKV)
+//                  O[t%2] += P[(j-1)%2] V_{j-1} (P from SMEM, V MN-major)
+//   8 SiLU warps : S -> regs, silu = h + h*tanh(h) (h = s/2: FMUL2, MUFU.TANH,
+//                  FFMA2), mask only on the boundary key tile, bf16 pack,
+//                  swizzled st.shared into P[j%2], fence.proxy.async, arrive.
+//   4 epilogue warps: O[t%2] -> regs, x s_i, + self term for T rows, bf16 out
+//                  (overlaps the next tile's key loop).
+// Q and O are double-buffered, so consecutive tiles of a CTA pipeline.
 #pragma once
 
 #include "common.cuh"
@@ -66,49 +69,62 @@ struct Cfg {
     static constexpr int KV_TILE_BYTES = BKV * D * 2;       // one of K or V
     static constexpr int STAGE_BYTES = 2 * KV_TILE_BYTES;
     static constexpr int P_BYTES = 128 * BKV * 2;
-    static constexpr int kStages = D <= 64 ? 3 : 2;
-    static constexpr int SMEM = Q_BYTES + kStages * STAGE_BYTES + 2 * P_BYTES + 1024 + 512;
+    static constexpr int QB = D <= 64 ? 2 : 1;              // Q buffers
+    static constexpr int kStages = D <= 64 ? 4 : 2;
+    static constexpr int SMEM = QB * Q_BYTES + kStages * STAGE_BYTES + 2 * P_BYTES + 1024 + 512;
     static constexpr uint32_t TMEM_COLS = 512;
     static constexpr uint32_t S_COL = 0;                    // S buffers at [0, 2*BKV)
     static constexpr uint32_t O_COL = 2 * BKV;
-    static_assert(O_COL + D <= 512, "TMEM budget");
+    static constexpr int OB = (2 * BKV + 2 * D <= 512) ? 2 : 1;  // O buffers
+    static constexpr int kThreads = 512;
+    static_assert(O_COL + OB * D <= 512, "TMEM budget");
     static_assert(SMEM <= 227 * 1024, "SMEM budget");
 };
 
-// Byte offset of element (row, k) of a K-major SW128 [128 x 64] slab.
+// Byte offset of 16-byte chunk `chunk16` of row `row` in a K-major SW128 slab.
 __device__ __forceinline__ uint32_t sw128_off(uint32_t row, uint32_t chunk16) {
     return (row >> 3) * 1024 + (row & 7) * 128 + ((chunk16 ^ (row & 7)) << 4);
 }
 
-__device__ __forceinline__ float silu_fast(float x) {
-    // silu(x) = h + h*tanh(h), h = x/2 : one MUFU op per element
-    const float h = 0.5f * x;
-    float t;
-    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(h));
-    return fmaf(h, t, h);
+// Two SiLUs -> packed bf16x2: h = s/2 (FMUL2), t = tanh(h) (MUFU), h + h*t (FFMA2).
+__device__ __forceinline__ uint32_t silu2_bf16(float s0, float s1) {
+    uint64_t sv, hv, tv, rv;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(sv) : "f"(s0), "f"(s1));
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(hv) : "l"(sv), "l"(0x3f0000003f000000ull));
+    float h0, h1, t0, t1;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(h0), "=f"(h1) : "l"(hv));
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t0) : "f"(h0));
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t1) : "f"(h1));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(tv) : "f"(t0), "f"(t1));
+    asm("fma.rn.f32x2 %0, %1, %2, %1;" : "=l"(rv) : "l"(hv), "l"(tv));
+    float r0, r1;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r0), "=f"(r1) : "l"(rv));
+    uint32_t out;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(out) : "f"(r1), "f"(r0));
+    return out;
 }
 
 }  // namespace attn_detail
 
 template <int D>
-__global__ void __launch_bounds__(384, 1) attn_tc_kernel(const __grid_constant__ AttnParams prm) {
+__global__ void __launch_bounds__(512, 1) attn_tc_kernel(const __grid_constant__ AttnParams prm) {
     using C = attn_detail::Cfg<D>;
     constexpr int BKV = C::BKV;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sQ = smem;
-    uint8_t* sKV = sQ + C::Q_BYTES;
+    uint8_t* sKV = sQ + C::QB * C::Q_BYTES;
     uint8_t* sP = sKV + C::kStages * C::STAGE_BYTES;
     uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * C::P_BYTES);
-    uint64_t* q_full = bars + 0;
-    uint64_t* q_empty = bars + 1;
-    uint64_t* o_full = bars + 2;
-    uint64_t* o_empty = bars + 3;
-    uint64_t* s_full = bars + 4;   // [2]
-    uint64_t* s_empty = bars + 6;  // [2]
-    uint64_t* p_full = bars + 8;   // [2]
-    uint64_t* p_empty = bars + 10; // [2]
-    uint64_t* kv_full = bars + 12; // [kStages]
+    uint64_t* q_full = bars + 0;   // [2]
+    uint64_t* q_empty = bars + 2;  // [2]
+    uint64_t* o_full = bars + 4;   // [2]
+    uint64_t* o_empty = bars + 6;  // [2]
+    uint64_t* s_full = bars + 8;   // [2]
+    uint64_t* s_empty = bars + 10; // [2]
+    uint64_t* p_full = bars + 12;  // [2]
+    uint64_t* p_empty = bars + 14; // [2]
+    uint64_t* kv_full = bars + 16; // [kStages]
     uint64_t* kv_empty = kv_full + C::kStages;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kv_empty + C::kStages);
 
@@ -117,11 +133,11 @@ __global__ void __launch_bounds__(384, 1) attn_tc_kernel(const __grid_constant__
     const int r_per_g = prm.heads / prm.kv_heads;
 
     if (warp == 0 && lane == 0) {
-        ptx::mbar_init(q_full, 1);
-        ptx::mbar_init(q_empty, 1);
-        ptx::mbar_init(o_full, 1);
-        ptx::mbar_init(o_empty, 8);
         for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(&q_full[i], 1);
+            ptx::mbar_init(&q_empty[i], 1);
+            ptx::mbar_init(&o_full[i], 1);
+            ptx::mbar_init(&o_empty[i], 4);
             ptx::mbar_init(&s_full[i], 1);
             ptx::mbar_init(&s_empty[i], 8);
             ptx::mbar_init(&p_full[i], 8);
@@ -145,18 +161,21 @@ __global__ void __launch_bounds__(384, 1) attn_tc_kernel(const __grid_constant__
         // ------------------------------------------------ TMA producer
         if (ptx::elect_one()) {
             int stage = 0;
-            uint32_t phase = 0, q_phase = 0;
-            for (int t = blockIdx.x; t < prm.n_tiles; t += gridDim.x) {
+            uint32_t phase = 0;
+            int it = 0;
+            for (int t = blockIdx.x; t < prm.n_tiles; t += gridDim.x, ++it) {
                 const AttnTile tile = prm.tiles[t];
                 const int g = tile.head0 / r_per_g;
                 const int n_kv = (tile.kmax + BKV - 1) / BKV;
-                ptx::mbar_wait(q_empty, q_phase ^ 1);
-                ptx::mbar_arrive_expect_tx(q_full, C::Q_BYTES);
+                const int qb = it % C::QB;
+                const uint32_t qpar = (it / C::QB) & 1;
+                ptx::mbar_wait(&q_empty[qb], qpar ^ 1);
+                ptx::mbar_arrive_expect_tx(&q_full[qb], C::Q_BYTES);
+                uint8_t* q_dst = sQ + qb * C::Q_BYTES;
                 for (int hs = 0; hs < prm.hs; ++hs)
                     for (int sl = 0; sl < C::SLABS; ++sl)
-                        ptx::tma_load_2d(sQ + sl * (128 * C::ROWB) + hs * prm.rt * C::ROWB, &prm.tma_q, q_full,
+                        ptx::tma_load_2d(q_dst + sl * (128 * C::ROWB) + hs * prm.rt * C::ROWB, &prm.tma_q, &q_full[qb],
                                          prm.q_col0 + (tile.head0 + hs) * D + sl * C::CHUNK, tile.q_row0);
-                q_phase ^= 1;
                 for (int j = 0; j < n_kv; ++j) {
                     ptx::mbar_wait(&kv_empty[stage], phase ^ 1);
                     uint8_t* sk = sKV + stage * C::STAGE_BYTES;
@@ -181,17 +200,19 @@ __global__ void __launch_bounds__(384, 1) attn_tc_kernel(const __grid_constant__
         const uint32_t idesc_s = ptx::instr_desc_bf16(128, BKV, false, false);
         const uint32_t idesc_o = ptx::instr_desc_bf16(128, D, false, true);
         int stage = 0;
-        uint32_t phase = 0, q_phase = 0, o_phase = 0;
+        uint32_t phase = 0;
         uint32_t s_cnt = 0;  // global key-tile counter (S/P buffer parity)
-        for (int t = blockIdx.x; t < prm.n_tiles; t += gridDim.x) {
+        int it = 0;
+        for (int t = blockIdx.x; t < prm.n_tiles; t += gridDim.x, ++it) {
             const AttnTile tile = prm.tiles[t];
             const int n_kv = (tile.kmax + BKV - 1) / BKV;
-            ptx::mbar_wait(q_full, q_phase);
-            q_phase ^= 1;
-            ptx::mbar_wait(o_empty, o_phase ^ 1);
-            o_phase ^= 1;
+            const int qb = it % C::QB;
+            const int ob = it % C::OB;
+            ptx::mbar_wait(&q_full[qb], (it / C::QB) & 1);
+            ptx::mbar_wait(&o_empty[ob], ((it / C::OB) & 1) ^ 1);
             ptx::tc_fence_after();
-            const uint32_t sq = ptx::smem_u32(sQ);
+            const uint32_t sq = ptx::smem_u32(sQ + qb * C::Q_BYTES);
+            const uint32_t o_tmem = tmem + C::O_COL + ob * D;
             int prev_stage = -1;
             for (int j = 0; j <= n_kv; ++j) {
                 if (j < n_kv) {
@@ -210,7 +231,7 @@ __global__ void __launch_bounds__(384, 1) attn_tc_kernel(const __grid_constant__
                             const uint64_t db = ptx::smem_desc(sk + sl * (BKV * C::ROWB) + in, 16, 8 * C::ROWB, C::LAYOUT);
                             ptx::umma_bf16(tmem + C::S_COL + buf * BKV, da, db, idesc_s, kk > 0);
                         }
-                        if (j == n_kv - 1) ptx::umma_commit(q_empty);
+                        if (j == n_kv - 1) ptx::umma_commit(&q_empty[qb]);
                         ptx::umma_commit(&s_full[buf]);
                     }
                     __syncwarp();
@@ -230,11 +251,11 @@ __global__ void __launch_bounds__(384, 1) attn_tc_kernel(const __grid_constant__
                             const uint32_t pin = ((kk * 16) % 64) * 2;
                             const uint64_t da = ptx::smem_desc(sp + psl * (128 * 128) + pin, 16, 1024, 2);
                             const uint64_t db = ptx::smem_desc(sv + kk * 16 * C::ROWB, BKV * C::ROWB, 8 * C::ROWB, C::LAYOUT);
-                            ptx::umma_bf16(tmem + C::O_COL, da, db, idesc_o, (j > 1 || kk > 0));
+                            ptx::umma_bf16(o_tmem, da, db, idesc_o, (j > 1 || kk > 0));
                         }
                         ptx::umma_commit(&kv_empty[prev_stage]);
                         ptx::umma_commit(&p_empty[buf]);
-                        if (j == n_kv) ptx::umma_commit(o_full);
+                        if (j == n_kv) ptx::umma_commit(&o_full[ob]);
                     }
                     __syncwarp();
                 }
@@ -248,53 +269,59 @@ __global__ void __launch_bounds__(384, 1) attn_tc_kernel(const __grid_constant__
                 }
             }
             if (n_kv == 0) {
-                // no visible context keys: release Q, signal an all-zero O
+                // no visible context keys: release Q, signal an (unused) O
                 if (ptx::elect_one()) {
-                    ptx::umma_commit(q_empty);
-                    ptx::umma_commit(o_full);
+                    ptx::umma_commit(&q_empty[qb]);
+                    ptx::umma_commit(&o_full[ob]);
                 }
                 __syncwarp();
             }
         }
-    } else if (warp >= 4) {
-        // ------------------------------------------------ SiLU + epilogue warps
+    } else if (warp >= 4 && warp < 12) {
+        // ------------------------------------------------ SiLU warps
         const uint32_t q = warp & 3;
         const uint32_t half = (warp - 4) >> 2;
         const uint32_t m = q * 32 + lane;  // MMA row == TMEM lane
         const uint32_t lane_addr = (q * 32u) << 16;
-        uint32_t s_cnt = 0, o_phase = 0;
+        uint32_t s_cnt = 0;
         for (int t = blockIdx.x; t < prm.n_tiles; t += gridDim.x) {
             const AttnTile tile = prm.tiles[t];
             const int n_kv = (tile.kmax + BKV - 1) / BKV;
             const int hs = m / prm.rt;
             const int i = m - hs * prm.rt;
-            const bool valid = i < tile.n_rows;
-            const int qrow = tile.q_row0 + i;
-            const int prefix = valid ? __ldg(prm.q_prefix + qrow) : 0;
+            const int prefix = i < tile.n_rows ? __ldg(prm.q_prefix + tile.q_row0 + i) : 0;
             for (int j = 0; j < n_kv; ++j, ++s_cnt) {
                 const uint32_t buf = s_cnt & 1;
                 const uint32_t par = (s_cnt >> 1) & 1;
+                const int key0 = j * BKV + half * (BKV / 2);  // first key of my column half
+                const int nvalid = prefix - key0;             // >= BKV/2: no masking needed
                 ptx::mbar_wait(&s_full[buf], par);
                 ptx::tc_fence_after();
-                uint32_t packed[BKV / 4];  // my half: BKV/2 values -> BKV/4 bf16x2
+                float v[BKV / 2];
 #pragma unroll
                 for (int c = 0; c < BKV / 32; ++c) {
-                    float v[16];
-                    const int col = half * (BKV / 2) + c * 16;
-                    ptx::tmem_ld16(tmem + lane_addr + C::S_COL + buf * BKV + col, v);
-                    ptx::tmem_ld_wait();
-                    const int key0 = j * BKV + col;
+                    float tmp[16];
+                    ptx::tmem_ld16(tmem + lane_addr + C::S_COL + buf * BKV + half * (BKV / 2) + c * 16, tmp);
 #pragma unroll
-                    for (int e = 0; e < 16; e += 2) {
-                        const float w0 = (key0 + e < prefix) ? attn_detail::silu_fast(v[e]) : 0.f;
-                        const float w1 = (key0 + e + 1 < prefix) ? attn_detail::silu_fast(v[e + 1]) : 0.f;
-                        packed[c * 8 + e / 2] = pack_bf16(w0, w1);
-                    }
+                    for (int e = 0; e < 16; ++e) v[c * 16 + e] = tmp[e];
                 }
+                ptx::tmem_ld_wait();
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&s_empty[buf]);
-                // P buffer must have been consumed by the MMA two tiles ago
+                uint32_t packed[BKV / 4];
+                if (__all_sync(0xffffffffu, nvalid >= BKV / 2)) {
+#pragma unroll
+                    for (int e = 0; e < BKV / 2; e += 2) packed[e / 2] = attn_detail::silu2_bf16(v[e], v[e + 1]);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < BKV / 2; e += 2) {
+                        const uint32_t w = attn_detail::silu2_bf16(v[e], v[e + 1]);
+                        const uint32_t keep = (e + 1 < nvalid) ? 0xffffffffu : (e < nvalid ? 0x0000ffffu : 0u);
+                        packed[e / 2] = w & keep;
+                    }
+                }
+                // P buffer must have been consumed by the MMA two key tiles ago
                 ptx::mbar_wait(&p_empty[buf], par ^ 1);
                 uint8_t* pb = sP + buf * C::P_BYTES;
 #pragma unroll
@@ -312,12 +339,24 @@ __global__ void __launch_bounds__(384, 1) attn_tc_kernel(const __grid_constant__
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&p_full[buf]);
             }
-            // ---------------- epilogue
-            ptx::mbar_wait(o_full, o_phase);
-            o_phase ^= 1;
-            ptx::tc_fence_after();
+        }
+    } else if (warp >= 12) {
+        // ------------------------------------------------ epilogue warps
+        const uint32_t q = warp & 3;
+        const uint32_t m = q * 32 + lane;
+        const uint32_t lane_addr = (q * 32u) << 16;
+        int it = 0;
+        for (int t = blockIdx.x; t < prm.n_tiles; t += gridDim.x, ++it) {
+            const AttnTile tile = prm.tiles[t];
+            const int n_kv = (tile.kmax + BKV - 1) / BKV;
+            const int ob = it % C::OB;
+            const int hs = m / prm.rt;
+            const int i = m - hs * prm.rt;
+            const bool valid = i < tile.n_rows;
+            const int qrow = tile.q_row0 + i;
             const int head = tile.head0 + hs;
             const int g = tile.head0 / r_per_g;
+            // self term inputs (T rows) are independent of O: fetch before waiting
             float scale = 0.f, wself = 0.f;
             int self_row = -1;
             if (valid) {
@@ -327,47 +366,67 @@ __global__ void __launch_bounds__(384, 1) attn_tc_kernel(const __grid_constant__
                     const __nv_bfloat16* qp = prm.q_ptr + (long long)qrow * prm.ldq + prm.q_col0 + head * D;
                     const __nv_bfloat16* kp = prm.kv_ptr + (long long)self_row * prm.ldkv + prm.k_col0 + g * D;
                     float dot = 0.f;
-                    for (int e = 0; e < D; ++e) dot += to_f32(qp[e]) * to_f32(kp[e]);
+#pragma unroll 4
+                    for (int e = 0; e < D; e += 8) {
+                        const uint4 a = *reinterpret_cast<const uint4*>(qp + e);
+                        const uint4 b = *reinterpret_cast<const uint4*>(kp + e);
+                        const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
+                        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b);
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const float2 fa = __bfloat1622float2(a2[k]), fb = __bfloat1622float2(b2[k]);
+                            dot = fmaf(fa.x, fb.x, dot);
+                            dot = fmaf(fa.y, fb.y, dot);
+                        }
+                    }
                     wself = silu_precise(dot);
                 }
             }
-            constexpr int DCOLS = D >= 32 ? D / 2 : D;
-            if (D >= 32 || half == 0) {
-                const int c0 = D >= 32 ? half * DCOLS : 0;
+            ptx::mbar_wait(&o_full[ob], (it / C::OB) & 1);
+            ptx::tc_fence_after();
 #pragma unroll 1
-                for (int c = c0; c < c0 + DCOLS; c += 16) {
-                    float v[16];
-                    ptx::tmem_ld16(tmem + lane_addr + C::O_COL + c, v);
-                    ptx::tmem_ld_wait();
-                    if (n_kv == 0) {
+            for (int c = 0; c < D; c += 16) {
+                float v[16];
+                ptx::tmem_ld16(tmem + lane_addr + C::O_COL + ob * D + c, v);
+                ptx::tmem_ld_wait();
+                if (n_kv == 0) {
 #pragma unroll
-                        for (int e = 0; e < 16; ++e) v[e] = 0.f;
-                    }
-                    if (valid) {
-                        if (self_row >= 0) {
-                            const __nv_bfloat16* vp =
-                                prm.kv_ptr + (long long)self_row * prm.ldkv + prm.v_col0 + g * D + c;
+                    for (int e = 0; e < 16; ++e) v[e] = 0.f;
+                }
+                if (valid) {
+                    if (self_row >= 0) {
+                        const __nv_bfloat16* vp =
+                            prm.kv_ptr + (long long)self_row * prm.ldkv + prm.v_col0 + g * D + c;
+                        const uint4 a = *reinterpret_cast<const uint4*>(vp);
+                        const uint4 b = *reinterpret_cast<const uint4*>(vp + 8);
+                        const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
+                        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b);
 #pragma unroll
-                            for (int e = 0; e < 16; ++e) v[e] += wself * to_f32(vp[e]);
+                        for (int k = 0; k < 4; ++k) {
+                            const float2 fa = __bfloat1622float2(a2[k]), fb = __bfloat1622float2(b2[k]);
+                            v[2 * k] += wself * fa.x;
+                            v[2 * k + 1] += wself * fa.y;
+                            v[8 + 2 * k] += wself * fb.x;
+                            v[8 + 2 * k + 1] += wself * fb.y;
                         }
-                        __nv_bfloat16* o = prm.out + (long long)qrow * prm.ldo + head * D + c;
-                        uint4 w0, w1;
-                        w0.x = pack_bf16(v[0] * scale, v[1] * scale);
-                        w0.y = pack_bf16(v[2] * scale, v[3] * scale);
-                        w0.z = pack_bf16(v[4] * scale, v[5] * scale);
-                        w0.w = pack_bf16(v[6] * scale, v[7] * scale);
-                        w1.x = pack_bf16(v[8] * scale, v[9] * scale);
-                        w1.y = pack_bf16(v[10] * scale, v[11] * scale);
-                        w1.z = pack_bf16(v[12] * scale, v[13] * scale);
-                        w1.w = pack_bf16(v[14] * scale, v[15] * scale);
-                        reinterpret_cast<uint4*>(o)[0] = w0;
-                        reinterpret_cast<uint4*>(o)[1] = w1;
                     }
+                    __nv_bfloat16* o = prm.out + (long long)qrow * prm.ldo + head * D + c;
+                    uint4 w0, w1;
+                    w0.x = pack_bf16(v[0] * scale, v[1] * scale);
+                    w0.y = pack_bf16(v[2] * scale, v[3] * scale);
+                    w0.z = pack_bf16(v[4] * scale, v[5] * scale);
+                    w0.w = pack_bf16(v[6] * scale, v[7] * scale);
+                    w1.x = pack_bf16(v[8] * scale, v[9] * scale);
+                    w1.y = pack_bf16(v[10] * scale, v[11] * scale);
+                    w1.z = pack_bf16(v[12] * scale, v[13] * scale);
+                    w1.w = pack_bf16(v[14] * scale, v[15] * scale);
+                    reinterpret_cast<uint4*>(o)[0] = w0;
+                    reinterpret_cast<uint4*>(o)[1] = w1;
                 }
             }
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(o_empty);
+            if (lane == 0) ptx::mbar_arrive(&o_empty[ob]);
         }
     }
     ptx::tc_fence_before();

@@ -2,18 +2,28 @@
 //
 //   C[m, n] = epilogue( sum_k A[m, k] * Bt[n, k] + bias[n] )
 //
-// A: bf16 row-major [M][K] (K-major), Bt: bf16 row-major [N][K] (the weight
-// pre-transposed at upload, K-major). K is a multiple of 64 (buffers are
-// zero-padded). One launch serves up to kMaxProblems independent problems
-// (tokenizer sources, fuq+fkv of a target layer, ...): the persistent CTAs
-// walk one global tile list, tile t -> (problem, m-block, n-block) with n
-// fastest so the CTAs resident at one time share A tiles through L2.
+// Bt: bf16 row-major [N][K] (the weight pre-transposed at upload, K-major),
+// always TMA-loaded. A (128 x 64 bf16 per k-block, SW128 K-major in SMEM)
+// comes from one of three producers (GemmArgs::a_mode, uniform per launch):
+//   A_TMA  : a bf16 row-major matrix, TMA-loaded.
+//   A_LN   : group LayerNorm fused in (hta.hpp:104-109): four producer warps
+//            read fp32 X rows and write bf16((x - mu) * rstd * gain[g] +
+//            bias[g]) straight into the swizzled stage (mu/rstd from a row
+//            stats pass), so the normalised activations never touch HBM.
+//   A_GATE : the gate of hta.hpp:153/179 fused in: bf16(gln(A) * U) from the
+//            attention output A and the U projection, both bf16.
+// One launch serves up to kMaxProblems independent problems (tokenizer
+// sources, fkv+fuq of a target layer, ...): the persistent CTAs walk one
+// global tile list, tile t -> (problem, m-block, n-block), n fastest, so the
+// CTAs resident at one time share A tiles through L2.
 //
-// Roles (384 threads): warp 0 TMA producer, warp 1 MMA issuer (one elected
-// lane), warp 2 TMEM allocator, warps 4..11 epilogue (two warps per TMEM lane
-// quarter, each owning half the columns). Pipelines: kStages smem stages
-// (full/empty mbarriers) and 2 TMEM accumulator stages (tmem_full/empty), so
-// the epilogue of tile i overlaps the MMAs of tile i+1.
+// Roles (512 threads): warp 0 TMA, warp 1 MMA issuer (one elected lane),
+// warp 2 TMEM allocator, warps 4..11 epilogue (two per TMEM lane quarter,
+// each owning half the columns), warps 12..15 A-transform producers.
+// Pipelines: kStages SMEM stages (full/empty mbarriers) and 2 TMEM
+// accumulator stages (tmem_full/empty), so the epilogue of tile i overlaps
+// the MMAs of tile i+1. The epilogue stages each 32 x 32 block through
+// XOR-swizzled SMEM so global stores are 128-byte row segments.
 #pragma once
 
 #include "common.cuh"
@@ -28,12 +38,15 @@ enum GemmEpi : int {
     EPI_BIAS_BF16 = 3,   // out_bf16[m][n] = acc + bias
 };
 
+enum GemmAMode : int { A_TMA = 0, A_LN = 1, A_GATE = 2 };
+
 constexpr int kMaxProblems = 16;
 
 struct GemmProblem {
-    CUtensorMap tma_a;      // box {64, 128}, SW128
+    CUtensorMap tma_a;      // box {64, 128}, SW128 (A_TMA only)
     CUtensorMap tma_b;      // box {64, BN}, SW128
-    int M, N, K;
+    int M, N, K;            // K padded to a multiple of 64
+    int Kv;                 // true K (columns of a_src / gain rows)
     int tile_start;         // first global tile of this problem
     int tiles_n;
     int epi;
@@ -43,11 +56,23 @@ struct GemmProblem {
     const int* row_map;     // optional output row indirection (f32 epilogues)
     long long row_offset;   // added to the output row when row_map is null
     const float* resid;     // EPI_RESID_F32
+    // transform producers (A_LN / A_GATE)
+    const void* a_src;      // fp32 X (A_LN) or bf16 attention output (A_GATE)
+    long long lda;
+    long long a_row0;       // GEMM row m reads a_src / stats row m + a_row0
+    const float2* stats;    // (mean, rstd) per a_src row
+    const int* row_group;   // GLN group per row, indexed m + g_row0
+    long long g_row0;
+    const float* gain;      // [groups][K]
+    const float* gbias;     // [groups][K]
+    const __nv_bfloat16* u_src;  // A_GATE: U rows (m), ldu
+    long long ldu;
 };
 
 struct GemmArgs {
     int n_problems;
     int n_tiles;
+    int a_mode;
     GemmProblem p[kMaxProblems];
 };
 
@@ -56,13 +81,15 @@ namespace gemm_detail {
 template <int BN>
 struct Cfg {
     static constexpr int BM = 128, BK = 64;
-    static constexpr int kStages = BN >= 256 ? 4 : 6;
+    static constexpr int kStages = BN >= 256 ? 3 : (BN >= 128 ? 5 : 6);
     static constexpr int A_BYTES = BM * BK * 2;
     static constexpr int B_BYTES = BN * BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
-    static constexpr int SMEM = kStages * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-    static constexpr int kThreads = 384;
+    static constexpr int STG_BYTES = 8 * 32 * 32 * 4;  // per epilogue warp: 32 rows x 32 fp32
+    static constexpr int SMEM = kStages * STAGE_BYTES + STG_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int kThreads = 512;
+    static_assert(SMEM <= 227 * 1024, "SMEM budget");
 };
 
 __device__ __forceinline__ void decode_tile(const GemmArgs& a, int t, int& pi, int& mb, int& nb) {
@@ -75,14 +102,92 @@ __device__ __forceinline__ void decode_tile(const GemmArgs& a, int t, int& pi, i
     nb = local - mb * a.p[pi].tiles_n;
 }
 
+__device__ __forceinline__ void unpack8(const uint4 u, float (&f)[8]) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float2 t = __bfloat1622float2(h[i]);
+        f[2 * i] = t.x;
+        f[2 * i + 1] = t.y;
+    }
+}
+
+// Produces one 128 x 64 A k-block (SW128 K-major) from global memory with the
+// LayerNorm / gate transform. 128 producer threads, 8 x 16-byte chunks each;
+// one warp instruction covers 4 rows x 8 chunks (coalesced 256 B / 128 B rows).
+// Processed in two halves of 4 chunks to bound register use.
+__device__ __forceinline__ void produce_a(const GemmProblem& p, int mode, int m0, int k0, uint8_t* sa, int pt) {
+    const int c8 = pt & 7;
+    const int k = k0 + c8 * 8;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        float xv[4][8];
+        float2 st[4];
+        int grp[4];
+        bool ok[4];
+        // issue all loads of the half first (memory-level parallelism), then transform
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int r = (pt >> 3) + 16 * (4 * h + i);
+            const int m = m0 + r;
+            ok[i] = m < p.M && k < p.Kv;
+            if (ok[i]) {
+                const long long ar = m + p.a_row0;
+                st[i] = __ldg(p.stats + ar);
+                grp[i] = __ldg(p.row_group + m + p.g_row0);
+                if (mode == A_LN) {
+                    const float* x = static_cast<const float*>(p.a_src) + ar * p.lda + k;
+                    const float4 a = __ldcs(reinterpret_cast<const float4*>(x));
+                    const float4 b = __ldcs(reinterpret_cast<const float4*>(x + 4));
+                    xv[i][0] = a.x; xv[i][1] = a.y; xv[i][2] = a.z; xv[i][3] = a.w;
+                    xv[i][4] = b.x; xv[i][5] = b.y; xv[i][6] = b.z; xv[i][7] = b.w;
+                } else {
+                    const uint4 a = __ldcs(reinterpret_cast<const uint4*>(
+                        static_cast<const __nv_bfloat16*>(p.a_src) + ar * p.lda + k));
+                    unpack8(a, xv[i]);
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int r = (pt >> 3) + 16 * (4 * h + i);
+            uint4 outv = make_uint4(0, 0, 0, 0);
+            if (ok[i]) {
+                const int g = grp[i] < 0 ? 0 : grp[i];
+                const float* gp = p.gain + (long long)g * p.Kv + k;
+                const float* bp = p.gbias + (long long)g * p.Kv + k;
+                const float4 ga = __ldg(reinterpret_cast<const float4*>(gp));
+                const float4 gb = __ldg(reinterpret_cast<const float4*>(gp + 4));
+                const float4 ba = __ldg(reinterpret_cast<const float4*>(bp));
+                const float4 bb = __ldg(reinterpret_cast<const float4*>(bp + 4));
+                const float gv[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
+                const float bv[8] = {ba.x, ba.y, ba.z, ba.w, bb.x, bb.y, bb.z, bb.w};
+                float y[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) y[e] = ((xv[i][e] - st[i].x) * st[i].y) * gv[e] + bv[e];
+                if (mode == A_GATE) {
+                    float u[8];
+                    unpack8(__ldg(reinterpret_cast<const uint4*>(p.u_src + (long long)(m0 + r) * p.ldu + k)), u);
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) y[e] *= u[e];
+                }
+                outv = make_uint4(pack_bf16(y[0], y[1]), pack_bf16(y[2], y[3]), pack_bf16(y[4], y[5]),
+                                  pack_bf16(y[6], y[7]));
+            }
+            *reinterpret_cast<uint4*>(sa + (r >> 3) * 1024 + (r & 7) * 128 + ((c8 ^ (r & 7)) << 4)) = outv;
+        }
+    }
+}
+
 }  // namespace gemm_detail
 
 template <int BN>
-__global__ void __launch_bounds__(384, 1) gemm_tc_kernel(const __grid_constant__ GemmArgs args) {
+__global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__ GemmArgs args) {
     using C = gemm_detail::Cfg<BN>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::kStages * C::STAGE_BYTES);
+    float* stg_all = reinterpret_cast<float*>(smem + C::kStages * C::STAGE_BYTES);
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::kStages * C::STAGE_BYTES + C::STG_BYTES);
     uint64_t* empty_bar = full_bar + C::kStages;
     uint64_t* tfull_bar = empty_bar + C::kStages;
     uint64_t* tempty_bar = tfull_bar + 2;
@@ -90,10 +195,11 @@ __global__ void __launch_bounds__(384, 1) gemm_tc_kernel(const __grid_constant__
 
     const uint32_t warp = ptx::warp_id();
     const uint32_t lane = ptx::lane_id();
+    const int a_mode = args.a_mode;
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < C::kStages; ++s) {
-            ptx::mbar_init(&full_bar[s], 1);
+            ptx::mbar_init(&full_bar[s], a_mode == A_TMA ? 1 : 1 + 4);
             ptx::mbar_init(&empty_bar[s], 1);
         }
         for (int s = 0; s < 2; ++s) {
@@ -102,7 +208,7 @@ __global__ void __launch_bounds__(384, 1) gemm_tc_kernel(const __grid_constant__
         }
         ptx::fence_mbar_init();
         for (int i = 0; i < args.n_problems; ++i) {
-            ptx::tma_prefetch(&args.p[i].tma_a);
+            if (a_mode == A_TMA) ptx::tma_prefetch(&args.p[i].tma_a);
             ptx::tma_prefetch(&args.p[i].tma_b);
         }
     }
@@ -113,6 +219,7 @@ __global__ void __launch_bounds__(384, 1) gemm_tc_kernel(const __grid_constant__
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
+        // ------------------------------------------------ TMA producer (B, and A in A_TMA mode)
         if (ptx::elect_one()) {
             int stage = 0;
             uint32_t phase = 0;
@@ -125,8 +232,12 @@ __global__ void __launch_bounds__(384, 1) gemm_tc_kernel(const __grid_constant__
                     ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
                     uint8_t* sa = smem + stage * C::STAGE_BYTES;
                     uint8_t* sb = sa + C::A_BYTES;
-                    ptx::mbar_arrive_expect_tx(&full_bar[stage], C::STAGE_BYTES);
-                    ptx::tma_load_2d(sa, &p.tma_a, &full_bar[stage], kb * C::BK, mb * C::BM);
+                    if (a_mode == A_TMA) {
+                        ptx::mbar_arrive_expect_tx(&full_bar[stage], C::STAGE_BYTES);
+                        ptx::tma_load_2d(sa, &p.tma_a, &full_bar[stage], kb * C::BK, mb * C::BM);
+                    } else {
+                        ptx::mbar_arrive_expect_tx(&full_bar[stage], C::B_BYTES);
+                    }
                     ptx::tma_load_2d(sb, &p.tma_b, &full_bar[stage], kb * C::BK, nb * BN);
                     if (++stage == C::kStages) {
                         stage = 0;
@@ -135,7 +246,32 @@ __global__ void __launch_bounds__(384, 1) gemm_tc_kernel(const __grid_constant__
                 }
             }
         }
+    } else if (warp >= 12) {
+        // ------------------------------------------------ A-transform producers
+        if (a_mode != A_TMA) {
+            const int pt = (warp - 12) * 32 + lane;
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < args.n_tiles; t += gridDim.x) {
+                int pi, mb, nb;
+                gemm_detail::decode_tile(args, t, pi, mb, nb);
+                const GemmProblem& p = args.p[pi];
+                const int kblocks = p.K / C::BK;
+                for (int kb = 0; kb < kblocks; ++kb) {
+                    ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+                    gemm_detail::produce_a(p, a_mode, mb * C::BM, kb * C::BK, smem + stage * C::STAGE_BYTES, pt);
+                    ptx::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&full_bar[stage]);
+                    if (++stage == C::kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
     } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer
         const uint32_t idesc = ptx::instr_desc_bf16(128, BN, false, false);
         int stage = 0;
         uint32_t phase = 0;
@@ -175,8 +311,14 @@ __global__ void __launch_bounds__(384, 1) gemm_tc_kernel(const __grid_constant__
             }
         }
     } else if (warp >= 4) {
-        const uint32_t q = warp & 3;               // TMEM lane quarter
-        const uint32_t half = (warp - 4) >> 2;     // column half
+        // ------------------------------------------------ epilogue
+        // TMEM -> registers (bias, SiLU) -> XOR-swizzled SMEM staging ->
+        // coalesced row-segment stores (8 lanes x 16 B per row).
+        const uint32_t q = warp & 3;            // TMEM lane quarter
+        const uint32_t half = (warp - 4) >> 2;  // column half
+        float* stg = stg_all + (warp - 4) * 32 * 32;
+        const int sub = lane >> 3;              // row within a 4-row group
+        const int ch = lane & 7;                // 16-byte chunk within a 32-column row slice
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int t = blockIdx.x; t < args.n_tiles; t += gridDim.x) {
@@ -185,69 +327,94 @@ __global__ void __launch_bounds__(384, 1) gemm_tc_kernel(const __grid_constant__
             const GemmProblem& p = args.p[pi];
             ptx::mbar_wait(&tfull_bar[acc], acc_phase);
             ptx::tc_fence_after();
-            const int m = mb * C::BM + q * 32 + lane;
-            const bool row_ok = m < p.M;
-            long long orow = 0;
-            if (row_ok) orow = p.row_map ? static_cast<long long>(p.row_map[m]) : p.row_offset + m;
+            const int row0 = mb * C::BM + q * 32;
             const int n_begin = half * (BN / 2);
 #pragma unroll 1
-            for (int c = n_begin; c < n_begin + BN / 2; c += 16) {
-                float v[16];
-                ptx::tmem_ld16(tmem_base + ((q * 32u) << 16) + acc * BN + c, v);
-                ptx::tmem_ld_wait();
+            for (int c = n_begin; c < n_begin + BN / 2; c += 32) {
                 const int n0 = nb * BN + c;
-                if (!row_ok || n0 >= p.N) continue;
-                const int nvalid = min(16, p.N - n0);
-                if (p.bias) {
+                if (n0 >= p.N) break;  // warp-uniform
+                {
+                    float v[32];
+                    ptx::tmem_ld16(tmem_base + ((q * 32u) << 16) + acc * BN + c, *reinterpret_cast<float(*)[16]>(v));
+                    ptx::tmem_ld16(tmem_base + ((q * 32u) << 16) + acc * BN + c + 16,
+                                   *reinterpret_cast<float(*)[16]>(v + 16));
+                    ptx::tmem_ld_wait();
+                    if (p.bias) {
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) v[i] += (i < nvalid) ? __ldg(p.bias + n0 + i) : 0.f;
-                }
-                if (p.epi == EPI_SILU_BF16 || p.epi == EPI_BIAS_BF16) {
-                    __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out) + orow * p.ldo + n0;
+                        for (int i = 0; i < 32; ++i) v[i] += (n0 + i < p.N) ? __ldg(p.bias + n0 + i) : 0.f;
+                    }
                     if (p.epi == EPI_SILU_BF16) {
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) v[i] = ptx::silu_f32(v[i]);
+                        for (int i = 0; i < 32; ++i) v[i] = ptx::silu_fast(v[i]);
                     }
-                    if (nvalid == 16 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
-                        uint4 w0, w1;
-                        w0.x = pack_bf16(v[0], v[1]);
-                        w0.y = pack_bf16(v[2], v[3]);
-                        w0.z = pack_bf16(v[4], v[5]);
-                        w0.w = pack_bf16(v[6], v[7]);
-                        w1.x = pack_bf16(v[8], v[9]);
-                        w1.y = pack_bf16(v[10], v[11]);
-                        w1.z = pack_bf16(v[12], v[13]);
-                        w1.w = pack_bf16(v[14], v[15]);
-                        reinterpret_cast<uint4*>(o)[0] = w0;
-                        reinterpret_cast<uint4*>(o)[1] = w1;
-                    } else {
-                        for (int i = 0; i < nvalid; ++i) o[i] = __float2bfloat16_rn(v[i]);
-                    }
-                } else {
-                    float* o = static_cast<float*>(p.out) + orow * p.ldo + n0;
-                    if (p.epi == EPI_RESID_F32) {
-                        const float* r = p.resid + orow * p.ldo + n0;
-                        if (nvalid == 16 && (reinterpret_cast<uintptr_t>(r) & 15) == 0) {
+                    // stage: row = lane, chunk k stored at (k ^ (lane & 7))
 #pragma unroll
-                            for (int i = 0; i < 16; i += 4) {
-                                float4 rr = *reinterpret_cast<const float4*>(r + i);
-                                v[i] += rr.x;
-                                v[i + 1] += rr.y;
-                                v[i + 2] += rr.z;
-                                v[i + 3] += rr.w;
-                            }
+                    for (int k = 0; k < 8; ++k)
+                        *reinterpret_cast<float4*>(stg + lane * 32 + ((k ^ (lane & 7)) << 2)) =
+                            make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+                }
+                __syncwarp();
+                const int col = n0 + 4 * ch;
+                const int nval = min(4, p.N - col);
+                long long orow[8];
+#pragma unroll
+                for (int g = 0; g < 8; ++g) {
+                    const int m = row0 + 4 * g + sub;
+                    orow[g] = (m < p.M && nval > 0)
+                                  ? (p.row_map ? static_cast<long long>(__ldg(p.row_map + m)) : p.row_offset + m)
+                                  : -1;
+                }
+                if (p.epi == EPI_SILU_BF16 || p.epi == EPI_BIAS_BF16) {
+#pragma unroll
+                    for (int g = 0; g < 8; ++g) {
+                        const int r = 4 * g + sub;
+                        const float4 w = *reinterpret_cast<const float4*>(stg + r * 32 + ((ch ^ (r & 7)) << 2));
+                        if (orow[g] < 0) continue;
+                        __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out) + orow[g] * p.ldo + col;
+                        if (nval == 4) {
+                            *reinterpret_cast<uint2*>(o) = make_uint2(pack_bf16(w.x, w.y), pack_bf16(w.z, w.w));
                         } else {
-                            for (int i = 0; i < nvalid; ++i) v[i] += r[i];
+                            const float ww[4] = {w.x, w.y, w.z, w.w};
+                            for (int i = 0; i < nval; ++i) o[i] = __float2bfloat16_rn(ww[i]);
                         }
                     }
-                    if (nvalid == 16 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
+                } else {
+                    // f32 outputs: load every residual first (resid may alias out), then store
+                    float4 rr[8];
+                    if (p.epi == EPI_RESID_F32) {
 #pragma unroll
-                        for (int i = 0; i < 16; i += 4)
-                            *reinterpret_cast<float4*>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-                    } else {
-                        for (int i = 0; i < nvalid; ++i) o[i] = v[i];
+                        for (int g = 0; g < 8; ++g) {
+                            rr[g] = make_float4(0.f, 0.f, 0.f, 0.f);
+                            if (orow[g] >= 0 && nval == 4) {
+                                rr[g] = *reinterpret_cast<const float4*>(p.resid + orow[g] * p.ldo + col);
+                            } else if (orow[g] >= 0) {
+                                float t4[4] = {0.f, 0.f, 0.f, 0.f};
+                                for (int i = 0; i < nval; ++i) t4[i] = p.resid[orow[g] * p.ldo + col + i];
+                                rr[g] = make_float4(t4[0], t4[1], t4[2], t4[3]);
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int g = 0; g < 8; ++g) {
+                        const int r = 4 * g + sub;
+                        float4 w = *reinterpret_cast<const float4*>(stg + r * 32 + ((ch ^ (r & 7)) << 2));
+                        if (orow[g] < 0) continue;
+                        if (p.epi == EPI_RESID_F32) {
+                            w.x += rr[g].x;
+                            w.y += rr[g].y;
+                            w.z += rr[g].z;
+                            w.w += rr[g].w;
+                        }
+                        float* o = static_cast<float*>(p.out) + orow[g] * p.ldo + col;
+                        if (nval == 4) {
+                            *reinterpret_cast<float4*>(o) = w;
+                        } else {
+                            const float ww[4] = {w.x, w.y, w.z, w.w};
+                            for (int i = 0; i < nval; ++i) o[i] = ww[i];
+                        }
                     }
                 }
+                __syncwarp();
             }
             ptx::tc_fence_before();
             __syncwarp();

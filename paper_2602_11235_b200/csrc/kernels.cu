@@ -378,55 +378,88 @@ template void launch_gather<__nv_bfloat16>(const DevBatch&, const SourceInfo*, c
 
 // ---------------------------------------------------------------- GLN
 // row_normalize (kernels.hpp:132-153) + group_affine (eval_ctx.hpp:130-143).
-template <typename TIn>
-__device__ __forceinline__ void load_row(const TIn* p, int d, int lane, float (&v)[32]) {
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-        const int c = lane + 32 * i;
-        v[i] = c < d ? to_f32(p[c]) : 0.f;
-    }
+// One warp per row, 4 consecutive columns per lane per 128-column slice,
+// vectorised loads/stores (memory-bound: one read + one write of the row).
+constexpr int kMaxSlices = 8;  // d <= 1024
+
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ float4 ld4(const __nv_bfloat16* p) {
+    const uint2 u = *reinterpret_cast<const uint2*>(p);
+    const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(&u.x);
+    const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&u.y);
+    const float2 fa = __bfloat1622float2(a), fb = __bfloat1622float2(b);
+    return make_float4(fa.x, fa.y, fb.x, fb.y);
+}
+__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+__device__ __forceinline__ void st4(__nv_bfloat16* p, float4 v) {
+    uint2 u;
+    u.x = pack_bf16(v.x, v.y);
+    u.y = pack_bf16(v.z, v.w);
+    *reinterpret_cast<uint2*>(p) = u;
 }
 
-__device__ __forceinline__ void normalize_row(float (&v)[32], int d, int lane, float eps) {
+// Normalises the row held as float4 slices (c = 128*i + 4*lane) in place.
+template <int NS>
+__device__ __forceinline__ void normalize_slices(float4 (&v)[NS], int d, int lane, float eps) {
     float s = 0.f;
 #pragma unroll
-    for (int i = 0; i < 32; ++i) s += v[i];
+    for (int i = 0; i < NS; ++i)
+        if (128 * i + 4 * lane < d) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
     s = warp_sum(s);
     const float mean = __fdiv_rn(s, static_cast<float>(d));
     float q = 0.f;
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-        const int c = lane + 32 * i;
-        const float x = c < d ? v[i] - mean : 0.f;
-        q += x * x;
-    }
+    for (int i = 0; i < NS; ++i)
+        if (128 * i + 4 * lane < d) {
+            v[i].x -= mean;
+            v[i].y -= mean;
+            v[i].z -= mean;
+            v[i].w -= mean;
+            q += (v[i].x * v[i].x + v[i].y * v[i].y) + (v[i].z * v[i].z + v[i].w * v[i].w);
+        }
     q = warp_sum(q);
     const float var = __fdiv_rn(q, static_cast<float>(d));
     const float inv = __fdiv_rn(1.f, sqrtf(var + eps));
 #pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = (v[i] - mean) * inv;
+    for (int i = 0; i < NS; ++i) {
+        v[i].x *= inv;
+        v[i].y *= inv;
+        v[i].z *= inv;
+        v[i].w *= inv;
+    }
 }
 
-template <typename T>
-__global__ void gln_kernel(const float* __restrict__ x, long long ldx, long long r0, long long n_rows, int d,
-                           const int* __restrict__ row_src, const float* __restrict__ gain,
-                           const float* __restrict__ bias, float eps, T* __restrict__ out, long long ldo) {
+template <typename T, int NS>
+__global__ void __launch_bounds__(256) gln_kernel(const float* __restrict__ x, long long ldx, long long r0,
+                                                  long long n_rows, int d, const int* __restrict__ row_src,
+                                                  const float* __restrict__ gain, const float* __restrict__ bias,
+                                                  float eps, T* __restrict__ out, long long ldo) {
     const int lane = threadIdx.x & 31;
     const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
     for (long long i = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); i < n_rows; i += warps) {
         const long long r = r0 + i;
-        float v[32];
-        load_row(x + r * ldx, d, lane, v);
-        normalize_row(v, d, lane, eps);
+        const float* xr = x + r * ldx;
         int g = row_src[r];
+        float4 v[NS];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+            const int c = 128 * k + 4 * lane;
+            v[k] = c < d ? __ldcs(reinterpret_cast<const float4*>(xr + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        normalize_slices<NS>(v, d, lane, eps);
         g = g < 0 ? 0 : g;
         const float* gg = gain + (long long)g * d;
         const float* bb = bias + (long long)g * d;
         T* o = out + i * ldo;
 #pragma unroll
-        for (int k = 0; k < 32; ++k) {
-            const int c = lane + 32 * k;
-            if (c < d) o[c] = from_f32<T>(v[k] * __ldg(gg + c) + __ldg(bb + c));
+        for (int k = 0; k < NS; ++k) {
+            const int c = 128 * k + 4 * lane;
+            if (c < d) {
+                const float4 ga = __ldg(reinterpret_cast<const float4*>(gg + c));
+                const float4 be = __ldg(reinterpret_cast<const float4*>(bb + c));
+                st4(o + c, make_float4(v[k].x * ga.x + be.x, v[k].y * ga.y + be.y, v[k].z * ga.z + be.z,
+                                       v[k].w * ga.w + be.w));
+            }
         }
     }
 }
@@ -435,8 +468,12 @@ template <typename T>
 void launch_gln(const float* x, long long ldx, long long r0, long long n_rows, int d, const int* row_src,
                 const float* gain, const float* bias, float eps, T* out, long long ldo, cudaStream_t st) {
     if (n_rows == 0) return;
-    const int blocks = static_cast<int>(std::min<long long>(cdiv(n_rows, 8), 148ll * 32));
-    gln_kernel<T><<<blocks, 256, 0, st>>>(x, ldx, r0, n_rows, d, row_src, gain, bias, eps, out, ldo);
+    const int blocks = static_cast<int>(std::min<long long>(cdiv(n_rows, 8), 148ll * 16));
+    const int ns = static_cast<int>(cdiv(d, 128));
+    if (ns <= 1) gln_kernel<T, 1><<<blocks, 256, 0, st>>>(x, ldx, r0, n_rows, d, row_src, gain, bias, eps, out, ldo);
+    else if (ns == 2) gln_kernel<T, 2><<<blocks, 256, 0, st>>>(x, ldx, r0, n_rows, d, row_src, gain, bias, eps, out, ldo);
+    else if (ns <= 4) gln_kernel<T, 4><<<blocks, 256, 0, st>>>(x, ldx, r0, n_rows, d, row_src, gain, bias, eps, out, ldo);
+    else gln_kernel<T, 8><<<blocks, 256, 0, st>>>(x, ldx, r0, n_rows, d, row_src, gain, bias, eps, out, ldo);
 }
 template void launch_gln<float>(const float*, long long, long long, long long, int, const int*, const float*,
                                 const float*, float, float*, long long, cudaStream_t);
@@ -444,26 +481,40 @@ template void launch_gln<__nv_bfloat16>(const float*, long long, long long, long
                                         const float*, const float*, float, __nv_bfloat16*, long long,
                                         cudaStream_t);
 
-template <typename T>
-__global__ void gate_kernel(const T* __restrict__ a, long long lda, const T* __restrict__ u, long long ldu,
-                            long long n_rows, int d, const int* __restrict__ row_src, const float* __restrict__ gain,
-                            const float* __restrict__ bias, float eps, T* __restrict__ out, long long ldo) {
+template <typename T, int NS>
+__global__ void __launch_bounds__(256) gate_kernel(const T* __restrict__ a, long long lda, const T* __restrict__ u,
+                                                   long long ldu, long long n_rows, int d,
+                                                   const int* __restrict__ row_src, const float* __restrict__ gain,
+                                                   const float* __restrict__ bias, float eps, T* __restrict__ out,
+                                                   long long ldo) {
     const int lane = threadIdx.x & 31;
     const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
     for (long long i = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); i < n_rows; i += warps) {
-        float v[32];
-        load_row(a + i * lda, d, lane, v);
-        normalize_row(v, d, lane, eps);
+        const T* ar = a + i * lda;
+        const T* ur = u + i * ldu;
         int g = row_src[i];
+        float4 v[NS], uu[NS];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+            const int c = 128 * k + 4 * lane;
+            const bool ok = c < d;
+            v[k] = ok ? ld4(ar + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+            uu[k] = ok ? ld4(ur + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        normalize_slices<NS>(v, d, lane, eps);
         g = g < 0 ? 0 : g;
         const float* gg = gain + (long long)g * d;
         const float* bb = bias + (long long)g * d;
-        const T* ur = u + i * ldu;
         T* o = out + i * ldo;
 #pragma unroll
-        for (int k = 0; k < 32; ++k) {
-            const int c = lane + 32 * k;
-            if (c < d) o[c] = from_f32<T>((v[k] * __ldg(gg + c) + __ldg(bb + c)) * to_f32(ur[c]));
+        for (int k = 0; k < NS; ++k) {
+            const int c = 128 * k + 4 * lane;
+            if (c < d) {
+                const float4 ga = __ldg(reinterpret_cast<const float4*>(gg + c));
+                const float4 be = __ldg(reinterpret_cast<const float4*>(bb + c));
+                st4(o + c, make_float4((v[k].x * ga.x + be.x) * uu[k].x, (v[k].y * ga.y + be.y) * uu[k].y,
+                                       (v[k].z * ga.z + be.z) * uu[k].z, (v[k].w * ga.w + be.w) * uu[k].w));
+            }
         }
     }
 }
@@ -473,14 +524,66 @@ void launch_gate(const T* a, long long lda, const T* u, long long ldu, long long
                  const int* row_src_of_rows, const float* gain, const float* bias, float eps, T* out,
                  long long ldo, cudaStream_t st) {
     if (n_rows == 0) return;
-    const int blocks = static_cast<int>(std::min<long long>(cdiv(n_rows, 8), 148ll * 32));
-    gate_kernel<T><<<blocks, 256, 0, st>>>(a, lda, u, ldu, n_rows, d, row_src_of_rows, gain, bias, eps, out, ldo);
+    const int blocks = static_cast<int>(std::min<long long>(cdiv(n_rows, 8), 148ll * 16));
+    const int ns = static_cast<int>(cdiv(d, 128));
+#define MTFM_GATE(NS) gate_kernel<T, NS><<<blocks, 256, 0, st>>>(a, lda, u, ldu, n_rows, d, row_src_of_rows, gain, bias, eps, out, ldo)
+    if (ns <= 1) MTFM_GATE(1);
+    else if (ns == 2) MTFM_GATE(2);
+    else if (ns <= 4) MTFM_GATE(4);
+    else MTFM_GATE(8);
+#undef MTFM_GATE
 }
 template void launch_gate<float>(const float*, long long, const float*, long long, long long, int, const int*,
                                  const float*, const float*, float, float*, long long, cudaStream_t);
 template void launch_gate<__nv_bfloat16>(const __nv_bfloat16*, long long, const __nv_bfloat16*, long long,
                                          long long, int, const int*, const float*, const float*, float,
                                          __nv_bfloat16*, long long, cudaStream_t);
+
+template <typename T, int NS>
+__global__ void __launch_bounds__(256) row_stats_kernel(const T* __restrict__ x, long long ldx, long long n_rows,
+                                                        int d, float eps, float2* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long i = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); i < n_rows; i += warps) {
+        const T* xr = x + i * ldx;
+        float4 v[NS];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+            const int c = 128 * k + 4 * lane;
+            v[k] = c < d ? ld4(xr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        float s = 0.f;
+#pragma unroll
+        for (int k = 0; k < NS; ++k)
+            if (128 * k + 4 * lane < d) s += (v[k].x + v[k].y) + (v[k].z + v[k].w);
+        s = warp_sum(s);
+        const float mean = __fdiv_rn(s, static_cast<float>(d));
+        float q = 0.f;
+#pragma unroll
+        for (int k = 0; k < NS; ++k)
+            if (128 * k + 4 * lane < d) {
+                const float a = v[k].x - mean, b = v[k].y - mean, c = v[k].z - mean, e = v[k].w - mean;
+                q += (a * a + b * b) + (c * c + e * e);
+            }
+        q = warp_sum(q);
+        const float var = __fdiv_rn(q, static_cast<float>(d));
+        if (lane == 0) out[i] = make_float2(mean, __fdiv_rn(1.f, sqrtf(var + eps)));
+    }
+}
+
+template <typename T>
+void launch_row_stats(const T* x, long long ldx, long long n_rows, int d, float eps, float2* out, cudaStream_t st) {
+    if (n_rows == 0) return;
+    const int blocks = static_cast<int>(std::min<long long>(cdiv(n_rows, 8), 148ll * 16));
+    const int ns = static_cast<int>(cdiv(d, 128));
+    if (ns <= 1) row_stats_kernel<T, 1><<<blocks, 256, 0, st>>>(x, ldx, n_rows, d, eps, out);
+    else if (ns == 2) row_stats_kernel<T, 2><<<blocks, 256, 0, st>>>(x, ldx, n_rows, d, eps, out);
+    else if (ns <= 4) row_stats_kernel<T, 4><<<blocks, 256, 0, st>>>(x, ldx, n_rows, d, eps, out);
+    else row_stats_kernel<T, 8><<<blocks, 256, 0, st>>>(x, ldx, n_rows, d, eps, out);
+}
+template void launch_row_stats<float>(const float*, long long, long long, int, float, float2*, cudaStream_t);
+template void launch_row_stats<__nv_bfloat16>(const __nv_bfloat16*, long long, long long, int, float, float2*,
+                                              cudaStream_t);
 
 __global__ void to_bf16_kernel(const float* __restrict__ x, long long n_rows, int d, __nv_bfloat16* __restrict__ out,
                                long long ldo) {
@@ -500,10 +603,16 @@ void launch_to_bf16(const float* x, long long n_rows, int d, __nv_bfloat16* out,
 // ---------------------------------------------------------------- heads
 // mmoe_forward (heads.hpp:47-99) for one T row per warp, then the record of
 // model.hpp:284-311: probability = clamp(sigmoid(z), 1e-12, 1 - 1e-12).
-__global__ void heads_kernel(HeadArgs a) {
+// The task gates (softmax over E, kernels.hpp:155-173) are computed first,
+// then every expert activation silu(x W_e + b_e) once, shared by all tasks.
+constexpr int kMaxTasks = 8;
+
+__global__ void __launch_bounds__(256) heads_kernel(HeadArgs a) {
     const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    __shared__ float s_gate[8][kMaxTasks][32];
     const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
-    for (long long t = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); t < a.n_t; t += warps) {
+    for (long long t = blockIdx.x * (long long)(blockDim.x >> 5) + wib; t < a.n_t; t += warps) {
         const int scen = a.t_scen[t];
         int s = -1;
         for (int i = 0; i < a.n_src; ++i)
@@ -511,43 +620,57 @@ __global__ void heads_kernel(HeadArgs a) {
         if (s < 0) continue;  // reported by the plan
         const SourceInfo si = a.src[s];
         const float* y = a.y + t * a.ldy;
-        for (int k = 0; k < si.ntasks; ++k) {
-            const int task = si.task0 + k;
-            // softmax over the E gate logits (kernels.hpp:155-173)
-            float g[32];
-            float mx = -INFINITY;
-            for (int e = 0; e < a.E; ++e) {
-                g[e & 31] = y[a.E * a.de + task * a.E + e] + a.gate_bias[task * a.E + e];
-                mx = fmaxf(mx, g[e & 31]);
+        for (int k0 = 0; k0 < si.ntasks; k0 += kMaxTasks) {
+            const int nk = min(kMaxTasks, si.ntasks - k0);
+            // gates: lane e holds logit e of each task
+            for (int k = 0; k < nk; ++k) {
+                const int task = si.task0 + k0 + k;
+                const float g = lane < a.E ? y[a.E * a.de + task * a.E + lane] + a.gate_bias[task * a.E + lane]
+                                           : -INFINITY;
+                float mx = g;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                const float e = lane < a.E ? expf(g - mx) : 0.f;
+                // sequential sum over e, as softmax_rows does
+                float sum = 0.f;
+                for (int i = 0; i < a.E; ++i) sum += __shfl_sync(0xffffffffu, e, i);
+                s_gate[wib][k][lane] = e * __fdiv_rn(1.f, sum);
             }
-            float sum = 0.f;
-            for (int e = 0; e < a.E; ++e) {
-                g[e & 31] = expf(g[e & 31] - mx);
-                sum += g[e & 31];
-            }
-            const float inv = __fdiv_rn(1.f, sum);
-            for (int e = 0; e < a.E; ++e) g[e & 31] *= inv;
-            float z = 0.f;
+            __syncwarp();
+            float z[kMaxTasks];
+#pragma unroll
+            for (int k = 0; k < kMaxTasks; ++k) z[k] = 0.f;
             for (int c = lane; c < a.de; c += 32) {
-                float m = 0.f;
+                float m[kMaxTasks];
+#pragma unroll
+                for (int k = 0; k < kMaxTasks; ++k) m[k] = 0.f;
                 for (int e = 0; e < a.E; ++e) {
-                    const float pre = y[e * a.de + c] + a.exp_bias[e * a.de + c];
-                    m += silu_precise(pre) * g[e & 31];
+                    const float act = silu_precise(y[e * a.de + c] + a.exp_bias[e * a.de + c]);
+#pragma unroll
+                    for (int k = 0; k < kMaxTasks; ++k)
+                        if (k < nk) m[k] += act * s_gate[wib][k][e];
                 }
-                z += m * a.tower_w[(long long)task * a.de + c];
+#pragma unroll
+                for (int k = 0; k < kMaxTasks; ++k)
+                    if (k < nk) z[k] += m[k] * a.tower_w[(long long)(si.task0 + k0 + k) * a.de + c];
             }
-            z = warp_sum(z) + a.tower_b[task];
-            if (lane == 0) {
-                const long long r = a.t_rec0[t] + (long long)k * a.t_rec_stride[t];
-                double p = static_cast<double>(sigmoid_precise(z));
-                p = p < 1e-12 ? 1e-12 : (p > 1.0 - 1e-12 ? 1.0 - 1e-12 : p);
-                a.rec_user[r] = a.user_id[a.t_user[t]];
-                a.rec_scen[r] = scen;
-                a.rec_exp[r] = a.t_exp_ref[t];
-                a.rec_task[r] = k;
-                if (a.rec_logit) a.rec_logit[r] = z;
-                a.rec_prob[r] = p;
+#pragma unroll
+            for (int k = 0; k < kMaxTasks; ++k) {
+                if (k >= nk) break;
+                const float zz = warp_sum(z[k]) + a.tower_b[si.task0 + k0 + k];
+                if (lane == 0) {
+                    const long long r = a.t_rec0[t] + (long long)(k0 + k) * a.t_rec_stride[t];
+                    double p = static_cast<double>(sigmoid_precise(zz));
+                    p = p < 1e-12 ? 1e-12 : (p > 1.0 - 1e-12 ? 1.0 - 1e-12 : p);
+                    a.rec_user[r] = a.user_id[a.t_user[t]];
+                    a.rec_scen[r] = scen;
+                    a.rec_exp[r] = a.t_exp_ref[t];
+                    a.rec_task[r] = k0 + k;
+                    if (a.rec_logit) a.rec_logit[r] = zz;
+                    a.rec_prob[r] = p;
+                }
             }
+            __syncwarp();
         }
     }
 }

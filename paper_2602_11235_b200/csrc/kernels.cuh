@@ -98,6 +98,11 @@ void launch_gate(const T* a, long long lda, const T* u, long long ldu, long long
                  const int* row_src_of_rows, const float* gain, const float* bias, float eps, T* out,
                  long long ldo, cudaStream_t st);
 
+// Per-row (mean, rstd) of row_normalize (kernels.hpp:132-153) for the
+// LayerNorm / gate transforms fused into the GEMM A producer.
+template <typename T>
+void launch_row_stats(const T* x, long long ldx, long long n_rows, int d, float eps, float2* out, cudaStream_t st);
+
 // f32 -> bf16 copy of rows (head input in the fast path)
 void launch_to_bf16(const float* x, long long n_rows, int d, __nv_bfloat16* out, long long ldo, cudaStream_t st);
 

@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -194,6 +195,7 @@ struct mtfm_cuda_model {
     mtfm_run_stats stats{};
     // per-stage profiling (CUDA events around every launch) — off by default
     bool profiling = false;
+    int fuse = 0;  // bit 0: GLN1 fused into the projection GEMM, bit 1: gate fused into f2 (MTFM_FUSE)
     struct Prof {
         std::string name;
         cudaEvent_t a = nullptr, b = nullptr;
@@ -219,7 +221,7 @@ struct mtfm_cuda_batch {
     mtfm::DevBuf r_src, r_item, r_prefix, r_scale, r_self, r_keybase, r_src_rows, t_user, t_exp_ref, t_scen, t_rec0,
         t_rec_stride, err;
     // activations
-    mtfm::DevBuf X, XN, P, KV, UQ, A, Gt, E, HID, Y;
+    mtfm::DevBuf X, XN, P, KV, UQ, A, Gt, E, HID, Y, statX, statA;
     // attention tiles
     std::vector<mtfm::AttnTile> h_tiles_full, h_tiles_tgt;
     mtfm::DevBuf tiles_full, tiles_tgt;
@@ -470,6 +472,17 @@ struct TcProblem {
     const int* row_map;
     long long row_offset;
     const float* resid;
+    // fused A transform (GemmAMode): A is built from a_src instead of TMA-loaded
+    int amode = A_TMA;
+    const void* a_src = nullptr;
+    long long a_row0 = 0;
+    const float2* stats = nullptr;
+    const int* row_group = nullptr;
+    long long g_row0 = 0;
+    const float* gain = nullptr;
+    const float* gbias = nullptr;
+    const __nv_bfloat16* u_src = nullptr;
+    long long ldu = 0;
 };
 
 int pick_bn(const std::vector<TcProblem>& ps) {
@@ -498,15 +511,28 @@ void run_gemm_tc(std::vector<TcProblem> ps, cudaStream_t st, long long& launches
     for (size_t i0 = 0; i0 < ps.size(); i0 += kMaxProblems) {
         GemmArgs a;
         std::memset(&a, 0, sizeof(a));
+        a.a_mode = ps[i0].amode;
         int tiles = 0;
         for (size_t i = i0; i < std::min(ps.size(), i0 + kMaxProblems); ++i) {
             const auto& s = ps[i];
+            if (s.amode != a.a_mode) fail(MTFM_CONTRACT_ERROR, "mixed A modes in one grouped GEMM");
             GemmProblem& p = a.p[a.n_problems++];
-            p.tma_a = tma_2d(s.A, s.M, s.K, s.lda, 64, 128, 128);
+            if (s.amode == A_TMA) p.tma_a = tma_2d(s.A, s.M, s.K, s.lda, 64, 128, 128);
             p.tma_b = tma_2d(s.Bt, s.N, s.K, s.ldb, 64, bn, 128);
             p.M = s.M;
             p.N = s.N;
             p.K = static_cast<int>(round_up(s.K, 64));
+            p.Kv = s.K;
+            p.a_src = s.a_src;
+            p.lda = s.lda;
+            p.a_row0 = s.a_row0;
+            p.stats = s.stats;
+            p.row_group = s.row_group;
+            p.g_row0 = s.g_row0;
+            p.gain = s.gain;
+            p.gbias = s.gbias;
+            p.u_src = s.u_src;
+            p.ldu = s.ldu;
             p.tile_start = tiles;
             p.tiles_n = static_cast<int>(cdiv(s.N, bn));
             p.epi = s.epi;
@@ -568,7 +594,7 @@ void launch_attn_tc_d(const AttnParams& p, cudaStream_t st) {
         attr = true;
     }
     const int grid = std::min(p.n_tiles, kNumSMs);
-    attn_tc_kernel<D><<<grid, 384, C::SMEM, st>>>(p);
+    attn_tc_kernel<D><<<grid, C::kThreads, C::SMEM, st>>>(p);
     ck(cudaGetLastError(), "attn_tc launch");
 }
 
@@ -757,6 +783,8 @@ void prepare(mtfm_cuda_model& m, const mtfm_packed_batch* hb, int only_scenario,
     ia(B.E, eb, el);
     ia(B.HID, hbse, el);
     ia(B.Y, T * m.head_ld, 4);
+    ia(B.statX, R, 8);
+    ia(B.statA, R, 8);
     const long long nr = B.n_records;
     ia(B.rec_user, nr, 8);
     ia(B.rec_scen, nr, 4);
@@ -964,6 +992,193 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
     // attention FLOPs need sum(c_i): known after the plan; use the value of
     // the previous results() (same batch) for the profile annotation
     const double sc_full = static_cast<double>(B.sum_c_ctx + B.sum_c_t), sc_t = static_cast<double>(B.sum_c_t);
+    float2* statX = B.statX.as<float2>();
+    float2* statA = B.statA.as<float2>();
+    if constexpr (kTc) {
+        // bf16 tensor-core path: GLN1 and the gate are fused into the GEMM A producers
+        bool ctx_stats_valid = false;  // X context rows only change in full layers
+        for (const auto& Lw : m.layers) {
+            if (m.fuse & 1) {
+                const long long r0 = ctx_stats_valid ? NE : 0;
+                StageScope sc(m, "row_stats", 0, (Rd - r0) * d * 4.0);
+                launch_row_stats<float>(X + r0 * d, d, R - r0, d, eps, statX + r0, st);
+                ++L;
+            }
+            if (!Lw->target) {
+                // full layer (hta.hpp:138-155)
+                if (m.fuse & 1) {
+                    StageScope sc(m, "proj_full", 2.0 * Rd * d * pw, Rd * d * 4 + Rd * pw * el);
+                    TcProblem tp{nullptr, d, Lw->t1.as<__nv_bfloat16>(), d, static_cast<int>(R), pw, d, EPI_SILU_BF16,
+                                 Lw->b1.as<float>(), Pm, pw, nullptr, 0, nullptr};
+                    tp.amode = A_LN;
+                    tp.a_src = X;
+                    tp.stats = statX;
+                    tp.row_group = rm.src;
+                    tp.gain = Lw->g1g.as<float>();
+                    tp.gbias = Lw->g1b.as<float>();
+                    run_gemm_tc({tp}, st, L);
+                } else {
+                    {
+                        StageScope sc(m, "gln1", 0, Rd * d * (4 + el));
+                        launch_gln<T>(X, d, 0, R, d, rm.src, Lw->g1g.as<float>(), Lw->g1b.as<float>(), eps, XN, d, st);
+                        ++L;
+                    }
+                    StageScope sc(m, "proj_full", 2.0 * Rd * d * pw, Rd * d * el + Rd * pw * el);
+                    run_gemm_tc({{XN, d, Lw->t1.as<__nv_bfloat16>(), d, static_cast<int>(R), pw, d, EPI_SILU_BF16,
+                                  Lw->b1.as<float>(), Pm, pw, nullptr, 0, nullptr}},
+                                st, L);
+                }
+                {
+                    StageScope sc(m, "attn_full", 4.0 * hd * sc_full, Rd * (hd + 2 * gd) * el + Rd * hd * el);
+                    AttnParams ap{};
+                    ap.tiles = B.tiles_full.as<AttnTile>();
+                    ap.n_tiles = n_full;
+                    ap.q_col0 = hd;
+                    ap.k_col0 = 2 * hd;
+                    ap.v_col0 = 2 * hd + gd;
+                    ap.heads = m.H;
+                    ap.kv_heads = m.G;
+                    ap.hs = ag.hs;
+                    ap.rt = ag.rt;
+                    ap.q_prefix = rm.prefix;
+                    ap.q_scale = rm.scale;
+                    ap.q_self = rm.self;
+                    ap.q_ptr = Pm;
+                    ap.ldq = pw;
+                    ap.kv_ptr = Pm;
+                    ap.ldkv = pw;
+                    ap.out = A;
+                    ap.ldo = hd;
+                    run_attn_tc(m, ap, Pm, R, pw, R, pw, st);
+                    ++L;
+                }
+                if (m.fuse & 2) {
+                    {
+                        StageScope sc(m, "attn_stats", 0, Rd * hd * el);
+                        launch_row_stats<__nv_bfloat16>(A, hd, R, hd, eps, statA, st);
+                        ++L;
+                    }
+                    StageScope sc(m, "f2_full", 2.0 * Rd * hd * d, Rd * hd * el * 2 + Rd * d * 8);
+                    TcProblem tp{nullptr, hd, Lw->tf2.as<__nv_bfloat16>(), hd, static_cast<int>(R), d, hd,
+                                 EPI_RESID_F32, Lw->f2b.as<float>(), X, d, nullptr, 0, X};
+                    tp.amode = A_GATE;
+                    tp.a_src = A;
+                    tp.stats = statA;
+                    tp.row_group = rm.src;
+                    tp.gain = Lw->g2g.as<float>();
+                    tp.gbias = Lw->g2b.as<float>();
+                    tp.u_src = Pm;
+                    tp.ldu = pw;
+                    run_gemm_tc({tp}, st, L);
+                } else {
+                    {
+                        StageScope sc(m, "gate", 0, Rd * hd * el * 3);
+                        launch_gate<T>(A, hd, Pm, pw, R, hd, rm.src, Lw->g2g.as<float>(), Lw->g2b.as<float>(), eps, G,
+                                       hd, st);
+                        ++L;
+                    }
+                    StageScope sc(m, "f2_full", 2.0 * Rd * hd * d, Rd * hd * el + Rd * d * 8);
+                    run_gemm_tc({{G, hd, Lw->tf2.as<__nv_bfloat16>(), hd, static_cast<int>(R), d, hd, EPI_RESID_F32,
+                                  Lw->f2b.as<float>(), X, d, nullptr, 0, X}},
+                                st, L);
+                }
+                ctx_stats_valid = false;
+            } else {
+                // target layer (hta.hpp:158-184): T rows only; H/R rows untouched
+                if (!(m.fuse & 1)) {
+                    {
+                        StageScope sc(m, "gln1", 0, Rd * d * (4 + el));
+                        launch_gln<T>(X, d, 0, R, d, rm.src, Lw->g1g.as<float>(), Lw->g1b.as<float>(), eps, XN, d, st);
+                        ++L;
+                    }
+                    StageScope sc(m, "proj_target", 2.0 * (Rd * d * 2 * gd + Td * d * 2 * hd),
+                                  Rd * d * el + Rd * 2 * gd * el + Td * 2 * hd * el);
+                    run_gemm_tc({{XN, d, Lw->tkv.as<__nv_bfloat16>(), d, static_cast<int>(R), 2 * gd, d, EPI_SILU_BF16,
+                                  Lw->bkv.as<float>(), KV, 2 * gd, nullptr, 0, nullptr},
+                                 {XN + NE * d, d, Lw->t1.as<__nv_bfloat16>(), d, static_cast<int>(NT), 2 * hd, d,
+                                  EPI_SILU_BF16, Lw->b1.as<float>(), UQ, 2 * hd, nullptr, 0, nullptr}},
+                                st, L);
+                } else {
+                    StageScope sc(m, "proj_target", 2.0 * (Rd * d * 2 * gd + Td * d * 2 * hd),
+                                  Rd * d * 4 + Rd * 2 * gd * el + Td * 2 * hd * el);
+                    TcProblem kv{nullptr, d, Lw->tkv.as<__nv_bfloat16>(), d, static_cast<int>(R), 2 * gd, d,
+                                 EPI_SILU_BF16, Lw->bkv.as<float>(), KV, 2 * gd, nullptr, 0, nullptr};
+                    kv.amode = A_LN;
+                    kv.a_src = X;
+                    kv.stats = statX;
+                    kv.row_group = rm.src;
+                    kv.gain = Lw->g1g.as<float>();
+                    kv.gbias = Lw->g1b.as<float>();
+                    TcProblem uq = kv;
+                    uq.Bt = Lw->t1.as<__nv_bfloat16>();
+                    uq.M = static_cast<int>(NT);
+                    uq.N = 2 * hd;
+                    uq.bias = Lw->b1.as<float>();
+                    uq.out = UQ;
+                    uq.ldo = 2 * hd;
+                    uq.a_row0 = NE;
+                    uq.g_row0 = NE;
+                    run_gemm_tc({kv, uq}, st, L);
+                }
+                {
+                    StageScope sc(m, "attn_target", 4.0 * hd * sc_t, Rd * 2 * gd * el + Td * 2 * hd * el);
+                    AttnParams ap{};
+                    ap.tiles = B.tiles_tgt.as<AttnTile>();
+                    ap.n_tiles = n_tgt;
+                    ap.q_col0 = hd;
+                    ap.k_col0 = 0;
+                    ap.v_col0 = gd;
+                    ap.heads = m.H;
+                    ap.kv_heads = m.G;
+                    ap.hs = ag.hs;
+                    ap.rt = ag.rt;
+                    ap.q_prefix = rm.prefix + NE;
+                    ap.q_scale = rm.scale + NE;
+                    ap.q_self = rm.self + NE;
+                    ap.q_ptr = UQ;
+                    ap.ldq = 2 * hd;
+                    ap.kv_ptr = KV;
+                    ap.ldkv = 2 * gd;
+                    ap.out = A;
+                    ap.ldo = hd;
+                    run_attn_tc(m, ap, UQ, NT, 2 * hd, R, 2 * gd, st);
+                    ++L;
+                }
+                if (!(m.fuse & 2)) {
+                    {
+                        StageScope sc(m, "gate", 0, Td * hd * el * 3);
+                        launch_gate<T>(A, hd, UQ, 2 * hd, NT, hd, rm.src + NE, Lw->g2g.as<float>(), Lw->g2b.as<float>(),
+                                       eps, G, hd, st);
+                        ++L;
+                    }
+                    StageScope sc(m, "f2_target", 2.0 * Td * hd * d, Td * hd * el + Td * d * 8);
+                    run_gemm_tc({{G, hd, Lw->tf2.as<__nv_bfloat16>(), hd, static_cast<int>(NT), d, hd, EPI_RESID_F32,
+                                  Lw->f2b.as<float>(), X, d, nullptr, NE, X}},
+                                st, L);
+                } else {
+                    {
+                        StageScope sc(m, "attn_stats", 0, Td * hd * el);
+                        launch_row_stats<__nv_bfloat16>(A, hd, NT, hd, eps, statA, st);
+                        ++L;
+                    }
+                    StageScope sc(m, "f2_target", 2.0 * Td * hd * d, Td * hd * el * 2 + Td * d * 8);
+                    TcProblem tp{nullptr, hd, Lw->tf2.as<__nv_bfloat16>(), hd, static_cast<int>(NT), d, hd,
+                                 EPI_RESID_F32, Lw->f2b.as<float>(), X, d, nullptr, NE, X};
+                    tp.amode = A_GATE;
+                    tp.a_src = A;
+                    tp.stats = statA;
+                    tp.row_group = rm.src;
+                    tp.g_row0 = NE;
+                    tp.gain = Lw->g2g.as<float>();
+                    tp.gbias = Lw->g2b.as<float>();
+                    tp.u_src = UQ;
+                    tp.ldu = 2 * hd;
+                    run_gemm_tc({tp}, st, L);
+                }
+                ctx_stats_valid = true;
+            }
+        }
+    } else {
     for (const auto& Lw : m.layers) {
         {
             StageScope sc(m, "gln1", 0, Rd * d * (4 + el));
@@ -1100,6 +1315,8 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                                   st, L);
             }
         }
+    }
+
     }
 
     // ---- K5: heads (heads.hpp:47-99) + records
@@ -1302,6 +1519,7 @@ mtfm_status mtfm_cuda_create(int device, const mtfm_model_desc* md, const mtfm_s
         m->slot_param.assign(m->slots.size(), "");
         register_params(*m);
         ck(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking), "stream");
+        if (const char* f = std::getenv("MTFM_FUSE")) m->fuse = std::atoi(f);
         *out = m.release();
     });
 }

@@ -158,6 +158,15 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
 }
 
 // ---------------------------------------------------------------- math
+// silu(x) = h + h*tanh(h), h = x/2: a single MUFU op (tanh.approx), used
+// where the result is rounded to bf16 anyway.
+__device__ __forceinline__ float silu_fast(float x) {
+    const float h = 0.5f * x;
+    float t;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(h));
+    return fmaf(h, t, h);
+}
+
 __device__ __forceinline__ float silu_f32(float x) {
     // x * sigmoid(x), sigmoid split by sign like kernels.hpp:96-103
     const float e = __expf(-fabsf(x));
