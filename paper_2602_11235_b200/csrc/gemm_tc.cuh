@@ -45,6 +45,8 @@ constexpr int kMaxProblems = 16;
 struct GemmProblem {
     CUtensorMap tma_a;      // box {64, 128}, SW128 (A_TMA only)
     CUtensorMap tma_b;      // box {64, BN}, SW128
+    CUtensorMap tma_c;      // output, box {32, 32}: bf16 SW64 / f32 SW128 (use_tma_c)
+    int use_tma_c;          // plain row-major output rows [0, M): bulk-tensor stores
     int M, N, K;            // K padded to a multiple of 64
     int Kv;                 // true K (columns of a_src / gain rows)
     int tile_start;         // first global tile of this problem
@@ -86,7 +88,7 @@ struct Cfg {
     static constexpr int B_BYTES = BN * BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
-    static constexpr int STG_BYTES = 8 * 32 * 32 * 4;  // per epilogue warp: 32 rows x 32 fp32
+    static constexpr int STG_BYTES = 8 * 2 * 32 * 32 * 4;  // per epilogue warp: 2 x (32 rows x 32 fp32)
     static constexpr int SMEM = kStages * STAGE_BYTES + STG_BYTES + 1024 /*align*/ + 256 /*barriers*/;
     static constexpr int kThreads = 512;
     static_assert(SMEM <= 227 * 1024, "SMEM budget");
@@ -312,15 +314,18 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
         }
     } else if (warp >= 4) {
         // ------------------------------------------------ epilogue
-        // TMEM -> registers (bias, SiLU) -> XOR-swizzled SMEM staging ->
-        // coalesced row-segment stores (8 lanes x 16 B per row).
+        // TMEM -> registers (bias, SiLU) -> swizzled SMEM staging (double
+        // buffered per warp) -> TMA bulk-tensor store, or for row-mapped /
+        // residual outputs coalesced 16-byte row-segment stores.
         const uint32_t q = warp & 3;            // TMEM lane quarter
         const uint32_t half = (warp - 4) >> 2;  // column half
-        float* stg = stg_all + (warp - 4) * 32 * 32;
+        float* stg_base = stg_all + (warp - 4) * 2 * 32 * 32;
         const int sub = lane >> 3;              // row within a 4-row group
         const int ch = lane & 7;                // 16-byte chunk within a 32-column row slice
         int acc = 0;
         uint32_t acc_phase = 0;
+        uint32_t nstore = 0;                    // staging buffers used by this warp
+        constexpr int kChunks = BN / 2 / 32 > 0 ? BN / 2 / 32 : 1;
         for (int t = blockIdx.x; t < args.n_tiles; t += gridDim.x) {
             int pi, mb, nb;
             gemm_detail::decode_tile(args, t, pi, mb, nb);
@@ -329,30 +334,85 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
             ptx::tc_fence_after();
             const int row0 = mb * C::BM + q * 32;
             const int n_begin = half * (BN / 2);
+            const bool bf16_out = p.epi == EPI_SILU_BF16 || p.epi == EPI_BIAS_BF16;
 #pragma unroll 1
-            for (int c = n_begin; c < n_begin + BN / 2; c += 32) {
+            for (int ci = 0; ci < kChunks; ++ci) {
+                const int c = n_begin + ci * 32;
                 const int n0 = nb * BN + c;
-                if (n0 >= p.N) break;  // warp-uniform
-                {
-                    float v[32];
+                const bool live = n0 < p.N && c < BN;  // warp-uniform
+                float v[32];
+                if (c < BN) {
                     ptx::tmem_ld16(tmem_base + ((q * 32u) << 16) + acc * BN + c, *reinterpret_cast<float(*)[16]>(v));
                     ptx::tmem_ld16(tmem_base + ((q * 32u) << 16) + acc * BN + c + 16,
                                    *reinterpret_cast<float(*)[16]>(v + 16));
                     ptx::tmem_ld_wait();
-                    if (p.bias) {
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) v[i] += (n0 + i < p.N) ? __ldg(p.bias + n0 + i) : 0.f;
-                    }
-                    if (p.epi == EPI_SILU_BF16) {
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) v[i] = ptx::silu_fast(v[i]);
-                    }
-                    // stage: row = lane, chunk k stored at (k ^ (lane & 7))
-#pragma unroll
-                    for (int k = 0; k < 8; ++k)
-                        *reinterpret_cast<float4*>(stg + lane * 32 + ((k ^ (lane & 7)) << 2)) =
-                            make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
                 }
+                if (ci == kChunks - 1) {
+                    // accumulator fully read: hand it back to the MMA warp early
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&tempty_bar[acc]);
+                }
+                if (!live) continue;
+                if (p.bias) {
+                    const float* bp = p.bias + n0;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        float4 b4;
+                        if (n0 + 4 * k + 3 < p.N) {
+                            b4 = __ldg(reinterpret_cast<const float4*>(bp) + k);
+                        } else {
+                            b4.x = n0 + 4 * k < p.N ? __ldg(bp + 4 * k) : 0.f;
+                            b4.y = n0 + 4 * k + 1 < p.N ? __ldg(bp + 4 * k + 1) : 0.f;
+                            b4.z = n0 + 4 * k + 2 < p.N ? __ldg(bp + 4 * k + 2) : 0.f;
+                            b4.w = 0.f;
+                        }
+                        v[4 * k] += b4.x;
+                        v[4 * k + 1] += b4.y;
+                        v[4 * k + 2] += b4.z;
+                        v[4 * k + 3] += b4.w;
+                    }
+                }
+                if (p.epi == EPI_SILU_BF16) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v[i] = ptx::silu_fast(v[i]);
+                }
+                float* stg = stg_base + (nstore & 1) * 32 * 32;
+                if (p.use_tma_c) {
+                    // the staging buffer written two stores ago must have been read by the TMA engine
+                    if (lane == 0) ptx::bulk_wait_read<1>();
+                    __syncwarp();
+                    if (bf16_out) {
+                        // 32 rows x 64 B, SWIZZLE_64B: 16 B chunk k of row r at (k ^ ((r >> 1) & 3))
+                        uint8_t* sb = reinterpret_cast<uint8_t*>(stg);
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            *reinterpret_cast<uint4*>(sb + lane * 64 + ((k ^ ((lane >> 1) & 3)) << 4)) =
+                                make_uint4(pack_bf16(v[8 * k], v[8 * k + 1]), pack_bf16(v[8 * k + 2], v[8 * k + 3]),
+                                           pack_bf16(v[8 * k + 4], v[8 * k + 5]), pack_bf16(v[8 * k + 6], v[8 * k + 7]));
+                    } else {
+                        // 32 rows x 128 B, SWIZZLE_128B: chunk k of row r at (k ^ (r & 7))
+#pragma unroll
+                        for (int k = 0; k < 8; ++k)
+                            *reinterpret_cast<float4*>(stg + lane * 32 + ((k ^ (lane & 7)) << 2)) =
+                                make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+                    }
+                    ptx::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        ptx::tma_store_2d(&p.tma_c, stg, n0, row0);
+                        ptx::bulk_commit();
+                    }
+                    ++nstore;
+                    continue;
+                }
+                // ---- manual path (row-mapped scatter / residual)
+                if (lane == 0) ptx::bulk_wait_read<1>();
+                __syncwarp();
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    *reinterpret_cast<float4*>(stg + lane * 32 + ((k ^ (lane & 7)) << 2)) =
+                        make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
                 __syncwarp();
                 const int col = n0 + 4 * ch;
                 const int nval = min(4, p.N - col);
@@ -364,7 +424,7 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                                   ? (p.row_map ? static_cast<long long>(__ldg(p.row_map + m)) : p.row_offset + m)
                                   : -1;
                 }
-                if (p.epi == EPI_SILU_BF16 || p.epi == EPI_BIAS_BF16) {
+                if (bf16_out) {
 #pragma unroll
                     for (int g = 0; g < 8; ++g) {
                         const int r = 4 * g + sub;
@@ -415,15 +475,15 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                     }
                 }
                 __syncwarp();
+                ++nstore;
             }
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&tempty_bar[acc]);
             if (++acc == 2) {
                 acc = 0;
                 acc_phase ^= 1;
             }
         }
+        if (lane == 0) ptx::bulk_wait<0>();  // all bulk stores complete before exit
+        __syncwarp();
     }
     ptx::tc_fence_before();
     __syncthreads();

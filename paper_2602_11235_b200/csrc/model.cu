@@ -76,21 +76,22 @@ EncodeFn encode_fn() {
     return fn;
 }
 
-// 2-D bf16 tensor map over a row-major [rows][cols] matrix with row stride ld.
+// 2-D tensor map over a row-major [rows][cols] matrix with row stride ld (elements).
 CUtensorMap tma_2d(const void* ptr, long long rows, long long cols, long long ld, int box_cols, int box_rows,
-                   int swizzle_bytes) {
+                   int swizzle_bytes, int elem_bytes = 2) {
     CUtensorMap m;
     std::memset(&m, 0, sizeof(m));
     if (rows == 0) return m;
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
-    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * elem_bytes)};
     cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
     cuuint32_t es[2] = {1, 1};
     CUtensorMapSwizzle sw = swizzle_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
                             : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
                             : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
                                                   : CU_TENSOR_MAP_SWIZZLE_NONE;
-    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+    CUresult r = encode_fn()(&m, elem_bytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                             2, const_cast<void*>(ptr), dims, strides, box, es,
                              CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) fail(MTFM_CUDA_ERROR, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
@@ -542,6 +543,15 @@ void run_gemm_tc(std::vector<TcProblem> ps, cudaStream_t st, long long& launches
             p.row_map = s.row_map;
             p.row_offset = s.row_offset;
             p.resid = s.resid;
+            // bulk-tensor stores for plain row-major outputs (rows [row_offset, row_offset + M))
+            const bool bf16_out = s.epi == EPI_SILU_BF16 || s.epi == EPI_BIAS_BF16;
+            const int eb = bf16_out ? 2 : 4;
+            p.use_tma_c = !s.row_map && s.epi != EPI_RESID_F32 && (s.ldo * eb) % 16 == 0 &&
+                          (reinterpret_cast<uintptr_t>(s.out) % 16) == 0 && std::getenv("MTFM_NO_TMA_STORE") == nullptr;
+            if (p.use_tma_c) {
+                const char* base = static_cast<const char*>(s.out) + s.row_offset * s.ldo * eb;
+                p.tma_c = tma_2d(base, s.M, s.N, s.ldo, 32, 32, bf16_out ? 64 : 128, eb);
+            }
             tiles += static_cast<int>(cdiv(s.M, 128)) * p.tiles_n;
         }
         a.n_tiles = tiles;
