@@ -15,10 +15,10 @@
 // so every K/V tile TMA-loaded into SMEM is shared by the HS query heads that
 // read it. Per key tile j:
 //   MMA warp     : S[j%2] = Q K_j^T            (TMEM, fp32, 128 x BKV)
-//                  O[t%2] += P[(j-1)%2] V_{j-1} (P from SMEM, V MN-major)
-//   8 SiLU warps : S -> regs, silu = h + h*tanh(h) (h = s/2: FMUL2, MUFU.TANH,
+//                  O[t%2] += P[(j-2)%2] V_{j-2} (P from TMEM, V MN-major SMEM)
+//   16 SiLU warps: S -> regs, silu = h + h*tanh(h) (h = s/2: FMUL2, MUFU.TANH,
 //                  FFMA2), mask only on the boundary key tile, bf16 pack,
-//                  swizzled st.shared into P[j%2], fence.proxy.async, arrive.
+//                  tcgen05.st into the TMEM P[j%2] buffer, arrive.
 //   4 epilogue warps: O[t%2] -> regs, x s_i, + self term for T rows, bf16 out
 //                  (overlaps the next tile's key loop).
 // Q and O are double-buffered, so consecutive tiles of a CTA pipeline.
@@ -60,7 +60,7 @@ namespace attn_detail {
 
 template <int D>
 struct Cfg {
-    static constexpr int BKV = D <= 128 ? 128 : 64;
+    static constexpr int BKV = D <= 64 ? 128 : 64;
     static constexpr int CHUNK = D < 64 ? D : 64;          // elements per swizzle row
     static constexpr int SLABS = D / CHUNK;
     static constexpr int ROWB = CHUNK * 2;                  // bytes per swizzled row
@@ -70,13 +70,17 @@ struct Cfg {
     static constexpr int STAGE_BYTES = 2 * KV_TILE_BYTES;
     static constexpr int P_BYTES = 128 * BKV * 2;
     static constexpr int QB = D <= 64 ? 2 : 1;              // Q buffers
-    static constexpr int kStages = D <= 64 ? 4 : 2;
-    static constexpr int SMEM = QB * Q_BYTES + kStages * STAGE_BYTES + 2 * P_BYTES + 1024 + 512;
+    static constexpr int kStages = D <= 128 ? (D <= 64 ? 4 : 3) : 2;
+    static constexpr int LAG = kStages >= 3 ? 2 : 1;        // PV of key tile i issued after S of tile i+LAG
+    static constexpr int SMEM = QB * Q_BYTES + kStages * STAGE_BYTES + 1024 + 512;
     static constexpr uint32_t TMEM_COLS = 512;
     static constexpr uint32_t S_COL = 0;                    // S buffers at [0, 2*BKV)
-    static constexpr uint32_t O_COL = 2 * BKV;
-    static constexpr int OB = (2 * BKV + 2 * D <= 512) ? 2 : 1;  // O buffers
-    static constexpr int kThreads = 512;
+    static constexpr uint32_t P_COL = 2 * BKV;               // P (packed bf16) buffers at [2*BKV, 3*BKV)
+    static constexpr uint32_t O_COL = 3 * BKV;
+    static constexpr int OB = (3 * BKV + 2 * D <= 512) ? 2 : 1;  // O buffers
+    static constexpr int kSilu = 16;                        // SiLU warps (4 per TMEM lane quarter)
+    static constexpr int CPW = BKV / 4;                     // key columns per SiLU warp
+    static constexpr int kThreads = (4 + kSilu + 4) * 32;   // + TMA/MMA/alloc/spare + 4 epilogue warps
     static_assert(O_COL + OB * D <= 512, "TMEM budget");
     static_assert(SMEM <= 227 * 1024, "SMEM budget");
 };
@@ -107,15 +111,14 @@ __device__ __forceinline__ uint32_t silu2_bf16(float s0, float s1) {
 }  // namespace attn_detail
 
 template <int D>
-__global__ void __launch_bounds__(512, 1) attn_tc_kernel(const __grid_constant__ AttnParams prm) {
+__global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__ AttnParams prm) {
     using C = attn_detail::Cfg<D>;
     constexpr int BKV = C::BKV;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sQ = smem;
     uint8_t* sKV = sQ + C::QB * C::Q_BYTES;
-    uint8_t* sP = sKV + C::kStages * C::STAGE_BYTES;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * C::P_BYTES);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + C::kStages * C::STAGE_BYTES);
     uint64_t* q_full = bars + 0;   // [2]
     uint64_t* q_empty = bars + 2;  // [2]
     uint64_t* o_full = bars + 4;   // [2]
@@ -139,8 +142,8 @@ __global__ void __launch_bounds__(512, 1) attn_tc_kernel(const __grid_constant__
             ptx::mbar_init(&o_full[i], 1);
             ptx::mbar_init(&o_empty[i], 4);
             ptx::mbar_init(&s_full[i], 1);
-            ptx::mbar_init(&s_empty[i], 8);
-            ptx::mbar_init(&p_full[i], 8);
+            ptx::mbar_init(&s_empty[i], C::kSilu);
+            ptx::mbar_init(&p_full[i], C::kSilu);
             ptx::mbar_init(&p_empty[i], 1);
         }
         for (int i = 0; i < C::kStages; ++i) {
@@ -197,11 +200,59 @@ __global__ void __launch_bounds__(512, 1) attn_tc_kernel(const __grid_constant__
         }
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer
+        // One continuous stream of key tiles across query tiles: S of item i is
+        // issued as soon as its K tile and S buffer are free; the P.V of item
+        // i - LAG follows, so S always runs LAG key tiles ahead of the SiLU warps.
         const uint32_t idesc_s = ptx::instr_desc_bf16(128, BKV, false, false);
         const uint32_t idesc_o = ptx::instr_desc_bf16(128, D, false, true);
+        struct Item {
+            int ob, stage, j, n_kv, it;
+            uint32_t cnt;  // key-tile counter (S/P buffer and parity)
+            bool dummy;    // query tile without visible keys: no MMA, O signalled empty
+        };
+        Item p0{}, p1{};  // pending P.V items (oldest first), at most LAG
+        int size = 0;
         int stage = 0;
         uint32_t phase = 0;
-        uint32_t s_cnt = 0;  // global key-tile counter (S/P buffer parity)
+        uint32_t s_cnt = 0;
+        auto issue_pv = [&](const Item& x) {
+            if (x.dummy || x.j == 0) {
+                ptx::mbar_wait(&o_empty[x.ob], ((x.it / C::OB) & 1) ^ 1);
+                ptx::tc_fence_after();
+            }
+            if (x.dummy) {
+                if (ptx::elect_one()) ptx::umma_commit(&o_full[x.ob]);
+                __syncwarp();
+                return;
+            }
+            const uint32_t buf = x.cnt & 1;
+            ptx::mbar_wait(&p_full[buf], (x.cnt >> 1) & 1);
+            ptx::tc_fence_after();
+            if (ptx::elect_one()) {
+                const uint32_t p_tmem = tmem + C::P_COL + buf * (BKV / 2);
+                const uint32_t sv = ptx::smem_u32(sKV + x.stage * C::STAGE_BYTES + C::KV_TILE_BYTES);
+                const uint32_t o_tmem = tmem + C::O_COL + x.ob * D;
+#pragma unroll
+                for (int kk = 0; kk < BKV / 16; ++kk) {
+                    const uint64_t db = ptx::smem_desc(sv + kk * 16 * C::ROWB, BKV * C::ROWB, 8 * C::ROWB, C::LAYOUT);
+                    ptx::umma_bf16_ts(o_tmem, p_tmem + kk * 8, db, idesc_o, (x.j > 0 || kk > 0));
+                }
+                ptx::umma_commit(&kv_empty[x.stage]);
+                ptx::umma_commit(&p_empty[buf]);
+                if (x.j == x.n_kv - 1) ptx::umma_commit(&o_full[x.ob]);
+            }
+            __syncwarp();
+        };
+        auto push = [&](const Item& x) {
+            if (size == C::LAG) {  // oldest pending item is now LAG key tiles behind
+                issue_pv(p0);
+                p0 = p1;
+                --size;
+            }
+            if (size == 0) p0 = x;
+            else p1 = x;
+            ++size;
+        };
         int it = 0;
         for (int t = blockIdx.x; t < prm.n_tiles; t += gridDim.x, ++it) {
             const AttnTile tile = prm.tiles[t];
@@ -209,79 +260,49 @@ __global__ void __launch_bounds__(512, 1) attn_tc_kernel(const __grid_constant__
             const int qb = it % C::QB;
             const int ob = it % C::OB;
             ptx::mbar_wait(&q_full[qb], (it / C::QB) & 1);
-            ptx::mbar_wait(&o_empty[ob], ((it / C::OB) & 1) ^ 1);
             ptx::tc_fence_after();
-            const uint32_t sq = ptx::smem_u32(sQ + qb * C::Q_BYTES);
-            const uint32_t o_tmem = tmem + C::O_COL + ob * D;
-            int prev_stage = -1;
-            for (int j = 0; j <= n_kv; ++j) {
-                if (j < n_kv) {
-                    const uint32_t buf = s_cnt & 1;
-                    const uint32_t par = (s_cnt >> 1) & 1;
-                    ptx::mbar_wait(&kv_full[stage], phase);
-                    ptx::mbar_wait(&s_empty[buf], par ^ 1);
-                    ptx::tc_fence_after();
-                    if (ptx::elect_one()) {
-                        const uint32_t sk = ptx::smem_u32(sKV + stage * C::STAGE_BYTES);
-#pragma unroll
-                        for (int kk = 0; kk < D / 16; ++kk) {
-                            const uint32_t sl = (kk * 16) / C::CHUNK;
-                            const uint32_t in = ((kk * 16) % C::CHUNK) * 2;
-                            const uint64_t da = ptx::smem_desc(sq + sl * (128 * C::ROWB) + in, 16, 8 * C::ROWB, C::LAYOUT);
-                            const uint64_t db = ptx::smem_desc(sk + sl * (BKV * C::ROWB) + in, 16, 8 * C::ROWB, C::LAYOUT);
-                            ptx::umma_bf16(tmem + C::S_COL + buf * BKV, da, db, idesc_s, kk > 0);
-                        }
-                        if (j == n_kv - 1) ptx::umma_commit(&q_empty[qb]);
-                        ptx::umma_commit(&s_full[buf]);
-                    }
-                    __syncwarp();
-                }
-                if (j >= 1) {
-                    const uint32_t pc = s_cnt - 1;  // P of key tile j-1
-                    const uint32_t buf = pc & 1;
-                    const uint32_t par = (pc >> 1) & 1;
-                    ptx::mbar_wait(&p_full[buf], par);
-                    ptx::tc_fence_after();
-                    if (ptx::elect_one()) {
-                        const uint32_t sp = ptx::smem_u32(sP + buf * C::P_BYTES);
-                        const uint32_t sv = ptx::smem_u32(sKV + prev_stage * C::STAGE_BYTES + C::KV_TILE_BYTES);
-#pragma unroll
-                        for (int kk = 0; kk < BKV / 16; ++kk) {
-                            const uint32_t psl = (kk * 16) / 64;
-                            const uint32_t pin = ((kk * 16) % 64) * 2;
-                            const uint64_t da = ptx::smem_desc(sp + psl * (128 * 128) + pin, 16, 1024, 2);
-                            const uint64_t db = ptx::smem_desc(sv + kk * 16 * C::ROWB, BKV * C::ROWB, 8 * C::ROWB, C::LAYOUT);
-                            ptx::umma_bf16(o_tmem, da, db, idesc_o, (j > 1 || kk > 0));
-                        }
-                        ptx::umma_commit(&kv_empty[prev_stage]);
-                        ptx::umma_commit(&p_empty[buf]);
-                        if (j == n_kv) ptx::umma_commit(&o_full[ob]);
-                    }
-                    __syncwarp();
-                }
-                if (j < n_kv) {
-                    prev_stage = stage;
-                    ++s_cnt;
-                    if (++stage == C::kStages) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
-                }
-            }
             if (n_kv == 0) {
-                // no visible context keys: release Q, signal an (unused) O
+                if (ptx::elect_one()) ptx::umma_commit(&q_empty[qb]);
+                __syncwarp();
+                push(Item{ob, 0, 0, 0, it, 0u, true});
+                continue;
+            }
+            const uint32_t sq = ptx::smem_u32(sQ + qb * C::Q_BYTES);
+            for (int j = 0; j < n_kv; ++j) {
+                const uint32_t buf = s_cnt & 1;
+                ptx::mbar_wait(&kv_full[stage], phase);
+                ptx::mbar_wait(&s_empty[buf], ((s_cnt >> 1) & 1) ^ 1);
+                ptx::tc_fence_after();
                 if (ptx::elect_one()) {
-                    ptx::umma_commit(&q_empty[qb]);
-                    ptx::umma_commit(&o_full[ob]);
+                    const uint32_t sk = ptx::smem_u32(sKV + stage * C::STAGE_BYTES);
+#pragma unroll
+                    for (int kk = 0; kk < D / 16; ++kk) {
+                        const uint32_t sl = (kk * 16) / C::CHUNK;
+                        const uint32_t in = ((kk * 16) % C::CHUNK) * 2;
+                        const uint64_t da = ptx::smem_desc(sq + sl * (128 * C::ROWB) + in, 16, 8 * C::ROWB, C::LAYOUT);
+                        const uint64_t db = ptx::smem_desc(sk + sl * (BKV * C::ROWB) + in, 16, 8 * C::ROWB, C::LAYOUT);
+                        ptx::umma_bf16(tmem + C::S_COL + buf * BKV, da, db, idesc_s, kk > 0);
+                    }
+                    if (j == n_kv - 1) ptx::umma_commit(&q_empty[qb]);
+                    ptx::umma_commit(&s_full[buf]);
                 }
                 __syncwarp();
+                push(Item{ob, stage, j, n_kv, it, s_cnt, false});
+                ++s_cnt;
+                if (++stage == C::kStages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
             }
         }
-    } else if (warp >= 4 && warp < 12) {
+        if (size > 0) issue_pv(p0);
+        if (size > 1) issue_pv(p1);
+    } else if (warp >= 4 && warp < 4 + C::kSilu) {
         // ------------------------------------------------ SiLU warps
+        constexpr int CPW = C::CPW;
         const uint32_t q = warp & 3;
-        const uint32_t half = (warp - 4) >> 2;
-        const uint32_t m = q * 32 + lane;  // MMA row == TMEM lane
+        const uint32_t slice = (warp - 4) >> 2;  // column slice of CPW keys
+        const uint32_t m = q * 32 + lane;        // MMA row == TMEM lane
         const uint32_t lane_addr = (q * 32u) << 16;
         uint32_t s_cnt = 0;
         for (int t = blockIdx.x; t < prm.n_tiles; t += gridDim.x) {
@@ -293,29 +314,26 @@ __global__ void __launch_bounds__(512, 1) attn_tc_kernel(const __grid_constant__
             for (int j = 0; j < n_kv; ++j, ++s_cnt) {
                 const uint32_t buf = s_cnt & 1;
                 const uint32_t par = (s_cnt >> 1) & 1;
-                const int key0 = j * BKV + half * (BKV / 2);  // first key of my column half
-                const int nvalid = prefix - key0;             // >= BKV/2: no masking needed
+                const int col0 = slice * CPW;           // key column within tile
+                const int nvalid = prefix - (j * BKV + col0);  // >= CPW: no masking needed
                 ptx::mbar_wait(&s_full[buf], par);
                 ptx::tc_fence_after();
-                float v[BKV / 2];
+                float v[CPW];
 #pragma unroll
-                for (int c = 0; c < BKV / 32; ++c) {
-                    float tmp[16];
-                    ptx::tmem_ld16(tmem + lane_addr + C::S_COL + buf * BKV + half * (BKV / 2) + c * 16, tmp);
-#pragma unroll
-                    for (int e = 0; e < 16; ++e) v[c * 16 + e] = tmp[e];
-                }
+                for (int c = 0; c < CPW / 16; ++c)
+                    ptx::tmem_ld16(tmem + lane_addr + C::S_COL + buf * BKV + col0 + c * 16,
+                                   *reinterpret_cast<float(*)[16]>(v + c * 16));
                 ptx::tmem_ld_wait();
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&s_empty[buf]);
-                uint32_t packed[BKV / 4];
-                if (__all_sync(0xffffffffu, nvalid >= BKV / 2)) {
+                uint32_t packed[CPW / 2];
+                if (__all_sync(0xffffffffu, nvalid >= CPW)) {
 #pragma unroll
-                    for (int e = 0; e < BKV / 2; e += 2) packed[e / 2] = attn_detail::silu2_bf16(v[e], v[e + 1]);
+                    for (int e = 0; e < CPW; e += 2) packed[e / 2] = attn_detail::silu2_bf16(v[e], v[e + 1]);
                 } else {
 #pragma unroll
-                    for (int e = 0; e < BKV / 2; e += 2) {
+                    for (int e = 0; e < CPW; e += 2) {
                         const uint32_t w = attn_detail::silu2_bf16(v[e], v[e + 1]);
                         const uint32_t keep = (e + 1 < nvalid) ? 0xffffffffu : (e < nvalid ? 0x0000ffffu : 0u);
                         packed[e / 2] = w & keep;
@@ -323,24 +341,22 @@ __global__ void __launch_bounds__(512, 1) attn_tc_kernel(const __grid_constant__
                 }
                 // P buffer must have been consumed by the MMA two key tiles ago
                 ptx::mbar_wait(&p_empty[buf], par ^ 1);
-                uint8_t* pb = sP + buf * C::P_BYTES;
-#pragma unroll
-                for (int c = 0; c < BKV / 32; ++c) {
-                    const int col = half * (BKV / 2) + c * 16;  // key column within tile
-                    const int slab = col / 64;
-                    const uint32_t ch = (col % 64) / 8;         // 16B chunk index (8 bf16)
-                    uint8_t* base = pb + slab * (128 * 128);
-                    *reinterpret_cast<uint4*>(base + attn_detail::sw128_off(m, ch)) =
-                        make_uint4(packed[c * 8 + 0], packed[c * 8 + 1], packed[c * 8 + 2], packed[c * 8 + 3]);
-                    *reinterpret_cast<uint4*>(base + attn_detail::sw128_off(m, ch + 1)) =
-                        make_uint4(packed[c * 8 + 4], packed[c * 8 + 5], packed[c * 8 + 6], packed[c * 8 + 7]);
+                ptx::tc_fence_after();
+                {
+                    const uint32_t pa = tmem + lane_addr + C::P_COL + buf * (BKV / 2) + col0 / 2;
+                    if constexpr (CPW == 32) {
+                        ptx::tmem_st16(pa, *reinterpret_cast<const uint32_t(*)[16]>(packed));
+                    } else {
+                        ptx::tmem_st8(pa, *reinterpret_cast<const uint32_t(*)[8]>(packed));
+                    }
                 }
-                ptx::fence_proxy_async_smem();
+                ptx::tmem_st_wait();
+                ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&p_full[buf]);
             }
         }
-    } else if (warp >= 12) {
+    } else if (warp >= 4 + C::kSilu) {
         // ------------------------------------------------ epilogue warps
         const uint32_t q = warp & 3;
         const uint32_t m = q * 32 + lane;
