@@ -182,8 +182,16 @@ def main():
     from paper_2602_11235_b200.schema import BATCH_KEYS, batch_nbytes
 
     wl = datagen.WORKLOADS[CONFIGS[args.config][0]]()
-    wl.seed = wl.seed + 1000 * rank  # every rank scores its own users (weak scaling)
-    batch = datagen.generate(wl, n_users=args.users)
+    per_gpu = args.users or wl.n_users
+    if world == 1:
+        batch = datagen.generate(wl, n_users=per_gpu)
+    else:
+        # one global batch of world x per_gpu users, sharded by LPT on estimated
+        # cost; no collective touches the data path (weak scaling)
+        from paper_2602_11235_b200.shard import shard_plan, take_users
+        full = datagen.generate(wl, n_users=per_gpu * world)
+        batch = take_users(full, shard_plan(full, world)[rank])
+        del full
     model = Model(wl.schemas, wl.cfg, precision="bf16", device=local)
     model.set_params(datagen.random_params(model.param_specs(), seed=7))
     n_targets = int(len(batch["exp_ts"]))

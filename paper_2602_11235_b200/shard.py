@@ -1,0 +1,86 @@
+"""User sharding across GPUs: users are independent, so a batch
+is partitioned across ranks with no collective on the data path.
+
+shard_plan(batch, world)   greedy LPT over an estimated per-user cost (full
+                           layers ~ N^2 attention + N projections, target
+                           layers ~ N): returns a list of user-index arrays.
+take_users(batch, users)   re-packs a subset of users into a new packed batch
+                           (include/mtfm_cuda.h layout), preserving order.
+"""
+from __future__ import annotations
+
+import heapq
+
+import numpy as np
+
+from .schema import normalize_batch
+
+
+def user_costs(batch, d_model=256, full_layers=1, target_layers=3):
+    b = normalize_batch(batch)
+    U = len(b["user_id"])
+    ev0 = b["ev_off"][b["seq_off"][:-1]] if len(b["ev_off"]) > 1 else np.zeros(U, np.int64)
+    ev1 = b["ev_off"][b["seq_off"][1:]] if len(b["ev_off"]) > 1 else np.zeros(U, np.int64)
+    n_ctx = (ev1 - ev0).astype(np.float64)
+    n_t = np.diff(b["exp_off"]).astype(np.float64)
+    n = n_ctx + n_t
+    # projection MACs ~ N*d*(4d) per full layer, attention ~ 2*d*N*n_ctx;
+    # target layers ~ N*d*d (fkv) + n_t * (2*d*n_ctx)
+    full = n * d_model * 4 * d_model + 2.0 * d_model * n * n_ctx
+    tgt = n * d_model * d_model + n_t * (2.0 * d_model * n_ctx + 3 * d_model * d_model)
+    return full_layers * full + target_layers * tgt + 1.0
+
+
+def shard_plan(batch, world, costs=None):
+    """Greedy longest-processing-time assignment; each shard keeps batch order."""
+    if costs is None:
+        costs = user_costs(batch)
+    order = np.argsort(-costs, kind="stable")
+    heap = [(0.0, r) for r in range(world)]
+    owner = np.empty(len(costs), np.int64)
+    for u in order:
+        load, r = heapq.heappop(heap)
+        owner[u] = r
+        heapq.heappush(heap, (load + float(costs[u]), r))
+    return [np.nonzero(owner == r)[0] for r in range(world)]
+
+
+def take_users(batch, users):
+    """Packed sub-batch of the given users (in the given order)."""
+    b = normalize_batch(batch)
+    users = np.asarray(users, np.int64)
+    seq_off, ev_off, exp_off = b["seq_off"], b["ev_off"], b["exp_off"]
+    ev_fo, ex_fo = b["ev_feat_off"], b["exp_feat_off"]
+    seqs = [np.arange(seq_off[u], seq_off[u + 1]) for u in users]
+    seq_idx = np.concatenate(seqs) if seqs else np.zeros(0, np.int64)
+    n_seq = np.array([len(s) for s in seqs], np.int64)
+    ev_len = (ev_off[seq_idx + 1] - ev_off[seq_idx]).astype(np.int64)
+    evs = np.concatenate([np.arange(ev_off[s], ev_off[s + 1]) for s in seq_idx]) if len(seq_idx) else \
+        np.zeros(0, np.int64)
+    xs = np.concatenate([np.arange(exp_off[u], exp_off[u + 1]) for u in users]) if len(users) else \
+        np.zeros(0, np.int64)
+    n_x = np.array([exp_off[u + 1] - exp_off[u] for u in users], np.int64)
+
+    def cat_ranges(off, idx):
+        parts = [np.arange(off[i], off[i + 1]) for i in idx]
+        return np.concatenate(parts) if parts else np.zeros(0, np.int64)
+
+    ev_flen = (ev_fo[evs + 1] - ev_fo[evs]).astype(np.int64) if len(evs) else np.zeros(0, np.int64)
+    ex_flen = (ex_fo[xs + 1] - ex_fo[xs]).astype(np.int64) if len(xs) else np.zeros(0, np.int64)
+    out = dict(
+        user_id=b["user_id"][users],
+        seq_off=np.concatenate([[0], np.cumsum(n_seq)]),
+        seq_kind=b["seq_kind"][seq_idx],
+        seq_schema=b["seq_schema"][seq_idx],
+        ev_off=np.concatenate([[0], np.cumsum(ev_len)]),
+        ev_ts=b["ev_ts"][evs],
+        ev_feat_off=np.concatenate([[0], np.cumsum(ev_flen)]),
+        ev_feats=b["ev_feats"][cat_ranges(ev_fo, evs)],
+        exp_off=np.concatenate([[0], np.cumsum(n_x)]),
+        exp_scenario=b["exp_scenario"][xs],
+        exp_ts=b["exp_ts"][xs],
+        exp_feat_off=np.concatenate([[0], np.cumsum(ex_flen)]),
+        exp_blk=b["exp_blk"].reshape(-1, 3)[xs].reshape(-1),
+        exp_feats=b["exp_feats"][cat_ranges(ex_fo, xs)],
+    )
+    return normalize_batch(out)
