@@ -47,6 +47,7 @@ struct GemmProblem {
     CUtensorMap tma_b;      // box {64, BN}, SW128
     CUtensorMap tma_c;      // output, box {32, 32}: bf16 SW64 / f32 SW128 (use_tma_c)
     int use_tma_c;          // plain row-major output rows [0, M): bulk-tensor stores
+    int use_tma_r;          // EPI_RESID_F32 with resid == out: residual blocks TMA-prefetched via tma_c
     int M, N, K;            // K padded to a multiple of 64
     int Kv;                 // true K (columns of a_src / gain rows)
     int tile_start;         // first global tile of this problem
@@ -89,7 +90,7 @@ struct Cfg {
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
     static constexpr int STG_BYTES = 8 * 2 * 32 * 32 * 4;  // per epilogue warp: 2 x (32 rows x 32 fp32)
-    static constexpr int SMEM = kStages * STAGE_BYTES + STG_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int SMEM = kStages * STAGE_BYTES + STG_BYTES + 1024 /*align*/ + 384 /*barriers*/;
     static constexpr int kThreads = 512;
     static_assert(SMEM <= 227 * 1024, "SMEM budget");
 };
@@ -193,7 +194,8 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
     uint64_t* empty_bar = full_bar + C::kStages;
     uint64_t* tfull_bar = empty_bar + C::kStages;
     uint64_t* tempty_bar = tfull_bar + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+    uint64_t* res_bar = tempty_bar + 2;  // [8 epilogue warps][2 staging buffers]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(res_bar + 16);
 
     const uint32_t warp = ptx::warp_id();
     const uint32_t lane = ptx::lane_id();
@@ -208,6 +210,7 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
             ptx::mbar_init(&tfull_bar[s], 1);
             ptx::mbar_init(&tempty_bar[s], 8);  // one arrive per epilogue warp
         }
+        for (int s = 0; s < 16; ++s) ptx::mbar_init(&res_bar[s], 1);
         ptx::fence_mbar_init();
         for (int i = 0; i < args.n_problems; ++i) {
             if (a_mode == A_TMA) ptx::tma_prefetch(&args.p[i].tma_a);
@@ -325,15 +328,26 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
         int acc = 0;
         uint32_t acc_phase = 0;
         uint32_t nstore = 0;                    // staging buffers used by this warp
+        uint32_t res_phase = 0;                 // parity bit per staging buffer
+        uint64_t* my_res = res_bar + (warp - 4) * 2;
         constexpr int kChunks = BN / 2 / 32 > 0 ? BN / 2 / 32 : 1;
+        // residual prefetch of one 32 x 32 fp32 block into staging buffer b
+        auto res_load = [&](const GemmProblem& pp, int b, int col, int row) {
+            if (lane == 0) {
+                ptx::bulk_wait_read<1>();  // the store that last used buffer b has read it
+                ptx::mbar_arrive_expect_tx(&my_res[b], 32 * 32 * 4);
+                ptx::tma_load_2d(stg_base + b * 32 * 32, &pp.tma_c, &my_res[b], col, row);
+            }
+        };
         for (int t = blockIdx.x; t < args.n_tiles; t += gridDim.x) {
             int pi, mb, nb;
             gemm_detail::decode_tile(args, t, pi, mb, nb);
             const GemmProblem& p = args.p[pi];
-            ptx::mbar_wait(&tfull_bar[acc], acc_phase);
-            ptx::tc_fence_after();
             const int row0 = mb * C::BM + q * 32;
             const int n_begin = half * (BN / 2);
+            if (p.use_tma_r && nb * BN + n_begin < p.N) res_load(p, nstore & 1, nb * BN + n_begin, row0);
+            ptx::mbar_wait(&tfull_bar[acc], acc_phase);
+            ptx::tc_fence_after();
             const bool bf16_out = p.epi == EPI_SILU_BF16 || p.epi == EPI_BIAS_BF16;
 #pragma unroll 1
             for (int ci = 0; ci < kChunks; ++ci) {
@@ -378,6 +392,28 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                     for (int i = 0; i < 32; ++i) v[i] = ptx::silu_fast(v[i]);
                 }
                 float* stg = stg_base + (nstore & 1) * 32 * 32;
+                if (p.use_tma_r) {
+                    const int b = nstore & 1;
+                    ptx::mbar_wait(&my_res[b], (res_phase >> b) & 1);
+                    res_phase ^= 1u << b;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        float4* cell = reinterpret_cast<float4*>(stg + lane * 32 + ((k ^ (lane & 7)) << 2));
+                        const float4 r4 = *cell;
+                        *cell = make_float4(v[4 * k] + r4.x, v[4 * k + 1] + r4.y, v[4 * k + 2] + r4.z,
+                                            v[4 * k + 3] + r4.w);
+                    }
+                    ptx::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        ptx::tma_store_2d(&p.tma_c, stg, n0, row0);
+                        ptx::bulk_commit();
+                    }
+                    ++nstore;
+                    // prefetch the next chunk's residual into the other buffer
+                    if (ci + 1 < kChunks && n0 + 32 < p.N && c + 32 < BN) res_load(p, nstore & 1, n0 + 32, row0);
+                    continue;
+                }
                 if (p.use_tma_c) {
                     // the staging buffer written two stores ago must have been read by the TMA engine
                     if (lane == 0) ptx::bulk_wait_read<1>();

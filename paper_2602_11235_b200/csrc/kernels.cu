@@ -645,7 +645,16 @@ __global__ void __launch_bounds__(256) heads_kernel(HeadArgs a) {
 #pragma unroll
                 for (int k = 0; k < kMaxTasks; ++k) m[k] = 0.f;
                 for (int e = 0; e < a.E; ++e) {
-                    const float act = silu_precise(y[e * a.de + c] + a.exp_bias[e * a.de + c]);
+                    const float pre = y[e * a.de + c] + a.exp_bias[e * a.de + c];
+                    float act;
+                    if (a.precise) {
+                        act = silu_precise(pre);
+                    } else {
+                        const float h = 0.5f * pre;
+                        float th;
+                        asm("tanh.approx.f32 %0, %1;" : "=f"(th) : "f"(h));
+                        act = fmaf(h, th, h);
+                    }
 #pragma unroll
                     for (int k = 0; k < kMaxTasks; ++k)
                         if (k < nk) m[k] += act * s_gate[wib][k][e];

@@ -546,8 +546,10 @@ void run_gemm_tc(std::vector<TcProblem> ps, cudaStream_t st, long long& launches
             // bulk-tensor stores for plain row-major outputs (rows [row_offset, row_offset + M))
             const bool bf16_out = s.epi == EPI_SILU_BF16 || s.epi == EPI_BIAS_BF16;
             const int eb = bf16_out ? 2 : 4;
-            p.use_tma_c = !s.row_map && s.epi != EPI_RESID_F32 && (s.ldo * eb) % 16 == 0 &&
-                          (reinterpret_cast<uintptr_t>(s.out) % 16) == 0 && std::getenv("MTFM_NO_TMA_STORE") == nullptr;
+            const bool tma_ok = !s.row_map && (s.ldo * eb) % 16 == 0 && (reinterpret_cast<uintptr_t>(s.out) % 16) == 0 &&
+                                std::getenv("MTFM_NO_TMA_STORE") == nullptr;
+            p.use_tma_c = tma_ok && (s.epi != EPI_RESID_F32 || s.resid == s.out);
+            p.use_tma_r = p.use_tma_c && s.epi == EPI_RESID_F32;
             if (p.use_tma_c) {
                 const char* base = static_cast<const char*>(s.out) + s.row_offset * s.ldo * eb;
                 p.tma_c = tma_2d(base, s.M, s.N, s.ldo, 32, 32, bf16_out ? 64 : 128, eb);
@@ -1366,7 +1368,7 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
     ha.t_rec_stride = rm.t_rec_stride;
     ha.user_id = B.user_id.as<long long>();
     ha.n_t = NT;
-    ha.precise = true;
+    ha.precise = !kTc;  // fp32 check mode: expf-based SiLU; bf16 mode: one MUFU.TANH
     ha.rec_user = B.rec_user.as<long long>();
     ha.rec_scen = B.rec_scen.as<int>();
     ha.rec_exp = B.rec_exp.as<int>();
