@@ -195,6 +195,12 @@ MTFM_API int64_t mtfm_cuda_profile_count(const mtfm_cuda_model* m);
 MTFM_API const char* mtfm_cuda_profile_entry(const mtfm_cuda_model* m, int64_t i, double* ms, double* flops,
                                              double* bytes);
 
+/* Test hook: one plain tensor-core GEMM on device buffers, out = epi(A[M][K] .
+ * Bt[N][K]^T + bias) with epi 0 = silu -> bf16, 1 = f32, 2 = f32 += (residual
+ * in out), 3 = bf16. A, Bt bf16 row-major; enqueued on `stream`. */
+MTFM_API mtfm_status mtfm_cuda_debug_gemm(const void* A, const void* Bt, const float* bias, void* out, int64_t M,
+                                          int64_t N, int64_t K, int32_t epi, void* stream);
+
 /* Debug / test hooks over device buffers of the last run (row-major). which:
  * "x" final activations [rows][d] f32, "plan" int32 [rows][4] = (source,
  * item, prefix, self), "scale" f32 [rows]. Returns elements copied. */

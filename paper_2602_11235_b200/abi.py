@@ -114,6 +114,8 @@ SIGNATURES = [
     ("mtfm_cuda_profile_count", C.c_int64, [C.c_void_p]),
     ("mtfm_cuda_profile_entry", C.c_char_p, [C.c_void_p, C.c_int64, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                              C.POINTER(C.c_double)]),
+    ("mtfm_cuda_debug_gemm", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
+                                       C.c_int64, C.c_int32, C.c_void_p]),
     ("mtfm_cuda_debug_fetch", C.c_int64, [C.c_void_p, C.c_void_p, C.c_char_p, C.c_void_p, C.c_int64]),
 ]
 

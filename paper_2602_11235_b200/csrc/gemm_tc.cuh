@@ -17,9 +17,10 @@
 // global tile list, tile t -> (problem, m-block, n-block), n fastest, so the
 // CTAs resident at one time share A tiles through L2.
 //
-// Roles (512 threads): warp 0 TMA, warp 1 MMA issuer (one elected lane),
-// warp 2 TMEM allocator, warps 4..11 epilogue (two per TMEM lane quarter,
-// each owning half the columns), warps 12..15 A-transform producers.
+// Roles (512 threads): warp 15 MMA issuer (one elected lane), warp 14 TMA,
+// warp 13 TMEM allocator, warps 0..7 (0..11) epilogue (warp & 3 = TMEM lane
+// quarter), warps 8..11 A-transform producers. The single-thread roles sit at
+// the highest warp ids because the issue arbiter favours higher ids.
 // Pipelines: kStages SMEM stages (full/empty mbarriers) and 2 TMEM
 // accumulator stages (tmem_full/empty), so the epilogue of tile i overlaps
 // the MMAs of tile i+1. The epilogue stages each 32 x 32 block through
@@ -72,11 +73,25 @@ struct GemmProblem {
     long long ldu;
 };
 
+// B-resident schedule: CTA b owns (problem pi, n-block nb) for the whole launch,
+// keeps that weight slice in SMEM and walks m-blocks m0, m0 + mstep, ...
+struct CtaWork {
+    short pi, nb;
+    int m0, mstep, mcount;
+};
+
 struct GemmArgs {
     int n_problems;
     int n_tiles;
     int a_mode;
+    int b_res;        // 1: B-resident schedule (cta[]), 0: streaming over the global tile list
+    int n_stages;     // SMEM pipeline stages
+    int stage_bytes;  // A_BYTES (+ B_BYTES when streaming B)
+    int bres_bytes;   // resident B slice bytes (b_res)
+    int n_epi;        // epilogue warps: 8, or 12 when A comes from TMA (warps 12..15 free)
+    int debug;        // bit 0: skip output stores, bit 1: skip SiLU (timing experiments only)
     GemmProblem p[kMaxProblems];
+    CtaWork cta[kNumSMs];
 };
 
 namespace gemm_detail {
@@ -84,15 +99,39 @@ namespace gemm_detail {
 template <int BN>
 struct Cfg {
     static constexpr int BM = 128, BK = 64;
-    static constexpr int kStages = BN >= 256 ? 3 : (BN >= 128 ? 5 : 6);
+    static constexpr int kStages = BN >= 256 ? 3 : (BN >= 128 ? 5 : 6);  // streaming schedule
     static constexpr int A_BYTES = BM * BK * 2;
     static constexpr int B_BYTES = BN * BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
-    static constexpr int STG_BYTES = 8 * 2 * 32 * 32 * 4;  // per epilogue warp: 2 x (32 rows x 32 fp32)
-    static constexpr int SMEM = kStages * STAGE_BYTES + STG_BYTES + 1024 /*align*/ + 384 /*barriers*/;
+    static constexpr int STG_WARP = 2 * 32 * 32 * 4;  // per epilogue warp: 2 x (32 rows x 32 fp32)
+    static constexpr int BAR_BYTES = 512;
+    static constexpr int SMEM = kStages * STAGE_BYTES + 8 * STG_WARP + 1024 /*align*/ + BAR_BYTES;
+    static constexpr int kMaxSmem = 227 * 1024;
     static constexpr int kThreads = 512;
-    static_assert(SMEM <= 227 * 1024, "SMEM budget");
+    static_assert(SMEM <= kMaxSmem, "SMEM budget");
+};
+
+// The tile sequence of this CTA (identical for every role).
+struct TileSeq {
+    int t, i;
+    __device__ TileSeq() : t(blockIdx.x), i(0) {}
+    template <typename Decode>
+    __device__ bool next(const GemmArgs& a, Decode decode, int& pi, int& mb, int& nb) {
+        if (a.b_res) {
+            const CtaWork& w = a.cta[blockIdx.x];
+            if (i >= w.mcount) return false;
+            pi = w.pi;
+            nb = w.nb;
+            mb = w.m0 + i * w.mstep;
+            ++i;
+            return true;
+        }
+        if (t >= a.n_tiles) return false;
+        decode(a, t, pi, mb, nb);
+        t += gridDim.x;
+        return true;
+    }
 };
 
 __device__ __forceinline__ void decode_tile(const GemmArgs& a, int t, int& pi, int& mb, int& nb) {
@@ -188,124 +227,152 @@ template <int BN>
 __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__ GemmArgs args) {
     using C = gemm_detail::Cfg<BN>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    float* stg_all = reinterpret_cast<float*>(smem + C::kStages * C::STAGE_BYTES);
-    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::kStages * C::STAGE_BYTES + C::STG_BYTES);
-    uint64_t* empty_bar = full_bar + C::kStages;
-    uint64_t* tfull_bar = empty_bar + C::kStages;
+    uint8_t* smem0 = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* bres = smem0;                               // resident B slice (b_res)
+    uint8_t* smem = smem0 + args.bres_bytes;             // pipeline stages
+    const int n_stages = args.n_stages;
+    const int stage_bytes = args.stage_bytes;
+    float* stg_all = reinterpret_cast<float*>(smem + n_stages * stage_bytes);
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + n_stages * stage_bytes + args.n_epi * C::STG_WARP);
+    uint64_t* empty_bar = full_bar + 8;
+    uint64_t* tfull_bar = empty_bar + 8;
     uint64_t* tempty_bar = tfull_bar + 2;
-    uint64_t* res_bar = tempty_bar + 2;  // [8 epilogue warps][2 staging buffers]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(res_bar + 16);
+    uint64_t* res_bar = tempty_bar + 2;  // [12 epilogue warps][2 staging buffers]
+    uint64_t* bres_bar = res_bar + 24;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres_bar + 1);
 
     const uint32_t warp = ptx::warp_id();
     const uint32_t lane = ptx::lane_id();
     const int a_mode = args.a_mode;
+    // Warp roles. The issue arbiter favours higher warp ids, so the latency-
+    // critical single-thread roles sit at the top: 15 MMA issuer, 14 TMA
+    // producer, 13 TMEM allocator; epilogue warps 0..n_epi-1 (warp & 3 = TMEM
+    // lane quarter); 8..11 A-transform producers when A is not TMA-loaded.
+    constexpr uint32_t kWarpMma = 15, kWarpTma = 14, kWarpAlloc = 13;
 
-    if (warp == 0 && lane == 0) {
-        for (int s = 0; s < C::kStages; ++s) {
+    if (warp == kWarpTma && lane == 0) {
+        for (int s = 0; s < n_stages; ++s) {
             ptx::mbar_init(&full_bar[s], a_mode == A_TMA ? 1 : 1 + 4);
             ptx::mbar_init(&empty_bar[s], 1);
         }
+        ptx::mbar_init(bres_bar, 1);
         for (int s = 0; s < 2; ++s) {
             ptx::mbar_init(&tfull_bar[s], 1);
-            ptx::mbar_init(&tempty_bar[s], 8);  // one arrive per epilogue warp
+            ptx::mbar_init(&tempty_bar[s], args.n_epi);  // one arrive per epilogue warp
         }
-        for (int s = 0; s < 16; ++s) ptx::mbar_init(&res_bar[s], 1);
+        for (int s = 0; s < 24; ++s) ptx::mbar_init(&res_bar[s], 1);
         ptx::fence_mbar_init();
         for (int i = 0; i < args.n_problems; ++i) {
             if (a_mode == A_TMA) ptx::tma_prefetch(&args.p[i].tma_a);
             ptx::tma_prefetch(&args.p[i].tma_b);
         }
     }
-    if (warp == 2) ptx::tmem_alloc<C::TMEM_COLS>(tmem_slot);
+    if (warp == kWarpAlloc) ptx::tmem_alloc<C::TMEM_COLS>(tmem_slot);
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    if (warp == 0) {
+    if (warp == kWarpTma) {
         // ------------------------------------------------ TMA producer (B, and A in A_TMA mode)
         if (ptx::elect_one()) {
+            if (args.b_res && args.cta[blockIdx.x].mcount > 0) {
+                // resident weight slice: every k-block of this CTA's (problem, n-block), once
+                const CtaWork& w = args.cta[blockIdx.x];
+                const GemmProblem& p = args.p[w.pi];
+                const int kblocks = p.K / C::BK;
+                ptx::mbar_arrive_expect_tx(bres_bar, kblocks * C::B_BYTES);
+                for (int kb = 0; kb < kblocks; ++kb)
+                    ptx::tma_load_2d(bres + kb * C::B_BYTES, &p.tma_b, bres_bar, kb * C::BK, w.nb * BN);
+            }
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = blockIdx.x; t < args.n_tiles; t += gridDim.x) {
-                int pi, mb, nb;
-                gemm_detail::decode_tile(args, t, pi, mb, nb);
+            gemm_detail::TileSeq seq;
+            int pi, mb, nb;
+            while (seq.next(args, gemm_detail::decode_tile, pi, mb, nb)) {
                 const GemmProblem& p = args.p[pi];
                 const int kblocks = p.K / C::BK;
                 for (int kb = 0; kb < kblocks; ++kb) {
                     ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
-                    uint8_t* sa = smem + stage * C::STAGE_BYTES;
+                    uint8_t* sa = smem + stage * stage_bytes;
                     uint8_t* sb = sa + C::A_BYTES;
-                    if (a_mode == A_TMA) {
-                        ptx::mbar_arrive_expect_tx(&full_bar[stage], C::STAGE_BYTES);
-                        ptx::tma_load_2d(sa, &p.tma_a, &full_bar[stage], kb * C::BK, mb * C::BM);
-                    } else {
-                        ptx::mbar_arrive_expect_tx(&full_bar[stage], C::B_BYTES);
-                    }
-                    ptx::tma_load_2d(sb, &p.tma_b, &full_bar[stage], kb * C::BK, nb * BN);
-                    if (++stage == C::kStages) {
+                    const int bytes = (a_mode == A_TMA ? C::A_BYTES : 0) + (args.b_res ? 0 : C::B_BYTES);
+                    if (bytes > 0)
+                        ptx::mbar_arrive_expect_tx(&full_bar[stage], bytes);
+                    else
+                        ptx::mbar_arrive(&full_bar[stage]);
+                    if (a_mode == A_TMA) ptx::tma_load_2d(sa, &p.tma_a, &full_bar[stage], kb * C::BK, mb * C::BM);
+                    if (!args.b_res) ptx::tma_load_2d(sb, &p.tma_b, &full_bar[stage], kb * C::BK, nb * BN);
+                    if (++stage == n_stages) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
             }
         }
-    } else if (warp >= 12) {
+    } else if (warp >= 8 && warp < 12 && a_mode != A_TMA) {
         // ------------------------------------------------ A-transform producers
-        if (a_mode != A_TMA) {
-            const int pt = (warp - 12) * 32 + lane;
+        {
+            const int pt = (warp - 8) * 32 + lane;
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = blockIdx.x; t < args.n_tiles; t += gridDim.x) {
-                int pi, mb, nb;
-                gemm_detail::decode_tile(args, t, pi, mb, nb);
+            gemm_detail::TileSeq seq;
+            int pi, mb, nb;
+            while (seq.next(args, gemm_detail::decode_tile, pi, mb, nb)) {
                 const GemmProblem& p = args.p[pi];
                 const int kblocks = p.K / C::BK;
                 for (int kb = 0; kb < kblocks; ++kb) {
                     ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
-                    gemm_detail::produce_a(p, a_mode, mb * C::BM, kb * C::BK, smem + stage * C::STAGE_BYTES, pt);
+                    gemm_detail::produce_a(p, a_mode, mb * C::BM, kb * C::BK, smem + stage * stage_bytes, pt);
                     ptx::fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(&full_bar[stage]);
-                    if (++stage == C::kStages) {
+                    if (++stage == n_stages) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
             }
         }
-    } else if (warp == 1) {
+    } else if (warp == kWarpMma) {
         // ------------------------------------------------ MMA issuer
         const uint32_t idesc = ptx::instr_desc_bf16(128, BN, false, false);
         int stage = 0;
         uint32_t phase = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int t = blockIdx.x; t < args.n_tiles; t += gridDim.x) {
-            int pi, mb, nb;
-            gemm_detail::decode_tile(args, t, pi, mb, nb);
+        bool bres_ready = false;
+        gemm_detail::TileSeq seq;
+        int pi, mb, nb;
+        while (seq.next(args, gemm_detail::decode_tile, pi, mb, nb)) {
             const int kblocks = args.p[pi].K / C::BK;
-            ptx::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+            if (args.b_res && !bres_ready) {
+                ptx::mbar_wait(bres_bar, 0);
+                bres_ready = true;
+            }
+            // the epilogue hands every accumulator back (bias-initialised when the
+            // tile has a bias, see below), including before its first use
+            ptx::mbar_wait(&tempty_bar[acc], acc_phase);
             ptx::tc_fence_after();
             const uint32_t d_tmem = tmem_base + acc * BN;
+            const uint32_t acc0 = args.p[pi].bias ? 1u : 0u;
             for (int kb = 0; kb < kblocks; ++kb) {
                 ptx::mbar_wait(&full_bar[stage], phase);
                 ptx::tc_fence_after();
                 if (ptx::elect_one()) {
-                    const uint32_t sa = ptx::smem_u32(smem + stage * C::STAGE_BYTES);
-                    const uint32_t sb = sa + C::A_BYTES;
+                    const uint32_t sa = ptx::smem_u32(smem + stage * stage_bytes);
+                    const uint32_t sb = args.b_res ? ptx::smem_u32(bres + kb * C::B_BYTES) : sa + C::A_BYTES;
 #pragma unroll
                     for (int k = 0; k < C::BK / 16; ++k) {
                         const uint64_t da = ptx::smem_desc(sa + k * 32, 16, 1024, 2);
                         const uint64_t db = ptx::smem_desc(sb + k * 32, 16, 1024, 2);
-                        ptx::umma_bf16(d_tmem, da, db, idesc, (kb | k) != 0);
+                        ptx::umma_bf16(d_tmem, da, db, idesc, ((kb | k) != 0) ? 1u : acc0);
                     }
                     ptx::umma_commit(&empty_bar[stage]);
                     if (kb == kblocks - 1) ptx::umma_commit(&tfull_bar[acc]);
                 }
                 __syncwarp();
-                if (++stage == C::kStages) {
+                if (++stage == n_stages) {
                     stage = 0;
                     phase ^= 1;
                 }
@@ -315,22 +382,67 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                 acc_phase ^= 1;
             }
         }
-    } else if (warp >= 4) {
+    } else if (warp < static_cast<uint32_t>(args.n_epi)) {
         // ------------------------------------------------ epilogue
-        // TMEM -> registers (bias, SiLU) -> swizzled SMEM staging (double
-        // buffered per warp) -> TMA bulk-tensor store, or for row-mapped /
-        // residual outputs coalesced 16-byte row-segment stores.
-        const uint32_t q = warp & 3;            // TMEM lane quarter
-        const uint32_t half = (warp - 4) >> 2;  // column half
-        float* stg_base = stg_all + (warp - 4) * 2 * 32 * 32;
-        const int sub = lane >> 3;              // row within a 4-row group
-        const int ch = lane & 7;                // 16-byte chunk within a 32-column row slice
+        // TMEM -> registers (SiLU) -> swizzled SMEM staging (double buffered
+        // per warp) -> TMA bulk-tensor store, or for row-mapped outputs
+        // coalesced 16-byte row-segment stores. The bias never touches the
+        // epilogue's math: each accumulator buffer is re-initialised with the
+        // bias of the tile that will use it next before it is handed back to
+        // the MMA warp, which then accumulates on top of it.
+        const uint32_t q = warp & 3;                    // TMEM lane quarter
+        const int group = warp >> 2;                    // column-chunk group of this quarter
+        const int n_groups = args.n_epi >> 2;
+        float* stg_base = stg_all + warp * 2 * 32 * 32;
+        const int sub = lane >> 3;                      // row within a 4-row group
+        const int ch = lane & 7;                        // 16-byte chunk within a 32-column row slice
+        const uint32_t lane_base = tmem_base + ((q * 32u) << 16);
+        constexpr int kChunks = BN / 32;                // 32-column chunks per tile row quarter
         int acc = 0;
         uint32_t acc_phase = 0;
-        uint32_t nstore = 0;                    // staging buffers used by this warp
-        uint32_t res_phase = 0;                 // parity bit per staging buffer
-        uint64_t* my_res = res_bar + (warp - 4) * 2;
-        constexpr int kChunks = BN / 2 / 32 > 0 ? BN / 2 / 32 : 1;
+        uint32_t nstore = 0;                            // staging buffers used by this warp
+        uint32_t res_phase = 0;                         // parity bit per staging buffer
+        uint64_t* my_res = res_bar + warp * 2;
+        // bias of (problem, n-block) into accumulator buffer b, my chunks only
+        // column unit per warp: 64 for bf16 bulk-stored outputs (128-byte rows), else 32
+        auto unit_of = [&](const GemmProblem& pp) {
+            return ((pp.epi == EPI_SILU_BF16 || pp.epi == EPI_BIAS_BF16) && pp.use_tma_c && BN >= 64) ? 64 : 32;
+        };
+        auto init_bias = [&](const GemmProblem& pp, int nbk, int b) {
+            const float* bias = pp.bias;
+            if (!bias) return;
+            const int N = pp.N;
+            const int unit = unit_of(pp);
+            for (int ui = group; ui < BN / unit; ui += n_groups) {
+#pragma unroll 1
+                for (int cc = 0; cc < unit; cc += 16) {
+                    const int c = ui * unit + cc;
+                    const int n0 = nbk * BN + c;
+                    uint32_t r[16];
+                    if (n0 + 16 <= N) {
+                        // lane-uniform address: one broadcast float4 load per 4 columns
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + n0) + k);
+                            r[4 * k] = __float_as_uint(b4.x);
+                            r[4 * k + 1] = __float_as_uint(b4.y);
+                            r[4 * k + 2] = __float_as_uint(b4.z);
+                            r[4 * k + 3] = __float_as_uint(b4.w);
+                        }
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(n0 + i < N ? __ldg(bias + n0 + i) : 0.f);
+                    }
+                    ptx::tmem_st16(lane_base + b * BN + c, r);
+                }
+            }
+        };
+        auto release = [&](int b) {
+            ptx::tmem_st_wait();
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tempty_bar[b]);
+        };
         // residual prefetch of one 32 x 32 fp32 block into staging buffer b
         auto res_load = [&](const GemmProblem& pp, int b, int col, int row) {
             if (lane == 0) {
@@ -339,58 +451,72 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                 ptx::tma_load_2d(stg_base + b * 32 * 32, &pp.tma_c, &my_res[b], col, row);
             }
         };
-        for (int t = blockIdx.x; t < args.n_tiles; t += gridDim.x) {
-            int pi, mb, nb;
-            gemm_detail::decode_tile(args, t, pi, mb, nb);
+        gemm_detail::TileSeq seq;
+        {
+            // prepare both accumulator buffers for the first two tiles
+            gemm_detail::TileSeq la = seq;
+            int lpi, lmb, lnb;
+            for (int b = 0; b < 2; ++b) {
+                if (la.next(args, gemm_detail::decode_tile, lpi, lmb, lnb)) init_bias(args.p[lpi], lnb, b);
+                release(b);
+            }
+        }
+        int pi, mb, nb;
+        while (seq.next(args, gemm_detail::decode_tile, pi, mb, nb)) {
             const GemmProblem& p = args.p[pi];
             const int row0 = mb * C::BM + q * 32;
-            const int n_begin = half * (BN / 2);
-            if (p.use_tma_r && nb * BN + n_begin < p.N) res_load(p, nstore & 1, nb * BN + n_begin, row0);
+            const bool bf16_out = p.epi == EPI_SILU_BF16 || p.epi == EPI_BIAS_BF16;
+            const int unit = unit_of(p);
+            const int step = n_groups * unit / 32;  // in 32-column chunks
+            int ci = group * unit / 32;
+            if (p.use_tma_r && ci < kChunks && nb * BN + ci * 32 < p.N) res_load(p, nstore & 1, nb * BN + ci * 32, row0);
             ptx::mbar_wait(&tfull_bar[acc], acc_phase);
             ptx::tc_fence_after();
-            const bool bf16_out = p.epi == EPI_SILU_BF16 || p.epi == EPI_BIAS_BF16;
 #pragma unroll 1
-            for (int ci = 0; ci < kChunks; ++ci) {
-                const int c = n_begin + ci * 32;
+            for (; ci < kChunks; ci += step) {
+                const int c = ci * 32;
                 const int n0 = nb * BN + c;
-                const bool live = n0 < p.N && c < BN;  // warp-uniform
-                float v[32];
-                if (c < BN) {
-                    ptx::tmem_ld16(tmem_base + ((q * 32u) << 16) + acc * BN + c, *reinterpret_cast<float(*)[16]>(v));
-                    ptx::tmem_ld16(tmem_base + ((q * 32u) << 16) + acc * BN + c + 16,
-                                   *reinterpret_cast<float(*)[16]>(v + 16));
+                if (bf16_out && p.use_tma_c && unit == 64) {
+                    // ---- fast path: 64 columns -> bf16 (SiLU) -> one 32 x 128 B SW128 box
+                    if (n0 >= p.N) continue;  // warp-uniform (TMEM reads below are all-or-nothing)
+                    float v[64];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        ptx::tmem_ld16(lane_base + acc * BN + c + 16 * k, *reinterpret_cast<float(*)[16]>(v + 16 * k));
                     ptx::tmem_ld_wait();
-                }
-                if (ci == kChunks - 1) {
-                    // accumulator fully read: hand it back to the MMA warp early
-                    ptx::tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(&tempty_bar[acc]);
-                }
-                if (!live) continue;
-                if (p.bias) {
-                    const float* bp = p.bias + n0;
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        float4 b4;
-                        if (n0 + 4 * k + 3 < p.N) {
-                            b4 = __ldg(reinterpret_cast<const float4*>(bp) + k);
-                        } else {
-                            b4.x = n0 + 4 * k < p.N ? __ldg(bp + 4 * k) : 0.f;
-                            b4.y = n0 + 4 * k + 1 < p.N ? __ldg(bp + 4 * k + 1) : 0.f;
-                            b4.z = n0 + 4 * k + 2 < p.N ? __ldg(bp + 4 * k + 2) : 0.f;
-                            b4.w = 0.f;
-                        }
-                        v[4 * k] += b4.x;
-                        v[4 * k + 1] += b4.y;
-                        v[4 * k + 2] += b4.z;
-                        v[4 * k + 3] += b4.w;
+                    if (args.debug & 4) {  // timing experiment: TMEM read only
+                        if (v[0] == 12345.f) ++nstore;
+                        continue;
                     }
-                }
-                if (p.epi == EPI_SILU_BF16) {
+                    uint32_t w[32];
+                    if (p.epi == EPI_SILU_BF16 && !(args.debug & 2)) {
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) v[i] = ptx::silu_fast(v[i]);
+                        for (int e = 0; e < 64; e += 2) w[e / 2] = ptx::silu2_bf16(v[e], v[e + 1]);
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 64; e += 2) w[e / 2] = pack_bf16(v[e], v[e + 1]);
+                    }
+                    uint8_t* sb = reinterpret_cast<uint8_t*>(stg_base + (nstore & 1) * 32 * 32) + lane * 128;
+                    if (lane == 0) ptx::bulk_wait_read<1>();
+                    __syncwarp();
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        *reinterpret_cast<uint4*>(sb + ((k ^ (lane & 7)) << 4)) =
+                            make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+                    ptx::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0 && !(args.debug & 1)) {
+                        ptx::tma_store_2d(&p.tma_c, stg_base + (nstore & 1) * 32 * 32, n0, row0);
+                        ptx::bulk_commit();
+                    }
+                    ++nstore;
+                    continue;
                 }
+                float v[32];
+                ptx::tmem_ld16(lane_base + acc * BN + c, *reinterpret_cast<float(*)[16]>(v));
+                ptx::tmem_ld16(lane_base + acc * BN + c + 16, *reinterpret_cast<float(*)[16]>(v + 16));
+                ptx::tmem_ld_wait();
+                if (n0 >= p.N) continue;  // warp-uniform
                 float* stg = stg_base + (nstore & 1) * 32 * 32;
                 if (p.use_tma_r) {
                     const int b = nstore & 1;
@@ -411,21 +537,39 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                     }
                     ++nstore;
                     // prefetch the next chunk's residual into the other buffer
-                    if (ci + 1 < kChunks && n0 + 32 < p.N && c + 32 < BN) res_load(p, nstore & 1, n0 + 32, row0);
+                    const int cn = ci + step;
+                    if (cn < kChunks && nb * BN + cn * 32 < p.N) res_load(p, nstore & 1, nb * BN + cn * 32, row0);
                     continue;
                 }
                 if (p.use_tma_c) {
-                    // the staging buffer written two stores ago must have been read by the TMA engine
                     if (lane == 0) ptx::bulk_wait_read<1>();
                     __syncwarp();
                     if (bf16_out) {
-                        // 32 rows x 64 B, SWIZZLE_64B: 16 B chunk k of row r at (k ^ ((r >> 1) & 3))
+                        // 64-column unit: this chunk and the next (loaded below) -> one
+                        // 32 rows x 128 B SW128 box (chunk k of row r at (k ^ (r & 7)))
                         uint8_t* sb = reinterpret_cast<uint8_t*>(stg);
 #pragma unroll
-                        for (int k = 0; k < 4; ++k)
-                            *reinterpret_cast<uint4*>(sb + lane * 64 + ((k ^ ((lane >> 1) & 3)) << 4)) =
-                                make_uint4(pack_bf16(v[8 * k], v[8 * k + 1]), pack_bf16(v[8 * k + 2], v[8 * k + 3]),
-                                           pack_bf16(v[8 * k + 4], v[8 * k + 5]), pack_bf16(v[8 * k + 6], v[8 * k + 7]));
+                        for (int hh = 0; hh < 2; ++hh) {
+                            if (hh == 1) {
+                                ptx::tmem_ld16(lane_base + acc * BN + c + 32, *reinterpret_cast<float(*)[16]>(v));
+                                ptx::tmem_ld16(lane_base + acc * BN + c + 48, *reinterpret_cast<float(*)[16]>(v + 16));
+                                ptx::tmem_ld_wait();
+                            }
+                            uint32_t w[16];
+                            if (p.epi == EPI_SILU_BF16 && !(args.debug & 2)) {
+#pragma unroll
+                                for (int e = 0; e < 32; e += 2) w[e / 2] = ptx::silu2_bf16(v[e], v[e + 1]);
+                            } else {
+#pragma unroll
+                                for (int e = 0; e < 32; e += 2) w[e / 2] = pack_bf16(v[e], v[e + 1]);
+                            }
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                const int kk = hh * 4 + k;
+                                *reinterpret_cast<uint4*>(sb + lane * 128 + ((kk ^ (lane & 7)) << 4)) =
+                                    make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+                            }
+                        }
                     } else {
                         // 32 rows x 128 B, SWIZZLE_128B: chunk k of row r at (k ^ (r & 7))
 #pragma unroll
@@ -435,14 +579,18 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                     }
                     ptx::fence_proxy_async_smem();
                     __syncwarp();
-                    if (lane == 0) {
+                    if (lane == 0 && !(args.debug & 1)) {
                         ptx::tma_store_2d(&p.tma_c, stg, n0, row0);
                         ptx::bulk_commit();
                     }
                     ++nstore;
                     continue;
                 }
-                // ---- manual path (row-mapped scatter / residual)
+                // ---- manual path (row-mapped scatter / residual without TMA)
+                if (p.epi == EPI_SILU_BF16) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v[i] = ptx::silu_fast(v[i]);
+                }
                 if (lane == 0) ptx::bulk_wait_read<1>();
                 __syncwarp();
 #pragma unroll
@@ -513,6 +661,15 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                 __syncwarp();
                 ++nstore;
             }
+            // hand the buffer back, initialised for the tile that uses it next
+            {
+                gemm_detail::TileSeq la = seq;
+                int lpi, lmb, lnb;
+                if (la.next(args, gemm_detail::decode_tile, lpi, lmb, lnb) &&
+                    la.next(args, gemm_detail::decode_tile, lpi, lmb, lnb))
+                    init_bias(args.p[lpi], lnb, acc);
+                release(acc);
+            }
             if (++acc == 2) {
                 acc = 0;
                 acc_phase ^= 1;
@@ -523,7 +680,7 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
     }
     ptx::tc_fence_before();
     __syncthreads();
-    if (warp == 2) {
+    if (warp == kWarpAlloc) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc<C::TMEM_COLS>(tmem_base);
     }

@@ -447,16 +447,17 @@ void finalize(mtfm_cuda_model& m) {
 
 // ---------------------------------------------------------------- GEMM launch helpers
 template <int BN>
-void launch_gemm_tc_bn(GemmArgs& a, cudaStream_t st) {
+void launch_gemm_tc_bn(GemmArgs& a, int grid, cudaStream_t st) {
     using C = gemm_detail::Cfg<BN>;
     static bool attr = false;
     if (!attr) {
-        ck(cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM),
+        ck(cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kMaxSmem),
            "gemm smem attr");
         attr = true;
     }
-    const int grid = std::min(a.n_tiles, kNumSMs);
-    gemm_tc_kernel<BN><<<grid, C::kThreads, C::SMEM, st>>>(a);
+    const int smem = 1024 + a.bres_bytes + a.n_stages * a.stage_bytes + a.n_epi * C::STG_WARP + C::BAR_BYTES;
+    if (smem > C::kMaxSmem) fail(MTFM_CONTRACT_ERROR, "gemm smem plan exceeds 227 KB");
+    gemm_tc_kernel<BN><<<grid, C::kThreads, smem, st>>>(a);
     ck(cudaGetLastError(), "gemm_tc launch");
 }
 
@@ -504,17 +505,88 @@ int pick_bn(const std::vector<TcProblem>& ps) {
     return best;
 }
 
+// B-resident plan (weights slice kept in SMEM, A streamed once per CTA group)
+// when every problem's slice fits; otherwise the streaming schedule.
+constexpr int kBresMax = 96 * 1024;
+
+int pick_bn_resident(const std::vector<TcProblem>& ps) {
+    int best = 0;
+    double best_eff = -1;
+    for (int bn : {256, 128, 64}) {
+        bool fits = true;
+        double used = 0, padded = 0;
+        for (const auto& p : ps) {
+            fits = fits && round_up(p.K, 64) * bn * 2 <= kBresMax;
+            used += p.N;
+            padded += static_cast<double>(cdiv(p.N, bn) * bn);
+        }
+        if (!fits) continue;
+        const double eff = used / std::max(padded, 1.0);
+        if (eff > best_eff + 0.02) {
+            best_eff = eff;
+            best = bn;
+        }
+    }
+    return best;
+}
+
 void run_gemm_tc(std::vector<TcProblem> ps, cudaStream_t st, long long& launches) {
     ps.erase(std::remove_if(ps.begin(), ps.end(), [](const TcProblem& p) { return p.M == 0 || p.N == 0; }),
              ps.end());
     if (ps.empty()) return;
-    const int bn = pick_bn(ps);
+    static const bool stream_only = std::getenv("MTFM_GEMM_STREAM") != nullptr;
+    static const int force_bn = std::getenv("MTFM_GEMM_BN") ? std::atoi(std::getenv("MTFM_GEMM_BN")) : 0;
+    static const int force_stages = std::getenv("MTFM_GEMM_STAGES") ? std::atoi(std::getenv("MTFM_GEMM_STAGES")) : 0;
+    static const int force_epi = std::getenv("MTFM_GEMM_EPI") ? std::atoi(std::getenv("MTFM_GEMM_EPI")) : 0;
+    int bn_res = stream_only ? 0 : pick_bn_resident(ps);
+    if (bn_res && force_bn) bn_res = force_bn;
     for (size_t i0 = 0; i0 < ps.size(); i0 += kMaxProblems) {
+        const size_t i1 = std::min(ps.size(), i0 + kMaxProblems);
         GemmArgs a;
         std::memset(&a, 0, sizeof(a));
         a.a_mode = ps[i0].amode;
+        // ---- schedule
+        int bn = bn_res;
+        int grid = 0;
+        if (bn) {
+            // CTAs per problem proportional to its work, a multiple of its n-slices so
+            // the CTAs sharing an m-block (one per slice) run in lockstep (A read once)
+            double W = 0;
+            for (size_t i = i0; i < i1; ++i) W += static_cast<double>(cdiv(ps[i].M, 128) * cdiv(ps[i].N, bn));
+            int n = 0;
+            bool ok = true;
+            for (size_t i = i0; i < i1 && ok; ++i) {
+                const int ns = static_cast<int>(cdiv(ps[i].N, bn));
+                const int mb = static_cast<int>(cdiv(ps[i].M, 128));
+                const double share = kNumSMs * static_cast<double>(mb) * ns / W;
+                int cps = std::max(1, static_cast<int>(share / ns));
+                cps = std::min(cps, mb);
+                for (int j = 0; j < cps && ok; ++j)
+                    for (int nb = 0; nb < ns; ++nb) {
+                        if (n >= kNumSMs) {
+                            ok = false;
+                            break;
+                        }
+                        CtaWork& w = a.cta[n++];
+                        w.pi = static_cast<short>(i - i0);
+                        w.nb = static_cast<short>(nb);
+                        w.m0 = j;
+                        w.mstep = cps;
+                        w.mcount = static_cast<int>(cdiv(mb - j, cps));
+                    }
+            }
+            if (ok) {
+                grid = n;
+                a.b_res = 1;
+            } else {
+                std::memset(a.cta, 0, sizeof(a.cta));
+                bn = 0;
+            }
+        }
+        if (!bn) bn = force_bn ? force_bn : pick_bn(std::vector<TcProblem>(ps.begin() + i0, ps.begin() + i1));
         int tiles = 0;
-        for (size_t i = i0; i < std::min(ps.size(), i0 + kMaxProblems); ++i) {
+        int kmax = 0;
+        for (size_t i = i0; i < i1; ++i) {
             const auto& s = ps[i];
             if (s.amode != a.a_mode) fail(MTFM_CONTRACT_ERROR, "mixed A modes in one grouped GEMM");
             GemmProblem& p = a.p[a.n_problems++];
@@ -523,6 +595,7 @@ void run_gemm_tc(std::vector<TcProblem> ps, cudaStream_t st, long long& launches
             p.M = s.M;
             p.N = s.N;
             p.K = static_cast<int>(round_up(s.K, 64));
+            kmax = std::max(kmax, p.K);
             p.Kv = s.K;
             p.a_src = s.a_src;
             p.lda = s.lda;
@@ -551,15 +624,36 @@ void run_gemm_tc(std::vector<TcProblem> ps, cudaStream_t st, long long& launches
             p.use_tma_c = tma_ok && (s.epi != EPI_RESID_F32 || s.resid == s.out);
             p.use_tma_r = p.use_tma_c && s.epi == EPI_RESID_F32;
             if (p.use_tma_c) {
+                // 32 rows x 128 B boxes: 64 bf16 columns or 32 fp32 columns (SW128)
                 const char* base = static_cast<const char*>(s.out) + s.row_offset * s.ldo * eb;
-                p.tma_c = tma_2d(base, s.M, s.N, s.ldo, 32, 32, bf16_out ? 64 : 128, eb);
+                const bool wide = bf16_out && bn >= 64;
+                p.tma_c = tma_2d(base, s.M, s.N, s.ldo, wide ? 64 : 32, 32, wide ? 128 : (bf16_out ? 64 : 128), eb);
             }
             tiles += static_cast<int>(cdiv(s.M, 128)) * p.tiles_n;
         }
         a.n_tiles = tiles;
-        if (bn == 256) launch_gemm_tc_bn<256>(a, st);
-        else if (bn == 128) launch_gemm_tc_bn<128>(a, st);
-        else launch_gemm_tc_bn<64>(a, st);
+        static const int dbg = std::getenv("MTFM_GEMM_DEBUG") ? std::atoi(std::getenv("MTFM_GEMM_DEBUG")) : 0;
+        a.debug = dbg;
+        const int a_bytes = 128 * 64 * 2;
+        const int b_bytes = bn * 64 * 2;
+        const int stg_warp = 2 * 32 * 32 * 4;
+        if (!a.b_res) grid = std::min(tiles, kNumSMs);
+        a.bres_bytes = a.b_res ? (kmax / 64) * b_bytes : 0;
+        a.stage_bytes = a.b_res ? a_bytes : a_bytes + b_bytes;
+        // 12 epilogue warps when A is TMA-loaded and >= 3 stages still fit, else 8
+        for (int ne : {12, 8}) {
+            if (ne == 12 && a.a_mode != A_TMA) continue;
+            if (force_epi && ne != force_epi) continue;
+            const int avail = 227 * 1024 - 1024 - 512 - ne * stg_warp - a.bres_bytes;
+            a.n_epi = ne;
+            a.n_stages = std::min(8, avail / a.stage_bytes);
+            if (force_stages) a.n_stages = std::min(a.n_stages, force_stages);
+            if (a.n_stages >= 3) break;
+        }
+        if (a.n_stages < 2) fail(MTFM_CONTRACT_ERROR, "gemm pipeline does not fit in SMEM");
+        if (bn == 256) launch_gemm_tc_bn<256>(a, grid, st);
+        else if (bn == 128) launch_gemm_tc_bn<128>(a, grid, st);
+        else launch_gemm_tc_bn<64>(a, grid, st);
         ++launches;
     }
 }
@@ -1706,6 +1800,17 @@ mtfm_status mtfm_cuda_last_stats(const mtfm_cuda_model* m, mtfm_run_stats* out) 
     return guard([&] {
         if (!m || !out) fail(MTFM_CONTRACT_ERROR, "null argument");
         *out = m->stats;
+    });
+}
+
+mtfm_status mtfm_cuda_debug_gemm(const void* A, const void* Bt, const float* bias, void* out, int64_t M, int64_t N,
+                                 int64_t K, int32_t epi, void* stream) {
+    return guard([&] {
+        long long L = 0;
+        TcProblem tp{static_cast<const __nv_bfloat16*>(A), K, static_cast<const __nv_bfloat16*>(Bt), K,
+                     static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), epi, bias, out, N, nullptr, 0,
+                     epi == EPI_RESID_F32 ? static_cast<const float*>(out) : nullptr};
+        run_gemm_tc({tp}, static_cast<cudaStream_t>(stream), L);
     });
 }
 

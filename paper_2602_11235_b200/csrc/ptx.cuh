@@ -210,6 +210,24 @@ __device__ __forceinline__ float silu_fast(float x) {
     return fmaf(h, t, h);
 }
 
+// Two SiLUs -> packed bf16x2: h = s/2 (FMUL2), t = tanh(h) (MUFU), h + h*t (FFMA2).
+__device__ __forceinline__ uint32_t silu2_bf16(float s0, float s1) {
+    uint64_t sv, hv, tv, rv;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(sv) : "f"(s0), "f"(s1));
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(hv) : "l"(sv), "l"(0x3f0000003f000000ull));
+    float h0, h1, t0, t1;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(h0), "=f"(h1) : "l"(hv));
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t0) : "f"(h0));
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t1) : "f"(h1));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(tv) : "f"(t0), "f"(t1));
+    asm("fma.rn.f32x2 %0, %1, %2, %1;" : "=l"(rv) : "l"(hv), "l"(tv));
+    float r0, r1;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r0), "=f"(r1) : "l"(rv));
+    uint32_t out;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(out) : "f"(r1), "f"(r0));
+    return out;
+}
+
 __device__ __forceinline__ float silu_f32(float x) {
     // x * sigmoid(x), sigmoid split by sign like kernels.hpp:96-103
     const float e = __expf(-fabsf(x));
