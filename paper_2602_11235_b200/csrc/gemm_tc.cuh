@@ -54,7 +54,8 @@ struct GemmProblem {
     int tile_start;         // first global tile of this problem
     int tiles_n;
     int epi;
-    const float* bias;      // [N] (may be null)
+    int has_bias;           // bias added by one extra K=16 MMA: ones(128 x 16) x bias_t(BN x 16)^T
+    CUtensorMap tma_bias;   // bias_t bf16 [N][16] = (hi, lo, 0, ...), box {16, BN}, SW32
     void* out;
     long long ldo;          // elements
     const int* row_map;     // optional output row indirection (f32 epilogues)
@@ -89,7 +90,10 @@ struct GemmArgs {
     int stage_bytes;  // A_BYTES (+ B_BYTES when streaming B)
     int bres_bytes;   // resident B slice bytes (b_res)
     int n_epi;        // epilogue warps: 8, or 12 when A comes from TMA (warps 12..15 free)
-    int debug;        // bit 0: skip output stores, bit 1: skip SiLU (timing experiments only)
+    int stg_warp;     // epilogue staging bytes per warp: 8 KB (2 fp32 blocks), 4 KB when every problem is a bf16 bulk store
+    int bias_bytes;   // BN x 32 B bias tile: after the resident B slice (b_res) or at the end of every stage
+    unsigned long long* trace;  // timing experiments only: CTA 0 clock64 stamps (MTFM_GEMM_TRACE)
+    int debug;        // timing experiments only: 1 no stores, 2 no SiLU, 8 no A loads, 16 no MMAs, 32 epilogue handshakes only
     GemmProblem p[kMaxProblems];
     CtaWork cta[kNumSMs];
 };
@@ -103,9 +107,10 @@ struct Cfg {
     static constexpr int A_BYTES = BM * BK * 2;
     static constexpr int B_BYTES = BN * BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
+    static constexpr int kAcc = BN >= 256 ? 2 : 4;  // TMEM accumulator buffers
+    static constexpr int TMEM_COLS = kAcc * BN <= 32 ? 32 : (kAcc * BN <= 64 ? 64 : (kAcc * BN <= 128 ? 128 : (kAcc * BN <= 256 ? 256 : 512)));
     static constexpr int STG_WARP = 2 * 32 * 32 * 4;  // per epilogue warp: 2 x (32 rows x 32 fp32)
-    static constexpr int BAR_BYTES = 512;
+    static constexpr int BAR_BYTES = 1024;  // mbarriers, TMEM slot, per-problem tables
     static constexpr int SMEM = kStages * STAGE_BYTES + 8 * STG_WARP + 1024 /*align*/ + BAR_BYTES;
     static constexpr int kMaxSmem = 227 * 1024;
     static constexpr int kThreads = 512;
@@ -113,22 +118,41 @@ struct Cfg {
 };
 
 // The tile sequence of this CTA (identical for every role).
+// B-resident: the CTA's (problem, n-block, m-blocks) held in registers;
+// streaming: global tile t -> (problem, m, n) through the SMEM tile_start table.
 struct TileSeq {
     int t, i;
-    __device__ TileSeq() : t(blockIdx.x), i(0) {}
+    int b_res, pi0, nb0, m0, mstep, mcount, n_tiles, n_problems;
+    const int* tile_start;  // SMEM: first global tile of each problem
+    const int* tiles_n;     // SMEM: n-blocks of each problem
+    __device__ TileSeq(const GemmArgs& a, const int* ts, const int* tn)
+        : t(blockIdx.x), i(0), b_res(a.b_res), n_tiles(a.n_tiles), n_problems(a.n_problems), tile_start(ts),
+          tiles_n(tn) {
+        const CtaWork w = a.cta[blockIdx.x];
+        pi0 = w.pi;
+        nb0 = w.nb;
+        m0 = w.m0;
+        mstep = w.mstep;
+        mcount = w.mcount;
+    }
     template <typename Decode>
-    __device__ bool next(const GemmArgs& a, Decode decode, int& pi, int& mb, int& nb) {
-        if (a.b_res) {
-            const CtaWork& w = a.cta[blockIdx.x];
-            if (i >= w.mcount) return false;
-            pi = w.pi;
-            nb = w.nb;
-            mb = w.m0 + i * w.mstep;
+    __device__ __forceinline__ bool next(const GemmArgs&, Decode, int& pi, int& mb, int& nb) {
+        if (b_res) {
+            if (i >= mcount) return false;
+            pi = pi0;
+            nb = nb0;
+            mb = m0 + i * mstep;
             ++i;
             return true;
         }
-        if (t >= a.n_tiles) return false;
-        decode(a, t, pi, mb, nb);
+        if (t >= n_tiles) return false;
+        pi = 0;
+#pragma unroll 1
+        for (int k = 1; k < n_problems; ++k)
+            if (t >= tile_start[k]) pi = k;
+        const int local = t - tile_start[pi];
+        mb = local / tiles_n[pi];
+        nb = local - mb * tiles_n[pi];
         t += gridDim.x;
         return true;
     }
@@ -228,22 +252,49 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
     using C = gemm_detail::Cfg<BN>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem0 = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* bres = smem0;                               // resident B slice (b_res)
-    uint8_t* smem = smem0 + args.bres_bytes;             // pipeline stages
+    uint8_t* bres = smem0;                               // resident B slice (+ its bias tile) (b_res)
+    uint8_t* ones = smem0 + args.bres_bytes;             // 128 x 16 bf16 ones tile (SW32), A operand of the bias MMA
+    uint8_t* smem = ones + 4096;                         // pipeline stages
     const int n_stages = args.n_stages;
     const int stage_bytes = args.stage_bytes;
     float* stg_all = reinterpret_cast<float*>(smem + n_stages * stage_bytes);
-    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + n_stages * stage_bytes + args.n_epi * C::STG_WARP);
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + n_stages * stage_bytes + args.n_epi * args.stg_warp);
     uint64_t* empty_bar = full_bar + 8;
     uint64_t* tfull_bar = empty_bar + 8;
-    uint64_t* tempty_bar = tfull_bar + 2;
-    uint64_t* res_bar = tempty_bar + 2;  // [12 epilogue warps][2 staging buffers]
+    uint64_t* tempty_bar = tfull_bar + 4;
+    uint64_t* res_bar = tempty_bar + 4;  // [12 epilogue warps][2 staging buffers]
     uint64_t* bres_bar = res_bar + 24;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres_bar + 1);
+    int* s_tile_start = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(full_bar) + 512);
+    int* s_tiles_n = s_tile_start + kMaxProblems;
+    int* s_kblocks = s_tiles_n + kMaxProblems;
+    int* s_has_bias = s_kblocks + kMaxProblems;
+    if (threadIdx.x < static_cast<unsigned>(args.n_problems)) {
+        const GemmProblem& p = args.p[threadIdx.x];
+        s_tile_start[threadIdx.x] = p.tile_start;
+        s_tiles_n[threadIdx.x] = p.tiles_n;
+        s_kblocks[threadIdx.x] = p.K / C::BK;
+        s_has_bias[threadIdx.x] = p.has_bias;
+    }
+
+    // ones tile: every 16-byte chunk = (1, 1, 0, ..., 0). With bias_t = (hi, lo, 0, ...)
+    // the K=16 MMA adds hi + lo whichever chunk the swizzle puts first.
+    for (int i = threadIdx.x; i < 4096 / 16; i += blockDim.x)
+        reinterpret_cast<uint4*>(ones)[i] = make_uint4(0x3f803f80u, 0u, 0u, 0u);
+    ptx::fence_proxy_async_smem();
 
     const uint32_t warp = ptx::warp_id();
     const uint32_t lane = ptx::lane_id();
     const int a_mode = args.a_mode;
+#ifdef MTFM_GEMM_TRACE
+    constexpr bool kTrace = true;   // timing experiments: build with -DMTFM_GEMM_TRACE
+#else
+    constexpr bool kTrace = false;
+#endif
+    auto trace = [&](int slot) {
+        if (kTrace && args.trace && blockIdx.x == 0 && lane == 0) args.trace[slot] = clock64();
+    };
+    if (threadIdx.x == 0) trace(0);
     // Warp roles. The issue arbiter favours higher warp ids, so the latency-
     // critical single-thread roles sit at the top: 15 MMA issuer, 14 TMA
     // producer, 13 TMEM allocator; epilogue warps 0..n_epi-1 (warp & 3 = TMEM
@@ -256,9 +307,9 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
             ptx::mbar_init(&empty_bar[s], 1);
         }
         ptx::mbar_init(bres_bar, 1);
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < C::kAcc; ++s) {
             ptx::mbar_init(&tfull_bar[s], 1);
-            ptx::mbar_init(&tempty_bar[s], args.n_epi);  // one arrive per epilogue warp
+            ptx::mbar_init(&tempty_bar[s], 4);  // one arrive per warp of the epilogue group
         }
         for (int s = 0; s < 24; ++s) ptx::mbar_init(&res_bar[s], 1);
         ptx::fence_mbar_init();
@@ -272,6 +323,7 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (threadIdx.x == 0) trace(1);
 
     if (warp == kWarpTma) {
         // ------------------------------------------------ TMA producer (B, and A in A_TMA mode)
@@ -281,28 +333,38 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                 const CtaWork& w = args.cta[blockIdx.x];
                 const GemmProblem& p = args.p[w.pi];
                 const int kblocks = p.K / C::BK;
-                ptx::mbar_arrive_expect_tx(bres_bar, kblocks * C::B_BYTES);
+                ptx::mbar_arrive_expect_tx(bres_bar, kblocks * C::B_BYTES + (p.has_bias ? BN * 32 : 0));
                 for (int kb = 0; kb < kblocks; ++kb)
                     ptx::tma_load_2d(bres + kb * C::B_BYTES, &p.tma_b, bres_bar, kb * C::BK, w.nb * BN);
+                if (p.has_bias) ptx::tma_load_2d(bres + kblocks * C::B_BYTES, &p.tma_bias, bres_bar, 0, w.nb * BN);
             }
             int stage = 0;
             uint32_t phase = 0;
-            gemm_detail::TileSeq seq;
+            int ntile = 0;
+            gemm_detail::TileSeq seq(args, s_tile_start, s_tiles_n);
             int pi, mb, nb;
             while (seq.next(args, gemm_detail::decode_tile, pi, mb, nb)) {
                 const GemmProblem& p = args.p[pi];
-                const int kblocks = p.K / C::BK;
+                const int kblocks = s_kblocks[pi];
+                const bool p_bias = s_has_bias[pi];
+                if (ntile < 64) trace(320 + ntile);
+                ++ntile;
                 for (int kb = 0; kb < kblocks; ++kb) {
                     ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+                    if (ntile - 1 < 8 && kb < 8) trace(640 + (ntile - 1) * 16 + kb);
                     uint8_t* sa = smem + stage * stage_bytes;
                     uint8_t* sb = sa + C::A_BYTES;
-                    const int bytes = (a_mode == A_TMA ? C::A_BYTES : 0) + (args.b_res ? 0 : C::B_BYTES);
+                    const bool skip_a = args.debug & 8;  // timing experiment: no A loads
+                    const bool bias_here = !args.b_res && p_bias && kb == kblocks - 1;  // streaming: bias tile with the last k-block
+                    const int bytes = (a_mode == A_TMA && !skip_a ? C::A_BYTES : 0) + (args.b_res ? 0 : C::B_BYTES) +
+                                      (bias_here ? BN * 32 : 0);
                     if (bytes > 0)
                         ptx::mbar_arrive_expect_tx(&full_bar[stage], bytes);
                     else
                         ptx::mbar_arrive(&full_bar[stage]);
-                    if (a_mode == A_TMA) ptx::tma_load_2d(sa, &p.tma_a, &full_bar[stage], kb * C::BK, mb * C::BM);
+                    if (a_mode == A_TMA && !skip_a) ptx::tma_load_2d(sa, &p.tma_a, &full_bar[stage], kb * C::BK, mb * C::BM);
                     if (!args.b_res) ptx::tma_load_2d(sb, &p.tma_b, &full_bar[stage], kb * C::BK, nb * BN);
+                    if (bias_here) ptx::tma_load_2d(sb + C::B_BYTES, &p.tma_bias, &full_bar[stage], 0, nb * BN);
                     if (++stage == n_stages) {
                         stage = 0;
                         phase ^= 1;
@@ -316,11 +378,11 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
             const int pt = (warp - 8) * 32 + lane;
             int stage = 0;
             uint32_t phase = 0;
-            gemm_detail::TileSeq seq;
+            gemm_detail::TileSeq seq(args, s_tile_start, s_tiles_n);
             int pi, mb, nb;
             while (seq.next(args, gemm_detail::decode_tile, pi, mb, nb)) {
                 const GemmProblem& p = args.p[pi];
-                const int kblocks = p.K / C::BK;
+                const int kblocks = s_kblocks[pi];
                 for (int kb = 0; kb < kblocks; ++kb) {
                     ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
                     gemm_detail::produce_a(p, a_mode, mb * C::BM, kb * C::BK, smem + stage * stage_bytes, pt);
@@ -335,49 +397,64 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
             }
         }
     } else if (warp == kWarpMma) {
-        // ------------------------------------------------ MMA issuer
+        // ------------------------------------------------ MMA issuer (one elected lane per k-block)
         const uint32_t idesc = ptx::instr_desc_bf16(128, BN, false, false);
         int stage = 0;
         uint32_t phase = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
         bool bres_ready = false;
-        gemm_detail::TileSeq seq;
+        int ntile = 0;
+        gemm_detail::TileSeq seq(args, s_tile_start, s_tiles_n);
         int pi, mb, nb;
         while (seq.next(args, gemm_detail::decode_tile, pi, mb, nb)) {
-            const int kblocks = args.p[pi].K / C::BK;
+            const int kblocks = s_kblocks[pi];
             if (args.b_res && !bres_ready) {
                 ptx::mbar_wait(bres_bar, 0);
                 bres_ready = true;
+                trace(2);
             }
-            // the epilogue hands every accumulator back (bias-initialised when the
-            // tile has a bias, see below), including before its first use
+            // the epilogue hands every accumulator back, including before its first use
             ptx::mbar_wait(&tempty_bar[acc], acc_phase);
             ptx::tc_fence_after();
+            if (ntile < 64) trace(64 + ntile);
             const uint32_t d_tmem = tmem_base + acc * BN;
-            const uint32_t acc0 = args.p[pi].bias ? 1u : 0u;
+            const bool has_bias = s_has_bias[pi];
             for (int kb = 0; kb < kblocks; ++kb) {
+                // TMA -> MMA is async-proxy to async-proxy through the mbarrier: no
+                // tcgen05 fence here (one per k-block drains the tensor pipe)
                 ptx::mbar_wait(&full_bar[stage], phase);
-                ptx::tc_fence_after();
+                if (a_mode != A_TMA) ptx::tc_fence_after();  // generic-proxy producers (fence.proxy.async on their side)
+                if (ntile < 8 && kb < 8) trace(512 + ntile * 16 + kb * 2);
                 if (ptx::elect_one()) {
                     const uint32_t sa = ptx::smem_u32(smem + stage * stage_bytes);
                     const uint32_t sb = args.b_res ? ptx::smem_u32(bres + kb * C::B_BYTES) : sa + C::A_BYTES;
 #pragma unroll
                     for (int k = 0; k < C::BK / 16; ++k) {
+                        if (args.debug & 16) break;  // timing experiment: no MMAs
                         const uint64_t da = ptx::smem_desc(sa + k * 32, 16, 1024, 2);
                         const uint64_t db = ptx::smem_desc(sb + k * 32, 16, 1024, 2);
-                        ptx::umma_bf16(d_tmem, da, db, idesc, ((kb | k) != 0) ? 1u : acc0);
+                        ptx::umma_bf16(d_tmem, da, db, idesc, ((kb | k) != 0) ? 1u : 0u);
+                    }
+                    if (has_bias && kb == kblocks - 1) {
+                        // D += ones(128 x 16) * bias_t(BN x 16)^T: the bias, exact to ~2^-17 (hi + lo)
+                        const uint32_t sbias = args.b_res ? ptx::smem_u32(bres + kblocks * C::B_BYTES) : sb + C::B_BYTES;
+                        ptx::umma_bf16(d_tmem, ptx::smem_desc(ptx::smem_u32(ones), 16, 256, 6),
+                                       ptx::smem_desc(sbias, 16, 256, 6), idesc, 1u);
                     }
                     ptx::umma_commit(&empty_bar[stage]);
                     if (kb == kblocks - 1) ptx::umma_commit(&tfull_bar[acc]);
                 }
                 __syncwarp();
+                if (ntile < 8 && kb < 8) trace(512 + ntile * 16 + kb * 2 + 1);
                 if (++stage == n_stages) {
                     stage = 0;
                     phase ^= 1;
                 }
             }
-            if (++acc == 2) {
+            if (ntile < 64) trace(128 + ntile);
+            ++ntile;
+            if (++acc == C::kAcc) {
                 acc = 0;
                 acc_phase ^= 1;
             }
@@ -386,14 +463,13 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
         // ------------------------------------------------ epilogue
         // TMEM -> registers (SiLU) -> swizzled SMEM staging (double buffered
         // per warp) -> TMA bulk-tensor store, or for row-mapped outputs
-        // coalesced 16-byte row-segment stores. The bias never touches the
-        // epilogue's math: each accumulator buffer is re-initialised with the
-        // bias of the tile that will use it next before it is handed back to
-        // the MMA warp, which then accumulates on top of it.
+        // coalesced 16-byte row-segment stores. The bias is already in the
+        // accumulator (added by the MMA warp).
         const uint32_t q = warp & 3;                    // TMEM lane quarter
-        const int group = warp >> 2;                    // column-chunk group of this quarter
+        const int group = warp >> 2;                    // epilogue group: tiles j = group (mod n_groups)
         const int n_groups = args.n_epi >> 2;
-        float* stg_base = stg_all + warp * 2 * 32 * 32;
+        float* stg_base = stg_all + warp * (args.stg_warp / 4);
+        const bool stg_single = args.stg_warp < C::STG_WARP;  // one 4 KB buffer (bf16 bulk-store launches)
         const int sub = lane >> 3;                      // row within a 4-row group
         const int ch = lane & 7;                        // 16-byte chunk within a 32-column row slice
         const uint32_t lane_base = tmem_base + ((q * 32u) << 16);
@@ -403,42 +479,17 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
         uint32_t nstore = 0;                            // staging buffers used by this warp
         uint32_t res_phase = 0;                         // parity bit per staging buffer
         uint64_t* my_res = res_bar + warp * 2;
-        // bias of (problem, n-block) into accumulator buffer b, my chunks only
+        int ntile = 0;
         // column unit per warp: 64 for bf16 bulk-stored outputs (128-byte rows), else 32
         auto unit_of = [&](const GemmProblem& pp) {
             return ((pp.epi == EPI_SILU_BF16 || pp.epi == EPI_BIAS_BF16) && pp.use_tma_c && BN >= 64) ? 64 : 32;
         };
-        auto init_bias = [&](const GemmProblem& pp, int nbk, int b) {
-            const float* bias = pp.bias;
-            if (!bias) return;
-            const int N = pp.N;
-            const int unit = unit_of(pp);
-            for (int ui = group; ui < BN / unit; ui += n_groups) {
-#pragma unroll 1
-                for (int cc = 0; cc < unit; cc += 16) {
-                    const int c = ui * unit + cc;
-                    const int n0 = nbk * BN + c;
-                    uint32_t r[16];
-                    if (n0 + 16 <= N) {
-                        // lane-uniform address: one broadcast float4 load per 4 columns
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + n0) + k);
-                            r[4 * k] = __float_as_uint(b4.x);
-                            r[4 * k + 1] = __float_as_uint(b4.y);
-                            r[4 * k + 2] = __float_as_uint(b4.z);
-                            r[4 * k + 3] = __float_as_uint(b4.w);
-                        }
-                    } else {
-#pragma unroll
-                        for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(n0 + i < N ? __ldg(bias + n0 + i) : 0.f);
-                    }
-                    ptx::tmem_st16(lane_base + b * BN + c, r);
-                }
-            }
+        int fk = 0;  // fine-trace index within the tile
+        auto ftrace = [&]() {
+            if (warp == 0 && ntile < 8 && fk < 16) trace(384 + ntile * 16 + fk);
+            ++fk;
         };
         auto release = [&](int b) {
-            ptx::tmem_st_wait();
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&tempty_bar[b]);
@@ -451,62 +502,74 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                 ptx::tma_load_2d(stg_base + b * 32 * 32, &pp.tma_c, &my_res[b], col, row);
             }
         };
-        gemm_detail::TileSeq seq;
+        // Group g owns the CTA's tiles j = g, g + n_groups, ...; tile j uses
+        // accumulator j % kAcc, so n_groups tiles are drained concurrently while
+        // the MMA warp runs up to kAcc tiles ahead.
+        gemm_detail::TileSeq seq(args, s_tile_start, s_tiles_n);
         {
-            // prepare both accumulator buffers for the first two tiles
-            gemm_detail::TileSeq la = seq;
-            int lpi, lmb, lnb;
-            for (int b = 0; b < 2; ++b) {
-                if (la.next(args, gemm_detail::decode_tile, lpi, lmb, lnb)) init_bias(args.p[lpi], lnb, b);
-                release(b);
-            }
+            // hand out the accumulators of the first kAcc tiles (each by the group that drains it)
+            for (int b = 0; b < C::kAcc; ++b)
+                if (b % n_groups == group) release(b);
         }
         int pi, mb, nb;
-        while (seq.next(args, gemm_detail::decode_tile, pi, mb, nb)) {
+        for (int j = 0; seq.next(args, gemm_detail::decode_tile, pi, mb, nb); ++j) {
+            if (j % n_groups != group) continue;
+            acc = j % C::kAcc;
+            acc_phase = (j / C::kAcc) & 1;
             const GemmProblem& p = args.p[pi];
             const int row0 = mb * C::BM + q * 32;
             const bool bf16_out = p.epi == EPI_SILU_BF16 || p.epi == EPI_BIAS_BF16;
             const int unit = unit_of(p);
-            const int step = n_groups * unit / 32;  // in 32-column chunks
-            int ci = group * unit / 32;
+            const int step = unit / 32;  // in 32-column chunks
+            int ci = 0;
             if (p.use_tma_r && ci < kChunks && nb * BN + ci * 32 < p.N) res_load(p, nstore & 1, nb * BN + ci * 32, row0);
             ptx::mbar_wait(&tfull_bar[acc], acc_phase);
             ptx::tc_fence_after();
+            if (warp == 0 && ntile < 64) trace(192 + ntile);
+            fk = 0;
 #pragma unroll 1
             for (; ci < kChunks; ci += step) {
                 const int c = ci * 32;
                 const int n0 = nb * BN + c;
+                if (args.debug & 32) continue;  // timing experiment: epilogue does nothing but the handshakes
                 if (bf16_out && p.use_tma_c && unit == 64) {
                     // ---- fast path: 64 columns -> bf16 (SiLU) -> one 32 x 128 B SW128 box
                     if (n0 >= p.N) continue;  // warp-uniform (TMEM reads below are all-or-nothing)
-                    float v[64];
+                    float* stg = stg_base + (stg_single ? 0 : (nstore & 1) * 32 * 32);
+                    uint8_t* sb = reinterpret_cast<uint8_t*>(stg) + lane * 128;
+                    uint32_t w[2][16];
 #pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        ptx::tmem_ld16(lane_base + acc * BN + c + 16 * k, *reinterpret_cast<float(*)[16]>(v + 16 * k));
-                    ptx::tmem_ld_wait();
-                    if (args.debug & 4) {  // timing experiment: TMEM read only
-                        if (v[0] == 12345.f) ++nstore;
-                        continue;
+                    for (int hh = 0; hh < 2; ++hh) {
+                        // 32 columns at a time: TMEM -> SiLU (batched MUFU) -> bf16 -> staging
+                        float v[32];
+                        ptx::tmem_ld16(lane_base + acc * BN + c + 32 * hh, *reinterpret_cast<float(*)[16]>(v));
+                        ptx::tmem_ld16(lane_base + acc * BN + c + 32 * hh + 16, *reinterpret_cast<float(*)[16]>(v + 16));
+                        ptx::tmem_ld_wait();
+                        ftrace();
+                        if (p.epi == EPI_SILU_BF16 && !(args.debug & 2)) {
+                            ptx::silu_bf16_batch<16>(v, w[hh]);
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < 32; e += 2) w[hh][e / 2] = pack_bf16(v[e], v[e + 1]);
+                        }
                     }
-                    uint32_t w[32];
-                    if (p.epi == EPI_SILU_BF16 && !(args.debug & 2)) {
-#pragma unroll
-                        for (int e = 0; e < 64; e += 2) w[e / 2] = ptx::silu2_bf16(v[e], v[e + 1]);
-                    } else {
-#pragma unroll
-                        for (int e = 0; e < 64; e += 2) w[e / 2] = pack_bf16(v[e], v[e + 1]);
+                    ftrace();
+                    // the bulk store that last read this staging buffer must be done with it
+                    if (lane == 0) {
+                        if (stg_single) ptx::bulk_wait_read<0>();
+                        else ptx::bulk_wait_read<1>();
                     }
-                    uint8_t* sb = reinterpret_cast<uint8_t*>(stg_base + (nstore & 1) * 32 * 32) + lane * 128;
-                    if (lane == 0) ptx::bulk_wait_read<1>();
                     __syncwarp();
+                    ftrace();
 #pragma unroll
                     for (int k = 0; k < 8; ++k)
                         *reinterpret_cast<uint4*>(sb + ((k ^ (lane & 7)) << 4)) =
-                            make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+                            make_uint4(w[k >> 2][4 * (k & 3)], w[k >> 2][4 * (k & 3) + 1], w[k >> 2][4 * (k & 3) + 2],
+                                       w[k >> 2][4 * (k & 3) + 3]);
                     ptx::fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0 && !(args.debug & 1)) {
-                        ptx::tma_store_2d(&p.tma_c, stg_base + (nstore & 1) * 32 * 32, n0, row0);
+                        ptx::tma_store_2d(&p.tma_c, stg, n0, row0);
                         ptx::bulk_commit();
                     }
                     ++nstore;
@@ -661,20 +724,12 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                 __syncwarp();
                 ++nstore;
             }
-            // hand the buffer back, initialised for the tile that uses it next
-            {
-                gemm_detail::TileSeq la = seq;
-                int lpi, lmb, lnb;
-                if (la.next(args, gemm_detail::decode_tile, lpi, lmb, lnb) &&
-                    la.next(args, gemm_detail::decode_tile, lpi, lmb, lnb))
-                    init_bias(args.p[lpi], lnb, acc);
-                release(acc);
-            }
-            if (++acc == 2) {
-                acc = 0;
-                acc_phase ^= 1;
-            }
+            ftrace();
+            release(acc);  // hand the accumulator back to the MMA warp (tile j + kAcc)
+            if (warp == 0 && ntile < 64) trace(256 + ntile);
+            ++ntile;
         }
+        if (warp == 0) trace(3);
         if (lane == 0) ptx::bulk_wait<0>();  // all bulk stores complete before exit
         __syncwarp();
     }

@@ -123,6 +123,35 @@ struct DevBuf {
     }
 };
 
+// Bias tiles for the tensor-core GEMM: bias_t[n] = (hi, lo, 0 x 14) in bf16 with
+// hi + lo = bias[n] to ~2^-17, added by one K=16 MMA against a ones tile.
+__global__ void bias_tile_kernel(const float* __restrict__ bias, int N, __nv_bfloat16* __restrict__ t) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N * 16) return;
+    const int n = i >> 4, c = i & 15;
+    const float b = bias[n];
+    const __nv_bfloat16 hi = __float2bfloat16_rn(b);
+    float v = 0.f;
+    if (c == 0) v = __bfloat162float(hi);
+    if (c == 1) v = b - __bfloat162float(hi);
+    t[i] = c == 0 ? hi : __float2bfloat16_rn(v);
+}
+
+struct BiasTiles {
+    std::map<std::pair<const float*, int>, std::unique_ptr<DevBuf>> tiles;
+    bool rebuild = false;  // re-derive on every use (debug entry: caller-owned bias buffers)
+    const __nv_bfloat16* get(const float* bias, int N, cudaStream_t st) {
+        auto& slot = tiles[{bias, N}];
+        if (!slot || rebuild) {
+            if (!slot) slot = std::make_unique<DevBuf>();
+            slot->alloc(static_cast<size_t>(N) * 16 * 2);
+            bias_tile_kernel<<<static_cast<int>(cdiv(N * 16, 256)), 256, 0, st>>>(bias, N, slot->as<__nv_bfloat16>());
+            ck(cudaGetLastError(), "bias tile");
+        }
+        return slot->as<__nv_bfloat16>();
+    }
+};
+
 template <typename T>
 void upload(DevBuf& d, const std::vector<T>& h, cudaStream_t st) {
     d.alloc(std::max<size_t>(h.size() * sizeof(T), 16));
@@ -187,6 +216,7 @@ struct mtfm_cuda_model {
     cudaStream_t stream = nullptr;
     // device weights
     mtfm::DevBuf d_src, d_slots;
+    mtfm::BiasTiles bias_tiles;  // GEMM bias tiles, built on first use
     mtfm::DevBuf emb_f32, emb_bf16;
     std::vector<std::unique_ptr<mtfm::SourceW>> srcw;
     std::vector<std::unique_ptr<mtfm::LayerW>> layers;
@@ -446,6 +476,7 @@ void finalize(mtfm_cuda_model& m) {
 }
 
 // ---------------------------------------------------------------- GEMM launch helpers
+
 template <int BN>
 void launch_gemm_tc_bn(GemmArgs& a, int grid, cudaStream_t st) {
     using C = gemm_detail::Cfg<BN>;
@@ -455,7 +486,7 @@ void launch_gemm_tc_bn(GemmArgs& a, int grid, cudaStream_t st) {
            "gemm smem attr");
         attr = true;
     }
-    const int smem = 1024 + a.bres_bytes + a.n_stages * a.stage_bytes + a.n_epi * C::STG_WARP + C::BAR_BYTES;
+    const int smem = 1024 + a.bres_bytes + 4096 + a.n_stages * a.stage_bytes + a.n_epi * a.stg_warp + C::BAR_BYTES;
     if (smem > C::kMaxSmem) fail(MTFM_CONTRACT_ERROR, "gemm smem plan exceeds 227 KB");
     gemm_tc_kernel<BN><<<grid, C::kThreads, smem, st>>>(a);
     ck(cudaGetLastError(), "gemm_tc launch");
@@ -530,7 +561,7 @@ int pick_bn_resident(const std::vector<TcProblem>& ps) {
     return best;
 }
 
-void run_gemm_tc(std::vector<TcProblem> ps, cudaStream_t st, long long& launches) {
+void run_gemm_tc(std::vector<TcProblem> ps, cudaStream_t st, long long& launches, BiasTiles& bias_tiles) {
     ps.erase(std::remove_if(ps.begin(), ps.end(), [](const TcProblem& p) { return p.M == 0 || p.N == 0; }),
              ps.end());
     if (ps.empty()) return;
@@ -610,7 +641,8 @@ void run_gemm_tc(std::vector<TcProblem> ps, cudaStream_t st, long long& launches
             p.tile_start = tiles;
             p.tiles_n = static_cast<int>(cdiv(s.N, bn));
             p.epi = s.epi;
-            p.bias = s.bias;
+            p.has_bias = s.bias != nullptr;
+            if (p.has_bias) p.tma_bias = tma_2d(bias_tiles.get(s.bias, s.N, st), s.N, 16, 16, 16, bn, 32);
             p.out = s.out;
             p.ldo = s.ldo;
             p.row_map = s.row_map;
@@ -634,17 +666,34 @@ void run_gemm_tc(std::vector<TcProblem> ps, cudaStream_t st, long long& launches
         a.n_tiles = tiles;
         static const int dbg = std::getenv("MTFM_GEMM_DEBUG") ? std::atoi(std::getenv("MTFM_GEMM_DEBUG")) : 0;
         a.debug = dbg;
+        static unsigned long long* trace_buf = nullptr;
+        if (std::getenv("MTFM_GEMM_TRACE")) {
+            if (!trace_buf) ck(cudaMalloc(&trace_buf, 1024 * 8), "trace alloc");
+            ck(cudaMemsetAsync(trace_buf, 0, 1024 * 8, st), "trace clear");
+            a.trace = trace_buf;
+        }
         const int a_bytes = 128 * 64 * 2;
         const int b_bytes = bn * 64 * 2;
-        const int stg_warp = 2 * 32 * 32 * 4;
+        // bf16 bulk-store epilogues (64-column units) need one 4 KB staging buffer per warp
+        bool all_fast = true;
+        for (int i = 0; i < a.n_problems; ++i) {
+            const GemmProblem& p = a.p[i];
+            all_fast = all_fast && p.use_tma_c && bn >= 64 && (p.epi == EPI_SILU_BF16 || p.epi == EPI_BIAS_BF16);
+        }
+        static const bool stg_double = std::getenv("MTFM_GEMM_STG2") != nullptr;
+        const int stg_warp = (all_fast && !stg_double) ? 4096 : 8192;
+        a.stg_warp = stg_warp;
         if (!a.b_res) grid = std::min(tiles, kNumSMs);
-        a.bres_bytes = a.b_res ? (kmax / 64) * b_bytes : 0;
-        a.stage_bytes = a.b_res ? a_bytes : a_bytes + b_bytes;
+        bool any_bias = false;
+        for (int i = 0; i < a.n_problems; ++i) any_bias = any_bias || a.p[i].has_bias;
+        a.bias_bytes = any_bias ? bn * 32 : 0;
+        a.bres_bytes = a.b_res ? (kmax / 64) * b_bytes + a.bias_bytes : 0;
+        a.stage_bytes = a.b_res ? a_bytes : a_bytes + b_bytes + a.bias_bytes;
         // 12 epilogue warps when A is TMA-loaded and >= 3 stages still fit, else 8
         for (int ne : {12, 8}) {
-            if (ne == 12 && a.a_mode != A_TMA) continue;
+            if (ne == 12 && (a.a_mode != A_TMA || bn >= 256)) continue;  // epilogue groups <= accumulator buffers
             if (force_epi && ne != force_epi) continue;
-            const int avail = 227 * 1024 - 1024 - 512 - ne * stg_warp - a.bres_bytes;
+            const int avail = 227 * 1024 - 1024 - gemm_detail::Cfg<128>::BAR_BYTES - 4096 - ne * stg_warp - a.bres_bytes;
             a.n_epi = ne;
             a.n_stages = std::min(8, avail / a.stage_bytes);
             if (force_stages) a.n_stages = std::min(a.n_stages, force_stages);
@@ -655,6 +704,38 @@ void run_gemm_tc(std::vector<TcProblem> ps, cudaStream_t st, long long& launches
         else if (bn == 128) launch_gemm_tc_bn<128>(a, grid, st);
         else launch_gemm_tc_bn<64>(a, grid, st);
         ++launches;
+        if (a.trace) {
+            unsigned long long h[1024];
+            ck(cudaMemcpyAsync(h, a.trace, sizeof(h), cudaMemcpyDeviceToHost, st), "trace fetch");
+            ck(cudaStreamSynchronize(st), "trace sync");
+            const unsigned long long t0 = h[0];
+            auto rel = [&](int i) { return h[i] ? static_cast<long long>(h[i] - t0) : -1LL; };
+            std::fprintf(stderr, "trace bn=%d grid=%d stages=%d: start->sync %lld bres %lld end %lld\n", bn, grid,
+                         a.n_stages, rel(1), rel(2), rel(3));
+            for (int i = 0; i < 12; ++i)
+                std::fprintf(stderr, "  tile %2d: tma %7lld  mma_go %7lld  mma_done %7lld  epi_go %7lld  epi_done %7lld\n", i,
+                             rel(320 + i), rel(64 + i), rel(128 + i), rel(192 + i), rel(256 + i));
+            for (int i = 0; i < 8; ++i) {
+                std::fprintf(stderr, "  epi tile %d:", i);
+                long long prev = rel(192 + i);
+                for (int k = 0; k < 16; ++k) {
+                    const long long t = rel(384 + i * 16 + k);
+                    if (t < 0) break;
+                    std::fprintf(stderr, " +%lld", t - prev);
+                    prev = t;
+                }
+                std::fprintf(stderr, " | release +%lld\n", rel(256 + i) - prev);
+            }
+            for (int i = 0; i < 8; ++i) {
+                std::fprintf(stderr, "  mma tile %d (go %lld):", i, rel(64 + i));
+                for (int k = 0; k < 8; ++k) {
+                    if (rel(512 + i * 16 + 2 * k) < 0) break;
+                    std::fprintf(stderr, " [tma %lld full %lld iss %lld]", rel(640 + i * 16 + k), rel(512 + i * 16 + 2 * k),
+                                 rel(512 + i * 16 + 2 * k + 1));
+                }
+                std::fprintf(stderr, "\n");
+            }
+        }
     }
 }
 
@@ -967,6 +1048,7 @@ struct StageScope {
 // ---------------------------------------------------------------- the forward
 template <typename T>
 void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
+    BiasTiles& BT = m.bias_tiles;
     constexpr bool kTc = std::is_same<T, __nv_bfloat16>::value;
     constexpr double el = sizeof(T);
     cudaStream_t st = m.stream;
@@ -1042,11 +1124,11 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
         }
         {
             StageScope sc(m, "tok_mlp1", tok_f1, tok_in * el + Rd * 2 * d * el);
-            run_gemm_tc(p1, st, L);
+            run_gemm_tc(p1, st, L, BT);
         }
         {
             StageScope sc(m, "tok_mlp2", tok_f2, Rd * 2 * d * el + Rd * d * 4);
-            run_gemm_tc(p2, st, L);
+            run_gemm_tc(p2, st, L, BT);
         }
     } else {
         std::vector<SimtGemm> p1, p2;
@@ -1122,7 +1204,7 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                     tp.row_group = rm.src;
                     tp.gain = Lw->g1g.as<float>();
                     tp.gbias = Lw->g1b.as<float>();
-                    run_gemm_tc({tp}, st, L);
+                    run_gemm_tc({tp}, st, L, BT);
                 } else {
                     {
                         StageScope sc(m, "gln1", 0, Rd * d * (4 + el));
@@ -1132,7 +1214,7 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                     StageScope sc(m, "proj_full", 2.0 * Rd * d * pw, Rd * d * el + Rd * pw * el);
                     run_gemm_tc({{XN, d, Lw->t1.as<__nv_bfloat16>(), d, static_cast<int>(R), pw, d, EPI_SILU_BF16,
                                   Lw->b1.as<float>(), Pm, pw, nullptr, 0, nullptr}},
-                                st, L);
+                                st, L, BT);
                 }
                 {
                     StageScope sc(m, "attn_full", 4.0 * hd * sc_full, Rd * (hd + 2 * gd) * el + Rd * hd * el);
@@ -1175,7 +1257,7 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                     tp.gbias = Lw->g2b.as<float>();
                     tp.u_src = Pm;
                     tp.ldu = pw;
-                    run_gemm_tc({tp}, st, L);
+                    run_gemm_tc({tp}, st, L, BT);
                 } else {
                     {
                         StageScope sc(m, "gate", 0, Rd * hd * el * 3);
@@ -1186,7 +1268,7 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                     StageScope sc(m, "f2_full", 2.0 * Rd * hd * d, Rd * hd * el + Rd * d * 8);
                     run_gemm_tc({{G, hd, Lw->tf2.as<__nv_bfloat16>(), hd, static_cast<int>(R), d, hd, EPI_RESID_F32,
                                   Lw->f2b.as<float>(), X, d, nullptr, 0, X}},
-                                st, L);
+                                st, L, BT);
                 }
                 ctx_stats_valid = false;
             } else {
@@ -1203,7 +1285,7 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                                   Lw->bkv.as<float>(), KV, 2 * gd, nullptr, 0, nullptr},
                                  {XN + NE * d, d, Lw->t1.as<__nv_bfloat16>(), d, static_cast<int>(NT), 2 * hd, d,
                                   EPI_SILU_BF16, Lw->b1.as<float>(), UQ, 2 * hd, nullptr, 0, nullptr}},
-                                st, L);
+                                st, L, BT);
                 } else {
                     StageScope sc(m, "proj_target", 2.0 * (Rd * d * 2 * gd + Td * d * 2 * hd),
                                   Rd * d * 4 + Rd * 2 * gd * el + Td * 2 * hd * el);
@@ -1224,7 +1306,7 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                     uq.ldo = 2 * hd;
                     uq.a_row0 = NE;
                     uq.g_row0 = NE;
-                    run_gemm_tc({kv, uq}, st, L);
+                    run_gemm_tc({kv, uq}, st, L, BT);
                 }
                 {
                     StageScope sc(m, "attn_target", 4.0 * hd * sc_t, Rd * 2 * gd * el + Td * 2 * hd * el);
@@ -1260,7 +1342,7 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                     StageScope sc(m, "f2_target", 2.0 * Td * hd * d, Td * hd * el + Td * d * 8);
                     run_gemm_tc({{G, hd, Lw->tf2.as<__nv_bfloat16>(), hd, static_cast<int>(NT), d, hd, EPI_RESID_F32,
                                   Lw->f2b.as<float>(), X, d, nullptr, NE, X}},
-                                st, L);
+                                st, L, BT);
                 } else {
                     {
                         StageScope sc(m, "attn_stats", 0, Td * hd * el);
@@ -1279,7 +1361,7 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                     tp.gbias = Lw->g2b.as<float>();
                     tp.u_src = UQ;
                     tp.ldu = 2 * hd;
-                    run_gemm_tc({tp}, st, L);
+                    run_gemm_tc({tp}, st, L, BT);
                 }
                 ctx_stats_valid = true;
             }
@@ -1298,7 +1380,7 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                 if constexpr (kTc)
                     run_gemm_tc({{XN, d, Lw->t1.as<__nv_bfloat16>(), d, static_cast<int>(R), pw, d, EPI_SILU_BF16,
                                   Lw->b1.as<float>(), Pm, pw, nullptr, 0, nullptr}},
-                                st, L);
+                                st, L, BT);
                 else
                     run_gemm_simt({{reinterpret_cast<const float*>(XN), d, Lw->w1.as<float>(), static_cast<int>(R), pw,
                                     d, Lw->b1.as<float>(), EPI_SILU_BF16, Pm, pw, nullptr, 0, nullptr}},
@@ -1346,7 +1428,7 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                 if constexpr (kTc)
                     run_gemm_tc({{G, hd, Lw->tf2.as<__nv_bfloat16>(), hd, static_cast<int>(R), d, hd, EPI_RESID_F32,
                                   Lw->f2b.as<float>(), X, d, nullptr, 0, X}},
-                                st, L);
+                                st, L, BT);
                 else
                     run_gemm_simt({{reinterpret_cast<const float*>(G), hd, Lw->f2.as<float>(), static_cast<int>(R), d,
                                     hd, Lw->f2b.as<float>(), EPI_RESID_F32, X, d, nullptr, 0, X}},
@@ -1362,7 +1444,7 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                                   Lw->bkv.as<float>(), KV, 2 * gd, nullptr, 0, nullptr},
                                  {XN + NE * d, d, Lw->t1.as<__nv_bfloat16>(), d, static_cast<int>(NT), 2 * hd, d,
                                   EPI_SILU_BF16, Lw->b1.as<float>(), UQ, 2 * hd, nullptr, 0, nullptr}},
-                                st, L);
+                                st, L, BT);
                 else
                     run_gemm_simt({{reinterpret_cast<const float*>(XN), d, Lw->wkv.as<float>(), static_cast<int>(R),
                                     2 * gd, d, Lw->bkv.as<float>(), EPI_SILU_BF16, KV, 2 * gd, nullptr, 0, nullptr},
@@ -1414,7 +1496,7 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                 if constexpr (kTc)
                     run_gemm_tc({{G, hd, Lw->tf2.as<__nv_bfloat16>(), hd, static_cast<int>(NT), d, hd, EPI_RESID_F32,
                                   Lw->f2b.as<float>(), X, d, nullptr, NE, X}},
-                                st, L);
+                                st, L, BT);
                 else
                     run_gemm_simt({{reinterpret_cast<const float*>(G), hd, Lw->f2.as<float>(), static_cast<int>(NT), d,
                                     hd, Lw->f2b.as<float>(), EPI_RESID_F32, X, d, nullptr, NE, X}},
@@ -1437,7 +1519,7 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
         StageScope sc(m, "heads_gemm", hflops, Td * d * 2 + Td * m.head_n * 4);
         run_gemm_tc({{XN, d, m.head_t.as<__nv_bfloat16>(), d, static_cast<int>(NT), m.head_n, d, EPI_BIAS_F32, nullptr,
                       Y, m.head_ld, nullptr, 0, nullptr}},
-                    st, L);
+                    st, L, BT);
     } else {
         StageScope sc(m, "heads_gemm", hflops, Td * d * 4 + Td * m.head_n * 4);
         run_gemm_simt({{X + NE * d, d, m.head_w.as<float>(), static_cast<int>(NT), m.head_n, d, nullptr, EPI_BIAS_F32, Y,
@@ -1810,7 +1892,9 @@ mtfm_status mtfm_cuda_debug_gemm(const void* A, const void* Bt, const float* bia
         TcProblem tp{static_cast<const __nv_bfloat16*>(A), K, static_cast<const __nv_bfloat16*>(Bt), K,
                      static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), epi, bias, out, N, nullptr, 0,
                      epi == EPI_RESID_F32 ? static_cast<const float*>(out) : nullptr};
-        run_gemm_tc({tp}, static_cast<cudaStream_t>(stream), L);
+        static BiasTiles BT;
+        BT.rebuild = true;
+        run_gemm_tc({tp}, static_cast<cudaStream_t>(stream), L, BT);
     });
 }
 

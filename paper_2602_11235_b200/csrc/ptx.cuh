@@ -210,6 +210,38 @@ __device__ __forceinline__ float silu_fast(float x) {
     return fmaf(h, t, h);
 }
 
+// 2n SiLUs -> n packed bf16x2, batched: all MUFU.TANH results are produced
+// into distinct registers before the FFMA2s consume them, so the MUFU latency
+// is paid once per batch instead of once per pair (a single-pair helper lets
+// the register allocator funnel every tanh through one register pair).
+template <int N2>
+__device__ __forceinline__ void silu_bf16_batch(const float* v, uint32_t* w) {
+    uint64_t hv[N2];
+    float t[2 * N2];
+#pragma unroll
+    for (int i = 0; i < N2; ++i) {
+        uint64_t sv;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(sv) : "f"(v[2 * i]), "f"(v[2 * i + 1]));
+        asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(hv[i]) : "l"(sv), "l"(0x3f0000003f000000ull));
+    }
+#pragma unroll
+    for (int i = 0; i < N2; ++i) {
+        float h0, h1;
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(h0), "=f"(h1) : "l"(hv[i]));
+        asm("tanh.approx.f32 %0, %1;" : "=f"(t[2 * i]) : "f"(h0));
+        asm("tanh.approx.f32 %0, %1;" : "=f"(t[2 * i + 1]) : "f"(h1));
+    }
+#pragma unroll
+    for (int i = 0; i < N2; ++i) {
+        uint64_t tv, rv;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(tv) : "f"(t[2 * i]), "f"(t[2 * i + 1]));
+        asm("fma.rn.f32x2 %0, %1, %2, %1;" : "=l"(rv) : "l"(hv[i]), "l"(tv));
+        float r0, r1;
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(r0), "=f"(r1) : "l"(rv));
+        asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(w[i]) : "f"(r1), "f"(r0));
+    }
+}
+
 // Two SiLUs -> packed bf16x2: h = s/2 (FMUL2), t = tanh(h) (MUFU), h + h*t (FFMA2).
 __device__ __forceinline__ uint32_t silu2_bf16(float s0, float s1) {
     uint64_t sv, hv, tv, rv;

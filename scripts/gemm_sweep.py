@@ -28,10 +28,20 @@ for name, M, K, N, epi in shapes:
     for _ in range(3):
         run()
     torch.cuda.synchronize()
+    # replay a captured graph of 10 launches: no host gaps inside the timed region
+    g = torch.cuda.CUDAGraph()
+    cs = torch.cuda.Stream()
+    with torch.cuda.stream(cs):
+        st = cs
+        with torch.cuda.graph(g, stream=cs):
+            for _ in range(10):
+                run()
+    st = torch.cuda.current_stream()
+    g.replay()
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(10):
-        run()
+    g.replay()
     e1.record()
     e1.synchronize()
     ms = e0.elapsed_time(e1) / 10

@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdint>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 __device__ __forceinline__ float silu_tanh(float x) {
     float h = 0.5f * x, t;
@@ -49,6 +50,29 @@ __global__ void bench(float* out, int iters, long long* clk) {
         if (V == 0) { a = silu_tanh(a + 0.5f); b = silu_tanh(b - 0.25f); c = silu_tanh(c + 0.1f); d = silu_tanh(d - 0.3f); }
         if (V == 1) { a = silu_ex2rcp(a + 0.5f); b = silu_ex2rcp(b - 0.25f); c = silu_ex2rcp(c + 0.1f); d = silu_ex2rcp(d - 0.3f); }
         if (V == 2) { a = silu_poly(a + 0.5f); b = silu_poly(b - 0.25f); c = silu_poly(c + 0.1f); d = silu_poly(d - 0.3f); }
+        if (V == 4) {
+            // tanh.approx.f16x2: h in f16, silu = h + h*tanh(h) in f32
+            uint32_t ha, hb;
+            asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(ha) : "f"(0.5f * a + 0.25f), "f"(0.5f * b - 0.125f));
+            asm("tanh.approx.f16x2 %0, %0;" : "+r"(ha));
+            asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hb) : "f"(0.5f * c + 0.05f), "f"(0.5f * d - 0.15f));
+            asm("tanh.approx.f16x2 %0, %0;" : "+r"(hb));
+            a = __half2float(__ushort_as_half(ha & 0xffff));
+            b = __half2float(__ushort_as_half(ha >> 16));
+            c = __half2float(__ushort_as_half(hb & 0xffff));
+            d = __half2float(__ushort_as_half(hb >> 16));
+        }
+        if (V == 5) {
+            uint32_t ha, hb;
+            asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(ha) : "f"(0.5f * a + 0.25f), "f"(0.5f * b - 0.125f));
+            asm("ex2.approx.f16x2 %0, %0;" : "+r"(ha));
+            asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hb) : "f"(0.5f * c + 0.05f), "f"(0.5f * d - 0.15f));
+            asm("ex2.approx.f16x2 %0, %0;" : "+r"(hb));
+            a = __half2float(__ushort_as_half(ha & 0xffff));
+            b = __half2float(__ushort_as_half(ha >> 16));
+            c = __half2float(__ushort_as_half(hb & 0xffff));
+            d = __half2float(__ushort_as_half(hb >> 16));
+        }
         if (V == 3) {
             uint32_t ha, hb;
             asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(ha) : "f"(0.5f * a + 0.25f), "f"(0.5f * b - 0.125f));
@@ -72,8 +96,8 @@ int main() {
     cudaMalloc(&out, 148 * 1024 * 4 * 4);
     cudaMalloc(&clk, 8);
     const int iters = 4096;
-    const char* names[4] = {"tanh", "ex2rcp", "poly", "tanhbf16x2"};
-    for (int v = 0; v < 4; ++v) {
+    const char* names[6] = {"tanh", "ex2rcp", "poly", "tanhbf16x2", "tanhf16x2", "ex2f16x2"};
+    for (int v = 0; v < 6; ++v) {
         for (int rep = 0; rep < 2; ++rep) {
             cudaEvent_t e0, e1;
             cudaEventCreate(&e0);
@@ -84,6 +108,8 @@ int main() {
             if (v == 1) bench<1><<<blocks, threads>>>(out, iters, clk);
             if (v == 2) bench<2><<<blocks, threads>>>(out, iters, clk);
             if (v == 3) bench<3><<<blocks, threads>>>(out, iters, clk);
+            if (v == 4) bench<4><<<blocks, threads>>>(out, iters, clk);
+            if (v == 5) bench<5><<<blocks, threads>>>(out, iters, clk);
             cudaEventRecord(e1);
             cudaEventSynchronize(e1);
             float ms;
