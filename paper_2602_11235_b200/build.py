@@ -30,6 +30,15 @@ def _stale(obj, deps):
 
 def build(verbose=False, extra_flags=()):
     os.makedirs(BUILD, exist_ok=True)
+    # objects remember the flags they were built with: a flag change rebuilds
+    stamp = os.path.join(BUILD, "flags.txt")
+    want = " ".join(FLAGS + list(extra_flags))
+    if not os.path.exists(stamp) or open(stamp).read() != want:
+        for f in os.listdir(BUILD):
+            if f.endswith(".o"):
+                os.remove(os.path.join(BUILD, f))
+        with open(stamp, "w") as fh:
+            fh.write(want)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     headers.append(os.path.join(ROOT, "include", "mtfm_cuda.h"))
     objs = []

@@ -44,8 +44,8 @@ enum GemmAMode : int { A_TMA = 0, A_LN = 1, A_GATE = 2 };
 constexpr int kMaxProblems = 16;
 
 struct GemmProblem {
-    CUtensorMap tma_a;      // box {64, 128}, SW128 (A_TMA only)
-    CUtensorMap tma_b;      // box {64, BN}, SW128
+    CUtensorMap tma_a;      // box {64, 128} (2D) or {64, 128, stage_kb} (3D k-block view), SW128 (A_TMA only)
+    CUtensorMap tma_b;      // box {64, BN} or {64, BN, stage_kb}, SW128
     CUtensorMap tma_c;      // output, box {32, 32}: bf16 SW64 / f32 SW128 (use_tma_c)
     int use_tma_c;          // plain row-major output rows [0, M): bulk-tensor stores
     int use_tma_r;          // EPI_RESID_F32 with resid == out: residual blocks TMA-prefetched via tma_c
@@ -87,7 +87,8 @@ struct GemmArgs {
     int a_mode;
     int b_res;        // 1: B-resident schedule (cta[]), 0: streaming over the global tile list
     int n_stages;     // SMEM pipeline stages
-    int stage_bytes;  // A_BYTES (+ B_BYTES when streaming B)
+    int stage_kb;     // k-blocks per stage: > 1 only when every K is a multiple of 64 (3D tensor maps, one TMA per stage)
+    int stage_bytes;  // stage_kb x (A_BYTES (+ B_BYTES when streaming B)) (+ bias tile)
     int bres_bytes;   // resident B slice bytes (b_res)
     int n_epi;        // epilogue warps: 8, or 12 when A comes from TMA (warps 12..15 free)
     int stg_warp;     // epilogue staging bytes per warp: 8 KB (2 fp32 blocks), 4 KB when every problem is a bf16 bulk store
@@ -257,6 +258,7 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
     uint8_t* smem = ones + 4096;                         // pipeline stages
     const int n_stages = args.n_stages;
     const int stage_bytes = args.stage_bytes;
+    const int KS = args.stage_kb;
     float* stg_all = reinterpret_cast<float*>(smem + n_stages * stage_bytes);
     uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + n_stages * stage_bytes + args.n_epi * args.stg_warp);
     uint64_t* empty_bar = full_bar + 8;
@@ -349,22 +351,29 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                 const bool p_bias = s_has_bias[pi];
                 if (ntile < 64) trace(320 + ntile);
                 ++ntile;
-                for (int kb = 0; kb < kblocks; ++kb) {
+                for (int kb = 0; kb < kblocks; kb += KS) {
                     ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
                     if (ntile - 1 < 8 && kb < 8) trace(640 + (ntile - 1) * 16 + kb);
                     uint8_t* sa = smem + stage * stage_bytes;
-                    uint8_t* sb = sa + C::A_BYTES;
+                    uint8_t* sb = sa + KS * C::A_BYTES;
                     const bool skip_a = args.debug & 8;  // timing experiment: no A loads
-                    const bool bias_here = !args.b_res && p_bias && kb == kblocks - 1;  // streaming: bias tile with the last k-block
-                    const int bytes = (a_mode == A_TMA && !skip_a ? C::A_BYTES : 0) + (args.b_res ? 0 : C::B_BYTES) +
-                                      (bias_here ? BN * 32 : 0);
+                    const bool bias_here = !args.b_res && p_bias && kb + KS >= kblocks;  // streaming: bias tile with the last stage
+                    const int bytes = (a_mode == A_TMA && !skip_a ? KS * C::A_BYTES : 0) +
+                                      (args.b_res ? 0 : KS * C::B_BYTES) + (bias_here ? BN * 32 : 0);
                     if (bytes > 0)
                         ptx::mbar_arrive_expect_tx(&full_bar[stage], bytes);
                     else
                         ptx::mbar_arrive(&full_bar[stage]);
-                    if (a_mode == A_TMA && !skip_a) ptx::tma_load_2d(sa, &p.tma_a, &full_bar[stage], kb * C::BK, mb * C::BM);
-                    if (!args.b_res) ptx::tma_load_2d(sb, &p.tma_b, &full_bar[stage], kb * C::BK, nb * BN);
-                    if (bias_here) ptx::tma_load_2d(sb + C::B_BYTES, &p.tma_bias, &full_bar[stage], 0, nb * BN);
+                    // one TMA instruction per operand and stage (each costs ~150 clk of issue)
+                    if (a_mode == A_TMA && !skip_a) {
+                        if (KS > 1) ptx::tma_load_3d(sa, &p.tma_a, &full_bar[stage], 0, mb * C::BM, kb);
+                        else ptx::tma_load_2d(sa, &p.tma_a, &full_bar[stage], kb * C::BK, mb * C::BM);
+                    }
+                    if (!args.b_res) {
+                        if (KS > 1) ptx::tma_load_3d(sb, &p.tma_b, &full_bar[stage], 0, nb * BN, kb);
+                        else ptx::tma_load_2d(sb, &p.tma_b, &full_bar[stage], kb * C::BK, nb * BN);
+                    }
+                    if (bias_here) ptx::tma_load_2d(sb + KS * C::B_BYTES, &p.tma_bias, &full_bar[stage], 0, nb * BN);
                     if (++stage == n_stages) {
                         stage = 0;
                         phase ^= 1;
@@ -420,30 +429,35 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
             if (ntile < 64) trace(64 + ntile);
             const uint32_t d_tmem = tmem_base + acc * BN;
             const bool has_bias = s_has_bias[pi];
-            for (int kb = 0; kb < kblocks; ++kb) {
-                // TMA -> MMA is async-proxy to async-proxy through the mbarrier: no
-                // tcgen05 fence here (one per k-block drains the tensor pipe)
+            for (int kb0 = 0; kb0 < kblocks; kb0 += KS) {
+                // TMA -> MMA is async-proxy to async-proxy through the mbarrier
                 ptx::mbar_wait(&full_bar[stage], phase);
+                const int kb = kb0;
                 if (a_mode != A_TMA) ptx::tc_fence_after();  // generic-proxy producers (fence.proxy.async on their side)
                 if (ntile < 8 && kb < 8) trace(512 + ntile * 16 + kb * 2);
+                const int nk = min(KS, kblocks - kb0);
+                const bool last = kb0 + KS >= kblocks;
                 if (ptx::elect_one()) {
-                    const uint32_t sa = ptx::smem_u32(smem + stage * stage_bytes);
-                    const uint32_t sb = args.b_res ? ptx::smem_u32(bres + kb * C::B_BYTES) : sa + C::A_BYTES;
+                    const uint32_t sa0 = ptx::smem_u32(smem + stage * stage_bytes);
+                    const uint32_t sb0 = args.b_res ? ptx::smem_u32(bres + kb0 * C::B_BYTES) : sa0 + KS * C::A_BYTES;
+                    for (int kbi = 0; kbi < nk; ++kbi) {
+                        const uint32_t sa = sa0 + kbi * C::A_BYTES, sb = sb0 + kbi * C::B_BYTES;
 #pragma unroll
-                    for (int k = 0; k < C::BK / 16; ++k) {
-                        if (args.debug & 16) break;  // timing experiment: no MMAs
-                        const uint64_t da = ptx::smem_desc(sa + k * 32, 16, 1024, 2);
-                        const uint64_t db = ptx::smem_desc(sb + k * 32, 16, 1024, 2);
-                        ptx::umma_bf16(d_tmem, da, db, idesc, ((kb | k) != 0) ? 1u : 0u);
+                        for (int k = 0; k < C::BK / 16; ++k) {
+                            if (args.debug & 16) break;  // timing experiment: no MMAs
+                            const uint64_t da = ptx::smem_desc(sa + k * 32, 16, 1024, 2);
+                            const uint64_t db = ptx::smem_desc(sb + k * 32, 16, 1024, 2);
+                            ptx::umma_bf16(d_tmem, da, db, idesc, ((kb0 | kbi | k) != 0) ? 1u : 0u);
+                        }
                     }
-                    if (has_bias && kb == kblocks - 1) {
+                    if (has_bias && last) {
                         // D += ones(128 x 16) * bias_t(BN x 16)^T: the bias, exact to ~2^-17 (hi + lo)
-                        const uint32_t sbias = args.b_res ? ptx::smem_u32(bres + kblocks * C::B_BYTES) : sb + C::B_BYTES;
+                        const uint32_t sbias = args.b_res ? ptx::smem_u32(bres + kblocks * C::B_BYTES) : sa0 + KS * (C::A_BYTES + C::B_BYTES);
                         ptx::umma_bf16(d_tmem, ptx::smem_desc(ptx::smem_u32(ones), 16, 256, 6),
                                        ptx::smem_desc(sbias, 16, 256, 6), idesc, 1u);
                     }
                     ptx::umma_commit(&empty_bar[stage]);
-                    if (kb == kblocks - 1) ptx::umma_commit(&tfull_bar[acc]);
+                    if (last) ptx::umma_commit(&tfull_bar[acc]);
                 }
                 __syncwarp();
                 if (ntile < 8 && kb < 8) trace(512 + ntile * 16 + kb * 2 + 1);

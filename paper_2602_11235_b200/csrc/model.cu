@@ -98,6 +98,23 @@ CUtensorMap tma_2d(const void* ptr, long long rows, long long cols, long long ld
     return m;
 }
 
+// k-block view of a row-major bf16 matrix with K % 64 == 0: dims {64, rows, K/64},
+// box {64, box_rows, box_kb} -> box_kb SW128 [box_rows][64] tiles back to back in SMEM.
+CUtensorMap tma_3d_kb(const void* ptr, long long rows, long long cols, long long ld, int box_rows, int box_kb) {
+    CUtensorMap m;
+    std::memset(&m, 0, sizeof(m));
+    if (rows == 0) return m;
+    cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(cols / 64)};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld * 2), 128};
+    cuuint32_t box[3] = {64, static_cast<cuuint32_t>(box_rows), static_cast<cuuint32_t>(box_kb)};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(MTFM_CUDA_ERROR, "cuTensorMapEncodeTiled (3D) failed (" + std::to_string(int(r)) + ")");
+    return m;
+}
+
 // ---------------------------------------------------------------- device buffers
 struct DevBuf {
     void* p = nullptr;
@@ -617,12 +634,21 @@ void run_gemm_tc(std::vector<TcProblem> ps, cudaStream_t st, long long& launches
         if (!bn) bn = force_bn ? force_bn : pick_bn(std::vector<TcProblem>(ps.begin() + i0, ps.begin() + i1));
         int tiles = 0;
         int kmax = 0;
+        // k-blocks per pipeline stage: 2 (one 3D TMA per operand per 2 k-blocks) when
+        // every K is a multiple of 64 and A is TMA-loaded, else 1
+        static const int force_kb = std::getenv("MTFM_GEMM_STAGE_KB") ? std::atoi(std::getenv("MTFM_GEMM_STAGE_KB")) : 0;
+        int ks = a.a_mode == A_TMA ? 2 : 1;
+        for (size_t i = i0; i < i1; ++i)
+            if (ps[i].K % 64 != 0 || ps[i].K < 128) ks = 1;
+        if (force_kb && ks > 1) ks = force_kb;
+        a.stage_kb = ks;
         for (size_t i = i0; i < i1; ++i) {
             const auto& s = ps[i];
             if (s.amode != a.a_mode) fail(MTFM_CONTRACT_ERROR, "mixed A modes in one grouped GEMM");
             GemmProblem& p = a.p[a.n_problems++];
-            if (s.amode == A_TMA) p.tma_a = tma_2d(s.A, s.M, s.K, s.lda, 64, 128, 128);
-            p.tma_b = tma_2d(s.Bt, s.N, s.K, s.ldb, 64, bn, 128);
+            if (s.amode == A_TMA) p.tma_a = ks > 1 ? tma_3d_kb(s.A, s.M, s.K, s.lda, 128, ks) : tma_2d(s.A, s.M, s.K, s.lda, 64, 128, 128);
+            // B: 2D boxes for the resident slice (loaded once per CTA), 3D per stage when streaming
+            p.tma_b = (ks > 1 && !a.b_res) ? tma_3d_kb(s.Bt, s.N, s.K, s.ldb, bn, ks) : tma_2d(s.Bt, s.N, s.K, s.ldb, 64, bn, 128);
             p.M = s.M;
             p.N = s.N;
             p.K = static_cast<int>(round_up(s.K, 64));
@@ -688,9 +714,21 @@ void run_gemm_tc(std::vector<TcProblem> ps, cudaStream_t st, long long& launches
         for (int i = 0; i < a.n_problems; ++i) any_bias = any_bias || a.p[i].has_bias;
         a.bias_bytes = any_bias ? bn * 32 : 0;
         a.bres_bytes = a.b_res ? (kmax / 64) * b_bytes + a.bias_bytes : 0;
-        a.stage_bytes = a.b_res ? a_bytes : a_bytes + b_bytes + a.bias_bytes;
+        a.stage_bytes = a.b_res ? ks * a_bytes : ks * (a_bytes + b_bytes) + a.bias_bytes;
         // 12 epilogue warps when A is TMA-loaded and >= 3 stages still fit, else 8
-        for (int ne : {12, 8}) {
+        for (int ne : {12, 8, 0}) {
+            if (ne == 0) {
+                // nothing fits with multi-k-block stages: fall back to one k-block per stage
+                if (a.stage_kb == 1) break;
+                a.stage_kb = 1;
+                for (int i = 0; i < a.n_problems; ++i) {
+                    const auto& s = ps[i0 + i];
+                    if (s.amode == A_TMA) a.p[i].tma_a = tma_2d(s.A, s.M, s.K, s.lda, 64, 128, 128);
+                    if (!a.b_res) a.p[i].tma_b = tma_2d(s.Bt, s.N, s.K, s.ldb, 64, bn, 128);
+                }
+                a.stage_bytes = a.b_res ? a_bytes : a_bytes + b_bytes + a.bias_bytes;
+                ne = 8;
+            }
             if (ne == 12 && (a.a_mode != A_TMA || bn >= 256)) continue;  // epilogue groups <= accumulator buffers
             if (force_epi && ne != force_epi) continue;
             const int avail = 227 * 1024 - 1024 - gemm_detail::Cfg<128>::BAR_BYTES - 4096 - ne * stg_warp - a.bres_bytes;
