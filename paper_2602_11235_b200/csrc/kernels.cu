@@ -481,6 +481,52 @@ template void launch_gln<__nv_bfloat16>(const float*, long long, long long, long
                                         const float*, const float*, float, __nv_bfloat16*, long long,
                                         cudaStream_t);
 
+template <int NS>
+__global__ void __launch_bounds__(256) gln_multi_kernel(const float* __restrict__ x, long long ldx, long long n_rows,
+                                                        int d, const int* __restrict__ row_src,
+                                                        const __grid_constant__ GlnCopies c, float eps, long long ldo) {
+    const int lane = threadIdx.x & 31;
+    const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long r = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); r < n_rows; r += warps) {
+        const float* xr = x + r * ldx;
+        int g = row_src[r];
+        float4 v[NS];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+            const int col = 128 * k + 4 * lane;
+            v[k] = col < d ? __ldcs(reinterpret_cast<const float4*>(xr + col)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        normalize_slices<NS>(v, d, lane, eps);
+        g = g < 0 ? 0 : g;
+        for (int l = 0; l < c.n; ++l) {
+            const float* gg = c.gain[l] + (long long)g * d;
+            const float* bb = c.bias[l] + (long long)g * d;
+            __nv_bfloat16* o = static_cast<__nv_bfloat16*>(c.out[l]) + r * ldo;
+#pragma unroll
+            for (int k = 0; k < NS; ++k) {
+                const int col = 128 * k + 4 * lane;
+                if (col < d) {
+                    const float4 ga = __ldg(reinterpret_cast<const float4*>(gg + col));
+                    const float4 be = __ldg(reinterpret_cast<const float4*>(bb + col));
+                    st4(o + col, make_float4(v[k].x * ga.x + be.x, v[k].y * ga.y + be.y, v[k].z * ga.z + be.z,
+                                             v[k].w * ga.w + be.w));
+                }
+            }
+        }
+    }
+}
+
+void launch_gln_multi_bf16(const float* x, long long ldx, long long n_rows, int d, const int* row_src,
+                           const GlnCopies& c, float eps, long long ldo, cudaStream_t st) {
+    if (n_rows == 0 || c.n == 0) return;
+    const int blocks = static_cast<int>(std::min<long long>(cdiv(n_rows, 8), 148ll * 16));
+    const int ns = static_cast<int>(cdiv(d, 128));
+    if (ns <= 1) gln_multi_kernel<1><<<blocks, 256, 0, st>>>(x, ldx, n_rows, d, row_src, c, eps, ldo);
+    else if (ns == 2) gln_multi_kernel<2><<<blocks, 256, 0, st>>>(x, ldx, n_rows, d, row_src, c, eps, ldo);
+    else if (ns <= 4) gln_multi_kernel<4><<<blocks, 256, 0, st>>>(x, ldx, n_rows, d, row_src, c, eps, ldo);
+    else gln_multi_kernel<8><<<blocks, 256, 0, st>>>(x, ldx, n_rows, d, row_src, c, eps, ldo);
+}
+
 template <typename T, int NS>
 __global__ void __launch_bounds__(256) gate_kernel(const T* __restrict__ a, long long lda, const T* __restrict__ u,
                                                    long long ldu, long long n_rows, int d,

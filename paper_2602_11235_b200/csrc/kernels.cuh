@@ -92,6 +92,19 @@ template <typename T>
 void launch_gln(const float* x, long long ldx, long long r0, long long n_rows, int d, const int* row_src,
                 const float* gain, const float* bias, float eps, T* out, long long ldo, cudaStream_t st);
 
+// The same rows normalised once and written with L different (gain, bias)
+// pairs: the GLN1 inputs of a block's target layers for the context rows, which
+// those layers never modify (hta.hpp:158-184 only update T rows).
+constexpr int kMaxGlnCopies = 8;
+struct GlnCopies {
+    const float* gain[kMaxGlnCopies];
+    const float* bias[kMaxGlnCopies];
+    void* out[kMaxGlnCopies];
+    int n;
+};
+void launch_gln_multi_bf16(const float* x, long long ldx, long long n_rows, int d, const int* row_src,
+                           const GlnCopies& c, float eps, long long ldo, cudaStream_t st);
+
 // Gate: out[r] = gln(a[r]) * u[r]   (hta.hpp:153,179)
 template <typename T>
 void launch_gate(const T* a, long long lda, const T* u, long long ldu, long long n_rows, int d,

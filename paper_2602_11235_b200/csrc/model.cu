@@ -27,6 +27,7 @@
 #include "common.cuh"
 #include "gemm_tc.cuh"
 #include "kernels.cuh"
+#include "tok_tc.cuh"
 
 namespace mtfm {
 
@@ -507,6 +508,17 @@ void launch_gemm_tc_bn(GemmArgs& a, int grid, cudaStream_t st) {
     if (smem > C::kMaxSmem) fail(MTFM_CONTRACT_ERROR, "gemm smem plan exceeds 227 KB");
     gemm_tc_kernel<BN><<<grid, C::kThreads, smem, st>>>(a);
     ck(cudaGetLastError(), "gemm_tc launch");
+}
+
+void launch_tok_fused(const TokArgs& a, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        ck(cudaFuncSetAttribute(tok_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tok_detail::SMEM),
+           "tok smem attr");
+        attr = true;
+    }
+    tok_fused_kernel<<<std::min(a.n_tiles, kNumSMs), 512, tok_detail::SMEM, st>>>(a);
+    ck(cudaGetLastError(), "tok_fused launch");
 }
 
 struct TcProblem {
@@ -999,9 +1011,12 @@ void prepare(mtfm_cuda_model& m, const mtfm_packed_batch* hb, int only_scenario,
     const size_t el = m.precision == MTFM_PRECISION_BF16 ? 2 : 4;
     const int pw = 2 * m.hd + 2 * m.gd;
     ia(B.X, R * m.d, 4);
-    ia(B.XN, R * m.d, el);
+    // bf16 path: GLN1 copies of the context rows for every target layer of a run,
+    // then the T rows; K|V rows per target layer of the run
+    const long long kt = std::max(1, m.cfg.target_layers);
+    ia(B.XN, std::max(R, kt * B.n_events + T) * m.d, el);
     ia(B.P, R * pw, el);
-    ia(B.KV, R * 2 * m.gd, el);
+    ia(B.KV, kt * R * 2 * m.gd, el);
     ia(B.UQ, T * 2 * m.hd, el);
     ia(B.A, R * m.hd, el);
     ia(B.Gt, R * m.hd, el);
@@ -1151,7 +1166,34 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
     float* X = B.X.as<float>();
     if constexpr (kTc) {
         std::vector<TcProblem> p1, p2;
+        // sequence sources with one k-block of embeddings: fused MLP (tok_tc.cuh)
+        static const bool tok_fused = std::getenv("MTFM_TOK_FUSED") == nullptr ||
+                                      std::atoi(std::getenv("MTFM_TOK_FUSED")) != 0;
+        TokArgs ta{};
+        std::vector<int> fused_src;
+        if (tok_fused && d == 256) {
+            for (int s = 0; s < n_src && ta.n_src < kTokMaxSrc; ++s) {
+                const auto& si = m.sources[s];
+                const int M = static_cast<int>(B.src_cnt[s]);
+                if (si.k_pad > 64 || M == 0) continue;
+                const auto& w = *m.srcw[s];
+                TokSource& ts = ta.s[ta.n_src++];
+                ts.tma_e = tma_2d(E + B.emb_base[s], M, si.k_pad, si.k_pad, 64, 128, 128);
+                ts.tma_w1 = tma_2d(w.t1.p, 2 * d, si.k_pad, si.k_pad, 64, 64, 128);
+                ts.tma_w2 = tma_2d(w.t2.p, d, 2 * d, 2 * d, 64, 256, 128);
+                ts.tma_b1 = tma_2d(BT.get(w.b1.as<float>(), 2 * d, st), 2 * d, 16, 16, 16, 64, 32);
+                ts.tma_b2 = tma_2d(BT.get(w.b2.as<float>(), d, st), d, 16, 16, 16, 256, 32);
+                ts.row_map = rm.src_rows + B.src_base[s];
+                ts.M = M;
+                ts.k_steps = static_cast<int>(cdiv(si.k_pad, 16));
+                ts.tile_start = ta.n_tiles;
+                ta.n_tiles += static_cast<int>(cdiv(M, 128));
+                fused_src.push_back(s);
+            }
+            ta.X = X;
+        }
         for (int s = 0; s < n_src; ++s) {
+            if (std::find(fused_src.begin(), fused_src.end(), s) != fused_src.end()) continue;
             const auto& si = m.sources[s];
             const auto& w = *m.srcw[s];
             const int M = static_cast<int>(B.src_cnt[s]);
@@ -1159,6 +1201,11 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                           EPI_SILU_BF16, w.b1.as<float>(), HID + B.hid_base[s], 2 * d, nullptr, 0, nullptr});
             p2.push_back({HID + B.hid_base[s], 2 * d, w.t2.as<__nv_bfloat16>(), 2 * d, M, d, 2 * d, EPI_BIAS_F32,
                           w.b2.as<float>(), X, d, rm.src_rows + B.src_base[s], 0, nullptr});
+        }
+        if (ta.n_tiles > 0) {
+            StageScope sc(m, "tok_fused", tok_f1 + tok_f2, tok_in * el + Rd * d * 4);
+            launch_tok_fused(ta, st);
+            ++L;
         }
         {
             StageScope sc(m, "tok_mlp1", tok_f1, tok_in * el + Rd * 2 * d * el);
@@ -1223,7 +1270,9 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
     if constexpr (kTc) {
         // bf16 tensor-core path: GLN1 and the gate are fused into the GEMM A producers
         bool ctx_stats_valid = false;  // X context rows only change in full layers
-        for (const auto& Lw : m.layers) {
+        int tl = 0;                     // index of the current target layer within its run
+        for (size_t li = 0; li < m.layers.size(); ++li) {
+            const auto& Lw = m.layers[li];
             if (m.fuse & 1) {
                 const long long r0 = ctx_stats_valid ? NE : 0;
                 StageScope sc(m, "row_stats", 0, (Rd - r0) * d * 4.0);
@@ -1311,19 +1360,55 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                 ctx_stats_valid = false;
             } else {
                 // target layer (hta.hpp:158-184): T rows only; H/R rows untouched
+                T* KVl = KV;  // this layer's K|V rows (context rows first, then T rows)
                 if (!(m.fuse & 1)) {
+                    // The context rows X[0, NE) are the same for every target layer of a
+                    // run (only T rows change), so at the first layer of the run their
+                    // GLN1 is computed once for all the run's layers and their K|V
+                    // projections go out in one grouped GEMM.
+                    if (li == 0 || !m.layers[li - 1]->target) {
+                        size_t lj = li;
+                        while (lj < m.layers.size() && m.layers[lj]->target) ++lj;
+                        const int kt = static_cast<int>(lj - li);
+                        for (int c0 = 0; c0 < kt; c0 += kMaxGlnCopies) {
+                            GlnCopies gc{};
+                            gc.n = std::min(kt - c0, kMaxGlnCopies);
+                            for (int c = 0; c < gc.n; ++c) {
+                                gc.gain[c] = m.layers[li + c0 + c]->g1g.as<float>();
+                                gc.bias[c] = m.layers[li + c0 + c]->g1b.as<float>();
+                                gc.out[c] = XN + static_cast<long long>(c0 + c) * NE * d;
+                            }
+                            StageScope sc(m, "gln1", 0, NE * d * (4.0 + gc.n * el));
+                            launch_gln_multi_bf16(X, d, NE, d, rm.src, gc, eps, d, st);
+                            ++L;
+                        }
+                        std::vector<TcProblem> kvp;
+                        for (int c = 0; c < kt; ++c) {
+                            const auto& Lc = m.layers[li + c];
+                            kvp.push_back({XN + static_cast<long long>(c) * NE * d, d, Lc->tkv.as<__nv_bfloat16>(), d,
+                                           static_cast<int>(NE), 2 * gd, d, EPI_SILU_BF16, Lc->bkv.as<float>(),
+                                           KV + static_cast<long long>(c) * R * 2 * gd, 2 * gd, nullptr, 0, nullptr});
+                        }
+                        StageScope sc(m, "proj_ctx_kv", 2.0 * kt * NE * d * 2 * gd,
+                                      kt * NE * (d + 2.0 * gd) * el);
+                        run_gemm_tc(kvp, st, L, BT);
+                        tl = 0;
+                    }
+                    KVl = KV + static_cast<long long>(tl) * R * 2 * gd;
+                    T* XNT = XN + static_cast<long long>(m.cfg.target_layers) * NE * d;
                     {
-                        StageScope sc(m, "gln1", 0, Rd * d * (4 + el));
-                        launch_gln<T>(X, d, 0, R, d, rm.src, Lw->g1g.as<float>(), Lw->g1b.as<float>(), eps, XN, d, st);
+                        StageScope sc(m, "gln1", 0, Td * d * (4 + el));
+                        launch_gln<T>(X, d, NE, NT, d, rm.src, Lw->g1g.as<float>(), Lw->g1b.as<float>(), eps, XNT, d,
+                                      st);
                         ++L;
                     }
-                    StageScope sc(m, "proj_target", 2.0 * (Rd * d * 2 * gd + Td * d * 2 * hd),
-                                  Rd * d * el + Rd * 2 * gd * el + Td * 2 * hd * el);
-                    run_gemm_tc({{XN, d, Lw->tkv.as<__nv_bfloat16>(), d, static_cast<int>(R), 2 * gd, d, EPI_SILU_BF16,
-                                  Lw->bkv.as<float>(), KV, 2 * gd, nullptr, 0, nullptr},
-                                 {XN + NE * d, d, Lw->t1.as<__nv_bfloat16>(), d, static_cast<int>(NT), 2 * hd, d,
+                    StageScope sc(m, "proj_target", 2.0 * Td * d * (2 * gd + 2 * hd), Td * d * el + Td * (2 * gd + 2 * hd) * el);
+                    run_gemm_tc({{XNT, d, Lw->tkv.as<__nv_bfloat16>(), d, static_cast<int>(NT), 2 * gd, d, EPI_SILU_BF16,
+                                  Lw->bkv.as<float>(), KVl + NE * 2 * gd, 2 * gd, nullptr, 0, nullptr},
+                                 {XNT, d, Lw->t1.as<__nv_bfloat16>(), d, static_cast<int>(NT), 2 * hd, d,
                                   EPI_SILU_BF16, Lw->b1.as<float>(), UQ, 2 * hd, nullptr, 0, nullptr}},
                                 st, L, BT);
+                    ++tl;
                 } else {
                     StageScope sc(m, "proj_target", 2.0 * (Rd * d * 2 * gd + Td * d * 2 * hd),
                                   Rd * d * 4 + Rd * 2 * gd * el + Td * 2 * hd * el);
@@ -1363,7 +1448,7 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                     ap.q_self = rm.self + NE;
                     ap.q_ptr = UQ;
                     ap.ldq = 2 * hd;
-                    ap.kv_ptr = KV;
+                    ap.kv_ptr = KVl;
                     ap.ldkv = 2 * gd;
                     ap.out = A;
                     ap.ldo = hd;
