@@ -517,8 +517,36 @@ void launch_tok_fused(const TokArgs& a, cudaStream_t st) {
            "tok smem attr");
         attr = true;
     }
-    tok_fused_kernel<<<std::min(a.n_tiles, kNumSMs), 512, tok_detail::SMEM, st>>>(a);
+    TokArgs aa = a;
+    static unsigned long long* tr = nullptr;
+    const bool tracing = std::getenv("MTFM_TOK_TRACE") != nullptr;
+    if (tracing) {
+        if (!tr) ck(cudaMalloc(&tr, 1024 * 8), "trace alloc");
+        ck(cudaMemsetAsync(tr, 0, 1024 * 8, st), "trace clear");
+        aa.trace = tr;
+    }
+    tok_fused_kernel<<<std::min(a.n_tiles, kNumSMs), 512, tok_detail::SMEM, st>>>(aa);
     ck(cudaGetLastError(), "tok_fused launch");
+    if (tracing) {
+        unsigned long long h[1024];
+        ck(cudaMemcpyAsync(h, tr, sizeof(h), cudaMemcpyDeviceToHost, st), "trace fetch");
+        ck(cudaStreamSynchronize(st), "trace sync");
+        const unsigned long long t0 = h[0] ? h[0] : 1;
+        auto rel = [&](int i) { return h[i] ? static_cast<long long>(h[i] - t0) : -1LL; };
+        for (int t = 0; t < 3; ++t)
+            for (int c = 0; c < 8; ++c) {
+                const int b = 16 * (t * 8 + c);
+                std::fprintf(stderr, "t%d c%d g1: start %lld ready %lld | g2: start %lld ready %lld\n", t, c, rel(b),
+                             rel(b + 1), rel(b + 4), rel(b + 5));
+            }
+        for (int k = 0; k < 12; ++k)
+            std::fprintf(stderr, "silu k%d: g0 [%lld %lld %lld %lld] g1 [%lld %lld %lld %lld]\n", k, rel(512 + 8 * k),
+                         rel(513 + 8 * k), rel(514 + 8 * k), rel(515 + 8 * k), rel(516 + 8 * k), rel(517 + 8 * k),
+                         rel(518 + 8 * k), rel(519 + 8 * k));
+        for (int t = 0; t < 3; ++t)
+            std::fprintf(stderr, "y t%d: start %lld full %lld drained %lld\n", t, rel(900 + 4 * t), rel(901 + 4 * t),
+                         rel(902 + 4 * t));
+    }
 }
 
 struct TcProblem {
@@ -1181,7 +1209,7 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                 ts.tma_e = tma_2d(E + B.emb_base[s], M, si.k_pad, si.k_pad, 64, 128, 128);
                 ts.tma_w1 = tma_2d(w.t1.p, 2 * d, si.k_pad, si.k_pad, 64, 64, 128);
                 ts.tma_w2 = tma_2d(w.t2.p, d, 2 * d, 2 * d, 64, 256, 128);
-                ts.tma_b1 = tma_2d(BT.get(w.b1.as<float>(), 2 * d, st), 2 * d, 16, 16, 16, 64, 32);
+                ts.tma_b1 = tma_2d(BT.get(w.b1.as<float>(), 2 * d, st), 2 * d, 16, 16, 16, 256, 32);
                 ts.tma_b2 = tma_2d(BT.get(w.b2.as<float>(), d, st), d, 16, 16, 16, 256, 32);
                 ts.row_map = rm.src_rows + B.src_base[s];
                 ts.M = M;

@@ -16,10 +16,13 @@
 //
 // Roles (512 threads): warps 0..7 SiLU (two groups of 4, group g owns Hacc[g] /
 // Hb[g], i.e. chunks c = g mod 2), warps 8..11 Y epilogue, warp 12 TMEM
-// allocator, warp 14 TMA producer, warp 15 MMA issuer.
+// allocator + GEMM1 issuer, warp 13 W2 producer, warp 14 tile + W1 producer,
+// warp 15 GEMM2 issuer. Two producer and two MMA threads: one thread issues
+// a TMA load only every ~150-300 clk (scripts/ubench_tma.cu), and the
+// per-chunk barrier waits of one MMA thread would serialise both GEMMs.
 // TMEM columns: Y [0, 256), Hacc [256, 384), Hb [384, 448).
-// SMEM: 2 x tile stages (E tile 16 KB + b2 tile 8 KB), 3 x chunk stages
-// (W1 chunk 8 KB + W2 chunk 32 KB + b1 chunk 2 KB), ones tile, Y staging.
+// SMEM: 2 x tile stages (E tile 16 KB + b1 tile 16 KB + b2 tile 8 KB),
+// 3 x W1 chunk stages (8 KB), 3 x W2 chunk stages (32 KB), ones tile, Y staging.
 #pragma once
 
 #include "common.cuh"
@@ -33,7 +36,7 @@ struct TokSource {
     CUtensorMap tma_e;    // E_s [M][k_pad] bf16, box {64, 128}, SW128 (columns >= k_pad zero-filled)
     CUtensorMap tma_w1;   // W1^T [512][k_pad] bf16, box {64, 64}, SW128
     CUtensorMap tma_w2;   // W2^T [256][512] bf16, box {64, 256}, SW128
-    CUtensorMap tma_b1;   // b1 tile [512][16] bf16, box {16, 64}, SW32
+    CUtensorMap tma_b1;   // b1 tile [512][16] bf16, box {16, 256}, SW32
     CUtensorMap tma_b2;   // b2 tile [256][16] bf16, box {16, 256}, SW32
     const int* row_map;   // X row of source row m
     int M;                // rows
@@ -46,22 +49,27 @@ struct TokArgs {
     int n_src;
     int n_tiles;
     float* X;             // [rows][256] fp32
+    unsigned long long* trace;  // timing experiments only (-DMTFM_TOK_TRACE): CTA 0 clock stamps
 };
 
 namespace tok_detail {
 constexpr int BM = 128, D = 256, HC = 64, NCH = 8;  // rows per tile, d_model, hidden chunk, chunks
 constexpr int E_BYTES = BM * 64 * 2;                // 16 KB
+constexpr int B1_BYTES = 2 * D * 32;                // 16 KB: b1 tile [512][16]
 constexpr int B2_BYTES = D * 32;                    // 8 KB
-constexpr int XS_BYTES = E_BYTES + B2_BYTES;        // tile stage
+constexpr int XS_BYTES = E_BYTES + B1_BYTES + B2_BYTES;  // tile stage
 constexpr int W1_BYTES = HC * 64 * 2;               // 8 KB
 constexpr int W2_BYTES = D * 64 * 2;                // 32 KB
-constexpr int B1_BYTES = HC * 32;                   // 2 KB
-constexpr int WS_BYTES = 43 * 1024;                 // chunk stage (42 KB used)
 constexpr int kXStages = 2, kWStages = 3;
 constexpr int ONES_BYTES = 4096;
-constexpr int STG_BYTES = 4 * 32 * 32 * 4;          // Y staging, one 32 x 32 fp32 block per Y warp
+constexpr int STG_BYTES = 12 * 32 * 8 * 4;          // Y drain staging: 32 rows x 8 fp32 per epilogue warp
+#ifndef MTFM_TOK_DRAIN_SLOTS
+#define MTFM_TOK_DRAIN_SLOTS 1
+#endif
+constexpr int kDrainSlots = MTFM_TOK_DRAIN_SLOTS;   // 1: the 4 Y warps drain Y; 3: the SiLU warps help
 constexpr int BAR_BYTES = 1024;
-constexpr int SMEM = 1024 + kXStages * XS_BYTES + kWStages * WS_BYTES + ONES_BYTES + STG_BYTES + BAR_BYTES;
+constexpr int SMEM = 1024 + kXStages * XS_BYTES + kWStages * (W1_BYTES + W2_BYTES) + ONES_BYTES + STG_BYTES +
+                     BAR_BYTES;
 static_assert(SMEM <= 227 * 1024, "tok SMEM budget");
 constexpr uint32_t Y_COL = 0, HACC_COL = 256, HB_COL = 384;
 
@@ -79,24 +87,34 @@ __global__ void __launch_bounds__(512, 1) tok_fused_kernel(const __grid_constant
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* xs = base;                                  // tile stages
-    uint8_t* ws = xs + kXStages * XS_BYTES;              // chunk stages
-    uint8_t* ones = ws + kWStages * WS_BYTES;
+    uint8_t* w1s = xs + kXStages * XS_BYTES;             // W1 chunk stages
+    uint8_t* w2s = w1s + kWStages * W1_BYTES;            // W2 chunk stages
+    uint8_t* ones = w2s + kWStages * W2_BYTES;
     float* stg = reinterpret_cast<float*>(ones + ONES_BYTES);
     uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(stg) + STG_BYTES);
     uint64_t* x_full = bars;             // [2]
     uint64_t* x_empty = bars + 2;        // [2]
-    uint64_t* w_full = bars + 4;         // [3]
-    uint64_t* w_empty = bars + 7;        // [3]
+    uint64_t* w1_full = bars + 4;        // [3]
+    uint64_t* w1_empty = bars + 7;       // [3]
     uint64_t* hacc_full = bars + 10;     // [2]
     uint64_t* hacc_empty = bars + 12;    // [2]
     uint64_t* hb_full = bars + 14;       // [2]
     uint64_t* hb_empty = bars + 16;      // [2]
     uint64_t* y_full = bars + 18;
     uint64_t* y_empty = bars + 19;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
+    uint64_t* w2_full = bars + 20;       // [3]
+    uint64_t* w2_empty = bars + 23;      // [3]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 26);
 
     const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
-    constexpr uint32_t kWarpMma = 15, kWarpTma = 14, kWarpAlloc = 12;
+#ifdef MTFM_TOK_TRACE
+    auto trace = [&](int slot) {
+        if (args.trace && blockIdx.x == 0 && lane == 0 && slot < 1024) args.trace[slot] = clock64();
+    };
+#else
+    auto trace = [&](int) {};
+#endif
+    constexpr uint32_t kWarpMma = 15, kWarpTma = 14, kWarpTmaW2 = 13, kWarpAlloc = 12;
 
     for (int i = threadIdx.x; i < ONES_BYTES / 16; i += blockDim.x)
         reinterpret_cast<uint4*>(ones)[i] = make_uint4(0x3f803f80u, 0u, 0u, 0u);
@@ -104,18 +122,20 @@ __global__ void __launch_bounds__(512, 1) tok_fused_kernel(const __grid_constant
     if (warp == kWarpTma && lane == 0) {
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&x_full[i], 1);
-            ptx::mbar_init(&x_empty[i], 1);
+            ptx::mbar_init(&x_empty[i], 2);  // GEMM1 warp (E, b1) + GEMM2 warp (b2)
             ptx::mbar_init(&hacc_full[i], 1);
             ptx::mbar_init(&hacc_empty[i], 4);
             ptx::mbar_init(&hb_full[i], 4);
             ptx::mbar_init(&hb_empty[i], 1);
         }
         for (int i = 0; i < kWStages; ++i) {
-            ptx::mbar_init(&w_full[i], 1);
-            ptx::mbar_init(&w_empty[i], 1);
+            ptx::mbar_init(&w1_full[i], 1);
+            ptx::mbar_init(&w1_empty[i], 1);
+            ptx::mbar_init(&w2_full[i], 1);
+            ptx::mbar_init(&w2_empty[i], 1);
         }
         ptx::mbar_init(y_full, 1);
-        ptx::mbar_init(y_empty, 4);
+        ptx::mbar_init(y_empty, 4 * kDrainSlots);  // every draining warp arrives
         ptx::fence_mbar_init();
         for (int i = 0; i < args.n_src; ++i) {
             ptx::tma_prefetch(&args.s[i].tma_e);
@@ -129,6 +149,59 @@ __global__ void __launch_bounds__(512, 1) tok_fused_kernel(const __grid_constant
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
+    // Y drain, shared by all 12 epilogue warps once a tile's GEMM2 is done:
+    // warp (quarter q, slot ds of 3) takes column blocks cb = ds, ds + 3, ...
+    // of its 32 rows; each 32 x 8 fp32 sub-block goes through a 1 KB staging
+    // slot (lane = row on the way in, 2 lanes per row on the way out) so every
+    // global store writes whole 32 B sectors of 16 rows. Y is handed back to the
+    // GEMM2 warp as soon as the TMEM reads are done.
+    auto drain = [&](uint32_t n_t, int t, uint32_t q, int ds, int slot, int nslots) {
+        int s, m0;
+        tok_detail::decode(args, t, s, m0);
+        const TokSource& src = args.s[s];
+        float* sbuf = stg + slot * 32 * 8;
+        const int half = lane & 1;       // 16 B half of a 32 B row segment (store phase)
+        long long orow[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int m = m0 + static_cast<int>(q * 32) + 16 * j + (lane >> 1);
+            orow[j] = m < src.M ? static_cast<long long>(__ldg(src.row_map + m)) : -1;
+        }
+        const uint32_t lane_addr = (q * 32u) << 16;
+        ptx::mbar_wait(y_full, n_t & 1);
+        ptx::tc_fence_after();
+#pragma unroll 1
+        for (int cb = ds; cb < D / 32; cb += nslots) {
+            float v[32];
+            ptx::tmem_ld16(tmem + lane_addr + Y_COL + cb * 32, *reinterpret_cast<float(*)[16]>(v));
+            ptx::tmem_ld16(tmem + lane_addr + Y_COL + cb * 32 + 16, *reinterpret_cast<float(*)[16]>(v + 16));
+            ptx::tmem_ld_wait();
+            if (cb + nslots >= D / 32) {
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(y_empty);  // Y is free for the next tile's GEMM2
+            }
+#pragma unroll
+            for (int sb8 = 0; sb8 < 4; ++sb8) {
+                // row r = lane: chunk h (16 B) of its 32 B segment at (h ^ (r >> 2 & 1))
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+                    *reinterpret_cast<float4*>(sbuf + lane * 8 + ((h ^ ((lane >> 2) & 1)) << 2)) =
+                        make_float4(v[8 * sb8 + 4 * h], v[8 * sb8 + 4 * h + 1], v[8 * sb8 + 4 * h + 2],
+                                    v[8 * sb8 + 4 * h + 3]);
+                __syncwarp();
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const int r = 16 * j + (lane >> 1);
+                    const float4 w = *reinterpret_cast<const float4*>(sbuf + r * 8 + ((half ^ ((r >> 2) & 1)) << 2));
+                    if (orow[j] >= 0)
+                        __stcs(reinterpret_cast<float4*>(args.X + orow[j] * D + cb * 32 + sb8 * 8 + 4 * half), w);
+                }
+                __syncwarp();
+            }
+        }
+    };
+
     if (warp == kWarpTma) {
         // ------------------------------------------------ TMA producer
         if (ptx::elect_one()) {
@@ -139,54 +212,79 @@ __global__ void __launch_bounds__(512, 1) tok_fused_kernel(const __grid_constant
                 const TokSource& src = args.s[s];
                 const uint32_t xb = n_t & 1;
                 ptx::mbar_wait(&x_empty[xb], ((n_t >> 1) & 1) ^ 1);
+                uint8_t* xst = xs + xb * XS_BYTES;
                 ptx::mbar_arrive_expect_tx(&x_full[xb], XS_BYTES);
-                ptx::tma_load_2d(xs + xb * XS_BYTES, &src.tma_e, &x_full[xb], 0, m0);
-                ptx::tma_load_2d(xs + xb * XS_BYTES + E_BYTES, &src.tma_b2, &x_full[xb], 0, 0);
+                ptx::tma_load_2d(xst, &src.tma_e, &x_full[xb], 0, m0);
+                ptx::tma_load_2d(xst + E_BYTES, &src.tma_b1, &x_full[xb], 0, 0);
+                ptx::tma_load_2d(xst + E_BYTES + B1_BYTES / 2, &src.tma_b1, &x_full[xb], 0, 256);
+                ptx::tma_load_2d(xst + E_BYTES + B1_BYTES, &src.tma_b2, &x_full[xb], 0, 0);
                 for (int c = 0; c < NCH; ++c, ++n_w) {
                     const uint32_t wb = n_w % kWStages;
-                    ptx::mbar_wait(&w_empty[wb], ((n_w / kWStages) & 1) ^ 1);
-                    uint8_t* st = ws + wb * WS_BYTES;
-                    ptx::mbar_arrive_expect_tx(&w_full[wb], W1_BYTES + W2_BYTES + B1_BYTES);
-                    ptx::tma_load_2d(st, &src.tma_w1, &w_full[wb], 0, c * HC);
-                    ptx::tma_load_2d(st + W1_BYTES, &src.tma_w2, &w_full[wb], c * HC, 0);
-                    ptx::tma_load_2d(st + W1_BYTES + W2_BYTES, &src.tma_b1, &w_full[wb], 0, c * HC);
+                    ptx::mbar_wait(&w1_empty[wb], ((n_w / kWStages) & 1) ^ 1);
+                    ptx::mbar_arrive_expect_tx(&w1_full[wb], W1_BYTES);
+                    ptx::tma_load_2d(w1s + wb * W1_BYTES, &src.tma_w1, &w1_full[wb], 0, c * HC);
+                }
+            }
+        }
+    } else if (warp == kWarpTmaW2) {
+        // ------------------------------------------------ W2 producer
+        if (ptx::elect_one()) {
+            uint32_t n_w = 0;
+            for (int t = blockIdx.x; t < args.n_tiles; t += gridDim.x) {
+                int s, m0;
+                decode(args, t, s, m0);
+                const TokSource& src = args.s[s];
+                for (int c = 0; c < NCH; ++c, ++n_w) {
+                    const uint32_t wb = n_w % kWStages;
+                    ptx::mbar_wait(&w2_empty[wb], ((n_w / kWStages) & 1) ^ 1);
+                    ptx::mbar_arrive_expect_tx(&w2_full[wb], W2_BYTES);
+                    ptx::tma_load_2d(w2s + wb * W2_BYTES, &src.tma_w2, &w2_full[wb], c * HC, 0);
                 }
             }
         }
     } else if (warp == kWarpMma) {
-        // ------------------------------------------------ MMA issuer
-        const uint32_t idesc1 = ptx::instr_desc_bf16(128, HC, false, false);
+        // ------------------------------------------------ GEMM2 issuer: Y += Hb . W2_c^T (+ b2)
         const uint32_t idesc2 = ptx::instr_desc_bf16(128, D, false, false);
         const uint64_t ones_desc = ptx::smem_desc(ptx::smem_u32(ones), 16, 256, 6);
-        uint32_t n_t = 0, n_w = 0, n_h = 0;  // tiles, chunk stages, hidden chunks (= n_w)
-        // GEMM2 of hidden chunk h (stage wb) for tile n_t; c = chunk within the tile
-        auto gemm2 = [&](uint32_t h, uint32_t wb, int c, const uint8_t* xst) {
-            const uint32_t hb = h & 1;
-            if (c == 0) {
-                ptx::mbar_wait(y_empty, (n_t & 1) ^ 1);  // the previous tile's Y has been read out
+        uint32_t n_t = 0, h = 0;
+        for (int t = blockIdx.x; t < args.n_tiles; t += gridDim.x, ++n_t) {
+            const uint32_t xb = n_t & 1;
+            uint8_t* xst = xs + xb * XS_BYTES;
+            ptx::mbar_wait(&x_full[xb], (n_t >> 1) & 1);         // b2 tile
+            ptx::mbar_wait(y_empty, (n_t & 1) ^ 1);              // the previous tile's Y has been read out
+            for (int c = 0; c < NCH; ++c, ++h) {
+                const uint32_t hb = h & 1, wb = h % kWStages;
+                trace(16 * (n_t * 8 + c) + 4);
+                ptx::mbar_wait(&hb_full[hb], (h >> 1) & 1);
+                ptx::mbar_wait(&w2_full[wb], (h / kWStages) & 1);
+                trace(16 * (n_t * 8 + c) + 5);
                 ptx::tc_fence_after();
-            }
-            ptx::mbar_wait(&hb_full[hb], (h >> 1) & 1);
-            ptx::tc_fence_after();
-            if (ptx::elect_one()) {
-                const uint32_t w2 = ptx::smem_u32(ws + wb * WS_BYTES + W1_BYTES);
+                if (ptx::elect_one()) {
+                    const uint32_t w2 = ptx::smem_u32(w2s + wb * W2_BYTES);
 #pragma unroll
-                for (int k = 0; k < HC / 16; ++k)
-                    ptx::umma_bf16_ts(tmem + Y_COL, tmem + HB_COL + hb * (HC / 2) + k * 8,
-                                      ptx::smem_desc(w2 + k * 32, 16, 1024, 2), idesc2, (c > 0 || k > 0) ? 1u : 0u);
-                if (c == NCH - 1) {
-                    ptx::umma_bf16(tmem + Y_COL, ones_desc,
-                                   ptx::smem_desc(ptx::smem_u32(xst + E_BYTES), 16, 256, 6), idesc2, 1u);
+                    for (int k = 0; k < HC / 16; ++k)
+                        ptx::umma_bf16_ts(tmem + Y_COL, tmem + HB_COL + hb * (HC / 2) + k * 8,
+                                          ptx::smem_desc(w2 + k * 32, 16, 1024, 2), idesc2, (c > 0 || k > 0) ? 1u : 0u);
+                    if (c == NCH - 1)
+                        ptx::umma_bf16(tmem + Y_COL, ones_desc,
+                                       ptx::smem_desc(ptx::smem_u32(xst + E_BYTES + B1_BYTES), 16, 256, 6), idesc2, 1u);
+                    ptx::umma_commit(&hb_empty[hb]);
+                    ptx::umma_commit(&w2_empty[wb]);
+                    if (c == NCH - 1) {
+                        ptx::umma_commit(&x_empty[xb]);  // b2 tile consumed (the GEMM1 warp releases E)
+                        ptx::umma_commit(y_full);
+                    }
                 }
-                ptx::umma_commit(&hb_empty[hb]);
-                ptx::umma_commit(&w_empty[wb]);
-                if (c == NCH - 1) {
-                    ptx::umma_commit(&x_empty[n_t & 1]);  // E tile and the b2 tile of this stage are consumed
-                    ptx::umma_commit(y_full);
-                }
+                __syncwarp();
             }
-            __syncwarp();
-        };
+        }
+    } else if (warp == kWarpAlloc) {
+        // ------------------------------------------------ GEMM1 issuer: Hacc = E . W1_c^T + b1_c
+        // (a second MMA-issuing warp: the per-chunk waits and issues of the two
+        // GEMMs overlap instead of adding up in one thread)
+        const uint32_t idesc1 = ptx::instr_desc_bf16(128, HC, false, false);
+        const uint64_t ones_desc = ptx::smem_desc(ptx::smem_u32(ones), 16, 256, 6);
+        uint32_t n_t = 0, h = 0;
         for (int t = blockIdx.x; t < args.n_tiles; t += gridDim.x, ++n_t) {
             int s, m0;
             tok_detail::decode(args, t, s, m0);
@@ -194,37 +292,40 @@ __global__ void __launch_bounds__(512, 1) tok_fused_kernel(const __grid_constant
             const uint32_t xb = n_t & 1;
             uint8_t* xst = xs + xb * XS_BYTES;
             ptx::mbar_wait(&x_full[xb], (n_t >> 1) & 1);
-            uint32_t prev_wb = 0;
-            for (int c = 0; c < NCH; ++c, ++n_w, ++n_h) {
-                const uint32_t wb = n_w % kWStages, hb = n_h & 1;
-                // GEMM1 chunk c -> Hacc[hb]
-                ptx::mbar_wait(&w_full[wb], (n_w / kWStages) & 1);
-                ptx::mbar_wait(&hacc_empty[hb], ((n_h >> 1) & 1) ^ 1);
+            for (int c = 0; c < NCH; ++c, ++h) {
+                const uint32_t wb = h % kWStages, hb = h & 1;
+                trace(16 * (n_t * 8 + c) + 0);
+                ptx::mbar_wait(&w1_full[wb], (h / kWStages) & 1);
+                ptx::mbar_wait(&hacc_empty[hb], ((h >> 1) & 1) ^ 1);
+                trace(16 * (n_t * 8 + c) + 1);
                 ptx::tc_fence_after();
                 if (ptx::elect_one()) {
-                    const uint32_t e = ptx::smem_u32(xst), w1 = ptx::smem_u32(ws + wb * WS_BYTES);
+                    const uint32_t e = ptx::smem_u32(xst), w1 = ptx::smem_u32(w1s + wb * W1_BYTES);
                     for (int k = 0; k < k_steps; ++k)
                         ptx::umma_bf16(tmem + HACC_COL + hb * HC, ptx::smem_desc(e + k * 32, 16, 1024, 2),
                                        ptx::smem_desc(w1 + k * 32, 16, 1024, 2), idesc1, k > 0 ? 1u : 0u);
+                    // + b1 rows [64c, 64c + 64) of the tile's b1 tile (SW32, 256 B per 8 rows)
                     ptx::umma_bf16(tmem + HACC_COL + hb * HC, ones_desc,
-                                   ptx::smem_desc(w1 + W1_BYTES + W2_BYTES, 16, 256, 6), idesc1, 1u);
+                                   ptx::smem_desc(ptx::smem_u32(xst + E_BYTES) + c * HC * 32, 16, 256, 6), idesc1, 1u);
                     ptx::umma_commit(&hacc_full[hb]);
+                    ptx::umma_commit(&w1_empty[wb]);
+                    if (c == NCH - 1) ptx::umma_commit(&x_empty[xb]);  // E and b1 tiles consumed
                 }
                 __syncwarp();
-                // GEMM2 of the previous chunk overlaps the SiLU of this one
-                if (c > 0) gemm2(n_h - 1, prev_wb, c - 1, xst);
-                prev_wb = wb;
             }
-            gemm2(n_h - 1, prev_wb, NCH - 1, xst);
         }
     } else if (warp < 8) {
         // ------------------------------------------------ SiLU warps: Hacc -> silu -> bf16 Hb
         const uint32_t q = warp & 3, g = warp >> 2;
         const uint32_t lane_addr = (q * 32u) << 16;
         uint32_t k = 0;  // chunks of this group
-        for (int t = blockIdx.x; t < args.n_tiles; t += gridDim.x) {
+        uint32_t n_t = 0;
+        for (int t = blockIdx.x; t < args.n_tiles; t += gridDim.x, ++n_t) {
             for (int c = g; c < NCH; c += 2, ++k) {
+                const int sb = 512 + 8 * static_cast<int>(k) + 4 * static_cast<int>(g);
+                if (q == 0) trace(sb + 0);
                 ptx::mbar_wait(&hacc_full[g], k & 1);
+                if (q == 0) trace(sb + 1);
                 ptx::tc_fence_after();
                 uint32_t packed[HC / 2];
 #pragma unroll
@@ -239,8 +340,10 @@ __global__ void __launch_bounds__(512, 1) tok_fused_kernel(const __grid_constant
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&hacc_empty[g]);
+                if (q == 0) trace(sb + 2);
                 // Hb[g] must have been consumed by GEMM2 of this group's previous chunk
                 ptx::mbar_wait(&hb_empty[g], (k & 1) ^ 1);
+                if (q == 0) trace(sb + 3);
                 ptx::tc_fence_after();
                 ptx::tmem_st16(tmem + lane_addr + HB_COL + g * (HC / 2), *reinterpret_cast<uint32_t(*)[16]>(packed));
                 ptx::tmem_st16(tmem + lane_addr + HB_COL + g * (HC / 2) + 16,
@@ -250,55 +353,13 @@ __global__ void __launch_bounds__(512, 1) tok_fused_kernel(const __grid_constant
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&hb_full[g]);
             }
+            if (kDrainSlots == 3) drain(n_t, t, q, static_cast<int>(g), static_cast<int>(warp), 3);
         }
     } else if (warp < 12) {
-        // ------------------------------------------------ Y epilogue: TMEM -> X rows (fp32)
-        const uint32_t q = warp & 3;
-        const uint32_t lane_addr = (q * 32u) << 16;
-        float* sb = stg + q * 32 * 32;
-        const int sub = lane >> 3, ch = lane & 7;
+        // ------------------------------------------------ Y epilogue (third drain slot)
         uint32_t n_t = 0;
-        for (int t = blockIdx.x; t < args.n_tiles; t += gridDim.x, ++n_t) {
-            int s, m0;
-            tok_detail::decode(args, t, s, m0);
-            const TokSource& src = args.s[s];
-            const int rbase = m0 + q * 32;
-            int orow[8];
-#pragma unroll
-            for (int gg = 0; gg < 8; ++gg) {
-                const int m = rbase + 4 * gg + sub;
-                orow[gg] = m < src.M ? __ldg(src.row_map + m) : -1;
-            }
-            ptx::mbar_wait(y_full, n_t & 1);
-            ptx::tc_fence_after();
-#pragma unroll 1
-            for (int cb = 0; cb < D / 32; ++cb) {
-                float v[32];
-                ptx::tmem_ld16(tmem + lane_addr + Y_COL + cb * 32, *reinterpret_cast<float(*)[16]>(v));
-                ptx::tmem_ld16(tmem + lane_addr + Y_COL + cb * 32 + 16, *reinterpret_cast<float(*)[16]>(v + 16));
-                ptx::tmem_ld_wait();
-                if (cb == D / 32 - 1) {
-                    ptx::tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(y_empty);  // Y is free for the next tile's GEMM2
-                }
-                // 32 x 32 block through XOR-swizzled SMEM: lane = row on the way in,
-                // 4 rows x 128 B per warp store on the way out
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk)
-                    *reinterpret_cast<float4*>(sb + lane * 32 + ((kk ^ (lane & 7)) << 2)) =
-                        make_float4(v[4 * kk], v[4 * kk + 1], v[4 * kk + 2], v[4 * kk + 3]);
-                __syncwarp();
-#pragma unroll
-                for (int gg = 0; gg < 8; ++gg) {
-                    const int r = 4 * gg + sub;
-                    const float4 w = *reinterpret_cast<const float4*>(sb + r * 32 + ((ch ^ (r & 7)) << 2));
-                    if (orow[gg] >= 0)
-                        __stcs(reinterpret_cast<float4*>(args.X + static_cast<long long>(orow[gg]) * D + cb * 32 + 4 * ch), w);
-                }
-                __syncwarp();
-            }
-        }
+        for (int t = blockIdx.x; t < args.n_tiles; t += gridDim.x, ++n_t)
+            drain(n_t, t, warp & 3, kDrainSlots - 1, static_cast<int>(warp), kDrainSlots);
     }
     ptx::tc_fence_before();
     __syncthreads();
