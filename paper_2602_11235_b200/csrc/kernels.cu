@@ -729,8 +729,125 @@ __global__ void __launch_bounds__(256) heads_kernel(HeadArgs a) {
         }
     }
 }
-void launch_heads(const HeadArgs& a, cudaStream_t st) {
+// Fast path: one warp per target with everything per-target in registers and
+// the small per-model tables (expert bias, gate bias, tower weights) in SMEM.
+// Lane l owns columns 4l + 128j (j < NJ) of every expert: the expert
+// pre-activations are read as coalesced float4 rows, SiLU'd once, and every
+// task's gate mix and tower dot product reuse them.
+template <int E, int NJ>
+__global__ void __launch_bounds__(256) heads_fast_kernel(HeadArgs a, int n_tasks_total) {
+    extern __shared__ float hsm[];
+    const int de = NJ * 128;
+    float* s_eb = hsm;                          // [E*de]
+    float* s_tw = s_eb + E * de;                // [n_tasks_total*de]
+    float* s_gb = s_tw + n_tasks_total * de;    // [n_tasks_total*E]
+    float* s_tb = s_gb + n_tasks_total * E;     // [n_tasks_total]
+    for (int i = threadIdx.x; i < E * de; i += blockDim.x) s_eb[i] = a.exp_bias[i];
+    for (int i = threadIdx.x; i < n_tasks_total * de; i += blockDim.x) s_tw[i] = a.tower_w[i];
+    for (int i = threadIdx.x; i < n_tasks_total * E; i += blockDim.x) s_gb[i] = a.gate_bias[i];
+    for (int i = threadIdx.x; i < n_tasks_total; i += blockDim.x) s_tb[i] = a.tower_b[i];
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long t = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); t < a.n_t; t += warps) {
+        const int scen = a.t_scen[t];
+        int s = -1;
+        for (int i = 0; i < a.n_src; ++i)
+            if (a.src[i].kind == 2 && a.src[i].id == scen) s = i;
+        if (s < 0) continue;  // reported by the plan
+        const int task0 = a.src[s].task0, ntasks = a.src[s].ntasks;
+        const float* y = a.y + t * a.ldy;
+        float act[E][NJ][4];
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) {
+                const int c = 4 * lane + 128 * j;
+                const float4 v = __ldcs(reinterpret_cast<const float4*>(y + e * de + c));
+                const float4 b = *reinterpret_cast<const float4*>(s_eb + e * de + c);
+                const float pre[4] = {v.x + b.x, v.y + b.y, v.z + b.z, v.w + b.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    if (a.precise) {
+                        act[e][j][i] = silu_precise(pre[i]);
+                    } else {
+                        const float h = 0.5f * pre[i];
+                        float th;
+                        asm("tanh.approx.f32 %0, %1;" : "=f"(th) : "f"(h));
+                        act[e][j][i] = fmaf(h, th, h);
+                    }
+                }
+            }
+        for (int k = 0; k < ntasks; ++k) {
+            const int task = task0 + k;
+            // softmax over the E gate logits (every lane; sequential sum as softmax_rows)
+            float g[E], mx = -INFINITY;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                g[e] = y[E * de + task * E + e] + s_gb[task * E + e];
+                mx = fmaxf(mx, g[e]);
+            }
+            float sum = 0.f;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                g[e] = expf(g[e] - mx);
+                sum += g[e];
+            }
+            const float inv = __fdiv_rn(1.f, sum);
+            float z = 0.f;
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) {
+                const float4 w = *reinterpret_cast<const float4*>(s_tw + task * de + 4 * lane + 128 * j);
+                const float wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    float m = 0.f;
+#pragma unroll
+                    for (int e = 0; e < E; ++e) m += act[e][j][i] * (g[e] * inv);
+                    z += m * wv[i];
+                }
+            }
+            const float zz = warp_sum(z) + s_tb[task];
+            if (lane == 0) {
+                const long long r = a.t_rec0[t] + (long long)k * a.t_rec_stride[t];
+                double p = static_cast<double>(sigmoid_precise(zz));
+                p = p < 1e-12 ? 1e-12 : (p > 1.0 - 1e-12 ? 1.0 - 1e-12 : p);
+                a.rec_user[r] = a.user_id[a.t_user[t]];
+                a.rec_scen[r] = scen;
+                a.rec_exp[r] = a.t_exp_ref[t];
+                a.rec_task[r] = k;
+                if (a.rec_logit) a.rec_logit[r] = zz;
+                a.rec_prob[r] = p;
+            }
+        }
+    }
+}
+
+template <int E, int NJ>
+bool try_heads_fast(const HeadArgs& a, int n_tasks_total, cudaStream_t st) {
+    if (a.E != E || a.de != NJ * 128) return false;
+    const size_t smem = sizeof(float) * (static_cast<size_t>(E) * a.de + static_cast<size_t>(n_tasks_total) * a.de +
+                                         static_cast<size_t>(n_tasks_total) * E + n_tasks_total);
+    if (smem > 160 * 1024) return false;
+    static int attr_set = 0;
+    if (static_cast<int>(smem) > attr_set) {
+        cudaFuncSetAttribute(heads_fast_kernel<E, NJ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+        attr_set = static_cast<int>(smem);
+    }
+    const int blocks = static_cast<int>(std::min<long long>(cdiv(a.n_t, 8), 148ll * 4));
+    heads_fast_kernel<E, NJ><<<blocks, 256, smem, st>>>(a, n_tasks_total);
+    return true;
+}
+
+void launch_heads(const HeadArgs& a, cudaStream_t st, int n_tasks_total) {
     if (a.n_t == 0) return;
+    if (n_tasks_total > 0 &&
+        (try_heads_fast<4, 1>(a, n_tasks_total, st) || try_heads_fast<4, 2>(a, n_tasks_total, st) ||
+         try_heads_fast<4, 4>(a, n_tasks_total, st) || try_heads_fast<2, 2>(a, n_tasks_total, st) ||
+         try_heads_fast<8, 2>(a, n_tasks_total, st) || try_heads_fast<3, 1>(a, n_tasks_total, st) ||
+         try_heads_fast<3, 2>(a, n_tasks_total, st)))
+        return;
     const int blocks = static_cast<int>(std::min<long long>(cdiv(a.n_t, 8), 148ll * 32));
     heads_kernel<<<blocks, 256, 0, st>>>(a);
 }

@@ -146,7 +146,7 @@ struct HeadArgs {
     float* rec_logit;
     double* rec_prob;
 };
-void launch_heads(const HeadArgs& a, cudaStream_t st);
+void launch_heads(const HeadArgs& a, cudaStream_t st, int n_tasks_total);  // n_tasks_total: rows of tower_w
 
 // ---------------------------------------------------------------- SIMT (check mode)
 struct SimtGemm {

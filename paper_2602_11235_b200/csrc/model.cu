@@ -1705,7 +1705,7 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
     {
         StageScope sc(m, "heads", 2.0 * B.n_records * m.cfg.experts * m.cfg.d_expert,
                       Td * m.head_ld * 4 + B.n_records * 32.0);
-        launch_heads(ha, st);
+        launch_heads(ha, st, m.n_tasks_total);
         ck(cudaGetLastError(), "heads launch");
         ++L;
     }
