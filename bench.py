@@ -263,6 +263,16 @@ def main():
         roof = {"bound": "hbm", "kernel": tname, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "traffic": None, "launches": tcnt, "per_launch_ms": tms / tcnt,
                 "algorithmic_per_launch": tby / tcnt, "share_of_step": tms / total_prof, "peak_kind": peak_kind}
+    if tname.startswith("attn") and tfl > 0:
+        # attention weights are silu(QK^T): one MUFU.TANH per visible (head, query, key) score,
+        # 4 * d_h flops each, against the SFU's 16 ops/clk/SM (scripts/ubench_silu.cu)
+        dh = wl.cfg.hta.d_model // wl.cfg.hta.heads
+        sfu_ops = tfl / (4.0 * dh)
+        sfu_peak = 16.0 * 148 * 1.965e9
+        sfu_ach = sfu_ops / (tms / 1000.0)
+        roof["sfu"] = {"achieved_Gops": sfu_ach / 1e9, "peak_Gops": sfu_peak / 1e9, "frac": sfu_ach / sfu_peak,
+                       "tensor_ceiling_frac": sfu_peak * 4.0 * dh / (tflops * 1e12),
+                       "note": "SFU-bound at this head dim: the tensor fraction cannot exceed tensor_ceiling_frac"}
     total_flops = sum(v[1] for v in stages.values())
     step_tflops = total_flops / (ms / 1000.0) / 1e12
     traffic_path = os.path.join(ROOT, "profiles", "traffic.json")
@@ -271,7 +281,10 @@ def main():
             with open(traffic_path) as f:
                 tr = json.load(f).get(args.config, {}).get(tname)
             if tr:
-                roof["traffic"] = tr
+                # dram__bytes_read.sum + dram__bytes_write.sum of one launch (ncu --set full)
+                roof["traffic"] = tr["dram_bytes_per_launch"] if isinstance(tr, dict) else tr
+                if isinstance(tr, dict):
+                    roof["traffic_source"] = tr.get("source")
         except Exception:
             pass
 
