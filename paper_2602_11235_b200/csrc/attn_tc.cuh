@@ -315,6 +315,10 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
                 if (__all_sync(0xffffffffu, nvalid >= CPW)) {
 #pragma unroll
                     for (int e = 0; e < CPW; e += 2) packed[e / 2] = attn_detail::silu2_bf16(v[e], v[e + 1]);
+                } else if (__all_sync(0xffffffffu, nvalid <= 0)) {
+                    // slice entirely beyond every row's prefix: no MUFU work
+#pragma unroll
+                    for (int e = 0; e < CPW / 2; ++e) packed[e] = 0u;
                 } else {
 #pragma unroll
                     for (int e = 0; e < CPW; e += 2) {
