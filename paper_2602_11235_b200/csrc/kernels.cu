@@ -1,5 +1,6 @@
 // kernels.cu — planning (K0), tokenizer gather (K1 prologue), group LayerNorm,
 // gate, heads (K5 epilogue) and the fp32 SIMT check-mode GEMM / attention.
+#include <type_traits>
 #include <climits>
 
 #include "common.cuh"
@@ -565,11 +566,97 @@ __global__ void __launch_bounds__(256) gate_kernel(const T* __restrict__ a, long
     }
 }
 
+// bf16, d == 256: lane owns 8 consecutive columns (one 16-byte load per tensor
+// and row) and each warp carries RPW rows at once, so 2*RPW independent loads
+// are in flight per warp instead of 2.
+template <int RPW>
+__global__ void __launch_bounds__(256, 4) gate_bf16_d256_kernel(const __nv_bfloat16* __restrict__ a, long long lda,
+                                                             const __nv_bfloat16* __restrict__ u, long long ldu,
+                                                             long long n_rows, const int* __restrict__ row_src,
+                                                             const float* __restrict__ gain,
+                                                             const float* __restrict__ bias, float eps,
+                                                             __nv_bfloat16* __restrict__ out, long long ldo) {
+    const int lane = threadIdx.x & 31;
+    const int c = 8 * lane;
+    const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long i0 = (blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5)) * RPW; i0 < n_rows;
+         i0 += warps * RPW) {
+        uint4 av[RPW], uv[RPW];
+        int g[RPW];
+#pragma unroll
+        for (int r = 0; r < RPW; ++r) {
+            const long long i = i0 + r;
+            if (i < n_rows) {
+                av[r] = __ldcs(reinterpret_cast<const uint4*>(a + i * lda + c));
+                uv[r] = __ldcs(reinterpret_cast<const uint4*>(u + i * ldu + c));
+                g[r] = row_src[i];
+            } else {
+                av[r] = make_uint4(0, 0, 0, 0);
+                uv[r] = make_uint4(0, 0, 0, 0);
+                g[r] = 0;
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < RPW; ++r) {
+            const long long i = i0 + r;
+            float x[8], y[8];
+            const __nv_bfloat162* ah = reinterpret_cast<const __nv_bfloat162*>(&av[r]);
+            const __nv_bfloat162* uh = reinterpret_cast<const __nv_bfloat162*>(&uv[r]);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float2 fa = __bfloat1622float2(ah[k]), fu = __bfloat1622float2(uh[k]);
+                x[2 * k] = fa.x;
+                x[2 * k + 1] = fa.y;
+                y[2 * k] = fu.x;
+                y[2 * k + 1] = fu.y;
+            }
+            float sum = 0.f;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) sum += x[k];
+            sum = warp_sum(sum);
+            const float mean = __fdiv_rn(sum, 256.f);
+            float q = 0.f;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                x[k] -= mean;
+                q += x[k] * x[k];
+            }
+            q = warp_sum(q);
+            const float inv = __fdiv_rn(1.f, sqrtf(__fdiv_rn(q, 256.f) + eps));
+            if (i >= n_rows) continue;
+            const int gg = g[r] < 0 ? 0 : g[r];
+            const float4 g0 = __ldg(reinterpret_cast<const float4*>(gain + gg * 256 + c));
+            const float4 g1 = __ldg(reinterpret_cast<const float4*>(gain + gg * 256 + c + 4));
+            const float4 b0 = __ldg(reinterpret_cast<const float4*>(bias + gg * 256 + c));
+            const float4 b1 = __ldg(reinterpret_cast<const float4*>(bias + gg * 256 + c + 4));
+            const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+            const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+            uint32_t o[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float lo = ((x[2 * k] * inv) * gv[2 * k] + bv[2 * k]) * y[2 * k];
+                const float hi = ((x[2 * k + 1] * inv) * gv[2 * k + 1] + bv[2 * k + 1]) * y[2 * k + 1];
+                const __nv_bfloat162 h2 = __floats2bfloat162_rn(lo, hi);
+                o[k] = *reinterpret_cast<const uint32_t*>(&h2);
+            }
+            *reinterpret_cast<uint4*>(out + i * ldo + c) = make_uint4(o[0], o[1], o[2], o[3]);
+        }
+    }
+}
+
 template <typename T>
 void launch_gate(const T* a, long long lda, const T* u, long long ldu, long long n_rows, int d,
                  const int* row_src_of_rows, const float* gain, const float* bias, float eps, T* out,
                  long long ldo, cudaStream_t st) {
     if (n_rows == 0) return;
+    if constexpr (std::is_same_v<T, __nv_bfloat16>) {
+        if (d == 256 && lda % 8 == 0 && ldu % 8 == 0 && ldo % 8 == 0) {
+            const int blocks = static_cast<int>(std::min<long long>(cdiv(n_rows, 8 * 2), 148ll * 16));
+            gate_bf16_d256_kernel<2><<<blocks, 256, 0, st>>>(a, lda, u, ldu, n_rows, row_src_of_rows, gain, bias,
+                                                             eps, out, ldo);
+            return;
+        }
+    }
     const int blocks = static_cast<int>(std::min<long long>(cdiv(n_rows, 8), 148ll * 16));
     const int ns = static_cast<int>(cdiv(d, 128));
 #define MTFM_GATE(NS) gate_kernel<T, NS><<<blocks, 256, 0, st>>>(a, lda, u, ldu, n_rows, d, row_src_of_rows, gain, bias, eps, out, ldo)

@@ -1326,19 +1326,32 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                         launch_gln<T>(X, d, 0, R, d, rm.src, Lw->g1g.as<float>(), Lw->g1b.as<float>(), eps, XN, d, st);
                         ++L;
                     }
+                    // U and Q|K|V as two contiguous matrices (one grouped launch): the gate
+                    // then streams U rows and the attention Q|K|V rows without gaps
                     StageScope sc(m, "proj_full", 2.0 * Rd * d * pw, Rd * d * el + Rd * pw * el);
-                    run_gemm_tc({{XN, d, Lw->t1.as<__nv_bfloat16>(), d, static_cast<int>(R), pw, d, EPI_SILU_BF16,
-                                  Lw->b1.as<float>(), Pm, pw, nullptr, 0, nullptr}},
+                    run_gemm_tc({{XN, d, Lw->t1.as<__nv_bfloat16>(), d, static_cast<int>(R), hd, d, EPI_SILU_BF16,
+                                  Lw->b1.as<float>(), Pm, hd, nullptr, 0, nullptr},
+                                 {XN, d, Lw->t1.as<__nv_bfloat16>() + static_cast<long long>(hd) * d, d,
+                                  static_cast<int>(R), hd + 2 * gd, d, EPI_SILU_BF16, Lw->b1.as<float>() + hd,
+                                  Pm + R * hd, hd + 2 * gd, nullptr, 0, nullptr}},
                                 st, L, BT);
                 }
+                // P layout: split [U][R x hd] then [Q|K|V][R x (hd + 2gd)] unless the fused-LN
+                // path wrote the interleaved [R][U|Q|K|V]
+                const bool split_p = !(m.fuse & 1);
+                T* Uptr = Pm;
+                const long long ldu_p = split_p ? hd : pw;
+                T* QKV = split_p ? Pm + R * hd : Pm;
+                const long long ldqkv = split_p ? hd + 2 * gd : pw;
+                const int qc0 = split_p ? 0 : hd;
                 {
                     StageScope sc(m, "attn_full", 4.0 * hd * sc_full, Rd * (hd + 2 * gd) * el + Rd * hd * el);
                     AttnParams ap{};
                     ap.tiles = B.tiles_full.as<AttnTile>();
                     ap.n_tiles = n_full;
-                    ap.q_col0 = hd;
-                    ap.k_col0 = 2 * hd;
-                    ap.v_col0 = 2 * hd + gd;
+                    ap.q_col0 = qc0;
+                    ap.k_col0 = qc0 + hd;
+                    ap.v_col0 = qc0 + hd + gd;
                     ap.heads = m.H;
                     ap.kv_heads = m.G;
                     ap.hs = ag.hs;
@@ -1346,13 +1359,13 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                     ap.q_prefix = rm.prefix;
                     ap.q_scale = rm.scale;
                     ap.q_self = rm.self;
-                    ap.q_ptr = Pm;
-                    ap.ldq = pw;
-                    ap.kv_ptr = Pm;
-                    ap.ldkv = pw;
+                    ap.q_ptr = QKV;
+                    ap.ldq = ldqkv;
+                    ap.kv_ptr = QKV;
+                    ap.ldkv = ldqkv;
                     ap.out = A;
                     ap.ldo = hd;
-                    run_attn_tc(m, ap, Pm, R, pw, R, pw, st);
+                    run_attn_tc(m, ap, QKV, R, ldqkv, R, ldqkv, st);
                     ++L;
                 }
                 if (m.fuse & 2) {
@@ -1370,13 +1383,13 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                     tp.row_group = rm.src;
                     tp.gain = Lw->g2g.as<float>();
                     tp.gbias = Lw->g2b.as<float>();
-                    tp.u_src = Pm;
-                    tp.ldu = pw;
+                    tp.u_src = Uptr;
+                    tp.ldu = ldu_p;
                     run_gemm_tc({tp}, st, L, BT);
                 } else {
                     {
                         StageScope sc(m, "gate", 0, Rd * hd * el * 3);
-                        launch_gate<T>(A, hd, Pm, pw, R, hd, rm.src, Lw->g2g.as<float>(), Lw->g2b.as<float>(), eps, G,
+                        launch_gate<T>(A, hd, Uptr, ldu_p, R, hd, rm.src, Lw->g2g.as<float>(), Lw->g2b.as<float>(), eps, G,
                                        hd, st);
                         ++L;
                     }
