@@ -13,6 +13,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -141,6 +143,39 @@ struct DevBuf {
     }
 };
 
+// Page-locked host staging (grows, never shrinks): host-computed layout tables
+// are written here and copied with truly asynchronous H2D transfers.
+struct PinnedBuf {
+    void* p = nullptr;
+    size_t bytes = 0, used = 0;
+    PinnedBuf() = default;
+    PinnedBuf(const PinnedBuf&) = delete;
+    PinnedBuf& operator=(const PinnedBuf&) = delete;
+    ~PinnedBuf() {
+        if (p) cudaFreeHost(p);
+    }
+    void reserve(size_t n) {
+        if (n <= bytes) return;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        bytes = 0;
+        ck(cudaMallocHost(&p, n), "cudaMallocHost");
+        bytes = n;
+    }
+    // copy h into the staging area (16-byte aligned slot) and enqueue H2D into d
+    template <typename T>
+    void upload(DevBuf& d, const std::vector<T>& h, cudaStream_t st) {
+        d.alloc(std::max<size_t>(h.size() * sizeof(T), 16));
+        if (h.empty()) return;
+        const size_t nb = h.size() * sizeof(T);
+        if (used + nb > bytes) fail(MTFM_CONTRACT_ERROR, "pinned staging overflow");
+        void* dst = static_cast<char*>(p) + used;
+        std::memcpy(dst, h.data(), nb);
+        used += (nb + 15) & ~size_t(15);
+        ck(cudaMemcpyAsync(d.p, dst, nb, cudaMemcpyHostToDevice, st), "H2D");
+    }
+};
+
 // Bias tiles for the tensor-core GEMM: bias_t[n] = (hi, lo, 0 x 14) in bf16 with
 // hi + lo = bias[n] to ~2^-17, added by one K=16 MMA against a ones tile.
 __global__ void bias_tile_kernel(const float* __restrict__ bias, int N, __nv_bfloat16* __restrict__ t) {
@@ -235,6 +270,7 @@ struct mtfm_cuda_model {
     // device weights
     mtfm::DevBuf d_src, d_slots;
     mtfm::BiasTiles bias_tiles;  // GEMM bias tiles, built on first use
+    std::vector<int> src_lookup;  // [kind][id < 4096] -> source, built on first prepare
     mtfm::DevBuf emb_f32, emb_bf16;
     std::vector<std::unique_ptr<mtfm::SourceW>> srcw;
     std::vector<std::unique_ptr<mtfm::LayerW>> layers;
@@ -272,11 +308,13 @@ struct mtfm_cuda_batch {
     // activations
     mtfm::DevBuf X, XN, P, KV, UQ, A, Gt, E, HID, Y, statX, statA;
     // attention tiles
-    std::vector<mtfm::AttnTile> h_tiles_full, h_tiles_tgt;
+    long long n_tiles_full = 0, n_tiles_tgt = 0;
+    mtfm::DevBuf d_tile_off;  // per-user first tile, full then target tables
     mtfm::DevBuf tiles_full, tiles_tgt;
     // records
     mtfm::DevBuf rec_user, rec_scen, rec_exp, rec_task, rec_logit, rec_prob;
     mtfm::DevBuf stat_buf;
+    mtfm::PinnedBuf pin;  // staging of the host-computed layout tables + stats read-back
     long long launches = 0;
     unsigned long long sum_c_ctx = 0, sum_c_t = 0;  // sum of visible keys (stats)
 };
@@ -888,13 +926,73 @@ long long next_pow2(long long n) {
     return p;
 }
 
-int source_of(const mtfm_cuda_model& m, int kind, int id, int only_scenario) {
+int source_of_slow(const mtfm_cuda_model& m, int kind, int id, int only_scenario) {
     for (size_t s = 0; s < m.sources.size(); ++s)
         if (m.sources[s].kind == kind && m.sources[s].id == id) {
             if (kind == 2 && only_scenario >= 0 && id != only_scenario) return -1;
             return static_cast<int>(s);
         }
     return -1;
+}
+
+// Attention tile tables on the device: user u owns tiles [off[u], off[u+1]) of the
+// full table (per head group: context query tiles then T query tiles) and the
+// matching T tiles of the target table (same order as the host layout had).
+__global__ void tile_expand_kernel(const long long* __restrict__ toff, const int* __restrict__ seq_off,
+                                   const int* __restrict__ ev_off, const int* __restrict__ exp_off, int n_users,
+                                   int n_seqs, long long n_events, int rt, int hs, int r, int G,
+                                   AttnTile* __restrict__ tf, AttnTile* __restrict__ tt) {
+    const int u = blockIdx.x;
+    if (u >= n_users) return;
+    const long long ev0 = n_seqs ? ev_off[seq_off[u]] : 0, ev1 = n_seqs ? ev_off[seq_off[u + 1]] : 0;
+    const long long x0 = exp_off[u], x1 = exp_off[u + 1];
+    const int qc = static_cast<int>((ev1 - ev0 + rt - 1) / rt), qt = static_cast<int>((x1 - x0 + rt - 1) / rt);
+    const int per_group = qc + qt;
+    const int hpg = (r + hs - 1) / hs;
+    const long long f0 = toff[u], t0 = toff[n_users + 1 + u];
+    for (int i = threadIdx.x; i < G * hpg * per_group; i += blockDim.x) {
+        const int grp = i / per_group, k = i - grp * per_group;
+        const int g = grp / hpg, hb0 = (grp - g * hpg) * hs;
+        const int head0 = g * r + hb0;
+        if (k < qc) {
+            const long long q = ev0 + static_cast<long long>(k) * rt;
+            tf[f0 + i] = {static_cast<int>(q), static_cast<int>(min(static_cast<long long>(rt), ev1 - q)),
+                          static_cast<int>(ev0), head0, 0, {0, 0, 0}};
+        } else {
+            const long long q = x0 + static_cast<long long>(k - qc) * rt;
+            const int n = static_cast<int>(min(static_cast<long long>(rt), x1 - q));
+            tf[f0 + i] = {static_cast<int>(n_events + q), n, static_cast<int>(ev0), head0, 0, {0, 0, 0}};
+            tt[t0 + grp * qt + (k - qc)] = {static_cast<int>(q), n, static_cast<int>(ev0), head0, 0, {0, 0, 0}};
+        }
+    }
+}
+
+void launch_tile_expand(mtfm_cuda_batch& B, int rt, int hs, int r, int G, cudaStream_t st) {
+    tile_expand_kernel<<<static_cast<int>(B.n_users), 128, 0, st>>>(
+        B.d_tile_off.as<long long>(), B.seq_off.as<int>(), B.ev_off.as<int>(), B.exp_off.as<int>(),
+        static_cast<int>(B.n_users), 1 /* ev_off always holds >= 1 entry */, B.n_events, rt, hs, r, G,
+        B.tiles_full.as<AttnTile>(), B.tiles_tgt.as<AttnTile>());
+    ck(cudaGetLastError(), "tile_expand launch");
+}
+
+// (kind, id) -> source through direct tables for ids in [0, 4096) (model-owned)
+void build_source_lookup(mtfm_cuda_model& m) {
+    m.src_lookup.assign(3 * 4096, -1);
+    for (size_t s = 0; s < m.sources.size(); ++s) {
+        const auto& si = m.sources[s];
+        if (si.kind >= 0 && si.kind < 3 && si.id >= 0 && si.id < 4096 && m.src_lookup[si.kind * 4096 + si.id] < 0)
+            m.src_lookup[si.kind * 4096 + si.id] = static_cast<int>(s);
+    }
+}
+inline int source_of_fast(const mtfm_cuda_model& m, int kind, int id, int only_scenario) {
+    if (id >= 0 && id < 4096) {
+        if (kind == 2 && only_scenario >= 0 && id != only_scenario) return -1;
+        return m.src_lookup[kind * 4096 + id];
+    }
+    return source_of_slow(m, kind, id, only_scenario);
+}
+int source_of(const mtfm_cuda_model& m, int kind, int id, int only_scenario) {
+    return source_of_slow(m, kind, id, only_scenario);
 }
 
 void check_batch(const mtfm_packed_batch* b) {
@@ -912,6 +1010,10 @@ void check_batch(const mtfm_packed_batch* b) {
 }
 
 void prepare(mtfm_cuda_model& m, const mtfm_packed_batch* hb, int only_scenario, mtfm_cuda_batch& B) {
+    static const bool host_timing = std::getenv("MTFM_HOST_TIMING") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto dus = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+    const auto p0 = now();
     check_batch(hb);
     finalize(m);
     cudaStream_t st = m.stream;
@@ -942,21 +1044,23 @@ void prepare(mtfm_cuda_model& m, const mtfm_packed_batch* hb, int only_scenario,
     upload_raw(B.exp_blk, hb->exp_blk, 3ll * hb->n_exposures, st);
     upload_raw(B.exp_feats, hb->exp_feats, hb->n_exp_feats, st);
 
+    const auto p1 = now();
     // host layout: per (user, source) counts -> source regions, record offsets
     std::vector<long long> us(static_cast<size_t>(B.n_users) * n_src, 0);
     std::vector<long long> rec_off(B.n_users + 1, 0);
     long long max_sort = 1;
+    if (m.src_lookup.empty()) build_source_lookup(m);
     for (int u = 0; u < hb->n_users; ++u) {
         long long n_ev = 0;
         for (int s = hb->seq_off[u]; s < hb->seq_off[u + 1]; ++s) {
-            const int src = source_of(m, hb->seq_kind[s] ? 1 : 0, hb->seq_schema[s], -1);
+            const int src = source_of_fast(m, hb->seq_kind[s] ? 1 : 0, hb->seq_schema[s], -1);
             const long long len = hb->ev_off[s + 1] - hb->ev_off[s];
             n_ev += len;
             if (src >= 0) us[static_cast<size_t>(u) * n_src + src] += len;
         }
         long long recs = 0;
         for (int x = hb->exp_off[u]; x < hb->exp_off[u + 1]; ++x) {
-            const int src = source_of(m, 2, hb->exp_scenario[x], only_scenario);
+            const int src = source_of_fast(m, 2, hb->exp_scenario[x], only_scenario);
             if (src >= 0) {
                 us[static_cast<size_t>(u) * n_src + src] += 1;
                 recs += m.sources[src].ntasks;
@@ -989,37 +1093,54 @@ void prepare(mtfm_cuda_model& m, const mtfm_packed_batch* hb, int only_scenario,
         eb += B.src_cnt[s] * m.sources[s].k_pad;
         hbse += B.src_cnt[s] * 2 * m.d;
     }
-    upload(B.d_us_off, us_off, st);
-    upload(B.d_src_base, B.src_base, st);
-    upload(B.d_src_cnt, B.src_cnt, st);
-    upload(B.d_emb_base, B.emb_base, st);
-    upload(B.d_rec_off, rec_off, st);
+    // (the previous forward on this batch has completed: results() synchronised)
+    // tile tables: per user and head group ceil(n/rt) query tiles, at most (n + rt - 1) / rt each
+    const AttnGeom ag0 = attn_geom(m);
+    const size_t hg0 = static_cast<size_t>(m.G) * ((m.H / m.G + ag0.hs - 1) / ag0.hs);
+    const size_t tiles_est = hg0 * (static_cast<size_t>(B.n_events + 2 * B.n_exp) / ag0.rt + 3 * B.n_users) + 64;
+    B.pin.reserve((us_off.size() + 4 * static_cast<size_t>(n_src) + rec_off.size()) * 8 + tiles_est * sizeof(AttnTile) +
+                  4096);
+    B.pin.used = 64;  // first 64 bytes: stats read-back
+    B.pin.upload(B.d_us_off, us_off, st);
+    B.pin.upload(B.d_src_base, B.src_base, st);
+    B.pin.upload(B.d_src_cnt, B.src_cnt, st);
+    B.pin.upload(B.d_emb_base, B.emb_base, st);
+    B.pin.upload(B.d_rec_off, rec_off, st);
 
+    const auto p2 = now();
     // attention tiles
     const AttnGeom ag = attn_geom(m);
     const int r = m.H / m.G;
-    B.h_tiles_full.clear();
-    B.h_tiles_tgt.clear();
+    // count, then write straight into the pinned staging area (one H2D per table)
+    const int hgroups = m.G * ((r + ag.hs - 1) / ag.hs);
+    long long nf = 0, nt = 0;
     for (int u = 0; u < hb->n_users; ++u) {
         const long long ev0 = hb->n_seqs ? hb->ev_off[hb->seq_off[u]] : 0;
         const long long ev1 = hb->n_seqs ? hb->ev_off[hb->seq_off[u + 1]] : 0;
-        const long long x0 = hb->exp_off[u], x1 = hb->exp_off[u + 1];
-        for (int g = 0; g < m.G; ++g)
-            for (int hb0 = 0; hb0 < r; hb0 += ag.hs) {
-                const int head0 = g * r + hb0;
-                for (long long q = ev0; q < ev1; q += ag.rt)
-                    B.h_tiles_full.push_back({static_cast<int>(q), static_cast<int>(std::min<long long>(ag.rt, ev1 - q)),
-                                              static_cast<int>(ev0), head0, 0, {0, 0, 0}});
-                for (long long q = x0; q < x1; q += ag.rt) {
-                    const int n = static_cast<int>(std::min<long long>(ag.rt, x1 - q));
-                    B.h_tiles_full.push_back({static_cast<int>(B.n_events + q), n, static_cast<int>(ev0), head0, 0, {0, 0, 0}});
-                    B.h_tiles_tgt.push_back({static_cast<int>(q), n, static_cast<int>(ev0), head0, 0, {0, 0, 0}});
-                }
-            }
+        const long long tq = cdiv(hb->exp_off[u + 1] - hb->exp_off[u], ag.rt);
+        nf += hgroups * (cdiv(ev1 - ev0, ag.rt) + tq);
+        nt += hgroups * tq;
     }
-    upload(B.tiles_full, B.h_tiles_full, st);
-    upload(B.tiles_tgt, B.h_tiles_tgt, st);
-
+    B.n_tiles_full = nf;
+    B.n_tiles_tgt = nt;
+    // per-user tile offsets go to the device; tile_expand_kernel writes the tables
+    std::vector<long long> toff(static_cast<size_t>(2 * (B.n_users + 1)), 0);  // [full offsets | target offsets]
+    for (int u = 0; u < hb->n_users; ++u) {
+        const long long ev0 = hb->n_seqs ? hb->ev_off[hb->seq_off[u]] : 0;
+        const long long ev1 = hb->n_seqs ? hb->ev_off[hb->seq_off[u + 1]] : 0;
+        const long long tq = cdiv(hb->exp_off[u + 1] - hb->exp_off[u], ag.rt);
+        toff[u + 1] = toff[u] + hgroups * (cdiv(ev1 - ev0, ag.rt) + tq);
+        toff[B.n_users + 1 + u + 1] = toff[B.n_users + 1 + u] + hgroups * tq;
+    }
+    B.pin.upload(B.d_tile_off, toff, st);
+    B.tiles_full.alloc(std::max<size_t>(static_cast<size_t>(nf) * sizeof(AttnTile), 16));
+    B.tiles_tgt.alloc(std::max<size_t>(static_cast<size_t>(nt) * sizeof(AttnTile), 16));
+    if (B.n_users > 0)
+        launch_tile_expand(B, ag.rt, ag.hs, r, m.G, st);
+    const auto p3 = now();
+    if (host_timing)
+        std::fprintf(stderr, "prepare: raw uploads %.0f us, layout %.0f us, tiles %.0f us\n", dus(p0, p1), dus(p1, p2),
+                     dus(p2, p3));
     // row meta + activations
     const long long R = B.rows, T = B.n_exp;
     auto ia = [&](DevBuf& b, long long n, size_t el) { b.alloc(std::max<size_t>(static_cast<size_t>(n) * el, 16)); };
@@ -1267,8 +1388,8 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
 
     // ---- attention tile extents (max visible prefix per tile)
     const AttnGeom ag = attn_geom(m);
-    const int n_full = static_cast<int>(B.h_tiles_full.size());
-    const int n_tgt = static_cast<int>(B.h_tiles_tgt.size());
+    const int n_full = static_cast<int>(B.n_tiles_full);
+    const int n_tgt = static_cast<int>(B.n_tiles_tgt);
     if (kTc && (n_full || n_tgt)) {
         StageScope sc(m, "tile_kmax", 0, (n_full + n_tgt) * 32.0);
         if (n_full) {
@@ -1724,11 +1845,22 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
     }
 }
 
+void launch_sum_valid(mtfm_cuda_batch& B, cudaStream_t st);
+
 void results(mtfm_cuda_model& m, mtfm_cuda_batch& B, mtfm_records* out) {
     cudaStream_t st = m.stream;
-    unsigned long long err = ~0ull;
-    if (B.n_users > 0) ck(cudaMemcpyAsync(&err, B.err.p, 8, cudaMemcpyDeviceToHost, st), "D2H err");
+    // error key + the visible-key sums of the stats, read back with one synchronisation
+    B.pin.reserve(4096);
+    auto* hb = static_cast<unsigned long long*>(B.pin.p);
+    hb[0] = ~0ull;
+    hb[1] = hb[2] = 0;
+    if (B.n_users > 0) ck(cudaMemcpyAsync(hb, B.err.p, 8, cudaMemcpyDeviceToHost, st), "D2H err");
+    launch_sum_valid(B, st);
+    ck(cudaMemcpyAsync(hb + 1, B.stat_buf.p, 16, cudaMemcpyDeviceToHost, st), "D2H stats");
     ck(cudaStreamSynchronize(st), "forward");
+    B.sum_c_ctx = hb[1];
+    B.sum_c_t = hb[2];
+    const unsigned long long err = hb[0];
     if (err != ~0ull) {
         const int code = static_cast<int>(err & 7);
         const long long user = static_cast<long long>(err >> 42);
@@ -1762,6 +1894,7 @@ void results(mtfm_cuda_model& m, mtfm_cuda_batch& B, mtfm_records* out) {
     out->n_records = B.n_records;
 }
 
+void launch_sum_valid(mtfm_cuda_batch& B, cudaStream_t st);
 // Algorithmic FLOPs of the run: projections per complexity.hpp:54-64,
 // mask-aware attention 4*d_h*H*sum(c_i) per layer, tokenizer MLPs, heads.
 __global__ void sum_valid_kernel(const int* prefix, const int* self, long long n, unsigned long long* out) {
@@ -1770,6 +1903,17 @@ __global__ void sum_valid_kernel(const int* prefix, const int* self, long long n
         s += static_cast<unsigned long long>(prefix[i] + (self[i] >= 0 ? 1 : 0));
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if ((threadIdx.x & 31) == 0) atomicAdd(out, s);
+}
+
+void launch_sum_valid(mtfm_cuda_batch& B, cudaStream_t st) {
+    B.stat_buf.alloc(16);
+    ck(cudaMemsetAsync(B.stat_buf.p, 0, 16, st), "memset stats");
+    auto* a = B.stat_buf.as<unsigned long long>();
+    if (B.n_events)
+        sum_valid_kernel<<<64, 256, 0, st>>>(B.r_prefix.as<int>(), B.r_self.as<int>(), B.n_events, a);
+    if (B.n_exp)
+        sum_valid_kernel<<<64, 256, 0, st>>>(B.r_prefix.as<int>() + B.n_events, B.r_self.as<int>() + B.n_events,
+                                             B.n_exp, a + 1);
 }
 
 }  // namespace
@@ -1957,23 +2101,8 @@ mtfm_status mtfm_cuda_batch_results(mtfm_cuda_model* m, mtfm_cuda_batch* b, mtfm
     return guard([&] {
         if (!m || !b) fail(MTFM_CONTRACT_ERROR, "null argument");
         results(*m, *b, out);
-        // algorithmic FLOPs
-        DevBuf acc;
-        acc.alloc(16);
-        ck(cudaMemsetAsync(acc.p, 0, 16, m->stream), "memset");
-        const auto* a = acc.as<unsigned long long>();
-        if (b->n_events)
-            sum_valid_kernel<<<64, 256, 0, m->stream>>>(b->r_prefix.as<int>(), b->r_self.as<int>(), b->n_events,
-                                                        const_cast<unsigned long long*>(a));
-        if (b->n_exp)
-            sum_valid_kernel<<<64, 256, 0, m->stream>>>(b->r_prefix.as<int>() + b->n_events,
-                                                        b->r_self.as<int>() + b->n_events, b->n_exp,
-                                                        const_cast<unsigned long long*>(a) + 1);
-        unsigned long long h[2] = {0, 0};
-        ck(cudaMemcpyAsync(h, acc.p, 16, cudaMemcpyDeviceToHost, m->stream), "D2H");
-        ck(cudaStreamSynchronize(m->stream), "stats");
-        b->sum_c_ctx = h[0];
-        b->sum_c_t = h[1];
+        // algorithmic FLOPs; visible-key sums read back by results()
+        const unsigned long long h[2] = {b->sum_c_ctx, b->sum_c_t};
         if (m->profiling)
             for (size_t i = 0; i < m->prof_n; ++i) {
                 float ms = 0;
@@ -2011,14 +2140,30 @@ mtfm_status mtfm_cuda_batch_free(mtfm_cuda_batch* b) {
 
 mtfm_status mtfm_cuda_forward(mtfm_cuda_model* m, const mtfm_packed_batch* b, int32_t only_scenario,
                               mtfm_records* out) {
+    const auto t0 = std::chrono::steady_clock::now();
     mtfm_status s = guard([&] {
         if (!m) fail(MTFM_CONTRACT_ERROR, "null argument");
         ck(cudaSetDevice(m->device), "cudaSetDevice");
         if (!m->ws) m->ws = std::make_unique<mtfm_cuda_batch>();  // device buffers only grow
         prepare(*m, b, only_scenario, *m->ws);
     });
+    static const bool host_timing = std::getenv("MTFM_HOST_TIMING") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto t1 = now();
+    if (host_timing) cudaStreamSynchronize(m->stream);
+    auto t2 = now();
     if (s == MTFM_OK) s = mtfm_cuda_batch_run(m, m->ws.get());
+    auto t3 = now();
+    if (host_timing) cudaStreamSynchronize(m->stream);
+    auto t4 = now();
     if (s == MTFM_OK) s = mtfm_cuda_batch_results(m, m->ws.get(), out);
+    auto t5 = now();
+    if (host_timing) {
+        auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+        std::fprintf(stderr, "host timing: prepare %.0f us, ", us(t0, t1));
+        std::fprintf(stderr, "h2d-drain %.0f us, run enqueue %.0f us, device %.0f us, results %.0f us\n",
+                     us(t1, t2), us(t2, t3), us(t3, t4), us(t4, t5));
+    }
     return s;
 }
 

@@ -160,8 +160,10 @@ class Model:
     def forward_batch(self, batch: dict, only_scenario=-1) -> RecordArrays:
         b = normalize_batch(batch)
         pb = self._packed(b)
-        n = int(abi.lib().mtfm_cuda_count_records(self._h, C.byref(pb)))
-        out, rec = self._record_buffers(n)
+        # capacity bound instead of a counting pass: every exposure yields at most
+        # max-tasks records (the library reports the exact count)
+        max_tasks = max((len(t) for t in self._tasks.values()), default=0)
+        out, rec = self._record_buffers(int(len(b["exp_ts"])) * max_tasks)
         abi.check(abi.lib().mtfm_cuda_forward(self._h, C.byref(pb), only_scenario, C.byref(rec)))
         k = int(rec.n_records)
         return RecordArrays(*(a[:k] for a in out))
