@@ -54,6 +54,7 @@ struct AttnParams {
     long long ldkv;
     __nv_bfloat16* out;          // A rows indexed like Q rows
     long long ldo;
+    unsigned long long* trace;   // timing experiments only (-DMTFM_ATTN_TRACE): CTA 0 clock stamps
 };
 
 namespace attn_detail {
@@ -70,8 +71,10 @@ struct Cfg {
     static constexpr int STAGE_BYTES = 2 * KV_TILE_BYTES;
     static constexpr int P_BYTES = 128 * BKV * 2;
     static constexpr int QB = D <= 64 ? 2 : 1;              // Q buffers
-    static constexpr int kStages = D <= 128 ? (D <= 64 ? 4 : 3) : 2;
-    static constexpr int LAG = kStages >= 3 ? 2 : 1;        // PV of key tile i issued after S of tile i+LAG
+    // K|V ring as deep as ~200 KB of SMEM allows: the S warp runs ahead of the
+    // PV warp by a few tiles, and TMA latency must hide behind the rest
+    static constexpr int kStagesRaw = (200 * 1024 - QB * Q_BYTES) / STAGE_BYTES;
+    static constexpr int kStages = kStagesRaw > 12 ? 12 : kStagesRaw;
     static constexpr int SMEM = QB * Q_BYTES + kStages * STAGE_BYTES + 1024 + 512;
     static constexpr uint32_t TMEM_COLS = 512;
     static constexpr uint32_t S_COL = 0;                    // S buffers at [0, 2*BKV)
@@ -118,6 +121,13 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
     const uint32_t warp = ptx::warp_id();
     const uint32_t lane = ptx::lane_id();
     const int r_per_g = prm.heads / prm.kv_heads;
+#ifdef MTFM_ATTN_TRACE
+    auto trace = [&](int slot) {
+        if (prm.trace && blockIdx.x == 0 && lane == 0 && slot >= 0 && slot < 2048) prm.trace[slot] = clock64();
+    };
+#else
+    auto trace = [&](int) {};
+#endif
 
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < 2; ++i) {
@@ -126,13 +136,13 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
             ptx::mbar_init(&o_full[i], 1);
             ptx::mbar_init(&o_empty[i], 4);
             ptx::mbar_init(&s_full[i], 1);
-            ptx::mbar_init(&s_empty[i], C::kSilu);
-            ptx::mbar_init(&p_full[i], C::kSilu);
+            ptx::mbar_init(&s_empty[i], C::kSilu / 2);
+            ptx::mbar_init(&p_full[i], C::kSilu / 2);
             ptx::mbar_init(&p_empty[i], 1);
         }
         for (int i = 0; i < C::kStages; ++i) {
             ptx::mbar_init(&kv_full[i], 1);
-            ptx::mbar_init(&kv_empty[i], 1);
+            ptx::mbar_init(&kv_empty[i], 2);  // S warp (K) + PV warp (V)
         }
         ptx::fence_mbar_init();
         ptx::tma_prefetch(&prm.tma_q);
@@ -183,79 +193,32 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
             }
         }
     } else if (warp == 1) {
-        // ------------------------------------------------ MMA issuer
-        // One continuous stream of key tiles across query tiles: S of item i is
-        // issued as soon as its K tile and S buffer are free; the P.V of item
-        // i - LAG follows, so S always runs LAG key tiles ahead of the SiLU warps.
+        // ------------------------------------------------ S issuer: S[buf] = Q K_j^T
+        // Runs ahead of the SiLU warps, bounded only by free S buffers and K tiles.
         const uint32_t idesc_s = ptx::instr_desc_bf16(128, BKV, false, false);
-        const uint32_t idesc_o = ptx::instr_desc_bf16(128, D, false, true);
-        struct Item {
-            int ob, stage, j, n_kv, it;
-            uint32_t cnt;  // key-tile counter (S/P buffer and parity)
-            bool dummy;    // query tile without visible keys: no MMA, O signalled empty
-        };
-        Item p0{}, p1{};  // pending P.V items (oldest first), at most LAG
-        int size = 0;
         int stage = 0;
         uint32_t phase = 0;
         uint32_t s_cnt = 0;
-        auto issue_pv = [&](const Item& x) {
-            if (x.dummy || x.j == 0) {
-                ptx::mbar_wait(&o_empty[x.ob], ((x.it / C::OB) & 1) ^ 1);
-                ptx::tc_fence_after();
-            }
-            if (x.dummy) {
-                if (ptx::elect_one()) ptx::umma_commit(&o_full[x.ob]);
-                __syncwarp();
-                return;
-            }
-            const uint32_t buf = x.cnt & 1;
-            ptx::mbar_wait(&p_full[buf], (x.cnt >> 1) & 1);
-            ptx::tc_fence_after();
-            if (ptx::elect_one()) {
-                const uint32_t p_tmem = tmem + C::P_COL + buf * (BKV / 2);
-                const uint32_t sv = ptx::smem_u32(sKV + x.stage * C::STAGE_BYTES + C::KV_TILE_BYTES);
-                const uint32_t o_tmem = tmem + C::O_COL + x.ob * D;
-#pragma unroll
-                for (int kk = 0; kk < BKV / 16; ++kk) {
-                    const uint64_t db = ptx::smem_desc(sv + kk * 16 * C::ROWB, BKV * C::ROWB, 8 * C::ROWB, C::LAYOUT);
-                    ptx::umma_bf16_ts(o_tmem, p_tmem + kk * 8, db, idesc_o, (x.j > 0 || kk > 0));
-                }
-                ptx::umma_commit(&kv_empty[x.stage]);
-                ptx::umma_commit(&p_empty[buf]);
-                if (x.j == x.n_kv - 1) ptx::umma_commit(&o_full[x.ob]);
-            }
-            __syncwarp();
-        };
-        auto push = [&](const Item& x) {
-            if (size == C::LAG) {  // oldest pending item is now LAG key tiles behind
-                issue_pv(p0);
-                p0 = p1;
-                --size;
-            }
-            if (size == 0) p0 = x;
-            else p1 = x;
-            ++size;
-        };
         int it = 0;
         for (int t = blockIdx.x; t < prm.n_tiles; t += gridDim.x, ++it) {
             const AttnTile tile = prm.tiles[t];
             const int n_kv = (tile.kmax + BKV - 1) / BKV;
             const int qb = it % C::QB;
-            const int ob = it % C::OB;
             ptx::mbar_wait(&q_full[qb], (it / C::QB) & 1);
             ptx::tc_fence_after();
             if (n_kv == 0) {
                 if (ptx::elect_one()) ptx::umma_commit(&q_empty[qb]);
                 __syncwarp();
-                push(Item{ob, 0, 0, 0, it, 0u, true});
                 continue;
             }
             const uint32_t sq = ptx::smem_u32(sQ + qb * C::Q_BYTES);
             for (int j = 0; j < n_kv; ++j) {
                 const uint32_t buf = s_cnt & 1;
+                if (s_cnt < 128) trace(1024 + 4 * s_cnt + 0);
                 ptx::mbar_wait(&kv_full[stage], phase);
+                if (s_cnt < 128) trace(1024 + 4 * s_cnt + 1);
                 ptx::mbar_wait(&s_empty[buf], ((s_cnt >> 1) & 1) ^ 1);
+                if (s_cnt < 128) trace(1024 + 4 * s_cnt + 2);
                 ptx::tc_fence_after();
                 if (ptx::elect_one()) {
                     const uint32_t sk = ptx::smem_u32(sKV + stage * C::STAGE_BYTES);
@@ -269,9 +232,9 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
                     }
                     if (j == n_kv - 1) ptx::umma_commit(&q_empty[qb]);
                     ptx::umma_commit(&s_full[buf]);
+                    ptx::umma_commit(&kv_empty[stage]);  // K consumed (the PV warp releases V)
                 }
                 __syncwarp();
-                push(Item{ob, stage, j, n_kv, it, s_cnt, false});
                 ++s_cnt;
                 if (++stage == C::kStages) {
                     stage = 0;
@@ -279,13 +242,56 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
                 }
             }
         }
-        if (size > 0) issue_pv(p0);
-        if (size > 1) issue_pv(p1);
+    } else if (warp == 3) {
+        // ------------------------------------------------ PV issuer: O[ob] += P[buf] V_j
+        // A second MMA-issuing warp: the eight K=16 steps of every P.V do not
+        // delay the next S, and vice versa.
+        const uint32_t idesc_o = ptx::instr_desc_bf16(128, D, false, true);
+        int stage = 0;
+        uint32_t phase_unused = 0;
+        (void)phase_unused;
+        uint32_t cnt = 0;
+        int it = 0;
+        for (int t = blockIdx.x; t < prm.n_tiles; t += gridDim.x, ++it) {
+            const AttnTile tile = prm.tiles[t];
+            const int n_kv = (tile.kmax + BKV - 1) / BKV;
+            const int ob = it % C::OB;
+            ptx::mbar_wait(&o_empty[ob], ((it / C::OB) & 1) ^ 1);
+            ptx::tc_fence_after();
+            if (n_kv == 0) {
+                if (ptx::elect_one()) ptx::umma_commit(&o_full[ob]);
+                __syncwarp();
+                continue;
+            }
+            for (int j = 0; j < n_kv; ++j, ++cnt) {
+                const uint32_t buf = cnt & 1;
+                ptx::mbar_wait(&p_full[buf], (cnt >> 1) & 1);
+                if (cnt < 128) trace(1024 + 4 * cnt + 3);
+                ptx::tc_fence_after();
+                if (ptx::elect_one()) {
+                    const uint32_t p_tmem = tmem + C::P_COL + buf * (BKV / 2);
+                    const uint32_t sv = ptx::smem_u32(sKV + stage * C::STAGE_BYTES + C::KV_TILE_BYTES);
+                    const uint32_t o_tmem = tmem + C::O_COL + ob * D;
+#pragma unroll
+                    for (int kk = 0; kk < BKV / 16; ++kk) {
+                        const uint64_t db = ptx::smem_desc(sv + kk * 16 * C::ROWB, BKV * C::ROWB, 8 * C::ROWB, C::LAYOUT);
+                        ptx::umma_bf16_ts(o_tmem, p_tmem + kk * 8, db, idesc_o, (j > 0 || kk > 0));
+                    }
+                    ptx::umma_commit(&kv_empty[stage]);
+                    ptx::umma_commit(&p_empty[buf]);
+                    if (j == n_kv - 1) ptx::umma_commit(&o_full[ob]);
+                }
+                __syncwarp();
+                if (++stage == C::kStages) stage = 0;
+            }
+        }
     } else if (warp >= 4 && warp < 4 + C::kSilu) {
         // ------------------------------------------------ SiLU warps
         constexpr int CPW = C::CPW;
+        constexpr int CPW2 = BKV / 2;
         const uint32_t q = warp & 3;
-        const uint32_t slice = (warp - 4) >> 2;  // column slice of CPW keys
+        const uint32_t slice = (warp - 4) >> 2;
+        const uint32_t grp = slice >> 1, half = slice & 1;
         const uint32_t m = q * 32 + lane;        // MMA row == TMEM lane
         const uint32_t lane_addr = (q * 32u) << 16;
         uint32_t s_cnt = 0;
@@ -296,47 +302,56 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
             const int i = m - hs * prm.rt;
             const int prefix = i < tile.n_rows ? __ldg(prm.q_prefix + tile.q_row0 + i) : 0;
             for (int j = 0; j < n_kv; ++j, ++s_cnt) {
-                const uint32_t buf = s_cnt & 1;
+                // key tile s_cnt belongs to phase group s_cnt & 1 (S/P buffer = group)
+                if ((s_cnt & 1u) != grp) continue;
+                const uint32_t buf = grp;
                 const uint32_t par = (s_cnt >> 1) & 1;
-                const int col0 = slice * CPW;           // key column within tile
-                const int nvalid = prefix - (j * BKV + col0);  // >= CPW: no masking needed
+                const bool tr = (warp == 4 || warp == 12) && s_cnt < 128;
+                if (tr) trace(4 * s_cnt + 0);
                 ptx::mbar_wait(&s_full[buf], par);
+                if (tr) trace(4 * s_cnt + 1);
                 ptx::tc_fence_after();
-                float v[CPW];
+                uint32_t packed[CPW2 / 2];
 #pragma unroll
-                for (int c = 0; c < CPW / 16; ++c)
-                    ptx::tmem_ld16(tmem + lane_addr + C::S_COL + buf * BKV + col0 + c * 16,
-                                   *reinterpret_cast<float(*)[16]>(v + c * 16));
-                ptx::tmem_ld_wait();
-                ptx::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&s_empty[buf]);
-                uint32_t packed[CPW / 2];
-                if (__all_sync(0xffffffffu, nvalid >= CPW)) {
+                for (int c = 0; c < CPW2 / CPW; ++c) {
+                    const int col0 = half * CPW2 + c * CPW;         // key column within the tile
+                    const int nvalid = prefix - (j * BKV + col0);   // >= CPW: no masking needed
+                    float v[CPW];
 #pragma unroll
-                    for (int e = 0; e < CPW; e += 2) packed[e / 2] = attn_detail::silu2_bf16(v[e], v[e + 1]);
-                } else if (__all_sync(0xffffffffu, nvalid <= 0)) {
-                    // slice entirely beyond every row's prefix: no MUFU work
+                    for (int k = 0; k < CPW / 16; ++k)
+                        ptx::tmem_ld16(tmem + lane_addr + C::S_COL + buf * BKV + col0 + k * 16,
+                                       *reinterpret_cast<float(*)[16]>(v + k * 16));
+                    ptx::tmem_ld_wait();
+                    if (c == CPW2 / CPW - 1) {
+                        ptx::tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) ptx::mbar_arrive(&s_empty[buf]);
+                    }
+                    uint32_t* pk = packed + c * (CPW / 2);
+                    if (__all_sync(0xffffffffu, nvalid >= CPW)) {
 #pragma unroll
-                    for (int e = 0; e < CPW / 2; ++e) packed[e] = 0u;
-                } else {
+                        for (int e = 0; e < CPW; e += 2) pk[e / 2] = attn_detail::silu2_bf16(v[e], v[e + 1]);
+                    } else if (__all_sync(0xffffffffu, nvalid <= 0)) {
 #pragma unroll
-                    for (int e = 0; e < CPW; e += 2) {
-                        const uint32_t w = attn_detail::silu2_bf16(v[e], v[e + 1]);
-                        const uint32_t keep = (e + 1 < nvalid) ? 0xffffffffu : (e < nvalid ? 0x0000ffffu : 0u);
-                        packed[e / 2] = w & keep;
+                        for (int e = 0; e < CPW / 2; ++e) pk[e] = 0u;
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < CPW; e += 2) {
+                            const uint32_t w = attn_detail::silu2_bf16(v[e], v[e + 1]);
+                            const uint32_t keep = (e + 1 < nvalid) ? 0xffffffffu : (e < nvalid ? 0x0000ffffu : 0u);
+                            pk[e / 2] = w & keep;
+                        }
                     }
                 }
-                // P buffer must have been consumed by the MMA two key tiles ago
+                if (tr) trace(4 * s_cnt + 2);
                 ptx::mbar_wait(&p_empty[buf], par ^ 1);
+                if (tr) trace(4 * s_cnt + 3);
                 ptx::tc_fence_after();
                 {
-                    const uint32_t pa = tmem + lane_addr + C::P_COL + buf * (BKV / 2) + col0 / 2;
-                    if constexpr (CPW == 32) {
-                        ptx::tmem_st16(pa, *reinterpret_cast<const uint32_t(*)[16]>(packed));
-                    } else {
-                        ptx::tmem_st8(pa, *reinterpret_cast<const uint32_t(*)[8]>(packed));
-                    }
+                    const uint32_t pa = tmem + lane_addr + C::P_COL + buf * (BKV / 2) + half * (CPW2 / 2);
+#pragma unroll
+                    for (int k = 0; k < CPW2 / 32; ++k)
+                        ptx::tmem_st16(pa + 16 * k, *reinterpret_cast<const uint32_t(*)[16]>(packed + 16 * k));
                 }
                 ptx::tmem_st_wait();
                 ptx::tc_fence_before();

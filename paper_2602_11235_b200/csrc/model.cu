@@ -911,7 +911,32 @@ void run_attn_tc(const mtfm_cuda_model& m, AttnParams p, const __nv_bfloat16* q,
     p.tma_kv = tma_2d(p.kv_ptr, kv_rows, kv_cols, p.ldkv, chunk, bkv, chunk * 2);
     switch (D) {
         case 16: launch_attn_tc_d<16>(p, st); break;
-        case 32: launch_attn_tc_d<32>(p, st); break;
+        case 32: {
+            static unsigned long long* tr = nullptr;
+            static int calls = 0;
+            const bool tracing = std::getenv("MTFM_ATTN_TRACE") != nullptr && p.n_tiles > 20000 && calls++ == 1;
+            if (tracing) {
+                if (!tr) ck(cudaMalloc(&tr, 2048 * 8), "trace alloc");
+                ck(cudaMemsetAsync(tr, 0, 2048 * 8, st), "trace clear");
+                p.trace = tr;
+            }
+            launch_attn_tc_d<32>(p, st);
+            p.trace = nullptr;
+            if (tracing) {
+                unsigned long long h[2048];
+                ck(cudaMemcpyAsync(h, tr, sizeof(h), cudaMemcpyDeviceToHost, st), "trace fetch");
+                ck(cudaStreamSynchronize(st), "trace sync");
+                const unsigned long long t0 = h[1024];
+                auto rel = [&](int i) { return h[i] ? static_cast<long long>(h[i] - t0) : -1LL; };
+                for (int k = 0; k < 48; ++k)
+                    std::fprintf(stderr,
+                                 "s%2d mma: start %6lld kv %6lld s_empty %6lld | pv p_full %6lld || silu: start %6lld "
+                                 "s_full %6lld silu_done %6lld p_empty %6lld\n",
+                                 k, rel(1024 + 4 * k), rel(1025 + 4 * k), rel(1026 + 4 * k), rel(1027 + 4 * k),
+                                 rel(4 * k), rel(4 * k + 1), rel(4 * k + 2), rel(4 * k + 3));
+            }
+            break;
+        }
         case 64: launch_attn_tc_d<64>(p, st); break;
         case 128: launch_attn_tc_d<128>(p, st); break;
         case 256: launch_attn_tc_d<256>(p, st); break;
