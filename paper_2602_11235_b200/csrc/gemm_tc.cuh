@@ -12,6 +12,9 @@
 //            stats pass), so the normalised activations never touch HBM.
 //   A_GATE : the gate of hta.hpp:153/179 fused in: bf16(gln(A) * U) from the
 //            attention output A and the U projection, both bf16.
+//   A_GATE_TMA : the same gate, but A and U k-blocks are TMA-loaded into the
+//            stage and four transform warps rewrite the A block in place
+//            (SMEM -> SMEM, no exposed global latency) before the MMA.
 // One launch serves up to kMaxProblems independent problems (tokenizer
 // sources, fkv+fuq of a target layer, ...): the persistent CTAs walk one
 // global tile list, tile t -> (problem, m-block, n-block), n fastest, so the
@@ -39,12 +42,13 @@ enum GemmEpi : int {
     EPI_BIAS_BF16 = 3,   // out_bf16[m][n] = acc + bias
 };
 
-enum GemmAMode : int { A_TMA = 0, A_LN = 1, A_GATE = 2 };
+enum GemmAMode : int { A_TMA = 0, A_LN = 1, A_GATE = 2, A_GATE_TMA = 3 };
 
 constexpr int kMaxProblems = 16;
 
 struct GemmProblem {
-    CUtensorMap tma_a;      // box {64, 128} (2D) or {64, 128, stage_kb} (3D k-block view), SW128 (A_TMA only)
+    CUtensorMap tma_a;      // box {64, 128} (2D) or {64, 128, stage_kb} (3D k-block view), SW128 (A_TMA, A_GATE_TMA)
+    CUtensorMap tma_u;      // A_GATE_TMA: U rows, box {64, 128}, SW128
     CUtensorMap tma_b;      // box {64, BN} or {64, BN, stage_kb}, SW128
     CUtensorMap tma_c;      // output, box {32, 32}: bf16 SW64 / f32 SW128 (use_tma_c)
     int use_tma_c;          // plain row-major output rows [0, M): bulk-tensor stores
@@ -267,6 +271,7 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
     uint64_t* res_bar = tempty_bar + 4;  // [12 epilogue warps][2 staging buffers]
     uint64_t* bres_bar = res_bar + 24;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres_bar + 1);
+    uint64_t* raw_bar = bres_bar + 2;  // [8] A_GATE_TMA: raw A|U k-block landed
     int* s_tile_start = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(full_bar) + 512);
     int* s_tiles_n = s_tile_start + kMaxProblems;
     int* s_kblocks = s_tiles_n + kMaxProblems;
@@ -305,8 +310,9 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
 
     if (warp == kWarpTma && lane == 0) {
         for (int s = 0; s < n_stages; ++s) {
-            ptx::mbar_init(&full_bar[s], a_mode == A_TMA ? 1 : 1 + 4);
+            ptx::mbar_init(&full_bar[s], a_mode == A_TMA ? 1 : (a_mode == A_GATE_TMA ? 4 : 1 + 4));
             ptx::mbar_init(&empty_bar[s], 1);
+            ptx::mbar_init(&raw_bar[s], 1);
         }
         ptx::mbar_init(bres_bar, 1);
         for (int s = 0; s < C::kAcc; ++s) {
@@ -316,7 +322,8 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
         for (int s = 0; s < 24; ++s) ptx::mbar_init(&res_bar[s], 1);
         ptx::fence_mbar_init();
         for (int i = 0; i < args.n_problems; ++i) {
-            if (a_mode == A_TMA) ptx::tma_prefetch(&args.p[i].tma_a);
+            if (a_mode == A_TMA || a_mode == A_GATE_TMA) ptx::tma_prefetch(&args.p[i].tma_a);
+            if (a_mode == A_GATE_TMA) ptx::tma_prefetch(&args.p[i].tma_u);
             ptx::tma_prefetch(&args.p[i].tma_b);
         }
     }
@@ -358,6 +365,22 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                     uint8_t* sb = sa + KS * C::A_BYTES;
                     const bool skip_a = args.debug & 8;  // timing experiment: no A loads
                     const bool bias_here = !args.b_res && p_bias && kb + KS >= kblocks;  // streaming: bias tile with the last stage
+                    if (a_mode == A_GATE_TMA) {
+                        // raw A and U k-blocks (+ B when streaming) -> raw_bar; the transform
+                        // warps rewrite A in place and arrive on full_bar
+                        uint8_t* sbg = sa + 2 * C::A_BYTES;
+                        ptx::mbar_arrive_expect_tx(&raw_bar[stage], 2 * C::A_BYTES + (args.b_res ? 0 : C::B_BYTES) +
+                                                                        (bias_here ? BN * 32 : 0));
+                        ptx::tma_load_2d(sa, &p.tma_a, &raw_bar[stage], kb * C::BK, mb * C::BM);
+                        ptx::tma_load_2d(sa + C::A_BYTES, &p.tma_u, &raw_bar[stage], kb * C::BK, mb * C::BM);
+                        if (!args.b_res) ptx::tma_load_2d(sbg, &p.tma_b, &raw_bar[stage], kb * C::BK, nb * BN);
+                        if (bias_here) ptx::tma_load_2d(sbg + C::B_BYTES, &p.tma_bias, &raw_bar[stage], 0, nb * BN);
+                        if (++stage == n_stages) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
+                        continue;
+                    }
                     const int bytes = (a_mode == A_TMA && !skip_a ? KS * C::A_BYTES : 0) +
                                       (args.b_res ? 0 : KS * C::B_BYTES) + (bias_here ? BN * 32 : 0);
                     if (bytes > 0)
@@ -378,6 +401,64 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                         stage = 0;
                         phase ^= 1;
                     }
+                }
+            }
+        }
+    } else if (warp >= 8 && warp < 12 && a_mode == A_GATE_TMA) {
+        // ------------------------------------------------ gate transform, SMEM -> SMEM
+        // thread = tile row: its 8 A chunks and 8 U chunks (SW128: chunk c of row r
+        // at (c ^ (r & 7))) -> bf16(((a - mu) * rstd * gain[g] + bias[g]) * u) in place
+        const int r = static_cast<int>((warp - 8) * 32 + lane);
+        int stage = 0;
+        uint32_t phase = 0;
+        gemm_detail::TileSeq seq(args, s_tile_start, s_tiles_n);
+        int pi, mb, nb;
+        while (seq.next(args, gemm_detail::decode_tile, pi, mb, nb)) {
+            const GemmProblem& p = args.p[pi];
+            const int kblocks = s_kblocks[pi];
+            const int m = mb * C::BM + r;
+            const bool ok = m < p.M;
+            float2 st = make_float2(0.f, 0.f);
+            int g = 0;
+            if (ok) {
+                st = __ldg(p.stats + m + p.a_row0);
+                g = __ldg(p.row_group + m + p.g_row0);
+                g = g < 0 ? 0 : g;
+            }
+            for (int kb = 0; kb < kblocks; ++kb) {
+                ptx::mbar_wait(&raw_bar[stage], phase);
+                uint8_t* sa = smem + stage * stage_bytes;
+                if (ok) {
+                    uint8_t* arow = sa + r * 128;
+                    const uint8_t* urow = sa + C::A_BYTES + r * 128;
+                    const float* gp = p.gain + (long long)g * p.Kv + kb * C::BK;
+                    const float* bp = p.gbias + (long long)g * p.Kv + kb * C::BK;
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const int off = (c ^ (r & 7)) << 4;
+                        float a8[8], u8[8];
+                        gemm_detail::unpack8(*reinterpret_cast<const uint4*>(arow + off), a8);
+                        gemm_detail::unpack8(*reinterpret_cast<const uint4*>(urow + off), u8);
+                        const float4 g0 = __ldg(reinterpret_cast<const float4*>(gp + 8 * c));
+                        const float4 g1 = __ldg(reinterpret_cast<const float4*>(gp + 8 * c + 4));
+                        const float4 b0 = __ldg(reinterpret_cast<const float4*>(bp + 8 * c));
+                        const float4 b1 = __ldg(reinterpret_cast<const float4*>(bp + 8 * c + 4));
+                        const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+                        const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+                        float y[8];
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) y[e] = (((a8[e] - st.x) * st.y) * gv[e] + bv[e]) * u8[e];
+                        *reinterpret_cast<uint4*>(arow + off) =
+                            make_uint4(pack_bf16(y[0], y[1]), pack_bf16(y[2], y[3]), pack_bf16(y[4], y[5]),
+                                       pack_bf16(y[6], y[7]));
+                    }
+                }
+                ptx::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&full_bar[stage]);
+                if (++stage == n_stages) {
+                    stage = 0;
+                    phase ^= 1;
                 }
             }
         }
@@ -439,7 +520,8 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                 const bool last = kb0 + KS >= kblocks;
                 if (ptx::elect_one()) {
                     const uint32_t sa0 = ptx::smem_u32(smem + stage * stage_bytes);
-                    const uint32_t sb0 = args.b_res ? ptx::smem_u32(bres + kb0 * C::B_BYTES) : sa0 + KS * C::A_BYTES;
+                    const uint32_t sb0 = args.b_res ? ptx::smem_u32(bres + kb0 * C::B_BYTES)
+                                                    : sa0 + KS * C::A_BYTES * (a_mode == A_GATE_TMA ? 2 : 1);
                     for (int kbi = 0; kbi < nk; ++kbi) {
                         const uint32_t sa = sa0 + kbi * C::A_BYTES, sb = sb0 + kbi * C::B_BYTES;
 #pragma unroll
@@ -452,7 +534,8 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                     }
                     if (has_bias && last) {
                         // D += ones(128 x 16) * bias_t(BN x 16)^T: the bias, exact to ~2^-17 (hi + lo)
-                        const uint32_t sbias = args.b_res ? ptx::smem_u32(bres + kblocks * C::B_BYTES) : sa0 + KS * (C::A_BYTES + C::B_BYTES);
+                        const uint32_t sbias = args.b_res ? ptx::smem_u32(bres + kblocks * C::B_BYTES)
+                                                          : sb0 + KS * C::B_BYTES;
                         ptx::umma_bf16(d_tmem, ptx::smem_desc(ptx::smem_u32(ones), 16, 256, 6),
                                        ptx::smem_desc(sbias, 16, 256, 6), idesc, 1u);
                     }

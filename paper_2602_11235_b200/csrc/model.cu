@@ -725,6 +725,10 @@ void run_gemm_tc(std::vector<TcProblem> ps, cudaStream_t st, long long& launches
             if (s.amode != a.a_mode) fail(MTFM_CONTRACT_ERROR, "mixed A modes in one grouped GEMM");
             GemmProblem& p = a.p[a.n_problems++];
             if (s.amode == A_TMA) p.tma_a = ks > 1 ? tma_3d_kb(s.A, s.M, s.K, s.lda, 128, ks) : tma_2d(s.A, s.M, s.K, s.lda, 64, 128, 128);
+            if (s.amode == A_GATE_TMA) {
+                p.tma_a = tma_2d(s.a_src, s.M, s.K, s.lda, 64, 128, 128);
+                p.tma_u = tma_2d(s.u_src, s.M, s.K, s.ldu, 64, 128, 128);
+            }
             // B: 2D boxes for the resident slice (loaded once per CTA), 3D per stage when streaming
             p.tma_b = (ks > 1 && !a.b_res) ? tma_3d_kb(s.Bt, s.N, s.K, s.ldb, bn, ks) : tma_2d(s.Bt, s.N, s.K, s.ldb, 64, bn, 128);
             p.M = s.M;
@@ -792,7 +796,8 @@ void run_gemm_tc(std::vector<TcProblem> ps, cudaStream_t st, long long& launches
         for (int i = 0; i < a.n_problems; ++i) any_bias = any_bias || a.p[i].has_bias;
         a.bias_bytes = any_bias ? bn * 32 : 0;
         a.bres_bytes = a.b_res ? (kmax / 64) * b_bytes + a.bias_bytes : 0;
-        a.stage_bytes = a.b_res ? ks * a_bytes : ks * (a_bytes + b_bytes) + a.bias_bytes;
+        const int a_stage = a.a_mode == A_GATE_TMA ? 2 * a_bytes : a_bytes;  // raw A + U k-blocks
+        a.stage_bytes = a.b_res ? ks * a_stage : ks * (a_stage + b_bytes) + a.bias_bytes;
         // 12 epilogue warps when A is TMA-loaded and >= 3 stages still fit, else 8
         for (int ne : {12, 8, 0}) {
             if (ne == 0) {
@@ -1523,7 +1528,7 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                     StageScope sc(m, "f2_full", 2.0 * Rd * hd * d, Rd * hd * el * 2 + Rd * d * 8);
                     TcProblem tp{nullptr, hd, Lw->tf2.as<__nv_bfloat16>(), hd, static_cast<int>(R), d, hd,
                                  EPI_RESID_F32, Lw->f2b.as<float>(), X, d, nullptr, 0, X};
-                    tp.amode = A_GATE;
+                    tp.amode = A_GATE_TMA;
                     tp.a_src = A;
                     tp.stats = statA;
                     tp.row_group = rm.src;
@@ -1662,7 +1667,7 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                     StageScope sc(m, "f2_target", 2.0 * Td * hd * d, Td * hd * el * 2 + Td * d * 8);
                     TcProblem tp{nullptr, hd, Lw->tf2.as<__nv_bfloat16>(), hd, static_cast<int>(NT), d, hd,
                                  EPI_RESID_F32, Lw->f2b.as<float>(), X, d, nullptr, NE, X};
-                    tp.amode = A_GATE;
+                    tp.amode = A_GATE_TMA;
                     tp.a_src = A;
                     tp.stats = statA;
                     tp.row_group = rm.src;
