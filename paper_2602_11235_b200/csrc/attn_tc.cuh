@@ -153,6 +153,8 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // prologue done (barriers, TMEM, SMEM tables): wait for the producer of our inputs
+    MTFM_PDL_ENTRY();
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer

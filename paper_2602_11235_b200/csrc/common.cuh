@@ -3,6 +3,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -12,6 +13,52 @@ constexpr int kNumSMs = 148;
 
 __host__ __device__ inline long long cdiv(long long a, long long b) { return (a + b - 1) / b; }
 __host__ __device__ inline long long round_up(long long a, long long b) { return cdiv(a, b) * b; }
+
+// ---------------------------------------------------------------- programmatic dependent launch
+// Every kernel of the forward is launched with programmatic stream
+// serialization: the next kernel's CTAs are scheduled as the predecessor's
+// CTAs retire, run their prologue (barrier init, TMEM allocation, SMEM
+// tables), and block in griddepcontrol.wait until the predecessor grid has
+// completed and its writes are visible: launch latency and prologues overlap
+// the predecessor's tail.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Measured: an explicit early trigger lets dependents flood the SMs while the
+// persistent predecessor still runs (2% slower); without it the dependent grid
+// is released as the predecessor's CTAs retire (2% faster than no PDL).
+__device__ __forceinline__ void pdl_trigger() {
+#ifdef MTFM_PDL_EARLY_TRIGGER
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+// entry of a kernel that reads predecessor outputs from its first instruction on
+#define MTFM_PDL_ENTRY()     \
+    do {                     \
+        ::mtfm::pdl_wait();    \
+        ::mtfm::pdl_trigger(); \
+    } while (0)
+
+inline bool pdl_enabled() {  // MTFM_PDL=0 switches it off (A/B timing)
+    static const bool on = [] {
+        const char* e = std::getenv("MTFM_PDL");
+        return e == nullptr || std::atoi(e) != 0;
+    }();
+    return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);

@@ -332,7 +332,9 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    if (threadIdx.x == 0) trace(1);
+    if (threadIdx.x == 0) trace(1);    // prologue done (barriers, TMEM, SMEM tables): wait for the producer of our inputs
+    MTFM_PDL_ENTRY();
+
 
     if (warp == kWarpTma) {
         // ------------------------------------------------ TMA producer (B, and A in A_TMA mode)

@@ -108,6 +108,7 @@ __device__ __forceinline__ float row_scale_of(int norm, int c, int n_tokens) {
 // One CTA per user: plan_tokens (tokenizer.hpp:53-134) + make_stack_geom
 // (hta.hpp:40-71) in prefix form + record slots + input validation.
 __global__ void plan_kernel(PlanArgs a) {
+    MTFM_PDL_ENTRY();
     extern __shared__ long long sm_sort[];
     long long* s_ts = sm_sort;
     long long* s_sec = sm_sort + a.max_sort;
@@ -306,7 +307,7 @@ void launch_plan(const PlanArgs& a, int smem_elems, cudaStream_t st) {
     if (a.b.n_users == 0) return;
     const size_t smem = static_cast<size_t>(smem_elems) * 16;
     cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    plan_kernel<<<a.b.n_users, 256, smem, st>>>(a);
+    launch_k(plan_kernel, dim3(a.b.n_users), dim3(256), smem, st, a);
 }
 
 // ---------------------------------------------------------------- gather
@@ -316,6 +317,7 @@ __global__ void gather_kernel(DevBatch b, const SourceInfo* __restrict__ srcs, c
                               const long long* __restrict__ src_base, const long long* __restrict__ src_cnt,
                               const long long* __restrict__ emb_base, const T* __restrict__ tables, int d_emb,
                               int n_src, long long total_rows, int max_slots, T* __restrict__ out) {
+    MTFM_PDL_ENTRY();
     const long long n_items = total_rows * (max_slots + 1);
     for (long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x; w < n_items;
          w += (long long)gridDim.x * blockDim.x) {
@@ -366,7 +368,7 @@ void launch_gather(const DevBatch& b, const SourceInfo* src_dev, const SlotInfo*
     if (total_rows == 0) return;
     const long long n = total_rows * (max_slots + 1);
     const int blocks = static_cast<int>(std::min<long long>(cdiv(n, 256), 148ll * 16));
-    gather_kernel<T><<<blocks, 256, 0, st>>>(b, src_dev, slots_dev, rm.src_rows, rm.item, src_base_dev, src_cnt_dev,
+    launch_k(gather_kernel<T>, dim3(blocks), dim3(256), 0, st, b, src_dev, slots_dev, rm.src_rows, rm.item, src_base_dev, src_cnt_dev,
                                              emb_base_dev, tables, d_emb, n_src, total_rows, max_slots, out);
 }
 template void launch_gather<float>(const DevBatch&, const SourceInfo*, const SlotInfo*, const RowMeta&,
@@ -435,6 +437,7 @@ __global__ void __launch_bounds__(256) gln_kernel(const float* __restrict__ x, l
                                                   long long n_rows, int d, const int* __restrict__ row_src,
                                                   const float* __restrict__ gain, const float* __restrict__ bias,
                                                   float eps, T* __restrict__ out, long long ldo) {
+    MTFM_PDL_ENTRY();
     const int lane = threadIdx.x & 31;
     const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
     for (long long i = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); i < n_rows; i += warps) {
@@ -471,10 +474,10 @@ void launch_gln(const float* x, long long ldx, long long r0, long long n_rows, i
     if (n_rows == 0) return;
     const int blocks = static_cast<int>(std::min<long long>(cdiv(n_rows, 8), 148ll * 16));
     const int ns = static_cast<int>(cdiv(d, 128));
-    if (ns <= 1) gln_kernel<T, 1><<<blocks, 256, 0, st>>>(x, ldx, r0, n_rows, d, row_src, gain, bias, eps, out, ldo);
-    else if (ns == 2) gln_kernel<T, 2><<<blocks, 256, 0, st>>>(x, ldx, r0, n_rows, d, row_src, gain, bias, eps, out, ldo);
-    else if (ns <= 4) gln_kernel<T, 4><<<blocks, 256, 0, st>>>(x, ldx, r0, n_rows, d, row_src, gain, bias, eps, out, ldo);
-    else gln_kernel<T, 8><<<blocks, 256, 0, st>>>(x, ldx, r0, n_rows, d, row_src, gain, bias, eps, out, ldo);
+    if (ns <= 1) launch_k(gln_kernel<T, 1>, dim3(blocks), dim3(256), 0, st, x, ldx, r0, n_rows, d, row_src, gain, bias, eps, out, ldo);
+    else if (ns == 2) launch_k(gln_kernel<T, 2>, dim3(blocks), dim3(256), 0, st, x, ldx, r0, n_rows, d, row_src, gain, bias, eps, out, ldo);
+    else if (ns <= 4) launch_k(gln_kernel<T, 4>, dim3(blocks), dim3(256), 0, st, x, ldx, r0, n_rows, d, row_src, gain, bias, eps, out, ldo);
+    else launch_k(gln_kernel<T, 8>, dim3(blocks), dim3(256), 0, st, x, ldx, r0, n_rows, d, row_src, gain, bias, eps, out, ldo);
 }
 template void launch_gln<float>(const float*, long long, long long, long long, int, const int*, const float*,
                                 const float*, float, float*, long long, cudaStream_t);
@@ -486,6 +489,7 @@ template <int NS>
 __global__ void __launch_bounds__(256) gln_multi_kernel(const float* __restrict__ x, long long ldx, long long n_rows,
                                                         int d, const int* __restrict__ row_src,
                                                         const __grid_constant__ GlnCopies c, float eps, long long ldo) {
+    MTFM_PDL_ENTRY();
     const int lane = threadIdx.x & 31;
     const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
     for (long long r = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); r < n_rows; r += warps) {
@@ -522,10 +526,10 @@ void launch_gln_multi_bf16(const float* x, long long ldx, long long n_rows, int 
     if (n_rows == 0 || c.n == 0) return;
     const int blocks = static_cast<int>(std::min<long long>(cdiv(n_rows, 8), 148ll * 16));
     const int ns = static_cast<int>(cdiv(d, 128));
-    if (ns <= 1) gln_multi_kernel<1><<<blocks, 256, 0, st>>>(x, ldx, n_rows, d, row_src, c, eps, ldo);
-    else if (ns == 2) gln_multi_kernel<2><<<blocks, 256, 0, st>>>(x, ldx, n_rows, d, row_src, c, eps, ldo);
-    else if (ns <= 4) gln_multi_kernel<4><<<blocks, 256, 0, st>>>(x, ldx, n_rows, d, row_src, c, eps, ldo);
-    else gln_multi_kernel<8><<<blocks, 256, 0, st>>>(x, ldx, n_rows, d, row_src, c, eps, ldo);
+    if (ns <= 1) launch_k(gln_multi_kernel<1>, dim3(blocks), dim3(256), 0, st, x, ldx, n_rows, d, row_src, c, eps, ldo);
+    else if (ns == 2) launch_k(gln_multi_kernel<2>, dim3(blocks), dim3(256), 0, st, x, ldx, n_rows, d, row_src, c, eps, ldo);
+    else if (ns <= 4) launch_k(gln_multi_kernel<4>, dim3(blocks), dim3(256), 0, st, x, ldx, n_rows, d, row_src, c, eps, ldo);
+    else launch_k(gln_multi_kernel<8>, dim3(blocks), dim3(256), 0, st, x, ldx, n_rows, d, row_src, c, eps, ldo);
 }
 
 template <typename T, int NS>
@@ -534,6 +538,7 @@ __global__ void __launch_bounds__(256) gate_kernel(const T* __restrict__ a, long
                                                    const int* __restrict__ row_src, const float* __restrict__ gain,
                                                    const float* __restrict__ bias, float eps, T* __restrict__ out,
                                                    long long ldo) {
+    MTFM_PDL_ENTRY();
     const int lane = threadIdx.x & 31;
     const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
     for (long long i = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); i < n_rows; i += warps) {
@@ -576,6 +581,7 @@ __global__ void __launch_bounds__(256, 4) gate_bf16_d256_kernel(const __nv_bfloa
                                                              const float* __restrict__ gain,
                                                              const float* __restrict__ bias, float eps,
                                                              __nv_bfloat16* __restrict__ out, long long ldo) {
+    MTFM_PDL_ENTRY();
     const int lane = threadIdx.x & 31;
     const int c = 8 * lane;
     const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
@@ -652,14 +658,14 @@ void launch_gate(const T* a, long long lda, const T* u, long long ldu, long long
     if constexpr (std::is_same_v<T, __nv_bfloat16>) {
         if (d == 256 && lda % 8 == 0 && ldu % 8 == 0 && ldo % 8 == 0) {
             const int blocks = static_cast<int>(std::min<long long>(cdiv(n_rows, 8 * 2), 148ll * 16));
-            gate_bf16_d256_kernel<2><<<blocks, 256, 0, st>>>(a, lda, u, ldu, n_rows, row_src_of_rows, gain, bias,
+            launch_k(gate_bf16_d256_kernel<2>, dim3(blocks), dim3(256), 0, st, a, lda, u, ldu, n_rows, row_src_of_rows, gain, bias,
                                                              eps, out, ldo);
             return;
         }
     }
     const int blocks = static_cast<int>(std::min<long long>(cdiv(n_rows, 8), 148ll * 16));
     const int ns = static_cast<int>(cdiv(d, 128));
-#define MTFM_GATE(NS) gate_kernel<T, NS><<<blocks, 256, 0, st>>>(a, lda, u, ldu, n_rows, d, row_src_of_rows, gain, bias, eps, out, ldo)
+#define MTFM_GATE(NS) launch_k(gate_kernel<T, NS>, dim3(blocks), dim3(256), 0, st, a, lda, u, ldu, n_rows, d, row_src_of_rows, gain, bias, eps, out, ldo)
     if (ns <= 1) MTFM_GATE(1);
     else if (ns == 2) MTFM_GATE(2);
     else if (ns <= 4) MTFM_GATE(4);
@@ -675,6 +681,7 @@ template void launch_gate<__nv_bfloat16>(const __nv_bfloat16*, long long, const 
 template <typename T, int NS>
 __global__ void __launch_bounds__(256) row_stats_kernel(const T* __restrict__ x, long long ldx, long long n_rows,
                                                         int d, float eps, float2* __restrict__ out) {
+    MTFM_PDL_ENTRY();
     const int lane = threadIdx.x & 31;
     const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
     for (long long i = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); i < n_rows; i += warps) {
@@ -709,10 +716,10 @@ void launch_row_stats(const T* x, long long ldx, long long n_rows, int d, float 
     if (n_rows == 0) return;
     const int blocks = static_cast<int>(std::min<long long>(cdiv(n_rows, 8), 148ll * 16));
     const int ns = static_cast<int>(cdiv(d, 128));
-    if (ns <= 1) row_stats_kernel<T, 1><<<blocks, 256, 0, st>>>(x, ldx, n_rows, d, eps, out);
-    else if (ns == 2) row_stats_kernel<T, 2><<<blocks, 256, 0, st>>>(x, ldx, n_rows, d, eps, out);
-    else if (ns <= 4) row_stats_kernel<T, 4><<<blocks, 256, 0, st>>>(x, ldx, n_rows, d, eps, out);
-    else row_stats_kernel<T, 8><<<blocks, 256, 0, st>>>(x, ldx, n_rows, d, eps, out);
+    if (ns <= 1) launch_k(row_stats_kernel<T, 1>, dim3(blocks), dim3(256), 0, st, x, ldx, n_rows, d, eps, out);
+    else if (ns == 2) launch_k(row_stats_kernel<T, 2>, dim3(blocks), dim3(256), 0, st, x, ldx, n_rows, d, eps, out);
+    else if (ns <= 4) launch_k(row_stats_kernel<T, 4>, dim3(blocks), dim3(256), 0, st, x, ldx, n_rows, d, eps, out);
+    else launch_k(row_stats_kernel<T, 8>, dim3(blocks), dim3(256), 0, st, x, ldx, n_rows, d, eps, out);
 }
 template void launch_row_stats<float>(const float*, long long, long long, int, float, float2*, cudaStream_t);
 template void launch_row_stats<__nv_bfloat16>(const __nv_bfloat16*, long long, long long, int, float, float2*,
@@ -720,6 +727,7 @@ template void launch_row_stats<__nv_bfloat16>(const __nv_bfloat16*, long long, l
 
 __global__ void to_bf16_kernel(const float* __restrict__ x, long long n_rows, int d, __nv_bfloat16* __restrict__ out,
                                long long ldo) {
+    MTFM_PDL_ENTRY();
     const long long n = n_rows * d;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         const long long r = i / d;
@@ -730,7 +738,7 @@ __global__ void to_bf16_kernel(const float* __restrict__ x, long long n_rows, in
 void launch_to_bf16(const float* x, long long n_rows, int d, __nv_bfloat16* out, long long ldo, cudaStream_t st) {
     if (n_rows == 0) return;
     const int blocks = static_cast<int>(std::min<long long>(cdiv(n_rows * d, 256), 148ll * 16));
-    to_bf16_kernel<<<blocks, 256, 0, st>>>(x, n_rows, d, out, ldo);
+    launch_k(to_bf16_kernel, dim3(blocks), dim3(256), 0, st, x, n_rows, d, out, ldo);
 }
 
 // ---------------------------------------------------------------- heads
@@ -741,6 +749,7 @@ void launch_to_bf16(const float* x, long long n_rows, int d, __nv_bfloat16* out,
 constexpr int kMaxTasks = 8;
 
 __global__ void __launch_bounds__(256) heads_kernel(HeadArgs a) {
+    MTFM_PDL_ENTRY();
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     __shared__ float s_gate[8][kMaxTasks][32];
@@ -823,6 +832,7 @@ __global__ void __launch_bounds__(256) heads_kernel(HeadArgs a) {
 // task's gate mix and tower dot product reuse them.
 template <int E, int NJ>
 __global__ void __launch_bounds__(256) heads_fast_kernel(HeadArgs a, int n_tasks_total) {
+    MTFM_PDL_ENTRY();
     extern __shared__ float hsm[];
     const int de = NJ * 128;
     float* s_eb = hsm;                          // [E*de]
@@ -923,7 +933,7 @@ bool try_heads_fast(const HeadArgs& a, int n_tasks_total, cudaStream_t st) {
         attr_set = static_cast<int>(smem);
     }
     const int blocks = static_cast<int>(std::min<long long>(cdiv(a.n_t, 8), 148ll * 4));
-    heads_fast_kernel<E, NJ><<<blocks, 256, smem, st>>>(a, n_tasks_total);
+    launch_k(heads_fast_kernel<E, NJ>, dim3(blocks), dim3(256), smem, st, a, n_tasks_total);
     return true;
 }
 
@@ -936,7 +946,7 @@ void launch_heads(const HeadArgs& a, cudaStream_t st, int n_tasks_total) {
          try_heads_fast<3, 2>(a, n_tasks_total, st)))
         return;
     const int blocks = static_cast<int>(std::min<long long>(cdiv(a.n_t, 8), 148ll * 32));
-    heads_kernel<<<blocks, 256, 0, st>>>(a);
+    launch_k(heads_kernel, dim3(blocks), dim3(256), 0, st, a);
 }
 
 // ---------------------------------------------------------------- SIMT GEMM (check mode)
@@ -946,6 +956,7 @@ struct SimtGemmBatch {
 };
 
 __global__ void __launch_bounds__(256) gemm_simt_kernel(const __grid_constant__ SimtGemmBatch bt) {
+    MTFM_PDL_ENTRY();
     const SimtGemm& p = bt.p[blockIdx.z];
     const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
     if (m0 >= p.M || n0 >= p.N) return;
@@ -1004,13 +1015,14 @@ void launch_gemm_simt(const SimtGemm* probs, int n, cudaStream_t st) {
     }
     bt.n = n;
     if (gm == 0 || gn == 0) return;
-    gemm_simt_kernel<<<dim3(gn, gm, n), 256, 0, st>>>(bt);
+    launch_k(gemm_simt_kernel, dim3(dim3(gn, gm, n)), dim3(256), 0, st, bt);
 }
 
 // ---------------------------------------------------------------- SIMT attention (check mode)
 // One warp per (query row, head); keys in order j = 0.. prefix-1 (gemm_nn
 // accumulation order of hta.hpp:128-131), then the T self key.
 __global__ void attn_simt_kernel(SimtAttn a) {
+    MTFM_PDL_ENTRY();
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     extern __shared__ float q_sm[];
@@ -1076,7 +1088,7 @@ void launch_attn_simt(const SimtAttn& a, cudaStream_t st) {
     if (a.n_q == 0) return;
     const int wpb = 8;
     const int blocks = static_cast<int>(std::min<long long>(cdiv(a.n_q * a.heads, wpb), 148ll * 64));
-    attn_simt_kernel<<<blocks, wpb * 32, wpb * a.dh * sizeof(float), st>>>(a);
+    launch_k(attn_simt_kernel, dim3(blocks), dim3(wpb * 32), wpb * a.dh * sizeof(float), st, a);
 }
 
 }  // namespace mtfm

@@ -179,6 +179,7 @@ struct PinnedBuf {
 // Bias tiles for the tensor-core GEMM: bias_t[n] = (hi, lo, 0 x 14) in bf16 with
 // hi + lo = bias[n] to ~2^-17, added by one K=16 MMA against a ones tile.
 __global__ void bias_tile_kernel(const float* __restrict__ bias, int N, __nv_bfloat16* __restrict__ t) {
+    MTFM_PDL_ENTRY();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N * 16) return;
     const int n = i >> 4, c = i & 15;
@@ -544,7 +545,7 @@ void launch_gemm_tc_bn(GemmArgs& a, int grid, cudaStream_t st) {
     }
     const int smem = 1024 + a.bres_bytes + 4096 + a.n_stages * a.stage_bytes + a.n_epi * a.stg_warp + C::BAR_BYTES;
     if (smem > C::kMaxSmem) fail(MTFM_CONTRACT_ERROR, "gemm smem plan exceeds 227 KB");
-    gemm_tc_kernel<BN><<<grid, C::kThreads, smem, st>>>(a);
+    launch_k(gemm_tc_kernel<BN>, dim3(grid), dim3(C::kThreads), smem, st, a);
     ck(cudaGetLastError(), "gemm_tc launch");
 }
 
@@ -563,7 +564,7 @@ void launch_tok_fused(const TokArgs& a, cudaStream_t st) {
         ck(cudaMemsetAsync(tr, 0, 1024 * 8, st), "trace clear");
         aa.trace = tr;
     }
-    tok_fused_kernel<<<std::min(a.n_tiles, kNumSMs), 512, tok_detail::SMEM, st>>>(aa);
+    launch_k(tok_fused_kernel, dim3(std::min(a.n_tiles, kNumSMs)), dim3(512), tok_detail::SMEM, st, aa);
     ck(cudaGetLastError(), "tok_fused launch");
     if (tracing) {
         unsigned long long h[1024];
@@ -872,6 +873,7 @@ void run_gemm_simt(std::vector<SimtGemm> ps, cudaStream_t st, long long& launche
 
 // ---------------------------------------------------------------- attention helpers
 __global__ void tile_kmax_kernel(AttnTile* tiles, int n, const int* prefix, int rt_unused) {
+    MTFM_PDL_ENTRY();
     const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (t >= n) return;
@@ -902,7 +904,7 @@ void launch_attn_tc_d(const AttnParams& p, cudaStream_t st) {
         attr = true;
     }
     const int grid = std::min(p.n_tiles, kNumSMs);
-    attn_tc_kernel<D><<<grid, C::kThreads, C::SMEM, st>>>(p);
+    launch_k(attn_tc_kernel<D>, dim3(grid), dim3(C::kThreads), C::SMEM, st, p);
     ck(cudaGetLastError(), "attn_tc launch");
 }
 
@@ -972,6 +974,7 @@ __global__ void tile_expand_kernel(const long long* __restrict__ toff, const int
                                    const int* __restrict__ ev_off, const int* __restrict__ exp_off, int n_users,
                                    int n_seqs, long long n_events, int rt, int hs, int r, int G,
                                    AttnTile* __restrict__ tf, AttnTile* __restrict__ tt) {
+    MTFM_PDL_ENTRY();
     const int u = blockIdx.x;
     if (u >= n_users) return;
     const long long ev0 = n_seqs ? ev_off[seq_off[u]] : 0, ev1 = n_seqs ? ev_off[seq_off[u + 1]] : 0;
@@ -1928,6 +1931,7 @@ void launch_sum_valid(mtfm_cuda_batch& B, cudaStream_t st);
 // Algorithmic FLOPs of the run: projections per complexity.hpp:54-64,
 // mask-aware attention 4*d_h*H*sum(c_i) per layer, tokenizer MLPs, heads.
 __global__ void sum_valid_kernel(const int* prefix, const int* self, long long n, unsigned long long* out) {
+    MTFM_PDL_ENTRY();
     unsigned long long s = 0;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
         s += static_cast<unsigned long long>(prefix[i] + (self[i] >= 0 ? 1 : 0));
@@ -1940,9 +1944,9 @@ void launch_sum_valid(mtfm_cuda_batch& B, cudaStream_t st) {
     ck(cudaMemsetAsync(B.stat_buf.p, 0, 16, st), "memset stats");
     auto* a = B.stat_buf.as<unsigned long long>();
     if (B.n_events)
-        sum_valid_kernel<<<64, 256, 0, st>>>(B.r_prefix.as<int>(), B.r_self.as<int>(), B.n_events, a);
+        launch_k(sum_valid_kernel, dim3(64), dim3(256), 0, st, B.r_prefix.as<int>(), B.r_self.as<int>(), B.n_events, a);
     if (B.n_exp)
-        sum_valid_kernel<<<64, 256, 0, st>>>(B.r_prefix.as<int>() + B.n_events, B.r_self.as<int>() + B.n_events,
+        launch_k(sum_valid_kernel, dim3(64), dim3(256), 0, st, B.r_prefix.as<int>() + B.n_events, B.r_self.as<int>() + B.n_events,
                                              B.n_exp, a + 1);
 }
 

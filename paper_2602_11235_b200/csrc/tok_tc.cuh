@@ -148,6 +148,8 @@ __global__ void __launch_bounds__(512, 1) tok_fused_kernel(const __grid_constant
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // prologue done (barriers, TMEM, SMEM tables): wait for the producer of our inputs
+    MTFM_PDL_ENTRY();
 
     // Y drain, shared by all 12 epilogue warps once a tile's GEMM2 is done:
     // warp (quarter q, slot ds of 3) takes column blocks cb = ds, ds + 3, ...
