@@ -402,14 +402,16 @@ __device__ __forceinline__ void st4(__nv_bfloat16* p, float4 v) {
 }
 
 // Normalises the row held as float4 slices (c = 128*i + 4*lane) in place.
-template <int NS>
+template <int NS, bool kFast = false>
 __device__ __forceinline__ void normalize_slices(float4 (&v)[NS], int d, int lane, float eps) {
     float s = 0.f;
 #pragma unroll
     for (int i = 0; i < NS; ++i)
         if (128 * i + 4 * lane < d) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
     s = warp_sum(s);
-    const float mean = __fdiv_rn(s, static_cast<float>(d));
+    // kFast (bf16 outputs): multiply by the rounded reciprocal (exact for power-of-two d)
+    const float rd = kFast ? 1.f / static_cast<float>(d) : 0.f;
+    const float mean = kFast ? s * rd : __fdiv_rn(s, static_cast<float>(d));
     float q = 0.f;
 #pragma unroll
     for (int i = 0; i < NS; ++i)
@@ -421,8 +423,8 @@ __device__ __forceinline__ void normalize_slices(float4 (&v)[NS], int d, int lan
             q += (v[i].x * v[i].x + v[i].y * v[i].y) + (v[i].z * v[i].z + v[i].w * v[i].w);
         }
     q = warp_sum(q);
-    const float var = __fdiv_rn(q, static_cast<float>(d));
-    const float inv = __fdiv_rn(1.f, sqrtf(var + eps));
+    const float var = kFast ? q * rd : __fdiv_rn(q, static_cast<float>(d));
+    const float inv = kFast ? rsqrtf(var + eps) : __fdiv_rn(1.f, sqrtf(var + eps));
 #pragma unroll
     for (int i = 0; i < NS; ++i) {
         v[i].x *= inv;
@@ -450,7 +452,7 @@ __global__ void __launch_bounds__(256) gln_kernel(const float* __restrict__ x, l
             const int c = 128 * k + 4 * lane;
             v[k] = c < d ? __ldcs(reinterpret_cast<const float4*>(xr + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        normalize_slices<NS>(v, d, lane, eps);
+        normalize_slices<NS, std::is_same_v<T, __nv_bfloat16>>(v, d, lane, eps);
         g = g < 0 ? 0 : g;
         const float* gg = gain + (long long)g * d;
         const float* bb = bias + (long long)g * d;
@@ -501,7 +503,7 @@ __global__ void __launch_bounds__(256) gln_multi_kernel(const float* __restrict_
             const int col = 128 * k + 4 * lane;
             v[k] = col < d ? __ldcs(reinterpret_cast<const float4*>(xr + col)) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        normalize_slices<NS>(v, d, lane, eps);
+        normalize_slices<NS, true>(v, d, lane, eps);
         g = g < 0 ? 0 : g;
         for (int l = 0; l < c.n; ++l) {
             const float* gg = c.gain[l] + (long long)g * d;
@@ -553,7 +555,7 @@ __global__ void __launch_bounds__(256) gate_kernel(const T* __restrict__ a, long
             v[k] = ok ? ld4(ar + c) : make_float4(0.f, 0.f, 0.f, 0.f);
             uu[k] = ok ? ld4(ur + c) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        normalize_slices<NS>(v, d, lane, eps);
+        normalize_slices<NS, std::is_same_v<T, __nv_bfloat16>>(v, d, lane, eps);
         g = g < 0 ? 0 : g;
         const float* gg = gain + (long long)g * d;
         const float* bb = bias + (long long)g * d;
@@ -620,7 +622,7 @@ __global__ void __launch_bounds__(256, 4) gate_bf16_d256_kernel(const __nv_bfloa
 #pragma unroll
             for (int k = 0; k < 8; ++k) sum += x[k];
             sum = warp_sum(sum);
-            const float mean = __fdiv_rn(sum, 256.f);
+            const float mean = sum * (1.f / 256.f);  // exact: power-of-two divisor
             float q = 0.f;
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
@@ -628,7 +630,8 @@ __global__ void __launch_bounds__(256, 4) gate_bf16_d256_kernel(const __nv_bfloa
                 q += x[k] * x[k];
             }
             q = warp_sum(q);
-            const float inv = __fdiv_rn(1.f, sqrtf(__fdiv_rn(q, 256.f) + eps));
+            // bf16 output: MUFU.RSQ (~2 ulp) instead of the IEEE sqrt + divide sequence
+            const float inv = rsqrtf(q * (1.f / 256.f) + eps);
             if (i >= n_rows) continue;
             const int gg = g[r] < 0 ? 0 : g[r];
             const float4 g0 = __ldg(reinterpret_cast<const float4*>(gain + gg * 256 + c));

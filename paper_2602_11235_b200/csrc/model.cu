@@ -666,6 +666,14 @@ void run_gemm_tc(std::vector<TcProblem> ps, cudaStream_t st, long long& launches
     static const int force_stages = std::getenv("MTFM_GEMM_STAGES") ? std::atoi(std::getenv("MTFM_GEMM_STAGES")) : 0;
     static const int force_epi = std::getenv("MTFM_GEMM_EPI") ? std::atoi(std::getenv("MTFM_GEMM_EPI")) : 0;
     int bn_res = stream_only ? 0 : pick_bn_resident(ps);
+    // small launches (a few tiles per CTA): loading a resident weight slice per
+    // CTA costs more than streaming B with the A stages
+    static const long long small_tiles = std::getenv("MTFM_GEMM_SMALL") ? std::atoll(std::getenv("MTFM_GEMM_SMALL")) : 0;
+    if (bn_res && small_tiles > 0) {
+        long long t = 0;
+        for (const auto& p : ps) t += cdiv(p.M, 128) * cdiv(p.N, bn_res);
+        if (t < small_tiles) bn_res = 0;
+    }
     if (bn_res && force_bn) bn_res = force_bn;
     for (size_t i0 = 0; i0 < ps.size(); i0 += kMaxProblems) {
         const size_t i1 = std::min(ps.size(), i0 + kMaxProblems);
