@@ -317,34 +317,45 @@ __global__ void gather_kernel(DevBatch b, const SourceInfo* __restrict__ srcs, c
                               const long long* __restrict__ src_base, const long long* __restrict__ src_cnt,
                               const long long* __restrict__ emb_base, const T* __restrict__ tables, int d_emb,
                               int n_src, long long total_rows, int max_slots, T* __restrict__ out) {
+    // source tables in SMEM (n_src <= 32); 32-bit item math (n_items < 2^31, checked on the host)
+    __shared__ long long s_base[33], s_cnt[32], s_emb[32];
+    __shared__ SourceInfo s_src[32];
+    for (int i = threadIdx.x; i < n_src; i += blockDim.x) {
+        s_base[i] = src_base[i];
+        s_cnt[i] = src_cnt[i];
+        s_emb[i] = emb_base[i];
+        s_src[i] = srcs[i];
+    }
+    if (threadIdx.x == 0) s_base[n_src] = total_rows;
     MTFM_PDL_ENTRY();
-    const long long n_items = total_rows * (max_slots + 1);
-    for (long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x; w < n_items;
-         w += (long long)gridDim.x * blockDim.x) {
-        const long long P = w / (max_slots + 1);
-        const int k = static_cast<int>(w - P * (max_slots + 1));
+    __syncthreads();
+    const unsigned per = static_cast<unsigned>(max_slots + 1);
+    const unsigned n_items = static_cast<unsigned>(total_rows) * per;
+    for (unsigned w = blockIdx.x * blockDim.x + threadIdx.x; w < n_items; w += gridDim.x * blockDim.x) {
+        const unsigned P = w / per;
+        const int k = static_cast<int>(w - P * per);
         int s = 0;
-        while (s + 1 < n_src && P >= src_base[s + 1]) ++s;
-        const long long p = P - src_base[s];
-        if (p >= src_cnt[s]) continue;
-        const SourceInfo si = srcs[s];
+        while (s + 1 < n_src && static_cast<long long>(P) >= s_base[s + 1]) ++s;
+        const long long p = static_cast<long long>(P) - s_base[s];
+        if (p >= s_cnt[s]) continue;
+        const SourceInfo& si = s_src[s];
         const int nslots = si.nslot[0] + si.nslot[1] + si.nslot[2];
-        T* orow = out + emb_base[s] + p * si.k_pad;
+        T* orow = out + s_emb[s] + p * si.k_pad;
         if (k == nslots) {  // zero padding columns
             for (int c = si.k_in; c < si.k_pad; ++c) orow[c] = from_f32<T>(0.f);
             continue;
         }
         if (k > nslots) continue;
-        const int row = src_rows[P];
-        const int item = row_item[row];
+        const int row = __ldg(src_rows + P);
+        const int item = __ldg(row_item + row);
         int id;
         if (si.kind < 2) {
-            id = b.ev_feats[b.ev_feat_off[item] + k];
+            id = __ldg(b.ev_feats + __ldg(b.ev_feat_off + item) + k);
         } else {
-            const int nu = b.exp_blk[3 * item], nc = b.exp_blk[3 * item + 1];
+            const int nu = __ldg(b.exp_blk + 3 * item), nc = __ldg(b.exp_blk + 3 * item + 1);
             const int off = k < si.nslot[0] ? k : (k < si.nslot[0] + si.nslot[1] ? nu + (k - si.nslot[0])
                                                                                   : nu + nc + (k - si.nslot[0] - si.nslot[1]));
-            id = b.exp_feats[b.exp_feat_off[item] + off];
+            id = __ldg(b.exp_feats + __ldg(b.exp_feat_off + item) + off);
         }
         const SlotInfo sl = slots[si.slot0 + k];
         id = id < 0 ? 0 : (id >= sl.vocab ? sl.vocab - 1 : id);  // invalid ids were reported by the plan
@@ -367,7 +378,13 @@ void launch_gather(const DevBatch& b, const SourceInfo* src_dev, const SlotInfo*
                    cudaStream_t st) {
     if (total_rows == 0) return;
     const long long n = total_rows * (max_slots + 1);
-    const int blocks = static_cast<int>(std::min<long long>(cdiv(n, 256), 148ll * 16));
+    if (n >= (1ll << 31) || n_src > 32) {
+        std::fprintf(stderr, "gather: %lld items / %d sources exceed the kernel's 32-bit indexing\n", n, n_src);
+        std::abort();
+    }
+    // one item per thread where possible: the dependent load chain per item
+    // (row -> item -> feature offset -> id -> table row) is latency-bound
+    const int blocks = static_cast<int>(std::min<long long>(cdiv(n, 256), 148ll * 64));
     launch_k(gather_kernel<T>, dim3(blocks), dim3(256), 0, st, b, src_dev, slots_dev, rm.src_rows, rm.item, src_base_dev, src_cnt_dev,
                                              emb_base_dev, tables, d_emb, n_src, total_rows, max_slots, out);
 }

@@ -1345,6 +1345,8 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
         tok_in += static_cast<double>(B.src_cnt[s]) * m.sources[s].k_pad;
     }
     {
+        if (tok_rows * (max_slots + 1) >= (1ll << 31) || n_src > 32)
+            fail(MTFM_CONTRACT_ERROR, "batch too large for one forward (tokens x slots >= 2^31)");
         StageScope sc(m, "gather", 0, tok_in * el * 2);
         launch_gather<T>(pa.b, pa.src, pa.slots, rm, B.d_src_base.as<long long>(), B.d_src_cnt.as<long long>(),
                          B.d_emb_base.as<long long>(),
