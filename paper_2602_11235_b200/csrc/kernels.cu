@@ -114,6 +114,19 @@ __global__ void plan_kernel(PlanArgs a) {
     long long* s_sec = sm_sort + a.max_sort;
     __shared__ unsigned long long s_err;
     __shared__ int s_lh;
+    // per-CTA copies: the source table (find_source from SMEM) and, for the T
+    // tokens, a per-source histogram (records / pieces before a scenario)
+    constexpr int kMaxSrcSm = 32;
+    __shared__ SourceInfo s_srcs[kMaxSrcSm];
+    __shared__ int s_tcnt[kMaxSrcSm];
+    __shared__ int s_t_unknown;  // a T token without a source: exact slow path (error ordering)
+    const bool src_sm = a.n_src <= kMaxSrcSm;
+    for (int i = threadIdx.x; i < a.n_src && i < kMaxSrcSm; i += blockDim.x) {
+        s_srcs[i] = a.src[i];
+        s_tcnt[i] = 0;
+    }
+    if (threadIdx.x == 0) s_t_unknown = 0;
+    const SourceInfo* srcs = src_sm ? s_srcs : a.src;
     const DevBatch& b = a.b;
     const int u = blockIdx.x;
     const int tid = threadIdx.x;
@@ -164,7 +177,7 @@ __global__ void plan_kernel(PlanArgs a) {
         const int kind = static_cast<int>(s_sec[i] >> 32);
         const int e = ev0 + local;
         const int sq = find_seq(b.ev_off, s0, s1, e);
-        const int src = find_source(a.src, a.n_src, kind, b.seq_schema[sq], -1);
+        const int src = find_source(srcs, a.n_src, kind, b.seq_schema[sq], -1);
         const int row = e - local + i;  // == ev0 + i
         const int prefix = l_h + count_below(r_ts, l_r, s_ts[i]);
         a.rm.src[row] = src;
@@ -186,7 +199,7 @@ __global__ void plan_kernel(PlanArgs a) {
         const int sq = find_seq(b.ev_off, s0, s1, e);
         int piece = 0;
         for (int q = s0; q < sq; ++q) piece += b.ev_off[q + 1] > b.ev_off[q];
-        const int src = find_source(a.src, a.n_src, b.seq_kind[sq] ? 1 : 0, b.seq_schema[sq], -1);
+        const int src = find_source(srcs, a.n_src, b.seq_kind[sq] ? 1 : 0, b.seq_schema[sq], -1);
         const int r = e - b.ev_off[sq];
         unsigned long long k = ~0ull;
         if (src < 0) {
@@ -231,6 +244,15 @@ __global__ void plan_kernel(PlanArgs a) {
     }
     __syncthreads();
     if (n_t > 1) bitonic_sort(s_ts, s_sec, tpad, TLess{});
+    if (src_sm) {
+        for (int p = tid; p < n_t; p += blockDim.x) {
+            const int sc = find_source(srcs, a.n_src, 2, static_cast<int>(s_sec[p] >> 32), -1);
+            if (sc >= 0) atomicAdd(&s_tcnt[sc], 1);
+            else s_t_unknown = 1;
+        }
+        __syncthreads();
+    }
+    const bool t_fast = src_sm && !s_t_unknown;
     for (int p = tid; p < n_t; p += blockDim.x) {
         const int local = static_cast<int>(s_sec[p] & 0xffffffffll);
         const int scen = static_cast<int>(s_sec[p] >> 32);
@@ -240,13 +262,29 @@ __global__ void plan_kernel(PlanArgs a) {
         const int prefix = l_h + count_below(r_stash, l_r, s_ts[p]);
         int rho = 0, n_s = 0, distinct_below = 0;
         long long rec_before = 0;
-        for (int q = 0; q < n_t; ++q) {
+        if (t_fast) {
+            // every T scenario has a source: counts per scenario from the SMEM histogram
+            // (sources are distinct scenario ids), rank within the scenario by a scan
+            for (int sc = 0; sc < a.n_src; ++sc) {
+                const SourceInfo& si2 = srcs[sc];
+                if (si2.kind != 2 || s_tcnt[sc] == 0) continue;
+                if (si2.id == scen) {
+                    n_s = s_tcnt[sc];
+                } else if (si2.id < scen) {
+                    const bool kept = a.only_scenario < 0 || si2.id == a.only_scenario;
+                    rec_before += kept ? static_cast<long long>(s_tcnt[sc]) * si2.ntasks : 0;
+                    ++distinct_below;
+                }
+            }
+            for (int q = 0; q < p; ++q) rho += static_cast<int>(s_sec[q] >> 32) == scen;
+        }
+        for (int q = 0; q < n_t && !t_fast; ++q) {
             const int sq = static_cast<int>(s_sec[q] >> 32);
             if (sq == scen) {
                 ++n_s;
                 if (q < p) ++rho;
             } else if (sq < scen) {
-                const int ss = find_source(a.src, a.n_src, 2, sq, a.only_scenario);
+                const int ss = find_source(srcs, a.n_src, 2, sq, a.only_scenario);
                 rec_before += ss >= 0 ? a.src[ss].ntasks : 0;
                 // first occurrence of each smaller scenario counts as a piece
                 bool first = true;
@@ -258,7 +296,7 @@ __global__ void plan_kernel(PlanArgs a) {
                 distinct_below += first;
             }
         }
-        const int src = find_source(a.src, a.n_src, 2, scen, a.only_scenario);
+        const int src = find_source(srcs, a.n_src, 2, scen, a.only_scenario);
         a.rm.src[row] = src;
         a.rm.item[row] = x;
         a.rm.prefix[row] = prefix;
