@@ -1204,7 +1204,7 @@ void prepare(mtfm_cuda_model& m, const mtfm_packed_batch* hb, int only_scenario,
     // bf16 path: GLN1 copies of the context rows for every target layer of a run,
     // then the T rows; K|V rows per target layer of the run
     const long long kt = std::max(1, m.cfg.target_layers);
-    ia(B.XN, std::max(R, kt * B.n_events + T) * m.d, el);
+    ia(B.XN, (std::max(R, kt * B.n_events + T) + R) * m.d, el);  // + the full-layer copy (XNF)
     ia(B.P, R * pw, el);
     ia(B.KV, kt * R * 2 * m.gd, el);
     ia(B.UQ, T * 2 * m.hd, el);
@@ -1462,6 +1462,10 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
     if constexpr (kTc) {
         // bf16 tensor-core path: GLN1 and the gate are fused into the GEMM A producers
         bool ctx_stats_valid = false;  // X context rows only change in full layers
+        // full layer whose context-row GLN1 was produced by the preceding target run
+        // (same X context rows) into XNF rows [0, NE): only its T rows remain
+        size_t full_ctx_from_run = static_cast<size_t>(-1);
+        T* XNF = XN + (static_cast<long long>(std::max(1, m.cfg.target_layers)) * NE + NT) * d;
         int tl = 0;                     // index of the current target layer within its run
         for (size_t li = 0; li < m.layers.size(); ++li) {
             const auto& Lw = m.layers[li];
@@ -1485,7 +1489,14 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                     tp.gbias = Lw->g1b.as<float>();
                     run_gemm_tc({tp}, st, L, BT);
                 } else {
-                    {
+                    T* XNL = XN;
+                    if (full_ctx_from_run == li) {
+                        XNL = XNF;
+                        StageScope sc(m, "gln1", 0, Td * d * (4 + el));
+                        launch_gln<T>(X, d, NE, NT, d, rm.src, Lw->g1g.as<float>(), Lw->g1b.as<float>(), eps,
+                                      XNF + NE * d, d, st);
+                        ++L;
+                    } else {
                         StageScope sc(m, "gln1", 0, Rd * d * (4 + el));
                         launch_gln<T>(X, d, 0, R, d, rm.src, Lw->g1g.as<float>(), Lw->g1b.as<float>(), eps, XN, d, st);
                         ++L;
@@ -1493,9 +1504,9 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                     // U and Q|K|V as two contiguous matrices (one grouped launch): the gate
                     // then streams U rows and the attention Q|K|V rows without gaps
                     StageScope sc(m, "proj_full", 2.0 * Rd * d * pw, Rd * d * el + Rd * pw * el);
-                    run_gemm_tc({{XN, d, Lw->t1.as<__nv_bfloat16>(), d, static_cast<int>(R), hd, d, EPI_SILU_BF16,
+                    run_gemm_tc({{XNL, d, Lw->t1.as<__nv_bfloat16>(), d, static_cast<int>(R), hd, d, EPI_SILU_BF16,
                                   Lw->b1.as<float>(), Pm, hd, nullptr, 0, nullptr},
-                                 {XN, d, Lw->t1.as<__nv_bfloat16>() + static_cast<long long>(hd) * d, d,
+                                 {XNL, d, Lw->t1.as<__nv_bfloat16>() + static_cast<long long>(hd) * d, d,
                                   static_cast<int>(R), hd + 2 * gd, d, EPI_SILU_BF16, Lw->b1.as<float>() + hd,
                                   Pm + R * hd, hd + 2 * gd, nullptr, 0, nullptr}},
                                 st, L, BT);
@@ -1575,18 +1586,22 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                         size_t lj = li;
                         while (lj < m.layers.size() && m.layers[lj]->target) ++lj;
                         const int kt = static_cast<int>(lj - li);
-                        for (int c0 = 0; c0 < kt; c0 += kMaxGlnCopies) {
+                        // the full layer right after the run sees the same context rows
+                        const bool with_full = lj < m.layers.size() && !(m.fuse & 1) && kt + 1 <= kMaxGlnCopies;
+                        const int ncopy = kt + (with_full ? 1 : 0);
+                        for (int c0 = 0; c0 < ncopy; c0 += kMaxGlnCopies) {
                             GlnCopies gc{};
-                            gc.n = std::min(kt - c0, kMaxGlnCopies);
+                            gc.n = std::min(ncopy - c0, kMaxGlnCopies);
                             for (int c = 0; c < gc.n; ++c) {
                                 gc.gain[c] = m.layers[li + c0 + c]->g1g.as<float>();
                                 gc.bias[c] = m.layers[li + c0 + c]->g1b.as<float>();
-                                gc.out[c] = XN + static_cast<long long>(c0 + c) * NE * d;
+                                gc.out[c] = c0 + c < kt ? XN + static_cast<long long>(c0 + c) * NE * d : XNF;
                             }
                             StageScope sc(m, "gln1", 0, NE * d * (4.0 + gc.n * el));
                             launch_gln_multi_bf16(X, d, NE, d, rm.src, gc, eps, d, st);
                             ++L;
                         }
+                        if (with_full) full_ctx_from_run = lj;
                         std::vector<TcProblem> kvp;
                         for (int c = 0; c < kt; ++c) {
                             const auto& Lc = m.layers[li + c];
