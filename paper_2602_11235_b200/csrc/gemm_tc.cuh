@@ -15,6 +15,9 @@
 //   A_GATE_TMA : the same gate, but A and U k-blocks are TMA-loaded into the
 //            stage and four transform warps rewrite the A block in place
 //            (SMEM -> SMEM, no exposed global latency) before the MMA.
+//   A_AFFINE_TMA : A = bf16(xhat * gain[g] + bias[g]) from a TMA-loaded bf16
+//            xhat (the layer-independent normalised rows): one normalised copy
+//            serves the GLN1 of every layer that reads the same rows.
 // One launch serves up to kMaxProblems independent problems (tokenizer
 // sources, fkv+fuq of a target layer, ...): the persistent CTAs walk one
 // global tile list, tile t -> (problem, m-block, n-block), n fastest, so the
@@ -42,7 +45,7 @@ enum GemmEpi : int {
     EPI_BIAS_BF16 = 3,   // out_bf16[m][n] = acc + bias
 };
 
-enum GemmAMode : int { A_TMA = 0, A_LN = 1, A_GATE = 2, A_GATE_TMA = 3 };
+enum GemmAMode : int { A_TMA = 0, A_LN = 1, A_GATE = 2, A_GATE_TMA = 3, A_AFFINE_TMA = 4 };
 
 constexpr int kMaxProblems = 16;
 
@@ -310,7 +313,7 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
 
     if (warp == kWarpTma && lane == 0) {
         for (int s = 0; s < n_stages; ++s) {
-            ptx::mbar_init(&full_bar[s], a_mode == A_TMA ? 1 : (a_mode == A_GATE_TMA ? 4 : 1 + 4));
+            ptx::mbar_init(&full_bar[s], a_mode == A_TMA ? 1 : (a_mode >= A_GATE_TMA ? 4 : 1 + 4));
             ptx::mbar_init(&empty_bar[s], 1);
             ptx::mbar_init(&raw_bar[s], 1);
         }
@@ -322,7 +325,7 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
         for (int s = 0; s < 24; ++s) ptx::mbar_init(&res_bar[s], 1);
         ptx::fence_mbar_init();
         for (int i = 0; i < args.n_problems; ++i) {
-            if (a_mode == A_TMA || a_mode == A_GATE_TMA) ptx::tma_prefetch(&args.p[i].tma_a);
+            if (a_mode == A_TMA || a_mode >= A_GATE_TMA) ptx::tma_prefetch(&args.p[i].tma_a);
             if (a_mode == A_GATE_TMA) ptx::tma_prefetch(&args.p[i].tma_u);
             ptx::tma_prefetch(&args.p[i].tma_b);
         }
@@ -367,14 +370,15 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                     uint8_t* sb = sa + KS * C::A_BYTES;
                     const bool skip_a = args.debug & 8;  // timing experiment: no A loads
                     const bool bias_here = !args.b_res && p_bias && kb + KS >= kblocks;  // streaming: bias tile with the last stage
-                    if (a_mode == A_GATE_TMA) {
-                        // raw A and U k-blocks (+ B when streaming) -> raw_bar; the transform
+                    if (a_mode >= A_GATE_TMA) {
+                        // raw A (and U) k-blocks (+ B when streaming) -> raw_bar; the transform
                         // warps rewrite A in place and arrive on full_bar
-                        uint8_t* sbg = sa + 2 * C::A_BYTES;
-                        ptx::mbar_arrive_expect_tx(&raw_bar[stage], 2 * C::A_BYTES + (args.b_res ? 0 : C::B_BYTES) +
+                        const int na = a_mode == A_GATE_TMA ? 2 : 1;
+                        uint8_t* sbg = sa + na * C::A_BYTES;
+                        ptx::mbar_arrive_expect_tx(&raw_bar[stage], na * C::A_BYTES + (args.b_res ? 0 : C::B_BYTES) +
                                                                         (bias_here ? BN * 32 : 0));
                         ptx::tma_load_2d(sa, &p.tma_a, &raw_bar[stage], kb * C::BK, mb * C::BM);
-                        ptx::tma_load_2d(sa + C::A_BYTES, &p.tma_u, &raw_bar[stage], kb * C::BK, mb * C::BM);
+                        if (na == 2) ptx::tma_load_2d(sa + C::A_BYTES, &p.tma_u, &raw_bar[stage], kb * C::BK, mb * C::BM);
                         if (!args.b_res) ptx::tma_load_2d(sbg, &p.tma_b, &raw_bar[stage], kb * C::BK, nb * BN);
                         if (bias_here) ptx::tma_load_2d(sbg + C::B_BYTES, &p.tma_bias, &raw_bar[stage], 0, nb * BN);
                         if (++stage == n_stages) {
@@ -406,7 +410,7 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                 }
             }
         }
-    } else if (warp >= 8 && warp < 12 && a_mode == A_GATE_TMA) {
+    } else if (warp >= 8 && warp < 12 && a_mode >= A_GATE_TMA) {
         // ------------------------------------------------ gate transform, SMEM -> SMEM
         // thread = tile row: its 8 A chunks and 8 U chunks (SW128: chunk c of row r
         // at (c ^ (r & 7))) -> bf16(((a - mu) * rstd * gain[g] + bias[g]) * u) in place
@@ -420,10 +424,11 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
             const int kblocks = s_kblocks[pi];
             const int m = mb * C::BM + r;
             const bool ok = m < p.M;
-            float2 st = make_float2(0.f, 0.f);
+            const bool gate = a_mode == A_GATE_TMA;
+            float2 st = make_float2(0.f, 1.f);
             int g = 0;
             if (ok) {
-                st = __ldg(p.stats + m + p.a_row0);
+                if (gate) st = __ldg(p.stats + m + p.a_row0);
                 g = __ldg(p.row_group + m + p.g_row0);
                 g = g < 0 ? 0 : g;
             }
@@ -440,7 +445,12 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                         const int off = (c ^ (r & 7)) << 4;
                         float a8[8], u8[8];
                         gemm_detail::unpack8(*reinterpret_cast<const uint4*>(arow + off), a8);
-                        gemm_detail::unpack8(*reinterpret_cast<const uint4*>(urow + off), u8);
+                        if (gate) {
+                            gemm_detail::unpack8(*reinterpret_cast<const uint4*>(urow + off), u8);
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) u8[e] = 1.f;
+                        }
                         const float4 g0 = __ldg(reinterpret_cast<const float4*>(gp + 8 * c));
                         const float4 g1 = __ldg(reinterpret_cast<const float4*>(gp + 8 * c + 4));
                         const float4 b0 = __ldg(reinterpret_cast<const float4*>(bp + 8 * c));

@@ -561,9 +561,17 @@ __global__ void __launch_bounds__(256) gln_multi_kernel(const float* __restrict_
         normalize_slices<NS, true>(v, d, lane, eps);
         g = g < 0 ? 0 : g;
         for (int l = 0; l < c.n; ++l) {
+            __nv_bfloat16* o = static_cast<__nv_bfloat16*>(c.out[l]) + r * ldo;
+            if (c.gain[l] == nullptr) {  // the normalised rows themselves (xhat)
+#pragma unroll
+                for (int k = 0; k < NS; ++k) {
+                    const int col = 128 * k + 4 * lane;
+                    if (col < d) st4(o + col, v[k]);
+                }
+                continue;
+            }
             const float* gg = c.gain[l] + (long long)g * d;
             const float* bb = c.bias[l] + (long long)g * d;
-            __nv_bfloat16* o = static_cast<__nv_bfloat16*>(c.out[l]) + r * ldo;
 #pragma unroll
             for (int k = 0; k < NS; ++k) {
                 const int col = 128 * k + 4 * lane;

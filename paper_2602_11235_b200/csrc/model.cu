@@ -734,9 +734,9 @@ void run_gemm_tc(std::vector<TcProblem> ps, cudaStream_t st, long long& launches
             if (s.amode != a.a_mode) fail(MTFM_CONTRACT_ERROR, "mixed A modes in one grouped GEMM");
             GemmProblem& p = a.p[a.n_problems++];
             if (s.amode == A_TMA) p.tma_a = ks > 1 ? tma_3d_kb(s.A, s.M, s.K, s.lda, 128, ks) : tma_2d(s.A, s.M, s.K, s.lda, 64, 128, 128);
-            if (s.amode == A_GATE_TMA) {
+            if (s.amode == A_GATE_TMA || s.amode == A_AFFINE_TMA) {
                 p.tma_a = tma_2d(s.a_src, s.M, s.K, s.lda, 64, 128, 128);
-                p.tma_u = tma_2d(s.u_src, s.M, s.K, s.ldu, 64, 128, 128);
+                if (s.amode == A_GATE_TMA) p.tma_u = tma_2d(s.u_src, s.M, s.K, s.ldu, 64, 128, 128);
             }
             // B: 2D boxes for the resident slice (loaded once per CTA), 3D per stage when streaming
             p.tma_b = (ks > 1 && !a.b_res) ? tma_3d_kb(s.Bt, s.N, s.K, s.ldb, bn, ks) : tma_2d(s.Bt, s.N, s.K, s.ldb, 64, bn, 128);
@@ -1588,14 +1588,20 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                         const int kt = static_cast<int>(lj - li);
                         // the full layer right after the run sees the same context rows
                         const bool with_full = lj < m.layers.size() && !(m.fuse & 1) && kt + 1 <= kMaxGlnCopies;
-                        const int ncopy = kt + (with_full ? 1 : 0);
+                        // MTFM_XHAT=1: one normalised copy (xhat) + per-layer affine inside the
+                        // K|V GEMM's A producer (A_AFFINE_TMA) instead of one copy per layer
+                        static const bool use_xhat = std::getenv("MTFM_XHAT") && std::atoi(std::getenv("MTFM_XHAT")) != 0;
+                        const int ncopy = (use_xhat ? 1 : kt) + (with_full ? 1 : 0);
                         for (int c0 = 0; c0 < ncopy; c0 += kMaxGlnCopies) {
                             GlnCopies gc{};
                             gc.n = std::min(ncopy - c0, kMaxGlnCopies);
                             for (int c = 0; c < gc.n; ++c) {
-                                gc.gain[c] = m.layers[li + c0 + c]->g1g.as<float>();
-                                gc.bias[c] = m.layers[li + c0 + c]->g1b.as<float>();
-                                gc.out[c] = c0 + c < kt ? XN + static_cast<long long>(c0 + c) * NE * d : XNF;
+                                const int cc = c0 + c;
+                                const bool full_copy = with_full && cc == ncopy - 1;
+                                const auto& Lc = m.layers[full_copy ? lj : li + cc];
+                                gc.gain[c] = (use_xhat && !full_copy) ? nullptr : Lc->g1g.as<float>();
+                                gc.bias[c] = (use_xhat && !full_copy) ? nullptr : Lc->g1b.as<float>();
+                                gc.out[c] = full_copy ? XNF : XN + static_cast<long long>(cc) * NE * d;
                             }
                             StageScope sc(m, "gln1", 0, NE * d * (4.0 + gc.n * el));
                             launch_gln_multi_bf16(X, d, NE, d, rm.src, gc, eps, d, st);
@@ -1605,9 +1611,19 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                         std::vector<TcProblem> kvp;
                         for (int c = 0; c < kt; ++c) {
                             const auto& Lc = m.layers[li + c];
-                            kvp.push_back({XN + static_cast<long long>(c) * NE * d, d, Lc->tkv.as<__nv_bfloat16>(), d,
+                            T* a_in = XN + static_cast<long long>(use_xhat ? 0 : c) * NE * d;
+                            kvp.push_back({a_in, d, Lc->tkv.as<__nv_bfloat16>(), d,
                                            static_cast<int>(NE), 2 * gd, d, EPI_SILU_BF16, Lc->bkv.as<float>(),
                                            KV + static_cast<long long>(c) * R * 2 * gd, 2 * gd, nullptr, 0, nullptr});
+                            if (use_xhat) {
+                                TcProblem& tp = kvp.back();
+                                tp.amode = A_AFFINE_TMA;
+                                tp.a_src = a_in;
+                                tp.row_group = rm.src;
+                                tp.g_row0 = 0;
+                                tp.gain = Lc->g1g.as<float>();
+                                tp.gbias = Lc->g1b.as<float>();
+                            }
                         }
                         StageScope sc(m, "proj_ctx_kv", 2.0 * kt * NE * d * 2 * gd,
                                       kt * NE * (d + 2.0 * gd) * el);
