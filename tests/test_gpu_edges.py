@@ -1,0 +1,132 @@
+"""Edge cases of the CUDA path (through the C ABI): ragged and empty users,
+empty batches, the scenario-scoped forward, long users and the planning
+capacity. Needs a B200. Expected values come from the pinned numpy oracle or
+from the reference's own rules (tokenizer.hpp:240-268 for empty samples,
+model.hpp:244-312 for the scoped forward)."""
+import dataclasses
+
+import numpy as np
+import pytest
+
+from helpers import oracle_records, rel_err, to_oracle
+from paper_2602_11235_b200 import Model, abi, datagen
+from paper_2602_11235_b200.schema import normalize_batch
+from paper_2602_11235_b200.shard import take_users
+
+pytestmark = pytest.mark.gpu
+
+
+def _wl(name="small", **kw):
+    return dataclasses.replace(datagen.WORKLOADS[name](), **kw)
+
+
+def _model(wl, precision="bf16", seed=5):
+    m = Model(wl.schemas, wl.cfg, precision=precision)
+    P = datagen.random_params(m.param_specs(), seed=seed)
+    m.set_params(P)
+    return m, P
+
+
+def _cat(*batches):
+    """Concatenate packed batches user-wise (include/mtfm_cuda.h layout)."""
+    bs = [normalize_batch(b) for b in batches]
+    out = {}
+    for k in ("user_id", "seq_kind", "seq_schema", "ev_ts", "ev_feats", "exp_scenario", "exp_ts", "exp_blk",
+              "exp_feats"):
+        out[k] = np.concatenate([b[k] for b in bs])
+    out["user_id"] = np.arange(len(out["user_id"]), dtype=np.int64)
+
+    def offs(key, counts_key=None):
+        parts, base = [np.zeros(1, np.int64)], 0
+        for b in bs:
+            o = b[key].astype(np.int64)
+            parts.append(o[1:] + base)
+            base += int(o[-1])
+        return np.concatenate(parts)
+    for k in ("seq_off", "ev_off", "ev_feat_off", "exp_off", "exp_feat_off"):
+        out[k] = offs(k)
+    return normalize_batch(out)
+
+
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+def test_ragged_users_vs_oracle(precision):
+    """Users without events (targets attend only to themselves), users without
+    exposures (no records) and ordinary users in one batch."""
+    wl = _wl()
+    no_ev = datagen.generate(_wl(hist_len=0, rt_len=0, exp_per_scen=2, seed=21), n_users=2)
+    no_x = datagen.generate(_wl(hist_len=40, rt_len=9, exp_per_scen=0, seed=22), n_users=2)
+    ragged = datagen.generate(_wl(hist_len=("lognormal", 30, 1.0, 1, 300), rt_len=("lognormal", 8, 1.0, 0, 64),
+                                  exp_per_scen=("lognormal", 5, 0.8, 1, 20), seed=23), n_users=4)
+    b = _cat(no_ev, ragged, no_x)
+    m, P = _model(wl, precision)
+    osch, ocfg = to_oracle(wl.schemas, wl.cfg)
+    keys, z_ref, _ = oracle_records(osch, ocfg, P, b)
+    ra = m.forward_batch(b)
+    assert np.array_equal(np.stack([ra.user_id, ra.scenario_id, ra.exposure_index, ra.task_index], 1), keys)
+    if precision == "bf16":
+        assert np.max(np.abs(ra.logit - z_ref)) <= 2e-2
+    else:
+        assert rel_err(ra.logit.astype(np.float64), z_ref) <= 1e-4
+
+
+def test_empty_batch_and_sample_without_tokens():
+    wl = _wl()
+    m, _ = _model(wl)
+    b = datagen.generate(wl, n_users=3)
+    empty = take_users(b, np.zeros(0, np.int64))
+    assert len(m.forward_batch(empty).logit) == 0
+    # a user with neither events nor exposures: contract_error (tokenizer.hpp:240-268)
+    none = datagen.generate(_wl(hist_len=0, rt_len=0, exp_per_scen=0, seed=3), n_users=1)
+    with pytest.raises(abi.ContractError):
+        m.forward_batch(_cat(b, none))
+
+
+def test_scoped_forward():
+    """forward_scoped(only_scenario) (model.hpp:284-311): a sample whose exposures
+    all belong to the scenario scores exactly as unscoped; another scenario in
+    the sample is an integrity_error (the scenario subgraph has no tokenizer for it)."""
+    wl = _wl()
+    m, _ = _model(wl)
+    b = normalize_batch(datagen.generate(wl, n_users=8))
+    sid = int(wl.schemas.scenarios[2].scenario_id)
+    keep = np.nonzero(b["exp_scenario"] == sid)[0]
+    # batch restricted to one scenario's exposures
+    one = dict(b)
+    cnt = np.array([np.sum((keep >= b["exp_off"][u]) & (keep < b["exp_off"][u + 1]))
+                    for u in range(len(b["user_id"]))])
+    one["exp_off"] = np.concatenate([[0], np.cumsum(cnt)])
+    one["exp_scenario"] = b["exp_scenario"][keep]
+    one["exp_ts"] = b["exp_ts"][keep]
+    one["exp_blk"] = b["exp_blk"].reshape(-1, 3)[keep].reshape(-1)
+    fo = b["exp_feat_off"]
+    one["exp_feats"] = np.concatenate([b["exp_feats"][fo[x]:fo[x + 1]] for x in keep])
+    one["exp_feat_off"] = np.concatenate([[0], np.cumsum([fo[x + 1] - fo[x] for x in keep])])
+    one = normalize_batch(one)
+    full = m.forward_batch(one)
+    scoped = m.forward_batch(one, only_scenario=sid)
+    assert np.array_equal(scoped.logit, full.logit)
+    assert (scoped.scenario_id == sid).all()
+    with pytest.raises(abi.IntegrityError):
+        m.forward_batch(b, only_scenario=sid)
+
+
+def test_long_user_vs_oracle():
+    """One user far beyond the small shape (2 x 1500 history + 600 realtime +
+    100 targets): attention spans many key tiles and query tiles."""
+    wl = _wl(hist_len=1500, rt_len=600, exp_per_scen=25, seed=31)
+    b = datagen.generate(wl, n_users=1)
+    m, P = _model(wl)
+    osch, ocfg = to_oracle(wl.schemas, wl.cfg)
+    keys, z_ref, _ = oracle_records(osch, ocfg, P, b)
+    ra = m.forward_batch(b)
+    assert np.array_equal(np.stack([ra.user_id, ra.scenario_id, ra.exposure_index, ra.task_index], 1), keys)
+    assert np.max(np.abs(ra.logit - z_ref)) <= 2e-2
+
+
+def test_planning_capacity_is_contract_error():
+    """More tokens per user than one planning CTA sorts (12 288) fails loudly."""
+    wl = _wl(hist_len=6000, rt_len=1000, exp_per_scen=1, seed=41)
+    b = datagen.generate(wl, n_users=1)
+    m, _ = _model(wl)
+    with pytest.raises(abi.ContractError):
+        m.forward_batch(b)
