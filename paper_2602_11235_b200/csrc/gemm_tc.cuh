@@ -310,6 +310,13 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
     // producer, 13 TMEM allocator; epilogue warps 0..n_epi-1 (warp & 3 = TMEM
     // lane quarter); 8..11 A-transform producers when A is not TMA-loaded.
     constexpr uint32_t kWarpMma = 15, kWarpTma = 14, kWarpAlloc = 13;
+#ifdef MTFM_GEMM_TWO_MMA
+    constexpr bool kTwoMma = true;  // warp 13 (TMEM allocator) issues every other tile
+#else
+    constexpr bool kTwoMma = false;  // measured: no gain on the projections, halves the ring for K=512
+#endif
+    // two issuers only for TMA-loaded A (the transform producers walk one ring) and >= 4 stages
+    const bool two_mma = kTwoMma && a_mode == A_TMA && n_stages >= 4;
 
     if (warp == kWarpTma && lane == 0) {
         for (int s = 0; s < n_stages; ++s) {
@@ -352,12 +359,18 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                     ptx::tma_load_2d(bres + kb * C::B_BYTES, &p.tma_b, bres_bar, kb * C::BK, w.nb * BN);
                 if (p.has_bias) ptx::tma_load_2d(bres + kblocks * C::B_BYTES, &p.tma_bias, bres_bar, 0, w.nb * BN);
             }
-            int stage = 0;
-            uint32_t phase = 0;
+            // ring half r = tile % 2 when two MMA warps issue (see the MMA role), else one ring
+            int st_r[2] = {0, two_mma ? n_stages / 2 : 0};
+            uint32_t ph_r[2] = {0, 0};
+            const int ring_n = two_mma ? n_stages / 2 : n_stages;
             int ntile = 0;
             gemm_detail::TileSeq seq(args, s_tile_start, s_tiles_n);
             int pi, mb, nb;
             while (seq.next(args, gemm_detail::decode_tile, pi, mb, nb)) {
+                const int ring = two_mma ? (ntile & 1) : 0;
+                const int ring0 = ring * (two_mma ? n_stages / 2 : 0);
+                int& stage = st_r[ring];
+                uint32_t& phase = ph_r[ring];
                 const GemmProblem& p = args.p[pi];
                 const int kblocks = s_kblocks[pi];
                 const bool p_bias = s_has_bias[pi];
@@ -381,8 +394,8 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                         if (na == 2) ptx::tma_load_2d(sa + C::A_BYTES, &p.tma_u, &raw_bar[stage], kb * C::BK, mb * C::BM);
                         if (!args.b_res) ptx::tma_load_2d(sbg, &p.tma_b, &raw_bar[stage], kb * C::BK, nb * BN);
                         if (bias_here) ptx::tma_load_2d(sbg + C::B_BYTES, &p.tma_bias, &raw_bar[stage], 0, nb * BN);
-                        if (++stage == n_stages) {
-                            stage = 0;
+                        if (++stage == ring0 + ring_n) {
+                            stage = ring0;
                             phase ^= 1;
                         }
                         continue;
@@ -403,8 +416,8 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                         else ptx::tma_load_2d(sb, &p.tma_b, &full_bar[stage], kb * C::BK, nb * BN);
                     }
                     if (bias_here) ptx::tma_load_2d(sb + KS * C::B_BYTES, &p.tma_bias, &full_bar[stage], 0, nb * BN);
-                    if (++stage == n_stages) {
-                        stage = 0;
+                    if (++stage == ring0 + ring_n) {
+                        stage = ring0;
                         phase ^= 1;
                     }
                 }
@@ -498,10 +511,19 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                 }
             }
         }
-    } else if (warp == kWarpMma) {
-        // ------------------------------------------------ MMA issuer (one elected lane per k-block)
+    } else if (warp == kWarpMma || (two_mma && warp == kWarpAlloc)) {
+        // ------------------------------------------------ MMA issuers (one elected lane per k-block)
+        // Two issuing warps take alternate tiles (own accumulators, own stages of
+        // the shared ring): one thread issues a tcgen05.mma only every ~90 clk,
+        // short of the 64 clk an N=128 MMA occupies the tensor pipe.
+        // Each issuer owns half of the SMEM ring (the producer fills tile j into half
+        // j % 2), so the two never share a stage.
+        const int mma_id = warp == kWarpMma ? 0 : 1;
+        const int n_mma = two_mma ? 2 : 1;
+        const int ring0 = two_mma ? mma_id * (n_stages / 2) : 0;
+        const int ring_n = two_mma ? n_stages / 2 : n_stages;
         const uint32_t idesc = ptx::instr_desc_bf16(128, BN, false, false);
-        int stage = 0;
+        int stage = ring0;
         uint32_t phase = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
@@ -509,8 +531,16 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
         int ntile = 0;
         gemm_detail::TileSeq seq(args, s_tile_start, s_tiles_n);
         int pi, mb, nb;
-        while (seq.next(args, gemm_detail::decode_tile, pi, mb, nb)) {
+        for (int jt = 0; seq.next(args, gemm_detail::decode_tile, pi, mb, nb); ++jt) {
             const int kblocks = s_kblocks[pi];
+            if (jt % n_mma != mma_id) {
+                // the other issuer's tile (its own half of the ring): advance the accumulator only
+                if (++acc == C::kAcc) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+                continue;
+            }
             if (args.b_res && !bres_ready) {
                 ptx::mbar_wait(bres_bar, 0);
                 bres_ready = true;
@@ -556,8 +586,8 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                 }
                 __syncwarp();
                 if (ntile < 8 && kb < 8) trace(512 + ntile * 16 + kb * 2 + 1);
-                if (++stage == n_stages) {
-                    stage = 0;
+                if (++stage == ring0 + ring_n) {
+                    stage = ring0;
                     phase ^= 1;
                 }
             }
