@@ -173,12 +173,19 @@ MTFM_API int64_t mtfm_cuda_count_records(const mtfm_cuda_model* m, const mtfm_pa
 MTFM_API mtfm_status mtfm_cuda_forward(mtfm_cuda_model* m, const mtfm_packed_batch* b, int32_t only_scenario,
                               mtfm_records* out);
 
-/* Split forward. prepare: host layout + async H2D of the batch (the host
- * arrays may be released after the call returns). run: enqueues every
- * kernel on the model stream, no host synchronisation. results: waits, then
- * copies the records (and reports device-detected errors). */
+/* Split forward. prepare: host layout + H2D of the batch on the model's copy
+ * stream (returns once the host arrays have been read: they may be released;
+ * the kernels of other batches keep running meanwhile). update: the same into
+ * an existing batch object, reusing its device buffers (ordered after that
+ * batch's previous forward). run: enqueues every kernel on the model stream
+ * behind this batch's uploads, no host synchronisation. results: waits for
+ * this batch's forward only, then copies the records (and reports
+ * device-detected errors). Two batch objects used alternately pipeline one
+ * batch's host work and transfers with the other's kernels. */
 MTFM_API mtfm_status mtfm_cuda_batch_prepare(mtfm_cuda_model* m, const mtfm_packed_batch* b, int32_t only_scenario,
                                     mtfm_cuda_batch** out);
+MTFM_API mtfm_status mtfm_cuda_batch_update(mtfm_cuda_model* m, mtfm_cuda_batch* batch, const mtfm_packed_batch* b,
+                                   int32_t only_scenario);
 MTFM_API mtfm_status mtfm_cuda_batch_run(mtfm_cuda_model* m, mtfm_cuda_batch* b);
 MTFM_API mtfm_status mtfm_cuda_batch_results(mtfm_cuda_model* m, mtfm_cuda_batch* b, mtfm_records* out);
 MTFM_API mtfm_status mtfm_cuda_batch_free(mtfm_cuda_batch* b);

@@ -105,6 +105,7 @@ SIGNATURES = [
     ("mtfm_cuda_count_records", C.c_int64, [C.c_void_p, C.POINTER(PackedBatch)]),
     ("mtfm_cuda_forward", C.c_int, [C.c_void_p, C.POINTER(PackedBatch), C.c_int32, C.POINTER(Records)]),
     ("mtfm_cuda_batch_prepare", C.c_int, [C.c_void_p, C.POINTER(PackedBatch), C.c_int32, C.POINTER(C.c_void_p)]),
+    ("mtfm_cuda_batch_update", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(PackedBatch), C.c_int32]),
     ("mtfm_cuda_batch_run", C.c_int, [C.c_void_p, C.c_void_p]),
     ("mtfm_cuda_batch_results", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(Records)]),
     ("mtfm_cuda_batch_free", C.c_int, [C.c_void_p]),

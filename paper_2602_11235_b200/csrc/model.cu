@@ -267,7 +267,9 @@ struct mtfm_cuda_model {
     std::vector<mtfm::ParamSpec> params;
     std::map<std::string, size_t> by_name;
     bool finalized = false;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr;       // kernels
+    cudaStream_t copy_stream = nullptr;  // batch uploads (overlap the previous batch's kernels)
+    cudaStream_t d2h_stream = nullptr;   // record read-back (does not queue behind the next batch)
     // device weights
     mtfm::DevBuf d_src, d_slots;
     mtfm::BiasTiles bias_tiles;  // GEMM bias tiles, built on first use
@@ -316,6 +318,13 @@ struct mtfm_cuda_batch {
     mtfm::DevBuf rec_user, rec_scen, rec_exp, rec_task, rec_logit, rec_prob;
     mtfm::DevBuf stat_buf;
     mtfm::PinnedBuf pin;  // staging of the host-computed layout tables + stats read-back
+    cudaEvent_t ev_h2d = nullptr;   // uploads of the current contents done (copy stream)
+    cudaEvent_t ev_done = nullptr;  // forward of the current contents done (kernel stream)
+    bool ran = false;
+    ~mtfm_cuda_batch() {
+        if (ev_h2d) cudaEventDestroy(ev_h2d);
+        if (ev_done) cudaEventDestroy(ev_done);
+    }
     long long launches = 0;
     unsigned long long sum_c_ctx = 0, sum_c_t = 0;  // sum of visible keys (stats)
 };
@@ -1057,7 +1066,12 @@ void prepare(mtfm_cuda_model& m, const mtfm_packed_batch* hb, int only_scenario,
     const auto p0 = now();
     check_batch(hb);
     finalize(m);
-    cudaStream_t st = m.stream;
+    // uploads go on the copy stream, after the previous forward of this batch object
+    // (its device buffers are overwritten) and after the weights
+    cudaStream_t st = m.copy_stream;
+    if (!B.ev_h2d) ck(cudaEventCreateWithFlags(&B.ev_h2d, cudaEventDisableTiming), "event");
+    if (!B.ev_done) ck(cudaEventCreateWithFlags(&B.ev_done, cudaEventDisableTiming), "event");
+    if (B.ran) ck(cudaStreamWaitEvent(st, B.ev_done, 0), "wait previous forward");
     B.m = &m;
     B.only_scenario = only_scenario;
     B.n_users = hb->n_users;
@@ -1222,6 +1236,10 @@ void prepare(mtfm_cuda_model& m, const mtfm_packed_batch* hb, int only_scenario,
     ia(B.rec_task, nr, 4);
     ia(B.rec_logit, nr, 4);
     ia(B.rec_prob, nr, 8);
+    // every upload of this batch is enqueued: the host arrays may be released once they
+    // have been read (the kernels of the previous batch keep running meanwhile)
+    ck(cudaEventRecord(B.ev_h2d, st), "record h2d");
+    ck(cudaEventSynchronize(B.ev_h2d), "h2d");
 }
 
 DevBatch dev_batch(const mtfm_cuda_batch& B) {
@@ -1922,7 +1940,9 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
 void launch_sum_valid(mtfm_cuda_batch& B, cudaStream_t st);
 
 void results(mtfm_cuda_model& m, mtfm_cuda_batch& B, mtfm_records* out) {
-    cudaStream_t st = m.stream;
+    // read-back on its own stream, behind this batch's forward only
+    cudaStream_t st = m.d2h_stream;
+    if (B.ran) ck(cudaStreamWaitEvent(st, B.ev_done, 0), "wait forward");
     // error key + the visible-key sums of the stats, read back with one synchronisation
     B.pin.reserve(4096);
     auto* hb = static_cast<unsigned long long*>(B.pin.p);
@@ -2090,6 +2110,8 @@ mtfm_status mtfm_cuda_create(int device, const mtfm_model_desc* md, const mtfm_s
         m->slot_param.assign(m->slots.size(), "");
         register_params(*m);
         ck(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking), "stream");
+        ck(cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking), "copy stream");
+        ck(cudaStreamCreateWithFlags(&m->d2h_stream, cudaStreamNonBlocking), "d2h stream");
         if (const char* f = std::getenv("MTFM_FUSE")) m->fuse = std::atoi(f);
         *out = m.release();
     });
@@ -2099,13 +2121,17 @@ mtfm_status mtfm_cuda_destroy(mtfm_cuda_model* m) {
     return guard([&] {
         if (!m) return;
         if (m->stream) cudaStreamSynchronize(m->stream);
-        cudaStream_t st = m->stream;
+        if (m->copy_stream) cudaStreamSynchronize(m->copy_stream);
+        if (m->d2h_stream) cudaStreamSynchronize(m->d2h_stream);
+        cudaStream_t st = m->stream, cs = m->copy_stream, ds = m->d2h_stream;
         for (auto& e : m->prof) {
             if (e.a) cudaEventDestroy(e.a);
             if (e.b) cudaEventDestroy(e.b);
         }
         delete m;
         if (st) cudaStreamDestroy(st);
+        if (cs) cudaStreamDestroy(cs);
+        if (ds) cudaStreamDestroy(ds);
     });
 }
 
@@ -2156,15 +2182,28 @@ mtfm_status mtfm_cuda_batch_prepare(mtfm_cuda_model* m, const mtfm_packed_batch*
     });
 }
 
+mtfm_status mtfm_cuda_batch_update(mtfm_cuda_model* m, mtfm_cuda_batch* b, const mtfm_packed_batch* pb,
+                                   int32_t only_scenario) {
+    return guard([&] {
+        if (!m || !b || !pb) fail(MTFM_CONTRACT_ERROR, "null argument");
+        if (b->m && b->m != m) fail(MTFM_CONTRACT_ERROR, "batch belongs to another model");
+        ck(cudaSetDevice(m->device), "cudaSetDevice");
+        prepare(*m, pb, only_scenario, *b);
+    });
+}
+
 mtfm_status mtfm_cuda_batch_run(mtfm_cuda_model* m, mtfm_cuda_batch* b) {
     return guard([&] {
         if (!m || !b) fail(MTFM_CONTRACT_ERROR, "null argument");
         if (!m->finalized) fail(MTFM_CONTRACT_ERROR, "parameters changed after prepare; prepare the batch again");
         ck(cudaSetDevice(m->device), "cudaSetDevice");
+        ck(cudaStreamWaitEvent(m->stream, b->ev_h2d, 0), "wait uploads");
         if (m->precision == MTFM_PRECISION_BF16)
             run_forward<__nv_bfloat16>(*m, *b);
         else
             run_forward<float>(*m, *b);
+        ck(cudaEventRecord(b->ev_done, m->stream), "record forward");
+        b->ran = true;
         m->stats.kernel_launches = b->launches;
         m->stats.tokens = b->rows;
         m->stats.targets = b->n_exp;
@@ -2209,6 +2248,8 @@ mtfm_status mtfm_cuda_batch_free(mtfm_cuda_batch* b) {
     return guard([&] {
         if (!b) return;
         if (b->m && b->m->stream) cudaStreamSynchronize(b->m->stream);
+        if (b->m && b->m->copy_stream) cudaStreamSynchronize(b->m->copy_stream);
+        if (b->m && b->m->d2h_stream) cudaStreamSynchronize(b->m->d2h_stream);
         delete b;
     });
 }

@@ -51,6 +51,13 @@ class PreparedBatch:
         self._h = h
         self.n_records = int(abi.lib().mtfm_cuda_count_records(model._h, C.byref(self._pb)))
 
+    def update(self, batch: dict, only_scenario: int = -1):
+        """Load another batch into this object's device buffers (mtfm_cuda_batch_update)."""
+        self.batch = normalize_batch(batch)
+        self._pb = self.model._packed(self.batch)
+        abi.check(abi.lib().mtfm_cuda_batch_update(self.model._h, self._h, C.byref(self._pb), only_scenario))
+        self.n_records = int(abi.lib().mtfm_cuda_count_records(self.model._h, C.byref(self._pb)))
+
     def run(self):
         abi.check(abi.lib().mtfm_cuda_batch_run(self.model._h, self._h))
 
