@@ -43,6 +43,9 @@ CONFIGS = {
     "large": ("large", ["--d", "1024", "--blocks", "4", "--K", "3", "--P", "1", "--H", "16", "--G", "4",
                         "--dexp", "1024", "--lenmin", "896", "--lenmax", "896", "--rlen", "256",
                         "--expmin", "32", "--expmax", "32"]),
+    "paper": ("paper", ["--d", "768", "--blocks", "4", "--K", "3", "--P", "1", "--H", "3", "--G", "1",
+                        "--dexp", "768", "--lenmin", "896", "--lenmax", "896", "--rlen", "256",
+                        "--expmin", "32", "--expmax", "32"]),
 }
 
 

@@ -648,7 +648,10 @@ constexpr int kBresMax = 96 * 1024;
 int pick_bn_resident(const std::vector<TcProblem>& ps) {
     int best = 0;
     double best_eff = -1;
-    for (int bn : {256, 128, 64}) {
+    // a resident slice narrower than 128 columns makes N=64 MMAs (half the work per
+    // instruction) and re-reads A per slice: measured 2-3x slower than streaming
+    // B at BN=256 for K >= 512 (paper config projections), so it is not offered
+    for (int bn : {256, 128}) {
         bool fits = true;
         double used = 0, padded = 0;
         for (const auto& p : ps) {
