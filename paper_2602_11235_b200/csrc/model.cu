@@ -143,6 +143,13 @@ struct DevBuf {
     }
 };
 
+// Forward activations live in one model-level arena shared by every prepared
+// batch: forwards are serialised on the model stream, so only the inputs, the
+// layout tables and the records are per batch (two batches in flight cost one
+// set of activations). A batch records the bytes it needs; run_forward grows
+// the arena (after draining the stream) when a bigger batch arrives.
+enum ActId { ACT_X, ACT_XN, ACT_P, ACT_KV, ACT_UQ, ACT_A, ACT_GT, ACT_E, ACT_HID, ACT_Y, ACT_STATX, ACT_STATA, ACT_N };
+
 // Page-locked host staging (grows, never shrinks): host-computed layout tables
 // are written here and copied with truly asynchronous H2D transfers.
 struct PinnedBuf {
@@ -278,6 +285,7 @@ struct mtfm_cuda_model {
     std::vector<std::unique_ptr<mtfm::SourceW>> srcw;
     std::vector<std::unique_ptr<mtfm::LayerW>> layers;
     mtfm::DevBuf head_w, head_t, head_eb, head_gb, tower_w, tower_b;
+    mtfm::DevBuf act[mtfm::ACT_N];  // forward activation arena shared by all batches
     int head_n = 0;
     int head_ld = 0;  // head_n rounded up to 8 (16-byte rows)
     mtfm_run_stats stats{};
@@ -308,8 +316,8 @@ struct mtfm_cuda_batch {
     // row meta
     mtfm::DevBuf r_src, r_item, r_prefix, r_scale, r_self, r_keybase, r_src_rows, t_user, t_exp_ref, t_scen, t_rec0,
         t_rec_stride, err;
-    // activations
-    mtfm::DevBuf X, XN, P, KV, UQ, A, Gt, E, HID, Y, statX, statA;
+    // activation bytes this batch needs in the model arena (mtfm_cuda_model::act)
+    size_t act_bytes[mtfm::ACT_N] = {};
     // attention tiles
     long long n_tiles_full = 0, n_tiles_tgt = 0;
     mtfm::DevBuf d_tile_off;  // per-user first tile, full then target tables
@@ -1217,21 +1225,22 @@ void prepare(mtfm_cuda_model& m, const mtfm_packed_batch* hb, int only_scenario,
     ia(B.err, 1, 8);
     const size_t el = m.precision == MTFM_PRECISION_BF16 ? 2 : 4;
     const int pw = 2 * m.hd + 2 * m.gd;
-    ia(B.X, R * m.d, 4);
+    auto need = [&](int id, long long n, size_t e) { B.act_bytes[id] = std::max<size_t>(static_cast<size_t>(n) * e, 16); };
+    need(ACT_X, R * m.d, 4);
     // bf16 path: GLN1 copies of the context rows for every target layer of a run,
     // then the T rows; K|V rows per target layer of the run
     const long long kt = std::max(1, m.cfg.target_layers);
-    ia(B.XN, (std::max(R, kt * B.n_events + T) + R) * m.d, el);  // + the full-layer copy (XNF)
-    ia(B.P, R * pw, el);
-    ia(B.KV, kt * R * 2 * m.gd, el);
-    ia(B.UQ, T * 2 * m.hd, el);
-    ia(B.A, R * m.hd, el);
-    ia(B.Gt, R * m.hd, el);
-    ia(B.E, eb, el);
-    ia(B.HID, hbse, el);
-    ia(B.Y, T * m.head_ld, 4);
-    ia(B.statX, R, 8);
-    ia(B.statA, R, 8);
+    need(ACT_XN, (std::max(R, kt * B.n_events + T) + R) * m.d, el);  // + the full-layer copy (XNF)
+    need(ACT_P, R * pw, el);
+    need(ACT_KV, kt * R * 2 * m.gd, el);
+    need(ACT_UQ, T * 2 * m.hd, el);
+    need(ACT_A, R * m.hd, el);
+    need(ACT_GT, R * m.hd, el);
+    need(ACT_E, eb, el);
+    need(ACT_HID, hbse, el);
+    need(ACT_Y, T * m.head_ld, 4);
+    need(ACT_STATX, R, 8);
+    need(ACT_STATA, R, 8);
     const long long nr = B.n_records;
     ia(B.rec_user, nr, 8);
     ia(B.rec_scen, nr, 4);
@@ -1326,6 +1335,14 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
     const double Rd = static_cast<double>(R), Td = static_cast<double>(NT);
     const float eps = static_cast<float>(m.cfg.eps);
     if (B.n_users == 0) return;
+    {
+        bool grow = false;
+        for (int i = 0; i < ACT_N; ++i) grow |= B.act_bytes[i] > m.act[i].bytes;
+        if (grow) {  // earlier forwards may still read the arena
+            ck(cudaStreamSynchronize(st), "arena sync");
+            for (int i = 0; i < ACT_N; ++i) m.act[i].alloc(B.act_bytes[i]);
+        }
+    }
     RowMeta rm = row_meta(B);
     ck(cudaMemsetAsync(B.err.p, 0xff, 8, st), "memset err");
 
@@ -1353,8 +1370,8 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
     }
 
     // ---- K1: tokenizer (embedding gather + 2-layer SiLU MLP per source)
-    T* E = B.E.as<T>();
-    T* HID = B.HID.as<T>();
+    T* E = m.act[ACT_E].as<T>();
+    T* HID = m.act[ACT_HID].as<T>();
     int max_slots = 0;
     for (const auto& s : m.sources) max_slots = std::max(max_slots, s.nslot[0] + s.nslot[1] + s.nslot[2]);
     long long tok_rows = 0;
@@ -1376,7 +1393,7 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
         ck(cudaGetLastError(), "gather launch");
         ++L;
     }
-    float* X = B.X.as<float>();
+    float* X = m.act[ACT_X].as<float>();
     if constexpr (kTc) {
         std::vector<TcProblem> p1, p2;
         // sequence sources with one k-block of embeddings: fused MLP (tok_tc.cuh)
@@ -1469,17 +1486,17 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
     }
 
     // ---- K2..K4: the HTA stack (hta.hpp:188-212)
-    T* XN = B.XN.as<T>();
-    T* Pm = B.P.as<T>();
-    T* KV = B.KV.as<T>();
-    T* UQ = B.UQ.as<T>();
-    T* A = B.A.as<T>();
-    T* G = B.Gt.as<T>();
+    T* XN = m.act[ACT_XN].as<T>();
+    T* Pm = m.act[ACT_P].as<T>();
+    T* KV = m.act[ACT_KV].as<T>();
+    T* UQ = m.act[ACT_UQ].as<T>();
+    T* A = m.act[ACT_A].as<T>();
+    T* G = m.act[ACT_GT].as<T>();
     // attention FLOPs need sum(c_i): known after the plan; use the value of
     // the previous results() (same batch) for the profile annotation
     const double sc_full = static_cast<double>(B.sum_c_ctx + B.sum_c_t), sc_t = static_cast<double>(B.sum_c_t);
-    float2* statX = B.statX.as<float2>();
-    float2* statA = B.statA.as<float2>();
+    float2* statX = m.act[ACT_STATX].as<float2>();
+    float2* statA = m.act[ACT_STATA].as<float2>();
     if constexpr (kTc) {
         // bf16 tensor-core path: GLN1 and the gate are fused into the GEMM A producers
         bool ctx_stats_valid = false;  // X context rows only change in full layers
@@ -1888,7 +1905,7 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
     }
 
     // ---- K5: heads (heads.hpp:47-99) + records
-    float* Y = B.Y.as<float>();
+    float* Y = m.act[ACT_Y].as<float>();
     const double hflops = 2.0 * Td * d * m.head_n;
     if constexpr (kTc) {
         {
@@ -2336,7 +2353,7 @@ int64_t mtfm_cuda_debug_fetch(mtfm_cuda_model* m, mtfm_cuda_batch* b, const char
         return static_cast<int64_t>(bytes);
     };
     const size_t R = static_cast<size_t>(b->rows);
-    if (w == "x") return cp(b->X, R * m->d * 4);
+    if (w == "x") return cp(m->act[mtfm::ACT_X], R * m->d * 4);
     if (w == "src") return cp(b->r_src, R * 4);
     if (w == "item") return cp(b->r_item, R * 4);
     if (w == "prefix") return cp(b->r_prefix, R * 4);
