@@ -546,40 +546,56 @@ template <int NS>
 __global__ void __launch_bounds__(256) gln_multi_kernel(const float* __restrict__ x, long long ldx, long long n_rows,
                                                         int d, const int* __restrict__ row_src,
                                                         const __grid_constant__ GlnCopies c, float eps, long long ldo) {
+    // two rows per warp iteration: twice the loads in flight, and one gain/bias
+    // fetch serves both rows when they share a group (the common case)
     MTFM_PDL_ENTRY();
     const int lane = threadIdx.x & 31;
     const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
-    for (long long r = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); r < n_rows; r += warps) {
-        const float* xr = x + r * ldx;
-        int g = row_src[r];
-        float4 v[NS];
+    for (long long r0 = 2 * (blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5)); r0 < n_rows;
+         r0 += 2 * warps) {
+        const bool two = r0 + 1 < n_rows;
+        float4 v[NS], w[NS];
 #pragma unroll
         for (int k = 0; k < NS; ++k) {
             const int col = 128 * k + 4 * lane;
-            v[k] = col < d ? __ldcs(reinterpret_cast<const float4*>(xr + col)) : make_float4(0.f, 0.f, 0.f, 0.f);
+            v[k] = col < d ? __ldcs(reinterpret_cast<const float4*>(x + r0 * ldx + col)) : make_float4(0.f, 0.f, 0.f, 0.f);
+            w[k] = (two && col < d) ? __ldcs(reinterpret_cast<const float4*>(x + (r0 + 1) * ldx + col))
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
         }
+        int g0 = row_src[r0], g1 = two ? row_src[r0 + 1] : g0;
         normalize_slices<NS, true>(v, d, lane, eps);
-        g = g < 0 ? 0 : g;
+        normalize_slices<NS, true>(w, d, lane, eps);
+        g0 = g0 < 0 ? 0 : g0;
+        g1 = g1 < 0 ? 0 : g1;
         for (int l = 0; l < c.n; ++l) {
-            __nv_bfloat16* o = static_cast<__nv_bfloat16*>(c.out[l]) + r * ldo;
+            __nv_bfloat16* o = static_cast<__nv_bfloat16*>(c.out[l]) + r0 * ldo;
             if (c.gain[l] == nullptr) {  // the normalised rows themselves (xhat)
 #pragma unroll
                 for (int k = 0; k < NS; ++k) {
                     const int col = 128 * k + 4 * lane;
-                    if (col < d) st4(o + col, v[k]);
+                    if (col < d) {
+                        st4(o + col, v[k]);
+                        if (two) st4(o + ldo + col, w[k]);
+                    }
                 }
                 continue;
             }
-            const float* gg = c.gain[l] + (long long)g * d;
-            const float* bb = c.bias[l] + (long long)g * d;
 #pragma unroll
             for (int k = 0; k < NS; ++k) {
                 const int col = 128 * k + 4 * lane;
                 if (col < d) {
-                    const float4 ga = __ldg(reinterpret_cast<const float4*>(gg + col));
-                    const float4 be = __ldg(reinterpret_cast<const float4*>(bb + col));
+                    float4 ga = __ldg(reinterpret_cast<const float4*>(c.gain[l] + (long long)g0 * d + col));
+                    float4 be = __ldg(reinterpret_cast<const float4*>(c.bias[l] + (long long)g0 * d + col));
                     st4(o + col, make_float4(v[k].x * ga.x + be.x, v[k].y * ga.y + be.y, v[k].z * ga.z + be.z,
                                              v[k].w * ga.w + be.w));
+                    if (two) {
+                        if (g1 != g0) {
+                            ga = __ldg(reinterpret_cast<const float4*>(c.gain[l] + (long long)g1 * d + col));
+                            be = __ldg(reinterpret_cast<const float4*>(c.bias[l] + (long long)g1 * d + col));
+                        }
+                        st4(o + ldo + col, make_float4(w[k].x * ga.x + be.x, w[k].y * ga.y + be.y,
+                                                       w[k].z * ga.z + be.z, w[k].w * ga.w + be.w));
+                    }
                 }
             }
         }
@@ -589,11 +605,12 @@ __global__ void __launch_bounds__(256) gln_multi_kernel(const float* __restrict_
 void launch_gln_multi_bf16(const float* x, long long ldx, long long n_rows, int d, const int* row_src,
                            const GlnCopies& c, float eps, long long ldo, cudaStream_t st) {
     if (n_rows == 0 || c.n == 0) return;
-    const int blocks = static_cast<int>(std::min<long long>(cdiv(n_rows, 8), 148ll * 16));
+    const int blocks = static_cast<int>(std::min<long long>(cdiv(n_rows, 16), 148ll * 16));
     const int ns = static_cast<int>(cdiv(d, 128));
     if (ns <= 1) launch_k(gln_multi_kernel<1>, dim3(blocks), dim3(256), 0, st, x, ldx, n_rows, d, row_src, c, eps, ldo);
     else if (ns == 2) launch_k(gln_multi_kernel<2>, dim3(blocks), dim3(256), 0, st, x, ldx, n_rows, d, row_src, c, eps, ldo);
     else if (ns <= 4) launch_k(gln_multi_kernel<4>, dim3(blocks), dim3(256), 0, st, x, ldx, n_rows, d, row_src, c, eps, ldo);
+    else if (ns <= 6) launch_k(gln_multi_kernel<6>, dim3(blocks), dim3(256), 0, st, x, ldx, n_rows, d, row_src, c, eps, ldo);
     else launch_k(gln_multi_kernel<8>, dim3(blocks), dim3(256), 0, st, x, ldx, n_rows, d, row_src, c, eps, ldo);
 }
 
@@ -636,82 +653,88 @@ __global__ void __launch_bounds__(256) gate_kernel(const T* __restrict__ a, long
     }
 }
 
-// bf16, d == 256: lane owns 8 consecutive columns (one 16-byte load per tensor
-// and row) and each warp carries RPW rows at once, so 2*RPW independent loads
-// are in flight per warp instead of 2.
-template <int RPW>
-__global__ void __launch_bounds__(256, 4) gate_bf16_d256_kernel(const __nv_bfloat16* __restrict__ a, long long lda,
-                                                             const __nv_bfloat16* __restrict__ u, long long ldu,
-                                                             long long n_rows, const int* __restrict__ row_src,
-                                                             const float* __restrict__ gain,
-                                                             const float* __restrict__ bias, float eps,
-                                                             __nv_bfloat16* __restrict__ out, long long ldo) {
+// bf16, d = 256*NS8: lane owns 8 consecutive columns per 256-column slice (one
+// 16-byte load per tensor, slice and row) and each warp carries RPW rows at
+// once, so 2*RPW*NS8 independent loads are in flight per warp.
+template <int RPW, int NS8>
+__global__ void __launch_bounds__(256, 4) gate_bf16_kernel(const __nv_bfloat16* __restrict__ a, long long lda,
+                                                        const __nv_bfloat16* __restrict__ u, long long ldu,
+                                                        long long n_rows, const int* __restrict__ row_src,
+                                                        const float* __restrict__ gain,
+                                                        const float* __restrict__ bias, float eps,
+                                                        __nv_bfloat16* __restrict__ out, long long ldo) {
     MTFM_PDL_ENTRY();
+    constexpr int d = 256 * NS8;
     const int lane = threadIdx.x & 31;
-    const int c = 8 * lane;
     const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
     for (long long i0 = (blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5)) * RPW; i0 < n_rows;
          i0 += warps * RPW) {
-        uint4 av[RPW], uv[RPW];
+        uint4 av[RPW][NS8], uv[RPW][NS8];
         int g[RPW];
 #pragma unroll
         for (int r = 0; r < RPW; ++r) {
             const long long i = i0 + r;
-            if (i < n_rows) {
-                av[r] = __ldcs(reinterpret_cast<const uint4*>(a + i * lda + c));
-                uv[r] = __ldcs(reinterpret_cast<const uint4*>(u + i * ldu + c));
-                g[r] = row_src[i];
-            } else {
-                av[r] = make_uint4(0, 0, 0, 0);
-                uv[r] = make_uint4(0, 0, 0, 0);
-                g[r] = 0;
+#pragma unroll
+            for (int k = 0; k < NS8; ++k) {
+                const int c = 256 * k + 8 * lane;
+                av[r][k] = i < n_rows ? __ldcs(reinterpret_cast<const uint4*>(a + i * lda + c)) : make_uint4(0, 0, 0, 0);
+                uv[r][k] = i < n_rows ? __ldcs(reinterpret_cast<const uint4*>(u + i * ldu + c)) : make_uint4(0, 0, 0, 0);
             }
+            g[r] = i < n_rows ? row_src[i] : 0;
         }
 #pragma unroll
         for (int r = 0; r < RPW; ++r) {
             const long long i = i0 + r;
-            float x[8], y[8];
-            const __nv_bfloat162* ah = reinterpret_cast<const __nv_bfloat162*>(&av[r]);
-            const __nv_bfloat162* uh = reinterpret_cast<const __nv_bfloat162*>(&uv[r]);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const float2 fa = __bfloat1622float2(ah[k]), fu = __bfloat1622float2(uh[k]);
-                x[2 * k] = fa.x;
-                x[2 * k + 1] = fa.y;
-                y[2 * k] = fu.x;
-                y[2 * k + 1] = fu.y;
-            }
+            float x[NS8][8];
             float sum = 0.f;
 #pragma unroll
-            for (int k = 0; k < 8; ++k) sum += x[k];
+            for (int k = 0; k < NS8; ++k) {
+                const __nv_bfloat162* ah = reinterpret_cast<const __nv_bfloat162*>(&av[r][k]);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float2 fa = __bfloat1622float2(ah[j]);
+                    x[k][2 * j] = fa.x;
+                    x[k][2 * j + 1] = fa.y;
+                    sum += fa.x + fa.y;
+                }
+            }
             sum = warp_sum(sum);
-            const float mean = sum * (1.f / 256.f);  // exact: power-of-two divisor
+            // multiply by the rounded reciprocal (exact for power-of-two d), as normalize_slices<kFast>
+            const float mean = sum * (1.f / static_cast<float>(d));
             float q = 0.f;
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                x[k] -= mean;
-                q += x[k] * x[k];
-            }
+            for (int k = 0; k < NS8; ++k)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    x[k][j] -= mean;
+                    q += x[k][j] * x[k][j];
+                }
             q = warp_sum(q);
             // bf16 output: MUFU.RSQ (~2 ulp) instead of the IEEE sqrt + divide sequence
-            const float inv = rsqrtf(q * (1.f / 256.f) + eps);
+            const float inv = rsqrtf(q * (1.f / static_cast<float>(d)) + eps);
             if (i >= n_rows) continue;
             const int gg = g[r] < 0 ? 0 : g[r];
-            const float4 g0 = __ldg(reinterpret_cast<const float4*>(gain + gg * 256 + c));
-            const float4 g1 = __ldg(reinterpret_cast<const float4*>(gain + gg * 256 + c + 4));
-            const float4 b0 = __ldg(reinterpret_cast<const float4*>(bias + gg * 256 + c));
-            const float4 b1 = __ldg(reinterpret_cast<const float4*>(bias + gg * 256 + c + 4));
-            const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-            const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-            uint32_t o[4];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const float lo = ((x[2 * k] * inv) * gv[2 * k] + bv[2 * k]) * y[2 * k];
-                const float hi = ((x[2 * k + 1] * inv) * gv[2 * k + 1] + bv[2 * k + 1]) * y[2 * k + 1];
-                const __nv_bfloat162 h2 = __floats2bfloat162_rn(lo, hi);
-                o[k] = *reinterpret_cast<const uint32_t*>(&h2);
+            for (int k = 0; k < NS8; ++k) {
+                const int c = 256 * k + 8 * lane;
+                const float4 g0 = __ldg(reinterpret_cast<const float4*>(gain + gg * d + c));
+                const float4 g1 = __ldg(reinterpret_cast<const float4*>(gain + gg * d + c + 4));
+                const float4 b0 = __ldg(reinterpret_cast<const float4*>(bias + gg * d + c));
+                const float4 b1 = __ldg(reinterpret_cast<const float4*>(bias + gg * d + c + 4));
+                const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+                const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+                const __nv_bfloat162* uh = reinterpret_cast<const __nv_bfloat162*>(&uv[r][k]);
+                uint32_t o[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float2 fu = __bfloat1622float2(uh[j]);
+                    const float lo = ((x[k][2 * j] * inv) * gv[2 * j] + bv[2 * j]) * fu.x;
+                    const float hi = ((x[k][2 * j + 1] * inv) * gv[2 * j + 1] + bv[2 * j + 1]) * fu.y;
+                    const __nv_bfloat162 h2 = __floats2bfloat162_rn(lo, hi);
+                    o[j] = *reinterpret_cast<const uint32_t*>(&h2);
+                }
+                *reinterpret_cast<uint4*>(out + i * ldo + c) = make_uint4(o[0], o[1], o[2], o[3]);
             }
-            *reinterpret_cast<uint4*>(out + i * ldo + c) = make_uint4(o[0], o[1], o[2], o[3]);
         }
     }
 }
@@ -722,12 +745,15 @@ void launch_gate(const T* a, long long lda, const T* u, long long ldu, long long
                  long long ldo, cudaStream_t st) {
     if (n_rows == 0) return;
     if constexpr (std::is_same_v<T, __nv_bfloat16>) {
-        if (d == 256 && lda % 8 == 0 && ldu % 8 == 0 && ldo % 8 == 0) {
-            const int blocks = static_cast<int>(std::min<long long>(cdiv(n_rows, 8 * 2), 148ll * 16));
-            launch_k(gate_bf16_d256_kernel<2>, dim3(blocks), dim3(256), 0, st, a, lda, u, ldu, n_rows, row_src_of_rows, gain, bias,
-                                                             eps, out, ldo);
-            return;
-        }
+        const bool al = lda % 8 == 0 && ldu % 8 == 0 && ldo % 8 == 0;
+#define MTFM_GATE16(RPW, NS8)                                                                                     \
+    launch_k(gate_bf16_kernel<RPW, NS8>, dim3(static_cast<int>(std::min<long long>(cdiv(n_rows, 8 * RPW), 148ll * 16))), \
+             dim3(256), 0, st, a, lda, u, ldu, n_rows, row_src_of_rows, gain, bias, eps, out, ldo)
+        if (al && d == 256) { MTFM_GATE16(2, 1); return; }
+        if (al && d == 512) { MTFM_GATE16(2, 2); return; }
+        if (al && d == 768) { MTFM_GATE16(1, 3); return; }
+        if (al && d == 1024) { MTFM_GATE16(1, 4); return; }
+#undef MTFM_GATE16
     }
     const int blocks = static_cast<int>(std::min<long long>(cdiv(n_rows, 8), 148ll * 16));
     const int ns = static_cast<int>(cdiv(d, 128));

@@ -1,0 +1,61 @@
+"""The SURVEY §8(d) sweep axes on the CUDA path, against the pinned numpy
+oracle: layer mixes (K:P) in {(0:1), (1:1), (3:1), (5:1), (3:0)} (bench.hpp:43-58),
+targets per user in {4, 16, 64, 256} and the three AttnNorm row scales
+(model_config.hpp:18-24). Small users so the oracle finishes in seconds; the
+model width is the BASELINE small one (d=256, H=8, G=2). Needs a B200."""
+import dataclasses
+
+import numpy as np
+import pytest
+
+from helpers import oracle_records, rel_err, to_oracle
+from paper_2602_11235_b200 import Model, datagen
+
+pytestmark = pytest.mark.gpu
+
+BF16_TOL = 2e-2
+FP32_TOL = 1e-4
+
+
+def _run(wl, n_users, precision):
+    b = datagen.generate(wl, n_users=n_users)
+    m = Model(wl.schemas, wl.cfg, precision=precision)
+    P = datagen.random_params(m.param_specs(), seed=13)
+    m.set_params(P)
+    osch, ocfg = to_oracle(wl.schemas, wl.cfg)
+    keys, z_ref, _ = oracle_records(osch, ocfg, P, b)
+    ra = m.forward_batch(b)
+    assert np.array_equal(np.stack([ra.user_id, ra.scenario_id, ra.exposure_index, ra.task_index], 1), keys)
+    if precision == "bf16":
+        assert np.max(np.abs(ra.logit - z_ref)) <= BF16_TOL
+    else:
+        assert rel_err(ra.logit.astype(np.float64), z_ref) <= FP32_TOL
+
+
+def _wl(K, P, blocks=1, norm="valid", **kw):
+    wl = datagen.WORKLOADS["small"]()
+    hta = dataclasses.replace(wl.cfg.hta, target_layers=K, full_layers=P, blocks=blocks, norm=norm)
+    kw.setdefault("hist_len", 60)
+    kw.setdefault("rt_len", 20)
+    kw.setdefault("exp_per_scen", 3)
+    return dataclasses.replace(wl, cfg=dataclasses.replace(wl.cfg, hta=hta), **kw)
+
+
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+@pytest.mark.parametrize("K,P,blocks", [(0, 1, 2), (1, 1, 1), (3, 1, 2), (5, 1, 1), (3, 0, 1)])
+def test_layer_mix(K, P, blocks, precision):
+    """Target-layer runs longer than one multi-copy GLN launch (5:1), runs with
+    no full layer after them (3:0), full-only stacks (0:1) and repeated blocks."""
+    _run(_wl(K, P, blocks), 3, precision)
+
+
+@pytest.mark.parametrize("per_scen", [1, 4, 16, 64])
+def test_targets_per_user(per_scen):
+    """4 scenarios x per_scen exposures = 4..256 targets per user: T query
+    tiles from a fraction of one tile to two full tiles per scenario."""
+    _run(_wl(3, 1, hist_len=40, rt_len=10, exp_per_scen=per_scen, seed=17), 2, "bf16")
+
+
+@pytest.mark.parametrize("norm", ["valid", "seqlen", "none"])
+def test_attn_norm(norm):
+    _run(_wl(1, 1, norm=norm), 3, "bf16")
