@@ -97,7 +97,9 @@ using ptx::silu2_bf16;
 
 }  // namespace attn_detail
 
-template <int D>
+// EMU: of every 16 SiLU pairs in an unmasked chunk, EMU run on the FMA/ALU pipes
+// (silu2_bf16_fma) and the rest on MUFU.TANH, so neither pipe alone bounds the phase
+template <int D, int EMU = 0>
 __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__ AttnParams prm) {
     using C = attn_detail::Cfg<D>;
     constexpr int BKV = C::BKV;
@@ -332,7 +334,9 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
                     uint32_t* pk = packed + c * (CPW / 2);
                     if (__all_sync(0xffffffffu, nvalid >= CPW)) {
 #pragma unroll
-                        for (int e = 0; e < CPW; e += 2) pk[e / 2] = attn_detail::silu2_bf16(v[e], v[e + 1]);
+                        for (int e = 0; e < CPW; e += 2)
+                            pk[e / 2] = ((e / 2) * EMU) % 16 < EMU ? ptx::silu2_bf16_fma(v[e], v[e + 1])
+                                                                   : attn_detail::silu2_bf16(v[e], v[e + 1]);
                     } else if (__all_sync(0xffffffffu, nvalid <= 0)) {
 #pragma unroll
                         for (int e = 0; e < CPW / 2; ++e) pk[e] = 0u;

@@ -657,7 +657,7 @@ __global__ void __launch_bounds__(256) gate_kernel(const T* __restrict__ a, long
 // 16-byte load per tensor, slice and row) and each warp carries RPW rows at
 // once, so 2*RPW*NS8 independent loads are in flight per warp.
 template <int RPW, int NS8>
-__global__ void __launch_bounds__(256, 4) gate_bf16_kernel(const __nv_bfloat16* __restrict__ a, long long lda,
+__global__ void __launch_bounds__(256, NS8 * RPW <= 2 ? 4 : 2) gate_bf16_kernel(const __nv_bfloat16* __restrict__ a, long long lda,
                                                         const __nv_bfloat16* __restrict__ u, long long ldu,
                                                         long long n_rows, const int* __restrict__ row_src,
                                                         const float* __restrict__ gain,
@@ -685,7 +685,7 @@ __global__ void __launch_bounds__(256, 4) gate_bf16_kernel(const __nv_bfloat16* 
 #pragma unroll
         for (int r = 0; r < RPW; ++r) {
             const long long i = i0 + r;
-            float x[NS8][8];
+            // two passes over the packed row (sum, then centred squares): no unpacked copy
             float sum = 0.f;
 #pragma unroll
             for (int k = 0; k < NS8; ++k) {
@@ -693,8 +693,6 @@ __global__ void __launch_bounds__(256, 4) gate_bf16_kernel(const __nv_bfloat16* 
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const float2 fa = __bfloat1622float2(ah[j]);
-                    x[k][2 * j] = fa.x;
-                    x[k][2 * j + 1] = fa.y;
                     sum += fa.x + fa.y;
                 }
             }
@@ -703,12 +701,15 @@ __global__ void __launch_bounds__(256, 4) gate_bf16_kernel(const __nv_bfloat16* 
             const float mean = sum * (1.f / static_cast<float>(d));
             float q = 0.f;
 #pragma unroll
-            for (int k = 0; k < NS8; ++k)
+            for (int k = 0; k < NS8; ++k) {
+                const __nv_bfloat162* ah = reinterpret_cast<const __nv_bfloat162*>(&av[r][k]);
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    x[k][j] -= mean;
-                    q += x[k][j] * x[k][j];
+                for (int j = 0; j < 4; ++j) {
+                    const float2 fa = __bfloat1622float2(ah[j]);
+                    const float dx = fa.x - mean, dy = fa.y - mean;
+                    q += dx * dx + dy * dy;
                 }
+            }
             q = warp_sum(q);
             // bf16 output: MUFU.RSQ (~2 ulp) instead of the IEEE sqrt + divide sequence
             const float inv = rsqrtf(q * (1.f / static_cast<float>(d)) + eps);
@@ -723,13 +724,15 @@ __global__ void __launch_bounds__(256, 4) gate_bf16_kernel(const __nv_bfloat16* 
                 const float4 b1 = __ldg(reinterpret_cast<const float4*>(bias + gg * d + c + 4));
                 const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
                 const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+                const __nv_bfloat162* ah = reinterpret_cast<const __nv_bfloat162*>(&av[r][k]);
                 const __nv_bfloat162* uh = reinterpret_cast<const __nv_bfloat162*>(&uv[r][k]);
                 uint32_t o[4];
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
+                    const float2 fa = __bfloat1622float2(ah[j]);
                     const float2 fu = __bfloat1622float2(uh[j]);
-                    const float lo = ((x[k][2 * j] * inv) * gv[2 * j] + bv[2 * j]) * fu.x;
-                    const float hi = ((x[k][2 * j + 1] * inv) * gv[2 * j + 1] + bv[2 * j + 1]) * fu.y;
+                    const float lo = (((fa.x - mean) * inv) * gv[2 * j] + bv[2 * j]) * fu.x;
+                    const float hi = (((fa.y - mean) * inv) * gv[2 * j + 1] + bv[2 * j + 1]) * fu.y;
                     const __nv_bfloat162 h2 = __floats2bfloat162_rn(lo, hi);
                     o[j] = *reinterpret_cast<const uint32_t*>(&h2);
                 }
@@ -751,8 +754,8 @@ void launch_gate(const T* a, long long lda, const T* u, long long ldu, long long
              dim3(256), 0, st, a, lda, u, ldu, n_rows, row_src_of_rows, gain, bias, eps, out, ldo)
         if (al && d == 256) { MTFM_GATE16(2, 1); return; }
         if (al && d == 512) { MTFM_GATE16(2, 2); return; }
-        if (al && d == 768) { MTFM_GATE16(1, 3); return; }
-        if (al && d == 1024) { MTFM_GATE16(1, 4); return; }
+        if (al && d == 768) { MTFM_GATE16(2, 3); return; }
+        if (al && d == 1024) { MTFM_GATE16(2, 4); return; }
 #undef MTFM_GATE16
     }
     const int blocks = static_cast<int>(std::min<long long>(cdiv(n_rows, 8), 148ll * 16));
