@@ -67,9 +67,12 @@ template <typename Less>
 __device__ void bitonic_sort(long long* ts, long long* sec, int npad, Less less) {
     for (int k = 2; k <= npad; k <<= 1) {
         for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = threadIdx.x; i < npad; i += blockDim.x) {
-                const int ixj = i ^ j;
-                if (ixj > i) {
+            // one compare-exchange pair per thread and pass (no idle half):
+            // pair t -> lower index i (bit j clear), partner i + j
+            for (int t = threadIdx.x; t < (npad >> 1); t += blockDim.x) {
+                const int i = ((t & ~(j - 1)) << 1) | (t & (j - 1));
+                const int ixj = i + j;
+                {
                     const bool up = (i & k) == 0;
                     const long long ta = ts[i], sa = sec[i], tb = ts[ixj], sb = sec[ixj];
                     const bool swap = up ? less(tb, sb, ta, sa) : less(ta, sa, tb, sb);
@@ -107,7 +110,7 @@ __device__ __forceinline__ float row_scale_of(int norm, int c, int n_tokens) {
 
 // One CTA per user: plan_tokens (tokenizer.hpp:53-134) + make_stack_geom
 // (hta.hpp:40-71) in prefix form + record slots + input validation.
-__global__ void plan_kernel(PlanArgs a) {
+__global__ void __launch_bounds__(256, 8) plan_kernel(PlanArgs a) {
     MTFM_PDL_ENTRY();
     extern __shared__ long long sm_sort[];
     long long* s_ts = sm_sort;
@@ -194,8 +197,15 @@ __global__ void plan_kernel(PlanArgs a) {
             a.rm.src_rows[a.src_base[src] + a.us_off[(long long)u * a.n_src + src] + rank] = row;
         }
     }
-    // validation of sequence pieces (pile order = non-empty sequences in list order)
-    for (int e = ev0 + tid; e < ev1; e += blockDim.x) {
+    // validation of sequence pieces (pile order = non-empty sequences in list order),
+    // one (event, slot) check per thread: the smallest error key wins, which is
+    // each event's first failing slot as in the sequential rule
+    int cslots = 1;
+    for (int sc = 0; sc < a.n_src; ++sc)
+        if (srcs[sc].kind < 2) cslots = max(cslots, srcs[sc].nslot[0]);
+    for (int idx = tid; idx < n_ev * cslots; idx += blockDim.x) {
+        const int e = ev0 + idx / cslots;
+        const int s = idx - (e - ev0) * cslots;
         const int sq = find_seq(b.ev_off, s0, s1, e);
         int piece = 0;
         for (int q = s0; q < sq; ++q) piece += b.ev_off[q + 1] > b.ev_off[q];
@@ -203,20 +213,14 @@ __global__ void plan_kernel(PlanArgs a) {
         const int r = e - b.ev_off[sq];
         unsigned long long k = ~0ull;
         if (src < 0) {
-            k = err_key(u, piece, 0, 0, ERR_INTEGRITY);
-        } else {
-            const SourceInfo si = a.src[src];
+            if (s == 0) k = err_key(u, piece, 0, 0, ERR_INTEGRITY);
+        } else if (s < srcs[src].nslot[0]) {
             const int cnt = b.ev_feat_off[e + 1] - b.ev_feat_off[e];
-            for (int s = 0; s < si.nslot[0]; ++s) {
-                if (cnt <= s) {
-                    k = err_key(u, piece, 1 + 2 * s, r, ERR_DIMENSION);
-                    break;
-                }
+            if (cnt <= s) {
+                k = err_key(u, piece, 1 + 2 * s, r, ERR_DIMENSION);
+            } else {
                 const int id = b.ev_feats[b.ev_feat_off[e] + s];
-                if (id < 0 || id >= a.slots[si.slot0 + s].vocab) {
-                    k = err_key(u, piece, 2 + 2 * s, r, ERR_LOOKUP);
-                    break;
-                }
+                if (id < 0 || id >= a.slots[srcs[src].slot0 + s].vocab) k = err_key(u, piece, 2 + 2 * s, r, ERR_LOOKUP);
             }
         }
         if (k != ~0ull) atomicMin(&s_err, k);
@@ -309,30 +313,44 @@ __global__ void plan_kernel(PlanArgs a) {
         a.rm.t_rec0[t] = a.rec_off[u] + rec_before + rho;
         a.rm.t_rec_stride[t] = n_s;
         const int piece = n_pieces_seq + distinct_below;
+        if (src >= 0)
+            a.rm.src_rows[a.src_base[src] + a.us_off[(long long)u * a.n_src + src] + rho] = static_cast<int>(row);
+        // s_ts[p] is only read by this iteration: stash what the slot checks need
+        s_ts[p] = (static_cast<long long>(piece) << 40) | (static_cast<long long>(rho) << 16) | (src + 1);
+    }
+    __syncthreads();
+    // one (exposure, slot) check per thread (smallest key = first failing slot)
+    int tslots = 1;
+    for (int sc = 0; sc < a.n_src; ++sc)
+        if (srcs[sc].kind == 2) tslots = max(tslots, srcs[sc].nslot[0] + srcs[sc].nslot[1] + srcs[sc].nslot[2]);
+    for (int idx = tid; idx < n_t * tslots; idx += blockDim.x) {
+        const int p = idx / tslots;
+        const int gs = idx - p * tslots;
+        const long long pk = s_ts[p];
+        const int src = static_cast<int>(pk & 0xffff) - 1;
+        const int rho = static_cast<int>((pk >> 16) & 0xffffff);
+        const int piece = static_cast<int>(pk >> 40);
         unsigned long long k = ~0ull;
         if (src < 0) {
-            k = err_key(u, piece, 0, 0, ERR_INTEGRITY);
+            if (gs == 0) k = err_key(u, piece, 0, 0, ERR_INTEGRITY);
         } else {
-            a.rm.src_rows[a.src_base[src] + a.us_off[(long long)u * a.n_src + src] + rho] = static_cast<int>(row);
-            const SourceInfo si = a.src[src];
-            int slot_base = 0;
-            int blk_off = 0;
-            for (int blk = 0; blk < 3 && k == ~0ull; ++blk) {
-                const int cnt = b.exp_blk[3 * x + blk];
-                for (int s = 0; s < si.nslot[blk]; ++s) {
-                    const int gs = slot_base + s;
-                    if (cnt <= s) {
-                        k = err_key(u, piece, 1 + 2 * gs, rho, ERR_DIMENSION);
-                        break;
-                    }
-                    const int id = b.exp_feats[b.exp_feat_off[x] + blk_off + s];
-                    if (id < 0 || id >= a.slots[si.slot0 + gs].vocab) {
-                        k = err_key(u, piece, 2 + 2 * gs, rho, ERR_LOOKUP);
-                        break;
-                    }
+            const SourceInfo& si = srcs[src];
+            if (gs < si.nslot[0] + si.nslot[1] + si.nslot[2]) {
+                const int x = x0 + static_cast<int>(s_sec[p] & 0xffffffffll);
+                int blk = 0, base = 0, blk_off = 0;
+                while (gs >= base + si.nslot[blk]) {
+                    base += si.nslot[blk];
+                    blk_off += b.exp_blk[3 * x + blk];
+                    ++blk;
                 }
-                slot_base += si.nslot[blk];
-                blk_off += cnt;
+                const int sl = gs - base;
+                const int cnt = b.exp_blk[3 * x + blk];
+                if (cnt <= sl) {
+                    k = err_key(u, piece, 1 + 2 * gs, rho, ERR_DIMENSION);
+                } else {
+                    const int id = b.exp_feats[b.exp_feat_off[x] + blk_off + sl];
+                    if (id < 0 || id >= a.slots[si.slot0 + gs].vocab) k = err_key(u, piece, 2 + 2 * gs, rho, ERR_LOOKUP);
+                }
             }
         }
         if (k != ~0ull) atomicMin(&s_err, k);
