@@ -164,7 +164,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="small", choices=sorted(CONFIGS))
     ap.add_argument("--users", type=int, default=None, help="users per GPU (default: the config's)")
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=50, help="e2e steps per API (pipelined and synchronous)")
     ap.add_argument("--ref-users", type=int, default=96)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-json", default=None)
