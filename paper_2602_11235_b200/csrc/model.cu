@@ -967,7 +967,11 @@ void run_attn_tc(const mtfm_cuda_model& m, AttnParams p, const __nv_bfloat16* q,
         case 32: {
             static unsigned long long* tr = nullptr;
             static int calls = 0;
-            const bool tracing = std::getenv("MTFM_ATTN_TRACE") != nullptr && p.n_tiles > 20000 && calls++ == 1;
+            // MTFM_ATTN_TRACE=full|target: second launch of that layer kind (-DMTFM_ATTN_TRACE builds)
+            const char* tenv = std::getenv("MTFM_ATTN_TRACE");
+            const bool tracing = tenv != nullptr &&
+                                 (std::string(tenv) == "target" ? p.n_tiles < 20000 : p.n_tiles > 20000) &&
+                                 calls++ == 1;
             if (tracing) {
                 if (!tr) ck(cudaMalloc(&tr, 2048 * 8), "trace alloc");
                 ck(cudaMemsetAsync(tr, 0, 2048 * 8, st), "trace clear");
