@@ -99,10 +99,18 @@ using ptx::silu2_bf16;
 
 // EMU: of every 16 SiLU pairs in an unmasked chunk, EMU run on the FMA/ALU pipes
 // (silu2_bf16_fma) and the rest on MUFU.TANH, so neither pipe alone bounds the phase
-template <int D, int EMU = 0>
+// SPA: P aliases S. Three S/P TMEM buffers; each SiLU warp overwrites the
+// first half of its own S columns with packed bf16 P and every one of the 16
+// SiLU warps works on every key tile (a quarter of its columns); a buffer is
+// released to the S issuer only after the P.V that reads it completed.
+template <int D, int EMU = 0, bool SPA = false>
 __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__ AttnParams prm) {
     using C = attn_detail::Cfg<D>;
     constexpr int BKV = C::BKV;
+    constexpr int NB = SPA ? 3 : 2;                  // S (and, with SPA, P) buffers
+    constexpr uint32_t kOCol = SPA ? NB * BKV : C::O_COL;
+    constexpr int kOB = SPA ? ((NB * BKV + 2 * D <= 512) ? 2 : 1) : C::OB;
+    static_assert(kOCol + kOB * D <= 512, "TMEM budget");
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sQ = smem;
@@ -112,11 +120,11 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
     uint64_t* q_empty = bars + 2;  // [2]
     uint64_t* o_full = bars + 4;   // [2]
     uint64_t* o_empty = bars + 6;  // [2]
-    uint64_t* s_full = bars + 8;   // [2]
-    uint64_t* s_empty = bars + 10; // [2]
-    uint64_t* p_full = bars + 12;  // [2]
-    uint64_t* p_empty = bars + 14; // [2]
-    uint64_t* kv_full = bars + 16; // [kStages]
+    uint64_t* s_full = bars + 8;            // [NB]
+    uint64_t* s_empty = bars + 8 + NB;      // [NB] (SPA: released by the P.V commit)
+    uint64_t* p_full = bars + 8 + 2 * NB;   // [NB]
+    uint64_t* p_empty = bars + 8 + 3 * NB;  // [NB] (unused with SPA)
+    uint64_t* kv_full = bars + 8 + 4 * NB;  // [kStages]
     uint64_t* kv_empty = kv_full + C::kStages;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kv_empty + C::kStages);
 
@@ -137,9 +145,11 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
             ptx::mbar_init(&q_empty[i], 1);
             ptx::mbar_init(&o_full[i], 1);
             ptx::mbar_init(&o_empty[i], 4);
+        }
+        for (int i = 0; i < NB; ++i) {
             ptx::mbar_init(&s_full[i], 1);
-            ptx::mbar_init(&s_empty[i], C::kSilu / 2);
-            ptx::mbar_init(&p_full[i], C::kSilu / 2);
+            ptx::mbar_init(&s_empty[i], SPA ? 1 : C::kSilu / 2);
+            ptx::mbar_init(&p_full[i], SPA ? C::kSilu : C::kSilu / 2);
             ptx::mbar_init(&p_empty[i], 1);
         }
         for (int i = 0; i < C::kStages; ++i) {
@@ -217,11 +227,11 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
             }
             const uint32_t sq = ptx::smem_u32(sQ + qb * C::Q_BYTES);
             for (int j = 0; j < n_kv; ++j) {
-                const uint32_t buf = s_cnt & 1;
+                const uint32_t buf = s_cnt % NB;
                 if (s_cnt < 128) trace(1024 + 4 * s_cnt + 0);
                 ptx::mbar_wait(&kv_full[stage], phase);
                 if (s_cnt < 128) trace(1024 + 4 * s_cnt + 1);
-                ptx::mbar_wait(&s_empty[buf], ((s_cnt >> 1) & 1) ^ 1);
+                ptx::mbar_wait(&s_empty[buf], ((s_cnt / NB) & 1) ^ 1);
                 if (s_cnt < 128) trace(1024 + 4 * s_cnt + 2);
                 ptx::tc_fence_after();
                 if (ptx::elect_one()) {
@@ -259,8 +269,8 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
         for (int t = blockIdx.x; t < prm.n_tiles; t += gridDim.x, ++it) {
             const AttnTile tile = prm.tiles[t];
             const int n_kv = (tile.kmax + BKV - 1) / BKV;
-            const int ob = it % C::OB;
-            ptx::mbar_wait(&o_empty[ob], ((it / C::OB) & 1) ^ 1);
+            const int ob = it % kOB;
+            ptx::mbar_wait(&o_empty[ob], ((it / kOB) & 1) ^ 1);
             ptx::tc_fence_after();
             if (n_kv == 0) {
                 if (ptx::elect_one()) ptx::umma_commit(&o_full[ob]);
@@ -268,28 +278,93 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
                 continue;
             }
             for (int j = 0; j < n_kv; ++j, ++cnt) {
-                const uint32_t buf = cnt & 1;
-                ptx::mbar_wait(&p_full[buf], (cnt >> 1) & 1);
+                const uint32_t buf = cnt % NB;
+                ptx::mbar_wait(&p_full[buf], (cnt / NB) & 1);
                 if (cnt < 128) trace(1024 + 4 * cnt + 3);
                 ptx::tc_fence_after();
                 if (ptx::elect_one()) {
-                    const uint32_t p_tmem = tmem + C::P_COL + buf * (BKV / 2);
                     const uint32_t sv = ptx::smem_u32(sKV + stage * C::STAGE_BYTES + C::KV_TILE_BYTES);
-                    const uint32_t o_tmem = tmem + C::O_COL + ob * D;
+                    const uint32_t o_tmem = tmem + kOCol + ob * D;
 #pragma unroll
                     for (int kk = 0; kk < BKV / 16; ++kk) {
+                        uint32_t p_col;
+                        if constexpr (SPA) {
+                            // keys [16kk, 16kk+16) were packed by the SiLU warp owning
+                            // S columns [CW*c, CW*(c+1)), c = 16kk / CW, into its first CW/2
+                            constexpr int CW = BKV / 4;
+                            p_col = buf * BKV + ((16 * kk) / CW) * CW + ((16 * kk) % CW) / 2;
+                        } else {
+                            p_col = C::P_COL + buf * (BKV / 2) + kk * 8;
+                        }
                         const uint64_t db = ptx::smem_desc(sv + kk * 16 * C::ROWB, BKV * C::ROWB, 8 * C::ROWB, C::LAYOUT);
-                        ptx::umma_bf16_ts(o_tmem, p_tmem + kk * 8, db, idesc_o, (j > 0 || kk > 0));
+                        ptx::umma_bf16_ts(o_tmem, tmem + p_col, db, idesc_o, (j > 0 || kk > 0));
                     }
                     ptx::umma_commit(&kv_empty[stage]);
-                    ptx::umma_commit(&p_empty[buf]);
+                    ptx::umma_commit(SPA ? &s_empty[buf] : &p_empty[buf]);
                     if (j == n_kv - 1) ptx::umma_commit(&o_full[ob]);
                 }
                 __syncwarp();
                 if (++stage == C::kStages) stage = 0;
             }
         }
-    } else if (warp >= 4 && warp < 4 + C::kSilu) {
+    } else if (SPA && warp >= 4 && warp < 4 + C::kSilu) {
+        // ------------------------------------------------ SiLU warps, P aliasing S
+        constexpr int CW = BKV / 4;               // key columns per warp and key tile
+        const uint32_t q = warp & 3;              // TMEM lane quarter
+        const uint32_t cq = (warp - 4) >> 2;      // column quarter
+        const uint32_t m = q * 32 + lane;         // MMA row == TMEM lane
+        const uint32_t lane_addr = (q * 32u) << 16;
+        uint32_t s_cnt = 0;
+        for (int t = blockIdx.x; t < prm.n_tiles; t += gridDim.x) {
+            const AttnTile tile = prm.tiles[t];
+            const int n_kv = (tile.kmax + BKV - 1) / BKV;
+            const int hs = m / prm.rt;
+            const int i = m - hs * prm.rt;
+            const int prefix = i < tile.n_rows ? __ldg(prm.q_prefix + tile.q_row0 + i) : 0;
+            for (int j = 0; j < n_kv; ++j, ++s_cnt) {
+                const uint32_t buf = s_cnt % NB;
+                const bool tr = warp == 4 && s_cnt < 128;
+                if (tr) trace(4 * s_cnt + 0);
+                ptx::mbar_wait(&s_full[buf], (s_cnt / NB) & 1);
+                if (tr) trace(4 * s_cnt + 1);
+                ptx::tc_fence_after();
+                const uint32_t col = buf * BKV + cq * CW;
+                const int nvalid = prefix - (j * BKV + static_cast<int>(cq) * CW);  // >= CW: no masking
+                uint32_t pk[CW / 2];
+                if (__all_sync(0xffffffffu, nvalid <= 0)) {
+#pragma unroll
+                    for (int e = 0; e < CW / 2; ++e) pk[e] = 0u;
+                } else {
+                    float v[CW];
+#pragma unroll
+                    for (int k = 0; k < CW / 16; ++k)
+                        ptx::tmem_ld16(tmem + lane_addr + col + k * 16, *reinterpret_cast<float(*)[16]>(v + k * 16));
+                    ptx::tmem_ld_wait();
+                    if (__all_sync(0xffffffffu, nvalid >= CW)) {
+#pragma unroll
+                        for (int e = 0; e < CW; e += 2)
+                            pk[e / 2] = ((e / 2) * EMU) % 16 < EMU ? ptx::silu2_bf16_fma(v[e], v[e + 1])
+                                                                   : attn_detail::silu2_bf16(v[e], v[e + 1]);
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < CW; e += 2) {
+                            const uint32_t w = attn_detail::silu2_bf16(v[e], v[e + 1]);
+                            const uint32_t keep = (e + 1 < nvalid) ? 0xffffffffu : (e < nvalid ? 0x0000ffffu : 0u);
+                            pk[e / 2] = w & keep;
+                        }
+                    }
+                }
+                if (tr) trace(4 * s_cnt + 2);
+                if constexpr (CW / 2 == 16) ptx::tmem_st16(tmem + lane_addr + col, pk);
+                else ptx::tmem_st8(tmem + lane_addr + col, *reinterpret_cast<const uint32_t(*)[8]>(pk));
+                ptx::tmem_st_wait();
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&p_full[buf]);
+                if (tr) trace(4 * s_cnt + 3);
+            }
+        }
+    } else if (!SPA && warp >= 4 && warp < 4 + C::kSilu) {
         // ------------------------------------------------ SiLU warps
         constexpr int CPW = C::CPW;
         constexpr int CPW2 = BKV / 2;
@@ -374,7 +449,7 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
         for (int t = blockIdx.x; t < prm.n_tiles; t += gridDim.x, ++it) {
             const AttnTile tile = prm.tiles[t];
             const int n_kv = (tile.kmax + BKV - 1) / BKV;
-            const int ob = it % C::OB;
+            const int ob = it % kOB;
             const int hs = m / prm.rt;
             const int i = m - hs * prm.rt;
             const bool valid = i < tile.n_rows;
@@ -407,12 +482,12 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
                     wself = silu_precise(dot);
                 }
             }
-            ptx::mbar_wait(&o_full[ob], (it / C::OB) & 1);
+            ptx::mbar_wait(&o_full[ob], (it / kOB) & 1);
             ptx::tc_fence_after();
 #pragma unroll 1
             for (int c = 0; c < D; c += 16) {
                 float v[16];
-                ptx::tmem_ld16(tmem + lane_addr + C::O_COL + ob * D + c, v);
+                ptx::tmem_ld16(tmem + lane_addr + kOCol + ob * D + c, v);
                 ptx::tmem_ld_wait();
                 if (n_kv == 0) {
 #pragma unroll

@@ -917,6 +917,7 @@ struct AttnGeom {
     int hs, rt;
 };
 constexpr int kAttnEmuDefault = 0;
+constexpr bool kAttnSpaDefault = true;
 
 AttnGeom attn_geom(const mtfm_cuda_model& m) {
     const int r = m.H / m.G;
@@ -924,34 +925,34 @@ AttnGeom attn_geom(const mtfm_cuda_model& m) {
     return {1, 128};
 }
 
-template <int D, int EMU>
+template <int D, int EMU, bool SPA>
 void launch_attn_tc_de(const AttnParams& p, cudaStream_t st) {
     using C = attn_detail::Cfg<D>;
     static bool attr = false;
     if (!attr) {
-        ck(cudaFuncSetAttribute(attn_tc_kernel<D, EMU>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM),
+        ck(cudaFuncSetAttribute(attn_tc_kernel<D, EMU, SPA>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM),
            "attn smem attr");
         attr = true;
     }
     const int grid = std::min(p.n_tiles, kNumSMs);
-    launch_k(attn_tc_kernel<D, EMU>, dim3(grid), dim3(C::kThreads), C::SMEM, st, p);
+    launch_k(attn_tc_kernel<D, EMU, SPA>, dim3(grid), dim3(C::kThreads), C::SMEM, st, p);
     ck(cudaGetLastError(), "attn_tc launch");
 }
 
-// SiLU pairs (of 16) on the FMA pipes instead of the SFU (MTFM_ATTN_EMU overrides)
+// SiLU pairs (of 16) on the FMA pipes instead of the SFU (MTFM_ATTN_EMU), and
+// the P-aliasing-S pipeline (MTFM_ATTN_SPA); both override the defaults
 template <int D>
 void launch_attn_tc_d(const AttnParams& p, cudaStream_t st) {
     static const int emu = std::getenv("MTFM_ATTN_EMU") ? std::atoi(std::getenv("MTFM_ATTN_EMU")) : kAttnEmuDefault;
+    static const bool spa = std::getenv("MTFM_ATTN_SPA") ? std::atoi(std::getenv("MTFM_ATTN_SPA")) != 0 : kAttnSpaDefault;
     if constexpr (D == 32 || D == 64) {
         switch (emu) {
-            case 3: launch_attn_tc_de<D, 3>(p, st); return;
-            case 4: launch_attn_tc_de<D, 4>(p, st); return;
-            case 5: launch_attn_tc_de<D, 5>(p, st); return;
-            case 6: launch_attn_tc_de<D, 6>(p, st); return;
+            case 3: spa ? launch_attn_tc_de<D, 3, true>(p, st) : launch_attn_tc_de<D, 3, false>(p, st); return;
+            case 5: spa ? launch_attn_tc_de<D, 5, true>(p, st) : launch_attn_tc_de<D, 5, false>(p, st); return;
             default: break;
         }
     }
-    launch_attn_tc_de<D, 0>(p, st);
+    spa ? launch_attn_tc_de<D, 0, true>(p, st) : launch_attn_tc_de<D, 0, false>(p, st);
 }
 
 void run_attn_tc(const mtfm_cuda_model& m, AttnParams p, const __nv_bfloat16* q, long long n_q, long long q_cols,
