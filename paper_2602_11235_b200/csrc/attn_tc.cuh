@@ -314,19 +314,8 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
         const uint32_t cq = (warp - 4) >> 2;      // column quarter
         const uint32_t m = q * 32 + lane;         // MMA row == TMEM lane
         const uint32_t lane_addr = (q * 32u) << 16;
-        // The P store of key tile j is only waited for (and announced) after the
-        // S load of tile j+1 has been issued, so the two TMEM round trips overlap.
+        // (announcing P(j) only after issuing the S load of tile j+1 measured 3-5% slower)
         uint32_t s_cnt = 0;
-        int pend = -1;  // S/P buffer whose P store is still in flight
-        auto release_pending = [&]() {
-            if (pend >= 0) {
-                ptx::tmem_st_wait();
-                ptx::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&p_full[pend]);
-                pend = -1;
-            }
-        };
         for (int t = blockIdx.x; t < prm.n_tiles; t += gridDim.x) {
             const AttnTile tile = prm.tiles[t];
             const int n_kv = (tile.kmax + BKV - 1) / BKV;
@@ -344,7 +333,6 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
                 const int nvalid = prefix - (j * BKV + static_cast<int>(cq) * CW);  // >= CW: no masking
                 uint32_t pk[CW / 2];
                 if (__all_sync(0xffffffffu, nvalid <= 0)) {
-                    release_pending();
 #pragma unroll
                     for (int e = 0; e < CW / 2; ++e) pk[e] = 0u;
                 } else {
@@ -352,7 +340,6 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
 #pragma unroll
                     for (int k = 0; k < CW / 16; ++k)
                         ptx::tmem_ld16(tmem + lane_addr + col + k * 16, *reinterpret_cast<float(*)[16]>(v + k * 16));
-                    release_pending();
                     ptx::tmem_ld_wait();
                     if (__all_sync(0xffffffffu, nvalid >= CW)) {
 #pragma unroll
@@ -371,11 +358,13 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
                 if (tr) trace(4 * s_cnt + 2);
                 if constexpr (CW / 2 == 16) ptx::tmem_st16(tmem + lane_addr + col, pk);
                 else ptx::tmem_st8(tmem + lane_addr + col, *reinterpret_cast<const uint32_t(*)[8]>(pk));
-                pend = static_cast<int>(buf);
+                ptx::tmem_st_wait();
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&p_full[buf]);
                 if (tr) trace(4 * s_cnt + 3);
             }
         }
-        release_pending();
     } else if (!SPA && warp >= 4 && warp < 4 + C::kSilu) {
         // ------------------------------------------------ SiLU warps
         constexpr int CPW = C::CPW;
