@@ -56,6 +56,7 @@ struct GemmProblem {
     CUtensorMap tma_c;      // output, box {32, 32}: bf16 SW64 / f32 SW128 (use_tma_c)
     int use_tma_c;          // plain row-major output rows [0, M): bulk-tensor stores
     int use_tma_r;          // EPI_RESID_F32 with resid == out: residual blocks TMA-prefetched via tma_c
+    int use_scatter_c;      // bf16 output through row_map: staged like use_tma_c, then 128-byte row-segment stores
     int M, N, K;            // K padded to a multiple of 64
     int Kv;                 // true K (columns of a_src / gain rows)
     int tile_start;         // first global tile of this problem
@@ -621,7 +622,10 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
         int ntile = 0;
         // column unit per warp: 64 for bf16 bulk-stored outputs (128-byte rows), else 32
         auto unit_of = [&](const GemmProblem& pp) {
-            return ((pp.epi == EPI_SILU_BF16 || pp.epi == EPI_BIAS_BF16) && pp.use_tma_c && BN >= 64) ? 64 : 32;
+            return ((pp.epi == EPI_SILU_BF16 || pp.epi == EPI_BIAS_BF16) && (pp.use_tma_c || pp.use_scatter_c) &&
+                    BN >= 64)
+                       ? 64
+                       : 32;
         };
         int fk = 0;  // fine-trace index within the tile
         auto ftrace = [&]() {
@@ -662,6 +666,8 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
             const int step = unit / 32;  // in 32-column chunks
             int ci = 0;
             if (p.use_tma_r && ci < kChunks && nb * BN + ci * 32 < p.N) res_load(p, nstore & 1, nb * BN + ci * 32, row0);
+            // scattered bf16 rows: lane i holds the output row of tile row row0 + i
+            const int my_orow = (p.use_scatter_c && row0 + static_cast<int>(lane) < p.M) ? __ldg(p.row_map + row0 + lane) : -1;
             ptx::mbar_wait(&tfull_bar[acc], acc_phase);
             ptx::tc_fence_after();
             if (warp == 0 && ntile < 64) trace(192 + ntile);
@@ -671,7 +677,7 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                 const int c = ci * 32;
                 const int n0 = nb * BN + c;
                 if (args.debug & 32) continue;  // timing experiment: epilogue does nothing but the handshakes
-                if (bf16_out && p.use_tma_c && unit == 64) {
+                if (bf16_out && (p.use_tma_c || p.use_scatter_c) && unit == 64) {
                     // ---- fast path: 64 columns -> bf16 (SiLU) -> one 32 x 128 B SW128 box
                     if (n0 >= p.N) continue;  // warp-uniform (TMEM reads below are all-or-nothing)
                     float* stg = stg_base + (stg_single ? 0 : (nstore & 1) * 32 * 32);
@@ -705,6 +711,22 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                         *reinterpret_cast<uint4*>(sb + ((k ^ (lane & 7)) << 4)) =
                             make_uint4(w[k >> 2][4 * (k & 3)], w[k >> 2][4 * (k & 3) + 1], w[k >> 2][4 * (k & 3) + 2],
                                        w[k >> 2][4 * (k & 3) + 3]);
+                    if (p.use_scatter_c) {
+                        // row-mapped rows: 8 lanes per 128-byte row segment, 4 rows per pass
+                        __syncwarp();
+                        const uint8_t* s0 = reinterpret_cast<const uint8_t*>(stg);
+#pragma unroll
+                        for (int it = 0; it < 8; ++it) {
+                            const int r = it * 4 + sub;
+                            const uint4 val = *reinterpret_cast<const uint4*>(s0 + r * 128 + ((ch ^ (r & 7)) << 4));
+                            const int orow = __shfl_sync(0xffffffffu, my_orow, r);
+                            if (orow >= 0)
+                                *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) +
+                                                          static_cast<long long>(orow) * p.ldo + n0 + ch * 8) = val;
+                        }
+                        ++nstore;
+                        continue;
+                    }
                     ptx::fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0 && !(args.debug & 1)) {

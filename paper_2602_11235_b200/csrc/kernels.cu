@@ -572,15 +572,17 @@ __global__ void __launch_bounds__(256) gln_multi_kernel(const float* __restrict_
     for (long long r0 = 2 * (blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5)); r0 < n_rows;
          r0 += 2 * warps) {
         const bool two = r0 + 1 < n_rows;
+        const long long x0 = c.in_rows ? static_cast<long long>(__ldg(c.in_rows + r0)) : r0;
+        const long long x1 = two ? (c.in_rows ? static_cast<long long>(__ldg(c.in_rows + r0 + 1)) : r0 + 1) : x0;
         float4 v[NS], w[NS];
 #pragma unroll
         for (int k = 0; k < NS; ++k) {
             const int col = 128 * k + 4 * lane;
-            v[k] = col < d ? __ldcs(reinterpret_cast<const float4*>(x + r0 * ldx + col)) : make_float4(0.f, 0.f, 0.f, 0.f);
-            w[k] = (two && col < d) ? __ldcs(reinterpret_cast<const float4*>(x + (r0 + 1) * ldx + col))
+            v[k] = col < d ? __ldcs(reinterpret_cast<const float4*>(x + x0 * ldx + col)) : make_float4(0.f, 0.f, 0.f, 0.f);
+            w[k] = (two && col < d) ? __ldcs(reinterpret_cast<const float4*>(x + x1 * ldx + col))
                                     : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        int g0 = row_src[r0], g1 = two ? row_src[r0 + 1] : g0;
+        int g0 = row_src[x0], g1 = two ? row_src[x1] : g0;
         normalize_slices<NS, true>(v, d, lane, eps);
         normalize_slices<NS, true>(w, d, lane, eps);
         g0 = g0 < 0 ? 0 : g0;

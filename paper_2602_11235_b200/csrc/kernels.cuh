@@ -101,6 +101,7 @@ struct GlnCopies {
     const float* bias[kMaxGlnCopies];
     void* out[kMaxGlnCopies];
     int n;
+    const int* in_rows;  // optional: output row j normalises x row in_rows[j] (source-ordered copies)
 };
 void launch_gln_multi_bf16(const float* x, long long ldx, long long n_rows, int d, const int* row_src,
                            const GlnCopies& c, float eps, long long ldo, cudaStream_t st);

@@ -252,6 +252,10 @@ struct LayerW {
     DevBuf g1g, g1b, g2g, g2b;        // [n_groups][d] / [n_groups][hd]
     // bf16 K-major ([out][in]) for the tensor-core path
     DevBuf t1, tkv, tf2;
+    // GLN1 affine of each context source folded into the context-row projection
+    // (bf16 [n_ctx][N][d] K-major, fp32 [n_ctx][N]): x~W + b = xhat (gain (.) W) + (bias W + b)
+    // target: fkv (N = 2gd), full: f1 (N = 2hd + 2gd)
+    DevBuf tfold, bfold;
 };
 
 struct SourceW {
@@ -274,6 +278,7 @@ struct mtfm_cuda_model {
     std::vector<mtfm::ParamSpec> params;
     std::map<std::string, size_t> by_name;
     bool finalized = false;
+    int n_ctx_src = 0;  // leading sources of kind hist/rt (context rows) when they precede every scenario source
     cudaStream_t stream = nullptr;       // kernels
     cudaStream_t copy_stream = nullptr;  // batch uploads (overlap the previous batch's kernels)
     cudaStream_t d2h_stream = nullptr;   // record read-back (does not queue behind the next batch)
@@ -431,6 +436,8 @@ std::vector<uint16_t> to_kmajor_bf16(const std::vector<float>& w, long long rows
 
 void finalize(mtfm_cuda_model& m) {
     if (m.finalized) return;
+    // bias tiles are keyed by device pointer: rebuilt weights may reuse freed addresses
+    m.bias_tiles.tiles.clear();
     for (const auto& p : m.params)
         if (!p.set) fail(MTFM_CONFIG_ERROR, "parameter not set: " + p.name);
     cudaStream_t st = m.stream;
@@ -505,6 +512,30 @@ void finalize(mtfm_cuda_model& m) {
             }
             upload(L->g1g, g1g, st);
             upload(L->g1b, g1b, st);
+            if (m.n_ctx_src > 0) {
+                const auto& wf = P(m, base + (L->target ? "/fkv_w" : "/f1_w"));
+                const auto& bf = P(m, base + (L->target ? "/fkv_b" : "/f1_b"));
+                const int N = L->target ? 2 * gd : 2 * hd + 2 * gd;
+                std::vector<uint16_t> tf(static_cast<size_t>(m.n_ctx_src) * N * d);
+                std::vector<float> bb(static_cast<size_t>(m.n_ctx_src) * N);
+                std::vector<double> acc(N);
+                for (int g = 0; g < m.n_ctx_src; ++g) {
+                    const float* ga = g1g.data() + static_cast<size_t>(g) * d;
+                    const float* be = g1b.data() + static_cast<size_t>(g) * d;
+                    for (int n = 0; n < N; ++n) acc[n] = bf[n];
+                    for (int k = 0; k < d; ++k) {
+                        const float* wr = wf.data() + static_cast<size_t>(k) * N;
+                        uint16_t* tc = tf.data() + static_cast<size_t>(g) * N * d + k;
+                        for (int n = 0; n < N; ++n) {
+                            acc[n] += static_cast<double>(be[k]) * wr[n];
+                            tc[static_cast<size_t>(n) * d] = f2bf(ga[k] * wr[n]);
+                        }
+                    }
+                    for (int n = 0; n < N; ++n) bb[static_cast<size_t>(g) * N + n] = static_cast<float>(acc[n]);
+                }
+                upload(L->tfold, tf, st);
+                upload(L->bfold, bb, st);
+            }
             upload(L->g2g, g2g, st);
             upload(L->g2b, g2b, st);
             m.layers.push_back(std::move(L));
@@ -704,18 +735,36 @@ void run_gemm_tc(std::vector<TcProblem> ps, cudaStream_t st, long long& launches
         int bn = bn_res;
         int grid = 0;
         if (bn) {
-            // CTAs per problem proportional to its work, a multiple of its n-slices so
-            // the CTAs sharing an m-block (one per slice) run in lockstep (A read once)
-            double W = 0;
-            for (size_t i = i0; i < i1; ++i) W += static_cast<double>(cdiv(ps[i].M, 128) * cdiv(ps[i].N, bn));
+            // CTAs per problem: a multiple of its n-slices so the CTAs sharing an m-block
+            // (one per slice) run in lockstep (A read once).
+            // CTA rows per problem (a row = one CTA per n-slice, lockstep on an m-block):
+            // start at one row each, then repeatedly give a row to the problem whose CTAs
+            // walk the most m-blocks while the SMs last (min-makespan greedy; a proportional
+            // share rounded down leaves small problems' CTAs with ~2x the m-blocks)
+            std::vector<int> cpsv(i1 - i0, 1);
+            int used = 0;
+            for (size_t i = i0; i < i1; ++i) used += static_cast<int>(cdiv(ps[i].N, bn));
+            for (;;) {
+                int best = -1;
+                long long best_load = 0;
+                for (size_t i = i0; i < i1; ++i) {
+                    const long long load = cdiv(cdiv(ps[i].M, 128), cpsv[i - i0]);
+                    if (load > best_load) {
+                        best_load = load;
+                        best = static_cast<int>(i - i0);
+                    }
+                }
+                const int ns = best < 0 ? 0 : static_cast<int>(cdiv(ps[i0 + best].N, bn));
+                if (best < 0 || best_load <= 1 || used + ns > kNumSMs) break;
+                ++cpsv[best];
+                used += ns;
+            }
             int n = 0;
             bool ok = true;
             for (size_t i = i0; i < i1 && ok; ++i) {
                 const int ns = static_cast<int>(cdiv(ps[i].N, bn));
                 const int mb = static_cast<int>(cdiv(ps[i].M, 128));
-                const double share = kNumSMs * static_cast<double>(mb) * ns / W;
-                int cps = std::max(1, static_cast<int>(share / ns));
-                cps = std::min(cps, mb);
+                const int cps = cpsv[i - i0];
                 for (int j = 0; j < cps && ok; ++j)
                     for (int nb = 0; nb < ns; ++nb) {
                         if (n >= kNumSMs) {
@@ -792,6 +841,8 @@ void run_gemm_tc(std::vector<TcProblem> ps, cudaStream_t st, long long& launches
                                 std::getenv("MTFM_NO_TMA_STORE") == nullptr;
             p.use_tma_c = tma_ok && (s.epi != EPI_RESID_F32 || s.resid == s.out);
             p.use_tma_r = p.use_tma_c && s.epi == EPI_RESID_F32;
+            p.use_scatter_c = bf16_out && s.row_map && bn >= 64 && s.N % 64 == 0 && (s.ldo * 2) % 16 == 0 &&
+                              (reinterpret_cast<uintptr_t>(s.out) % 16) == 0 && std::getenv("MTFM_NO_SCATTER") == nullptr;
             if (p.use_tma_c) {
                 // 32 rows x 128 B boxes: 64 bf16 columns or 32 fp32 columns (SW128)
                 const char* base = static_cast<const char*>(s.out) + s.row_offset * s.ldo * eb;
@@ -815,7 +866,8 @@ void run_gemm_tc(std::vector<TcProblem> ps, cudaStream_t st, long long& launches
         bool all_fast = true;
         for (int i = 0; i < a.n_problems; ++i) {
             const GemmProblem& p = a.p[i];
-            all_fast = all_fast && p.use_tma_c && bn >= 64 && (p.epi == EPI_SILU_BF16 || p.epi == EPI_BIAS_BF16);
+            all_fast = all_fast && (p.use_tma_c || p.use_scatter_c) && bn >= 64 &&
+                       (p.epi == EPI_SILU_BF16 || p.epi == EPI_BIAS_BF16);
         }
         static const bool stg_double = std::getenv("MTFM_GEMM_STG2") != nullptr;
         const int stg_warp = (all_fast && !stg_double) ? 4096 : 8192;
@@ -1526,6 +1578,7 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
         // full layer whose context-row GLN1 was produced by the preceding target run
         // (same X context rows) into XNF rows [0, NE): only its T rows remain
         size_t full_ctx_from_run = static_cast<size_t>(-1);
+        bool full_ctx_folded = false;  // ... as source-ordered xhat rows XN[0, NE) with folded f1 weights
         T* XNF = XN + (static_cast<long long>(std::max(1, m.cfg.target_layers)) * NE + NT) * d;
         int tl = 0;                     // index of the current target layer within its run
         for (size_t li = 0; li < m.layers.size(); ++li) {
@@ -1565,6 +1618,28 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                     // U and Q|K|V as two contiguous matrices (one grouped launch): the gate
                     // then streams U rows and the attention Q|K|V rows without gaps
                     StageScope sc(m, "proj_full", 2.0 * Rd * d * pw, Rd * d * el + Rd * pw * el);
+                    if (full_ctx_from_run == li && full_ctx_folded) {
+                        // context rows: per source, xhat rows x folded f1, scattered to X-row order;
+                        // T rows: their GLN1 rows XNF[NE, R) x f1, at row offset NE
+                        std::vector<TcProblem> pp;
+                        for (int s = 0; s < m.n_ctx_src; ++s) {
+                            const __nv_bfloat16* wf = Lw->tfold.as<__nv_bfloat16>() + static_cast<long long>(s) * pw * d;
+                            const float* bfo = Lw->bfold.as<float>() + static_cast<long long>(s) * pw;
+                            const int Ms = static_cast<int>(B.src_cnt[s]);
+                            const int* rmap = rm.src_rows + B.src_base[s];
+                            pp.push_back({XN + B.src_base[s] * d, d, wf, d, Ms, hd, d, EPI_SILU_BF16, bfo, Pm, hd, rmap, 0,
+                                          nullptr});
+                            pp.push_back({XN + B.src_base[s] * d, d, wf + static_cast<long long>(hd) * d, d, Ms,
+                                          hd + 2 * gd, d, EPI_SILU_BF16, bfo + hd, Pm + R * hd, hd + 2 * gd, rmap, 0,
+                                          nullptr});
+                        }
+                        pp.push_back({XNF + NE * d, d, Lw->t1.as<__nv_bfloat16>(), d, static_cast<int>(NT), hd, d,
+                                      EPI_SILU_BF16, Lw->b1.as<float>(), Pm, hd, nullptr, NE, nullptr});
+                        pp.push_back({XNF + NE * d, d, Lw->t1.as<__nv_bfloat16>() + static_cast<long long>(hd) * d, d,
+                                      static_cast<int>(NT), hd + 2 * gd, d, EPI_SILU_BF16, Lw->b1.as<float>() + hd,
+                                      Pm + R * hd, hd + 2 * gd, nullptr, NE, nullptr});
+                        run_gemm_tc(pp, st, L, BT);
+                    } else
                     run_gemm_tc({{XNL, d, Lw->t1.as<__nv_bfloat16>(), d, static_cast<int>(R), hd, d, EPI_SILU_BF16,
                                   Lw->b1.as<float>(), Pm, hd, nullptr, 0, nullptr},
                                  {XNL, d, Lw->t1.as<__nv_bfloat16>() + static_cast<long long>(hd) * d, d,
@@ -1648,11 +1723,48 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                         while (lj < m.layers.size() && m.layers[lj]->target) ++lj;
                         const int kt = static_cast<int>(lj - li);
                         // the full layer right after the run sees the same context rows
-                        const bool with_full = lj < m.layers.size() && !(m.fuse & 1) && kt + 1 <= kMaxGlnCopies;
                         // MTFM_XHAT=1: one normalised copy (xhat) + per-layer affine inside the
                         // K|V GEMM's A producer (A_AFFINE_TMA) instead of one copy per layer
                         static const bool use_xhat = std::getenv("MTFM_XHAT") && std::atoi(std::getenv("MTFM_XHAT")) != 0;
-                        const int ncopy = (use_xhat ? 1 : kt) + (with_full ? 1 : 0);
+                        // default: one normalised copy of the context rows in source order (xhat,
+                        // no affine); every context source's GLN1 affine is folded into its own
+                        // copy of the K|V (and the following full layer's f1) weights, and the
+                        // GEMM outputs are scattered back to X-row order
+                        long long ctx_rows = 0;
+                        for (int s = 0; s < m.n_ctx_src; ++s) ctx_rows += B.src_cnt[s];
+                        const bool fold = m.n_ctx_src > 0 && !use_xhat && ctx_rows == NE;
+                        const bool with_full =
+                            lj < m.layers.size() && !(m.fuse & 1) && (fold || kt + 1 <= kMaxGlnCopies);
+                        if (fold) {
+                            {
+                                GlnCopies gc{};
+                                gc.n = 1;
+                                gc.out[0] = XN;
+                                gc.in_rows = rm.src_rows;
+                                StageScope sc(m, "gln1", 0, NE * d * (4.0 + el));
+                                launch_gln_multi_bf16(X, d, NE, d, rm.src, gc, eps, d, st);
+                                ++L;
+                            }
+                            if (with_full) {
+                                full_ctx_from_run = lj;
+                                full_ctx_folded = true;
+                            }
+                            std::vector<TcProblem> kvp;
+                            for (int c = 0; c < kt; ++c) {
+                                const auto& Lc = m.layers[li + c];
+                                for (int s = 0; s < m.n_ctx_src; ++s)
+                                    kvp.push_back({XN + B.src_base[s] * d, d,
+                                                   Lc->tfold.as<__nv_bfloat16>() + static_cast<long long>(s) * 2 * gd * d, d,
+                                                   static_cast<int>(B.src_cnt[s]), 2 * gd, d, EPI_SILU_BF16,
+                                                   Lc->bfold.as<float>() + s * 2 * gd,
+                                                   KV + static_cast<long long>(c) * R * 2 * gd, 2 * gd,
+                                                   rm.src_rows + B.src_base[s], 0, nullptr});
+                            }
+                            StageScope sc(m, "proj_ctx_kv", 2.0 * kt * NE * d * 2 * gd, NE * d * el + kt * NE * 2.0 * gd * el);
+                            run_gemm_tc(kvp, st, L, BT);
+                            tl = 0;
+                        }
+                        const int ncopy = fold ? 0 : (use_xhat ? 1 : kt) + (with_full ? 1 : 0);
                         for (int c0 = 0; c0 < ncopy; c0 += kMaxGlnCopies) {
                             GlnCopies gc{};
                             gc.n = std::min(ncopy - c0, kMaxGlnCopies);
@@ -1668,9 +1780,9 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                             launch_gln_multi_bf16(X, d, NE, d, rm.src, gc, eps, d, st);
                             ++L;
                         }
-                        if (with_full) full_ctx_from_run = lj;
+                        if (with_full && !fold) full_ctx_from_run = lj;
                         std::vector<TcProblem> kvp;
-                        for (int c = 0; c < kt; ++c) {
+                        for (int c = 0; c < kt && !fold; ++c) {
                             const auto& Lc = m.layers[li + c];
                             T* a_in = XN + static_cast<long long>(use_xhat ? 0 : c) * NE * d;
                             kvp.push_back({a_in, d, Lc->tkv.as<__nv_bfloat16>(), d,
@@ -1686,10 +1798,12 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                                 tp.gbias = Lc->g1b.as<float>();
                             }
                         }
-                        StageScope sc(m, "proj_ctx_kv", 2.0 * kt * NE * d * 2 * gd,
-                                      kt * NE * (d + 2.0 * gd) * el);
-                        run_gemm_tc(kvp, st, L, BT);
-                        tl = 0;
+                        if (!fold) {
+                            StageScope sc(m, "proj_ctx_kv", 2.0 * kt * NE * d * 2 * gd,
+                                          kt * NE * (d + 2.0 * gd) * el);
+                            run_gemm_tc(kvp, st, L, BT);
+                            tl = 0;
+                        }
                     }
                     KVl = KV + static_cast<long long>(tl) * R * 2 * gd;
                     T* XNT = XN + static_cast<long long>(m.cfg.target_layers) * NE * d;
@@ -2127,6 +2241,9 @@ mtfm_status mtfm_cuda_create(int device, const mtfm_model_desc* md, const mtfm_s
         add_seq(1, sd->n_rt, sd->rt_ids, sd->rt_nslots, sd->rt_vocabs);
         m->n_hist = sd->n_hist;
         m->n_rt = sd->n_rt;
+        // GLN1 folded into the context-row projections (bf16 path; MTFM_FOLD=0 keeps per-layer copies)
+        static const bool fold = std::getenv("MTFM_FOLD") == nullptr || std::atoi(std::getenv("MTFM_FOLD")) != 0;
+        if (fold && precision == MTFM_PRECISION_BF16) m->n_ctx_src = sd->n_hist + sd->n_rt;
         int p = 0, tp = 0;
         for (int i = 0; i < sd->n_scen; ++i) {
             SourceInfo s{};

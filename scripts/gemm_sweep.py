@@ -11,7 +11,10 @@ from paper_2602_11235_b200 import abi
 
 L = abi.lib()
 shapes = [("proj_full", 557056, 256, 640, 0), ("tok_mlp2", 557056, 512, 256, 1), ("fkv", 557056, 256, 128, 0),
-          ("f2_resid", 557056, 256, 256, 2), ("tok_mlp1", 557056, 64, 512, 0)]
+          ("f2_resid", 557056, 256, 256, 2), ("tok_mlp1", 557056, 64, 512, 0),
+          # MTFM-large shapes (M reduced to 2^20 rows)
+          ("f2_L", 1048576, 1024, 1024, 2), ("tok2_L", 1048576, 2048, 1024, 1), ("projU_L", 1048576, 1024, 1024, 0),
+          ("kv_L", 1048576, 1024, 512, 0)]
 only = os.environ.get("SHAPE")
 if only:
     shapes = [x for x in shapes if x[0] == only]
@@ -53,4 +56,5 @@ for name, M, K, N, epi in shapes:
         ref = torch.nn.functional.silu(ref)
     got = out[:256].float()
     err = "" if epi == 2 else " maxerr %.3g" % (got - ref).abs().max().item()
-    print(f"{tag:24s} {name:10s} {ms*1000:8.1f} us {byts/ms/1e6:7.0f} GB/s{err}", flush=True)
+    tf = 2.0 * M * N * K / (ms / 1e3) / 1e12
+    print(f"{tag:24s} {name:10s} {ms*1000:8.1f} us {byts/ms/1e6:7.0f} GB/s {tf:6.0f} TFLOP/s{err}", flush=True)
