@@ -57,6 +57,12 @@ struct GemmProblem {
     int use_tma_c;          // plain row-major output rows [0, M): bulk-tensor stores
     int use_tma_r;          // EPI_RESID_F32 with resid == out: residual blocks TMA-prefetched via tma_c
     int use_scatter_c;      // bf16 output through row_map: staged like use_tma_c, then 128-byte row-segment stores
+    // use_scatter_c only: columns [seg_n0[i], next) go to seg_out[i] (ld seg_ldo[i]) at column - seg_n0[i];
+    // segment 0 is (0, out, ldo). Lets problems sharing A rows share one launch slot (A read once).
+    int n_seg;
+    int seg_n0[4];
+    void* seg_out[4];
+    long long seg_ldo[4];
     int M, N, K;            // K padded to a multiple of 64
     int Kv;                 // true K (columns of a_src / gain rows)
     int tile_start;         // first global tile of this problem
@@ -715,14 +721,24 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                         // row-mapped rows: 8 lanes per 128-byte row segment, 4 rows per pass
                         __syncwarp();
                         const uint8_t* s0 = reinterpret_cast<const uint8_t*>(stg);
+                        void* so = p.out;
+                        long long sld = p.ldo;
+                        int sn = n0;
+                        for (int si = p.n_seg - 1; si >= 1; --si)
+                            if (n0 >= p.seg_n0[si]) {
+                                so = p.seg_out[si];
+                                sld = p.seg_ldo[si];
+                                sn = n0 - p.seg_n0[si];
+                                break;
+                            }
 #pragma unroll
                         for (int it = 0; it < 8; ++it) {
                             const int r = it * 4 + sub;
                             const uint4 val = *reinterpret_cast<const uint4*>(s0 + r * 128 + ((ch ^ (r & 7)) << 4));
                             const int orow = __shfl_sync(0xffffffffu, my_orow, r);
                             if (orow >= 0)
-                                *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) +
-                                                          static_cast<long long>(orow) * p.ldo + n0 + ch * 8) = val;
+                                *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(so) +
+                                                          static_cast<long long>(orow) * sld + sn + ch * 8) = val;
                         }
                         ++nstore;
                         continue;

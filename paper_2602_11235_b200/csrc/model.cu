@@ -256,6 +256,9 @@ struct LayerW {
     // (bf16 [n_ctx][N][d] K-major, fp32 [n_ctx][N]): x~W + b = xhat (gain (.) W) + (bias W + b)
     // target: fkv (N = 2gd), full: f1 (N = 2hd + 2gd)
     DevBuf tfold, bfold;
+    // first target layer of a run only: the folded K|V weights of the run's layers stacked per
+    // context source ([n_ctx][kt * 2gd][d], [n_ctx][kt * 2gd]) for one column-segmented GEMM
+    DevBuf kv_run, kvb_run;
 };
 
 struct SourceW {
@@ -540,6 +543,29 @@ void finalize(mtfm_cuda_model& m) {
             upload(L->g2b, g2b, st);
             m.layers.push_back(std::move(L));
         }
+    // stacked folded K|V weights per target run (column-segmented context K|V GEMM)
+    for (size_t li = 0; li < m.layers.size() && m.n_ctx_src > 0; ++li) {
+        if (!m.layers[li]->target || (li > 0 && m.layers[li - 1]->target)) continue;
+        size_t lj = li;
+        while (lj < m.layers.size() && m.layers[lj]->target) ++lj;
+        const int kt = static_cast<int>(lj - li);
+        if (kt > 4) continue;
+        auto& Lr = *m.layers[li];
+        const size_t wn = static_cast<size_t>(2 * gd) * d;
+        Lr.kv_run.alloc(static_cast<size_t>(m.n_ctx_src) * kt * wn * 2);
+        Lr.kvb_run.alloc(static_cast<size_t>(m.n_ctx_src) * kt * 2 * gd * 4);
+        for (int s = 0; s < m.n_ctx_src; ++s)
+            for (int c = 0; c < kt; ++c) {
+                const auto& Lc = *m.layers[li + c];
+                ck(cudaMemcpyAsync(static_cast<char*>(Lr.kv_run.p) + (static_cast<size_t>(s) * kt + c) * wn * 2,
+                                   static_cast<const char*>(Lc.tfold.p) + s * wn * 2, wn * 2, cudaMemcpyDeviceToDevice, st),
+                   "kv_run");
+                ck(cudaMemcpyAsync(static_cast<char*>(Lr.kvb_run.p) + (static_cast<size_t>(s) * kt + c) * 2 * gd * 4,
+                                   static_cast<const char*>(Lc.bfold.p) + static_cast<size_t>(s) * 2 * gd * 4, 2 * gd * 4,
+                                   cudaMemcpyDeviceToDevice, st),
+                   "kvb_run");
+            }
+    }
     // heads: [d][E*de | n_tasks*E]
     const int E = m.cfg.experts, dx = m.cfg.d_expert;
     m.head_n = E * dx + m.n_tasks_total * E;
@@ -660,6 +686,11 @@ struct TcProblem {
     const float* gbias = nullptr;
     const __nv_bfloat16* u_src = nullptr;
     long long ldu = 0;
+    // column segments (row-mapped bf16 outputs only): GemmProblem::seg_*
+    int n_seg = 0;
+    int seg_n0[4] = {0, 0, 0, 0};
+    void* seg_out[4] = {nullptr, nullptr, nullptr, nullptr};
+    long long seg_ldo[4] = {0, 0, 0, 0};
 };
 
 int pick_bn(const std::vector<TcProblem>& ps) {
@@ -843,6 +874,20 @@ void run_gemm_tc(std::vector<TcProblem> ps, cudaStream_t st, long long& launches
             p.use_tma_r = p.use_tma_c && s.epi == EPI_RESID_F32;
             p.use_scatter_c = bf16_out && s.row_map && bn >= 64 && s.N % 64 == 0 && (s.ldo * 2) % 16 == 0 &&
                               (reinterpret_cast<uintptr_t>(s.out) % 16) == 0 && std::getenv("MTFM_NO_SCATTER") == nullptr;
+            p.n_seg = 1;
+            if (s.n_seg > 1) {
+                bool seg_ok = p.use_scatter_c && s.n_seg <= 4;
+                for (int k = 1; k < s.n_seg && seg_ok; ++k)
+                    seg_ok = s.seg_n0[k] % 64 == 0 && s.seg_n0[k] > s.seg_n0[k - 1] && (s.seg_ldo[k] * 2) % 16 == 0 &&
+                             (reinterpret_cast<uintptr_t>(s.seg_out[k]) % 16) == 0;
+                if (!seg_ok) fail(MTFM_CONTRACT_ERROR, "column-segmented GEMM output needs the row-mapped bf16 epilogue");
+                p.n_seg = s.n_seg;
+                for (int k = 0; k < s.n_seg; ++k) {
+                    p.seg_n0[k] = s.seg_n0[k];
+                    p.seg_out[k] = s.seg_out[k];
+                    p.seg_ldo[k] = s.seg_ldo[k];
+                }
+            }
             if (p.use_tma_c) {
                 // 32 rows x 128 B boxes: 64 bf16 columns or 32 fp32 columns (SW128)
                 const char* base = static_cast<const char*>(s.out) + s.row_offset * s.ldo * eb;
@@ -1622,11 +1667,26 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                         // context rows: per source, xhat rows x folded f1, scattered to X-row order;
                         // T rows: their GLN1 rows XNF[NE, R) x f1, at row offset NE
                         std::vector<TcProblem> pp;
+                        const bool seg = hd % 64 == 0 && (hd + 2 * gd) % 64 == 0 && std::getenv("MTFM_SEG") != nullptr;
                         for (int s = 0; s < m.n_ctx_src; ++s) {
                             const __nv_bfloat16* wf = Lw->tfold.as<__nv_bfloat16>() + static_cast<long long>(s) * pw * d;
                             const float* bfo = Lw->bfold.as<float>() + static_cast<long long>(s) * pw;
                             const int Ms = static_cast<int>(B.src_cnt[s]);
                             const int* rmap = rm.src_rows + B.src_base[s];
+                            if (seg) {
+                                // U | Q|K|V as two column segments of one problem (A read once)
+                                TcProblem tp{XN + B.src_base[s] * d, d, wf, d, Ms, pw, d, EPI_SILU_BF16, bfo, Pm, hd,
+                                             rmap, 0, nullptr};
+                                tp.n_seg = 2;
+                                tp.seg_n0[0] = 0;
+                                tp.seg_out[0] = Pm;
+                                tp.seg_ldo[0] = hd;
+                                tp.seg_n0[1] = hd;
+                                tp.seg_out[1] = Pm + R * hd;
+                                tp.seg_ldo[1] = hd + 2 * gd;
+                                pp.push_back(tp);
+                                continue;
+                            }
                             pp.push_back({XN + B.src_base[s] * d, d, wf, d, Ms, hd, d, EPI_SILU_BF16, bfo, Pm, hd, rmap, 0,
                                           nullptr});
                             pp.push_back({XN + B.src_base[s] * d, d, wf + static_cast<long long>(hd) * d, d, Ms,
@@ -1749,16 +1809,37 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                                 full_ctx_from_run = lj;
                                 full_ctx_folded = true;
                             }
+                            // per context source: the run's layers' K|V as column segments of one
+                            // problem (weights of layers li.. of the run stacked in Lw->tkv_run)
                             std::vector<TcProblem> kvp;
-                            for (int c = 0; c < kt; ++c) {
-                                const auto& Lc = m.layers[li + c];
-                                for (int s = 0; s < m.n_ctx_src; ++s)
+                            const bool seg = kt <= 4 && (2 * gd) % 64 == 0 && m.layers[li]->kv_run.p != nullptr &&
+                                             std::getenv("MTFM_SEG") != nullptr;
+                            for (int s = 0; s < m.n_ctx_src; ++s) {
+                                if (seg) {
+                                    const auto& Lr = m.layers[li];
+                                    TcProblem tp{XN + B.src_base[s] * d, d,
+                                                 Lr->kv_run.as<__nv_bfloat16>() + static_cast<long long>(s) * kt * 2 * gd * d,
+                                                 d, static_cast<int>(B.src_cnt[s]), kt * 2 * gd, d, EPI_SILU_BF16,
+                                                 Lr->kvb_run.as<float>() + static_cast<long long>(s) * kt * 2 * gd, KV, 2 * gd,
+                                                 rm.src_rows + B.src_base[s], 0, nullptr};
+                                    tp.n_seg = kt;
+                                    for (int c = 0; c < kt; ++c) {
+                                        tp.seg_n0[c] = c * 2 * gd;
+                                        tp.seg_out[c] = KV + static_cast<long long>(c) * R * 2 * gd;
+                                        tp.seg_ldo[c] = 2 * gd;
+                                    }
+                                    kvp.push_back(tp);
+                                    continue;
+                                }
+                                for (int c = 0; c < kt; ++c) {
+                                    const auto& Lc = m.layers[li + c];
                                     kvp.push_back({XN + B.src_base[s] * d, d,
                                                    Lc->tfold.as<__nv_bfloat16>() + static_cast<long long>(s) * 2 * gd * d, d,
                                                    static_cast<int>(B.src_cnt[s]), 2 * gd, d, EPI_SILU_BF16,
                                                    Lc->bfold.as<float>() + s * 2 * gd,
                                                    KV + static_cast<long long>(c) * R * 2 * gd, 2 * gd,
                                                    rm.src_rows + B.src_base[s], 0, nullptr});
+                                }
                             }
                             StageScope sc(m, "proj_ctx_kv", 2.0 * kt * NE * d * 2 * gd, NE * d * el + kt * NE * 2.0 * gd * el);
                             run_gemm_tc(kvp, st, L, BT);
