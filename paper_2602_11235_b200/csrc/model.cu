@@ -444,7 +444,7 @@ void finalize(mtfm_cuda_model& m) {
     for (const auto& p : m.params)
         if (!p.set) fail(MTFM_CONFIG_ERROR, "parameter not set: " + p.name);
     cudaStream_t st = m.stream;
-    const int d = m.d, hd = m.hd, gd = m.gd, de = m.cfg.d_emb;
+    const int d = m.d, hd = m.hd, gd = m.gd;
     // embeddings: one flat table buffer
     std::vector<float> emb;
     for (size_t s = 0; s < m.slots.size(); ++s) {
