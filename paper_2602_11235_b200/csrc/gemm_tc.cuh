@@ -53,6 +53,7 @@ struct GemmProblem {
     CUtensorMap tma_a;      // box {64, 128} (2D) or {64, 128, stage_kb} (3D k-block view), SW128 (A_TMA, A_GATE_TMA)
     CUtensorMap tma_u;      // A_GATE_TMA: U rows, box {64, 128}, SW128
     CUtensorMap tma_b;      // box {64, BN} or {64, BN, stage_kb}, SW128
+    CUtensorMap tma_b_half; // cluster2: box {64, BN/2}, SW128 (each CTA of a pair loads and multicasts one half)
     CUtensorMap tma_c;      // output, box {32, 32}: bf16 SW64 / f32 SW128 (use_tma_c)
     int use_tma_c;          // plain row-major output rows [0, M): bulk-tensor stores
     int use_tma_r;          // EPI_RESID_F32 with resid == out: residual blocks TMA-prefetched via tma_c
@@ -107,6 +108,8 @@ struct GemmArgs {
     int n_epi;        // epilogue warps: 8, or 12 when A comes from TMA (warps 12..15 free)
     int stg_warp;     // epilogue staging bytes per warp: 8 KB (2 fp32 blocks), 4 KB when every problem is a bf16 bulk store
     int bias_bytes;   // BN x 32 B bias tile: after the resident B slice (b_res) or at the end of every stage
+    int cluster2;     // streaming with CTA pairs (cluster of 2): the pair takes m-blocks 2j, 2j+1 of one
+                      // (problem, n-block) and each CTA multicasts half of every B k-block to both
     unsigned long long* trace;  // timing experiments only: CTA 0 clock64 stamps (MTFM_GEMM_TRACE)
     int debug;        // timing experiments only: 1 no stores, 2 no SiLU, 8 no A loads, 16 no MMAs, 32 epilogue handshakes only
     GemmProblem p[kMaxProblems];
@@ -136,13 +139,14 @@ struct Cfg {
 // B-resident: the CTA's (problem, n-block, m-blocks) held in registers;
 // streaming: global tile t -> (problem, m, n) through the SMEM tile_start table.
 struct TileSeq {
-    int t, i;
+    int t, i, tstep, pair, rank;
     int b_res, pi0, nb0, m0, mstep, mcount, n_tiles, n_problems;
     const int* tile_start;  // SMEM: first global tile of each problem
     const int* tiles_n;     // SMEM: n-blocks of each problem
     __device__ TileSeq(const GemmArgs& a, const int* ts, const int* tn)
-        : t(blockIdx.x), i(0), b_res(a.b_res), n_tiles(a.n_tiles), n_problems(a.n_problems), tile_start(ts),
-          tiles_n(tn) {
+        : t(a.cluster2 ? blockIdx.x >> 1 : blockIdx.x), i(0), tstep(a.cluster2 ? gridDim.x >> 1 : gridDim.x),
+          pair(a.cluster2), rank(a.cluster2 ? static_cast<int>(blockIdx.x & 1) : 0), b_res(a.b_res),
+          n_tiles(a.n_tiles), n_problems(a.n_problems), tile_start(ts), tiles_n(tn) {
         const CtaWork w = a.cta[blockIdx.x];
         pi0 = w.pi;
         nb0 = w.nb;
@@ -168,7 +172,8 @@ struct TileSeq {
         const int local = t - tile_start[pi];
         mb = local / tiles_n[pi];
         nb = local - mb * tiles_n[pi];
-        t += gridDim.x;
+        if (pair) mb = 2 * mb + rank;  // pair tile -> this CTA's m-block
+        t += tstep;
         return true;
     }
 };
@@ -328,7 +333,7 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
     if (warp == kWarpTma && lane == 0) {
         for (int s = 0; s < n_stages; ++s) {
             ptx::mbar_init(&full_bar[s], a_mode == A_TMA ? 1 : (a_mode >= A_GATE_TMA ? 4 : 1 + 4));
-            ptx::mbar_init(&empty_bar[s], 1);
+            ptx::mbar_init(&empty_bar[s], args.cluster2 ? 2 : 1);  // cluster2: both CTAs' MMAs release the stage
             ptx::mbar_init(&raw_bar[s], 1);
         }
         ptx::mbar_init(bres_bar, 1);
@@ -348,6 +353,7 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
+    if (args.cluster2) ptx::cluster_sync();  // the peer's barriers are initialised before any multicast
     const uint32_t tmem_base = *tmem_slot;
     if (threadIdx.x == 0) trace(1);    // prologue done (barriers, TMEM, SMEM tables): wait for the producer of our inputs
     MTFM_PDL_ENTRY();
@@ -418,7 +424,12 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                         if (KS > 1) ptx::tma_load_3d(sa, &p.tma_a, &full_bar[stage], 0, mb * C::BM, kb);
                         else ptx::tma_load_2d(sa, &p.tma_a, &full_bar[stage], kb * C::BK, mb * C::BM);
                     }
-                    if (!args.b_res) {
+                    if (args.cluster2) {
+                        // our half of the B k-block, into both CTAs of the pair (KS == 1)
+                        const int h = static_cast<int>(blockIdx.x & 1);
+                        ptx::tma_load_2d_mc(sb + h * (BN / 2) * 128, &p.tma_b_half, &full_bar[stage], kb * C::BK,
+                                            nb * BN + h * (BN / 2), 0x3);
+                    } else if (!args.b_res) {
                         if (KS > 1) ptx::tma_load_3d(sb, &p.tma_b, &full_bar[stage], 0, nb * BN, kb);
                         else ptx::tma_load_2d(sb, &p.tma_b, &full_bar[stage], kb * C::BK, nb * BN);
                     }
@@ -588,7 +599,8 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                         ptx::umma_bf16(d_tmem, ptx::smem_desc(ptx::smem_u32(ones), 16, 256, 6),
                                        ptx::smem_desc(sbias, 16, 256, 6), idesc, 1u);
                     }
-                    ptx::umma_commit(&empty_bar[stage]);
+                    if (args.cluster2) ptx::umma_commit_mc(&empty_bar[stage], 0x3);
+                    else ptx::umma_commit(&empty_bar[stage]);
                     if (last) ptx::umma_commit(&tfull_bar[acc]);
                 }
                 __syncwarp();
@@ -912,6 +924,7 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
     }
     ptx::tc_fence_before();
     __syncthreads();
+    if (args.cluster2) ptx::cluster_sync();  // no CTA exits while its peer may still multicast / arrive into it
     if (warp == kWarpAlloc) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc<C::TMEM_COLS>(tmem_base);

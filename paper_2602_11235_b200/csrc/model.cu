@@ -619,7 +619,25 @@ void launch_gemm_tc_bn(GemmArgs& a, int grid, cudaStream_t st) {
     }
     const int smem = 1024 + a.bres_bytes + 4096 + a.n_stages * a.stage_bytes + a.n_epi * a.stg_warp + C::BAR_BYTES;
     if (smem > C::kMaxSmem) fail(MTFM_CONTRACT_ERROR, "gemm smem plan exceeds 227 KB");
-    launch_k(gemm_tc_kernel<BN>, dim3(grid), dim3(C::kThreads), smem, st, a);
+    if (a.cluster2) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(C::kThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[2];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[1].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = pdl_enabled() ? 2 : 1;
+        ck(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN>, a), "gemm_tc cluster launch");
+    } else {
+        launch_k(gemm_tc_kernel<BN>, dim3(grid), dim3(C::kThreads), smem, st, a);
+    }
     ck(cudaGetLastError(), "gemm_tc launch");
 }
 
@@ -828,6 +846,10 @@ void run_gemm_tc(std::vector<TcProblem> ps, cudaStream_t st, long long& launches
         for (size_t i = i0; i < i1; ++i)
             if (ps[i].K % 64 != 0 || ps[i].K < 128) ks = 1;
         if (force_kb && ks > 1) ks = force_kb;
+        // CTA pairs multicasting B (streaming, TMA-loaded A): MTFM_GEMM_CLUSTER=1
+        static const bool clus_env = std::getenv("MTFM_GEMM_CLUSTER") && std::atoi(std::getenv("MTFM_GEMM_CLUSTER")) != 0;
+        a.cluster2 = (!a.b_res && a.a_mode == A_TMA && bn >= 128 && clus_env) ? 1 : 0;
+        if (a.cluster2) ks = 1;
         a.stage_kb = ks;
         for (size_t i = i0; i < i1; ++i) {
             const auto& s = ps[i];
@@ -840,6 +862,7 @@ void run_gemm_tc(std::vector<TcProblem> ps, cudaStream_t st, long long& launches
             }
             // B: 2D boxes for the resident slice (loaded once per CTA), 3D per stage when streaming
             p.tma_b = (ks > 1 && !a.b_res) ? tma_3d_kb(s.Bt, s.N, s.K, s.ldb, bn, ks) : tma_2d(s.Bt, s.N, s.K, s.ldb, 64, bn, 128);
+            if (a.cluster2) p.tma_b_half = tma_2d(s.Bt, s.N, s.K, s.ldb, 64, bn / 2, 128);
             p.M = s.M;
             p.N = s.N;
             p.K = static_cast<int>(round_up(s.K, 64));
@@ -894,7 +917,8 @@ void run_gemm_tc(std::vector<TcProblem> ps, cudaStream_t st, long long& launches
                 const bool wide = bf16_out && bn >= 64;
                 p.tma_c = tma_2d(base, s.M, s.N, s.ldo, wide ? 64 : 32, 32, wide ? 128 : (bf16_out ? 64 : 128), eb);
             }
-            tiles += static_cast<int>(cdiv(s.M, 128)) * p.tiles_n;
+            // cluster2: pair tiles (m-blocks 2j, 2j+1 of one n-block)
+            tiles += static_cast<int>(a.cluster2 ? cdiv(cdiv(s.M, 128), 2) : cdiv(s.M, 128)) * p.tiles_n;
         }
         a.n_tiles = tiles;
         static const int dbg = std::getenv("MTFM_GEMM_DEBUG") ? std::atoi(std::getenv("MTFM_GEMM_DEBUG")) : 0;
@@ -917,7 +941,7 @@ void run_gemm_tc(std::vector<TcProblem> ps, cudaStream_t st, long long& launches
         static const bool stg_double = std::getenv("MTFM_GEMM_STG2") != nullptr;
         const int stg_warp = (all_fast && !stg_double) ? 4096 : 8192;
         a.stg_warp = stg_warp;
-        if (!a.b_res) grid = std::min(tiles, kNumSMs);
+        if (!a.b_res) grid = a.cluster2 ? 2 * std::min(tiles, kNumSMs / 2) : std::min(tiles, kNumSMs);
         bool any_bias = false;
         for (int i = 0; i < a.n_problems; ++i) any_bias = any_bias || a.p[i].has_bias;
         a.bias_bytes = any_bias ? bn * 32 : 0;
