@@ -1538,8 +1538,17 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
         ++L;
     }
     float* X = m.act[ACT_X].as<float>();
+    // the first target run's xhat (normalised context rows, source order) straight from the
+    // fused tokenizer's Y tiles when every context source goes through it (MTFM_TOK_XHAT=0: GLN pass)
+    bool xhat_from_tok = false;
     if constexpr (kTc) {
         std::vector<TcProblem> p1, p2;
+        static const bool tok_xhat = std::getenv("MTFM_TOK_XHAT") == nullptr || std::atoi(std::getenv("MTFM_TOK_XHAT")) != 0;
+        static const bool xhat_env = std::getenv("MTFM_XHAT") && std::atoi(std::getenv("MTFM_XHAT")) != 0;
+        long long ctx_rows0 = 0;
+        for (int s = 0; s < m.n_ctx_src; ++s) ctx_rows0 += B.src_cnt[s];
+        xhat_from_tok = tok_xhat && !xhat_env && m.n_ctx_src > 0 && ctx_rows0 == NE && !(m.fuse & 1) &&
+                        !m.layers.empty() && m.layers[0]->target;
         // sequence sources with one k-block of embeddings: fused MLP (tok_tc.cuh)
         static const bool tok_fused = std::getenv("MTFM_TOK_FUSED") == nullptr ||
                                       std::atoi(std::getenv("MTFM_TOK_FUSED")) != 0;
@@ -1561,11 +1570,19 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                 ts.M = M;
                 ts.k_steps = static_cast<int>(cdiv(si.k_pad, 16));
                 ts.tile_start = ta.n_tiles;
+                ts.xhat_row0 = s < m.n_ctx_src ? B.src_base[s] : -1;
                 ta.n_tiles += static_cast<int>(cdiv(M, 128));
                 fused_src.push_back(s);
             }
             ta.X = X;
+            ta.xhat = m.act[ACT_XN].as<__nv_bfloat16>();
+            ta.eps = static_cast<float>(m.cfg.eps);
         }
+        for (int s = 0; s < m.n_ctx_src; ++s)
+            if (B.src_cnt[s] > 0 && std::find(fused_src.begin(), fused_src.end(), s) == fused_src.end())
+                xhat_from_tok = false;
+        if (!xhat_from_tok)
+            for (int i = 0; i < ta.n_src; ++i) ta.s[i].xhat_row0 = -1;
         for (int s = 0; s < n_src; ++s) {
             if (std::find(fused_src.begin(), fused_src.end(), s) != fused_src.end()) continue;
             const auto& si = m.sources[s];
@@ -1820,7 +1837,7 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                         const bool with_full =
                             lj < m.layers.size() && !(m.fuse & 1) && (fold || kt + 1 <= kMaxGlnCopies);
                         if (fold) {
-                            {
+                            if (!(li == 0 && xhat_from_tok)) {
                                 GlnCopies gc{};
                                 gc.n = 1;
                                 gc.out[0] = XN;

@@ -42,6 +42,7 @@ struct TokSource {
     int M;                // rows
     int k_steps;          // ceil(k_pad / 16)
     int tile_start;       // first global tile
+    long long xhat_row0;  // >= 0: also write xhat = (y - mean) * rstd (bf16) to TokArgs::xhat rows xhat_row0 + m
 };
 
 struct TokArgs {
@@ -49,6 +50,8 @@ struct TokArgs {
     int n_src;
     int n_tiles;
     float* X;             // [rows][256] fp32
+    __nv_bfloat16* xhat;  // [rows][256] bf16, source order: the first target run's normalised context rows
+    float eps;
     unsigned long long* trace;  // timing experiments only (-DMTFM_TOK_TRACE): CTA 0 clock stamps
 };
 
@@ -170,6 +173,9 @@ __global__ void __launch_bounds__(512, 1) tok_fused_kernel(const __grid_constant
             orow[j] = m < src.M ? static_cast<long long>(__ldg(src.row_map + m)) : -1;
         }
         const uint32_t lane_addr = (q * 32u) << 16;
+        // xhat (one drain slot only: lane = row holds every column of its row across cb)
+        const bool xh = src.xhat_row0 >= 0 && nslots == 1;
+        float ssum = 0.f, ssq = 0.f;
         ptx::mbar_wait(y_full, n_t & 1);
         ptx::tc_fence_after();
 #pragma unroll 1
@@ -178,7 +184,14 @@ __global__ void __launch_bounds__(512, 1) tok_fused_kernel(const __grid_constant
             ptx::tmem_ld16(tmem + lane_addr + Y_COL + cb * 32, *reinterpret_cast<float(*)[16]>(v));
             ptx::tmem_ld16(tmem + lane_addr + Y_COL + cb * 32 + 16, *reinterpret_cast<float(*)[16]>(v + 16));
             ptx::tmem_ld_wait();
-            if (cb + nslots >= D / 32) {
+            if (xh) {
+#pragma unroll
+                for (int e = 0; e < 32; ++e) {
+                    ssum += v[e];
+                    ssq = fmaf(v[e], v[e], ssq);
+                }
+            }
+            if (!xh && cb + nslots >= D / 32) {
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(y_empty);  // Y is free for the next tile's GEMM2
@@ -200,6 +213,38 @@ __global__ void __launch_bounds__(512, 1) tok_fused_kernel(const __grid_constant
                         __stcs(reinterpret_cast<float4*>(args.X + orow[j] * D + cb * 32 + sb8 * 8 + 4 * half), w);
                 }
                 __syncwarp();
+            }
+        }
+        if (xh) {
+            // second pass over the row in TMEM: xhat = (y - mean) * rstd (population variance,
+            // GLN of hta.hpp:104-109 without the affine, which the folded K|V / f1 weights carry).
+            // Y goes back to the GEMM2 warp after this pass's last TMEM load. (Reading the row
+            // back from X instead, after releasing Y, was 3x slower: one row per lane.)
+            const float mean = ssum * (1.f / D);
+            const float var = fmaxf(ssq * (1.f / D) - mean * mean, 0.f);
+            const float rstd = rsqrtf(var + args.eps);
+            const int m = m0 + static_cast<int>(q * 32 + lane);
+            __nv_bfloat16* xr = args.xhat + (src.xhat_row0 + m) * D;
+#pragma unroll 1
+            for (int cb = 0; cb < D / 32; ++cb) {
+                float v[32];
+                ptx::tmem_ld16(tmem + lane_addr + Y_COL + cb * 32, *reinterpret_cast<float(*)[16]>(v));
+                ptx::tmem_ld16(tmem + lane_addr + Y_COL + cb * 32 + 16, *reinterpret_cast<float(*)[16]>(v + 16));
+                ptx::tmem_ld_wait();
+                if (cb == D / 32 - 1) {
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(y_empty);  // Y is free for the next tile's GEMM2
+                }
+                if (m < src.M) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        *reinterpret_cast<uint4*>(xr + cb * 32 + 8 * j) =
+                            make_uint4(pack_bf16((v[8 * j] - mean) * rstd, (v[8 * j + 1] - mean) * rstd),
+                                       pack_bf16((v[8 * j + 2] - mean) * rstd, (v[8 * j + 3] - mean) * rstd),
+                                       pack_bf16((v[8 * j + 4] - mean) * rstd, (v[8 * j + 5] - mean) * rstd),
+                                       pack_bf16((v[8 * j + 6] - mean) * rstd, (v[8 * j + 7] - mean) * rstd));
+                }
             }
         }
     };
