@@ -456,7 +456,6 @@ template void launch_gather<__nv_bfloat16>(const DevBatch&, const SourceInfo*, c
 // row_normalize (kernels.hpp:132-153) + group_affine (eval_ctx.hpp:130-143).
 // One warp per row, 4 consecutive columns per lane per 128-column slice,
 // vectorised loads/stores (memory-bound: one read + one write of the row).
-constexpr int kMaxSlices = 8;  // d <= 1024
 
 __device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
 __device__ __forceinline__ float4 ld4(const __nv_bfloat16* p) {
