@@ -1577,6 +1577,9 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
             ta.X = X;
             ta.xhat = m.act[ACT_XN].as<__nv_bfloat16>();
             ta.eps = static_cast<float>(m.cfg.eps);
+            // x̂ stores staged through shared memory (MTFM_TOK_XHAT=1: one row per lane, unstaged)
+            static const int tok_xhat_mode = std::getenv("MTFM_TOK_XHAT") ? std::atoi(std::getenv("MTFM_TOK_XHAT")) : 2;
+            ta.xhat_staged = tok_xhat_mode == 2 ? 1 : 0;
         }
         for (int s = 0; s < m.n_ctx_src; ++s)
             if (B.src_cnt[s] > 0 && std::find(fused_src.begin(), fused_src.end(), s) == fused_src.end())

@@ -52,6 +52,7 @@ struct TokArgs {
     float* X;             // [rows][256] fp32
     __nv_bfloat16* xhat;  // [rows][256] bf16, source order: the first target run's normalised context rows
     float eps;
+    int xhat_staged;      // 1: x̂ stores go through shared memory (8 rows x 64 B per store instruction)
     unsigned long long* trace;  // timing experiments only (-DMTFM_TOK_TRACE): CTA 0 clock stamps
 };
 
@@ -236,7 +237,29 @@ __global__ void __launch_bounds__(512, 1) tok_fused_kernel(const __grid_constant
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(y_empty);  // Y is free for the next tile's GEMM2
                 }
-                if (m < src.M) {
+                if (args.xhat_staged) {
+                    // 2 KB per warp from the staging slots the SiLU warps leave idle at one drain
+                    // slot: row r = lane, 16 B chunk j at (j ^ (r >> 1 & 3)) (conflict-free both ways);
+                    // then 4 lanes per row, 8 rows x 64 B per store instruction
+                    uint8_t* xb = reinterpret_cast<uint8_t*>(stg + (slot - 8) * 2 * 32 * 8);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        *reinterpret_cast<uint4*>(xb + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) =
+                            make_uint4(pack_bf16((v[8 * j] - mean) * rstd, (v[8 * j + 1] - mean) * rstd),
+                                       pack_bf16((v[8 * j + 2] - mean) * rstd, (v[8 * j + 3] - mean) * rstd),
+                                       pack_bf16((v[8 * j + 4] - mean) * rstd, (v[8 * j + 5] - mean) * rstd),
+                                       pack_bf16((v[8 * j + 6] - mean) * rstd, (v[8 * j + 7] - mean) * rstd));
+                    __syncwarp();
+                    const int c = lane & 3;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int rr = 8 * i + (lane >> 2);
+                        const uint4 w = *reinterpret_cast<const uint4*>(xb + rr * 64 + ((c ^ ((rr >> 1) & 3)) << 4));
+                        const int mr = m0 + static_cast<int>(q * 32) + rr;
+                        if (mr < src.M) *reinterpret_cast<uint4*>(args.xhat + (src.xhat_row0 + mr) * D + cb * 32 + c * 8) = w;
+                    }
+                    __syncwarp();
+                } else if (m < src.M) {
 #pragma unroll
                     for (int j = 0; j < 4; ++j)
                         *reinterpret_cast<uint4*>(xr + cb * 32 + 8 * j) =
