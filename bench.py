@@ -14,8 +14,11 @@ e2e   : the same metric through mtfm_cuda_forward with pinned host buffers:
 roofline: the dominant stage of a profiled step (CUDA events around each
         stage, same stream), algorithmic FLOPs / its duration
         vs MEASURED_PEAKS.json.
-cpu_baseline: the reference CPU path (oracle/_ref/ref_bench, compiled from the
-        unmodified reference sources) on this host's cores, bounded sample.
+cpu_baseline: the reference CPU path (ref_bench over the unmodified reference
+        sources, built on this host with the reference's -march=native when g++
+        and baseline/_ref/proj are present, else the x86-64-v3 oracle/_ref build)
+        on this host's cores, on the first --ref-users users of the GPU arm's own
+        batch (MTFMPB1 file: byte-identical inputs) with the GPU arm's weights.
 
 --impl reference runs only the reference CPU path (rank 0; other ranks exit).
 """
@@ -34,19 +37,75 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 REF_BENCH = os.path.join(ROOT, "oracle", "_ref", "ref_bench")
+REF_SRC = os.path.join(ROOT, "baseline", "_ref", "proj")
 
-CONFIGS = {
-    # name: (datagen workload, ref_bench flags of the same shape)
-    "small": ("small", ["--d", "256", "--blocks", "1", "--K", "3", "--P", "1", "--H", "8", "--G", "2",
-                        "--dexp", "256", "--lenmin", "224", "--lenmax", "224", "--rlen", "64",
-                        "--expmin", "8", "--expmax", "8"]),
-    "large": ("large", ["--d", "1024", "--blocks", "4", "--K", "3", "--P", "1", "--H", "16", "--G", "4",
-                        "--dexp", "1024", "--lenmin", "896", "--lenmax", "896", "--rlen", "256",
-                        "--expmin", "32", "--expmax", "32"]),
-    "paper": ("paper", ["--d", "768", "--blocks", "4", "--K", "3", "--P", "1", "--H", "3", "--G", "1",
-                        "--dexp", "768", "--lenmin", "896", "--lenmax", "896", "--rlen", "256",
-                        "--expmin", "32", "--expmax", "32"]),
-}
+# BASELINE.json configs (paper_2602_11235_b200/datagen.py WORKLOADS): small is
+# configs[1] (the 1-GPU headline), base configs[2] (heavy-tailed lengths),
+# large configs[3] (per-GPU shard), paper the north_star's paper-scale shape.
+CONFIGS = ("small", "base", "large", "paper")
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_tag():
+    """Model name + ISA flags: a -march=native binary is only reused on an identical CPU."""
+    import hashlib
+    flags = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("flags"):
+                    flags = line
+                    break
+    except OSError:
+        pass
+    return hashlib.sha1((cpu_model() + flags).encode()).hexdigest()[:12]
+
+
+def ref_bench_binary():
+    """(path, how): the reference CPU path built on this host with the reference's own
+    -march=native (proj/src/CMakeLists.txt:10-13), cached per CPU model; else the
+    x86-64-v3 build that travelled with the snapshot."""
+    import shutil
+    tag = cpu_tag()
+    native = os.path.join(ROOT, "baseline", "_ref", "bin", f"ref_bench_native_{tag}")
+    if os.path.exists(native):
+        return native, "-march=native (built on this host)"
+    why = None
+    if not os.path.isdir(REF_SRC):
+        why = "baseline/_ref/proj missing"
+    elif shutil.which("g++") is None:
+        why = "no g++ on this host"
+    else:
+        os.makedirs(os.path.dirname(native), exist_ok=True)
+        r = subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "native", "REF=" + REF_SRC,
+                            "OUT=" + os.path.dirname(native)], capture_output=True, text=True, timeout=600)
+        built = os.path.join(os.path.dirname(native), "ref_bench_native")
+        if r.returncode == 0 and os.path.exists(built):
+            os.replace(built, native)
+            return native, "-march=native (built on this host)"
+        why = "native build failed: " + r.stderr.strip()[-200:]
+    return REF_BENCH, f"-march=x86-64-v3 (prebuilt; {why})"
+
+
+def write_cpu_inputs(batch, schemas, cfg, params, order):
+    """The GPU arm's batch and weights as MTFMPB1 / MTFMPF1 files for ref_bench."""
+    import tempfile
+    from paper_2602_11235_b200 import packed_io
+    d = tempfile.mkdtemp(prefix="mtfm_ref_")
+    bp, pp = os.path.join(d, "batch.bin"), os.path.join(d, "params.bin")
+    packed_io.save_packed(bp, batch, schemas, cfg)
+    packed_io.save_params(pp, params, order)
+    return bp, pp
 
 
 def load_peaks():
@@ -103,17 +162,19 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def cpu_baseline(cfg_name, threads, users, reps=2):
-    flags = CONFIGS[cfg_name][1]
-    if not os.path.exists(REF_BENCH):
+def cpu_baseline(inputs, threads, users, reps=2):
+    exe, how = ref_bench_binary()
+    if not os.path.exists(exe):
         return None
-    cmd = [REF_BENCH, *flags, "--users", str(users), "--threads", str(threads), "--reps", str(reps), "--gseed", "3"]
+    bp, pp = inputs
+    cmd = [exe, "--batch", bp, "--params", pp, "--users", str(users), "--threads", str(threads), "--reps", str(reps)]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
     if out.returncode != 0:
         return {"error": out.stderr.strip()[-200:]}
     lines = [json.loads(x) for x in out.stdout.strip().splitlines() if x.startswith("{")]
     best = max(lines, key=lambda r: r["targets_per_sec"])
     best["per_rep"] = [r["targets_per_sec"] for r in lines]
+    best["build"] = how
     return best
 
 
@@ -124,15 +185,28 @@ def dist_setup():
     return world, rank, local
 
 
+def workload_inputs(args):
+    """The N=1 batch of the config (the GPU arm's rank-0 input at N=1) and its weights."""
+    from paper_2602_11235_b200 import datagen
+    from paper_2602_11235_b200.schema import param_specs
+    wl = datagen.WORKLOADS[args.config]()
+    batch = datagen.generate(wl, n_users=args.users or wl.n_users)
+    specs = param_specs(wl.schemas, wl.cfg)
+    params = datagen.random_params(specs, seed=7)
+    return wl, batch, params, [n for n, _, _ in specs]
+
+
 def run_reference(args, world, rank):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
     users = args.ref_users
     t0 = time.time()
+    wl, batch, params, order = workload_inputs(args)
+    inputs = write_cpu_inputs(batch, wl.schemas, wl.cfg, params, order)
     rows = []
     for _ in range(args.warmup + args.steps):
-        r = cpu_baseline(args.config, threads, users, reps=1)
+        r = cpu_baseline(inputs, threads, users, reps=1)
         if r is None or "error" in (r or {}):
             print(json.dumps({"impl": "reference", "unavailable": f"oracle/_ref/ref_bench missing or failed: {r}"}))
             return
@@ -146,10 +220,13 @@ def run_reference(args, world, rank):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * secs / len(timed),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"MTFM-{args.config}", "users_per_step": users, "threads": threads,
+                   "cpu_model": cpu_model(), "build": rows[-1].get("build"),
                    "note": "reference Model<float>::forward_sample striped over std::thread workers "
-                           "(train.hpp:157-170), compiled from the unmodified reference sources"},
+                           "(train.hpp:157-170), compiled from the unmodified reference sources; inputs are "
+                           "the first users of the GPU arm's N=1 batch (same bytes) with its weights"},
         "cpu_baseline": {"value": value, "unit": "targets/s", "cores": threads, "kind": "reference",
-                         "sample": f"{users} users x {args.steps} steps of the {args.config} shape"},
+                         "cpu_model": cpu_model(),
+                         "sample": f"first {users} users of the MTFM-{args.config} batch x {args.steps} steps"},
         "e2e": {"value": value, "unit": "targets/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": time.time() - t0,
     }
@@ -162,7 +239,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="small", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="small", choices=CONFIGS)
     ap.add_argument("--users", type=int, default=None, help="users per GPU (default: the config's)")
     ap.add_argument("--e2e-steps", type=int, default=50, help="e2e steps per API (pipelined and synchronous)")
     ap.add_argument("--ref-users", type=int, default=96)
@@ -184,21 +261,30 @@ def main():
     from paper_2602_11235_b200 import Model, abi, datagen
     from paper_2602_11235_b200.schema import BATCH_KEYS, batch_nbytes
 
-    wl = datagen.WORKLOADS[CONFIGS[args.config][0]]()
+    wl = datagen.WORKLOADS[args.config]()
     per_gpu = args.users or wl.n_users
     if world == 1:
         batch = datagen.generate(wl, n_users=per_gpu)
     else:
-        # one global batch of world x per_gpu users, sharded by LPT on estimated
-        # cost; no collective touches the data path (weak scaling)
+        # one global batch of world x per_gpu users, sharded by LPT on each user's
+        # algorithmic cost under this model config; no collective touches the data
+        # path (weak scaling)
         from paper_2602_11235_b200.shard import shard_plan, take_users
         full = datagen.generate(wl, n_users=per_gpu * world)
-        batch = take_users(full, shard_plan(full, world)[rank])
+        batch = take_users(full, shard_plan(full, world, cfg=wl.cfg)[rank])
         del full
     model = Model(wl.schemas, wl.cfg, precision="bf16", device=local)
-    model.set_params(datagen.random_params(model.param_specs(), seed=7))
+    params = datagen.random_params(model.param_specs(), seed=7)
+    model.set_params(params)
     n_targets = int(len(batch["exp_ts"]))
     n_tokens = int(len(batch["ev_ts"])) + n_targets
+    rank_targets = [n_targets]
+    if dist is not None:
+        t = torch.tensor([n_targets], device="cuda", dtype=torch.int64)
+        g = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(g, t)
+        rank_targets = [int(x.item()) for x in g]
+    total_targets = sum(rank_targets)
 
     stream = torch.cuda.ExternalStream(model.stream_handle(), device=torch.device("cuda", local))
 
@@ -236,7 +322,7 @@ def main():
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    value = n_targets * world / (ms / 1000.0)
+    value = total_targets / (ms / 1000.0)  # every rank's targets over the slowest rank's time
 
     # ---------------- profiled step: per-stage device times (roofline)
     model.set_profiling(True)
@@ -340,7 +426,7 @@ def main():
         t = torch.tensor([e2e_s, e2e_sync_s], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s, e2e_sync_s = float(t[0].item()), float(t[1].item())
-    e2e_value = n_targets * world / e2e_s
+    e2e_value = total_targets / e2e_s
 
     if rank != 0:
         if dist is not None:
@@ -350,11 +436,14 @@ def main():
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         threads = os.cpu_count() or 1
-        cb = cpu_baseline(args.config, threads, args.ref_users, reps=2)
+        inputs = write_cpu_inputs(batch, wl.schemas, wl.cfg, params, [n for n, _, _ in model.param_specs()])
+        cb = cpu_baseline(inputs, threads, args.ref_users, reps=2)
         if cb and "error" not in cb:
             cpu = {"value": cb["targets_per_sec"], "unit": "targets/s", "cores": threads, "kind": "reference",
-                   "sample": f"{cb['users']} users of the {args.config} shape ({cb['targets']} targets, best of 2 "
-                             f"reps), reference Model<float>::forward_sample on std::thread workers"}
+                   "cpu_model": cpu_model(), "build": cb["build"],
+                   "sample": f"first {cb['users']} users of this batch ({cb['targets']} targets, same bytes and "
+                             f"weights, best of 2 reps), reference Model<float>::forward_sample on std::thread "
+                             f"workers"}
         else:
             cpu = {"value": None, "unit": "targets/s", "cores": threads, "kind": "reference",
                    "sample": f"unavailable: {cb}"}
@@ -364,6 +453,7 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": f"MTFM-{args.config}", "users_per_gpu": int(len(batch["user_id"])),
+                   "targets_per_rank": rank_targets,
                    "tokens_per_gpu": n_tokens, "targets_per_gpu": n_targets,
                    "layers": f"({wl.cfg.hta.target_layers}:{wl.cfg.hta.full_layers})x{wl.cfg.hta.blocks}",
                    "d_model": wl.cfg.hta.d_model, "heads": wl.cfg.hta.heads, "kv_heads": wl.cfg.hta.kv_heads,
@@ -371,7 +461,7 @@ def main():
                    "l2": "inputs/activations > L2 (X alone is %.0f MB)" % (n_tokens * wl.cfg.hta.d_model * 4 / 1e6)},
         "e2e": {"value": e2e_value, "unit": "targets/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_s * 1000, "api": "batch_update/batch_run/batch_results, two batches in flight",
-                "sync_call": {"value": n_targets * world / e2e_sync_s, "ms_per_step": e2e_sync_s * 1000,
+                "sync_call": {"value": total_targets / e2e_sync_s, "ms_per_step": e2e_sync_s * 1000,
                               "api": "mtfm_cuda_forward, one call per step"}},
         "gpu_launches": launches_per_step * args.steps,
         "roofline": roof,

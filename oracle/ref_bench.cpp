@@ -6,6 +6,12 @@
 //
 // TEST / BASELINE INFRASTRUCTURE ONLY: used by bench.py's cpu_baseline leg and
 // by `bench.py --impl reference`. Prints one JSON line per rep.
+//
+// --batch FILE [--params FILE]: score the users of an MTFMPB1 packed batch (the
+// GPU arm's own input bytes, paper_2602_11235_b200/packed_io.py) with the
+// model config stored in it and, optionally, the GPU arm's parameters;
+// --users N limits the sample to the file's first N users. Without --batch the
+// reference generator (datagen.cpp) makes the users.
 #include <algorithm>
 #include <atomic>
 #include <chrono>
@@ -17,6 +23,7 @@
 
 #include "mtfm/datagen.hpp"
 #include "mtfm/model.hpp"
+#include "packed_io.hpp"
 
 using namespace mtfm;
 
@@ -43,6 +50,8 @@ int main(int argc, char** argv) {
     mc.d_expert = 256;
     int threads = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
     int reps = 1, rlen = -1;
+    std::string batch_file, params_file;
+    bool users_set = false;
     try {
         for (int i = 1; i < argc; ++i) {
             std::string a = argv[i];
@@ -50,7 +59,10 @@ int main(int argc, char** argv) {
                 if (i + 1 >= argc) throw config_error("missing value for " + a);
                 return argv[++i];
             };
-            if (a == "--users") gc.n_users = std::stoi(nxt());
+            if (a == "--users") {
+                gc.n_users = std::stoi(nxt());
+                users_set = true;
+            }
             else if (a == "--scen") gc.n_scenarios = std::stoi(nxt());
             else if (a == "--nh") gc.n_hist_seqs = std::stoi(nxt());
             else if (a == "--nr") gc.n_rt_seqs = std::stoi(nxt());
@@ -69,14 +81,25 @@ int main(int argc, char** argv) {
             else if (a == "--dexp") mc.d_expert = std::stoi(nxt());
             else if (a == "--threads") threads = std::stoi(nxt());
             else if (a == "--reps") reps = std::stoi(nxt());
+            else if (a == "--batch") batch_file = nxt();
+            else if (a == "--params") params_file = nxt();
             else throw config_error("unknown flag " + a);
         }
-        Dataset d = generate_dataset(gc);
-        if (rlen >= 0)
+        Dataset d;
+        if (!batch_file.empty()) {
+            mtfa::PackedFile pf = mtfa::load_packed(batch_file);
+            if (pf.has_model) mc = pf.cfg;
+            d = std::move(pf.data);
+            if (users_set && gc.n_users < static_cast<int>(d.samples.size())) d.samples.resize(static_cast<size_t>(gc.n_users));
+        } else {
+            d = generate_dataset(gc);
+        }
+        if (rlen >= 0 && batch_file.empty())
             for (auto& s : d.samples)
                 for (auto& rec : s.realtime_sequences)
                     if (static_cast<int>(rec.events.size()) > rlen) rec.events.resize(static_cast<size_t>(rlen));
         Model<float> model = Model<float>::build(SchemaSet::from(d), mc, 7);
+        if (!params_file.empty()) mtfa::load_params_into(params_file, model.params);
         size_t targets = 0, tokens = 0;
         for (const auto& s : d.samples) {
             targets += s.exposures.size();

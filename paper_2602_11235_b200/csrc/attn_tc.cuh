@@ -13,12 +13,14 @@
 //
 // Tile = 128 MMA rows = HS heads of one GQA group x RT query rows (HS*RT=128),
 // so every K/V tile TMA-loaded into SMEM is shared by the HS query heads that
-// read it. Per key tile j:
-//   MMA warp     : S[j%2] = Q K_j^T            (TMEM, fp32, 128 x BKV)
-//                  O[t%2] += P[(j-2)%2] V_{j-2} (P from TMEM, V MN-major SMEM)
-//   16 SiLU warps: S -> regs, silu = h + h*tanh(h) (h = s/2: FMUL2, MUFU.TANH,
-//                  FFMA2), mask only on the boundary key tile, bf16 pack,
-//                  tcgen05.st into the TMEM P[j%2] buffer, arrive.
+// read it. Per key tile j (three S/P TMEM buffers, b = j % 3):
+//   S warp       : S[b] = Q K_j^T              (TMEM, fp32, 128 x BKV)
+//   16 SiLU warps: each takes a quarter of every key tile's columns: S -> regs,
+//                  silu = h + h*tanh(h) (h = s/2: FMUL2, MUFU.TANH, FFMA2), mask
+//                  only on the boundary key tile, packed bf16 P written over the
+//                  first half of the warp's own S columns (tcgen05.st), arrive.
+//   PV warp      : O[t%2] += P[b] V_j (P from TMEM, V MN-major SMEM); its commit
+//                  hands S/P buffer b back to the S warp.
 //   4 epilogue warps: O[t%2] -> regs, x s_i, + self term for T rows, bf16 out
 //                  (overlaps the next tile's key loop).
 // Q and O are double-buffered, so consecutive tiles of a CTA pipeline.
@@ -54,7 +56,6 @@ struct AttnParams {
     long long ldkv;
     __nv_bfloat16* out;          // A rows indexed like Q rows
     long long ldo;
-    unsigned long long* trace;   // timing experiments only (-DMTFM_ATTN_TRACE): CTA 0 clock stamps
 };
 
 namespace attn_detail {
@@ -77,12 +78,10 @@ struct Cfg {
     static constexpr int kStages = kStagesRaw > 12 ? 12 : kStagesRaw;
     static constexpr int SMEM = QB * Q_BYTES + kStages * STAGE_BYTES + 1024 + 512;
     static constexpr uint32_t TMEM_COLS = 512;
-    static constexpr uint32_t S_COL = 0;                    // S buffers at [0, 2*BKV)
-    static constexpr uint32_t P_COL = 2 * BKV;               // P (packed bf16) buffers at [2*BKV, 3*BKV)
-    static constexpr uint32_t O_COL = 3 * BKV;
-    static constexpr int OB = (3 * BKV + 2 * D <= 512) ? 2 : 1;  // O buffers
+    static constexpr int NB = 3;                            // S/P TMEM buffers (P aliases S)
+    static constexpr uint32_t O_COL = NB * BKV;
+    static constexpr int OB = (NB * BKV + 2 * D <= 512) ? 2 : 1;  // O buffers
     static constexpr int kSilu = 16;                        // SiLU warps (4 per TMEM lane quarter)
-    static constexpr int CPW = BKV / 4;                     // key columns per SiLU warp
     static constexpr int kThreads = (4 + kSilu + 4) * 32;   // + TMA/MMA/alloc/spare + 4 epilogue warps
     static_assert(O_COL + OB * D <= 512, "TMEM budget");
     static_assert(SMEM <= 227 * 1024, "SMEM budget");
@@ -97,20 +96,17 @@ using ptx::silu2_bf16;
 
 }  // namespace attn_detail
 
-// EMU: of every 16 SiLU pairs in an unmasked chunk, EMU run on the FMA/ALU pipes
-// (silu2_bf16_fma) and the rest on MUFU.TANH, so neither pipe alone bounds the phase
-// SPA: P aliases S. Three S/P TMEM buffers; each SiLU warp overwrites the
-// first half of its own S columns with packed bf16 P and every one of the 16
-// SiLU warps works on every key tile (a quarter of its columns); a buffer is
-// released to the S issuer only after the P.V that reads it completed.
-template <int D, int EMU = 0, bool SPA = false>
+// P aliases S: each SiLU warp overwrites the first half of its own S columns
+// with packed bf16 P and every one of the 16 SiLU warps works on every key tile
+// (a quarter of its columns); a buffer is released to the S issuer only after
+// the P.V that reads it completed.
+template <int D>
 __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__ AttnParams prm) {
     using C = attn_detail::Cfg<D>;
     constexpr int BKV = C::BKV;
-    constexpr int NB = SPA ? 3 : 2;                  // S (and, with SPA, P) buffers
-    constexpr uint32_t kOCol = SPA ? NB * BKV : C::O_COL;
-    constexpr int kOB = SPA ? ((NB * BKV + 2 * D <= 512) ? 2 : 1) : C::OB;
-    static_assert(kOCol + kOB * D <= 512, "TMEM budget");
+    constexpr int NB = C::NB;
+    constexpr uint32_t kOCol = C::O_COL;
+    constexpr int kOB = C::OB;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sQ = smem;
@@ -121,23 +117,15 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
     uint64_t* o_full = bars + 4;   // [2]
     uint64_t* o_empty = bars + 6;  // [2]
     uint64_t* s_full = bars + 8;            // [NB]
-    uint64_t* s_empty = bars + 8 + NB;      // [NB] (SPA: released by the P.V commit)
+    uint64_t* s_empty = bars + 8 + NB;      // [NB] released by the P.V commit
     uint64_t* p_full = bars + 8 + 2 * NB;   // [NB]
-    uint64_t* p_empty = bars + 8 + 3 * NB;  // [NB] (unused with SPA)
-    uint64_t* kv_full = bars + 8 + 4 * NB;  // [kStages]
+    uint64_t* kv_full = bars + 8 + 3 * NB;  // [kStages]
     uint64_t* kv_empty = kv_full + C::kStages;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kv_empty + C::kStages);
 
     const uint32_t warp = ptx::warp_id();
     const uint32_t lane = ptx::lane_id();
     const int r_per_g = prm.heads / prm.kv_heads;
-#ifdef MTFM_ATTN_TRACE
-    auto trace = [&](int slot) {
-        if (prm.trace && blockIdx.x == 0 && lane == 0 && slot >= 0 && slot < 2048) prm.trace[slot] = clock64();
-    };
-#else
-    auto trace = [&](int) {};
-#endif
 
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < 2; ++i) {
@@ -148,9 +136,8 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
         }
         for (int i = 0; i < NB; ++i) {
             ptx::mbar_init(&s_full[i], 1);
-            ptx::mbar_init(&s_empty[i], SPA ? 1 : C::kSilu / 2);
-            ptx::mbar_init(&p_full[i], SPA ? C::kSilu : C::kSilu / 2);
-            ptx::mbar_init(&p_empty[i], 1);
+            ptx::mbar_init(&s_empty[i], 1);
+            ptx::mbar_init(&p_full[i], C::kSilu);
         }
         for (int i = 0; i < C::kStages; ++i) {
             ptx::mbar_init(&kv_full[i], 1);
@@ -228,11 +215,8 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
             const uint32_t sq = ptx::smem_u32(sQ + qb * C::Q_BYTES);
             for (int j = 0; j < n_kv; ++j) {
                 const uint32_t buf = s_cnt % NB;
-                if (s_cnt < 128) trace(1024 + 4 * s_cnt + 0);
                 ptx::mbar_wait(&kv_full[stage], phase);
-                if (s_cnt < 128) trace(1024 + 4 * s_cnt + 1);
                 ptx::mbar_wait(&s_empty[buf], ((s_cnt / NB) & 1) ^ 1);
-                if (s_cnt < 128) trace(1024 + 4 * s_cnt + 2);
                 ptx::tc_fence_after();
                 if (ptx::elect_one()) {
                     const uint32_t sk = ptx::smem_u32(sKV + stage * C::STAGE_BYTES);
@@ -242,7 +226,7 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
                         const uint32_t in = ((kk * 16) % C::CHUNK) * 2;
                         const uint64_t da = ptx::smem_desc(sq + sl * (128 * C::ROWB) + in, 16, 8 * C::ROWB, C::LAYOUT);
                         const uint64_t db = ptx::smem_desc(sk + sl * (BKV * C::ROWB) + in, 16, 8 * C::ROWB, C::LAYOUT);
-                        ptx::umma_bf16(tmem + C::S_COL + buf * BKV, da, db, idesc_s, kk > 0);
+                        ptx::umma_bf16(tmem + buf * BKV, da, db, idesc_s, kk > 0);
                     }
                     if (j == n_kv - 1) ptx::umma_commit(&q_empty[qb]);
                     ptx::umma_commit(&s_full[buf]);
@@ -280,34 +264,28 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
             for (int j = 0; j < n_kv; ++j, ++cnt) {
                 const uint32_t buf = cnt % NB;
                 ptx::mbar_wait(&p_full[buf], (cnt / NB) & 1);
-                if (cnt < 128) trace(1024 + 4 * cnt + 3);
                 ptx::tc_fence_after();
                 if (ptx::elect_one()) {
                     const uint32_t sv = ptx::smem_u32(sKV + stage * C::STAGE_BYTES + C::KV_TILE_BYTES);
                     const uint32_t o_tmem = tmem + kOCol + ob * D;
 #pragma unroll
                     for (int kk = 0; kk < BKV / 16; ++kk) {
-                        uint32_t p_col;
-                        if constexpr (SPA) {
-                            // keys [16kk, 16kk+16) were packed by the SiLU warp owning
-                            // S columns [CW*c, CW*(c+1)), c = 16kk / CW, into its first CW/2
-                            constexpr int CW = BKV / 4;
-                            p_col = buf * BKV + ((16 * kk) / CW) * CW + ((16 * kk) % CW) / 2;
-                        } else {
-                            p_col = C::P_COL + buf * (BKV / 2) + kk * 8;
-                        }
+                        // keys [16kk, 16kk+16) were packed by the SiLU warp owning
+                        // S columns [CW*c, CW*(c+1)), c = 16kk / CW, into its first CW/2
+                        constexpr int CW = BKV / 4;
+                        const uint32_t p_col = buf * BKV + ((16 * kk) / CW) * CW + ((16 * kk) % CW) / 2;
                         const uint64_t db = ptx::smem_desc(sv + kk * 16 * C::ROWB, BKV * C::ROWB, 8 * C::ROWB, C::LAYOUT);
                         ptx::umma_bf16_ts(o_tmem, tmem + p_col, db, idesc_o, (j > 0 || kk > 0));
                     }
                     ptx::umma_commit(&kv_empty[stage]);
-                    ptx::umma_commit(SPA ? &s_empty[buf] : &p_empty[buf]);
+                    ptx::umma_commit(&s_empty[buf]);
                     if (j == n_kv - 1) ptx::umma_commit(&o_full[ob]);
                 }
                 __syncwarp();
                 if (++stage == C::kStages) stage = 0;
             }
         }
-    } else if (SPA && warp >= 4 && warp < 4 + C::kSilu) {
+    } else if (warp >= 4 && warp < 4 + C::kSilu) {
         // ------------------------------------------------ SiLU warps, P aliasing S
         constexpr int CW = BKV / 4;               // key columns per warp and key tile
         const uint32_t q = warp & 3;              // TMEM lane quarter
@@ -324,10 +302,7 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
             const int prefix = i < tile.n_rows ? __ldg(prm.q_prefix + tile.q_row0 + i) : 0;
             for (int j = 0; j < n_kv; ++j, ++s_cnt) {
                 const uint32_t buf = s_cnt % NB;
-                const bool tr = warp == 4 && s_cnt < 128;
-                if (tr) trace(4 * s_cnt + 0);
                 ptx::mbar_wait(&s_full[buf], (s_cnt / NB) & 1);
-                if (tr) trace(4 * s_cnt + 1);
                 ptx::tc_fence_after();
                 const uint32_t col = buf * BKV + cq * CW;
                 const int nvalid = prefix - (j * BKV + static_cast<int>(cq) * CW);  // >= CW: no masking
@@ -344,8 +319,7 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
                     if (__all_sync(0xffffffffu, nvalid >= CW)) {
 #pragma unroll
                         for (int e = 0; e < CW; e += 2)
-                            pk[e / 2] = ((e / 2) * EMU) % 16 < EMU ? ptx::silu2_bf16_fma(v[e], v[e + 1])
-                                                                   : attn_detail::silu2_bf16(v[e], v[e + 1]);
+                            pk[e / 2] = attn_detail::silu2_bf16(v[e], v[e + 1]);
                     } else {
 #pragma unroll
                         for (int e = 0; e < CW; e += 2) {
@@ -355,86 +329,8 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
                         }
                     }
                 }
-                if (tr) trace(4 * s_cnt + 2);
                 if constexpr (CW / 2 == 16) ptx::tmem_st16(tmem + lane_addr + col, pk);
                 else ptx::tmem_st8(tmem + lane_addr + col, *reinterpret_cast<const uint32_t(*)[8]>(pk));
-                ptx::tmem_st_wait();
-                ptx::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&p_full[buf]);
-                if (tr) trace(4 * s_cnt + 3);
-            }
-        }
-    } else if (!SPA && warp >= 4 && warp < 4 + C::kSilu) {
-        // ------------------------------------------------ SiLU warps
-        constexpr int CPW = C::CPW;
-        constexpr int CPW2 = BKV / 2;
-        const uint32_t q = warp & 3;
-        const uint32_t slice = (warp - 4) >> 2;
-        const uint32_t grp = slice >> 1, half = slice & 1;
-        const uint32_t m = q * 32 + lane;        // MMA row == TMEM lane
-        const uint32_t lane_addr = (q * 32u) << 16;
-        uint32_t s_cnt = 0;
-        for (int t = blockIdx.x; t < prm.n_tiles; t += gridDim.x) {
-            const AttnTile tile = prm.tiles[t];
-            const int n_kv = (tile.kmax + BKV - 1) / BKV;
-            const int hs = m / prm.rt;
-            const int i = m - hs * prm.rt;
-            const int prefix = i < tile.n_rows ? __ldg(prm.q_prefix + tile.q_row0 + i) : 0;
-            for (int j = 0; j < n_kv; ++j, ++s_cnt) {
-                // key tile s_cnt belongs to phase group s_cnt & 1 (S/P buffer = group)
-                if ((s_cnt & 1u) != grp) continue;
-                const uint32_t buf = grp;
-                const uint32_t par = (s_cnt >> 1) & 1;
-                const bool tr = (warp == 4 || warp == 12) && s_cnt < 128;
-                if (tr) trace(4 * s_cnt + 0);
-                ptx::mbar_wait(&s_full[buf], par);
-                if (tr) trace(4 * s_cnt + 1);
-                ptx::tc_fence_after();
-                uint32_t packed[CPW2 / 2];
-#pragma unroll
-                for (int c = 0; c < CPW2 / CPW; ++c) {
-                    const int col0 = half * CPW2 + c * CPW;         // key column within the tile
-                    const int nvalid = prefix - (j * BKV + col0);   // >= CPW: no masking needed
-                    float v[CPW];
-#pragma unroll
-                    for (int k = 0; k < CPW / 16; ++k)
-                        ptx::tmem_ld16(tmem + lane_addr + C::S_COL + buf * BKV + col0 + k * 16,
-                                       *reinterpret_cast<float(*)[16]>(v + k * 16));
-                    ptx::tmem_ld_wait();
-                    if (c == CPW2 / CPW - 1) {
-                        ptx::tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) ptx::mbar_arrive(&s_empty[buf]);
-                    }
-                    uint32_t* pk = packed + c * (CPW / 2);
-                    if (__all_sync(0xffffffffu, nvalid >= CPW)) {
-#pragma unroll
-                        for (int e = 0; e < CPW; e += 2)
-                            pk[e / 2] = ((e / 2) * EMU) % 16 < EMU ? ptx::silu2_bf16_fma(v[e], v[e + 1])
-                                                                   : attn_detail::silu2_bf16(v[e], v[e + 1]);
-                    } else if (__all_sync(0xffffffffu, nvalid <= 0)) {
-#pragma unroll
-                        for (int e = 0; e < CPW / 2; ++e) pk[e] = 0u;
-                    } else {
-#pragma unroll
-                        for (int e = 0; e < CPW; e += 2) {
-                            const uint32_t w = attn_detail::silu2_bf16(v[e], v[e + 1]);
-                            const uint32_t keep = (e + 1 < nvalid) ? 0xffffffffu : (e < nvalid ? 0x0000ffffu : 0u);
-                            pk[e / 2] = w & keep;
-                        }
-                    }
-                }
-                if (tr) trace(4 * s_cnt + 2);
-                ptx::mbar_wait(&p_empty[buf], par ^ 1);
-                if (tr) trace(4 * s_cnt + 3);
-                ptx::tc_fence_after();
-                {
-                    const uint32_t pa = tmem + lane_addr + C::P_COL + buf * (BKV / 2) + half * (CPW2 / 2);
-#pragma unroll
-                    for (int k = 0; k < CPW2 / 32; ++k)
-                        ptx::tmem_st16(pa + 16 * k, *reinterpret_cast<const uint32_t(*)[16]>(packed + 16 * k));
-                }
                 ptx::tmem_st_wait();
                 ptx::tc_fence_before();
                 __syncwarp();

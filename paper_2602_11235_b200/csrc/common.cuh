@@ -37,14 +37,6 @@ __device__ __forceinline__ void pdl_trigger() {
         ::mtfm::pdl_trigger(); \
     } while (0)
 
-inline bool pdl_enabled() {  // MTFM_PDL=0 switches it off (A/B timing)
-    static const bool on = [] {
-        const char* e = std::getenv("MTFM_PDL");
-        return e == nullptr || std::atoi(e) != 0;
-    }();
-    return on;
-}
-
 template <typename... KArgs, typename... Args>
 inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
     cudaLaunchConfig_t cfg = {};
@@ -56,7 +48,7 @@ inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 

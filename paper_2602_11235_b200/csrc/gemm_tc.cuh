@@ -2,22 +2,9 @@
 //
 //   C[m, n] = epilogue( sum_k A[m, k] * Bt[n, k] + bias[n] )
 //
-// Bt: bf16 row-major [N][K] (the weight pre-transposed at upload, K-major),
-// always TMA-loaded. A (128 x 64 bf16 per k-block, SW128 K-major in SMEM)
-// comes from one of three producers (GemmArgs::a_mode, uniform per launch):
-//   A_TMA  : a bf16 row-major matrix, TMA-loaded.
-//   A_LN   : group LayerNorm fused in (hta.hpp:104-109): four producer warps
-//            read fp32 X rows and write bf16((x - mu) * rstd * gain[g] +
-//            bias[g]) straight into the swizzled stage (mu/rstd from a row
-//            stats pass), so the normalised activations never touch HBM.
-//   A_GATE : the gate of hta.hpp:153/179 fused in: bf16(gln(A) * U) from the
-//            attention output A and the U projection, both bf16.
-//   A_GATE_TMA : the same gate, but A and U k-blocks are TMA-loaded into the
-//            stage and four transform warps rewrite the A block in place
-//            (SMEM -> SMEM, no exposed global latency) before the MMA.
-//   A_AFFINE_TMA : A = bf16(xhat * gain[g] + bias[g]) from a TMA-loaded bf16
-//            xhat (the layer-independent normalised rows): one normalised copy
-//            serves the GLN1 of every layer that reads the same rows.
+// Bt: bf16 row-major [N][K] (the weight pre-transposed at upload, K-major) and
+// A: bf16 row-major [M][K], both TMA-loaded (128 x 64 / BN x 64 per k-block,
+// SW128 K-major in SMEM).
 // One launch serves up to kMaxProblems independent problems (tokenizer
 // sources, fkv+fuq of a target layer, ...): the persistent CTAs walk one
 // global tile list, tile t -> (problem, m-block, n-block), n fastest, so the
@@ -25,7 +12,7 @@
 //
 // Roles (512 threads): warp 15 MMA issuer (one elected lane), warp 14 TMA,
 // warp 13 TMEM allocator, warps 0..7 (0..11) epilogue (warp & 3 = TMEM lane
-// quarter), warps 8..11 A-transform producers. The single-thread roles sit at
+// quarter). The single-thread roles sit at
 // the highest warp ids because the issue arbiter favours higher ids.
 // Pipelines: kStages SMEM stages (full/empty mbarriers) and 2 TMEM
 // accumulator stages (tmem_full/empty), so the epilogue of tile i overlaps
@@ -45,27 +32,17 @@ enum GemmEpi : int {
     EPI_BIAS_BF16 = 3,   // out_bf16[m][n] = acc + bias
 };
 
-enum GemmAMode : int { A_TMA = 0, A_LN = 1, A_GATE = 2, A_GATE_TMA = 3, A_AFFINE_TMA = 4 };
 
 constexpr int kMaxProblems = 16;
 
 struct GemmProblem {
-    CUtensorMap tma_a;      // box {64, 128} (2D) or {64, 128, stage_kb} (3D k-block view), SW128 (A_TMA, A_GATE_TMA)
-    CUtensorMap tma_u;      // A_GATE_TMA: U rows, box {64, 128}, SW128
+    CUtensorMap tma_a;      // box {64, 128} (2D) or {64, 128, stage_kb} (3D k-block view), SW128
     CUtensorMap tma_b;      // box {64, BN} or {64, BN, stage_kb}, SW128
-    CUtensorMap tma_b_half; // cluster2: box {64, BN/2}, SW128 (each CTA of a pair loads and multicasts one half)
     CUtensorMap tma_c;      // output, box {32, 32}: bf16 SW64 / f32 SW128 (use_tma_c)
     int use_tma_c;          // plain row-major output rows [0, M): bulk-tensor stores
     int use_tma_r;          // EPI_RESID_F32 with resid == out: residual blocks TMA-prefetched via tma_c
     int use_scatter_c;      // bf16 output through row_map: staged like use_tma_c, then 128-byte row-segment stores
-    // use_scatter_c only: columns [seg_n0[i], next) go to seg_out[i] (ld seg_ldo[i]) at column - seg_n0[i];
-    // segment 0 is (0, out, ldo). Lets problems sharing A rows share one launch slot (A read once).
-    int n_seg;
-    int seg_n0[4];
-    void* seg_out[4];
-    long long seg_ldo[4];
     int M, N, K;            // K padded to a multiple of 64
-    int Kv;                 // true K (columns of a_src / gain rows)
     int tile_start;         // first global tile of this problem
     int tiles_n;
     int epi;
@@ -76,17 +53,6 @@ struct GemmProblem {
     const int* row_map;     // optional output row indirection (f32 epilogues)
     long long row_offset;   // added to the output row when row_map is null
     const float* resid;     // EPI_RESID_F32
-    // transform producers (A_LN / A_GATE)
-    const void* a_src;      // fp32 X (A_LN) or bf16 attention output (A_GATE)
-    long long lda;
-    long long a_row0;       // GEMM row m reads a_src / stats row m + a_row0
-    const float2* stats;    // (mean, rstd) per a_src row
-    const int* row_group;   // GLN group per row, indexed m + g_row0
-    long long g_row0;
-    const float* gain;      // [groups][K]
-    const float* gbias;     // [groups][K]
-    const __nv_bfloat16* u_src;  // A_GATE: U rows (m), ldu
-    long long ldu;
 };
 
 // B-resident schedule: CTA b owns (problem pi, n-block nb) for the whole launch,
@@ -99,19 +65,14 @@ struct CtaWork {
 struct GemmArgs {
     int n_problems;
     int n_tiles;
-    int a_mode;
     int b_res;        // 1: B-resident schedule (cta[]), 0: streaming over the global tile list
     int n_stages;     // SMEM pipeline stages
     int stage_kb;     // k-blocks per stage: > 1 only when every K is a multiple of 64 (3D tensor maps, one TMA per stage)
     int stage_bytes;  // stage_kb x (A_BYTES (+ B_BYTES when streaming B)) (+ bias tile)
     int bres_bytes;   // resident B slice bytes (b_res)
-    int n_epi;        // epilogue warps: 8, or 12 when A comes from TMA (warps 12..15 free)
+    int n_epi;        // epilogue warps: 8, or 12 when BN < 256 (more accumulators than 2 groups)
     int stg_warp;     // epilogue staging bytes per warp: 8 KB (2 fp32 blocks), 4 KB when every problem is a bf16 bulk store
     int bias_bytes;   // BN x 32 B bias tile: after the resident B slice (b_res) or at the end of every stage
-    int cluster2;     // streaming with CTA pairs (cluster of 2): the pair takes m-blocks 2j, 2j+1 of one
-                      // (problem, n-block) and each CTA multicasts half of every B k-block to both
-    unsigned long long* trace;  // timing experiments only: CTA 0 clock64 stamps (MTFM_GEMM_TRACE)
-    int debug;        // timing experiments only: 1 no stores, 2 no SiLU, 8 no A loads, 16 no MMAs, 32 epilogue handshakes only
     GemmProblem p[kMaxProblems];
     CtaWork cta[kNumSMs];
 };
@@ -121,32 +82,27 @@ namespace gemm_detail {
 template <int BN>
 struct Cfg {
     static constexpr int BM = 128, BK = 64;
-    static constexpr int kStages = BN >= 256 ? 3 : (BN >= 128 ? 5 : 6);  // streaming schedule
     static constexpr int A_BYTES = BM * BK * 2;
     static constexpr int B_BYTES = BN * BK * 2;
-    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int kAcc = BN >= 256 ? 2 : 4;  // TMEM accumulator buffers
     static constexpr int TMEM_COLS = kAcc * BN <= 32 ? 32 : (kAcc * BN <= 64 ? 64 : (kAcc * BN <= 128 ? 128 : (kAcc * BN <= 256 ? 256 : 512)));
     static constexpr int STG_WARP = 2 * 32 * 32 * 4;  // per epilogue warp: 2 x (32 rows x 32 fp32)
     static constexpr int BAR_BYTES = 1024;  // mbarriers, TMEM slot, per-problem tables
-    static constexpr int SMEM = kStages * STAGE_BYTES + 8 * STG_WARP + 1024 /*align*/ + BAR_BYTES;
     static constexpr int kMaxSmem = 227 * 1024;
     static constexpr int kThreads = 512;
-    static_assert(SMEM <= kMaxSmem, "SMEM budget");
 };
 
 // The tile sequence of this CTA (identical for every role).
 // B-resident: the CTA's (problem, n-block, m-blocks) held in registers;
 // streaming: global tile t -> (problem, m, n) through the SMEM tile_start table.
 struct TileSeq {
-    int t, i, tstep, pair, rank;
+    int t, i, tstep;
     int b_res, pi0, nb0, m0, mstep, mcount, n_tiles, n_problems;
     const int* tile_start;  // SMEM: first global tile of each problem
     const int* tiles_n;     // SMEM: n-blocks of each problem
     __device__ TileSeq(const GemmArgs& a, const int* ts, const int* tn)
-        : t(a.cluster2 ? blockIdx.x >> 1 : blockIdx.x), i(0), tstep(a.cluster2 ? gridDim.x >> 1 : gridDim.x),
-          pair(a.cluster2), rank(a.cluster2 ? static_cast<int>(blockIdx.x & 1) : 0), b_res(a.b_res),
-          n_tiles(a.n_tiles), n_problems(a.n_problems), tile_start(ts), tiles_n(tn) {
+        : t(blockIdx.x), i(0), tstep(gridDim.x), b_res(a.b_res), n_tiles(a.n_tiles), n_problems(a.n_problems),
+          tile_start(ts), tiles_n(tn) {
         const CtaWork w = a.cta[blockIdx.x];
         pi0 = w.pi;
         nb0 = w.nb;
@@ -154,8 +110,7 @@ struct TileSeq {
         mstep = w.mstep;
         mcount = w.mcount;
     }
-    template <typename Decode>
-    __device__ __forceinline__ bool next(const GemmArgs&, Decode, int& pi, int& mb, int& nb) {
+    __device__ __forceinline__ bool next(int& pi, int& mb, int& nb) {
         if (b_res) {
             if (i >= mcount) return false;
             pi = pi0;
@@ -172,98 +127,10 @@ struct TileSeq {
         const int local = t - tile_start[pi];
         mb = local / tiles_n[pi];
         nb = local - mb * tiles_n[pi];
-        if (pair) mb = 2 * mb + rank;  // pair tile -> this CTA's m-block
         t += tstep;
         return true;
     }
 };
-
-__device__ __forceinline__ void decode_tile(const GemmArgs& a, int t, int& pi, int& mb, int& nb) {
-    pi = 0;
-#pragma unroll 1
-    for (int i = 1; i < a.n_problems; ++i)
-        if (t >= a.p[i].tile_start) pi = i;
-    const int local = t - a.p[pi].tile_start;
-    mb = local / a.p[pi].tiles_n;
-    nb = local - mb * a.p[pi].tiles_n;
-}
-
-__device__ __forceinline__ void unpack8(const uint4 u, float (&f)[8]) {
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const float2 t = __bfloat1622float2(h[i]);
-        f[2 * i] = t.x;
-        f[2 * i + 1] = t.y;
-    }
-}
-
-// Produces one 128 x 64 A k-block (SW128 K-major) from global memory with the
-// LayerNorm / gate transform. 128 producer threads, 8 x 16-byte chunks each;
-// one warp instruction covers 4 rows x 8 chunks (coalesced 256 B / 128 B rows).
-// Processed in two halves of 4 chunks to bound register use.
-__device__ __forceinline__ void produce_a(const GemmProblem& p, int mode, int m0, int k0, uint8_t* sa, int pt) {
-    const int c8 = pt & 7;
-    const int k = k0 + c8 * 8;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        float xv[4][8];
-        float2 st[4];
-        int grp[4];
-        bool ok[4];
-        // issue all loads of the half first (memory-level parallelism), then transform
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int r = (pt >> 3) + 16 * (4 * h + i);
-            const int m = m0 + r;
-            ok[i] = m < p.M && k < p.Kv;
-            if (ok[i]) {
-                const long long ar = m + p.a_row0;
-                st[i] = __ldg(p.stats + ar);
-                grp[i] = __ldg(p.row_group + m + p.g_row0);
-                if (mode == A_LN) {
-                    const float* x = static_cast<const float*>(p.a_src) + ar * p.lda + k;
-                    const float4 a = __ldcs(reinterpret_cast<const float4*>(x));
-                    const float4 b = __ldcs(reinterpret_cast<const float4*>(x + 4));
-                    xv[i][0] = a.x; xv[i][1] = a.y; xv[i][2] = a.z; xv[i][3] = a.w;
-                    xv[i][4] = b.x; xv[i][5] = b.y; xv[i][6] = b.z; xv[i][7] = b.w;
-                } else {
-                    const uint4 a = __ldcs(reinterpret_cast<const uint4*>(
-                        static_cast<const __nv_bfloat16*>(p.a_src) + ar * p.lda + k));
-                    unpack8(a, xv[i]);
-                }
-            }
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int r = (pt >> 3) + 16 * (4 * h + i);
-            uint4 outv = make_uint4(0, 0, 0, 0);
-            if (ok[i]) {
-                const int g = grp[i] < 0 ? 0 : grp[i];
-                const float* gp = p.gain + (long long)g * p.Kv + k;
-                const float* bp = p.gbias + (long long)g * p.Kv + k;
-                const float4 ga = __ldg(reinterpret_cast<const float4*>(gp));
-                const float4 gb = __ldg(reinterpret_cast<const float4*>(gp + 4));
-                const float4 ba = __ldg(reinterpret_cast<const float4*>(bp));
-                const float4 bb = __ldg(reinterpret_cast<const float4*>(bp + 4));
-                const float gv[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
-                const float bv[8] = {ba.x, ba.y, ba.z, ba.w, bb.x, bb.y, bb.z, bb.w};
-                float y[8];
-#pragma unroll
-                for (int e = 0; e < 8; ++e) y[e] = ((xv[i][e] - st[i].x) * st[i].y) * gv[e] + bv[e];
-                if (mode == A_GATE) {
-                    float u[8];
-                    unpack8(__ldg(reinterpret_cast<const uint4*>(p.u_src + (long long)(m0 + r) * p.ldu + k)), u);
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) y[e] *= u[e];
-                }
-                outv = make_uint4(pack_bf16(y[0], y[1]), pack_bf16(y[2], y[3]), pack_bf16(y[4], y[5]),
-                                  pack_bf16(y[6], y[7]));
-            }
-            *reinterpret_cast<uint4*>(sa + (r >> 3) * 1024 + (r & 7) * 128 + ((c8 ^ (r & 7)) << 4)) = outv;
-        }
-    }
-}
 
 }  // namespace gemm_detail
 
@@ -286,7 +153,6 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
     uint64_t* res_bar = tempty_bar + 4;  // [12 epilogue warps][2 staging buffers]
     uint64_t* bres_bar = res_bar + 24;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres_bar + 1);
-    uint64_t* raw_bar = bres_bar + 2;  // [8] A_GATE_TMA: raw A|U k-block landed
     int* s_tile_start = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(full_bar) + 512);
     int* s_tiles_n = s_tile_start + kMaxProblems;
     int* s_kblocks = s_tiles_n + kMaxProblems;
@@ -307,34 +173,16 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
 
     const uint32_t warp = ptx::warp_id();
     const uint32_t lane = ptx::lane_id();
-    const int a_mode = args.a_mode;
-#ifdef MTFM_GEMM_TRACE
-    constexpr bool kTrace = true;   // timing experiments: build with -DMTFM_GEMM_TRACE
-#else
-    constexpr bool kTrace = false;
-#endif
-    auto trace = [&](int slot) {
-        if (kTrace && args.trace && blockIdx.x == 0 && lane == 0) args.trace[slot] = clock64();
-    };
-    if (threadIdx.x == 0) trace(0);
     // Warp roles. The issue arbiter favours higher warp ids, so the latency-
     // critical single-thread roles sit at the top: 15 MMA issuer, 14 TMA
     // producer, 13 TMEM allocator; epilogue warps 0..n_epi-1 (warp & 3 = TMEM
-    // lane quarter); 8..11 A-transform producers when A is not TMA-loaded.
+    // lane quarter).
     constexpr uint32_t kWarpMma = 15, kWarpTma = 14, kWarpAlloc = 13;
-#ifdef MTFM_GEMM_TWO_MMA
-    constexpr bool kTwoMma = true;  // warp 13 (TMEM allocator) issues every other tile
-#else
-    constexpr bool kTwoMma = false;  // measured: no gain on the projections, halves the ring for K=512
-#endif
-    // two issuers only for TMA-loaded A (the transform producers walk one ring) and >= 4 stages
-    const bool two_mma = kTwoMma && a_mode == A_TMA && n_stages >= 4;
 
     if (warp == kWarpTma && lane == 0) {
         for (int s = 0; s < n_stages; ++s) {
-            ptx::mbar_init(&full_bar[s], a_mode == A_TMA ? 1 : (a_mode >= A_GATE_TMA ? 4 : 1 + 4));
-            ptx::mbar_init(&empty_bar[s], args.cluster2 ? 2 : 1);  // cluster2: both CTAs' MMAs release the stage
-            ptx::mbar_init(&raw_bar[s], 1);
+            ptx::mbar_init(&full_bar[s], 1);
+            ptx::mbar_init(&empty_bar[s], 1);
         }
         ptx::mbar_init(bres_bar, 1);
         for (int s = 0; s < C::kAcc; ++s) {
@@ -344,8 +192,7 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
         for (int s = 0; s < 24; ++s) ptx::mbar_init(&res_bar[s], 1);
         ptx::fence_mbar_init();
         for (int i = 0; i < args.n_problems; ++i) {
-            if (a_mode == A_TMA || a_mode >= A_GATE_TMA) ptx::tma_prefetch(&args.p[i].tma_a);
-            if (a_mode == A_GATE_TMA) ptx::tma_prefetch(&args.p[i].tma_u);
+            ptx::tma_prefetch(&args.p[i].tma_a);
             ptx::tma_prefetch(&args.p[i].tma_b);
         }
     }
@@ -353,14 +200,12 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
-    if (args.cluster2) ptx::cluster_sync();  // the peer's barriers are initialised before any multicast
     const uint32_t tmem_base = *tmem_slot;
-    if (threadIdx.x == 0) trace(1);    // prologue done (barriers, TMEM, SMEM tables): wait for the producer of our inputs
+    // prologue done (barriers, TMEM, SMEM tables): wait for the producer of our inputs
     MTFM_PDL_ENTRY();
 
-
     if (warp == kWarpTma) {
-        // ------------------------------------------------ TMA producer (B, and A in A_TMA mode)
+        // ------------------------------------------------ TMA producer (A and B)
         if (ptx::elect_one()) {
             if (args.b_res && args.cta[blockIdx.x].mcount > 0) {
                 // resident weight slice: every k-block of this CTA's (problem, n-block), once
@@ -372,156 +217,29 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                     ptx::tma_load_2d(bres + kb * C::B_BYTES, &p.tma_b, bres_bar, kb * C::BK, w.nb * BN);
                 if (p.has_bias) ptx::tma_load_2d(bres + kblocks * C::B_BYTES, &p.tma_bias, bres_bar, 0, w.nb * BN);
             }
-            // ring half r = tile % 2 when two MMA warps issue (see the MMA role), else one ring
-            int st_r[2] = {0, two_mma ? n_stages / 2 : 0};
-            uint32_t ph_r[2] = {0, 0};
-            const int ring_n = two_mma ? n_stages / 2 : n_stages;
-            int ntile = 0;
-            gemm_detail::TileSeq seq(args, s_tile_start, s_tiles_n);
-            int pi, mb, nb;
-            while (seq.next(args, gemm_detail::decode_tile, pi, mb, nb)) {
-                const int ring = two_mma ? (ntile & 1) : 0;
-                const int ring0 = ring * (two_mma ? n_stages / 2 : 0);
-                int& stage = st_r[ring];
-                uint32_t& phase = ph_r[ring];
-                const GemmProblem& p = args.p[pi];
-                const int kblocks = s_kblocks[pi];
-                const bool p_bias = s_has_bias[pi];
-                if (ntile < 64) trace(320 + ntile);
-                ++ntile;
-                for (int kb = 0; kb < kblocks; kb += KS) {
-                    ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
-                    if (ntile - 1 < 8 && kb < 8) trace(640 + (ntile - 1) * 16 + kb);
-                    uint8_t* sa = smem + stage * stage_bytes;
-                    uint8_t* sb = sa + KS * C::A_BYTES;
-                    const bool skip_a = args.debug & 8;  // timing experiment: no A loads
-                    const bool bias_here = !args.b_res && p_bias && kb + KS >= kblocks;  // streaming: bias tile with the last stage
-                    if (a_mode >= A_GATE_TMA) {
-                        // raw A (and U) k-blocks (+ B when streaming) -> raw_bar; the transform
-                        // warps rewrite A in place and arrive on full_bar
-                        const int na = a_mode == A_GATE_TMA ? 2 : 1;
-                        uint8_t* sbg = sa + na * C::A_BYTES;
-                        ptx::mbar_arrive_expect_tx(&raw_bar[stage], na * C::A_BYTES + (args.b_res ? 0 : C::B_BYTES) +
-                                                                        (bias_here ? BN * 32 : 0));
-                        ptx::tma_load_2d(sa, &p.tma_a, &raw_bar[stage], kb * C::BK, mb * C::BM);
-                        if (na == 2) ptx::tma_load_2d(sa + C::A_BYTES, &p.tma_u, &raw_bar[stage], kb * C::BK, mb * C::BM);
-                        if (!args.b_res) ptx::tma_load_2d(sbg, &p.tma_b, &raw_bar[stage], kb * C::BK, nb * BN);
-                        if (bias_here) ptx::tma_load_2d(sbg + C::B_BYTES, &p.tma_bias, &raw_bar[stage], 0, nb * BN);
-                        if (++stage == ring0 + ring_n) {
-                            stage = ring0;
-                            phase ^= 1;
-                        }
-                        continue;
-                    }
-                    const int bytes = (a_mode == A_TMA && !skip_a ? KS * C::A_BYTES : 0) +
-                                      (args.b_res ? 0 : KS * C::B_BYTES) + (bias_here ? BN * 32 : 0);
-                    if (bytes > 0)
-                        ptx::mbar_arrive_expect_tx(&full_bar[stage], bytes);
-                    else
-                        ptx::mbar_arrive(&full_bar[stage]);
-                    // one TMA instruction per operand and stage (each costs ~150 clk of issue)
-                    if (a_mode == A_TMA && !skip_a) {
-                        if (KS > 1) ptx::tma_load_3d(sa, &p.tma_a, &full_bar[stage], 0, mb * C::BM, kb);
-                        else ptx::tma_load_2d(sa, &p.tma_a, &full_bar[stage], kb * C::BK, mb * C::BM);
-                    }
-                    if (args.cluster2) {
-                        // our half of the B k-block, into both CTAs of the pair (KS == 1)
-                        const int h = static_cast<int>(blockIdx.x & 1);
-                        ptx::tma_load_2d_mc(sb + h * (BN / 2) * 128, &p.tma_b_half, &full_bar[stage], kb * C::BK,
-                                            nb * BN + h * (BN / 2), 0x3);
-                    } else if (!args.b_res) {
-                        if (KS > 1) ptx::tma_load_3d(sb, &p.tma_b, &full_bar[stage], 0, nb * BN, kb);
-                        else ptx::tma_load_2d(sb, &p.tma_b, &full_bar[stage], kb * C::BK, nb * BN);
-                    }
-                    if (bias_here) ptx::tma_load_2d(sb + KS * C::B_BYTES, &p.tma_bias, &full_bar[stage], 0, nb * BN);
-                    if (++stage == ring0 + ring_n) {
-                        stage = ring0;
-                        phase ^= 1;
-                    }
-                }
-            }
-        }
-    } else if (warp >= 8 && warp < 12 && a_mode >= A_GATE_TMA) {
-        // ------------------------------------------------ gate transform, SMEM -> SMEM
-        // thread = tile row: its 8 A chunks and 8 U chunks (SW128: chunk c of row r
-        // at (c ^ (r & 7))) -> bf16(((a - mu) * rstd * gain[g] + bias[g]) * u) in place
-        const int r = static_cast<int>((warp - 8) * 32 + lane);
-        int stage = 0;
-        uint32_t phase = 0;
-        gemm_detail::TileSeq seq(args, s_tile_start, s_tiles_n);
-        int pi, mb, nb;
-        while (seq.next(args, gemm_detail::decode_tile, pi, mb, nb)) {
-            const GemmProblem& p = args.p[pi];
-            const int kblocks = s_kblocks[pi];
-            const int m = mb * C::BM + r;
-            const bool ok = m < p.M;
-            const bool gate = a_mode == A_GATE_TMA;
-            float2 st = make_float2(0.f, 1.f);
-            int g = 0;
-            if (ok) {
-                if (gate) st = __ldg(p.stats + m + p.a_row0);
-                g = __ldg(p.row_group + m + p.g_row0);
-                g = g < 0 ? 0 : g;
-            }
-            for (int kb = 0; kb < kblocks; ++kb) {
-                ptx::mbar_wait(&raw_bar[stage], phase);
-                uint8_t* sa = smem + stage * stage_bytes;
-                if (ok) {
-                    uint8_t* arow = sa + r * 128;
-                    const uint8_t* urow = sa + C::A_BYTES + r * 128;
-                    const float* gp = p.gain + (long long)g * p.Kv + kb * C::BK;
-                    const float* bp = p.gbias + (long long)g * p.Kv + kb * C::BK;
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        const int off = (c ^ (r & 7)) << 4;
-                        float a8[8], u8[8];
-                        gemm_detail::unpack8(*reinterpret_cast<const uint4*>(arow + off), a8);
-                        if (gate) {
-                            gemm_detail::unpack8(*reinterpret_cast<const uint4*>(urow + off), u8);
-                        } else {
-#pragma unroll
-                            for (int e = 0; e < 8; ++e) u8[e] = 1.f;
-                        }
-                        const float4 g0 = __ldg(reinterpret_cast<const float4*>(gp + 8 * c));
-                        const float4 g1 = __ldg(reinterpret_cast<const float4*>(gp + 8 * c + 4));
-                        const float4 b0 = __ldg(reinterpret_cast<const float4*>(bp + 8 * c));
-                        const float4 b1 = __ldg(reinterpret_cast<const float4*>(bp + 8 * c + 4));
-                        const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-                        const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-                        float y[8];
-#pragma unroll
-                        for (int e = 0; e < 8; ++e) y[e] = (((a8[e] - st.x) * st.y) * gv[e] + bv[e]) * u8[e];
-                        *reinterpret_cast<uint4*>(arow + off) =
-                            make_uint4(pack_bf16(y[0], y[1]), pack_bf16(y[2], y[3]), pack_bf16(y[4], y[5]),
-                                       pack_bf16(y[6], y[7]));
-                    }
-                }
-                ptx::fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&full_bar[stage]);
-                if (++stage == n_stages) {
-                    stage = 0;
-                    phase ^= 1;
-                }
-            }
-        }
-    } else if (warp >= 8 && warp < 12 && a_mode != A_TMA) {
-        // ------------------------------------------------ A-transform producers
-        {
-            const int pt = (warp - 8) * 32 + lane;
             int stage = 0;
             uint32_t phase = 0;
             gemm_detail::TileSeq seq(args, s_tile_start, s_tiles_n);
             int pi, mb, nb;
-            while (seq.next(args, gemm_detail::decode_tile, pi, mb, nb)) {
+            while (seq.next(pi, mb, nb)) {
                 const GemmProblem& p = args.p[pi];
                 const int kblocks = s_kblocks[pi];
-                for (int kb = 0; kb < kblocks; ++kb) {
+                const bool p_bias = s_has_bias[pi];
+                for (int kb = 0; kb < kblocks; kb += KS) {
                     ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
-                    gemm_detail::produce_a(p, a_mode, mb * C::BM, kb * C::BK, smem + stage * stage_bytes, pt);
-                    ptx::fence_proxy_async_smem();
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(&full_bar[stage]);
+                    uint8_t* sa = smem + stage * stage_bytes;
+                    uint8_t* sb = sa + KS * C::A_BYTES;
+                    const bool bias_here = !args.b_res && p_bias && kb + KS >= kblocks;  // streaming: bias tile with the last stage
+                    const int bytes = KS * C::A_BYTES + (args.b_res ? 0 : KS * C::B_BYTES) + (bias_here ? BN * 32 : 0);
+                    ptx::mbar_arrive_expect_tx(&full_bar[stage], bytes);
+                    // one TMA instruction per operand and stage (each costs ~150 clk of issue)
+                    if (KS > 1) ptx::tma_load_3d(sa, &p.tma_a, &full_bar[stage], 0, mb * C::BM, kb);
+                    else ptx::tma_load_2d(sa, &p.tma_a, &full_bar[stage], kb * C::BK, mb * C::BM);
+                    if (!args.b_res) {
+                        if (KS > 1) ptx::tma_load_3d(sb, &p.tma_b, &full_bar[stage], 0, nb * BN, kb);
+                        else ptx::tma_load_2d(sb, &p.tma_b, &full_bar[stage], kb * C::BK, nb * BN);
+                    }
+                    if (bias_here) ptx::tma_load_2d(sb + KS * C::B_BYTES, &p.tma_bias, &full_bar[stage], 0, nb * BN);
                     if (++stage == n_stages) {
                         stage = 0;
                         phase ^= 1;
@@ -529,64 +247,39 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                 }
             }
         }
-    } else if (warp == kWarpMma || (two_mma && warp == kWarpAlloc)) {
-        // ------------------------------------------------ MMA issuers (one elected lane per k-block)
-        // Two issuing warps take alternate tiles (own accumulators, own stages of
-        // the shared ring): one thread issues a tcgen05.mma only every ~90 clk,
-        // short of the 64 clk an N=128 MMA occupies the tensor pipe.
-        // Each issuer owns half of the SMEM ring (the producer fills tile j into half
-        // j % 2), so the two never share a stage.
-        const int mma_id = warp == kWarpMma ? 0 : 1;
-        const int n_mma = two_mma ? 2 : 1;
-        const int ring0 = two_mma ? mma_id * (n_stages / 2) : 0;
-        const int ring_n = two_mma ? n_stages / 2 : n_stages;
+    } else if (warp == kWarpMma) {
+        // ------------------------------------------------ MMA issuer (one elected lane per stage)
         const uint32_t idesc = ptx::instr_desc_bf16(128, BN, false, false);
-        int stage = ring0;
+        int stage = 0;
         uint32_t phase = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
         bool bres_ready = false;
-        int ntile = 0;
         gemm_detail::TileSeq seq(args, s_tile_start, s_tiles_n);
         int pi, mb, nb;
-        for (int jt = 0; seq.next(args, gemm_detail::decode_tile, pi, mb, nb); ++jt) {
+        while (seq.next(pi, mb, nb)) {
             const int kblocks = s_kblocks[pi];
-            if (jt % n_mma != mma_id) {
-                // the other issuer's tile (its own half of the ring): advance the accumulator only
-                if (++acc == C::kAcc) {
-                    acc = 0;
-                    acc_phase ^= 1;
-                }
-                continue;
-            }
             if (args.b_res && !bres_ready) {
                 ptx::mbar_wait(bres_bar, 0);
                 bres_ready = true;
-                trace(2);
             }
             // the epilogue hands every accumulator back, including before its first use
             ptx::mbar_wait(&tempty_bar[acc], acc_phase);
             ptx::tc_fence_after();
-            if (ntile < 64) trace(64 + ntile);
             const uint32_t d_tmem = tmem_base + acc * BN;
             const bool has_bias = s_has_bias[pi];
             for (int kb0 = 0; kb0 < kblocks; kb0 += KS) {
                 // TMA -> MMA is async-proxy to async-proxy through the mbarrier
                 ptx::mbar_wait(&full_bar[stage], phase);
-                const int kb = kb0;
-                if (a_mode != A_TMA) ptx::tc_fence_after();  // generic-proxy producers (fence.proxy.async on their side)
-                if (ntile < 8 && kb < 8) trace(512 + ntile * 16 + kb * 2);
                 const int nk = min(KS, kblocks - kb0);
                 const bool last = kb0 + KS >= kblocks;
                 if (ptx::elect_one()) {
                     const uint32_t sa0 = ptx::smem_u32(smem + stage * stage_bytes);
-                    const uint32_t sb0 = args.b_res ? ptx::smem_u32(bres + kb0 * C::B_BYTES)
-                                                    : sa0 + KS * C::A_BYTES * (a_mode == A_GATE_TMA ? 2 : 1);
+                    const uint32_t sb0 = args.b_res ? ptx::smem_u32(bres + kb0 * C::B_BYTES) : sa0 + KS * C::A_BYTES;
                     for (int kbi = 0; kbi < nk; ++kbi) {
                         const uint32_t sa = sa0 + kbi * C::A_BYTES, sb = sb0 + kbi * C::B_BYTES;
 #pragma unroll
                         for (int k = 0; k < C::BK / 16; ++k) {
-                            if (args.debug & 16) break;  // timing experiment: no MMAs
                             const uint64_t da = ptx::smem_desc(sa + k * 32, 16, 1024, 2);
                             const uint64_t db = ptx::smem_desc(sb + k * 32, 16, 1024, 2);
                             ptx::umma_bf16(d_tmem, da, db, idesc, ((kb0 | kbi | k) != 0) ? 1u : 0u);
@@ -599,19 +292,15 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                         ptx::umma_bf16(d_tmem, ptx::smem_desc(ptx::smem_u32(ones), 16, 256, 6),
                                        ptx::smem_desc(sbias, 16, 256, 6), idesc, 1u);
                     }
-                    if (args.cluster2) ptx::umma_commit_mc(&empty_bar[stage], 0x3);
-                    else ptx::umma_commit(&empty_bar[stage]);
+                    ptx::umma_commit(&empty_bar[stage]);
                     if (last) ptx::umma_commit(&tfull_bar[acc]);
                 }
                 __syncwarp();
-                if (ntile < 8 && kb < 8) trace(512 + ntile * 16 + kb * 2 + 1);
-                if (++stage == ring0 + ring_n) {
-                    stage = ring0;
+                if (++stage == n_stages) {
+                    stage = 0;
                     phase ^= 1;
                 }
             }
-            if (ntile < 64) trace(128 + ntile);
-            ++ntile;
             if (++acc == C::kAcc) {
                 acc = 0;
                 acc_phase ^= 1;
@@ -637,18 +326,12 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
         uint32_t nstore = 0;                            // staging buffers used by this warp
         uint32_t res_phase = 0;                         // parity bit per staging buffer
         uint64_t* my_res = res_bar + warp * 2;
-        int ntile = 0;
         // column unit per warp: 64 for bf16 bulk-stored outputs (128-byte rows), else 32
         auto unit_of = [&](const GemmProblem& pp) {
             return ((pp.epi == EPI_SILU_BF16 || pp.epi == EPI_BIAS_BF16) && (pp.use_tma_c || pp.use_scatter_c) &&
                     BN >= 64)
                        ? 64
                        : 32;
-        };
-        int fk = 0;  // fine-trace index within the tile
-        auto ftrace = [&]() {
-            if (warp == 0 && ntile < 8 && fk < 16) trace(384 + ntile * 16 + fk);
-            ++fk;
         };
         auto release = [&](int b) {
             ptx::tc_fence_before();
@@ -667,13 +350,11 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
         // accumulator j % kAcc, so n_groups tiles are drained concurrently while
         // the MMA warp runs up to kAcc tiles ahead.
         gemm_detail::TileSeq seq(args, s_tile_start, s_tiles_n);
-        {
-            // hand out the accumulators of the first kAcc tiles (each by the group that drains it)
-            for (int b = 0; b < C::kAcc; ++b)
-                if (b % n_groups == group) release(b);
-        }
+        // hand out the accumulators of the first kAcc tiles (each by the group that drains it)
+        for (int b = 0; b < C::kAcc; ++b)
+            if (b % n_groups == group) release(b);
         int pi, mb, nb;
-        for (int j = 0; seq.next(args, gemm_detail::decode_tile, pi, mb, nb); ++j) {
+        for (int j = 0; seq.next(pi, mb, nb); ++j) {
             if (j % n_groups != group) continue;
             acc = j % C::kAcc;
             acc_phase = (j / C::kAcc) & 1;
@@ -688,13 +369,10 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
             const int my_orow = (p.use_scatter_c && row0 + static_cast<int>(lane) < p.M) ? __ldg(p.row_map + row0 + lane) : -1;
             ptx::mbar_wait(&tfull_bar[acc], acc_phase);
             ptx::tc_fence_after();
-            if (warp == 0 && ntile < 64) trace(192 + ntile);
-            fk = 0;
 #pragma unroll 1
             for (; ci < kChunks; ci += step) {
                 const int c = ci * 32;
                 const int n0 = nb * BN + c;
-                if (args.debug & 32) continue;  // timing experiment: epilogue does nothing but the handshakes
                 if (bf16_out && (p.use_tma_c || p.use_scatter_c) && unit == 64) {
                     // ---- fast path: 64 columns -> bf16 (SiLU) -> one 32 x 128 B SW128 box
                     if (n0 >= p.N) continue;  // warp-uniform (TMEM reads below are all-or-nothing)
@@ -708,22 +386,19 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                         ptx::tmem_ld16(lane_base + acc * BN + c + 32 * hh, *reinterpret_cast<float(*)[16]>(v));
                         ptx::tmem_ld16(lane_base + acc * BN + c + 32 * hh + 16, *reinterpret_cast<float(*)[16]>(v + 16));
                         ptx::tmem_ld_wait();
-                        ftrace();
-                        if (p.epi == EPI_SILU_BF16 && !(args.debug & 2)) {
+                        if (p.epi == EPI_SILU_BF16) {
                             ptx::silu_bf16_batch<16>(v, w[hh]);
                         } else {
 #pragma unroll
                             for (int e = 0; e < 32; e += 2) w[hh][e / 2] = pack_bf16(v[e], v[e + 1]);
                         }
                     }
-                    ftrace();
                     // the bulk store that last read this staging buffer must be done with it
                     if (lane == 0) {
                         if (stg_single) ptx::bulk_wait_read<0>();
                         else ptx::bulk_wait_read<1>();
                     }
                     __syncwarp();
-                    ftrace();
 #pragma unroll
                     for (int k = 0; k < 8; ++k)
                         *reinterpret_cast<uint4*>(sb + ((k ^ (lane & 7)) << 4)) =
@@ -733,31 +408,21 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                         // row-mapped rows: 8 lanes per 128-byte row segment, 4 rows per pass
                         __syncwarp();
                         const uint8_t* s0 = reinterpret_cast<const uint8_t*>(stg);
-                        void* so = p.out;
-                        long long sld = p.ldo;
-                        int sn = n0;
-                        for (int si = p.n_seg - 1; si >= 1; --si)
-                            if (n0 >= p.seg_n0[si]) {
-                                so = p.seg_out[si];
-                                sld = p.seg_ldo[si];
-                                sn = n0 - p.seg_n0[si];
-                                break;
-                            }
 #pragma unroll
                         for (int it = 0; it < 8; ++it) {
                             const int r = it * 4 + sub;
                             const uint4 val = *reinterpret_cast<const uint4*>(s0 + r * 128 + ((ch ^ (r & 7)) << 4));
                             const int orow = __shfl_sync(0xffffffffu, my_orow, r);
                             if (orow >= 0)
-                                *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(so) +
-                                                          static_cast<long long>(orow) * sld + sn + ch * 8) = val;
+                                *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) +
+                                                          static_cast<long long>(orow) * p.ldo + n0 + ch * 8) = val;
                         }
                         ++nstore;
                         continue;
                     }
                     ptx::fence_proxy_async_smem();
                     __syncwarp();
-                    if (lane == 0 && !(args.debug & 1)) {
+                    if (lane == 0) {
                         ptx::tma_store_2d(&p.tma_c, stg, n0, row0);
                         ptx::bulk_commit();
                     }
@@ -808,7 +473,7 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                                 ptx::tmem_ld_wait();
                             }
                             uint32_t w[16];
-                            if (p.epi == EPI_SILU_BF16 && !(args.debug & 2)) {
+                            if (p.epi == EPI_SILU_BF16) {
 #pragma unroll
                                 for (int e = 0; e < 32; e += 2) w[e / 2] = ptx::silu2_bf16(v[e], v[e + 1]);
                             } else {
@@ -831,7 +496,7 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                     }
                     ptx::fence_proxy_async_smem();
                     __syncwarp();
-                    if (lane == 0 && !(args.debug & 1)) {
+                    if (lane == 0) {
                         ptx::tma_store_2d(&p.tma_c, stg, n0, row0);
                         ptx::bulk_commit();
                     }
@@ -913,18 +578,13 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                 __syncwarp();
                 ++nstore;
             }
-            ftrace();
             release(acc);  // hand the accumulator back to the MMA warp (tile j + kAcc)
-            if (warp == 0 && ntile < 64) trace(256 + ntile);
-            ++ntile;
         }
-        if (warp == 0) trace(3);
         if (lane == 0) ptx::bulk_wait<0>();  // all bulk stores complete before exit
         __syncwarp();
     }
     ptx::tc_fence_before();
     __syncthreads();
-    if (args.cluster2) ptx::cluster_sync();  // no CTA exits while its peer may still multicast / arrive into it
     if (warp == kWarpAlloc) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc<C::TMEM_COLS>(tmem_base);

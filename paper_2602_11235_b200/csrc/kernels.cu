@@ -428,26 +428,24 @@ __global__ void gather_kernel(DevBatch b, const SourceInfo* __restrict__ srcs, c
 }
 
 template <typename T>
-void launch_gather(const DevBatch& b, const SourceInfo* src_dev, const SlotInfo* slots_dev, const RowMeta& rm,
+bool launch_gather(const DevBatch& b, const SourceInfo* src_dev, const SlotInfo* slots_dev, const RowMeta& rm,
                    const long long* src_base_dev, const long long* src_cnt_dev, const long long* emb_base_dev,
                    const T* tables, int d_emb, int n_src, long long total_rows, int max_slots, T* out,
                    cudaStream_t st) {
-    if (total_rows == 0) return;
+    if (total_rows == 0) return true;
     const long long n = total_rows * (max_slots + 1);
-    if (n >= (1ll << 31) || n_src > 32) {
-        std::fprintf(stderr, "gather: %lld items / %d sources exceed the kernel's 32-bit indexing\n", n, n_src);
-        std::abort();
-    }
+    if (n >= (1ll << 31) || n_src > 32) return false;  // the kernel indexes items in 32 bits
     // one item per thread where possible: the dependent load chain per item
     // (row -> item -> feature offset -> id -> table row) is latency-bound
     const int blocks = static_cast<int>(std::min<long long>(cdiv(n, 256), 148ll * 64));
     launch_k(gather_kernel<T>, dim3(blocks), dim3(256), 0, st, b, src_dev, slots_dev, rm.src_rows, rm.item, src_base_dev, src_cnt_dev,
                                              emb_base_dev, tables, d_emb, n_src, total_rows, max_slots, out);
+    return true;
 }
-template void launch_gather<float>(const DevBatch&, const SourceInfo*, const SlotInfo*, const RowMeta&,
+template bool launch_gather<float>(const DevBatch&, const SourceInfo*, const SlotInfo*, const RowMeta&,
                                    const long long*, const long long*, const long long*, const float*, int, int,
                                    long long, int, float*, cudaStream_t);
-template void launch_gather<__nv_bfloat16>(const DevBatch&, const SourceInfo*, const SlotInfo*, const RowMeta&,
+template bool launch_gather<__nv_bfloat16>(const DevBatch&, const SourceInfo*, const SlotInfo*, const RowMeta&,
                                            const long long*, const long long*, const long long*,
                                            const __nv_bfloat16*, int, int, long long, int, __nv_bfloat16*,
                                            cudaStream_t);
@@ -791,53 +789,6 @@ template void launch_gate<float>(const float*, long long, const float*, long lon
 template void launch_gate<__nv_bfloat16>(const __nv_bfloat16*, long long, const __nv_bfloat16*, long long,
                                          long long, int, const int*, const float*, const float*, float,
                                          __nv_bfloat16*, long long, cudaStream_t);
-
-template <typename T, int NS>
-__global__ void __launch_bounds__(256) row_stats_kernel(const T* __restrict__ x, long long ldx, long long n_rows,
-                                                        int d, float eps, float2* __restrict__ out) {
-    MTFM_PDL_ENTRY();
-    const int lane = threadIdx.x & 31;
-    const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
-    for (long long i = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); i < n_rows; i += warps) {
-        const T* xr = x + i * ldx;
-        float4 v[NS];
-#pragma unroll
-        for (int k = 0; k < NS; ++k) {
-            const int c = 128 * k + 4 * lane;
-            v[k] = c < d ? ld4(xr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-        float s = 0.f;
-#pragma unroll
-        for (int k = 0; k < NS; ++k)
-            if (128 * k + 4 * lane < d) s += (v[k].x + v[k].y) + (v[k].z + v[k].w);
-        s = warp_sum(s);
-        const float mean = __fdiv_rn(s, static_cast<float>(d));
-        float q = 0.f;
-#pragma unroll
-        for (int k = 0; k < NS; ++k)
-            if (128 * k + 4 * lane < d) {
-                const float a = v[k].x - mean, b = v[k].y - mean, c = v[k].z - mean, e = v[k].w - mean;
-                q += (a * a + b * b) + (c * c + e * e);
-            }
-        q = warp_sum(q);
-        const float var = __fdiv_rn(q, static_cast<float>(d));
-        if (lane == 0) out[i] = make_float2(mean, __fdiv_rn(1.f, sqrtf(var + eps)));
-    }
-}
-
-template <typename T>
-void launch_row_stats(const T* x, long long ldx, long long n_rows, int d, float eps, float2* out, cudaStream_t st) {
-    if (n_rows == 0) return;
-    const int blocks = static_cast<int>(std::min<long long>(cdiv(n_rows, 8), 148ll * 16));
-    const int ns = static_cast<int>(cdiv(d, 128));
-    if (ns <= 1) launch_k(row_stats_kernel<T, 1>, dim3(blocks), dim3(256), 0, st, x, ldx, n_rows, d, eps, out);
-    else if (ns == 2) launch_k(row_stats_kernel<T, 2>, dim3(blocks), dim3(256), 0, st, x, ldx, n_rows, d, eps, out);
-    else if (ns <= 4) launch_k(row_stats_kernel<T, 4>, dim3(blocks), dim3(256), 0, st, x, ldx, n_rows, d, eps, out);
-    else launch_k(row_stats_kernel<T, 8>, dim3(blocks), dim3(256), 0, st, x, ldx, n_rows, d, eps, out);
-}
-template void launch_row_stats<float>(const float*, long long, long long, int, float, float2*, cudaStream_t);
-template void launch_row_stats<__nv_bfloat16>(const __nv_bfloat16*, long long, long long, int, float, float2*,
-                                              cudaStream_t);
 
 __global__ void to_bf16_kernel(const float* __restrict__ x, long long n_rows, int d, __nv_bfloat16* __restrict__ out,
                                long long ldo) {

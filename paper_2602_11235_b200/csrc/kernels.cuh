@@ -81,8 +81,9 @@ struct PlanArgs {
 void launch_plan(const PlanArgs& a, int smem_elems, cudaStream_t st);
 
 // Embedding gather into the per-source tokenizer input matrices.
+// false when the batch exceeds the kernel's 32-bit item indexing (nothing launched)
 template <typename T>
-void launch_gather(const DevBatch& b, const SourceInfo* src_dev, const SlotInfo* slots_dev, const RowMeta& rm,
+bool launch_gather(const DevBatch& b, const SourceInfo* src_dev, const SlotInfo* slots_dev, const RowMeta& rm,
                    const long long* src_base_dev, const long long* src_cnt_dev, const long long* emb_base_dev,
                    const T* tables, int d_emb, int n_src, long long total_rows, int max_kpad, T* out,
                    cudaStream_t st);
@@ -111,11 +112,6 @@ template <typename T>
 void launch_gate(const T* a, long long lda, const T* u, long long ldu, long long n_rows, int d,
                  const int* row_src_of_rows, const float* gain, const float* bias, float eps, T* out,
                  long long ldo, cudaStream_t st);
-
-// Per-row (mean, rstd) of row_normalize (kernels.hpp:132-153) for the
-// LayerNorm / gate transforms fused into the GEMM A producer.
-template <typename T>
-void launch_row_stats(const T* x, long long ldx, long long n_rows, int d, float eps, float2* out, cudaStream_t st);
 
 // f32 -> bf16 copy of rows (head input in the fast path)
 void launch_to_bf16(const float* x, long long n_rows, int d, __nv_bfloat16* out, long long ldo, cudaStream_t st);

@@ -13,7 +13,6 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <chrono>
 #include <cstdio>
 #include <cmath>
 #include <cstdlib>
@@ -148,7 +147,7 @@ struct DevBuf {
 // layout tables and the records are per batch (two batches in flight cost one
 // set of activations). A batch records the bytes it needs; run_forward grows
 // the arena (after draining the stream) when a bigger batch arrives.
-enum ActId { ACT_X, ACT_XN, ACT_P, ACT_KV, ACT_UQ, ACT_A, ACT_GT, ACT_E, ACT_HID, ACT_Y, ACT_STATX, ACT_STATA, ACT_N };
+enum ActId { ACT_X, ACT_XN, ACT_P, ACT_KV, ACT_UQ, ACT_A, ACT_GT, ACT_E, ACT_HID, ACT_Y, ACT_N };
 
 // Page-locked host staging (grows, never shrinks): host-computed layout tables
 // are written here and copied with truly asynchronous H2D transfers.
@@ -256,9 +255,6 @@ struct LayerW {
     // (bf16 [n_ctx][N][d] K-major, fp32 [n_ctx][N]): x~W + b = xhat (gain (.) W) + (bias W + b)
     // target: fkv (N = 2gd), full: f1 (N = 2hd + 2gd)
     DevBuf tfold, bfold;
-    // first target layer of a run only: the folded K|V weights of the run's layers stacked per
-    // context source ([n_ctx][kt * 2gd][d], [n_ctx][kt * 2gd]) for one column-segmented GEMM
-    DevBuf kv_run, kvb_run;
 };
 
 struct SourceW {
@@ -299,7 +295,6 @@ struct mtfm_cuda_model {
     mtfm_run_stats stats{};
     // per-stage profiling (CUDA events around every launch) — off by default
     bool profiling = false;
-    int fuse = 0;  // bit 0: GLN1 fused into the projection GEMM, bit 1: gate fused into f2 (MTFM_FUSE)
     struct Prof {
         std::string name;
         cudaEvent_t a = nullptr, b = nullptr;
@@ -543,29 +538,6 @@ void finalize(mtfm_cuda_model& m) {
             upload(L->g2b, g2b, st);
             m.layers.push_back(std::move(L));
         }
-    // stacked folded K|V weights per target run (column-segmented context K|V GEMM)
-    for (size_t li = 0; li < m.layers.size() && m.n_ctx_src > 0; ++li) {
-        if (!m.layers[li]->target || (li > 0 && m.layers[li - 1]->target)) continue;
-        size_t lj = li;
-        while (lj < m.layers.size() && m.layers[lj]->target) ++lj;
-        const int kt = static_cast<int>(lj - li);
-        if (kt > 4) continue;
-        auto& Lr = *m.layers[li];
-        const size_t wn = static_cast<size_t>(2 * gd) * d;
-        Lr.kv_run.alloc(static_cast<size_t>(m.n_ctx_src) * kt * wn * 2);
-        Lr.kvb_run.alloc(static_cast<size_t>(m.n_ctx_src) * kt * 2 * gd * 4);
-        for (int s = 0; s < m.n_ctx_src; ++s)
-            for (int c = 0; c < kt; ++c) {
-                const auto& Lc = *m.layers[li + c];
-                ck(cudaMemcpyAsync(static_cast<char*>(Lr.kv_run.p) + (static_cast<size_t>(s) * kt + c) * wn * 2,
-                                   static_cast<const char*>(Lc.tfold.p) + s * wn * 2, wn * 2, cudaMemcpyDeviceToDevice, st),
-                   "kv_run");
-                ck(cudaMemcpyAsync(static_cast<char*>(Lr.kvb_run.p) + (static_cast<size_t>(s) * kt + c) * 2 * gd * 4,
-                                   static_cast<const char*>(Lc.bfold.p) + static_cast<size_t>(s) * 2 * gd * 4, 2 * gd * 4,
-                                   cudaMemcpyDeviceToDevice, st),
-                   "kvb_run");
-            }
-    }
     // heads: [d][E*de | n_tasks*E]
     const int E = m.cfg.experts, dx = m.cfg.d_expert;
     m.head_n = E * dx + m.n_tasks_total * E;
@@ -619,25 +591,7 @@ void launch_gemm_tc_bn(GemmArgs& a, int grid, cudaStream_t st) {
     }
     const int smem = 1024 + a.bres_bytes + 4096 + a.n_stages * a.stage_bytes + a.n_epi * a.stg_warp + C::BAR_BYTES;
     if (smem > C::kMaxSmem) fail(MTFM_CONTRACT_ERROR, "gemm smem plan exceeds 227 KB");
-    if (a.cluster2) {
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(grid);
-        cfg.blockDim = dim3(C::kThreads);
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = st;
-        cudaLaunchAttribute attr[2];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = 2;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[1].val.programmaticStreamSerializationAllowed = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = pdl_enabled() ? 2 : 1;
-        ck(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN>, a), "gemm_tc cluster launch");
-    } else {
-        launch_k(gemm_tc_kernel<BN>, dim3(grid), dim3(C::kThreads), smem, st, a);
-    }
+    launch_k(gemm_tc_kernel<BN>, dim3(grid), dim3(C::kThreads), smem, st, a);
     ck(cudaGetLastError(), "gemm_tc launch");
 }
 
@@ -648,36 +602,8 @@ void launch_tok_fused(const TokArgs& a, cudaStream_t st) {
            "tok smem attr");
         attr = true;
     }
-    TokArgs aa = a;
-    static unsigned long long* tr = nullptr;
-    const bool tracing = std::getenv("MTFM_TOK_TRACE") != nullptr;
-    if (tracing) {
-        if (!tr) ck(cudaMalloc(&tr, 1024 * 8), "trace alloc");
-        ck(cudaMemsetAsync(tr, 0, 1024 * 8, st), "trace clear");
-        aa.trace = tr;
-    }
-    launch_k(tok_fused_kernel, dim3(std::min(a.n_tiles, kNumSMs)), dim3(512), tok_detail::SMEM, st, aa);
+    launch_k(tok_fused_kernel, dim3(std::min(a.n_tiles, kNumSMs)), dim3(512), tok_detail::SMEM, st, a);
     ck(cudaGetLastError(), "tok_fused launch");
-    if (tracing) {
-        unsigned long long h[1024];
-        ck(cudaMemcpyAsync(h, tr, sizeof(h), cudaMemcpyDeviceToHost, st), "trace fetch");
-        ck(cudaStreamSynchronize(st), "trace sync");
-        const unsigned long long t0 = h[0] ? h[0] : 1;
-        auto rel = [&](int i) { return h[i] ? static_cast<long long>(h[i] - t0) : -1LL; };
-        for (int t = 0; t < 3; ++t)
-            for (int c = 0; c < 8; ++c) {
-                const int b = 16 * (t * 8 + c);
-                std::fprintf(stderr, "t%d c%d g1: start %lld ready %lld | g2: start %lld ready %lld\n", t, c, rel(b),
-                             rel(b + 1), rel(b + 4), rel(b + 5));
-            }
-        for (int k = 0; k < 12; ++k)
-            std::fprintf(stderr, "silu k%d: g0 [%lld %lld %lld %lld] g1 [%lld %lld %lld %lld]\n", k, rel(512 + 8 * k),
-                         rel(513 + 8 * k), rel(514 + 8 * k), rel(515 + 8 * k), rel(516 + 8 * k), rel(517 + 8 * k),
-                         rel(518 + 8 * k), rel(519 + 8 * k));
-        for (int t = 0; t < 3; ++t)
-            std::fprintf(stderr, "y t%d: start %lld full %lld drained %lld\n", t, rel(900 + 4 * t), rel(901 + 4 * t),
-                         rel(902 + 4 * t));
-    }
 }
 
 struct TcProblem {
@@ -693,22 +619,6 @@ struct TcProblem {
     const int* row_map;
     long long row_offset;
     const float* resid;
-    // fused A transform (GemmAMode): A is built from a_src instead of TMA-loaded
-    int amode = A_TMA;
-    const void* a_src = nullptr;
-    long long a_row0 = 0;
-    const float2* stats = nullptr;
-    const int* row_group = nullptr;
-    long long g_row0 = 0;
-    const float* gain = nullptr;
-    const float* gbias = nullptr;
-    const __nv_bfloat16* u_src = nullptr;
-    long long ldu = 0;
-    // column segments (row-mapped bf16 outputs only): GemmProblem::seg_*
-    int n_seg = 0;
-    int seg_n0[4] = {0, 0, 0, 0};
-    void* seg_out[4] = {nullptr, nullptr, nullptr, nullptr};
-    long long seg_ldo[4] = {0, 0, 0, 0};
 };
 
 int pick_bn(const std::vector<TcProblem>& ps) {
@@ -761,35 +671,20 @@ void run_gemm_tc(std::vector<TcProblem> ps, cudaStream_t st, long long& launches
     ps.erase(std::remove_if(ps.begin(), ps.end(), [](const TcProblem& p) { return p.M == 0 || p.N == 0; }),
              ps.end());
     if (ps.empty()) return;
-    static const bool stream_only = std::getenv("MTFM_GEMM_STREAM") != nullptr;
-    static const int force_bn = std::getenv("MTFM_GEMM_BN") ? std::atoi(std::getenv("MTFM_GEMM_BN")) : 0;
-    static const int force_stages = std::getenv("MTFM_GEMM_STAGES") ? std::atoi(std::getenv("MTFM_GEMM_STAGES")) : 0;
-    static const int force_epi = std::getenv("MTFM_GEMM_EPI") ? std::atoi(std::getenv("MTFM_GEMM_EPI")) : 0;
-    int bn_res = stream_only ? 0 : pick_bn_resident(ps);
-    // small launches (a few tiles per CTA): loading a resident weight slice per
-    // CTA costs more than streaming B with the A stages
-    static const long long small_tiles = std::getenv("MTFM_GEMM_SMALL") ? std::atoll(std::getenv("MTFM_GEMM_SMALL")) : 0;
-    if (bn_res && small_tiles > 0) {
-        long long t = 0;
-        for (const auto& p : ps) t += cdiv(p.M, 128) * cdiv(p.N, bn_res);
-        if (t < small_tiles) bn_res = 0;
-    }
-    if (bn_res && force_bn) bn_res = force_bn;
+    const int bn_res = pick_bn_resident(ps);
     for (size_t i0 = 0; i0 < ps.size(); i0 += kMaxProblems) {
         const size_t i1 = std::min(ps.size(), i0 + kMaxProblems);
         GemmArgs a;
         std::memset(&a, 0, sizeof(a));
-        a.a_mode = ps[i0].amode;
         // ---- schedule
         int bn = bn_res;
         int grid = 0;
         if (bn) {
-            // CTAs per problem: a multiple of its n-slices so the CTAs sharing an m-block
-            // (one per slice) run in lockstep (A read once).
-            // CTA rows per problem (a row = one CTA per n-slice, lockstep on an m-block):
-            // start at one row each, then repeatedly give a row to the problem whose CTAs
-            // walk the most m-blocks while the SMs last (min-makespan greedy; a proportional
-            // share rounded down leaves small problems' CTAs with ~2x the m-blocks)
+            // CTA rows per problem (a row = one CTA per n-slice, lockstep on an m-block so
+            // A is read from HBM once): start at one row each, then repeatedly give a row to
+            // the problem whose CTAs walk the most m-blocks while the SMs last (min-makespan
+            // greedy; a proportional share rounded down leaves small problems' CTAs with ~2x
+            // the m-blocks)
             std::vector<int> cpsv(i1 - i0, 1);
             int used = 0;
             for (size_t i = i0; i < i1; ++i) used += static_cast<int>(cdiv(ps[i].N, bn));
@@ -836,48 +731,25 @@ void run_gemm_tc(std::vector<TcProblem> ps, cudaStream_t st, long long& launches
                 bn = 0;
             }
         }
-        if (!bn) bn = force_bn ? force_bn : pick_bn(std::vector<TcProblem>(ps.begin() + i0, ps.begin() + i1));
+        if (!bn) bn = pick_bn(std::vector<TcProblem>(ps.begin() + i0, ps.begin() + i1));
         int tiles = 0;
         int kmax = 0;
         // k-blocks per pipeline stage: 2 (one 3D TMA per operand per 2 k-blocks) when
-        // every K is a multiple of 64 and A is TMA-loaded, else 1
-        static const int force_kb = std::getenv("MTFM_GEMM_STAGE_KB") ? std::atoi(std::getenv("MTFM_GEMM_STAGE_KB")) : 0;
-        int ks = a.a_mode == A_TMA ? 2 : 1;
+        // every K is a multiple of 64, else 1
+        int ks = 2;
         for (size_t i = i0; i < i1; ++i)
             if (ps[i].K % 64 != 0 || ps[i].K < 128) ks = 1;
-        if (force_kb && ks > 1) ks = force_kb;
-        // CTA pairs multicasting B (streaming, TMA-loaded A): MTFM_GEMM_CLUSTER=1
-        static const bool clus_env = std::getenv("MTFM_GEMM_CLUSTER") && std::atoi(std::getenv("MTFM_GEMM_CLUSTER")) != 0;
-        a.cluster2 = (!a.b_res && a.a_mode == A_TMA && bn >= 128 && clus_env) ? 1 : 0;
-        if (a.cluster2) ks = 1;
         a.stage_kb = ks;
         for (size_t i = i0; i < i1; ++i) {
             const auto& s = ps[i];
-            if (s.amode != a.a_mode) fail(MTFM_CONTRACT_ERROR, "mixed A modes in one grouped GEMM");
             GemmProblem& p = a.p[a.n_problems++];
-            if (s.amode == A_TMA) p.tma_a = ks > 1 ? tma_3d_kb(s.A, s.M, s.K, s.lda, 128, ks) : tma_2d(s.A, s.M, s.K, s.lda, 64, 128, 128);
-            if (s.amode == A_GATE_TMA || s.amode == A_AFFINE_TMA) {
-                p.tma_a = tma_2d(s.a_src, s.M, s.K, s.lda, 64, 128, 128);
-                if (s.amode == A_GATE_TMA) p.tma_u = tma_2d(s.u_src, s.M, s.K, s.ldu, 64, 128, 128);
-            }
+            p.tma_a = ks > 1 ? tma_3d_kb(s.A, s.M, s.K, s.lda, 128, ks) : tma_2d(s.A, s.M, s.K, s.lda, 64, 128, 128);
             // B: 2D boxes for the resident slice (loaded once per CTA), 3D per stage when streaming
             p.tma_b = (ks > 1 && !a.b_res) ? tma_3d_kb(s.Bt, s.N, s.K, s.ldb, bn, ks) : tma_2d(s.Bt, s.N, s.K, s.ldb, 64, bn, 128);
-            if (a.cluster2) p.tma_b_half = tma_2d(s.Bt, s.N, s.K, s.ldb, 64, bn / 2, 128);
             p.M = s.M;
             p.N = s.N;
             p.K = static_cast<int>(round_up(s.K, 64));
             kmax = std::max(kmax, p.K);
-            p.Kv = s.K;
-            p.a_src = s.a_src;
-            p.lda = s.lda;
-            p.a_row0 = s.a_row0;
-            p.stats = s.stats;
-            p.row_group = s.row_group;
-            p.g_row0 = s.g_row0;
-            p.gain = s.gain;
-            p.gbias = s.gbias;
-            p.u_src = s.u_src;
-            p.ldu = s.ldu;
             p.tile_start = tiles;
             p.tiles_n = static_cast<int>(cdiv(s.N, bn));
             p.epi = s.epi;
@@ -891,44 +763,20 @@ void run_gemm_tc(std::vector<TcProblem> ps, cudaStream_t st, long long& launches
             // bulk-tensor stores for plain row-major outputs (rows [row_offset, row_offset + M))
             const bool bf16_out = s.epi == EPI_SILU_BF16 || s.epi == EPI_BIAS_BF16;
             const int eb = bf16_out ? 2 : 4;
-            const bool tma_ok = !s.row_map && (s.ldo * eb) % 16 == 0 && (reinterpret_cast<uintptr_t>(s.out) % 16) == 0 &&
-                                std::getenv("MTFM_NO_TMA_STORE") == nullptr;
+            const bool tma_ok = !s.row_map && (s.ldo * eb) % 16 == 0 && (reinterpret_cast<uintptr_t>(s.out) % 16) == 0;
             p.use_tma_c = tma_ok && (s.epi != EPI_RESID_F32 || s.resid == s.out);
             p.use_tma_r = p.use_tma_c && s.epi == EPI_RESID_F32;
             p.use_scatter_c = bf16_out && s.row_map && bn >= 64 && s.N % 64 == 0 && (s.ldo * 2) % 16 == 0 &&
-                              (reinterpret_cast<uintptr_t>(s.out) % 16) == 0 && std::getenv("MTFM_NO_SCATTER") == nullptr;
-            p.n_seg = 1;
-            if (s.n_seg > 1) {
-                bool seg_ok = p.use_scatter_c && s.n_seg <= 4;
-                for (int k = 1; k < s.n_seg && seg_ok; ++k)
-                    seg_ok = s.seg_n0[k] % 64 == 0 && s.seg_n0[k] > s.seg_n0[k - 1] && (s.seg_ldo[k] * 2) % 16 == 0 &&
-                             (reinterpret_cast<uintptr_t>(s.seg_out[k]) % 16) == 0;
-                if (!seg_ok) fail(MTFM_CONTRACT_ERROR, "column-segmented GEMM output needs the row-mapped bf16 epilogue");
-                p.n_seg = s.n_seg;
-                for (int k = 0; k < s.n_seg; ++k) {
-                    p.seg_n0[k] = s.seg_n0[k];
-                    p.seg_out[k] = s.seg_out[k];
-                    p.seg_ldo[k] = s.seg_ldo[k];
-                }
-            }
+                              (reinterpret_cast<uintptr_t>(s.out) % 16) == 0;
             if (p.use_tma_c) {
                 // 32 rows x 128 B boxes: 64 bf16 columns or 32 fp32 columns (SW128)
                 const char* base = static_cast<const char*>(s.out) + s.row_offset * s.ldo * eb;
                 const bool wide = bf16_out && bn >= 64;
                 p.tma_c = tma_2d(base, s.M, s.N, s.ldo, wide ? 64 : 32, 32, wide ? 128 : (bf16_out ? 64 : 128), eb);
             }
-            // cluster2: pair tiles (m-blocks 2j, 2j+1 of one n-block)
-            tiles += static_cast<int>(a.cluster2 ? cdiv(cdiv(s.M, 128), 2) : cdiv(s.M, 128)) * p.tiles_n;
+            tiles += static_cast<int>(cdiv(s.M, 128)) * p.tiles_n;
         }
         a.n_tiles = tiles;
-        static const int dbg = std::getenv("MTFM_GEMM_DEBUG") ? std::atoi(std::getenv("MTFM_GEMM_DEBUG")) : 0;
-        a.debug = dbg;
-        static unsigned long long* trace_buf = nullptr;
-        if (std::getenv("MTFM_GEMM_TRACE")) {
-            if (!trace_buf) ck(cudaMalloc(&trace_buf, 1024 * 8), "trace alloc");
-            ck(cudaMemsetAsync(trace_buf, 0, 1024 * 8, st), "trace clear");
-            a.trace = trace_buf;
-        }
         const int a_bytes = 128 * 64 * 2;
         const int b_bytes = bn * 64 * 2;
         // bf16 bulk-store epilogues (64-column units) need one 4 KB staging buffer per warp
@@ -938,17 +786,15 @@ void run_gemm_tc(std::vector<TcProblem> ps, cudaStream_t st, long long& launches
             all_fast = all_fast && (p.use_tma_c || p.use_scatter_c) && bn >= 64 &&
                        (p.epi == EPI_SILU_BF16 || p.epi == EPI_BIAS_BF16);
         }
-        static const bool stg_double = std::getenv("MTFM_GEMM_STG2") != nullptr;
-        const int stg_warp = (all_fast && !stg_double) ? 4096 : 8192;
+        const int stg_warp = all_fast ? 4096 : 8192;
         a.stg_warp = stg_warp;
-        if (!a.b_res) grid = a.cluster2 ? 2 * std::min(tiles, kNumSMs / 2) : std::min(tiles, kNumSMs);
+        if (!a.b_res) grid = std::min(tiles, kNumSMs);
         bool any_bias = false;
         for (int i = 0; i < a.n_problems; ++i) any_bias = any_bias || a.p[i].has_bias;
         a.bias_bytes = any_bias ? bn * 32 : 0;
         a.bres_bytes = a.b_res ? (kmax / 64) * b_bytes + a.bias_bytes : 0;
-        const int a_stage = a.a_mode == A_GATE_TMA ? 2 * a_bytes : a_bytes;  // raw A + U k-blocks
-        a.stage_bytes = a.b_res ? ks * a_stage : ks * (a_stage + b_bytes) + a.bias_bytes;
-        // 12 epilogue warps when A is TMA-loaded and >= 3 stages still fit, else 8
+        a.stage_bytes = a.b_res ? ks * a_bytes : ks * (a_bytes + b_bytes) + a.bias_bytes;
+        // 12 epilogue warps when >= 3 stages still fit (and there are 4 accumulators), else 8
         for (int ne : {12, 8, 0}) {
             if (ne == 0) {
                 // nothing fits with multi-k-block stages: fall back to one k-block per stage
@@ -956,18 +802,16 @@ void run_gemm_tc(std::vector<TcProblem> ps, cudaStream_t st, long long& launches
                 a.stage_kb = 1;
                 for (int i = 0; i < a.n_problems; ++i) {
                     const auto& s = ps[i0 + i];
-                    if (s.amode == A_TMA) a.p[i].tma_a = tma_2d(s.A, s.M, s.K, s.lda, 64, 128, 128);
+                    a.p[i].tma_a = tma_2d(s.A, s.M, s.K, s.lda, 64, 128, 128);
                     if (!a.b_res) a.p[i].tma_b = tma_2d(s.Bt, s.N, s.K, s.ldb, 64, bn, 128);
                 }
                 a.stage_bytes = a.b_res ? a_bytes : a_bytes + b_bytes + a.bias_bytes;
                 ne = 8;
             }
-            if (ne == 12 && (a.a_mode != A_TMA || bn >= 256)) continue;  // epilogue groups <= accumulator buffers
-            if (force_epi && ne != force_epi) continue;
+            if (ne == 12 && bn >= 256) continue;  // epilogue groups <= accumulator buffers
             const int avail = 227 * 1024 - 1024 - gemm_detail::Cfg<128>::BAR_BYTES - 4096 - ne * stg_warp - a.bres_bytes;
             a.n_epi = ne;
             a.n_stages = std::min(8, avail / a.stage_bytes);
-            if (force_stages) a.n_stages = std::min(a.n_stages, force_stages);
             if (a.n_stages >= 3) break;
         }
         if (a.n_stages < 2) fail(MTFM_CONTRACT_ERROR, "gemm pipeline does not fit in SMEM");
@@ -975,38 +819,6 @@ void run_gemm_tc(std::vector<TcProblem> ps, cudaStream_t st, long long& launches
         else if (bn == 128) launch_gemm_tc_bn<128>(a, grid, st);
         else launch_gemm_tc_bn<64>(a, grid, st);
         ++launches;
-        if (a.trace) {
-            unsigned long long h[1024];
-            ck(cudaMemcpyAsync(h, a.trace, sizeof(h), cudaMemcpyDeviceToHost, st), "trace fetch");
-            ck(cudaStreamSynchronize(st), "trace sync");
-            const unsigned long long t0 = h[0];
-            auto rel = [&](int i) { return h[i] ? static_cast<long long>(h[i] - t0) : -1LL; };
-            std::fprintf(stderr, "trace bn=%d grid=%d stages=%d: start->sync %lld bres %lld end %lld\n", bn, grid,
-                         a.n_stages, rel(1), rel(2), rel(3));
-            for (int i = 0; i < 12; ++i)
-                std::fprintf(stderr, "  tile %2d: tma %7lld  mma_go %7lld  mma_done %7lld  epi_go %7lld  epi_done %7lld\n", i,
-                             rel(320 + i), rel(64 + i), rel(128 + i), rel(192 + i), rel(256 + i));
-            for (int i = 0; i < 8; ++i) {
-                std::fprintf(stderr, "  epi tile %d:", i);
-                long long prev = rel(192 + i);
-                for (int k = 0; k < 16; ++k) {
-                    const long long t = rel(384 + i * 16 + k);
-                    if (t < 0) break;
-                    std::fprintf(stderr, " +%lld", t - prev);
-                    prev = t;
-                }
-                std::fprintf(stderr, " | release +%lld\n", rel(256 + i) - prev);
-            }
-            for (int i = 0; i < 8; ++i) {
-                std::fprintf(stderr, "  mma tile %d (go %lld):", i, rel(64 + i));
-                for (int k = 0; k < 8; ++k) {
-                    if (rel(512 + i * 16 + 2 * k) < 0) break;
-                    std::fprintf(stderr, " [tma %lld full %lld iss %lld]", rel(640 + i * 16 + k), rel(512 + i * 16 + 2 * k),
-                                 rel(512 + i * 16 + 2 * k + 1));
-                }
-                std::fprintf(stderr, "\n");
-            }
-        }
     }
 }
 
@@ -1037,8 +849,6 @@ __global__ void tile_kmax_kernel(AttnTile* tiles, int n, const int* prefix, int 
 struct AttnGeom {
     int hs, rt;
 };
-constexpr int kAttnEmuDefault = 0;
-constexpr bool kAttnSpaDefault = true;
 
 AttnGeom attn_geom(const mtfm_cuda_model& m) {
     const int r = m.H / m.G;
@@ -1046,34 +856,18 @@ AttnGeom attn_geom(const mtfm_cuda_model& m) {
     return {1, 128};
 }
 
-template <int D, int EMU, bool SPA>
-void launch_attn_tc_de(const AttnParams& p, cudaStream_t st) {
+template <int D>
+void launch_attn_tc_d(const AttnParams& p, cudaStream_t st) {
     using C = attn_detail::Cfg<D>;
     static bool attr = false;
     if (!attr) {
-        ck(cudaFuncSetAttribute(attn_tc_kernel<D, EMU, SPA>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM),
+        ck(cudaFuncSetAttribute(attn_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM),
            "attn smem attr");
         attr = true;
     }
     const int grid = std::min(p.n_tiles, kNumSMs);
-    launch_k(attn_tc_kernel<D, EMU, SPA>, dim3(grid), dim3(C::kThreads), C::SMEM, st, p);
+    launch_k(attn_tc_kernel<D>, dim3(grid), dim3(C::kThreads), C::SMEM, st, p);
     ck(cudaGetLastError(), "attn_tc launch");
-}
-
-// SiLU pairs (of 16) on the FMA pipes instead of the SFU (MTFM_ATTN_EMU), and
-// the P-aliasing-S pipeline (MTFM_ATTN_SPA); both override the defaults
-template <int D>
-void launch_attn_tc_d(const AttnParams& p, cudaStream_t st) {
-    static const int emu = std::getenv("MTFM_ATTN_EMU") ? std::atoi(std::getenv("MTFM_ATTN_EMU")) : kAttnEmuDefault;
-    static const bool spa = std::getenv("MTFM_ATTN_SPA") ? std::atoi(std::getenv("MTFM_ATTN_SPA")) != 0 : kAttnSpaDefault;
-    if constexpr (D == 32 || D == 64) {
-        switch (emu) {
-            case 3: spa ? launch_attn_tc_de<D, 3, true>(p, st) : launch_attn_tc_de<D, 3, false>(p, st); return;
-            case 5: spa ? launch_attn_tc_de<D, 5, true>(p, st) : launch_attn_tc_de<D, 5, false>(p, st); return;
-            default: break;
-        }
-    }
-    spa ? launch_attn_tc_de<D, 0, true>(p, st) : launch_attn_tc_de<D, 0, false>(p, st);
 }
 
 void run_attn_tc(const mtfm_cuda_model& m, AttnParams p, const __nv_bfloat16* q, long long n_q, long long q_cols,
@@ -1086,36 +880,7 @@ void run_attn_tc(const mtfm_cuda_model& m, AttnParams p, const __nv_bfloat16* q,
     p.tma_kv = tma_2d(p.kv_ptr, kv_rows, kv_cols, p.ldkv, chunk, bkv, chunk * 2);
     switch (D) {
         case 16: launch_attn_tc_d<16>(p, st); break;
-        case 32: {
-            static unsigned long long* tr = nullptr;
-            static int calls = 0;
-            // MTFM_ATTN_TRACE=full|target: second launch of that layer kind (-DMTFM_ATTN_TRACE builds)
-            const char* tenv = std::getenv("MTFM_ATTN_TRACE");
-            const bool tracing = tenv != nullptr &&
-                                 (std::string(tenv) == "target" ? p.n_tiles < 20000 : p.n_tiles > 20000) &&
-                                 calls++ == 1;
-            if (tracing) {
-                if (!tr) ck(cudaMalloc(&tr, 2048 * 8), "trace alloc");
-                ck(cudaMemsetAsync(tr, 0, 2048 * 8, st), "trace clear");
-                p.trace = tr;
-            }
-            launch_attn_tc_d<32>(p, st);
-            p.trace = nullptr;
-            if (tracing) {
-                unsigned long long h[2048];
-                ck(cudaMemcpyAsync(h, tr, sizeof(h), cudaMemcpyDeviceToHost, st), "trace fetch");
-                ck(cudaStreamSynchronize(st), "trace sync");
-                const unsigned long long t0 = h[1024];
-                auto rel = [&](int i) { return h[i] ? static_cast<long long>(h[i] - t0) : -1LL; };
-                for (int k = 0; k < 48; ++k)
-                    std::fprintf(stderr,
-                                 "s%2d mma: start %6lld kv %6lld s_empty %6lld | pv p_full %6lld || silu: start %6lld "
-                                 "s_full %6lld silu_done %6lld p_empty %6lld\n",
-                                 k, rel(1024 + 4 * k), rel(1025 + 4 * k), rel(1026 + 4 * k), rel(1027 + 4 * k),
-                                 rel(4 * k), rel(4 * k + 1), rel(4 * k + 2), rel(4 * k + 3));
-            }
-            break;
-        }
+        case 32: launch_attn_tc_d<32>(p, st); break;
         case 64: launch_attn_tc_d<64>(p, st); break;
         case 128: launch_attn_tc_d<128>(p, st); break;
         case 256: launch_attn_tc_d<256>(p, st); break;
@@ -1215,10 +980,6 @@ void check_batch(const mtfm_packed_batch* b) {
 }
 
 void prepare(mtfm_cuda_model& m, const mtfm_packed_batch* hb, int only_scenario, mtfm_cuda_batch& B) {
-    static const bool host_timing = std::getenv("MTFM_HOST_TIMING") != nullptr;
-    auto now = [] { return std::chrono::steady_clock::now(); };
-    auto dus = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
-    const auto p0 = now();
     check_batch(hb);
     finalize(m);
     // uploads go on the copy stream, after the previous forward of this batch object
@@ -1254,7 +1015,6 @@ void prepare(mtfm_cuda_model& m, const mtfm_packed_batch* hb, int only_scenario,
     upload_raw(B.exp_blk, hb->exp_blk, 3ll * hb->n_exposures, st);
     upload_raw(B.exp_feats, hb->exp_feats, hb->n_exp_feats, st);
 
-    const auto p1 = now();
     // host layout: per (user, source) counts -> source regions, record offsets
     std::vector<long long> us(static_cast<size_t>(B.n_users) * n_src, 0);
     std::vector<long long> rec_off(B.n_users + 1, 0);
@@ -1317,7 +1077,6 @@ void prepare(mtfm_cuda_model& m, const mtfm_packed_batch* hb, int only_scenario,
     B.pin.upload(B.d_emb_base, B.emb_base, st);
     B.pin.upload(B.d_rec_off, rec_off, st);
 
-    const auto p2 = now();
     // attention tiles
     const AttnGeom ag = attn_geom(m);
     const int r = m.H / m.G;
@@ -1347,10 +1106,6 @@ void prepare(mtfm_cuda_model& m, const mtfm_packed_batch* hb, int only_scenario,
     B.tiles_tgt.alloc(std::max<size_t>(static_cast<size_t>(nt) * sizeof(AttnTile), 16));
     if (B.n_users > 0)
         launch_tile_expand(B, ag.rt, ag.hs, r, m.G, st);
-    const auto p3 = now();
-    if (host_timing)
-        std::fprintf(stderr, "prepare: raw uploads %.0f us, layout %.0f us, tiles %.0f us\n", dus(p0, p1), dus(p1, p2),
-                     dus(p2, p3));
     // row meta + activations
     const long long R = B.rows, T = B.n_exp;
     auto ia = [&](DevBuf& b, long long n, size_t el) { b.alloc(std::max<size_t>(static_cast<size_t>(n) * el, 16)); };
@@ -1371,10 +1126,10 @@ void prepare(mtfm_cuda_model& m, const mtfm_packed_batch* hb, int only_scenario,
     const int pw = 2 * m.hd + 2 * m.gd;
     auto need = [&](int id, long long n, size_t e) { B.act_bytes[id] = std::max<size_t>(static_cast<size_t>(n) * e, 16); };
     need(ACT_X, R * m.d, 4);
-    // bf16 path: GLN1 copies of the context rows for every target layer of a run,
-    // then the T rows; K|V rows per target layer of the run
+    // bf16 path: [0, R) xhat of the context rows (source order) then the T rows' GLN1,
+    // [R, 2R) a full layer's GLN1 rows; K|V rows per target layer of a run
     const long long kt = std::max(1, m.cfg.target_layers);
-    need(ACT_XN, (std::max(R, kt * B.n_events + T) + R) * m.d, el);  // + the full-layer copy (XNF)
+    need(ACT_XN, 2 * R * m.d, el);
     need(ACT_P, R * pw, el);
     need(ACT_KV, kt * R * 2 * m.gd, el);
     need(ACT_UQ, T * 2 * m.hd, el);
@@ -1383,8 +1138,6 @@ void prepare(mtfm_cuda_model& m, const mtfm_packed_batch* hb, int only_scenario,
     need(ACT_E, eb, el);
     need(ACT_HID, hbse, el);
     need(ACT_Y, T * m.head_ld, 4);
-    need(ACT_STATX, R, 8);
-    need(ACT_STATA, R, 8);
     const long long nr = B.n_records;
     ia(B.rec_user, nr, 8);
     ia(B.rec_scen, nr, 4);
@@ -1530,31 +1283,30 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
         if (tok_rows * (max_slots + 1) >= (1ll << 31) || n_src > 32)
             fail(MTFM_CONTRACT_ERROR, "batch too large for one forward (tokens x slots >= 2^31)");
         StageScope sc(m, "gather", 0, tok_in * el * 2);
-        launch_gather<T>(pa.b, pa.src, pa.slots, rm, B.d_src_base.as<long long>(), B.d_src_cnt.as<long long>(),
-                         B.d_emb_base.as<long long>(),
-                         kTc ? static_cast<const T*>(m.emb_bf16.p) : static_cast<const T*>(m.emb_f32.p), m.cfg.d_emb,
-                         n_src, tok_rows, max_slots, E, st);
+        if (!launch_gather<T>(pa.b, pa.src, pa.slots, rm, B.d_src_base.as<long long>(), B.d_src_cnt.as<long long>(),
+                              B.d_emb_base.as<long long>(),
+                              kTc ? static_cast<const T*>(m.emb_bf16.p) : static_cast<const T*>(m.emb_f32.p),
+                              m.cfg.d_emb, n_src, tok_rows, max_slots, E, st))
+            fail(MTFM_CONTRACT_ERROR, "batch too large for one forward (tokens x slots >= 2^31)");
         ck(cudaGetLastError(), "gather launch");
         ++L;
     }
     float* X = m.act[ACT_X].as<float>();
     // the first target run's xhat (normalised context rows, source order) straight from the
-    // fused tokenizer's Y tiles when every context source goes through it (MTFM_TOK_XHAT=0: GLN pass)
+    // fused tokenizer's Y tiles when every context source goes through it (MTFM_TOK_XHAT=0:
+    // separate GLN pass, kept selectable for the parity test of the two)
     bool xhat_from_tok = false;
     if constexpr (kTc) {
         std::vector<TcProblem> p1, p2;
         static const bool tok_xhat = std::getenv("MTFM_TOK_XHAT") == nullptr || std::atoi(std::getenv("MTFM_TOK_XHAT")) != 0;
-        static const bool xhat_env = std::getenv("MTFM_XHAT") && std::atoi(std::getenv("MTFM_XHAT")) != 0;
         long long ctx_rows0 = 0;
         for (int s = 0; s < m.n_ctx_src; ++s) ctx_rows0 += B.src_cnt[s];
-        xhat_from_tok = tok_xhat && !xhat_env && m.n_ctx_src > 0 && ctx_rows0 == NE && !(m.fuse & 1) &&
-                        !m.layers.empty() && m.layers[0]->target;
+        xhat_from_tok = tok_xhat && m.n_ctx_src > 0 && ctx_rows0 == NE && !m.layers.empty() && m.layers[0]->target;
         // sequence sources with one k-block of embeddings: fused MLP (tok_tc.cuh)
-        static const bool tok_fused = std::getenv("MTFM_TOK_FUSED") == nullptr ||
-                                      std::atoi(std::getenv("MTFM_TOK_FUSED")) != 0;
         TokArgs ta{};
         std::vector<int> fused_src;
-        if (tok_fused && d == 256) {
+        double fused_f = 0, fused_in = 0, p_f1 = 0, p_f2 = 0, p_in = 0, p_rows = 0;
+        if (d == 256) {
             for (int s = 0; s < n_src && ta.n_src < kTokMaxSrc; ++s) {
                 const auto& si = m.sources[s];
                 const int M = static_cast<int>(B.src_cnt[s]);
@@ -1573,13 +1325,12 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                 ts.xhat_row0 = s < m.n_ctx_src ? B.src_base[s] : -1;
                 ta.n_tiles += static_cast<int>(cdiv(M, 128));
                 fused_src.push_back(s);
+                fused_f += 2.0 * M * (si.k_in * 2.0 * d + 2.0 * d * d);
+                fused_in += static_cast<double>(M) * si.k_pad;
             }
             ta.X = X;
             ta.xhat = m.act[ACT_XN].as<__nv_bfloat16>();
             ta.eps = static_cast<float>(m.cfg.eps);
-            // x̂ stores staged through shared memory (MTFM_TOK_XHAT=1: one row per lane, unstaged)
-            static const int tok_xhat_mode = std::getenv("MTFM_TOK_XHAT") ? std::atoi(std::getenv("MTFM_TOK_XHAT")) : 2;
-            ta.xhat_staged = tok_xhat_mode == 2 ? 1 : 0;
         }
         for (int s = 0; s < m.n_ctx_src; ++s)
             if (B.src_cnt[s] > 0 && std::find(fused_src.begin(), fused_src.end(), s) == fused_src.end())
@@ -1595,18 +1346,22 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                           EPI_SILU_BF16, w.b1.as<float>(), HID + B.hid_base[s], 2 * d, nullptr, 0, nullptr});
             p2.push_back({HID + B.hid_base[s], 2 * d, w.t2.as<__nv_bfloat16>(), 2 * d, M, d, 2 * d, EPI_BIAS_F32,
                           w.b2.as<float>(), X, d, rm.src_rows + B.src_base[s], 0, nullptr});
+            p_f1 += 2.0 * M * si.k_in * 2 * d;
+            p_f2 += 2.0 * M * 2 * d * d;
+            p_in += static_cast<double>(M) * si.k_pad;
+            p_rows += M;
         }
         if (ta.n_tiles > 0) {
-            StageScope sc(m, "tok_fused", tok_f1 + tok_f2, tok_in * el + Rd * d * 4);
+            StageScope sc(m, "tok_fused", fused_f, fused_in * el + (Rd - p_rows) * d * 4);
             launch_tok_fused(ta, st);
             ++L;
         }
         {
-            StageScope sc(m, "tok_mlp1", tok_f1, tok_in * el + Rd * 2 * d * el);
+            StageScope sc(m, "tok_mlp1", p_f1, p_in * el + p_rows * 2 * d * el);
             run_gemm_tc(p1, st, L, BT);
         }
         {
-            StageScope sc(m, "tok_mlp2", tok_f2, Rd * 2 * d * el + Rd * d * 4);
+            StageScope sc(m, "tok_mlp2", p_f2, p_rows * 2 * d * el + p_rows * d * 4);
             run_gemm_tc(p2, st, L, BT);
         }
     } else {
@@ -1659,114 +1414,70 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
     // attention FLOPs need sum(c_i): known after the plan; use the value of
     // the previous results() (same batch) for the profile annotation
     const double sc_full = static_cast<double>(B.sum_c_ctx + B.sum_c_t), sc_t = static_cast<double>(B.sum_c_t);
-    float2* statX = m.act[ACT_STATX].as<float2>();
-    float2* statA = m.act[ACT_STATA].as<float2>();
     if constexpr (kTc) {
-        // bf16 tensor-core path: GLN1 and the gate are fused into the GEMM A producers
-        bool ctx_stats_valid = false;  // X context rows only change in full layers
-        // full layer whose context-row GLN1 was produced by the preceding target run
-        // (same X context rows) into XNF rows [0, NE): only its T rows remain
-        size_t full_ctx_from_run = static_cast<size_t>(-1);
-        bool full_ctx_folded = false;  // ... as source-ordered xhat rows XN[0, NE) with folded f1 weights
-        T* XNF = XN + (static_cast<long long>(std::max(1, m.cfg.target_layers)) * NE + NT) * d;
-        int tl = 0;                     // index of the current target layer within its run
+        // Context rows X[0, NE) are the same for every target layer of a run and for the
+        // full layer right after it (target layers only update T rows, hta.hpp:158-184).
+        // At the start of a run they are normalised once, without the affine, into
+        // source order (xhat = XN[0, NE)); every context source's GLN1 affine is folded
+        // into its own copy of the K|V (target) / f1 (full) weights (LayerW::tfold), and
+        // the GEMM outputs are scattered back to X-row order.
+        size_t full_ctx_from_run = static_cast<size_t>(-1);  // full layer whose context rows come from xhat
+        T* XNT = XN + NE * d;                                 // T rows' GLN1 of the current target layer
+        T* XNF = XN + R * d;                                  // GLN1 of a full layer's rows (T rows only after a run)
+        int tl = 0;                                           // index of the current target layer within its run
         for (size_t li = 0; li < m.layers.size(); ++li) {
             const auto& Lw = m.layers[li];
-            if (m.fuse & 1) {
-                const long long r0 = ctx_stats_valid ? NE : 0;
-                StageScope sc(m, "row_stats", 0, (Rd - r0) * d * 4.0);
-                launch_row_stats<float>(X + r0 * d, d, R - r0, d, eps, statX + r0, st);
-                ++L;
-            }
             if (!Lw->target) {
                 // full layer (hta.hpp:138-155)
-                if (m.fuse & 1) {
-                    StageScope sc(m, "proj_full", 2.0 * Rd * d * pw, Rd * d * 4 + Rd * pw * el);
-                    TcProblem tp{nullptr, d, Lw->t1.as<__nv_bfloat16>(), d, static_cast<int>(R), pw, d, EPI_SILU_BF16,
-                                 Lw->b1.as<float>(), Pm, pw, nullptr, 0, nullptr};
-                    tp.amode = A_LN;
-                    tp.a_src = X;
-                    tp.stats = statX;
-                    tp.row_group = rm.src;
-                    tp.gain = Lw->g1g.as<float>();
-                    tp.gbias = Lw->g1b.as<float>();
-                    run_gemm_tc({tp}, st, L, BT);
+                const bool from_run = full_ctx_from_run == li;
+                if (from_run) {
+                    StageScope sc(m, "gln1", 0, Td * d * (4 + el));
+                    launch_gln<T>(X, d, NE, NT, d, rm.src, Lw->g1g.as<float>(), Lw->g1b.as<float>(), eps,
+                                  XNF + NE * d, d, st);
+                    ++L;
                 } else {
-                    T* XNL = XN;
-                    if (full_ctx_from_run == li) {
-                        XNL = XNF;
-                        StageScope sc(m, "gln1", 0, Td * d * (4 + el));
-                        launch_gln<T>(X, d, NE, NT, d, rm.src, Lw->g1g.as<float>(), Lw->g1b.as<float>(), eps,
-                                      XNF + NE * d, d, st);
-                        ++L;
-                    } else {
-                        StageScope sc(m, "gln1", 0, Rd * d * (4 + el));
-                        launch_gln<T>(X, d, 0, R, d, rm.src, Lw->g1g.as<float>(), Lw->g1b.as<float>(), eps, XN, d, st);
-                        ++L;
-                    }
-                    // U and Q|K|V as two contiguous matrices (one grouped launch): the gate
-                    // then streams U rows and the attention Q|K|V rows without gaps
+                    StageScope sc(m, "gln1", 0, Rd * d * (4 + el));
+                    launch_gln<T>(X, d, 0, R, d, rm.src, Lw->g1g.as<float>(), Lw->g1b.as<float>(), eps, XNF, d, st);
+                    ++L;
+                }
+                // U and Q|K|V as two contiguous matrices (one grouped launch): the gate
+                // then streams U rows and the attention Q|K|V rows without gaps
+                T* U = Pm;
+                T* QKV = Pm + R * hd;
+                const long long ldqkv = hd + 2 * gd;
+                {
                     StageScope sc(m, "proj_full", 2.0 * Rd * d * pw, Rd * d * el + Rd * pw * el);
-                    if (full_ctx_from_run == li && full_ctx_folded) {
-                        // context rows: per source, xhat rows x folded f1, scattered to X-row order;
-                        // T rows: their GLN1 rows XNF[NE, R) x f1, at row offset NE
-                        std::vector<TcProblem> pp;
-                        const bool seg = hd % 64 == 0 && (hd + 2 * gd) % 64 == 0 && std::getenv("MTFM_SEG") != nullptr;
+                    std::vector<TcProblem> pp;
+                    const long long r0 = from_run ? NE : 0;  // rows taken from XNF
+                    if (from_run) {
+                        // context rows: per source, xhat rows x folded f1, scattered to X-row order
                         for (int s = 0; s < m.n_ctx_src; ++s) {
                             const __nv_bfloat16* wf = Lw->tfold.as<__nv_bfloat16>() + static_cast<long long>(s) * pw * d;
                             const float* bfo = Lw->bfold.as<float>() + static_cast<long long>(s) * pw;
                             const int Ms = static_cast<int>(B.src_cnt[s]);
                             const int* rmap = rm.src_rows + B.src_base[s];
-                            if (seg) {
-                                // U | Q|K|V as two column segments of one problem (A read once)
-                                TcProblem tp{XN + B.src_base[s] * d, d, wf, d, Ms, pw, d, EPI_SILU_BF16, bfo, Pm, hd,
-                                             rmap, 0, nullptr};
-                                tp.n_seg = 2;
-                                tp.seg_n0[0] = 0;
-                                tp.seg_out[0] = Pm;
-                                tp.seg_ldo[0] = hd;
-                                tp.seg_n0[1] = hd;
-                                tp.seg_out[1] = Pm + R * hd;
-                                tp.seg_ldo[1] = hd + 2 * gd;
-                                pp.push_back(tp);
-                                continue;
-                            }
-                            pp.push_back({XN + B.src_base[s] * d, d, wf, d, Ms, hd, d, EPI_SILU_BF16, bfo, Pm, hd, rmap, 0,
+                            pp.push_back({XN + B.src_base[s] * d, d, wf, d, Ms, hd, d, EPI_SILU_BF16, bfo, U, hd, rmap, 0,
                                           nullptr});
                             pp.push_back({XN + B.src_base[s] * d, d, wf + static_cast<long long>(hd) * d, d, Ms,
-                                          hd + 2 * gd, d, EPI_SILU_BF16, bfo + hd, Pm + R * hd, hd + 2 * gd, rmap, 0,
-                                          nullptr});
+                                          hd + 2 * gd, d, EPI_SILU_BF16, bfo + hd, QKV, ldqkv, rmap, 0, nullptr});
                         }
-                        pp.push_back({XNF + NE * d, d, Lw->t1.as<__nv_bfloat16>(), d, static_cast<int>(NT), hd, d,
-                                      EPI_SILU_BF16, Lw->b1.as<float>(), Pm, hd, nullptr, NE, nullptr});
-                        pp.push_back({XNF + NE * d, d, Lw->t1.as<__nv_bfloat16>() + static_cast<long long>(hd) * d, d,
-                                      static_cast<int>(NT), hd + 2 * gd, d, EPI_SILU_BF16, Lw->b1.as<float>() + hd,
-                                      Pm + R * hd, hd + 2 * gd, nullptr, NE, nullptr});
-                        run_gemm_tc(pp, st, L, BT);
-                    } else
-                    run_gemm_tc({{XNL, d, Lw->t1.as<__nv_bfloat16>(), d, static_cast<int>(R), hd, d, EPI_SILU_BF16,
-                                  Lw->b1.as<float>(), Pm, hd, nullptr, 0, nullptr},
-                                 {XNL, d, Lw->t1.as<__nv_bfloat16>() + static_cast<long long>(hd) * d, d,
-                                  static_cast<int>(R), hd + 2 * gd, d, EPI_SILU_BF16, Lw->b1.as<float>() + hd,
-                                  Pm + R * hd, hd + 2 * gd, nullptr, 0, nullptr}},
-                                st, L, BT);
+                    }
+                    const int Mr = static_cast<int>(R - r0);
+                    pp.push_back({XNF + r0 * d, d, Lw->t1.as<__nv_bfloat16>(), d, Mr, hd, d, EPI_SILU_BF16,
+                                  Lw->b1.as<float>(), U, hd, nullptr, r0, nullptr});
+                    pp.push_back({XNF + r0 * d, d, Lw->t1.as<__nv_bfloat16>() + static_cast<long long>(hd) * d, d, Mr,
+                                  hd + 2 * gd, d, EPI_SILU_BF16, Lw->b1.as<float>() + hd, QKV, ldqkv, nullptr, r0,
+                                  nullptr});
+                    run_gemm_tc(pp, st, L, BT);
                 }
-                // P layout: split [U][R x hd] then [Q|K|V][R x (hd + 2gd)] unless the fused-LN
-                // path wrote the interleaved [R][U|Q|K|V]
-                const bool split_p = !(m.fuse & 1);
-                T* Uptr = Pm;
-                const long long ldu_p = split_p ? hd : pw;
-                T* QKV = split_p ? Pm + R * hd : Pm;
-                const long long ldqkv = split_p ? hd + 2 * gd : pw;
-                const int qc0 = split_p ? 0 : hd;
                 {
                     StageScope sc(m, "attn_full", 4.0 * hd * sc_full, Rd * (hd + 2 * gd) * el + Rd * hd * el);
                     AttnParams ap{};
                     ap.tiles = B.tiles_full.as<AttnTile>();
                     ap.n_tiles = n_full;
-                    ap.q_col0 = qc0;
-                    ap.k_col0 = qc0 + hd;
-                    ap.v_col0 = qc0 + hd + gd;
+                    ap.q_col0 = 0;
+                    ap.k_col0 = hd;
+                    ap.v_col0 = hd + gd;
                     ap.heads = m.H;
                     ap.kv_heads = m.G;
                     ap.hs = ag.hs;
@@ -1783,190 +1494,65 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                     run_attn_tc(m, ap, QKV, R, ldqkv, R, ldqkv, st);
                     ++L;
                 }
-                if (m.fuse & 2) {
-                    {
-                        StageScope sc(m, "attn_stats", 0, Rd * hd * el);
-                        launch_row_stats<__nv_bfloat16>(A, hd, R, hd, eps, statA, st);
-                        ++L;
-                    }
-                    StageScope sc(m, "f2_full", 2.0 * Rd * hd * d, Rd * hd * el * 2 + Rd * d * 8);
-                    TcProblem tp{nullptr, hd, Lw->tf2.as<__nv_bfloat16>(), hd, static_cast<int>(R), d, hd,
-                                 EPI_RESID_F32, Lw->f2b.as<float>(), X, d, nullptr, 0, X};
-                    tp.amode = A_GATE_TMA;
-                    tp.a_src = A;
-                    tp.stats = statA;
-                    tp.row_group = rm.src;
-                    tp.gain = Lw->g2g.as<float>();
-                    tp.gbias = Lw->g2b.as<float>();
-                    tp.u_src = Uptr;
-                    tp.ldu = ldu_p;
-                    run_gemm_tc({tp}, st, L, BT);
-                } else {
-                    {
-                        StageScope sc(m, "gate", 0, Rd * hd * el * 3);
-                        launch_gate<T>(A, hd, Uptr, ldu_p, R, hd, rm.src, Lw->g2g.as<float>(), Lw->g2b.as<float>(), eps, G,
-                                       hd, st);
-                        ++L;
-                    }
-                    StageScope sc(m, "f2_full", 2.0 * Rd * hd * d, Rd * hd * el + Rd * d * 8);
-                    run_gemm_tc({{G, hd, Lw->tf2.as<__nv_bfloat16>(), hd, static_cast<int>(R), d, hd, EPI_RESID_F32,
-                                  Lw->f2b.as<float>(), X, d, nullptr, 0, X}},
-                                st, L, BT);
+                {
+                    StageScope sc(m, "gate", 0, Rd * hd * el * 3);
+                    launch_gate<T>(A, hd, U, hd, R, hd, rm.src, Lw->g2g.as<float>(), Lw->g2b.as<float>(), eps, G, hd, st);
+                    ++L;
                 }
-                ctx_stats_valid = false;
+                StageScope sc(m, "f2_full", 2.0 * Rd * hd * d, Rd * hd * el + Rd * d * 8);
+                run_gemm_tc({{G, hd, Lw->tf2.as<__nv_bfloat16>(), hd, static_cast<int>(R), d, hd, EPI_RESID_F32,
+                              Lw->f2b.as<float>(), X, d, nullptr, 0, X}},
+                            st, L, BT);
             } else {
                 // target layer (hta.hpp:158-184): T rows only; H/R rows untouched
-                T* KVl = KV;  // this layer's K|V rows (context rows first, then T rows)
-                if (!(m.fuse & 1)) {
-                    // The context rows X[0, NE) are the same for every target layer of a
-                    // run (only T rows change), so at the first layer of the run their
-                    // GLN1 is computed once for all the run's layers and their K|V
-                    // projections go out in one grouped GEMM.
-                    if (li == 0 || !m.layers[li - 1]->target) {
-                        size_t lj = li;
-                        while (lj < m.layers.size() && m.layers[lj]->target) ++lj;
-                        const int kt = static_cast<int>(lj - li);
-                        // the full layer right after the run sees the same context rows
-                        // MTFM_XHAT=1: one normalised copy (xhat) + per-layer affine inside the
-                        // K|V GEMM's A producer (A_AFFINE_TMA) instead of one copy per layer
-                        static const bool use_xhat = std::getenv("MTFM_XHAT") && std::atoi(std::getenv("MTFM_XHAT")) != 0;
-                        // default: one normalised copy of the context rows in source order (xhat,
-                        // no affine); every context source's GLN1 affine is folded into its own
-                        // copy of the K|V (and the following full layer's f1) weights, and the
-                        // GEMM outputs are scattered back to X-row order
-                        long long ctx_rows = 0;
-                        for (int s = 0; s < m.n_ctx_src; ++s) ctx_rows += B.src_cnt[s];
-                        const bool fold = m.n_ctx_src > 0 && !use_xhat && ctx_rows == NE;
-                        const bool with_full =
-                            lj < m.layers.size() && !(m.fuse & 1) && (fold || kt + 1 <= kMaxGlnCopies);
-                        if (fold) {
-                            if (!(li == 0 && xhat_from_tok)) {
-                                GlnCopies gc{};
-                                gc.n = 1;
-                                gc.out[0] = XN;
-                                gc.in_rows = rm.src_rows;
-                                StageScope sc(m, "gln1", 0, NE * d * (4.0 + el));
-                                launch_gln_multi_bf16(X, d, NE, d, rm.src, gc, eps, d, st);
-                                ++L;
-                            }
-                            if (with_full) {
-                                full_ctx_from_run = lj;
-                                full_ctx_folded = true;
-                            }
-                            // per context source: the run's layers' K|V as column segments of one
-                            // problem (weights of layers li.. of the run stacked in Lw->tkv_run)
-                            std::vector<TcProblem> kvp;
-                            const bool seg = kt <= 4 && (2 * gd) % 64 == 0 && m.layers[li]->kv_run.p != nullptr &&
-                                             std::getenv("MTFM_SEG") != nullptr;
-                            for (int s = 0; s < m.n_ctx_src; ++s) {
-                                if (seg) {
-                                    const auto& Lr = m.layers[li];
-                                    TcProblem tp{XN + B.src_base[s] * d, d,
-                                                 Lr->kv_run.as<__nv_bfloat16>() + static_cast<long long>(s) * kt * 2 * gd * d,
-                                                 d, static_cast<int>(B.src_cnt[s]), kt * 2 * gd, d, EPI_SILU_BF16,
-                                                 Lr->kvb_run.as<float>() + static_cast<long long>(s) * kt * 2 * gd, KV, 2 * gd,
-                                                 rm.src_rows + B.src_base[s], 0, nullptr};
-                                    tp.n_seg = kt;
-                                    for (int c = 0; c < kt; ++c) {
-                                        tp.seg_n0[c] = c * 2 * gd;
-                                        tp.seg_out[c] = KV + static_cast<long long>(c) * R * 2 * gd;
-                                        tp.seg_ldo[c] = 2 * gd;
-                                    }
-                                    kvp.push_back(tp);
-                                    continue;
-                                }
-                                for (int c = 0; c < kt; ++c) {
-                                    const auto& Lc = m.layers[li + c];
-                                    kvp.push_back({XN + B.src_base[s] * d, d,
-                                                   Lc->tfold.as<__nv_bfloat16>() + static_cast<long long>(s) * 2 * gd * d, d,
-                                                   static_cast<int>(B.src_cnt[s]), 2 * gd, d, EPI_SILU_BF16,
-                                                   Lc->bfold.as<float>() + s * 2 * gd,
-                                                   KV + static_cast<long long>(c) * R * 2 * gd, 2 * gd,
-                                                   rm.src_rows + B.src_base[s], 0, nullptr});
-                                }
-                            }
-                            StageScope sc(m, "proj_ctx_kv", 2.0 * kt * NE * d * 2 * gd, NE * d * el + kt * NE * 2.0 * gd * el);
-                            run_gemm_tc(kvp, st, L, BT);
-                            tl = 0;
-                        }
-                        const int ncopy = fold ? 0 : (use_xhat ? 1 : kt) + (with_full ? 1 : 0);
-                        for (int c0 = 0; c0 < ncopy; c0 += kMaxGlnCopies) {
+                if (li == 0 || !m.layers[li - 1]->target) {
+                    // start of a target run: xhat of the context rows, then every layer's
+                    // context K|V from it in one grouped GEMM (per source and layer)
+                    size_t lj = li;
+                    while (lj < m.layers.size() && m.layers[lj]->target) ++lj;
+                    const int kt = static_cast<int>(lj - li);
+                    if (NE > 0) {
+                        if (!(li == 0 && xhat_from_tok)) {
                             GlnCopies gc{};
-                            gc.n = std::min(ncopy - c0, kMaxGlnCopies);
-                            for (int c = 0; c < gc.n; ++c) {
-                                const int cc = c0 + c;
-                                const bool full_copy = with_full && cc == ncopy - 1;
-                                const auto& Lc = m.layers[full_copy ? lj : li + cc];
-                                gc.gain[c] = (use_xhat && !full_copy) ? nullptr : Lc->g1g.as<float>();
-                                gc.bias[c] = (use_xhat && !full_copy) ? nullptr : Lc->g1b.as<float>();
-                                gc.out[c] = full_copy ? XNF : XN + static_cast<long long>(cc) * NE * d;
-                            }
-                            StageScope sc(m, "gln1", 0, NE * d * (4.0 + gc.n * el));
+                            gc.n = 1;
+                            gc.out[0] = XN;
+                            gc.in_rows = rm.src_rows;
+                            StageScope sc(m, "gln1", 0, NE * d * (4.0 + el));
                             launch_gln_multi_bf16(X, d, NE, d, rm.src, gc, eps, d, st);
                             ++L;
                         }
-                        if (with_full && !fold) full_ctx_from_run = lj;
                         std::vector<TcProblem> kvp;
-                        for (int c = 0; c < kt && !fold; ++c) {
-                            const auto& Lc = m.layers[li + c];
-                            T* a_in = XN + static_cast<long long>(use_xhat ? 0 : c) * NE * d;
-                            kvp.push_back({a_in, d, Lc->tkv.as<__nv_bfloat16>(), d,
-                                           static_cast<int>(NE), 2 * gd, d, EPI_SILU_BF16, Lc->bkv.as<float>(),
-                                           KV + static_cast<long long>(c) * R * 2 * gd, 2 * gd, nullptr, 0, nullptr});
-                            if (use_xhat) {
-                                TcProblem& tp = kvp.back();
-                                tp.amode = A_AFFINE_TMA;
-                                tp.a_src = a_in;
-                                tp.row_group = rm.src;
-                                tp.g_row0 = 0;
-                                tp.gain = Lc->g1g.as<float>();
-                                tp.gbias = Lc->g1b.as<float>();
+                        for (int s = 0; s < m.n_ctx_src; ++s)
+                            for (int c = 0; c < kt; ++c) {
+                                const auto& Lc = m.layers[li + c];
+                                kvp.push_back({XN + B.src_base[s] * d, d,
+                                               Lc->tfold.as<__nv_bfloat16>() + static_cast<long long>(s) * 2 * gd * d, d,
+                                               static_cast<int>(B.src_cnt[s]), 2 * gd, d, EPI_SILU_BF16,
+                                               Lc->bfold.as<float>() + s * 2 * gd,
+                                               KV + static_cast<long long>(c) * R * 2 * gd, 2 * gd,
+                                               rm.src_rows + B.src_base[s], 0, nullptr});
                             }
-                        }
-                        if (!fold) {
-                            StageScope sc(m, "proj_ctx_kv", 2.0 * kt * NE * d * 2 * gd,
-                                          kt * NE * (d + 2.0 * gd) * el);
-                            run_gemm_tc(kvp, st, L, BT);
-                            tl = 0;
-                        }
+                        StageScope sc(m, "proj_ctx_kv", 2.0 * kt * NE * d * 2 * gd, NE * d * el + kt * NE * 2.0 * gd * el);
+                        run_gemm_tc(kvp, st, L, BT);
                     }
-                    KVl = KV + static_cast<long long>(tl) * R * 2 * gd;
-                    T* XNT = XN + static_cast<long long>(m.cfg.target_layers) * NE * d;
-                    {
-                        StageScope sc(m, "gln1", 0, Td * d * (4 + el));
-                        launch_gln<T>(X, d, NE, NT, d, rm.src, Lw->g1g.as<float>(), Lw->g1b.as<float>(), eps, XNT, d,
-                                      st);
-                        ++L;
-                    }
+                    if (lj < m.layers.size()) full_ctx_from_run = lj;
+                    tl = 0;
+                }
+                T* KVl = KV + static_cast<long long>(tl) * R * 2 * gd;  // this layer's K|V rows (context, then T)
+                {
+                    StageScope sc(m, "gln1", 0, Td * d * (4 + el));
+                    launch_gln<T>(X, d, NE, NT, d, rm.src, Lw->g1g.as<float>(), Lw->g1b.as<float>(), eps, XNT, d, st);
+                    ++L;
+                }
+                {
                     StageScope sc(m, "proj_target", 2.0 * Td * d * (2 * gd + 2 * hd), Td * d * el + Td * (2 * gd + 2 * hd) * el);
                     run_gemm_tc({{XNT, d, Lw->tkv.as<__nv_bfloat16>(), d, static_cast<int>(NT), 2 * gd, d, EPI_SILU_BF16,
                                   Lw->bkv.as<float>(), KVl + NE * 2 * gd, 2 * gd, nullptr, 0, nullptr},
                                  {XNT, d, Lw->t1.as<__nv_bfloat16>(), d, static_cast<int>(NT), 2 * hd, d,
                                   EPI_SILU_BF16, Lw->b1.as<float>(), UQ, 2 * hd, nullptr, 0, nullptr}},
                                 st, L, BT);
-                    ++tl;
-                } else {
-                    StageScope sc(m, "proj_target", 2.0 * (Rd * d * 2 * gd + Td * d * 2 * hd),
-                                  Rd * d * 4 + Rd * 2 * gd * el + Td * 2 * hd * el);
-                    TcProblem kv{nullptr, d, Lw->tkv.as<__nv_bfloat16>(), d, static_cast<int>(R), 2 * gd, d,
-                                 EPI_SILU_BF16, Lw->bkv.as<float>(), KV, 2 * gd, nullptr, 0, nullptr};
-                    kv.amode = A_LN;
-                    kv.a_src = X;
-                    kv.stats = statX;
-                    kv.row_group = rm.src;
-                    kv.gain = Lw->g1g.as<float>();
-                    kv.gbias = Lw->g1b.as<float>();
-                    TcProblem uq = kv;
-                    uq.Bt = Lw->t1.as<__nv_bfloat16>();
-                    uq.M = static_cast<int>(NT);
-                    uq.N = 2 * hd;
-                    uq.bias = Lw->b1.as<float>();
-                    uq.out = UQ;
-                    uq.ldo = 2 * hd;
-                    uq.a_row0 = NE;
-                    uq.g_row0 = NE;
-                    run_gemm_tc({kv, uq}, st, L, BT);
                 }
+                ++tl;
                 {
                     StageScope sc(m, "attn_target", 4.0 * hd * sc_t, Rd * 2 * gd * el + Td * 2 * hd * el);
                     AttnParams ap{};
@@ -1991,38 +1577,16 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                     run_attn_tc(m, ap, UQ, NT, 2 * hd, R, 2 * gd, st);
                     ++L;
                 }
-                if (!(m.fuse & 2)) {
-                    {
-                        StageScope sc(m, "gate", 0, Td * hd * el * 3);
-                        launch_gate<T>(A, hd, UQ, 2 * hd, NT, hd, rm.src + NE, Lw->g2g.as<float>(), Lw->g2b.as<float>(),
-                                       eps, G, hd, st);
-                        ++L;
-                    }
-                    StageScope sc(m, "f2_target", 2.0 * Td * hd * d, Td * hd * el + Td * d * 8);
-                    run_gemm_tc({{G, hd, Lw->tf2.as<__nv_bfloat16>(), hd, static_cast<int>(NT), d, hd, EPI_RESID_F32,
-                                  Lw->f2b.as<float>(), X, d, nullptr, NE, X}},
-                                st, L, BT);
-                } else {
-                    {
-                        StageScope sc(m, "attn_stats", 0, Td * hd * el);
-                        launch_row_stats<__nv_bfloat16>(A, hd, NT, hd, eps, statA, st);
-                        ++L;
-                    }
-                    StageScope sc(m, "f2_target", 2.0 * Td * hd * d, Td * hd * el * 2 + Td * d * 8);
-                    TcProblem tp{nullptr, hd, Lw->tf2.as<__nv_bfloat16>(), hd, static_cast<int>(NT), d, hd,
-                                 EPI_RESID_F32, Lw->f2b.as<float>(), X, d, nullptr, NE, X};
-                    tp.amode = A_GATE_TMA;
-                    tp.a_src = A;
-                    tp.stats = statA;
-                    tp.row_group = rm.src;
-                    tp.g_row0 = NE;
-                    tp.gain = Lw->g2g.as<float>();
-                    tp.gbias = Lw->g2b.as<float>();
-                    tp.u_src = UQ;
-                    tp.ldu = 2 * hd;
-                    run_gemm_tc({tp}, st, L, BT);
+                {
+                    StageScope sc(m, "gate", 0, Td * hd * el * 3);
+                    launch_gate<T>(A, hd, UQ, 2 * hd, NT, hd, rm.src + NE, Lw->g2g.as<float>(), Lw->g2b.as<float>(),
+                                   eps, G, hd, st);
+                    ++L;
                 }
-                ctx_stats_valid = true;
+                StageScope sc(m, "f2_target", 2.0 * Td * hd * d, Td * hd * el + Td * d * 8);
+                run_gemm_tc({{G, hd, Lw->tf2.as<__nv_bfloat16>(), hd, static_cast<int>(NT), d, hd, EPI_RESID_F32,
+                              Lw->f2b.as<float>(), X, d, nullptr, NE, X}},
+                            st, L, BT);
             }
         }
     } else {
@@ -2168,7 +1732,9 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
 
     // ---- K5: heads (heads.hpp:47-99) + records
     float* Y = m.act[ACT_Y].as<float>();
-    const double hflops = 2.0 * Td * d * m.head_n;
+    // algorithmic head work: every T row's experts, and per record its task's gate;
+    // the GEMM also evaluates the other scenarios' gate columns, which are not counted
+    const double hflops = 2.0 * (Td * m.cfg.experts * d * m.cfg.d_expert + static_cast<double>(B.n_records) * d * m.cfg.experts);
     if constexpr (kTc) {
         {
             StageScope sc(m, "to_bf16", 0, Td * d * 6);
@@ -2211,7 +1777,7 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
     ha.rec_logit = B.rec_logit.as<float>();
     ha.rec_prob = B.rec_prob.as<double>();
     {
-        StageScope sc(m, "heads", 2.0 * B.n_records * m.cfg.experts * m.cfg.d_expert,
+        StageScope sc(m, "heads", 2.0 * B.n_records * m.cfg.d_expert,
                       Td * m.head_ld * 4 + B.n_records * 32.0);
         launch_heads(ha, st, m.n_tasks_total);
         ck(cudaGetLastError(), "heads launch");
@@ -2366,9 +1932,8 @@ mtfm_status mtfm_cuda_create(int device, const mtfm_model_desc* md, const mtfm_s
         add_seq(1, sd->n_rt, sd->rt_ids, sd->rt_nslots, sd->rt_vocabs);
         m->n_hist = sd->n_hist;
         m->n_rt = sd->n_rt;
-        // GLN1 folded into the context-row projections (bf16 path; MTFM_FOLD=0 keeps per-layer copies)
-        static const bool fold = std::getenv("MTFM_FOLD") == nullptr || std::atoi(std::getenv("MTFM_FOLD")) != 0;
-        if (fold && precision == MTFM_PRECISION_BF16) m->n_ctx_src = sd->n_hist + sd->n_rt;
+        // GLN1 folded into the context-row projections (bf16 path)
+        if (precision == MTFM_PRECISION_BF16) m->n_ctx_src = sd->n_hist + sd->n_rt;
         int p = 0, tp = 0;
         for (int i = 0; i < sd->n_scen; ++i) {
             SourceInfo s{};
@@ -2397,7 +1962,6 @@ mtfm_status mtfm_cuda_create(int device, const mtfm_model_desc* md, const mtfm_s
         ck(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking), "stream");
         ck(cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking), "copy stream");
         ck(cudaStreamCreateWithFlags(&m->d2h_stream, cudaStreamNonBlocking), "d2h stream");
-        if (const char* f = std::getenv("MTFM_FUSE")) m->fuse = std::atoi(f);
         *out = m.release();
     });
 }
@@ -2541,30 +2105,14 @@ mtfm_status mtfm_cuda_batch_free(mtfm_cuda_batch* b) {
 
 mtfm_status mtfm_cuda_forward(mtfm_cuda_model* m, const mtfm_packed_batch* b, int32_t only_scenario,
                               mtfm_records* out) {
-    const auto t0 = std::chrono::steady_clock::now();
     mtfm_status s = guard([&] {
         if (!m) fail(MTFM_CONTRACT_ERROR, "null argument");
         ck(cudaSetDevice(m->device), "cudaSetDevice");
         if (!m->ws) m->ws = std::make_unique<mtfm_cuda_batch>();  // device buffers only grow
         prepare(*m, b, only_scenario, *m->ws);
     });
-    static const bool host_timing = std::getenv("MTFM_HOST_TIMING") != nullptr;
-    auto now = [] { return std::chrono::steady_clock::now(); };
-    auto t1 = now();
-    if (host_timing) cudaStreamSynchronize(m->stream);
-    auto t2 = now();
     if (s == MTFM_OK) s = mtfm_cuda_batch_run(m, m->ws.get());
-    auto t3 = now();
-    if (host_timing) cudaStreamSynchronize(m->stream);
-    auto t4 = now();
     if (s == MTFM_OK) s = mtfm_cuda_batch_results(m, m->ws.get(), out);
-    auto t5 = now();
-    if (host_timing) {
-        auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
-        std::fprintf(stderr, "host timing: prepare %.0f us, ", us(t0, t1));
-        std::fprintf(stderr, "h2d-drain %.0f us, run enqueue %.0f us, device %.0f us, results %.0f us\n",
-                     us(t1, t2), us(t2, t3), us(t3, t4), us(t4, t5));
-    }
     return s;
 }
 

@@ -295,56 +295,6 @@ __device__ __forceinline__ uint32_t silu2_bf16(float s0, float s1) {
     return out;
 }
 
-// Two SiLUs -> packed bf16x2 without the SFU: y = s / (1 + 2^t), t = -s*log2(e)
-// clamped to [-126, 126]; 2^t = 2^round(t) * p(frac) with a degree-3 minimax
-// p (rel. err 7.5e-5) and the exponent added in the integer domain; the
-// reciprocal is a magic-constant seed plus two Newton steps. Relative error
-// <= 8e-5 over all finite s (scripts/silu_emu_check.py), below the bf16
-// rounding of the result. Runs on the FMA/ALU pipes, so attention can split
-// its SiLUs between this and MUFU.TANH (silu2_bf16).
-__device__ __forceinline__ uint32_t silu2_bf16_fma(float s0, float s1) {
-    uint64_t sv, tv, jv, nv, fv, pv, ev, dv, rv, qv, yv;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(sv) : "f"(s0), "f"(s1));
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(tv) : "l"(sv), "l"(0xbfb8aa3bbfb8aa3bull));  // -log2(e)
-    {
-        float t0, t1;
-        asm("mov.b64 {%0, %1}, %2;" : "=f"(t0), "=f"(t1) : "l"(tv));
-        t0 = fminf(fmaxf(t0, -126.f), 126.f);
-        t1 = fminf(fmaxf(t1, -126.f), 126.f);
-        asm("mov.b64 %0, {%1, %2};" : "=l"(tv) : "f"(t0), "f"(t1));
-    }
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(jv) : "l"(tv), "l"(0x4b4000004b400000ull));  // + 1.5*2^23: round
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(nv) : "l"(jv), "l"(0xcb400000cb400000ull));  // n = round(t)
-    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(fv) : "l"(tv), "l"(nv));                    // f in [-0.5, 0.5]
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(pv) : "l"(fv), "l"(0x3d61fbaf3d61fbafull), "l"(0x3e786f0e3e786f0eull));
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(pv) : "l"(pv), "l"(fv), "l"(0x3f31798d3f31798dull));
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(pv) : "l"(pv), "l"(fv), "l"(0x3f7ffb493f7ffb49ull));
-    {
-        uint32_t p0, p1, j0, j1;
-        asm("mov.b64 {%0, %1}, %2;" : "=r"(p0), "=r"(p1) : "l"(pv));
-        asm("mov.b64 {%0, %1}, %2;" : "=r"(j0), "=r"(j1) : "l"(jv));
-        p0 += j0 << 23;  // 2^n: n sits in the low mantissa bits of j
-        p1 += j1 << 23;
-        asm("mov.b64 %0, {%1, %2};" : "=l"(ev) : "r"(p0), "r"(p1));
-    }
-    asm("fma.rn.f32x2 %0, %1, %2, %2;" : "=l"(dv) : "l"(ev), "l"(0xbf800000bf800000ull));  // -(1 + e)
-    {
-        uint32_t d0, d1;
-        asm("mov.b64 {%0, %1}, %2;" : "=r"(d0), "=r"(d1) : "l"(dv));
-        asm("mov.b64 %0, {%1, %2};" : "=l"(rv) : "r"(0xfef311c3u - d0), "r"(0xfef311c3u - d1));  // ~1/(1+e)
-    }
-#pragma unroll
-    for (int it = 0; it < 2; ++it) {
-        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(qv) : "l"(dv), "l"(rv), "l"(0x3f8000003f800000ull));  // 1 - (1+e) r
-        asm("fma.rn.f32x2 %0, %1, %2, %1;" : "=l"(rv) : "l"(rv), "l"(qv));
-    }
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(yv) : "l"(sv), "l"(rv));
-    float y0, y1;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(y0), "=f"(y1) : "l"(yv));
-    uint32_t out;
-    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(out) : "f"(y1), "f"(y0));
-    return out;
-}
 
 __device__ __forceinline__ float silu_f32(float x) {
     // x * sigmoid(x), sigmoid split by sign like kernels.hpp:96-103

@@ -52,8 +52,6 @@ struct TokArgs {
     float* X;             // [rows][256] fp32
     __nv_bfloat16* xhat;  // [rows][256] bf16, source order: the first target run's normalised context rows
     float eps;
-    int xhat_staged;      // 1: x̂ stores go through shared memory (8 rows x 64 B per store instruction)
-    unsigned long long* trace;  // timing experiments only (-DMTFM_TOK_TRACE): CTA 0 clock stamps
 };
 
 namespace tok_detail {
@@ -66,11 +64,8 @@ constexpr int W1_BYTES = HC * 64 * 2;               // 8 KB
 constexpr int W2_BYTES = D * 64 * 2;                // 32 KB
 constexpr int kXStages = 2, kWStages = 3;
 constexpr int ONES_BYTES = 4096;
-constexpr int STG_BYTES = 12 * 32 * 8 * 4;          // Y drain staging: 32 rows x 8 fp32 per epilogue warp
-#ifndef MTFM_TOK_DRAIN_SLOTS
-#define MTFM_TOK_DRAIN_SLOTS 1
-#endif
-constexpr int kDrainSlots = MTFM_TOK_DRAIN_SLOTS;   // 1: the 4 Y warps drain Y; 3: the SiLU warps help
+// staging: [0, 8 KB) x̂ rows (2 KB per Y warp), [8 KB, 12 KB) Y drain (32 rows x 8 fp32 per Y warp)
+constexpr int STG_BYTES = 12 * 32 * 8 * 4;
 constexpr int BAR_BYTES = 1024;
 constexpr int SMEM = 1024 + kXStages * XS_BYTES + kWStages * (W1_BYTES + W2_BYTES) + ONES_BYTES + STG_BYTES +
                      BAR_BYTES;
@@ -111,13 +106,6 @@ __global__ void __launch_bounds__(512, 1) tok_fused_kernel(const __grid_constant
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 26);
 
     const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
-#ifdef MTFM_TOK_TRACE
-    auto trace = [&](int slot) {
-        if (args.trace && blockIdx.x == 0 && lane == 0 && slot < 1024) args.trace[slot] = clock64();
-    };
-#else
-    auto trace = [&](int) {};
-#endif
     constexpr uint32_t kWarpMma = 15, kWarpTma = 14, kWarpTmaW2 = 13, kWarpAlloc = 12;
 
     for (int i = threadIdx.x; i < ONES_BYTES / 16; i += blockDim.x)
@@ -139,7 +127,7 @@ __global__ void __launch_bounds__(512, 1) tok_fused_kernel(const __grid_constant
             ptx::mbar_init(&w2_empty[i], 1);
         }
         ptx::mbar_init(y_full, 1);
-        ptx::mbar_init(y_empty, 4 * kDrainSlots);  // every draining warp arrives
+        ptx::mbar_init(y_empty, 4);  // every draining warp arrives
         ptx::fence_mbar_init();
         for (int i = 0; i < args.n_src; ++i) {
             ptx::tma_prefetch(&args.s[i].tma_e);
@@ -155,13 +143,12 @@ __global__ void __launch_bounds__(512, 1) tok_fused_kernel(const __grid_constant
     // prologue done (barriers, TMEM, SMEM tables): wait for the producer of our inputs
     MTFM_PDL_ENTRY();
 
-    // Y drain, shared by all 12 epilogue warps once a tile's GEMM2 is done:
-    // warp (quarter q, slot ds of 3) takes column blocks cb = ds, ds + 3, ...
-    // of its 32 rows; each 32 x 8 fp32 sub-block goes through a 1 KB staging
+    // Y drain by the 4 Y warps once a tile's GEMM2 is done: warp (quarter q)
+    // takes its 32 rows; each 32 x 8 fp32 sub-block goes through a 1 KB staging
     // slot (lane = row on the way in, 2 lanes per row on the way out) so every
     // global store writes whole 32 B sectors of 16 rows. Y is handed back to the
     // GEMM2 warp as soon as the TMEM reads are done.
-    auto drain = [&](uint32_t n_t, int t, uint32_t q, int ds, int slot, int nslots) {
+    auto drain = [&](uint32_t n_t, int t, uint32_t q, int slot) {
         int s, m0;
         tok_detail::decode(args, t, s, m0);
         const TokSource& src = args.s[s];
@@ -174,25 +161,28 @@ __global__ void __launch_bounds__(512, 1) tok_fused_kernel(const __grid_constant
             orow[j] = m < src.M ? static_cast<long long>(__ldg(src.row_map + m)) : -1;
         }
         const uint32_t lane_addr = (q * 32u) << 16;
-        // xhat (one drain slot only: lane = row holds every column of its row across cb)
-        const bool xh = src.xhat_row0 >= 0 && nslots == 1;
-        float ssum = 0.f, ssq = 0.f;
+        // xhat: lane = row holds every column of its row across cb. Row sums are shifted by a
+        // pivot (the row's first value) so that |mean| >> std does not cancel in E[y^2] - mean^2
+        const bool xh = src.xhat_row0 >= 0;
+        float ssum = 0.f, ssq = 0.f, piv = 0.f;
         ptx::mbar_wait(y_full, n_t & 1);
         ptx::tc_fence_after();
 #pragma unroll 1
-        for (int cb = ds; cb < D / 32; cb += nslots) {
+        for (int cb = 0; cb < D / 32; ++cb) {
             float v[32];
             ptx::tmem_ld16(tmem + lane_addr + Y_COL + cb * 32, *reinterpret_cast<float(*)[16]>(v));
             ptx::tmem_ld16(tmem + lane_addr + Y_COL + cb * 32 + 16, *reinterpret_cast<float(*)[16]>(v + 16));
             ptx::tmem_ld_wait();
             if (xh) {
+                if (cb == 0) piv = v[0];
 #pragma unroll
                 for (int e = 0; e < 32; ++e) {
-                    ssum += v[e];
-                    ssq = fmaf(v[e], v[e], ssq);
+                    const float y = v[e] - piv;
+                    ssum += y;
+                    ssq = fmaf(y, y, ssq);
                 }
             }
-            if (!xh && cb + nslots >= D / 32) {
+            if (!xh && cb == D / 32 - 1) {
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(y_empty);  // Y is free for the next tile's GEMM2
@@ -221,11 +211,10 @@ __global__ void __launch_bounds__(512, 1) tok_fused_kernel(const __grid_constant
             // GLN of hta.hpp:104-109 without the affine, which the folded K|V / f1 weights carry).
             // Y goes back to the GEMM2 warp after this pass's last TMEM load. (Reading the row
             // back from X instead, after releasing Y, was 3x slower: one row per lane.)
-            const float mean = ssum * (1.f / D);
-            const float var = fmaxf(ssq * (1.f / D) - mean * mean, 0.f);
+            const float dm = ssum * (1.f / D);
+            const float mean = piv + dm;
+            const float var = fmaxf(ssq * (1.f / D) - dm * dm, 0.f);
             const float rstd = rsqrtf(var + args.eps);
-            const int m = m0 + static_cast<int>(q * 32 + lane);
-            __nv_bfloat16* xr = args.xhat + (src.xhat_row0 + m) * D;
 #pragma unroll 1
             for (int cb = 0; cb < D / 32; ++cb) {
                 float v[32];
@@ -237,10 +226,9 @@ __global__ void __launch_bounds__(512, 1) tok_fused_kernel(const __grid_constant
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(y_empty);  // Y is free for the next tile's GEMM2
                 }
-                if (args.xhat_staged) {
-                    // 2 KB per warp from the staging slots the SiLU warps leave idle at one drain
-                    // slot: row r = lane, 16 B chunk j at (j ^ (r >> 1 & 3)) (conflict-free both ways);
-                    // then 4 lanes per row, 8 rows x 64 B per store instruction
+                {
+                    // 2 KB per warp: row r = lane, 16 B chunk j at (j ^ (r >> 1 & 3)) (conflict-free
+                    // both ways); then 4 lanes per row, 8 rows x 64 B per store instruction
                     uint8_t* xb = reinterpret_cast<uint8_t*>(stg + (slot - 8) * 2 * 32 * 8);
 #pragma unroll
                     for (int j = 0; j < 4; ++j)
@@ -259,14 +247,6 @@ __global__ void __launch_bounds__(512, 1) tok_fused_kernel(const __grid_constant
                         if (mr < src.M) *reinterpret_cast<uint4*>(args.xhat + (src.xhat_row0 + mr) * D + cb * 32 + c * 8) = w;
                     }
                     __syncwarp();
-                } else if (m < src.M) {
-#pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        *reinterpret_cast<uint4*>(xr + cb * 32 + 8 * j) =
-                            make_uint4(pack_bf16((v[8 * j] - mean) * rstd, (v[8 * j + 1] - mean) * rstd),
-                                       pack_bf16((v[8 * j + 2] - mean) * rstd, (v[8 * j + 3] - mean) * rstd),
-                                       pack_bf16((v[8 * j + 4] - mean) * rstd, (v[8 * j + 5] - mean) * rstd),
-                                       pack_bf16((v[8 * j + 6] - mean) * rstd, (v[8 * j + 7] - mean) * rstd));
                 }
             }
         }
@@ -324,10 +304,8 @@ __global__ void __launch_bounds__(512, 1) tok_fused_kernel(const __grid_constant
             ptx::mbar_wait(y_empty, (n_t & 1) ^ 1);              // the previous tile's Y has been read out
             for (int c = 0; c < NCH; ++c, ++h) {
                 const uint32_t hb = h & 1, wb = h % kWStages;
-                trace(16 * (n_t * 8 + c) + 4);
                 ptx::mbar_wait(&hb_full[hb], (h >> 1) & 1);
                 ptx::mbar_wait(&w2_full[wb], (h / kWStages) & 1);
-                trace(16 * (n_t * 8 + c) + 5);
                 ptx::tc_fence_after();
                 if (ptx::elect_one()) {
                     const uint32_t w2 = ptx::smem_u32(w2s + wb * W2_BYTES);
@@ -364,10 +342,8 @@ __global__ void __launch_bounds__(512, 1) tok_fused_kernel(const __grid_constant
             ptx::mbar_wait(&x_full[xb], (n_t >> 1) & 1);
             for (int c = 0; c < NCH; ++c, ++h) {
                 const uint32_t wb = h % kWStages, hb = h & 1;
-                trace(16 * (n_t * 8 + c) + 0);
                 ptx::mbar_wait(&w1_full[wb], (h / kWStages) & 1);
                 ptx::mbar_wait(&hacc_empty[hb], ((h >> 1) & 1) ^ 1);
-                trace(16 * (n_t * 8 + c) + 1);
                 ptx::tc_fence_after();
                 if (ptx::elect_one()) {
                     const uint32_t e = ptx::smem_u32(xst), w1 = ptx::smem_u32(w1s + wb * W1_BYTES);
@@ -392,10 +368,7 @@ __global__ void __launch_bounds__(512, 1) tok_fused_kernel(const __grid_constant
         uint32_t n_t = 0;
         for (int t = blockIdx.x; t < args.n_tiles; t += gridDim.x, ++n_t) {
             for (int c = g; c < NCH; c += 2, ++k) {
-                const int sb = 512 + 8 * static_cast<int>(k) + 4 * static_cast<int>(g);
-                if (q == 0) trace(sb + 0);
                 ptx::mbar_wait(&hacc_full[g], k & 1);
-                if (q == 0) trace(sb + 1);
                 ptx::tc_fence_after();
                 uint32_t packed[HC / 2];
 #pragma unroll
@@ -410,10 +383,8 @@ __global__ void __launch_bounds__(512, 1) tok_fused_kernel(const __grid_constant
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&hacc_empty[g]);
-                if (q == 0) trace(sb + 2);
                 // Hb[g] must have been consumed by GEMM2 of this group's previous chunk
                 ptx::mbar_wait(&hb_empty[g], (k & 1) ^ 1);
-                if (q == 0) trace(sb + 3);
                 ptx::tc_fence_after();
                 ptx::tmem_st16(tmem + lane_addr + HB_COL + g * (HC / 2), *reinterpret_cast<uint32_t(*)[16]>(packed));
                 ptx::tmem_st16(tmem + lane_addr + HB_COL + g * (HC / 2) + 16,
@@ -423,13 +394,11 @@ __global__ void __launch_bounds__(512, 1) tok_fused_kernel(const __grid_constant
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&hb_full[g]);
             }
-            if (kDrainSlots == 3) drain(n_t, t, q, static_cast<int>(g), static_cast<int>(warp), 3);
         }
     } else if (warp < 12) {
-        // ------------------------------------------------ Y epilogue (third drain slot)
+        // ------------------------------------------------ Y epilogue
         uint32_t n_t = 0;
-        for (int t = blockIdx.x; t < args.n_tiles; t += gridDim.x, ++n_t)
-            drain(n_t, t, warp & 3, kDrainSlots - 1, static_cast<int>(warp), kDrainSlots);
+        for (int t = blockIdx.x; t < args.n_tiles; t += gridDim.x, ++n_t) drain(n_t, t, warp & 3, static_cast<int>(warp));
     }
     ptx::tc_fence_before();
     __syncthreads();

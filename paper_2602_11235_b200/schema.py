@@ -177,3 +177,56 @@ def normalize_batch(batch: dict) -> dict:
 
 def batch_nbytes(batch: dict) -> int:
     return int(sum(np.asarray(batch[k]).nbytes for k in BATCH_KEYS))
+
+
+def param_specs(schemas: SchemaSet, cfg: ModelConfig):
+    """[(name, rows, cols)] in Model::register_params order (model.hpp:377-463);
+    host-side, no device needed. The library registers the same list
+    (mtfm_cuda_param_name)."""
+    h = cfg.hta
+    d, de = h.d_model, cfg.d_emb
+    dh = d // h.heads
+    hd, gd = h.heads * dh, h.kv_heads * dh
+    out = []
+    srcs = ([("h", s.seq_id, [s.feature_vocabs]) for s in schemas.hist] +
+            [("r", s.seq_id, [s.feature_vocabs]) for s in schemas.rt] +
+            [("s", s.scenario_id, [s.user_feature_vocabs, s.cross_feature_vocabs, s.item_feature_vocabs])
+             for s in schemas.scenarios])
+    for kind, sid, blocks in srcs:
+        base = f"tok/{kind}{sid}"
+        k_in = 0
+        if kind != "s":
+            for k, v in enumerate(blocks[0]):
+                out.append((f"{base}/emb{k}", v, de))
+                k_in += de
+        else:
+            for pre, vs in zip(("emb_u", "emb_c", "emb_i"), blocks):
+                for k, v in enumerate(vs):
+                    out.append((f"{base}/{pre}{k}", v, de))
+                    k_in += de
+        out += [(f"{base}/mlp_w1", k_in, 2 * d), (f"{base}/mlp_b1", 1, 2 * d), (f"{base}/mlp_w2", 2 * d, d),
+                (f"{base}/mlp_b2", 1, d)]
+    keys = [("h", s.seq_id, False) for s in schemas.hist] + [("r", s.seq_id, False) for s in schemas.rt] + \
+        [("t", s.scenario_id, True) for s in schemas.scenarios]
+    for b in range(h.blocks):
+        for l in range(h.target_layers + h.full_layers):
+            tgt = l < h.target_layers
+            base = f"hta/b{b}/l{l}"
+            if tgt:
+                out += [(f"{base}/fuq_w", d, 2 * hd), (f"{base}/fuq_b", 1, 2 * hd), (f"{base}/fkv_w", d, 2 * gd),
+                        (f"{base}/fkv_b", 1, 2 * gd)]
+            else:
+                out += [(f"{base}/f1_w", d, 2 * hd + 2 * gd), (f"{base}/f1_b", 1, 2 * hd + 2 * gd)]
+            out += [(f"{base}/f2_w", hd, d), (f"{base}/f2_b", 1, d)]
+            for k, sid, scen in keys:
+                out += [(f"{base}/gln1/{k}{sid}/gain", 1, d), (f"{base}/gln1/{k}{sid}/bias", 1, d)]
+                if not tgt or scen:
+                    out += [(f"{base}/gln2/{k}{sid}/gain", 1, hd), (f"{base}/gln2/{k}{sid}/bias", 1, hd)]
+    for e in range(cfg.experts):
+        out += [(f"head/expert{e}_w", d, cfg.d_expert), (f"head/expert{e}_b", 1, cfg.d_expert)]
+    for s in schemas.scenarios:
+        for t in s.tasks:
+            base = f"head/s{s.scenario_id}/{t}"
+            out += [(f"{base}/gate_w", d, cfg.experts), (f"{base}/gate_b", 1, cfg.experts),
+                    (f"{base}/tower_w", cfg.d_expert, 1), (f"{base}/tower_b", 1, 1)]
+    return out

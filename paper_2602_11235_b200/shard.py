@@ -1,9 +1,10 @@
 """User sharding across GPUs: users are independent, so a batch
 is partitioned across ranks with no collective on the data path.
 
-shard_plan(batch, world)   greedy LPT over an estimated per-user cost (full
-                           layers ~ N^2 attention + N projections, target
-                           layers ~ N): returns a list of user-index arrays.
+shard_plan(batch, world, cfg=...)  greedy LPT over each user's algorithmic
+                           MACs under the model config (projections,
+                           mask-aware attention, tokenizer): returns a list
+                           of user-index arrays.
 take_users(batch, users)   re-packs a subset of users into a new packed batch
                            (include/mtfm_cuda.h layout), preserving order.
 """
@@ -16,7 +17,41 @@ import numpy as np
 from .schema import normalize_batch
 
 
-def user_costs(batch, d_model=256, full_layers=1, target_layers=3):
+def visible_keys(batch):
+    """Per user (sum of c_i over context rows, sum over T rows): the mask-aware
+    visible-key counts of mask.hpp:35-40 in the prefix form (row i sees the L_H
+    history keys, the realtime keys strictly older than it, and itself if it is
+    a T token)."""
+    b = normalize_batch(batch)
+    U = len(b["user_id"])
+    c_ctx = np.zeros(U, np.float64)
+    c_t = np.zeros(U, np.float64)
+    for u in range(U):
+        h, r = [], []
+        for q in range(b["seq_off"][u], b["seq_off"][u + 1]):
+            ts = b["ev_ts"][b["ev_off"][q]:b["ev_off"][q + 1]]
+            (r if b["seq_kind"][q] else h).append(ts)
+        h = np.concatenate(h) if h else np.zeros(0, np.int64)
+        r = np.sort(np.concatenate(r)) if r else np.zeros(0, np.int64)
+        t = b["exp_ts"][b["exp_off"][u]:b["exp_off"][u + 1]]
+        lh = len(h)
+        c_ctx[u] = lh * (lh + len(r)) + np.searchsorted(r, h, "left").sum() + np.searchsorted(r, r, "left").sum()
+        c_t[u] = len(t) * (lh + 1) + np.searchsorted(r, t, "left").sum()
+    return c_ctx, c_t
+
+
+def user_costs(batch, cfg=None):
+    """Algorithmic MACs per user: projections per complexity.hpp:54-64,
+    mask-aware attention 2*hd*sum(c_i) per layer, tokenizer MLPs. cfg is the
+    ModelConfig (default: MTFM-small)."""
+    if cfg is None:
+        from .schema import HTAConfig, ModelConfig
+        cfg = ModelConfig(HTAConfig(d_model=256, blocks=1, target_layers=3, full_layers=1, heads=8, kv_heads=2),
+                          d_expert=256)
+    h = cfg.hta
+    d = h.d_model
+    dh = d // h.heads
+    hd, gd = h.heads * dh, h.kv_heads * dh
     b = normalize_batch(batch)
     U = len(b["user_id"])
     ev0 = b["ev_off"][b["seq_off"][:-1]] if len(b["ev_off"]) > 1 else np.zeros(U, np.int64)
@@ -24,17 +59,17 @@ def user_costs(batch, d_model=256, full_layers=1, target_layers=3):
     n_ctx = (ev1 - ev0).astype(np.float64)
     n_t = np.diff(b["exp_off"]).astype(np.float64)
     n = n_ctx + n_t
-    # projection MACs ~ N*d*(4d) per full layer, attention ~ 2*d*N*n_ctx;
-    # target layers ~ N*d*d (fkv) + n_t * (2*d*n_ctx)
-    full = n * d_model * 4 * d_model + 2.0 * d_model * n * n_ctx
-    tgt = n * d_model * d_model + n_t * (2.0 * d_model * n_ctx + 3 * d_model * d_model)
-    return full_layers * full + target_layers * tgt + 1.0
+    c_ctx, c_t = visible_keys(b)
+    full = n * d * (2 * hd + 2 * gd) + n * hd * d + 2.0 * hd * (c_ctx + c_t)
+    tgt = n_t * d * 2 * hd + n * d * 2 * gd + n_t * hd * d + 2.0 * hd * c_t
+    tok = n * (3 * cfg.d_emb * 2 * d + 2 * d * d)
+    return h.blocks * (h.full_layers * full + h.target_layers * tgt) + tok + 1.0
 
 
-def shard_plan(batch, world, costs=None):
+def shard_plan(batch, world, costs=None, cfg=None):
     """Greedy longest-processing-time assignment; each shard keeps batch order."""
     if costs is None:
-        costs = user_costs(batch)
+        costs = user_costs(batch, cfg)
     order = np.argsort(-costs, kind="stable")
     heap = [(0.0, r) for r in range(world)]
     owner = np.empty(len(costs), np.int64)

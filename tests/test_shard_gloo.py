@@ -83,3 +83,28 @@ def test_take_users_roundtrip_and_lpt_balance():
         x0, x1 = b["exp_off"][u], b["exp_off"][u + 1]
         y0, y1 = sub["exp_off"][k], sub["exp_off"][k + 1]
         assert np.array_equal(b["exp_scenario"][x0:x1], sub["exp_scenario"][y0:y1])
+
+
+def test_visible_keys_match_reference_valid_counts():
+    """shard.visible_keys (the LPT cost's attention term) sums exactly the
+    reference's row_valid_counts (mask.hpp:35-40) over context / T rows."""
+    from golden_util import load
+    from paper_2602_11235_b200.shard import visible_keys
+    for name in ("tiny", "small4"):
+        a = load(name)
+        c_ctx, c_t = visible_keys(batch(name))
+        off, bounds, vc = a["plan/off"], a["plan/bounds"], a["plan/valid_count"]
+        for u in range(len(c_ctx)):
+            lh, lr, lt = bounds[u]
+            v = vc[off[u]:off[u + 1]].astype(np.int64)
+            assert c_ctx[u] == v[:lh + lr].sum() and c_t[u] == v[lh + lr:].sum()
+
+
+def test_lpt_cost_follows_model_config():
+    """Costs scale with the model config passed in (base: d=512, (3:1)x2)."""
+    from paper_2602_11235_b200.shard import user_costs
+    wl = datagen.WORKLOADS["base"]()
+    b = datagen.generate(wl, n_users=16)
+    small = user_costs(b)
+    base = user_costs(b, wl.cfg)
+    assert np.all(base > 3.5 * small)
