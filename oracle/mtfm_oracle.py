@@ -34,6 +34,7 @@ exp_feats).
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -79,6 +80,34 @@ def splitmix64(state):
     return state, z ^ (z >> 31)
 
 
+_RNG_LIB = []
+
+
+def _rng_lib():
+    """oracle/rng_block.c compiled on first use (gcc) into oracle/_ref/; None if unavailable."""
+    if _RNG_LIB:
+        return _RNG_LIB[0]
+    lib = None
+    try:
+        import ctypes
+        import subprocess
+        here = os.path.dirname(os.path.abspath(__file__))
+        src, so = os.path.join(here, "rng_block.c"), os.path.join(here, "_ref", "librng_block.so")
+        if not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(src):
+            os.makedirs(os.path.dirname(so), exist_ok=True)
+            tmp = so + f".{os.getpid()}"
+            subprocess.run(["gcc", "-O2", "-shared", "-fPIC", src, "-o", tmp], check=True, capture_output=True)
+            os.replace(tmp, so)
+        lib = ctypes.CDLL(so)
+        lib.rng_uniform_block.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
+                                          ctypes.c_void_p]
+        lib.rng_uniform_block.restype = None
+    except Exception:
+        lib = None
+    _RNG_LIB.append(lib)
+    return lib
+
+
 class Rng:
     def __init__(self, seed):
         sm = seed & MASK64
@@ -106,6 +135,16 @@ class Rng:
 
     def uniform_block(self, n, lo, hi):
         # lo + (hi - lo) * next_double(), element by element (rng.hpp:57)
+        fast = _rng_lib()
+        if fast is not None and n > 64:
+            st = np.array(self.s, dtype=np.uint64)
+            out = np.empty(n, dtype=np.float64)
+            fast.rng_uniform_block(st.ctypes.data, n, float(lo), float(hi), out.ctypes.data)
+            self.s = [int(x) for x in st]
+            return out
+        return self.uniform_block_py(n, lo, hi)
+
+    def uniform_block_py(self, n, lo, hi):
         s0, s1, s2, s3 = self.s
         out = np.empty(n, dtype=np.float64)
         span = hi - lo
@@ -181,6 +220,27 @@ class GroupTable:
         if gid not in table:
             raise ConfigError(f"unknown token group {'HRT'[kind]}{gid}")
         return table[gid]
+
+
+def jitter_params(P: dict, seed: int, tower_scale: float) -> dict:
+    """Restates oracle/ref_dump.cpp jitter_params (test fixtures only): the
+    reference's Rng (rng.hpp:57) drawn in registration order (model.hpp:371-463)
+    over gains (1 + U(-0.2, 0.2)), GLN biases (U(-0.1, 0.1)), biases (+ U(-0.1, 0.1))
+    and towers (x tower_scale), each value computed in double then rounded to f32."""
+    rng = Rng(seed)
+    out = {}
+    for n, v in P.items():
+        v = v.astype(np.float64)
+        if n.endswith("/gain"):
+            v = 1.0 + rng.uniform_block(v.size, -0.2, 0.2).reshape(v.shape)
+        elif "/gln" in n and n.endswith("/bias"):
+            v = rng.uniform_block(v.size, -0.1, 0.1).reshape(v.shape)
+        elif n.endswith("_b") or n.endswith("/mlp_b1") or n.endswith("/mlp_b2"):
+            v = v + rng.uniform_block(v.size, -0.1, 0.1).reshape(v.shape)
+        elif n.endswith("/tower_w"):
+            v = v * tower_scale
+        out[n] = v.astype(np.float32)
+    return out
 
 
 def build_params(sch: Schemas, cfg: Config, seed: int) -> dict:

@@ -23,6 +23,7 @@
 #include <string>
 #include <vector>
 
+#include "jitter.hpp"
 #include "mtfa.hpp"
 #include "mtfm/datagen.hpp"
 #include "mtfm/model.hpp"
@@ -41,6 +42,8 @@ struct Opts {
     int hlen = -1, rlen = -1;  // fixed lengths by order-preserving subsample
     int dump_x_users = 0;      // users whose per-layer activations are dumped
     bool params = false;       // dump full f32 parameters
+    uint64_t jitter = 0;       // != 0: perturb biases / GLN affines / towers (jitter_params)
+    double tower_scale = 1.0;
 };
 
 Opts parse(int argc, char** argv) {
@@ -95,6 +98,8 @@ Opts parse(int argc, char** argv) {
         else if (a == "--rlen") o.rlen = std::stoi(nxt());
         else if (a == "--dumpx") o.dump_x_users = std::stoi(nxt());
         else if (a == "--params") o.params = true;
+        else if (a == "--jitter") o.jitter = std::stoull(nxt());
+        else if (a == "--tower-scale") o.tower_scale = std::stod(nxt());
         else throw config_error("unknown flag " + a);
     }
     if (o.out.empty()) throw config_error("--out required");
@@ -229,6 +234,7 @@ int main(int argc, char** argv) {
         }
 
         Model<float> m32 = Model<float>::build(ss, o.mc, o.model_seed);
+        if (o.jitter) jitter_params(m32.params, o.jitter, o.tower_scale);
         Model<double> m64 = Model<double>::build(ss, o.mc, o.model_seed);
         // The f64 model carries exactly the f32 weights, so it is the exact
         // answer for the weights the GPU path receives.
@@ -245,6 +251,7 @@ int main(int argc, char** argv) {
                                                   o.mc.d_emb, o.mc.experts, o.mc.d_expert});
         w.put("config/eps", std::vector<double>{h.eps});
         w.put("config/model_seed", std::vector<int64_t>{static_cast<int64_t>(o.model_seed)});
+        w.put("config/jitter", std::vector<double>{static_cast<double>(o.jitter), o.tower_scale});
 
         int max_tasks = 0;
         for (const auto& s : ss.scenarios) max_tasks = std::max(max_tasks, static_cast<int>(s.tasks.size()));

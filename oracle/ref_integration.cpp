@@ -13,6 +13,7 @@
 #include <string>
 #include <vector>
 
+#include "jitter.hpp"
 #include "mtfm/datagen.hpp"
 #include "mtfm/model.hpp"
 #include "mtfm/subgraph.hpp"
@@ -50,6 +51,8 @@ int main(int argc, char** argv) {
     mc.hta.kv_heads = 2;
     mc.d_expert = 128;
     Model<float> model = Model<float>::build(SchemaSet::from(d), mc, 7);
+    // off the default init: every bias, GLN gain/bias, O(1) logits (jitter.hpp)
+    jitter_params(model.params, 201, 60.0);
 
     bool ok = true;
     double max_dp = 0, max_dz = 0;

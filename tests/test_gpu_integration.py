@@ -21,5 +21,6 @@ def test_reference_api_drop_in(flag):
     out = subprocess.run([BIN] + ([flag] if flag else []), capture_output=True, text=True, timeout=600)
     line = [l for l in out.stdout.splitlines() if l.startswith("{")][-1]
     r = json.loads(line)
+    print(line)
     assert out.returncode == 0 and r["ok"], r
     assert r["records"] > 0

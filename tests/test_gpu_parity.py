@@ -2,23 +2,30 @@
 and the pinned numpy oracle. Needs a B200.
 
 Tolerances (BASELINE.json north_star):
-  fp32 check mode : max |z - z_ref| / max(|z_ref|, 1e-3) <= 1e-4 on logits
-  bf16 fast mode  : max |z - z_ref| <= 2e-2 on logits
+  fp32 check mode : max |z - z_ref| / max(|z_ref|, floor) <= 1e-4 on logits
+                    (floor: helpers.check_floor, 1e-2 default-init / 1.0 jittered)
+  bf16 fast mode  : max |z - z_ref| <= 2e-2 on logits, and
+                    max |z - z_ref| / max(|z_ref|, 1) <= 1e-2 (relative)
   integer plan    : bit-exact
+The *_j fixtures carry parameters moved off the reference's default init
+(every bias, GLN gain/bias, O(1) logits; oracle/ref_dump.cpp --jitter).
+Observed errors are printed (run with -rA to see them in the log).
 """
 import numpy as np
 import pytest
 
 import mtfm_oracle as O
-from golden_util import NAMES, batch, load, model, ref_records
-from helpers import from_oracle, oracle_records, rel_err, to_oracle
+from golden_util import JITTERED, NAMES, batch, load, model, ref_records
+from helpers import check_floor, from_oracle, oracle_records, rel_err, to_oracle
 from paper_2602_11235_b200 import Model, abi, datagen
 
 pytestmark = pytest.mark.gpu
 
 FP32_TOL = 1e-4
 BF16_TOL = 2e-2
-BF16_OK = [n for n in NAMES if n != "micro"]  # micro has head_dim 8 (< 16): fp32 check mode only
+BF16_REL = 1e-2
+ALL = NAMES + JITTERED
+BF16_OK = [n for n in ALL if n != "micro"]  # micro has head_dim 8 (< 16): fp32 check mode only
 
 
 def _build(name, precision):
@@ -27,15 +34,21 @@ def _build(name, precision):
     return Model.build(sch, cfg, P, precision=precision)
 
 
-@pytest.mark.parametrize("name", NAMES)
+@pytest.mark.parametrize("name", ALL)
 def test_golden_fp32_check_mode(name):
     m = _build(name, "fp32")
     ra = m.forward_batch(batch(name))
     keys, z64, z32, p64, p32 = ref_records(name)
     got = np.stack([ra.user_id, ra.scenario_id, ra.exposure_index, ra.task_index], 1)
     assert np.array_equal(got, keys)
-    assert rel_err(ra.logit.astype(np.float64), z64) <= FP32_TOL
-    assert np.max(np.abs(ra.probability - p64)) <= 1e-5
+    fl = check_floor(name)
+    err = rel_err(ra.logit.astype(np.float64), z64, fl)
+    ref_err = rel_err(z32, z64, fl)
+    dp = float(np.max(np.abs(ra.probability - p64)))
+    print(f"fp32 {name}: rel err {err:.3e} (floor {fl}; reference Model<float>: {ref_err:.3e}), "
+          f"max |dz| {np.max(np.abs(ra.logit - z64)):.3e}, max |dp| {dp:.3e}, max |z| {np.max(np.abs(z64)):.2f}")
+    assert err <= FP32_TOL
+    assert dp <= 1e-5
 
 
 @pytest.mark.parametrize("name", BF16_OK)
@@ -45,10 +58,14 @@ def test_golden_bf16(name):
     keys, z64, *_ = ref_records(name)
     got = np.stack([ra.user_id, ra.scenario_id, ra.exposure_index, ra.task_index], 1)
     assert np.array_equal(got, keys)
-    assert np.max(np.abs(ra.logit.astype(np.float64) - z64)) <= BF16_TOL
+    dz = np.abs(ra.logit.astype(np.float64) - z64)
+    rel = float(np.max(dz / np.maximum(np.abs(z64), 1.0)))
+    print(f"bf16 {name}: max |dz| {dz.max():.3e}, rel (floor 1) {rel:.3e}, max |z| {np.max(np.abs(z64)):.2f}")
+    assert dz.max() <= BF16_TOL
+    assert rel <= BF16_REL
 
 
-@pytest.mark.parametrize("name", NAMES)
+@pytest.mark.parametrize("name", ALL)
 @pytest.mark.parametrize("precision", ["bf16", "fp32"])
 def test_plan_bit_exact(name, precision):
     if precision == "bf16" and name not in BF16_OK:
@@ -109,10 +126,13 @@ def test_synthetic_configs_vs_oracle(name, n_users):
     keys, z_ref, _ = oracle_records(osch, ocfg, P, b)
     ra = m16.forward_batch(b)
     assert np.array_equal(np.stack([ra.user_id, ra.scenario_id, ra.exposure_index, ra.task_index], 1), keys)
-    assert np.max(np.abs(ra.logit - z_ref)) <= BF16_TOL
+    e16 = float(np.max(np.abs(ra.logit - z_ref)))
     m32 = Model.build(wl.schemas, wl.cfg, P, precision="fp32")
     rb = m32.forward_batch(b)
-    assert rel_err(rb.logit.astype(np.float64), z_ref) <= FP32_TOL
+    e32 = rel_err(rb.logit.astype(np.float64), z_ref)
+    print(f"synthetic {name}: bf16 max |dz| {e16:.3e}, fp32 rel err {e32:.3e}, max |z| {np.max(np.abs(z_ref)):.3f}")
+    assert e16 <= BF16_TOL
+    assert e32 <= FP32_TOL
 
 
 def test_error_taxonomy_and_order():
