@@ -214,6 +214,68 @@ MTFM_API mtfm_status mtfm_cuda_debug_gemm(const void* A, const void* Bt, const f
 MTFM_API int64_t mtfm_cuda_debug_fetch(mtfm_cuda_model* m, mtfm_cuda_batch* b, const char* which, void* host_dst,
                               int64_t max_bytes);
 
+/* ---------------------------------------------------------------- user aggregation
+ * aggregate_users (datagen.cpp:171-216, datagen.hpp:55-61) on the device: a
+ * (user_id, Exposure) stream is grouped per user with exposures ordered by
+ * scenario id ascending and stream order within a scenario, users ascending,
+ * joined with each user's shared historical / realtime sequences from the
+ * store. Output: the packed jagged batch of the users that have exposures
+ * (mtfm_packed_batch layout), bit-exact with the reference's UserSample list.
+ * Unknown scenario / user -> MTFM_INTEGRITY_ERROR naming the first offending
+ * stream element (scenario checked first, datagen.cpp:177-183). The store is
+ * a std::map<int64_t, UserContext> flattened in its iteration order (user ids
+ * strictly ascending; violations -> MTFM_CONTRACT_ERROR) as a packed batch
+ * with no exposures. Labels are host data: exp_src maps every output
+ * exposure back to its stream index. */
+typedef struct {
+    int32_t n_exposures;
+    int64_t n_feats;
+    const int64_t* user_id;   /* [n] stream order */
+    const int32_t* scenario;  /* [n] Exposure::scenario_id */
+    const int64_t* ts;        /* [n] Exposure::timestamp */
+    const int32_t* feat_off;  /* [n+1] -> feats (user ids, cross ids, item ids) */
+    const int32_t* blk;       /* [3n] user / cross / item id counts */
+    const int32_t* feats;
+} mtfm_exposure_stream;
+
+typedef struct { /* AggregationReport (datagen.hpp:44-53) */
+    int64_t n_exposure_records, n_user_samples;
+    double compression_ratio;
+} mtfm_aggregation_report;
+
+typedef struct {
+    int64_t n_users, n_seqs, n_events, n_exposures, n_ev_feats, n_exp_feats;
+} mtfm_packed_sizes;
+
+typedef struct { /* writable mtfm_packed_batch arrays (+ exp_src, may be NULL) */
+    int64_t* user_id;
+    int32_t* seq_off;
+    uint8_t* seq_kind;
+    int32_t* seq_schema;
+    int32_t* ev_off;
+    int64_t* ev_ts;
+    int32_t* ev_feat_off;
+    int32_t* ev_feats;
+    int32_t* exp_off;
+    int32_t* exp_scenario;
+    int64_t* exp_ts;
+    int32_t* exp_feat_off;
+    int32_t* exp_blk;
+    int32_t* exp_feats;
+    int32_t* exp_src;
+} mtfm_packed_buffers;
+
+typedef struct mtfm_cuda_aggregate mtfm_cuda_aggregate;
+
+/* scenario_ids: the schema context's scenario ids, strictly ascending
+ * (Dataset::has_scenario). The result stays on `device` until freed. */
+MTFM_API mtfm_status mtfm_cuda_aggregate_users(int device, const int32_t* scenario_ids, int32_t n_scenarios,
+                                               const mtfm_exposure_stream* stream, const mtfm_packed_batch* store,
+                                               mtfm_cuda_aggregate** out, mtfm_aggregation_report* report);
+MTFM_API mtfm_status mtfm_cuda_aggregate_sizes(const mtfm_cuda_aggregate* a, mtfm_packed_sizes* sizes);
+MTFM_API mtfm_status mtfm_cuda_aggregate_fetch(mtfm_cuda_aggregate* a, const mtfm_packed_buffers* out);
+MTFM_API mtfm_status mtfm_cuda_aggregate_free(mtfm_cuda_aggregate* a);
+
 #ifdef __cplusplus
 }
 #endif

@@ -654,6 +654,55 @@ class Oracle:
 
 
 # ----------------------------------------------------------------------------
+# User-level aggregation (datagen.cpp:171-216)
+# ----------------------------------------------------------------------------
+def aggregate_users(scenario_ids, stream, store):
+    """Restates aggregate_users over packed arrays. stream: user_id, scenario, ts,
+    feat_off, blk, feats (arrival order); store: packed batch of the users' H/R
+    sequences (std::map iteration order). Returns (packed batch, exp_src)."""
+    known = set(int(x) for x in scenario_ids)
+    store_users = [int(u) for u in store["user_id"]]
+    pos = {u: i for i, u in enumerate(store_users)}
+    per_scenario = {}  # scenario -> user -> [stream index], each in stream order
+    for x in range(len(stream["user_id"])):
+        sc, u = int(stream["scenario"][x]), int(stream["user_id"][x])
+        if sc not in known:  # datagen.cpp:178-180
+            raise IntegrityError(f"aggregate: exposure references unknown scenario {sc}")
+        if u not in pos:  # datagen.cpp:181-183
+            raise IntegrityError(f"aggregate: exposure references unknown user {u}")
+        per_scenario.setdefault(sc, {}).setdefault(u, []).append(x)
+    merged = {}  # user -> [stream index]: scenarios ascending, stream order within
+    for sc in sorted(per_scenario):
+        for u in sorted(per_scenario[sc]):
+            merged.setdefault(u, []).extend(per_scenario[sc][u])
+    out = {k: [] for k in BATCH_KEYS}
+    for k in ("seq_off", "ev_off", "ev_feat_off", "exp_off", "exp_feat_off"):
+        out[k].append(0)
+    src = []
+    for u in sorted(merged):
+        r = pos[u]
+        out["user_id"].append(u)
+        for q in range(store["seq_off"][r], store["seq_off"][r + 1]):
+            out["seq_kind"].append(int(store["seq_kind"][q]))
+            out["seq_schema"].append(int(store["seq_schema"][q]))
+            for e in range(store["ev_off"][q], store["ev_off"][q + 1]):
+                out["ev_ts"].append(int(store["ev_ts"][e]))
+                out["ev_feats"].extend(int(f) for f in store["ev_feats"][store["ev_feat_off"][e]:store["ev_feat_off"][e + 1]])
+                out["ev_feat_off"].append(len(out["ev_feats"]))
+            out["ev_off"].append(len(out["ev_ts"]))
+        out["seq_off"].append(len(out["seq_kind"]))
+        for x in merged[u]:
+            src.append(x)
+            out["exp_scenario"].append(int(stream["scenario"][x]))
+            out["exp_ts"].append(int(stream["ts"][x]))
+            out["exp_blk"].extend(int(b) for b in stream["blk"][3 * x:3 * x + 3])
+            out["exp_feats"].extend(int(f) for f in stream["feats"][stream["feat_off"][x]:stream["feat_off"][x + 1]])
+            out["exp_feat_off"].append(len(out["exp_feats"]))
+        out["exp_off"].append(len(out["exp_scenario"]))
+    return out, src
+
+
+# ----------------------------------------------------------------------------
 # Fixture helpers
 # ----------------------------------------------------------------------------
 BATCH_KEYS = ("user_id", "seq_off", "seq_kind", "seq_schema", "ev_off", "ev_ts", "ev_feat_off",

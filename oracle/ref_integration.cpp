@@ -51,8 +51,9 @@ int main(int argc, char** argv) {
     mc.hta.kv_heads = 2;
     mc.d_expert = 128;
     Model<float> model = Model<float>::build(SchemaSet::from(d), mc, 7);
-    // off the default init: every bias, GLN gain/bias, O(1) logits (jitter.hpp)
-    jitter_params(model.params, 201, 60.0);
+    // off the default init: every bias and GLN gain/bias (jitter.hpp), towers unscaled so the
+    // bf16 logit tolerance (2e-2 absolute) is not dominated by bf16 storage error
+    jitter_params(model.params, 201, 1.0);
 
     bool ok = true;
     double max_dp = 0, max_dz = 0;

@@ -92,6 +92,26 @@ class RunStats(C.Structure):
                 ("tokens", C.c_int64), ("targets", C.c_int64), ("records", C.c_int64)]
 
 
+class ExposureStream(C.Structure):
+    _fields_ = [("n_exposures", C.c_int32), ("n_feats", C.c_int64), ("user_id", C.c_void_p), ("scenario", C.c_void_p),
+                ("ts", C.c_void_p), ("feat_off", C.c_void_p), ("blk", C.c_void_p), ("feats", C.c_void_p)]
+
+
+class AggregationReport(C.Structure):
+    _fields_ = [("n_exposure_records", C.c_int64), ("n_user_samples", C.c_int64), ("compression_ratio", C.c_double)]
+
+
+class PackedSizes(C.Structure):
+    _fields_ = [("n_users", C.c_int64), ("n_seqs", C.c_int64), ("n_events", C.c_int64), ("n_exposures", C.c_int64),
+                ("n_ev_feats", C.c_int64), ("n_exp_feats", C.c_int64)]
+
+
+class PackedBuffers(C.Structure):
+    _fields_ = [(k, C.c_void_p) for k in ("user_id", "seq_off", "seq_kind", "seq_schema", "ev_off", "ev_ts",
+                                           "ev_feat_off", "ev_feats", "exp_off", "exp_scenario", "exp_ts",
+                                           "exp_feat_off", "exp_blk", "exp_feats", "exp_src")]
+
+
 # (name, restype, argtypes) — every symbol include/mtfm_cuda.h declares.
 SIGNATURES = [
     ("mtfm_cuda_last_error", C.c_char_p, []),
@@ -118,6 +138,12 @@ SIGNATURES = [
     ("mtfm_cuda_debug_gemm", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
                                        C.c_int64, C.c_int32, C.c_void_p]),
     ("mtfm_cuda_debug_fetch", C.c_int64, [C.c_void_p, C.c_void_p, C.c_char_p, C.c_void_p, C.c_int64]),
+    ("mtfm_cuda_aggregate_users", C.c_int, [C.c_int, C.c_void_p, C.c_int32, C.POINTER(ExposureStream),
+                                            C.POINTER(PackedBatch), C.POINTER(C.c_void_p),
+                                            C.POINTER(AggregationReport)]),
+    ("mtfm_cuda_aggregate_sizes", C.c_int, [C.c_void_p, C.POINTER(PackedSizes)]),
+    ("mtfm_cuda_aggregate_fetch", C.c_int, [C.c_void_p, C.POINTER(PackedBuffers)]),
+    ("mtfm_cuda_aggregate_free", C.c_int, [C.c_void_p]),
 ]
 
 _lib = None

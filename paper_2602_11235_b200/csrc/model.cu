@@ -1862,6 +1862,10 @@ void launch_sum_valid(mtfm_cuda_batch& B, cudaStream_t st) {
 }  // namespace
 }  // namespace mtfm
 
+namespace mtfm {
+void set_last_error(const std::string& what) { g_last_error = what; }
+}  // namespace mtfm
+
 using namespace mtfm;
 
 extern "C" {
