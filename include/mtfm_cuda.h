@@ -163,6 +163,15 @@ MTFM_API mtfm_status mtfm_cuda_set_param(mtfm_cuda_model* m, const char* name, c
 MTFM_API int64_t mtfm_cuda_num_params(const mtfm_cuda_model* m);
 MTFM_API const char* mtfm_cuda_param_name(const mtfm_cuda_model* m, int64_t i, int64_t* rows, int64_t* cols);
 
+/* Scenario-subgraph deployment (extract_subgraph, subgraph.hpp:25-42): after
+ * this call the handle registers only the shared parameters and scenario_id's
+ * own (names::owner_scenario, model.hpp:71-87) — num_params / param_name list
+ * exactly the subgraph's ParamStore, set_param on another scenario's parameter
+ * is MTFM_CONFIG_ERROR — and every forward is scoped to scenario_id
+ * (infer_request, subgraph.hpp:47-62: another only_scenario is
+ * MTFM_INTEGRITY_ERROR). Unknown scenario -> MTFM_CONFIG_ERROR. */
+MTFM_API mtfm_status mtfm_cuda_restrict_to_scenario(mtfm_cuda_model* m, int32_t scenario_id);
+
 /* Records the batch will produce (host-side count: sum over exposures of the
  * task count of their scenario; exposures of unknown scenarios count 0). */
 MTFM_API int64_t mtfm_cuda_count_records(const mtfm_cuda_model* m, const mtfm_packed_batch* b);

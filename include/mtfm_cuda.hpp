@@ -24,6 +24,7 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "mtfm_cuda.h"
@@ -119,10 +120,23 @@ class GpuModel {
     template <typename Real>
     explicit GpuModel(const Model<Real>& model, int device = 0, int32_t precision = MTFM_PRECISION_BF16)
         : schemas_(model.schemas) {
-        const HTAConfig& h = model.cfg.hta;
+        init(model.cfg, model.params, device, precision, -1);
+    }
+    // A scenario deployment: ScenarioSubgraph<Real> from extract_subgraph(model, s)
+    // (subgraph.hpp:12-42) — only the subgraph's ParamStore (shared weights + scenario s)
+    // exists and is uploaded; every forward is scoped to s.
+    template <typename Sub, typename = decltype(std::declval<const Sub&>().scenario_id)>
+    explicit GpuModel(const Sub& sub, int device = 0, int32_t precision = MTFM_PRECISION_BF16)
+        : schemas_(sub.schemas), subgraph_(sub.scenario_id) {
+        init(sub.cfg, sub.params, device, precision, sub.scenario_id);
+    }
+
+  private:
+    template <typename Store>
+    void init(const ModelConfig& cfg, const Store& params, int device, int32_t precision, int subgraph) {
+        const HTAConfig& h = cfg.hta;
         mtfm_model_desc md{h.d_model, h.blocks, h.target_layers, h.full_layers, h.heads, h.kv_heads,
-                           static_cast<int32_t>(h.norm), h.eps, model.cfg.d_emb, model.cfg.experts,
-                           model.cfg.d_expert};
+                           static_cast<int32_t>(h.norm), h.eps, cfg.d_emb, cfg.experts, cfg.d_expert};
         std::vector<int32_t> hid, hns, hv, rid, rns, rv, sid, nu, nc, ni, sv, nt;
         std::vector<const char*> tasks;
         for (const auto& s : schemas_.hist) {
@@ -151,14 +165,16 @@ class GpuModel {
                             static_cast<int32_t>(sid.size()), sid.data(), nu.data(), nc.data(), ni.data(),
                             sv.data(), nt.data(), tasks.data()};
         check(mtfm_cuda_create(device, &md, &sd, precision, &h_));
+        if (subgraph >= 0) check(mtfm_cuda_restrict_to_scenario(h_, subgraph));
         std::vector<float> buf;
-        for (const auto& e : model.params) {
+        for (const auto& e : params) {
             buf.assign(e.value.size(), 0.f);
             for (size_t i = 0; i < buf.size(); ++i) buf[i] = static_cast<float>(e.value[i]);
             check(mtfm_cuda_set_param(h_, e.name.c_str(), buf.data(), static_cast<int64_t>(e.value.rows()),
                                       static_cast<int64_t>(e.value.cols())));
         }
     }
+  public:
     ~GpuModel() {
         if (h_) mtfm_cuda_destroy(h_);
     }
@@ -217,10 +233,33 @@ class GpuModel {
         return forward_samples(std::span<const UserSample>(&view, 1), r.scenario_id, false);
     }
 
+    // Many requests in ONE forward (each request one sample of the batch); per request
+    // the records equal infer_request(r): T tokens never see other users or each other.
+    std::vector<std::vector<PredictionRecord>> infer_requests(std::span<const InferenceRequest> rs) const {
+        std::vector<UserSample> views;
+        views.reserve(rs.size());
+        for (const auto& r : rs) {
+            if (subgraph_ >= 0 && r.scenario_id != subgraph_)
+                throw integrity_error("request scenario " + std::to_string(r.scenario_id) +
+                                      " does not match subgraph scenario " + std::to_string(subgraph_));
+            views.push_back(sample_view_of_request(r));
+        }
+        auto flat = forward_samples(std::span<const UserSample>(views.data(), views.size()), subgraph_, false);
+        std::vector<std::vector<PredictionRecord>> out(rs.size());
+        size_t k = 0;
+        for (size_t i = 0; i < rs.size(); ++i) {
+            const size_t n = rs[i].candidates.size() * schemas_.scenario(rs[i].scenario_id).tasks.size();
+            out[i].assign(flat.begin() + static_cast<long>(k), flat.begin() + static_cast<long>(k + n));
+            k += n;
+        }
+        return out;
+    }
+
     mtfm_cuda_model* handle() const { return h_; }
 
   private:
     SchemaSet schemas_;
+    int subgraph_ = -1;
     mtfm_cuda_model* h_ = nullptr;
 };
 

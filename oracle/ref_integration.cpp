@@ -104,6 +104,46 @@ int main(int argc, char** argv) {
             if (std::fabs(logit(rw[i].probability) - logit(rg[i].probability)) > tol) ok = false;
         }
 
+        // scenario deployment: only extract_subgraph(model, 1)'s ParamStore uploaded, and
+        // many requests in one forward == one infer_request each (subgraph.hpp:47-62)
+        cuda::GpuModel gsub(sub, 0, precision);
+        std::vector<InferenceRequest> reqs;
+        for (size_t u = 0; u < d.samples.size() && reqs.size() < 12; u += 2) {
+            InferenceRequest q = req;
+            q.user_id = d.samples[u].user_id;
+            q.timestamp = 1200 + static_cast<int64_t>(u);
+            q.historical_sequences = d.samples[u].historical_sequences;
+            q.realtime_sequences = d.samples[u].realtime_sequences;
+            q.candidates.resize(1 + u % 4, req.candidates[u % req.candidates.size()]);
+            reqs.push_back(q);
+        }
+        auto batched = gsub.infer_requests(reqs);
+        for (size_t i = 0; ok && i < reqs.size(); ++i) {
+            auto want1 = infer_request(model, sub, reqs[i]);
+            auto alone = gsub.infer_request(reqs[i]);
+            if (batched[i].size() != want1.size() || alone.size() != want1.size()) ok = false;
+            for (size_t j = 0; ok && j < want1.size(); ++j) {
+                if (batched[i][j].exposure_index != want1[j].exposure_index || batched[i][j].task != want1[j].task ||
+                    batched[i][j].user_id != want1[j].user_id)
+                    ok = false;
+                if (batched[i][j].probability != alone[j].probability) ok = false;  // batching is bitwise neutral
+                if (std::fabs(logit(batched[i][j].probability) - logit(want1[j].probability)) > tol) ok = false;
+            }
+        }
+        // a subgraph refuses another scenario's request (subgraph.hpp:51-55)
+        {
+            InferenceRequest other = req;
+            other.scenario_id = 2;
+            bool threw = false;
+            try {
+                gsub.infer_request(other);
+            } catch (const integrity_error&) {
+                threw = true;
+            }
+            if (!threw) ok = false;
+        }
+        if (!ok) std::printf("{\"stage\": \"subgraph\"}\n");
+
         // error taxonomy: out-of-vocab id -> lookup_error (eval_ctx.hpp:193-194)
         UserSample bad = d.samples[0];
         bad.exposures.at(0).item_features.at(0) = 1 << 20;

@@ -122,6 +122,7 @@ SIGNATURES = [
     ("mtfm_cuda_set_param", C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.c_int64, C.c_int64]),
     ("mtfm_cuda_num_params", C.c_int64, [C.c_void_p]),
     ("mtfm_cuda_param_name", C.c_char_p, [C.c_void_p, C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    ("mtfm_cuda_restrict_to_scenario", C.c_int, [C.c_void_p, C.c_int32]),
     ("mtfm_cuda_count_records", C.c_int64, [C.c_void_p, C.POINTER(PackedBatch)]),
     ("mtfm_cuda_forward", C.c_int, [C.c_void_p, C.POINTER(PackedBatch), C.c_int32, C.POINTER(Records)]),
     ("mtfm_cuda_batch_prepare", C.c_int, [C.c_void_p, C.POINTER(PackedBatch), C.c_int32, C.POINTER(C.c_void_p)]),

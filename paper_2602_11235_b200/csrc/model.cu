@@ -241,7 +241,25 @@ struct ParamSpec {
     long long rows, cols;
     std::vector<float> host;
     bool set = false;
+    int owner = -1;  // names::owner_scenario (model.hpp:71-87): scenario owning it, -1 shared
 };
+
+// model.hpp:71-87: the first path component "s<digits>" or "t<digits>" names the
+// owning scenario; everything else is shared (the subgraph extraction rule).
+int owner_scenario(const std::string& name) {
+    size_t pos = 0;
+    while (pos < name.size()) {
+        size_t end = name.find('/', pos);
+        if (end == std::string::npos) end = name.size();
+        if (end > pos + 1 && (name[pos] == 's' || name[pos] == 't')) {
+            bool digits = true;
+            for (size_t i = pos + 1; i < end; ++i) digits = digits && name[i] >= '0' && name[i] <= '9';
+            if (digits) return std::stoi(name.substr(pos + 1, end - pos - 1));
+        }
+        pos = end + 1;
+    }
+    return -1;
+}
 
 struct LayerW {
     bool target;
@@ -276,6 +294,10 @@ struct mtfm_cuda_model {
     int n_hist = 0, n_rt = 0, n_scen = 0, n_tasks_total = 0;
     std::vector<mtfm::ParamSpec> params;
     std::map<std::string, size_t> by_name;
+    // scenario subgraph (subgraph.hpp:25-42): >= 0 -> only the shared parameters and this
+    // scenario's are registered; every forward is scoped to it
+    int subgraph = -1;
+    std::vector<size_t> visible;  // registered parameters in registration order
     bool finalized = false;
     int n_ctx_src = 0;  // leading sources of kind hist/rt (context rows) when they precede every scenario source
     cudaStream_t stream = nullptr;       // kernels
@@ -347,7 +369,7 @@ void register_params(mtfm_cuda_model& m) {
     auto add = [&](const std::string& n, long long r, long long c) {
         if (m.by_name.count(n)) fail(MTFM_CONFIG_ERROR, "duplicate parameter name: " + n);
         m.by_name[n] = m.params.size();
-        m.params.push_back({n, r, c, {}, false});
+        m.params.push_back({n, r, c, {}, false, owner_scenario(n)});
     };
     const int d = m.d, hd = m.hd, gd = m.gd, de = m.cfg.d_emb;
     // model.hpp:377-463 registration order
@@ -436,8 +458,14 @@ void finalize(mtfm_cuda_model& m) {
     if (m.finalized) return;
     // bias tiles are keyed by device pointer: rebuilt weights may reuse freed addresses
     m.bias_tiles.tiles.clear();
-    for (const auto& p : m.params)
+    for (auto& p : m.params) {
+        if (m.subgraph >= 0 && p.owner >= 0 && p.owner != m.subgraph) {
+            // not part of the subgraph: never bound (forwards are scoped to the subgraph scenario)
+            p.host.assign(static_cast<size_t>(p.rows * p.cols), 0.f);
+            p.set = true;
+        }
         if (!p.set) fail(MTFM_CONFIG_ERROR, "parameter not set: " + p.name);
+    }
     cudaStream_t st = m.stream;
     const int d = m.d, hd = m.hd, gd = m.gd;
     // embeddings: one flat table buffer
@@ -981,6 +1009,13 @@ void check_batch(const mtfm_packed_batch* b) {
 
 void prepare(mtfm_cuda_model& m, const mtfm_packed_batch* hb, int only_scenario, mtfm_cuda_batch& B) {
     check_batch(hb);
+    if (m.subgraph >= 0) {
+        // infer_request (subgraph.hpp:51-55): a subgraph only scores its own scenario
+        if (only_scenario >= 0 && only_scenario != m.subgraph)
+            fail(MTFM_INTEGRITY_ERROR, "request scenario " + std::to_string(only_scenario) +
+                                           " does not match subgraph scenario " + std::to_string(m.subgraph));
+        only_scenario = m.subgraph;
+    }
     finalize(m);
     // uploads go on the copy stream, after the previous forward of this batch object
     // (its device buffers are overwritten) and after the weights
@@ -1963,6 +1998,7 @@ mtfm_status mtfm_cuda_create(int device, const mtfm_model_desc* md, const mtfm_s
         if (m->sources.empty()) fail(MTFM_CONFIG_ERROR, "schema set is empty");
         m->slot_param.assign(m->slots.size(), "");
         register_params(*m);
+        for (size_t i = 0; i < m->params.size(); ++i) m->visible.push_back(i);
         ck(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking), "stream");
         ck(cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking), "copy stream");
         ck(cudaStreamCreateWithFlags(&m->d2h_stream, cudaStreamNonBlocking), "d2h stream");
@@ -1992,7 +2028,9 @@ mtfm_status mtfm_cuda_set_param(mtfm_cuda_model* m, const char* name, const floa
     return guard([&] {
         if (!m || !name || (!v && rows * cols)) fail(MTFM_CONTRACT_ERROR, "null argument");
         auto it = m->by_name.find(name);
-        if (it == m->by_name.end()) fail(MTFM_CONFIG_ERROR, std::string("unknown parameter: ") + name);
+        if (it == m->by_name.end() ||
+            (m->subgraph >= 0 && m->params[it->second].owner >= 0 && m->params[it->second].owner != m->subgraph))
+            fail(MTFM_CONFIG_ERROR, std::string("unknown parameter: ") + name);
         auto& p = m->params[it->second];
         if (p.rows != rows || p.cols != cols)
             fail(MTFM_DIMENSION_ERROR, std::string("shape mismatch for '") + name + "': expected " +
@@ -2005,13 +2043,32 @@ mtfm_status mtfm_cuda_set_param(mtfm_cuda_model* m, const char* name, const floa
     });
 }
 
-int64_t mtfm_cuda_num_params(const mtfm_cuda_model* m) { return m ? static_cast<int64_t>(m->params.size()) : 0; }
+int64_t mtfm_cuda_num_params(const mtfm_cuda_model* m) { return m ? static_cast<int64_t>(m->visible.size()) : 0; }
 
 const char* mtfm_cuda_param_name(const mtfm_cuda_model* m, int64_t i, int64_t* rows, int64_t* cols) {
-    if (!m || i < 0 || i >= static_cast<int64_t>(m->params.size())) return nullptr;
-    if (rows) *rows = m->params[i].rows;
-    if (cols) *cols = m->params[i].cols;
-    return m->params[i].name.c_str();
+    if (!m || i < 0 || i >= static_cast<int64_t>(m->visible.size())) return nullptr;
+    const auto& p = m->params[m->visible[static_cast<size_t>(i)]];
+    if (rows) *rows = p.rows;
+    if (cols) *cols = p.cols;
+    return p.name.c_str();
+}
+
+mtfm_status mtfm_cuda_restrict_to_scenario(mtfm_cuda_model* m, int32_t scenario_id) {
+    return guard([&] {
+        if (!m) fail(MTFM_CONTRACT_ERROR, "null argument");
+        bool known = false;
+        for (const auto& s : m->sources) known = known || (s.kind == 2 && s.id == scenario_id);
+        if (!known) fail(MTFM_CONFIG_ERROR, "extract_subgraph: unknown scenario " + std::to_string(scenario_id));
+        if (m->subgraph >= 0 && m->subgraph != scenario_id)
+            fail(MTFM_CONTRACT_ERROR, "model is already restricted to scenario " + std::to_string(m->subgraph));
+        m->subgraph = scenario_id;
+        m->visible.clear();
+        for (size_t i = 0; i < m->params.size(); ++i)
+            if (m->params[i].owner < 0 || m->params[i].owner == scenario_id) m->visible.push_back(i);
+        m->finalized = false;
+        m->srcw.clear();
+        m->layers.clear();
+    });
 }
 
 int64_t mtfm_cuda_count_records(const mtfm_cuda_model* m, const mtfm_packed_batch* b) {

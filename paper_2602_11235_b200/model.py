@@ -149,6 +149,22 @@ class Model:
         m.set_params(params)
         return m
 
+    # ---- scenario subgraph (subgraph.hpp:25-42)
+    def restrict_to_scenario(self, scenario_id: int):
+        """Turns this handle into a ScenarioSubgraph deployment: only the shared
+        parameters and scenario_id's own are registered (param_specs() is the
+        subgraph's ParamStore) and every forward is scoped to scenario_id."""
+        abi.check(abi.lib().mtfm_cuda_restrict_to_scenario(self._h, int(scenario_id)))
+        self.subgraph = int(scenario_id)
+        return self
+
+    @classmethod
+    def build_subgraph(cls, schemas, cfg, sub_params, scenario_id, precision="bf16", device=0):
+        """A model holding exactly extract_subgraph(model, scenario_id).params."""
+        m = cls(schemas, cfg, precision, device).restrict_to_scenario(scenario_id)
+        m.set_params(sub_params)
+        return m
+
     # ---- forward
     def _packed(self, b):
         return abi.PackedBatch(len(b["user_id"]), len(b["seq_kind"]), len(b["ev_ts"]), len(b["exp_ts"]),
@@ -233,6 +249,34 @@ class Model:
             self.close()
         except Exception:
             pass
+
+
+def infer_requests(model: Model, requests):
+    """Request-level serving at scale: many InferenceRequests scored in ONE
+    forward, each request one user sample of the packed batch (its candidates
+    as T tokens, tokenizer.hpp:138-153). Per request the records equal
+    infer_request(model, sub, request) (subgraph.hpp:47-62): T tokens never see
+    other users or each other. Returns one record list per request."""
+    requests = list(requests)
+    sub = getattr(model, "subgraph", -1)
+    for r in requests:
+        if sub >= 0 and r.scenario_id != sub:
+            raise abi.IntegrityError(f"request scenario {r.scenario_id} does not match subgraph scenario {sub}")
+    views = [sample_view_of_request(r) for r in requests]
+    # a full model binds all scenarios: each sample only holds its request's scenario,
+    # so the unscoped forward equals the per-request scoped ones
+    ra = model.forward_batch(pack_samples(views), sub)
+    out, pos = [], 0
+    for r in requests:
+        n = len(r.candidates) * len(model._tasks.get(r.scenario_id, []))
+        recs = []
+        for i in range(pos, pos + n):
+            task = model._tasks[int(ra.scenario_id[i])][int(ra.task_index[i])]
+            recs.append(PredictionRecord(int(ra.user_id[i]), int(ra.scenario_id[i]), int(ra.exposure_index[i]),
+                                         task, float(ra.probability[i]), -1))
+        out.append(recs)
+        pos += n
+    return out
 
 
 def infer_request(model: Model, request: InferenceRequest):
