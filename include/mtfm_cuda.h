@@ -285,6 +285,32 @@ MTFM_API mtfm_status mtfm_cuda_aggregate_sizes(const mtfm_cuda_aggregate* a, mtf
 MTFM_API mtfm_status mtfm_cuda_aggregate_fetch(mtfm_cuda_aggregate* a, const mtfm_packed_buffers* out);
 MTFM_API mtfm_status mtfm_cuda_aggregate_free(mtfm_cuda_aggregate* a);
 
+/* ---------------------------------------------------------------- dataset ingestion
+ * load_dataset (dataset_io.cpp:110-221: header line with the schemas, one
+ * UserSample JSON object per line) straight into packed jagged batches of
+ * chunk_users users each, parsed by n_threads worker threads (<= 0: all
+ * cores) into page-locked host memory, so every chunk reaches the GPU by an
+ * asynchronous H2D (mtfm_cuda_batch_prepare / _update) without per-user
+ * re-packing. Errors as the reference: MTFM_PARSE_ERROR "line N: ..." for the
+ * first malformed line (exact key sets, require_keys dataset_io.cpp:16-31),
+ * then validate_dataset (schema.cpp:45-139) in its order (CONFIG / INTEGRITY /
+ * LOOKUP). Host-only: needs no GPU (pageable memory when there is none). */
+typedef struct mtfm_dataset mtfm_dataset;
+typedef struct {
+    int32_t format_version;
+    int64_t n_users, n_chunks;
+    int32_t max_tasks; /* label columns per exposure */
+} mtfm_dataset_info_t;
+
+MTFM_API mtfm_status mtfm_dataset_load(const char* path, int32_t n_threads, int32_t chunk_users, mtfm_dataset** out);
+MTFM_API mtfm_status mtfm_dataset_info(const mtfm_dataset* d, mtfm_dataset_info_t* info);
+/* Schemas as a mtfm_schema_desc (pointers owned by the dataset) for mtfm_cuda_create. */
+MTFM_API mtfm_status mtfm_dataset_schema_desc(const mtfm_dataset* d, mtfm_schema_desc* out);
+/* Zero-copy view of chunk i (offsets chunk-local); labels: [n_exposures][max_tasks]
+ * in scenario task order, -1 where absent. Valid until mtfm_dataset_free. */
+MTFM_API mtfm_status mtfm_dataset_chunk(const mtfm_dataset* d, int64_t i, mtfm_packed_batch* out, const int32_t** labels);
+MTFM_API void mtfm_dataset_free(mtfm_dataset* d);
+
 #ifdef __cplusplus
 }
 #endif

@@ -112,6 +112,11 @@ class PackedBuffers(C.Structure):
                                            "exp_feat_off", "exp_blk", "exp_feats", "exp_src")]
 
 
+class DatasetInfo(C.Structure):
+    _fields_ = [("format_version", C.c_int32), ("n_users", C.c_int64), ("n_chunks", C.c_int64),
+                ("max_tasks", C.c_int32)]
+
+
 # (name, restype, argtypes) — every symbol include/mtfm_cuda.h declares.
 SIGNATURES = [
     ("mtfm_cuda_last_error", C.c_char_p, []),
@@ -145,6 +150,11 @@ SIGNATURES = [
     ("mtfm_cuda_aggregate_sizes", C.c_int, [C.c_void_p, C.POINTER(PackedSizes)]),
     ("mtfm_cuda_aggregate_fetch", C.c_int, [C.c_void_p, C.POINTER(PackedBuffers)]),
     ("mtfm_cuda_aggregate_free", C.c_int, [C.c_void_p]),
+    ("mtfm_dataset_load", C.c_int, [C.c_char_p, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
+    ("mtfm_dataset_info", C.c_int, [C.c_void_p, C.POINTER(DatasetInfo)]),
+    ("mtfm_dataset_schema_desc", C.c_int, [C.c_void_p, C.POINTER(SchemaDesc)]),
+    ("mtfm_dataset_chunk", C.c_int, [C.c_void_p, C.c_int64, C.POINTER(PackedBatch), C.POINTER(C.POINTER(C.c_int32))]),
+    ("mtfm_dataset_free", None, [C.c_void_p]),
 ]
 
 _lib = None

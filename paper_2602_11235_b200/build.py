@@ -11,7 +11,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libmtfm_cuda.so")
 BUILD = os.path.join(ROOT, "build", "mtfm_cuda")
-SOURCES = ["kernels.cu", "model.cu", "aggregate.cu"]
+SOURCES = ["kernels.cu", "model.cu", "aggregate.cu", "ingest.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
