@@ -11,9 +11,7 @@ points where the CUDA fast path stores bf16 (paper_2602_11235_b200/csrc):
     layer right after it)                     folded bf16(gain (.) W), fp32 (bias W + b)
   projections silu(. W + b)                   bf16 (U, Q, K, V)
   attention weights silu(Q K^T)               bf16 P; the T self term and O stay fp32
-  attention output s_i * O                    bf16 A, except where the gate is fused
-                                              into the attention epilogue (d_h <= 64
-                                              shapes, model.cu gate_fuse): fp32 A
+  attention output s_i * O                    bf16 A
   gate gln2(A) * U                            bf16
   f2 + residual                               fp32
   head input (final T rows)                   bf16
@@ -35,21 +33,10 @@ def rb(x):
     return u.view(np.float32)
 
 
-def gate_fused(cfg):
-    """model.cu gate_fuse: every head group of a row block fits the attention CTA's TMEM."""
-    D = cfg.head_dim
-    r = cfg.heads // cfg.kv_heads
-    hs = r if (r <= 128 and 128 % r == 0 and 128 // r >= 8) else 1
-    tpi = cfg.kv_heads * ((r + hs - 1) // hs)
-    o_col = 3 * (128 if D <= 64 else 64)
-    return tpi <= 8 and o_col + tpi * D <= 512 and (cfg.heads * D) % 8 == 0
-
-
 class Bf16Oracle(O.Oracle):
     def __init__(self, sch, cfg, params):
         super().__init__(sch, cfg, params, np.float32)
         self.W = {}  # bf16-rounded weight cache
-        self.fused_gate = gate_fused(cfg)
 
     def w(self, name):
         if name not in self.W:
@@ -116,8 +103,7 @@ class Bf16Oracle(O.Oracle):
                 ws = O.silu(np.einsum("ij,ij->i", q[:, h * dh:(h + 1) * dh], kk[self_col]).astype(np.float32))
                 o = o + ws[:, None] * vv[self_col]
             outs.append(o * scale[:, None])
-        a = np.concatenate(outs, axis=1).astype(np.float32)
-        return a if self.fused_gate else rb(a)
+        return rb(np.concatenate(outs, axis=1))
 
     def gate(self, a, groups, prefix, u):
         return rb(self.gln_affine(O.row_normalize(a, self.cfg.eps), groups, prefix) * u)

@@ -54,19 +54,8 @@ struct AttnParams {
     long long ldq;
     const __nv_bfloat16* kv_ptr;
     long long ldkv;
-    __nv_bfloat16* out;          // A rows indexed like Q rows (gate mode: G = gln2(A) (.) U)
+    __nv_bfloat16* out;          // A rows indexed like Q rows
     long long ldo;
-    // Work items: tpi consecutive tiles (the same query rows, every head group) go to one
-    // CTA. gate_u != nullptr is the fused-gate mode (hta.hpp:153,179): all heads of the
-    // item's rows sit in TMEM together (o_sets sets of tpi O buffers), the epilogue takes
-    // the row statistics over the whole hd-wide row and writes gln2(s * O) (.) U instead of A.
-    int tpi, o_sets;
-    const __nv_bfloat16* gate_u;  // U rows indexed like Q rows
-    long long ldu;
-    const int* gate_group;        // GLN group per Q row
-    const float* gate_gain;       // [groups][hd]
-    const float* gate_bias;
-    float eps;
 };
 
 namespace attn_detail {
@@ -87,7 +76,7 @@ struct Cfg {
     // PV warp by a few tiles, and TMA latency must hide behind the rest
     static constexpr int kStagesRaw = (200 * 1024 - QB * Q_BYTES) / STAGE_BYTES;
     static constexpr int kStages = kStagesRaw > 12 ? 12 : kStagesRaw;
-    static constexpr int SMEM = QB * Q_BYTES + kStages * STAGE_BYTES + 1024 + 512 + 512;  // + gate row sums
+    static constexpr int SMEM = QB * Q_BYTES + kStages * STAGE_BYTES + 1024 + 512;
     static constexpr uint32_t TMEM_COLS = 512;
     static constexpr int NB = 3;                            // S/P TMEM buffers (P aliases S)
     static constexpr uint32_t O_COL = NB * BKV;
@@ -104,58 +93,6 @@ __device__ __forceinline__ uint32_t sw128_off(uint32_t row, uint32_t chunk16) {
 }
 
 using ptx::silu2_bf16;
-
-// silu(Q_head[qrow] . K_g[self_row]): the T self key's weight (one visible column
-// outside the prefix, mask.cpp:21-23), in fp32 from the bf16 operands.
-template <int D>
-__device__ __forceinline__ float self_weight(const AttnParams& prm, int qrow, int head, int self_row, int g) {
-    const __nv_bfloat16* qp = prm.q_ptr + (long long)qrow * prm.ldq + prm.q_col0 + head * D;
-    const __nv_bfloat16* kp = prm.kv_ptr + (long long)self_row * prm.ldkv + prm.k_col0 + g * D;
-    float dot = 0.f;
-#pragma unroll 4
-    for (int e = 0; e < D; e += 8) {
-        const uint4 a = *reinterpret_cast<const uint4*>(qp + e);
-        const uint4 b = *reinterpret_cast<const uint4*>(kp + e);
-        const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
-        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const float2 fa = __bfloat1622float2(a2[k]), fb = __bfloat1622float2(b2[k]);
-            dot = fmaf(fa.x, fb.x, dot);
-            dot = fmaf(fa.y, fb.y, dot);
-        }
-    }
-    return silu_precise(dot);
-}
-
-// 16 columns [c, c + 16) of one O row from TMEM (+ the self term), times `mul`.
-template <int D>
-__device__ __forceinline__ void o_chunk(const AttnParams& prm, uint32_t taddr, int n_kv, bool valid, int self_row,
-                                        float wself, int g, int c, float mul, float (&v)[16]) {
-    ptx::tmem_ld16(taddr, v);
-    ptx::tmem_ld_wait();
-    if (n_kv == 0) {
-#pragma unroll
-        for (int e = 0; e < 16; ++e) v[e] = 0.f;
-    }
-    if (valid && self_row >= 0) {
-        const __nv_bfloat16* vp = prm.kv_ptr + (long long)self_row * prm.ldkv + prm.v_col0 + g * D + c;
-        const uint4 a = *reinterpret_cast<const uint4*>(vp);
-        const uint4 b = *reinterpret_cast<const uint4*>(vp + 8);
-        const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
-        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const float2 fa = __bfloat1622float2(a2[k]), fb = __bfloat1622float2(b2[k]);
-            v[2 * k] += wself * fa.x;
-            v[2 * k + 1] += wself * fa.y;
-            v[8 + 2 * k] += wself * fb.x;
-            v[8 + 2 * k + 1] += wself * fb.y;
-        }
-    }
-#pragma unroll
-    for (int e = 0; e < 16; ++e) v[e] *= mul;
-}
 
 }  // namespace attn_detail
 
@@ -185,14 +122,10 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
     uint64_t* kv_full = bars + 8 + 3 * NB;  // [kStages]
     uint64_t* kv_empty = kv_full + C::kStages;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kv_empty + C::kStages);
-    float* red = reinterpret_cast<float*>(bars + 64);  // [128] per-lane partial row sums (gate epilogue)
 
     const uint32_t warp = ptx::warp_id();
     const uint32_t lane = ptx::lane_id();
     const int r_per_g = prm.heads / prm.kv_heads;
-    // k-th tile of this CTA: items (tpi consecutive tiles) strided over the grid
-    const int tpi = prm.tpi;
-    auto tile_at = [&](int k) { return (static_cast<int>(blockIdx.x) + (k / tpi) * static_cast<int>(gridDim.x)) * tpi + k % tpi; };
 
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < 2; ++i) {
@@ -227,7 +160,8 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
         if (ptx::elect_one()) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int it = 0, t = tile_at(0); t < prm.n_tiles; t = tile_at(++it)) {
+            int it = 0;
+            for (int t = blockIdx.x; t < prm.n_tiles; t += gridDim.x, ++it) {
                 const AttnTile tile = prm.tiles[t];
                 const int g = tile.head0 / r_per_g;
                 const int n_kv = (tile.kmax + BKV - 1) / BKV;
@@ -266,7 +200,8 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
         int stage = 0;
         uint32_t phase = 0;
         uint32_t s_cnt = 0;
-        for (int it = 0, t = tile_at(0); t < prm.n_tiles; t = tile_at(++it)) {
+        int it = 0;
+        for (int t = blockIdx.x; t < prm.n_tiles; t += gridDim.x, ++it) {
             const AttnTile tile = prm.tiles[t];
             const int n_kv = (tile.kmax + BKV - 1) / BKV;
             const int qb = it % C::QB;
@@ -314,22 +249,15 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
         uint32_t phase_unused = 0;
         (void)phase_unused;
         uint32_t cnt = 0;
-        for (int it = 0, t = tile_at(0); t < prm.n_tiles; t = tile_at(++it)) {
+        int it = 0;
+        for (int t = blockIdx.x; t < prm.n_tiles; t += gridDim.x, ++it) {
             const AttnTile tile = prm.tiles[t];
             const int n_kv = (tile.kmax + BKV - 1) / BKV;
-            // O buffer of this tile; the item's set is handed over as a whole (o_full after its
-            // last tile, o_empty once the epilogue read every buffer of the set)
-            const int item = it / tpi, gi = it % tpi;
-            const int n_sets = prm.gate_u != nullptr ? prm.o_sets : kOB;
-            const int set = item % n_sets;
-            const int ob = set * tpi + gi;
-            const bool last = gi == tpi - 1;
-            if (gi == 0) {
-                ptx::mbar_wait(&o_empty[set], ((item / n_sets) & 1) ^ 1);
-                ptx::tc_fence_after();
-            }
+            const int ob = it % kOB;
+            ptx::mbar_wait(&o_empty[ob], ((it / kOB) & 1) ^ 1);
+            ptx::tc_fence_after();
             if (n_kv == 0) {
-                if (last && ptx::elect_one()) ptx::umma_commit(&o_full[set]);
+                if (ptx::elect_one()) ptx::umma_commit(&o_full[ob]);
                 __syncwarp();
                 continue;
             }
@@ -351,7 +279,7 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
                     }
                     ptx::umma_commit(&kv_empty[stage]);
                     ptx::umma_commit(&s_empty[buf]);
-                    if (j == n_kv - 1 && last) ptx::umma_commit(&o_full[set]);
+                    if (j == n_kv - 1) ptx::umma_commit(&o_full[ob]);
                 }
                 __syncwarp();
                 if (++stage == C::kStages) stage = 0;
@@ -366,7 +294,7 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
         const uint32_t lane_addr = (q * 32u) << 16;
         // (announcing P(j) only after issuing the S load of tile j+1 measured 3-5% slower)
         uint32_t s_cnt = 0;
-        for (int it = 0, t = tile_at(0); t < prm.n_tiles; t = tile_at(++it)) {
+        for (int t = blockIdx.x; t < prm.n_tiles; t += gridDim.x) {
             const AttnTile tile = prm.tiles[t];
             const int n_kv = (tile.kmax + BKV - 1) / BKV;
             const int hs = m / prm.rt;
@@ -409,12 +337,13 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
                 if (lane == 0) ptx::mbar_arrive(&p_full[buf]);
             }
         }
-    } else if (warp >= 4 + C::kSilu && prm.gate_u == nullptr) {
-        // ------------------------------------------------ epilogue warps: s_i * (O + self term) -> bf16 A
+    } else if (warp >= 4 + C::kSilu) {
+        // ------------------------------------------------ epilogue warps
         const uint32_t q = warp & 3;
         const uint32_t m = q * 32 + lane;
         const uint32_t lane_addr = (q * 32u) << 16;
-        for (int it = 0, t = tile_at(0); t < prm.n_tiles; t = tile_at(++it)) {
+        int it = 0;
+        for (int t = blockIdx.x; t < prm.n_tiles; t += gridDim.x, ++it) {
             const AttnTile tile = prm.tiles[t];
             const int n_kv = (tile.kmax + BKV - 1) / BKV;
             const int ob = it % kOB;
@@ -430,15 +359,54 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
             if (valid) {
                 scale = __ldg(prm.q_scale + qrow);
                 self_row = __ldg(prm.q_self + qrow);
-                if (self_row >= 0) wself = attn_detail::self_weight<D>(prm, qrow, head, self_row, g);
+                if (self_row >= 0) {
+                    const __nv_bfloat16* qp = prm.q_ptr + (long long)qrow * prm.ldq + prm.q_col0 + head * D;
+                    const __nv_bfloat16* kp = prm.kv_ptr + (long long)self_row * prm.ldkv + prm.k_col0 + g * D;
+                    float dot = 0.f;
+#pragma unroll 4
+                    for (int e = 0; e < D; e += 8) {
+                        const uint4 a = *reinterpret_cast<const uint4*>(qp + e);
+                        const uint4 b = *reinterpret_cast<const uint4*>(kp + e);
+                        const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
+                        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b);
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const float2 fa = __bfloat1622float2(a2[k]), fb = __bfloat1622float2(b2[k]);
+                            dot = fmaf(fa.x, fb.x, dot);
+                            dot = fmaf(fa.y, fb.y, dot);
+                        }
+                    }
+                    wself = silu_precise(dot);
+                }
             }
             ptx::mbar_wait(&o_full[ob], (it / kOB) & 1);
             ptx::tc_fence_after();
 #pragma unroll 1
             for (int c = 0; c < D; c += 16) {
                 float v[16];
-                attn_detail::o_chunk<D>(prm, tmem + lane_addr + kOCol + ob * D + c, n_kv, valid, self_row, wself, g, c, 1.f, v);
+                ptx::tmem_ld16(tmem + lane_addr + kOCol + ob * D + c, v);
+                ptx::tmem_ld_wait();
+                if (n_kv == 0) {
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) v[e] = 0.f;
+                }
                 if (valid) {
+                    if (self_row >= 0) {
+                        const __nv_bfloat16* vp =
+                            prm.kv_ptr + (long long)self_row * prm.ldkv + prm.v_col0 + g * D + c;
+                        const uint4 a = *reinterpret_cast<const uint4*>(vp);
+                        const uint4 b = *reinterpret_cast<const uint4*>(vp + 8);
+                        const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
+                        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b);
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const float2 fa = __bfloat1622float2(a2[k]), fb = __bfloat1622float2(b2[k]);
+                            v[2 * k] += wself * fa.x;
+                            v[2 * k + 1] += wself * fa.y;
+                            v[8 + 2 * k] += wself * fb.x;
+                            v[8 + 2 * k + 1] += wself * fb.y;
+                        }
+                    }
                     __nv_bfloat16* o = prm.out + (long long)qrow * prm.ldo + head * D + c;
                     uint4 w0, w1;
                     w0.x = pack_bf16(v[0] * scale, v[1] * scale);
@@ -456,135 +424,6 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&o_empty[ob]);
-        }
-    } else if (warp >= 4 + C::kSilu) {
-        // ------------------------------------------------ epilogue warps, fused gate
-        // The item's rows: lane m holds row i = m % rt of head (m / rt) of each of the tpi
-        // tiles (buffers set*tpi + gi). x = s_i * (O + self term) in fp32; the GLN2 row
-        // statistics over all hd columns are reduced across the four epilogue warps through
-        // shared memory (two passes, centred), then G = (gln2(x)) (.) U goes out as bf16.
-        constexpr int kMaxTpi = 8;
-        const uint32_t q = warp & 3;
-        const uint32_t m = q * 32 + lane;
-        const uint32_t lane_addr = (q * 32u) << 16;
-        const int hs = m / prm.rt;
-        const int i = m - hs * prm.rt;
-        const int hd = prm.heads * D;
-        const float inv_hd = 1.f / static_cast<float>(hd);
-        for (int k = 0, item = 0, t0 = tile_at(0); t0 < prm.n_tiles; k += tpi, ++item, t0 = tile_at(k)) {
-            const AttnTile tile = prm.tiles[t0];
-            const int n_kv = (tile.kmax + BKV - 1) / BKV;
-            const int set = item % prm.o_sets;
-            const bool valid = i < tile.n_rows;
-            const int qrow = tile.q_row0 + i;
-            float scale = 0.f;
-            int self_row = -1, grp = 0;
-            float wself[kMaxTpi];
-            int head[kMaxTpi], g[kMaxTpi];
-#pragma unroll
-            for (int gi = 0; gi < kMaxTpi; ++gi) {
-                wself[gi] = 0.f;
-                head[gi] = 0;
-                g[gi] = 0;
-                if (gi < tpi) {
-                    const int h0 = prm.tiles[t0 + gi].head0;
-                    head[gi] = h0 + hs;
-                    g[gi] = h0 / r_per_g;
-                }
-            }
-            if (valid) {
-                scale = __ldg(prm.q_scale + qrow);
-                self_row = __ldg(prm.q_self + qrow);
-                grp = __ldg(prm.gate_group + qrow);
-                grp = grp < 0 ? 0 : grp;
-#pragma unroll
-                for (int gi = 0; gi < kMaxTpi; ++gi)
-                    if (gi < tpi && self_row >= 0) wself[gi] = attn_detail::self_weight<D>(prm, qrow, head[gi], self_row, g[gi]);
-            }
-            ptx::mbar_wait(&o_full[set], (item / prm.o_sets) & 1);
-            ptx::tc_fence_after();
-            auto xchunk = [&](int gi, int c, float (&v)[16]) {
-                attn_detail::o_chunk<D>(prm, tmem + lane_addr + kOCol + (set * tpi + gi) * D + c, n_kv, valid, self_row,
-                                        wself[gi], g[gi], c, scale, v);
-            };
-            // pass 1: row sums
-            float acc = 0.f;
-#pragma unroll 1
-            for (int gi = 0; gi < tpi; ++gi)
-#pragma unroll 1
-                for (int c = 0; c < D; c += 16) {
-                    float v[16];
-                    xchunk(gi, c, v);
-#pragma unroll
-                    for (int e = 0; e < 16; ++e) acc += v[e];
-                }
-            red[m] = acc;
-            ptx::named_bar_sync(1, 128);
-            float tot = 0.f;
-            for (int h = 0; h < prm.hs; ++h) tot += red[h * prm.rt + i];
-            const float mean = tot * inv_hd;
-            ptx::named_bar_sync(1, 128);
-            // pass 2: centred squares
-            acc = 0.f;
-#pragma unroll 1
-            for (int gi = 0; gi < tpi; ++gi)
-#pragma unroll 1
-                for (int c = 0; c < D; c += 16) {
-                    float v[16];
-                    xchunk(gi, c, v);
-#pragma unroll
-                    for (int e = 0; e < 16; ++e) acc += (v[e] - mean) * (v[e] - mean);
-                }
-            red[m] = acc;
-            ptx::named_bar_sync(1, 128);
-            tot = 0.f;
-            for (int h = 0; h < prm.hs; ++h) tot += red[h * prm.rt + i];
-            const float rstd = rsqrtf(tot * inv_hd + prm.eps);
-            ptx::named_bar_sync(1, 128);
-            // pass 3: G = ((x - mean) rstd gain + bias) (.) U
-#pragma unroll 1
-            for (int gi = 0; gi < tpi; ++gi)
-#pragma unroll 1
-                for (int c = 0; c < D; c += 16) {
-                    float v[16];
-                    xchunk(gi, c, v);
-                    if (!valid) continue;
-                    const int col = head[gi] * D + c;
-                    const float* ga = prm.gate_gain + (long long)grp * hd + col;
-                    const float* be = prm.gate_bias + (long long)grp * hd + col;
-                    const __nv_bfloat16* up = prm.gate_u + (long long)qrow * prm.ldu + col;
-                    const uint4 u0 = *reinterpret_cast<const uint4*>(up);
-                    const uint4 u1 = *reinterpret_cast<const uint4*>(up + 8);
-                    const __nv_bfloat162* uh0 = reinterpret_cast<const __nv_bfloat162*>(&u0);
-                    const __nv_bfloat162* uh1 = reinterpret_cast<const __nv_bfloat162*>(&u1);
-                    float u[16];
-#pragma unroll
-                    for (int k2 = 0; k2 < 4; ++k2) {
-                        const float2 a = __bfloat1622float2(uh0[k2]), b = __bfloat1622float2(uh1[k2]);
-                        u[2 * k2] = a.x;
-                        u[2 * k2 + 1] = a.y;
-                        u[8 + 2 * k2] = b.x;
-                        u[8 + 2 * k2 + 1] = b.y;
-                    }
-                    uint32_t w[8];
-#pragma unroll
-                    for (int e = 0; e < 16; e += 4) {
-                        const float4 gv = __ldg(reinterpret_cast<const float4*>(ga + e));
-                        const float4 bv = __ldg(reinterpret_cast<const float4*>(be + e));
-                        const float y0 = ((v[e] - mean) * rstd * gv.x + bv.x) * u[e];
-                        const float y1 = ((v[e + 1] - mean) * rstd * gv.y + bv.y) * u[e + 1];
-                        const float y2 = ((v[e + 2] - mean) * rstd * gv.z + bv.z) * u[e + 2];
-                        const float y3 = ((v[e + 3] - mean) * rstd * gv.w + bv.w) * u[e + 3];
-                        w[e / 2] = pack_bf16(y0, y1);
-                        w[e / 2 + 1] = pack_bf16(y2, y3);
-                    }
-                    uint4* o = reinterpret_cast<uint4*>(prm.out + (long long)qrow * prm.ldo + col);
-                    o[0] = make_uint4(w[0], w[1], w[2], w[3]);
-                    o[1] = make_uint4(w[4], w[5], w[6], w[7]);
-                }
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&o_empty[set]);
         }
     }
     ptx::tc_fence_before();

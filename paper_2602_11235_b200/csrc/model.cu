@@ -878,21 +878,6 @@ struct AttnGeom {
     int hs, rt;
 };
 
-// Fused gate (attn_tc.cuh, gate_u set): every head group of a row block in one CTA, all
-// of its O buffers in TMEM at once (d_h <= 64 shapes). Returns (on, tiles per item, O sets).
-struct GateFuse {
-    bool on;
-    int tpi, o_sets;
-};
-GateFuse gate_fuse(const mtfm_cuda_model& m, int hs) {
-    const int D = m.dh;
-    const int bkv = D <= 64 ? 128 : 64;
-    const int o_col = 3 * bkv;
-    const int tpi = m.G * ((m.H / m.G + hs - 1) / hs);
-    if (tpi > 8 || o_col + tpi * D > 512 || m.hd % 8) return {false, 1, 0};
-    return {true, tpi, o_col + 2 * tpi * D <= 512 ? 2 : 1};
-}
-
 AttnGeom attn_geom(const mtfm_cuda_model& m) {
     const int r = m.H / m.G;
     if (r <= 128 && 128 % r == 0 && 128 / r >= 8) return {r, 128 / r};
@@ -908,7 +893,7 @@ void launch_attn_tc_d(const AttnParams& p, cudaStream_t st) {
            "attn smem attr");
         attr = true;
     }
-    const int grid = std::min(p.n_tiles / p.tpi, kNumSMs);
+    const int grid = std::min(p.n_tiles, kNumSMs);
     launch_k(attn_tc_kernel<D>, dim3(grid), dim3(C::kThreads), C::SMEM, st, p);
     ck(cudaGetLastError(), "attn_tc launch");
 }
@@ -916,7 +901,6 @@ void launch_attn_tc_d(const AttnParams& p, cudaStream_t st) {
 void run_attn_tc(const mtfm_cuda_model& m, AttnParams p, const __nv_bfloat16* q, long long n_q, long long q_cols,
                  long long kv_rows, long long kv_cols, cudaStream_t st) {
     if (p.n_tiles == 0) return;
-    if (p.tpi < 1) p.tpi = 1;
     const int D = m.dh;
     const int chunk = std::min(D, 64);
     const int bkv = D <= 128 ? 128 : 64;
@@ -963,10 +947,9 @@ __global__ void tile_expand_kernel(const long long* __restrict__ toff, const int
     const int qc = static_cast<int>((ev1 - ev0 + rt - 1) / rt), qt = static_cast<int>((x1 - x0 + rt - 1) / rt);
     const int per_group = qc + qt;
     const int hpg = (r + hs - 1) / hs;
-    const int n_grp = G * hpg;  // tiles per row block: consecutive, so one CTA can own every head of the rows
     const long long f0 = toff[u], t0 = toff[n_users + 1 + u];
-    for (int i = threadIdx.x; i < n_grp * per_group; i += blockDim.x) {
-        const int k = i / n_grp, grp = i - k * n_grp;
+    for (int i = threadIdx.x; i < G * hpg * per_group; i += blockDim.x) {
+        const int grp = i / per_group, k = i - grp * per_group;
         const int g = grp / hpg, hb0 = (grp - g * hpg) * hs;
         const int head0 = g * r + hb0;
         if (k < qc) {
@@ -977,8 +960,7 @@ __global__ void tile_expand_kernel(const long long* __restrict__ toff, const int
             const long long q = x0 + static_cast<long long>(k - qc) * rt;
             const int n = static_cast<int>(min(static_cast<long long>(rt), x1 - q));
             tf[f0 + i] = {static_cast<int>(n_events + q), n, static_cast<int>(ev0), head0, 0, {0, 0, 0}};
-            tt[t0 + static_cast<long long>(k - qc) * n_grp + grp] = {static_cast<int>(q), n, static_cast<int>(ev0), head0,
-                                                                     0, {0, 0, 0}};
+            tt[t0 + grp * qt + (k - qc)] = {static_cast<int>(q), n, static_cast<int>(ev0), head0, 0, {0, 0, 0}};
         }
     }
 }
@@ -1475,7 +1457,6 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
         // into its own copy of the K|V (target) / f1 (full) weights (LayerW::tfold), and
         // the GEMM outputs are scattered back to X-row order.
         size_t full_ctx_from_run = static_cast<size_t>(-1);  // full layer whose context rows come from xhat
-        const GateFuse gf = gate_fuse(m, ag.hs);             // gate in the attention epilogue (small / base shapes)
         T* XNT = XN + NE * d;                                 // T rows' GLN1 of the current target layer
         T* XNF = XN + R * d;                                  // GLN1 of a full layer's rows (T rows only after a run)
         int tl = 0;                                           // index of the current target layer within its run
@@ -1525,8 +1506,7 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                     run_gemm_tc(pp, st, L, BT);
                 }
                 {
-                    StageScope sc(m, "attn_full", 4.0 * hd * sc_full,
-                                  Rd * (hd + 2 * gd) * el + Rd * hd * el * (gf.on ? 2 : 1));
+                    StageScope sc(m, "attn_full", 4.0 * hd * sc_full, Rd * (hd + 2 * gd) * el + Rd * hd * el);
                     AttnParams ap{};
                     ap.tiles = B.tiles_full.as<AttnTile>();
                     ap.n_tiles = n_full;
@@ -1544,20 +1524,12 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                     ap.ldq = ldqkv;
                     ap.kv_ptr = QKV;
                     ap.ldkv = ldqkv;
-                    ap.out = gf.on ? G : A;
+                    ap.out = A;
                     ap.ldo = hd;
-                    ap.tpi = gf.on ? gf.tpi : 1;
-                    ap.o_sets = gf.o_sets;
-                    ap.gate_u = gf.on ? U : nullptr;
-                    ap.ldu = hd;
-                    ap.gate_group = rm.src;
-                    ap.gate_gain = Lw->g2g.as<float>();
-                    ap.gate_bias = Lw->g2b.as<float>();
-                    ap.eps = eps;
                     run_attn_tc(m, ap, QKV, R, ldqkv, R, ldqkv, st);
                     ++L;
                 }
-                if (!gf.on) {
+                {
                     StageScope sc(m, "gate", 0, Rd * hd * el * 3);
                     launch_gate<T>(A, hd, U, hd, R, hd, rm.src, Lw->g2g.as<float>(), Lw->g2b.as<float>(), eps, G, hd, st);
                     ++L;
@@ -1617,8 +1589,7 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                 }
                 ++tl;
                 {
-                    StageScope sc(m, "attn_target", 4.0 * hd * sc_t,
-                                  Rd * 2 * gd * el + Td * 2 * hd * el + (gf.on ? Td * hd * el : 0));
+                    StageScope sc(m, "attn_target", 4.0 * hd * sc_t, Rd * 2 * gd * el + Td * 2 * hd * el);
                     AttnParams ap{};
                     ap.tiles = B.tiles_tgt.as<AttnTile>();
                     ap.n_tiles = n_tgt;
@@ -1636,20 +1607,12 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                     ap.ldq = 2 * hd;
                     ap.kv_ptr = KVl;
                     ap.ldkv = 2 * gd;
-                    ap.out = gf.on ? G : A;
+                    ap.out = A;
                     ap.ldo = hd;
-                    ap.tpi = gf.on ? gf.tpi : 1;
-                    ap.o_sets = gf.o_sets;
-                    ap.gate_u = gf.on ? UQ : nullptr;
-                    ap.ldu = 2 * hd;
-                    ap.gate_group = rm.src + NE;
-                    ap.gate_gain = Lw->g2g.as<float>();
-                    ap.gate_bias = Lw->g2b.as<float>();
-                    ap.eps = eps;
                     run_attn_tc(m, ap, UQ, NT, 2 * hd, R, 2 * gd, st);
                     ++L;
                 }
-                if (!gf.on) {
+                {
                     StageScope sc(m, "gate", 0, Td * hd * el * 3);
                     launch_gate<T>(A, hd, UQ, 2 * hd, NT, hd, rm.src + NE, Lw->g2g.as<float>(), Lw->g2b.as<float>(),
                                    eps, G, hd, st);
