@@ -285,6 +285,40 @@ MTFM_API mtfm_status mtfm_cuda_aggregate_sizes(const mtfm_cuda_aggregate* a, mtf
 MTFM_API mtfm_status mtfm_cuda_aggregate_fetch(mtfm_cuda_aggregate* a, const mtfm_packed_buffers* out);
 MTFM_API mtfm_status mtfm_cuda_aggregate_free(mtfm_cuda_aggregate* a);
 
+/* ---------------------------------------------------------------- training
+ * Trainer::train_step (train.hpp:111-147) on the GPU over every user of a
+ * prepared batch: build_loss (model.hpp:323-358: per sample the mean BCE over
+ * its records, tape.hpp:462-486) through the whole model, gradients summed
+ * over the batch and scaled by 1/global_batch, then ParamStore::adam_step
+ * (params.hpp:87-119: non-finite check, global-norm clip, bias-corrected
+ * Adam) on the device weights. fp32 (MTFM_PRECISION_FP32_CHECK handles only).
+ * labels: [n_exposures][max_tasks] int32 in batch order, the scenario's task
+ * order, -1 absent (a needed absent label -> MTFM_INTEGRITY_ERROR, like
+ * build_loss). Data parallel: after mtfm_cuda_dp_init every rank's gradients
+ * (and loss) are summed by one NCCL all-reduce before the clip and Adam, so
+ * the ranks stay identical; global_batch = users over all ranks. */
+typedef struct { /* AdamConfig (params.hpp:14-20) + the global batch */
+    double lr, beta1, beta2, eps, clip_norm;
+    int64_t global_batch; /* <= 0: this batch's users */
+} mtfm_train_config;
+
+typedef struct {
+    double loss;      /* mean per-sample loss of the (global) batch, as train_step returns */
+    double grad_norm; /* global gradient norm before clipping */
+    int64_t step;     /* Adam step count */
+    int64_t records;
+} mtfm_train_result;
+
+MTFM_API mtfm_status mtfm_cuda_train_step(mtfm_cuda_model* m, mtfm_cuda_batch* b, const int32_t* labels, int32_t max_tasks,
+                                          const mtfm_train_config* cfg, mtfm_train_result* out);
+/* Current value (device weights after training) / last step's gradient of a parameter. */
+MTFM_API mtfm_status mtfm_cuda_get_param(mtfm_cuda_model* m, const char* name, float* host, int64_t rows, int64_t cols);
+MTFM_API mtfm_status mtfm_cuda_get_grad(mtfm_cuda_model* m, const char* name, float* host, int64_t rows, int64_t cols);
+/* Data parallel over NCCL (NVLink / NVSwitch): rank 0 makes the 128-byte id, every rank
+ * passes it with its rank (one model handle per GPU). */
+MTFM_API mtfm_status mtfm_nccl_unique_id(void* out128);
+MTFM_API mtfm_status mtfm_cuda_dp_init(mtfm_cuda_model* m, int32_t nranks, int32_t rank, const void* unique_id128);
+
 /* ---------------------------------------------------------------- dataset ingestion
  * load_dataset (dataset_io.cpp:110-221: header line with the schemas, one
  * UserSample JSON object per line) straight into packed jagged batches of

@@ -27,6 +27,7 @@
 #include "mtfa.hpp"
 #include "mtfm/datagen.hpp"
 #include "mtfm/model.hpp"
+#include "mtfm/train.hpp"
 #include "mtfm/verify.hpp"
 
 using namespace mtfm;
@@ -44,6 +45,8 @@ struct Opts {
     bool params = false;       // dump full f32 parameters
     uint64_t jitter = 0;       // != 0: perturb biases / GLN affines / towers (jitter_params)
     double tower_scale = 1.0;
+    int train_steps = 0;       // > 0: Trainer::train_step over every user of the batch, dumped
+    double lr = 1e-3;
 };
 
 Opts parse(int argc, char** argv) {
@@ -100,6 +103,8 @@ Opts parse(int argc, char** argv) {
         else if (a == "--params") o.params = true;
         else if (a == "--jitter") o.jitter = std::stoull(nxt());
         else if (a == "--tower-scale") o.tower_scale = std::stod(nxt());
+        else if (a == "--train") o.train_steps = std::stoi(nxt());
+        else if (a == "--lr") o.lr = std::stod(nxt());
         else throw config_error("unknown flag " + a);
     }
     if (o.out.empty()) throw config_error("--out required");
@@ -426,6 +431,47 @@ int main(int argc, char** argv) {
         w.put("rec/prob32", prob32);
         w.put("rec/logit64", logit64);
         w.put("rec/logit32", logit32);
+        if (o.train_steps > 0) {
+            // Trainer::train_step (train.hpp:111-147) on the f64 model carrying the f32 weights:
+            // every user of the batch in one minibatch, one worker; the per-parameter gradients
+            // of step 1 (already x 1/batch, before clipping), the parameters after step 1 and
+            // after the last step, and the per-step losses
+            Model<double> mt = m64;
+            Dataset dd;
+            dd.hist_seq_schemas = ss.hist;
+            dd.rt_seq_schemas = ss.rt;
+            dd.scenarios = ss.scenarios;
+            dd.samples = samples;
+            TrainConfig tc;
+            tc.batch_size = static_cast<int>(samples.size());
+            tc.threads = 1;
+            tc.adam.lr = o.lr;
+            Trainer<double> tr(mt, dd, tc);
+            std::vector<const UserSample*> batch;
+            for (const auto& s : dd.samples) batch.push_back(&s);
+            std::vector<double> losses;
+            for (int step = 0; step < o.train_steps; ++step) {
+                losses.push_back(tr.train_step(batch));
+                if (step == 0)
+                    for (const auto& e : mt.params) {
+                        std::vector<float> g(e.grad.size()), v(e.value.size());
+                        for (size_t i = 0; i < g.size(); ++i) g[i] = static_cast<float>(e.grad[i]);
+                        for (size_t i = 0; i < v.size(); ++i) v[i] = static_cast<float>(e.value[i]);
+                        const std::vector<int64_t> sh{static_cast<int64_t>(e.value.rows()), static_cast<int64_t>(e.value.cols())};
+                        w.put("train/grad/" + e.name, g, sh);
+                        w.put("train/param1/" + e.name, v, sh);
+                    }
+            }
+            for (const auto& e : mt.params) {
+                std::vector<float> v(e.value.size());
+                for (size_t i = 0; i < v.size(); ++i) v[i] = static_cast<float>(e.value[i]);
+                w.put("train/paramN/" + e.name, v,
+                      {static_cast<int64_t>(e.value.rows()), static_cast<int64_t>(e.value.cols())});
+            }
+            w.put("train/loss", losses);
+            w.put("train/cfg", std::vector<double>{o.lr, tc.adam.beta1, tc.adam.beta2, tc.adam.eps, tc.adam.clip_norm,
+                                                   static_cast<double>(o.train_steps)});
+        }
         std::cerr << "ref_dump: " << samples.size() << " users, " << rec_user.size() << " records -> "
                   << o.out << "\n";
     } catch (const std::exception& e) {

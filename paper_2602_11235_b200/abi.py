@@ -112,6 +112,15 @@ class PackedBuffers(C.Structure):
                                            "exp_feat_off", "exp_blk", "exp_feats", "exp_src")]
 
 
+class TrainConfig(C.Structure):
+    _fields_ = [("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
+                ("clip_norm", C.c_double), ("global_batch", C.c_int64)]
+
+
+class TrainResult(C.Structure):
+    _fields_ = [("loss", C.c_double), ("grad_norm", C.c_double), ("step", C.c_int64), ("records", C.c_int64)]
+
+
 class DatasetInfo(C.Structure):
     _fields_ = [("format_version", C.c_int32), ("n_users", C.c_int64), ("n_chunks", C.c_int64),
                 ("max_tasks", C.c_int32)]
@@ -150,6 +159,12 @@ SIGNATURES = [
     ("mtfm_cuda_aggregate_sizes", C.c_int, [C.c_void_p, C.POINTER(PackedSizes)]),
     ("mtfm_cuda_aggregate_fetch", C.c_int, [C.c_void_p, C.POINTER(PackedBuffers)]),
     ("mtfm_cuda_aggregate_free", C.c_int, [C.c_void_p]),
+    ("mtfm_cuda_train_step", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(TrainConfig),
+                                       C.POINTER(TrainResult)]),
+    ("mtfm_cuda_get_param", C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.c_int64, C.c_int64]),
+    ("mtfm_cuda_get_grad", C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.c_int64, C.c_int64]),
+    ("mtfm_nccl_unique_id", C.c_int, [C.c_void_p]),
+    ("mtfm_cuda_dp_init", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
     ("mtfm_dataset_load", C.c_int, [C.c_char_p, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
     ("mtfm_dataset_info", C.c_int, [C.c_void_p, C.POINTER(DatasetInfo)]),
     ("mtfm_dataset_schema_desc", C.c_int, [C.c_void_p, C.POINTER(SchemaDesc)]),

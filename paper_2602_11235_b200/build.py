@@ -11,7 +11,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libmtfm_cuda.so")
 BUILD = os.path.join(ROOT, "build", "mtfm_cuda")
-SOURCES = ["kernels.cu", "model.cu", "aggregate.cu", "ingest.cpp"]
+SOURCES = ["kernels.cu", "model.cu", "aggregate.cu", "ingest.cpp", "train_kernels.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -52,7 +52,7 @@ def build(verbose=False, extra_flags=()):
                 print(" ".join(cmd), flush=True)
             subprocess.run(cmd, check=True)
     if _stale(OUT, objs):
-        cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", OUT]
+        cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", OUT, "-ldl"]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)

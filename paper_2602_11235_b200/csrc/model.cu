@@ -29,6 +29,7 @@
 #include "gemm_tc.cuh"
 #include "kernels.cuh"
 #include "tok_tc.cuh"
+#include "train_kernels.cuh"
 
 namespace mtfm {
 
@@ -280,6 +281,34 @@ struct SourceW {
     DevBuf t1, t2;          // bf16 [2d][k_pad], [d][2d]
 };
 
+// Where a registered parameter lives among the fp32 device weights:
+// rows x cols at element `off` of `buf`, row stride `ld` (mtfm_cuda_get_param).
+struct ParamView {
+    DevBuf* buf = nullptr;
+    long long off = 0, ld = 0;
+};
+
+// Training state (train_step.inc): one flat gradient buffer (one NCCL all-reduce),
+// Adam moments in the same layout, saved activations of the last step.
+struct TrainState {
+    struct Seg {
+        DevBuf* w;        // fp32 device weights
+        long long n;      // elements
+        long long off;    // offset in the flat gradient / moment buffers
+    };
+    std::vector<Seg> segs;
+    long long n_total = 0;
+    DevBuf grad, adam_m, adam_v, scratch;
+    int64_t t = 0;        // Adam step count (params.hpp:87-119)
+    std::vector<std::unique_ptr<DevBuf>> act;  // activation / gradient buffers, grown on demand
+    size_t act_used = 0;
+    float* grad_of(const DevBuf& w) const {
+        for (const auto& s : segs)
+            if (s.w == &w) return const_cast<float*>(grad.as<float>()) + s.off;
+        return nullptr;
+    }
+};
+
 }  // namespace mtfm
 
 struct mtfm_cuda_model {
@@ -325,6 +354,12 @@ struct mtfm_cuda_model {
     std::vector<Prof> prof;
     size_t prof_n = 0;
     std::unique_ptr<mtfm_cuda_batch> ws;  // reusable workspace of mtfm_cuda_forward
+    std::vector<mtfm::ParamView> views;    // per registered parameter (finalize)
+    std::unique_ptr<mtfm::TrainState> train;  // reset when parameters are set again (weights re-uploaded)
+    bool device_ahead = false;             // training updated the device weights past the host copies
+    void* nccl = nullptr;                  // ncclComm_t of the data-parallel group (owned)
+    int dp_ranks = 1, dp_rank = 0;
+    ~mtfm_cuda_model();
 };
 
 struct mtfm_cuda_batch {
@@ -603,6 +638,63 @@ void finalize(mtfm_cuda_model& m) {
     upload(m.tower_b, tb, st);
     upload(m.d_src, m.sources, st);
     ck(cudaStreamSynchronize(st), "weight upload");
+    // parameter views into the fp32 device weights (registration order)
+    m.views.assign(m.params.size(), ParamView{});
+    auto view = [&](const std::string& n, DevBuf& b, long long off, long long ld) {
+        auto it = m.by_name.find(n);
+        if (it != m.by_name.end()) m.views[it->second] = ParamView{&b, off, ld};
+    };
+    for (size_t sl = 0; sl < m.slots.size(); ++sl) view(m.slot_param[sl], m.emb_f32, m.slots[sl].emb_off, m.cfg.d_emb);
+    for (size_t si = 0; si < m.sources.size(); ++si) {
+        const auto& src = m.sources[si];
+        std::string base = src.kind == 0 ? "tok/h" : (src.kind == 1 ? "tok/r" : "tok/s");
+        base += std::to_string(src.id);
+        auto& w = *m.srcw[si];
+        view(base + "/mlp_w1", w.w1, 0, 2 * d);
+        view(base + "/mlp_b1", w.b1, 0, 2 * d);
+        view(base + "/mlp_w2", w.w2, 0, d);
+        view(base + "/mlp_b2", w.b2, 0, d);
+    }
+    for (int b = 0, li = 0; b < m.cfg.blocks; ++b)
+        for (int l = 0; l < m.cfg.target_layers + m.cfg.full_layers; ++l, ++li) {
+            auto& L = *m.layers[static_cast<size_t>(li)];
+            const std::string base = "hta/b" + std::to_string(b) + "/l" + std::to_string(l);
+            if (L.target) {
+                view(base + "/fuq_w", L.w1, 0, 2 * hd);
+                view(base + "/fuq_b", L.b1, 0, 2 * hd);
+                view(base + "/fkv_w", L.wkv, 0, 2 * gd);
+                view(base + "/fkv_b", L.bkv, 0, 2 * gd);
+            } else {
+                view(base + "/f1_w", L.w1, 0, 2 * hd + 2 * gd);
+                view(base + "/f1_b", L.b1, 0, 2 * hd + 2 * gd);
+            }
+            view(base + "/f2_w", L.f2, 0, d);
+            view(base + "/f2_b", L.f2b, 0, d);
+            for (int g = 0; g < n_groups; ++g) {
+                const auto& src = m.sources[static_cast<size_t>(g)];
+                const std::string key = std::string(src.kind == 0 ? "h" : (src.kind == 1 ? "r" : "t")) + std::to_string(src.id);
+                view(base + "/gln1/" + key + "/gain", L.g1g, static_cast<long long>(g) * d, d);
+                view(base + "/gln1/" + key + "/bias", L.g1b, static_cast<long long>(g) * d, d);
+                view(base + "/gln2/" + key + "/gain", L.g2g, static_cast<long long>(g) * hd, hd);
+                view(base + "/gln2/" + key + "/bias", L.g2b, static_cast<long long>(g) * hd, hd);
+            }
+        }
+    for (int e = 0; e < E; ++e) {
+        view("head/expert" + std::to_string(e) + "_w", m.head_w, static_cast<long long>(e) * dx, m.head_n);
+        view("head/expert" + std::to_string(e) + "_b", m.head_eb, static_cast<long long>(e) * dx, dx);
+    }
+    for (size_t si = 0, tg = 0; si < m.sources.size(); ++si) {
+        const auto& src = m.sources[si];
+        if (src.kind != 2) continue;
+        for (const auto& t : m.tasks[si]) {
+            const std::string base = "head/s" + std::to_string(src.id) + "/" + t;
+            view(base + "/gate_w", m.head_w, static_cast<long long>(E) * dx + static_cast<long long>(tg) * E, m.head_n);
+            view(base + "/gate_b", m.head_gb, static_cast<long long>(tg) * E, E);
+            view(base + "/tower_w", m.tower_w, static_cast<long long>(tg) * dx, 1);
+            view(base + "/tower_b", m.tower_b, static_cast<long long>(tg), 1);
+            ++tg;
+        }
+    }
     m.finalized = true;
 }
 
@@ -1901,6 +1993,17 @@ namespace mtfm {
 void set_last_error(const std::string& what) { g_last_error = what; }
 }  // namespace mtfm
 
+#include "train_step.inc"
+
+mtfm_cuda_model::~mtfm_cuda_model() {
+    if (nccl) {
+        try {
+            mtfm::nccl().destroy(nccl);
+        } catch (...) {
+        }
+    }
+}
+
 using namespace mtfm;
 
 extern "C" {
@@ -2035,9 +2138,24 @@ mtfm_status mtfm_cuda_set_param(mtfm_cuda_model* m, const char* name, const floa
         if (p.rows != rows || p.cols != cols)
             fail(MTFM_DIMENSION_ERROR, std::string("shape mismatch for '") + name + "': expected " +
                                            std::to_string(p.rows) + "x" + std::to_string(p.cols));
+        if (m->device_ahead) {
+            // training moved the device weights past the host copies: bring them back first
+            ck(cudaStreamSynchronize(m->stream), "sync");
+            for (size_t i = 0; i < m->params.size(); ++i) {
+                auto& q = m->params[i];
+                const ParamView& pv = m->views[i];
+                if (!pv.buf) continue;
+                ck(cudaMemcpy2D(q.host.data(), static_cast<size_t>(q.cols) * 4, pv.buf->as<float>() + pv.off,
+                                static_cast<size_t>(pv.ld) * 4, static_cast<size_t>(q.cols) * 4,
+                                static_cast<size_t>(q.rows), cudaMemcpyDeviceToHost),
+                   "D2H param");
+            }
+            m->device_ahead = false;
+        }
         p.host.assign(v, v + rows * cols);
         p.set = true;
         m->finalized = false;
+        m->train.reset();  // gradient segments point at the device weights about to be rebuilt
         m->srcw.clear();
         m->layers.clear();
     });
@@ -2175,6 +2293,81 @@ mtfm_status mtfm_cuda_forward(mtfm_cuda_model* m, const mtfm_packed_batch* b, in
     if (s == MTFM_OK) s = mtfm_cuda_batch_run(m, m->ws.get());
     if (s == MTFM_OK) s = mtfm_cuda_batch_results(m, m->ws.get(), out);
     return s;
+}
+
+mtfm_status mtfm_cuda_train_step(mtfm_cuda_model* m, mtfm_cuda_batch* b, const int32_t* labels, int32_t max_tasks,
+                                 const mtfm_train_config* cfg, mtfm_train_result* out) {
+    return guard([&] {
+        if (!m || !b || !cfg || (!labels && b->n_exp > 0)) fail(MTFM_CONTRACT_ERROR, "null argument");
+        if (b->m != m) fail(MTFM_CONTRACT_ERROR, "batch belongs to another model");
+        if (!m->finalized) fail(MTFM_CONTRACT_ERROR, "parameters changed after prepare; prepare the batch again");
+        ck(cudaSetDevice(m->device), "cudaSetDevice");
+        train_step(*m, *b, labels, max_tasks, *cfg, out);
+    });
+}
+
+mtfm_status mtfm_cuda_get_param(mtfm_cuda_model* m, const char* name, float* host, int64_t rows, int64_t cols) {
+    return guard([&] {
+        if (!m || !name || !host) fail(MTFM_CONTRACT_ERROR, "null argument");
+        auto it = m->by_name.find(name);
+        if (it == m->by_name.end()) fail(MTFM_CONFIG_ERROR, std::string("unknown parameter: ") + name);
+        const auto& p = m->params[it->second];
+        if (p.rows != rows || p.cols != cols) fail(MTFM_DIMENSION_ERROR, std::string("shape mismatch for '") + name + "'");
+        if (!m->finalized || m->views.empty() || !m->views[it->second].buf) {
+            if (!p.set) fail(MTFM_CONFIG_ERROR, std::string("parameter not set: ") + name);
+            std::memcpy(host, p.host.data(), static_cast<size_t>(rows * cols) * 4);
+            return;
+        }
+        const ParamView& v = m->views[it->second];
+        ck(cudaSetDevice(m->device), "cudaSetDevice");
+        ck(cudaStreamSynchronize(m->stream), "sync");
+        ck(cudaMemcpy2D(host, static_cast<size_t>(cols) * 4, v.buf->as<float>() + v.off, static_cast<size_t>(v.ld) * 4,
+                        static_cast<size_t>(cols) * 4, static_cast<size_t>(rows), cudaMemcpyDeviceToHost),
+           "D2H param");
+    });
+}
+
+mtfm_status mtfm_cuda_get_grad(mtfm_cuda_model* m, const char* name, float* host, int64_t rows, int64_t cols) {
+    return guard([&] {
+        if (!m || !name || !host) fail(MTFM_CONTRACT_ERROR, "null argument");
+        if (!m->train) fail(MTFM_CONTRACT_ERROR, "no training step has run");
+        auto it = m->by_name.find(name);
+        if (it == m->by_name.end()) fail(MTFM_CONFIG_ERROR, std::string("unknown parameter: ") + name);
+        const auto& p = m->params[it->second];
+        if (p.rows != rows || p.cols != cols) fail(MTFM_DIMENSION_ERROR, std::string("shape mismatch for '") + name + "'");
+        const ParamView& v = m->views[it->second];
+        const float* g = m->train->grad_of(*v.buf);
+        if (!g) fail(MTFM_CONTRACT_ERROR, "parameter has no gradient segment");
+        ck(cudaSetDevice(m->device), "cudaSetDevice");
+        ck(cudaStreamSynchronize(m->stream), "sync");
+        ck(cudaMemcpy2D(host, static_cast<size_t>(cols) * 4, g + v.off, static_cast<size_t>(v.ld) * 4,
+                        static_cast<size_t>(cols) * 4, static_cast<size_t>(rows), cudaMemcpyDeviceToHost),
+           "D2H grad");
+    });
+}
+
+mtfm_status mtfm_nccl_unique_id(void* out128) {
+    return guard([&] {
+        if (!out128) fail(MTFM_CONTRACT_ERROR, "null argument");
+        nccl_check(nccl().get_id(out128), "ncclGetUniqueId");
+    });
+}
+
+mtfm_status mtfm_cuda_dp_init(mtfm_cuda_model* m, int32_t nranks, int32_t rank, const void* unique_id128) {
+    return guard([&] {
+        if (!m || !unique_id128) fail(MTFM_CONTRACT_ERROR, "null argument");
+        if (nranks < 1 || rank < 0 || rank >= nranks) fail(MTFM_CONFIG_ERROR, "bad rank / world size");
+        ck(cudaSetDevice(m->device), "cudaSetDevice");
+        finalize(*m);
+        if (m->nccl) fail(MTFM_CONTRACT_ERROR, "data-parallel group already initialised");
+        NcclId id;
+        std::memcpy(id.b, unique_id128, 128);
+        using InitFn = int (*)(void**, int, NcclId, int);
+        auto init = reinterpret_cast<InitFn>(nccl().init_rank);
+        nccl_check(init(&m->nccl, nranks, id, rank), "ncclCommInitRank");
+        m->dp_ranks = nranks;
+        m->dp_rank = rank;
+    });
 }
 
 mtfm_status mtfm_cuda_set_profiling(mtfm_cuda_model* m, int32_t on) {

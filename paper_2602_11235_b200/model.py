@@ -218,6 +218,40 @@ class Model:
     def forward_with(self, sample, only_scenario=-1):
         return self.forward_samples([sample], only_scenario)
 
+    # ---- training (Trainer::train_step, train.hpp:111-147; fp32 handles)
+    def train_step(self, batch, labels, lr=3e-4, beta1=0.9, beta2=0.999, eps=1e-8, clip_norm=1.0, global_batch=0,
+                   prepared: "PreparedBatch" = None):
+        """One optimizer step over every user of `batch`; labels [n_exposures][max_tasks]
+        (scenario task order, -1 absent). Returns TrainResult (loss, grad_norm, step)."""
+        lab = np.ascontiguousarray(np.asarray(labels, dtype=np.int32))
+        if lab.ndim == 1:
+            lab = lab.reshape(-1, 1)
+        pb = prepared if prepared is not None else self.prepare(batch)
+        cfg = abi.TrainConfig(lr, beta1, beta2, eps, clip_norm, int(global_batch))
+        res = abi.TrainResult()
+        abi.check(abi.lib().mtfm_cuda_train_step(self._h, pb._h, abi.ptr(lab), lab.shape[1], C.byref(cfg), C.byref(res)))
+        return res
+
+    def get_param(self, name, rows, cols):
+        out = np.empty((rows, cols), np.float32)
+        abi.check(abi.lib().mtfm_cuda_get_param(self._h, name.encode(), abi.ptr(out), rows, cols))
+        return out
+
+    def get_grad(self, name, rows, cols):
+        out = np.empty((rows, cols), np.float32)
+        abi.check(abi.lib().mtfm_cuda_get_grad(self._h, name.encode(), abi.ptr(out), rows, cols))
+        return out
+
+    def dp_init(self, nranks, rank, unique_id: bytes):
+        buf = (C.c_char * 128).from_buffer_copy(unique_id)
+        abi.check(abi.lib().mtfm_cuda_dp_init(self._h, int(nranks), int(rank), C.cast(buf, C.c_void_p)))
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = (C.c_char * 128)()
+        abi.check(abi.lib().mtfm_nccl_unique_id(C.cast(buf, C.c_void_p)))
+        return bytes(buf)
+
     def last_stats(self):
         st = abi.RunStats()
         abi.check(abi.lib().mtfm_cuda_last_stats(self._h, C.byref(st)))

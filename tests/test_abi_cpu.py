@@ -12,7 +12,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _declared():
     src = open(os.path.join(ROOT, "include", "mtfm_cuda.h")).read()
-    return sorted(set(re.findall(r"MTFM_API[^;(]*?\b(mtfm_(?:cuda|dataset)_\w+)\s*\(", src)))
+    return sorted(set(re.findall(r"MTFM_API[^;(]*?\b(mtfm_(?:cuda|dataset|nccl)_\w+)\s*\(", src)))
 
 
 def test_header_declares_the_abi():

@@ -108,3 +108,39 @@ def test_lpt_cost_follows_model_config():
     small = user_costs(b)
     base = user_costs(b, wl.cfg)
     assert np.all(base > 3.5 * small)
+
+
+def _dp_split_worker(rank, world, port, q):
+    import torch.distributed as dist
+    from paper_2602_11235_b200.dp import share_unique_id, split_batch
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    b = batch("train_b")
+    from golden_util import load
+    lab = load("train_b")["batch/exp_labels"]
+    mine, ml = split_batch(b, lab, world, rank)
+    uid = share_unique_id(bytes(range(128)) if rank == 0 else None)
+    q.put((rank, [int(u) for u in mine["user_id"]], ml.tolist(), uid == bytes(range(128))))
+    dist.destroy_process_group()
+
+
+def test_dp_batch_split_and_id_broadcast_gloo():
+    """Data-parallel training's host side (paper_2602_11235_b200/dp.py) at world size 2:
+    the users and their label rows are partitioned exactly, and every rank receives
+    rank 0's NCCL unique id."""
+    import multiprocessing as mp
+    from golden_util import load
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29000 + os.getpid() % 1000
+    ps = [ctx.Process(target=_dp_split_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    got = sorted(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    b = batch("train_b")
+    lab = load("train_b")["batch/exp_labels"]
+    assert got[0][1] + got[1][1] == [int(u) for u in b["user_id"]]
+    assert got[0][2] + got[1][2] == lab.tolist()
+    assert got[0][3] and got[1][3]
