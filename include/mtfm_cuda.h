@@ -285,6 +285,18 @@ MTFM_API mtfm_status mtfm_cuda_aggregate_sizes(const mtfm_cuda_aggregate* a, mtf
 MTFM_API mtfm_status mtfm_cuda_aggregate_fetch(mtfm_cuda_aggregate* a, const mtfm_packed_buffers* out);
 MTFM_API mtfm_status mtfm_cuda_aggregate_free(mtfm_cuda_aggregate* a);
 
+/* ---------------------------------------------------------------- 2:4 pruning
+ * prune_model_projections (prune.hpp:92-103) on the device: every
+ * hta/.../{f1_w, fuq_w, fkv_w, f2_w} keeps, per output column and full group
+ * of 4 consecutive input rows, its two largest magnitudes (ties keep the
+ * earlier row, prune.hpp:33-70); a partial trailing group is exempt. The
+ * pruned weights become the model's parameters (get_param returns them; the
+ * bf16 copies are rebuilt). Report as PruneReport (prune.hpp:19-31). */
+typedef struct {
+    int64_t groups_covered, zeros_written, exempt_tail_rows, pruned_params;
+} mtfm_prune_report;
+MTFM_API mtfm_status mtfm_cuda_prune_projections(mtfm_cuda_model* m, mtfm_prune_report* report);
+
 /* ---------------------------------------------------------------- training
  * Trainer::train_step (train.hpp:111-147) on the GPU over every user of a
  * prepared batch: build_loss (model.hpp:323-358: per sample the mean BCE over

@@ -654,6 +654,40 @@ class Oracle:
 
 
 # ----------------------------------------------------------------------------
+# 2:4 pruning (prune.hpp)
+# ----------------------------------------------------------------------------
+def prune_2_4(w):
+    """prune_2_4_inplace (prune.hpp:33-70) on a copy: per column, each full group of
+    4 consecutive rows keeps its two largest |w| (ties keep the earlier row); a
+    partial trailing group is exempt. Returns (pruned, zeros_written, groups, tail)."""
+    w = np.array(w, dtype=np.float32, copy=True)
+    rows, cols = w.shape
+    full = rows // 4
+    zeros = 0
+    for j in range(cols):
+        for g in range(full):
+            mag = [abs(float(w[4 * g + i, j])) for i in range(4)]
+            k0, k1 = 0, 1
+            if mag[k1] > mag[k0]:
+                k0, k1 = k1, k0
+            for i in (2, 3):
+                if mag[i] > mag[k0]:
+                    k1, k0 = k0, i
+                elif mag[i] > mag[k1]:
+                    k1 = i
+            for i in range(4):
+                if i not in (k0, k1):
+                    w[4 * g + i, j] = 0.0
+                    zeros += 1
+    return w, zeros, full * cols, rows - full * 4
+
+
+def is_projection_param(name):
+    """prune.hpp:83-90."""
+    return name.startswith("hta/") and name.endswith(("/f1_w", "/fuq_w", "/fkv_w", "/f2_w"))
+
+
+# ----------------------------------------------------------------------------
 # User-level aggregation (datagen.cpp:171-216)
 # ----------------------------------------------------------------------------
 def aggregate_users(scenario_ids, stream, store):

@@ -27,6 +27,7 @@
 #include "mtfa.hpp"
 #include "mtfm/datagen.hpp"
 #include "mtfm/model.hpp"
+#include "mtfm/prune.hpp"
 #include "mtfm/train.hpp"
 #include "mtfm/verify.hpp"
 
@@ -46,6 +47,7 @@ struct Opts {
     uint64_t jitter = 0;       // != 0: perturb biases / GLN affines / towers (jitter_params)
     double tower_scale = 1.0;
     int train_steps = 0;       // > 0: Trainer::train_step over every user of the batch, dumped
+    bool prune = false;        // prune_model_projections (prune.hpp:92-103) before the forwards
     double lr = 1e-3;
 };
 
@@ -104,6 +106,7 @@ Opts parse(int argc, char** argv) {
         else if (a == "--jitter") o.jitter = std::stoull(nxt());
         else if (a == "--tower-scale") o.tower_scale = std::stod(nxt());
         else if (a == "--train") o.train_steps = std::stoi(nxt());
+        else if (a == "--prune") o.prune = true;
         else if (a == "--lr") o.lr = std::stod(nxt());
         else throw config_error("unknown flag " + a);
     }
@@ -240,6 +243,8 @@ int main(int argc, char** argv) {
 
         Model<float> m32 = Model<float>::build(ss, o.mc, o.model_seed);
         if (o.jitter) jitter_params(m32.params, o.jitter, o.tower_scale);
+        PruneReport prep;
+        if (o.prune) prep = prune_model_projections(m32.params);
         Model<double> m64 = Model<double>::build(ss, o.mc, o.model_seed);
         // The f64 model carries exactly the f32 weights, so it is the exact
         // answer for the weights the GPU path receives.
@@ -257,6 +262,18 @@ int main(int argc, char** argv) {
         w.put("config/eps", std::vector<double>{h.eps});
         w.put("config/model_seed", std::vector<int64_t>{static_cast<int64_t>(o.model_seed)});
         w.put("config/jitter", std::vector<double>{static_cast<double>(o.jitter), o.tower_scale});
+        if (o.prune) {
+            w.put("prune/report", std::vector<int64_t>{static_cast<int64_t>(prep.groups_covered),
+                                                      static_cast<int64_t>(prep.zeros_written),
+                                                      static_cast<int64_t>(prep.exempt_tail_rows),
+                                                      static_cast<int64_t>(prep.pruned_params.size())});
+            for (const auto& n : prep.pruned_params) {
+                const auto& t = m32.params.at(n).value;
+                std::vector<float> v(t.size());
+                for (size_t i = 0; i < v.size(); ++i) v[i] = t[i];
+                w.put("prune/param/" + n, v, {static_cast<int64_t>(t.rows()), static_cast<int64_t>(t.cols())});
+            }
+        }
 
         int max_tasks = 0;
         for (const auto& s : ss.scenarios) max_tasks = std::max(max_tasks, static_cast<int>(s.tasks.size()));

@@ -121,6 +121,11 @@ class TrainResult(C.Structure):
     _fields_ = [("loss", C.c_double), ("grad_norm", C.c_double), ("step", C.c_int64), ("records", C.c_int64)]
 
 
+class PruneReport(C.Structure):
+    _fields_ = [("groups_covered", C.c_int64), ("zeros_written", C.c_int64), ("exempt_tail_rows", C.c_int64),
+                ("pruned_params", C.c_int64)]
+
+
 class DatasetInfo(C.Structure):
     _fields_ = [("format_version", C.c_int32), ("n_users", C.c_int64), ("n_chunks", C.c_int64),
                 ("max_tasks", C.c_int32)]
@@ -159,6 +164,7 @@ SIGNATURES = [
     ("mtfm_cuda_aggregate_sizes", C.c_int, [C.c_void_p, C.POINTER(PackedSizes)]),
     ("mtfm_cuda_aggregate_fetch", C.c_int, [C.c_void_p, C.POINTER(PackedBuffers)]),
     ("mtfm_cuda_aggregate_free", C.c_int, [C.c_void_p]),
+    ("mtfm_cuda_prune_projections", C.c_int, [C.c_void_p, C.POINTER(PruneReport)]),
     ("mtfm_cuda_train_step", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(TrainConfig),
                                        C.POINTER(TrainResult)]),
     ("mtfm_cuda_get_param", C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.c_int64, C.c_int64]),

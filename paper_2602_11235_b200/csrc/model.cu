@@ -1995,6 +1995,61 @@ void set_last_error(const std::string& what) { g_last_error = what; }
 
 #include "train_step.inc"
 
+namespace mtfm {
+namespace {
+
+// device fp32 weights -> the host parameter copies (after training / pruning on the device)
+void sync_host_params(mtfm_cuda_model& m) {
+    ck(cudaStreamSynchronize(m.stream), "sync");
+    for (size_t i = 0; i < m.params.size(); ++i) {
+        auto& q = m.params[i];
+        const ParamView& pv = m.views[i];
+        if (!pv.buf) continue;
+        q.host.resize(static_cast<size_t>(q.rows * q.cols));
+        ck(cudaMemcpy2D(q.host.data(), static_cast<size_t>(q.cols) * 4, pv.buf->as<float>() + pv.off,
+                        static_cast<size_t>(pv.ld) * 4, static_cast<size_t>(q.cols) * 4, static_cast<size_t>(q.rows),
+                        cudaMemcpyDeviceToHost),
+           "D2H param");
+    }
+    m.device_ahead = false;
+}
+
+// prune_2_4_inplace (prune.hpp:33-70): per column, every full group of 4 consecutive input
+// rows keeps its two largest magnitudes (ties keep the earlier row); one thread per (group, column)
+__global__ void prune_2_4_kernel(float* w, int rows, int cols, unsigned long long* zeros) {
+    const long long n = static_cast<long long>(rows / 4) * cols;
+    unsigned long long z = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const long long g = i / cols;
+        const int j = static_cast<int>(i - g * cols);
+        float* c = w + g * 4 * cols + j;
+        auto mag = [&](int r) { return fabs(static_cast<double>(c[static_cast<long long>(r) * cols])); };
+        int keep0 = 0, keep1 = 1;
+        if (mag(keep1) > mag(keep0)) {
+            keep0 = 1;
+            keep1 = 0;
+        }
+        for (int r = 2; r < 4; ++r) {
+            if (mag(r) > mag(keep0)) {
+                keep1 = keep0;
+                keep0 = r;
+            } else if (mag(r) > mag(keep1)) {
+                keep1 = r;
+            }
+        }
+        for (int r = 0; r < 4; ++r)
+            if (r != keep0 && r != keep1) {
+                c[static_cast<long long>(r) * cols] = 0.f;
+                ++z;
+            }
+    }
+    z = static_cast<unsigned long long>(warp_sum(static_cast<double>(z)));
+    if ((threadIdx.x & 31) == 0 && z) atomicAdd(zeros, z);
+}
+
+}  // namespace
+}  // namespace mtfm
+
 mtfm_cuda_model::~mtfm_cuda_model() {
     if (nccl) {
         try {
@@ -2138,20 +2193,7 @@ mtfm_status mtfm_cuda_set_param(mtfm_cuda_model* m, const char* name, const floa
         if (p.rows != rows || p.cols != cols)
             fail(MTFM_DIMENSION_ERROR, std::string("shape mismatch for '") + name + "': expected " +
                                            std::to_string(p.rows) + "x" + std::to_string(p.cols));
-        if (m->device_ahead) {
-            // training moved the device weights past the host copies: bring them back first
-            ck(cudaStreamSynchronize(m->stream), "sync");
-            for (size_t i = 0; i < m->params.size(); ++i) {
-                auto& q = m->params[i];
-                const ParamView& pv = m->views[i];
-                if (!pv.buf) continue;
-                ck(cudaMemcpy2D(q.host.data(), static_cast<size_t>(q.cols) * 4, pv.buf->as<float>() + pv.off,
-                                static_cast<size_t>(pv.ld) * 4, static_cast<size_t>(q.cols) * 4,
-                                static_cast<size_t>(q.rows), cudaMemcpyDeviceToHost),
-                   "D2H param");
-            }
-            m->device_ahead = false;
-        }
+        if (m->device_ahead) sync_host_params(*m);  // training moved the device weights past the host copies
         p.host.assign(v, v + rows * cols);
         p.set = true;
         m->finalized = false;
@@ -2367,6 +2409,51 @@ mtfm_status mtfm_cuda_dp_init(mtfm_cuda_model* m, int32_t nranks, int32_t rank, 
         nccl_check(init(&m->nccl, nranks, id, rank), "ncclCommInitRank");
         m->dp_ranks = nranks;
         m->dp_rank = rank;
+    });
+}
+
+mtfm_status mtfm_cuda_prune_projections(mtfm_cuda_model* m, mtfm_prune_report* rep) {
+    return guard([&] {
+        if (!m) fail(MTFM_CONTRACT_ERROR, "null argument");
+        ck(cudaSetDevice(m->device), "cudaSetDevice");
+        finalize(*m);
+        if (m->device_ahead) sync_host_params(*m);
+        DevBuf zc;
+        zc.alloc(8);
+        ck(cudaMemsetAsync(zc.p, 0, 8, m->stream), "memset");
+        mtfm_prune_report r{};
+        // is_projection_param (prune.hpp:83-90): hta/.../{f1_w, fuq_w, fkv_w, f2_w}, in registration order
+        for (auto& Lp : m->layers) {
+            auto& L = *Lp;
+            std::vector<std::pair<DevBuf*, std::pair<int, int>>> mats;
+            const int n1 = L.target ? 2 * m->hd : 2 * m->hd + 2 * m->gd;
+            mats.push_back({&L.w1, {m->d, n1}});
+            if (L.target) mats.push_back({&L.wkv, {m->d, 2 * m->gd}});
+            mats.push_back({&L.f2, {m->hd, m->d}});
+            for (auto& [buf, rc] : mats) {
+                const int rows = rc.first, cols = rc.second;
+                const long long n = static_cast<long long>(rows / 4) * cols;
+                if (n > 0)
+                    prune_2_4_kernel<<<static_cast<int>(std::min<long long>(cdiv(n, 256), 148 * 8)), 256, 0, m->stream>>>(
+                        buf->as<float>(), rows, cols, zc.as<unsigned long long>());
+                r.groups_covered += n;
+                r.exempt_tail_rows += rows - (rows / 4) * 4;
+                ++r.pruned_params;
+            }
+        }
+        ck(cudaGetLastError(), "prune");
+        unsigned long long z = 0;
+        ck(cudaMemcpyAsync(&z, zc.p, 8, cudaMemcpyDeviceToHost, m->stream), "D2H");
+        ck(cudaStreamSynchronize(m->stream), "prune");
+        r.zeros_written = static_cast<int64_t>(z);
+        // the pruned fp32 weights become the parameters; bf16 / folded copies rebuild on next use
+        m->device_ahead = true;
+        sync_host_params(*m);
+        m->finalized = false;
+        m->srcw.clear();
+        m->layers.clear();
+        m->train.reset();
+        if (rep) *rep = r;
     });
 }
 

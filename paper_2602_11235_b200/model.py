@@ -232,6 +232,13 @@ class Model:
         abi.check(abi.lib().mtfm_cuda_train_step(self._h, pb._h, abi.ptr(lab), lab.shape[1], C.byref(cfg), C.byref(res)))
         return res
 
+    def prune_projections(self):
+        """prune_model_projections (prune.hpp:92-103): 2:4 pattern on every f1/fuq/fkv/f2."""
+        rep = abi.PruneReport()
+        abi.check(abi.lib().mtfm_cuda_prune_projections(self._h, C.byref(rep)))
+        return dict(groups_covered=rep.groups_covered, zeros_written=rep.zeros_written,
+                    exempt_tail_rows=rep.exempt_tail_rows, pruned_params=rep.pruned_params)
+
     def get_param(self, name, rows, cols):
         out = np.empty((rows, cols), np.float32)
         abi.check(abi.lib().mtfm_cuda_get_param(self._h, name.encode(), abi.ptr(out), rows, cols))
