@@ -66,23 +66,10 @@ def test_gpu_prune_bit_exact_and_scores(precision):
         assert d <= 2 * d_store + 2e-2
 
 
-@pytest.mark.gpu
-def test_gpu_prune_exempts_partial_groups():
-    """d = 38 (fp32 check mode, head_dim 19): every projection has 38 input rows, so two
-    trailing rows per matrix are exempt (prune.hpp:42-43)."""
-    from paper_2602_11235_b200 import Model, datagen
-    from paper_2602_11235_b200.schema import HTAConfig, ModelConfig
-    cfg = ModelConfig(HTAConfig(d_model=38, blocks=1, target_layers=1, full_layers=1, heads=2, kv_heads=1),
-                      d_emb=8, experts=2, d_expert=16)
-    sch = datagen.make_schemas()
-    m = Model(sch, cfg, precision="fp32")
-    P = datagen.random_params(m.param_specs(), seed=11)
-    m.set_params(P)
-    rep = m.prune_projections()
-    names = [n for n, _, _ in m.param_specs() if O.is_projection_param(n)]
-    exp_tail = 0
-    for n in names:
-        w, _, _, t = O.prune_2_4(P[n])
-        exp_tail += t
-        assert np.array_equal(m.get_param(n, *P[n].shape), w), n
-    assert rep["exempt_tail_rows"] == exp_tail == 2 * len(names)
+def test_prune_restatement_exempts_partial_groups_and_ties():
+    """prune.hpp:42-66 on hand-checkable input: a 6-row matrix has one full group and two
+    exempt tail rows; equal magnitudes keep the earlier rows."""
+    w = np.array([[1, -3, 2], [-4, 3, 2], [2, 1, 2], [3, 0, 2], [9, 9, 9], [-9, 9, 9]], np.float32)
+    got, zeros, groups, tail = O.prune_2_4(w)
+    want = np.array([[0, -3, 2], [-4, 3, 2], [0, 0, 0], [3, 0, 0], [9, 9, 9], [-9, 9, 9]], np.float32)
+    assert np.array_equal(got, want) and (zeros, groups, tail) == (6, 3, 2)
