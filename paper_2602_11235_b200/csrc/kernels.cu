@@ -24,7 +24,7 @@ __device__ __forceinline__ unsigned long long err_key(long long u, long long pie
            (static_cast<unsigned long long>(stage) << 20) | (static_cast<unsigned long long>(row) << 3) |
            static_cast<unsigned long long>(code);
 }
-enum { ERR_INTEGRITY = 2, ERR_DIMENSION = 3, ERR_LOOKUP = 5, ERR_CONTRACT = 6 };
+enum { ERR_META = 1, ERR_INTEGRITY = 2, ERR_DIMENSION = 3, ERR_LOOKUP = 5, ERR_CONTRACT = 6 };
 
 __device__ __forceinline__ int find_source(const SourceInfo* src, int n_src, int kind, int id, int only_scenario) {
     for (int s = 0; s < n_src; ++s)
@@ -166,6 +166,11 @@ __global__ void __launch_bounds__(256, 8) plan_kernel(PlanArgs a) {
         }
     }
     __syncthreads();
+    // check_meta_order (token_types.hpp:53-72, run by plan_tokens before any tokenizer
+    // check): the first H / R token of each block is compared with -1, so a context
+    // timestamp below -1 is a dimension_error that precedes every other error of the user
+    for (int i = tid; i < n_ev; i += blockDim.x)
+        if (b.ev_ts[ev0 + i] < -1) atomicMin(&s_err, err_key(u, 0, 0, 0, ERR_META));
     if (n_ev > 1) bitonic_sort(s_ts, s_sec, npad, CtxLess{});
     for (int i = tid; i < n_ev; i += blockDim.x)
         if ((s_sec[i] >> 32) == 0 && (i + 1 == n_ev || (s_sec[i + 1] >> 32) != 0)) s_lh = i + 1;

@@ -1935,6 +1935,7 @@ void results(mtfm_cuda_model& m, mtfm_cuda_batch& B, mtfm_records* out) {
         const long long user = static_cast<long long>(err >> 42);
         std::string what;
         switch (code) {
+            case 1: what = "token metas not time-sorted within block"; break;
             case 2: what = "no tokenizer for a sequence schema or scenario of the sample"; break;
             case 3: what = "embed_rows: feature slot missing"; break;
             case 5: what = "gather_rows: feature id out of range"; break;
@@ -1942,7 +1943,7 @@ void results(mtfm_cuda_model& m, mtfm_cuda_batch& B, mtfm_records* out) {
             default: what = "planning capacity exceeded";
         }
         const mtfm_status s = code == 2 ? MTFM_INTEGRITY_ERROR
-                              : code == 3 ? MTFM_DIMENSION_ERROR
+                              : (code == 3 || code == 1) ? MTFM_DIMENSION_ERROR
                               : code == 5 ? MTFM_LOOKUP_ERROR
                                           : MTFM_CONTRACT_ERROR;
         fail(s, what + " (user index " + std::to_string(user) + ")");

@@ -130,3 +130,25 @@ def test_planning_capacity_is_contract_error():
     m, _ = _model(wl)
     with pytest.raises(abi.ContractError):
         m.forward_batch(b)
+
+
+def test_context_timestamp_below_minus_one_is_dimension_error():
+    """check_meta_order (token_types.hpp:53-72): within the H and R blocks time must not
+    fall below the block's starting value -1, so an event at t = -5 makes plan_tokens
+    throw dimension_error before any tokenizer check; t = -1 is accepted."""
+    from golden_util import batch, model
+    from helpers import from_oracle
+    from paper_2602_11235_b200 import Model, abi
+    osch, ocfg, P = model("tiny")
+    sch, cfg = from_oracle(osch, ocfg)
+    m = Model.build(sch, cfg, P, precision="fp32")
+    b = {k: v.copy() for k, v in batch("tiny").items()}
+    u = 2
+    e0 = b["ev_off"][b["seq_off"][u]]
+    b["ev_ts"][e0] = -1
+    m.forward_batch(b)  # -1 is fine
+    b["ev_ts"][e0] = -5
+    b["exp_feats"][b["exp_feat_off"][b["exp_off"][u]]] = 10 ** 6  # a later lookup error of the same user
+    with pytest.raises(abi.DimensionError) as ei:
+        m.forward_batch(b)
+    assert "user index 2" in str(ei.value) and "time-sorted" in str(ei.value)
