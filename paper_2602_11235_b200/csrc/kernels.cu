@@ -113,8 +113,15 @@ __device__ __forceinline__ float row_scale_of(int norm, int c, int n_tokens) {
 __global__ void __launch_bounds__(256, 8) plan_kernel(PlanArgs a) {
     MTFM_PDL_ENTRY();
     extern __shared__ long long sm_sort[];
+    // sort area: SMEM, or a per-user global scratch slice for users above the SMEM
+    // capacity (same algorithm; __syncthreads orders the CTA's global accesses too)
+    long long cap = a.max_sort;
     long long* s_ts = sm_sort;
-    long long* s_sec = sm_sort + a.max_sort;
+    if (a.sort_off && a.sort_off[blockIdx.x + 1] > a.sort_off[blockIdx.x]) {
+        s_ts = a.sort_scratch + a.sort_off[blockIdx.x];
+        cap = (a.sort_off[blockIdx.x + 1] - a.sort_off[blockIdx.x]) / 2;
+    }
+    long long* s_sec = s_ts + cap;
     __shared__ unsigned long long s_err;
     __shared__ int s_lh;
     // per-CTA copies: the source table (find_source from SMEM) and, for the T
@@ -148,7 +155,7 @@ __global__ void __launch_bounds__(256, 8) plan_kernel(PlanArgs a) {
     while (npad < n_ev) npad <<= 1;
     int tpad = 1;
     while (tpad < n_t) tpad <<= 1;
-    if (npad > a.max_sort || tpad + n_ev > a.max_sort) {
+    if (npad > cap || tpad + n_ev > cap) {
         if (tid == 0) atomicMin(a.err, err_key(u, 0, 0, 0, ERR_CONTRACT) | 7ull);  // capacity
         return;
     }

@@ -76,6 +76,10 @@ struct PlanArgs {
     RowMeta rm;
     unsigned long long* err;     // min error key (see plan.cu)
     int max_sort;                // smem capacity (elements, power of two)
+    // users whose sort does not fit max_sort: [sort_off[u], sort_off[u+1]) of sort_scratch
+    // (2 x capacity elements) is their sort area in global memory; null when none
+    const long long* sort_off;   // [n_users + 1] or null
+    long long* sort_scratch;
 };
 
 void launch_plan(const PlanArgs& a, int smem_elems, cudaStream_t st);

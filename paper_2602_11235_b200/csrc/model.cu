@@ -373,6 +373,9 @@ struct mtfm_cuda_batch {
     std::vector<long long> src_cnt, src_base, emb_base, hid_base;
     mtfm::DevBuf d_us_off, d_src_base, d_src_cnt, d_emb_base, d_rec_off;
     int sort_cap = 0;
+    // plan sort areas of users above the SMEM capacity (global scratch); empty when none
+    std::vector<long long> sort_off;
+    mtfm::DevBuf d_sort_off, d_sort_scratch;
     // row meta
     mtfm::DevBuf r_src, r_item, r_prefix, r_scale, r_self, r_keybase, r_src_rows, t_user, t_exp_ref, t_scen, t_rec0,
         t_rec_stride, err;
@@ -1145,7 +1148,11 @@ void prepare(mtfm_cuda_model& m, const mtfm_packed_batch* hb, int only_scenario,
     // host layout: per (user, source) counts -> source regions, record offsets
     std::vector<long long> us(static_cast<size_t>(B.n_users) * n_src, 0);
     std::vector<long long> rec_off(B.n_users + 1, 0);
+    // plan sort area per user: max(pow2(n_ev), pow2(n_t) + n_ev) elements of (key, payload);
+    // SMEM up to kPlanSmemCap, larger users sort in a global scratch slice
+    constexpr long long kPlanSmemCap = 12288;
     long long max_sort = 1;
+    std::vector<long long> sort_need(hb->n_users, 1);
     if (m.src_lookup.empty()) build_source_lookup(m);
     for (int u = 0; u < hb->n_users; ++u) {
         long long n_ev = 0;
@@ -1165,12 +1172,20 @@ void prepare(mtfm_cuda_model& m, const mtfm_packed_batch* hb, int only_scenario,
         }
         rec_off[u + 1] = rec_off[u] + recs;
         const long long n_t = hb->exp_off[u + 1] - hb->exp_off[u];
-        max_sort = std::max({max_sort, next_pow2(n_ev), next_pow2(n_t) + n_ev});
+        sort_need[u] = std::max(next_pow2(n_ev), next_pow2(n_t) + n_ev);
+        if (sort_need[u] <= kPlanSmemCap) max_sort = std::max(max_sort, sort_need[u]);
     }
     B.n_records = rec_off[B.n_users];
-    if (max_sort > 12288)
-        fail(MTFM_CONTRACT_ERROR, "a user has more than 12288 tokens to plan (per-CTA sort capacity)");
     B.sort_cap = static_cast<int>(max_sort);
+    B.sort_off.clear();
+    for (int u = 0; u < hb->n_users; ++u)
+        if (sort_need[u] > kPlanSmemCap) {
+            B.sort_off.assign(hb->n_users + 1, 0);
+            for (int v = 0; v < hb->n_users; ++v)
+                B.sort_off[v + 1] = B.sort_off[v] + (sort_need[v] > kPlanSmemCap ? 2 * sort_need[v] : 0);
+            B.d_sort_scratch.alloc(static_cast<size_t>(B.sort_off.back()) * sizeof(long long));
+            break;
+        }
     B.src_cnt.assign(n_src, 0);
     B.src_base.assign(n_src, 0);
     B.emb_base.assign(n_src, 0);
@@ -1195,14 +1210,15 @@ void prepare(mtfm_cuda_model& m, const mtfm_packed_batch* hb, int only_scenario,
     const AttnGeom ag0 = attn_geom(m);
     const size_t hg0 = static_cast<size_t>(m.G) * ((m.H / m.G + ag0.hs - 1) / ag0.hs);
     const size_t tiles_est = hg0 * (static_cast<size_t>(B.n_events + 2 * B.n_exp) / ag0.rt + 3 * B.n_users) + 64;
-    B.pin.reserve((us_off.size() + 4 * static_cast<size_t>(n_src) + rec_off.size()) * 8 + tiles_est * sizeof(AttnTile) +
-                  4096);
+    B.pin.reserve((us_off.size() + 4 * static_cast<size_t>(n_src) + rec_off.size() + B.sort_off.size()) * 8 +
+                  tiles_est * sizeof(AttnTile) + 4096);
     B.pin.used = 64;  // first 64 bytes: stats read-back
     B.pin.upload(B.d_us_off, us_off, st);
     B.pin.upload(B.d_src_base, B.src_base, st);
     B.pin.upload(B.d_src_cnt, B.src_cnt, st);
     B.pin.upload(B.d_emb_base, B.emb_base, st);
     B.pin.upload(B.d_rec_off, rec_off, st);
+    if (!B.sort_off.empty()) B.pin.upload(B.d_sort_off, B.sort_off, st);
 
     // attention tiles
     const AttnGeom ag = attn_geom(m);
@@ -1386,6 +1402,8 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
     pa.rm = rm;
     pa.err = B.err.as<unsigned long long>();
     pa.max_sort = B.sort_cap;
+    pa.sort_off = B.sort_off.empty() ? nullptr : B.d_sort_off.as<long long>();
+    pa.sort_scratch = B.sort_off.empty() ? nullptr : B.d_sort_scratch.as<long long>();
     {
         StageScope sc(m, "plan", 0, Rd * 8 * 4 + Rd * 7 * 4);
         launch_plan(pa, B.sort_cap, st);
