@@ -22,7 +22,7 @@
 // per-chunk barrier waits of one MMA thread would serialise both GEMMs.
 // TMEM columns: Y [0, 256), Hacc [256, 384), Hb [384, 448).
 // SMEM: 2 x tile stages (E tile 16 KB + b1 tile 16 KB + b2 tile 8 KB),
-// 3 x W1 chunk stages (8 KB), 3 x W2 chunk stages (32 KB), ones tile, Y staging.
+// 3 x W1 chunk stages (8 KB), 3 x W2 chunk stages (32 KB), ones tile, Y / x̂ staging.
 #pragma once
 
 #include "common.cuh"
@@ -64,8 +64,8 @@ constexpr int W1_BYTES = HC * 64 * 2;               // 8 KB
 constexpr int W2_BYTES = D * 64 * 2;                // 32 KB
 constexpr int kXStages = 2, kWStages = 3;
 constexpr int ONES_BYTES = 4096;
-// staging: [0, 8 KB) x̂ rows (2 KB per Y warp), [8 KB, 12 KB) Y drain (32 rows x 8 fp32 per Y warp)
-constexpr int STG_BYTES = 12 * 32 * 8 * 4;
+// staging: 4 KB per Y warp (32 rows x 128 B of Y, or 32 rows x 64 B of x̂)
+constexpr int STG_BYTES = 4 * 4096;
 constexpr int BAR_BYTES = 1024;
 constexpr int SMEM = 1024 + kXStages * XS_BYTES + kWStages * (W1_BYTES + W2_BYTES) + ONES_BYTES + STG_BYTES +
                      BAR_BYTES;
@@ -144,22 +144,24 @@ __global__ void __launch_bounds__(512, 1) tok_fused_kernel(const __grid_constant
     MTFM_PDL_ENTRY();
 
     // Y drain by the 4 Y warps once a tile's GEMM2 is done: warp (quarter q)
-    // takes its 32 rows; each 32 x 8 fp32 sub-block goes through a 1 KB staging
-    // slot (lane = row on the way in, 2 lanes per row on the way out) so every
-    // global store writes whole 32 B sectors of 16 rows. Y is handed back to the
-    // GEMM2 warp as soon as the TMEM reads are done.
+    // takes its 32 rows. Each 32-column block goes through the warp's 4 KB staging
+    // slot (lane = row on the way in, 128 B per row, 16 B chunks XOR-swizzled by
+    // row; 8 lanes per row on the way out), so every store instruction writes four
+    // whole 128 B row segments. Y is handed back to the GEMM2 warp as soon as the
+    // TMEM reads are done.
     auto drain = [&](uint32_t n_t, int t, uint32_t q, int slot) {
         int s, m0;
         tok_detail::decode(args, t, s, m0);
         const TokSource& src = args.s[s];
-        float* sbuf = stg + slot * 32 * 8;
-        const int half = lane & 1;       // 16 B half of a 32 B row segment (store phase)
-        long long orow[2];
+        const uint32_t wst = ptx::smem_u32(stg) + static_cast<uint32_t>(slot - 8) * 4096u;
+        const int c16 = lane & 7;        // 16 B chunk of a 128 B row segment (store phase)
+        int orow[8];                     // store phase rows 4i + lane / 8 of the warp's 32
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            const int m = m0 + static_cast<int>(q * 32) + 16 * j + (lane >> 1);
-            orow[j] = m < src.M ? static_cast<long long>(__ldg(src.row_map + m)) : -1;
+        for (int i = 0; i < 8; ++i) {
+            const int m = m0 + static_cast<int>(q * 32) + 4 * i + (lane >> 3);
+            orow[i] = m < src.M ? __ldg(src.row_map + m) : -1;
         }
+        float* const X = args.X;
         const uint32_t lane_addr = (q * 32u) << 16;
         // xhat: lane = row holds every column of its row across cb. Row sums are shifted by a
         // pivot (the row's first value) so that |mean| >> std does not cancel in E[y^2] - mean^2
@@ -188,23 +190,18 @@ __global__ void __launch_bounds__(512, 1) tok_fused_kernel(const __grid_constant
                 if (lane == 0) ptx::mbar_arrive(y_empty);  // Y is free for the next tile's GEMM2
             }
 #pragma unroll
-            for (int sb8 = 0; sb8 < 4; ++sb8) {
-                // row r = lane: chunk h (16 B) of its 32 B segment at (h ^ (r >> 2 & 1))
+            for (int j = 0; j < 8; ++j)
+                ptx::sts128(wst + lane * 128 + ((j ^ (lane & 7)) << 4), v[4 * j], v[4 * j + 1], v[4 * j + 2],
+                            v[4 * j + 3]);
+            __syncwarp();
 #pragma unroll
-                for (int h = 0; h < 2; ++h)
-                    *reinterpret_cast<float4*>(sbuf + lane * 8 + ((h ^ ((lane >> 2) & 1)) << 2)) =
-                        make_float4(v[8 * sb8 + 4 * h], v[8 * sb8 + 4 * h + 1], v[8 * sb8 + 4 * h + 2],
-                                    v[8 * sb8 + 4 * h + 3]);
-                __syncwarp();
-#pragma unroll
-                for (int j = 0; j < 2; ++j) {
-                    const int r = 16 * j + (lane >> 1);
-                    const float4 w = *reinterpret_cast<const float4*>(sbuf + r * 8 + ((half ^ ((r >> 2) & 1)) << 2));
-                    if (orow[j] >= 0)
-                        __stcs(reinterpret_cast<float4*>(args.X + orow[j] * D + cb * 32 + sb8 * 8 + 4 * half), w);
-                }
-                __syncwarp();
+            for (int i = 0; i < 8; ++i) {
+                const int r = 4 * i + (lane >> 3);
+                const float4 w = ptx::lds128(wst + r * 128 + ((c16 ^ (r & 7)) << 4));
+                if (orow[i] >= 0)
+                    __stcs(reinterpret_cast<float4*>(X + static_cast<long long>(orow[i]) * D + cb * 32 + c16 * 4), w);
             }
+            __syncwarp();
         }
         if (xh) {
             // second pass over the row in TMEM: xhat = (y - mean) * rstd (population variance,
@@ -229,22 +226,22 @@ __global__ void __launch_bounds__(512, 1) tok_fused_kernel(const __grid_constant
                 {
                     // 2 KB per warp: row r = lane, 16 B chunk j at (j ^ (r >> 1 & 3)) (conflict-free
                     // both ways); then 4 lanes per row, 8 rows x 64 B per store instruction
-                    uint8_t* xb = reinterpret_cast<uint8_t*>(stg + (slot - 8) * 2 * 32 * 8);
+                    const uint32_t xb = ptx::smem_u32(stg) + static_cast<uint32_t>(slot - 8) * 4096u;
 #pragma unroll
                     for (int j = 0; j < 4; ++j)
-                        *reinterpret_cast<uint4*>(xb + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) =
-                            make_uint4(pack_bf16((v[8 * j] - mean) * rstd, (v[8 * j + 1] - mean) * rstd),
-                                       pack_bf16((v[8 * j + 2] - mean) * rstd, (v[8 * j + 3] - mean) * rstd),
-                                       pack_bf16((v[8 * j + 4] - mean) * rstd, (v[8 * j + 5] - mean) * rstd),
-                                       pack_bf16((v[8 * j + 6] - mean) * rstd, (v[8 * j + 7] - mean) * rstd));
+                        ptx::sts128(xb + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4),
+                                    __uint_as_float(pack_bf16((v[8 * j] - mean) * rstd, (v[8 * j + 1] - mean) * rstd)),
+                                    __uint_as_float(pack_bf16((v[8 * j + 2] - mean) * rstd, (v[8 * j + 3] - mean) * rstd)),
+                                    __uint_as_float(pack_bf16((v[8 * j + 4] - mean) * rstd, (v[8 * j + 5] - mean) * rstd)),
+                                    __uint_as_float(pack_bf16((v[8 * j + 6] - mean) * rstd, (v[8 * j + 7] - mean) * rstd)));
                     __syncwarp();
                     const int c = lane & 3;
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
                         const int rr = 8 * i + (lane >> 2);
-                        const uint4 w = *reinterpret_cast<const uint4*>(xb + rr * 64 + ((c ^ ((rr >> 1) & 3)) << 4));
+                        const float4 w = ptx::lds128(xb + rr * 64 + ((c ^ ((rr >> 1) & 3)) << 4));
                         const int mr = m0 + static_cast<int>(q * 32) + rr;
-                        if (mr < src.M) *reinterpret_cast<uint4*>(args.xhat + (src.xhat_row0 + mr) * D + cb * 32 + c * 8) = w;
+                        if (mr < src.M) *reinterpret_cast<float4*>(args.xhat + (src.xhat_row0 + mr) * D + cb * 32 + c * 8) = w;
                     }
                     __syncwarp();
                 }
