@@ -725,7 +725,7 @@ void launch_tok_fused(const TokArgs& a, cudaStream_t st) {
            "tok smem attr");
         attr = true;
     }
-    launch_k(tok_fused_kernel, dim3(std::min(a.n_tiles, kNumSMs)), dim3(512), tok_detail::SMEM, st, a);
+    launch_k(tok_fused_kernel, dim3(std::min(a.n_tiles, kNumSMs)), dim3(kTokThreads), tok_detail::SMEM, st, a);
     ck(cudaGetLastError(), "tok_fused launch");
 }
 

@@ -14,8 +14,9 @@
 // the two-GEMM path this removes the 2 x (rows x 512 x 2 B) hidden-layer round
 // trip through HBM.
 //
-// Roles (512 threads): warps 0..7 SiLU (two groups of 4, group g owns Hacc[g] /
-// Hb[g], i.e. chunks c = g mod 2), warps 8..11 Y epilogue, warp 12 TMEM
+// Roles (640 threads): warps 0..7 SiLU (two groups of 4, group g owns Hacc[g] /
+// Hb[g], i.e. chunks c = g mod 2), warps 8..11 and 16..19 Y epilogue (column
+// halves), warp 12 TMEM
 // allocator + GEMM1 issuer, warp 13 W2 producer, warp 14 tile + W1 producer,
 // warp 15 GEMM2 issuer. Two producer and two MMA threads: one thread issues
 // a TMA load only every ~150-300 clk (scripts/ubench_tma.cu), and the
@@ -31,6 +32,7 @@
 namespace mtfm {
 
 constexpr int kTokMaxSrc = 8;
+constexpr int kTokThreads = 640;
 
 struct TokSource {
     CUtensorMap tma_e;    // E_s [M][k_pad] bf16, box {64, 128}, SW128 (columns >= k_pad zero-filled)
@@ -64,11 +66,12 @@ constexpr int W1_BYTES = HC * 64 * 2;               // 8 KB
 constexpr int W2_BYTES = D * 64 * 2;                // 32 KB
 constexpr int kXStages = 2, kWStages = 3;
 constexpr int ONES_BYTES = 4096;
-// staging: 4 KB per Y warp (32 rows x 128 B of Y, or 32 rows x 64 B of x̂)
-constexpr int STG_BYTES = 4 * 4096;
+// staging: 2 KB per Y warp (32 rows x 64 B of Y or x̂), then the x̂ partial-sum exchange
+constexpr int STG_BYTES = 8 * 2048;
+constexpr int XCH_BYTES = 2 * 128 * 8;
 constexpr int BAR_BYTES = 1024;
 constexpr int SMEM = 1024 + kXStages * XS_BYTES + kWStages * (W1_BYTES + W2_BYTES) + ONES_BYTES + STG_BYTES +
-                     BAR_BYTES;
+                     XCH_BYTES + BAR_BYTES;
 static_assert(SMEM <= 227 * 1024, "tok SMEM budget");
 constexpr uint32_t Y_COL = 0, HACC_COL = 256, HB_COL = 384;
 
@@ -81,7 +84,7 @@ __device__ __forceinline__ void decode(const TokArgs& a, int t, int& s, int& m0)
 }
 }  // namespace tok_detail
 
-__global__ void __launch_bounds__(512, 1) tok_fused_kernel(const __grid_constant__ TokArgs args) {
+__global__ void __launch_bounds__(kTokThreads, 1) tok_fused_kernel(const __grid_constant__ TokArgs args) {
     using namespace tok_detail;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -90,7 +93,8 @@ __global__ void __launch_bounds__(512, 1) tok_fused_kernel(const __grid_constant
     uint8_t* w2s = w1s + kWStages * W1_BYTES;            // W2 chunk stages
     uint8_t* ones = w2s + kWStages * W2_BYTES;
     float* stg = reinterpret_cast<float*>(ones + ONES_BYTES);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(stg) + STG_BYTES);
+    float2* xch = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(stg) + STG_BYTES);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(stg) + STG_BYTES + XCH_BYTES);
     uint64_t* x_full = bars;             // [2]
     uint64_t* x_empty = bars + 2;        // [2]
     uint64_t* w1_full = bars + 4;        // [3]
@@ -127,7 +131,7 @@ __global__ void __launch_bounds__(512, 1) tok_fused_kernel(const __grid_constant
             ptx::mbar_init(&w2_empty[i], 1);
         }
         ptx::mbar_init(y_full, 1);
-        ptx::mbar_init(y_empty, 4);  // every draining warp arrives
+        ptx::mbar_init(y_empty, 8);  // every draining warp arrives
         ptx::fence_mbar_init();
         for (int i = 0; i < args.n_src; ++i) {
             ptx::tma_prefetch(&args.s[i].tma_e);
@@ -143,40 +147,43 @@ __global__ void __launch_bounds__(512, 1) tok_fused_kernel(const __grid_constant
     // prologue done (barriers, TMEM, SMEM tables): wait for the producer of our inputs
     MTFM_PDL_ENTRY();
 
-    // Y drain by the 4 Y warps once a tile's GEMM2 is done: warp (quarter q)
-    // takes its 32 rows. Each 32-column block goes through the warp's 4 KB staging
-    // slot (lane = row on the way in, 128 B per row, 16 B chunks XOR-swizzled by
-    // row; 8 lanes per row on the way out), so every store instruction writes four
-    // whole 128 B row segments. Y is handed back to the GEMM2 warp as soon as the
-    // TMEM reads are done.
-    auto drain = [&](uint32_t n_t, int t, uint32_t q, int slot) {
+    // Y drain by the 8 Y warps once a tile's GEMM2 is done: warp (quarter q, group g)
+    // takes its 32 rows and the columns [128 g, 128 g + 128). Each 16-column block goes
+    // through the warp's 2 KB staging slot (lane = row on the way in, 16 B chunks
+    // XOR-swizzled by row; 4 lanes per row on the way out: 8 row segments of 64 B per
+    // store instruction). x̂ needs whole-row statistics: the two warps of a quarter
+    // swap their partial sums (both shifted by the row's first value, so that
+    // |mean| >> std does not cancel in E[y^2] - mean^2). Y is handed back to the
+    // GEMM2 warp as soon as each warp's TMEM reads are done.
+    auto drain = [&](uint32_t n_t, int t, uint32_t q, uint32_t grp) {
         int s, m0;
         tok_detail::decode(args, t, s, m0);
         const TokSource& src = args.s[s];
-        const uint32_t wst = ptx::smem_u32(stg) + static_cast<uint32_t>(slot - 8) * 4096u;
-        const int c16 = lane & 7;        // 16 B chunk of a 128 B row segment (store phase)
-        int orow[8];                     // store phase rows 4i + lane / 8 of the warp's 32
+        const uint32_t slot = grp * 4 + q;
+        const uint32_t wst = ptx::smem_u32(stg) + slot * 2048u;
+        const int c4 = lane & 3;         // 16 B chunk of a 64 B row segment (store phase)
+        int orow[4];                     // store phase rows 8i + lane / 4 of the warp's 32
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int m = m0 + static_cast<int>(q * 32) + 4 * i + (lane >> 3);
+        for (int i = 0; i < 4; ++i) {
+            const int m = m0 + static_cast<int>(q * 32) + 8 * i + (lane >> 2);
             orow[i] = m < src.M ? __ldg(src.row_map + m) : -1;
         }
         float* const X = args.X;
         const uint32_t lane_addr = (q * 32u) << 16;
-        // xhat: lane = row holds every column of its row across cb. Row sums are shifted by a
-        // pivot (the row's first value) so that |mean| >> std does not cancel in E[y^2] - mean^2
+        const int cb0 = static_cast<int>(grp) * (D / 64);
         const bool xh = src.xhat_row0 >= 0;
         float ssum = 0.f, ssq = 0.f, piv = 0.f;
         ptx::mbar_wait(y_full, n_t & 1);
         ptx::tc_fence_after();
+        if (xh && grp == 1) piv = ptx::tmem_ld1(tmem + lane_addr + Y_COL);  // the row's first value
 #pragma unroll 1
-        for (int cb = 0; cb < D / 32; ++cb) {
+        for (int cb = cb0; cb < cb0 + D / 64; ++cb) {
             float v[32];
             ptx::tmem_ld16(tmem + lane_addr + Y_COL + cb * 32, *reinterpret_cast<float(*)[16]>(v));
             ptx::tmem_ld16(tmem + lane_addr + Y_COL + cb * 32 + 16, *reinterpret_cast<float(*)[16]>(v + 16));
             ptx::tmem_ld_wait();
             if (xh) {
-                if (cb == 0) piv = v[0];
+                if (grp == 0 && cb == 0) piv = v[0];
 #pragma unroll
                 for (int e = 0; e < 32; ++e) {
                     const float y = v[e] - piv;
@@ -184,67 +191,74 @@ __global__ void __launch_bounds__(512, 1) tok_fused_kernel(const __grid_constant
                     ssq = fmaf(y, y, ssq);
                 }
             }
-            if (!xh && cb == D / 32 - 1) {
+            if (!xh && cb == cb0 + D / 64 - 1) {
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(y_empty);  // Y is free for the next tile's GEMM2
             }
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-                ptx::sts128(wst + lane * 128 + ((j ^ (lane & 7)) << 4), v[4 * j], v[4 * j + 1], v[4 * j + 2],
-                            v[4 * j + 3]);
-            __syncwarp();
+            for (int hh = 0; hh < 2; ++hh) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int r = 4 * i + (lane >> 3);
-                const float4 w = ptx::lds128(wst + r * 128 + ((c16 ^ (r & 7)) << 4));
-                if (orow[i] >= 0)
-                    __stcs(reinterpret_cast<float4*>(X + static_cast<long long>(orow[i]) * D + cb * 32 + c16 * 4), w);
+                for (int j = 0; j < 4; ++j)
+                    ptx::sts128(wst + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4), v[16 * hh + 4 * j],
+                                v[16 * hh + 4 * j + 1], v[16 * hh + 4 * j + 2], v[16 * hh + 4 * j + 3]);
+                __syncwarp();
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int r = 8 * i + (lane >> 2);
+                    const float4 w = ptx::lds128(wst + r * 64 + ((c4 ^ ((r >> 1) & 3)) << 4));
+                    if (orow[i] >= 0)
+                        __stcs(reinterpret_cast<float4*>(X + static_cast<long long>(orow[i]) * D + cb * 32 + hh * 16 +
+                                                         c4 * 4),
+                               w);
+                }
+                __syncwarp();
             }
-            __syncwarp();
         }
         if (xh) {
-            // second pass over the row in TMEM: xhat = (y - mean) * rstd (population variance,
-            // GLN of hta.hpp:104-109 without the affine, which the folded K|V / f1 weights carry).
-            // Y goes back to the GEMM2 warp after this pass's last TMEM load. (Reading the row
-            // back from X instead, after releasing Y, was 3x slower: one row per lane.)
-            const float dm = ssum * (1.f / D);
+            // whole-row statistics from the two halves (same summation order in both warps)
+            xch[grp * 128 + q * 32 + lane] = make_float2(ssum, ssq);
+            ptx::named_bar_sync(1 + q, 64);
+            const float2 o = xch[(grp ^ 1) * 128 + q * 32 + lane];
+            const float s_all = grp == 0 ? ssum + o.x : o.x + ssum;
+            const float q_all = grp == 0 ? ssq + o.y : o.y + ssq;
+            // second pass over the warp's columns in TMEM: xhat = (y - mean) * rstd (population
+            // variance, GLN of hta.hpp:104-109 without the affine, which the folded K|V / f1
+            // weights carry). Y goes back to the GEMM2 warp after this pass's last TMEM load.
+            const float dm = s_all * (1.f / D);
             const float mean = piv + dm;
-            const float var = fmaxf(ssq * (1.f / D) - dm * dm, 0.f);
+            const float var = fmaxf(q_all * (1.f / D) - dm * dm, 0.f);
             const float rstd = rsqrtf(var + args.eps);
 #pragma unroll 1
-            for (int cb = 0; cb < D / 32; ++cb) {
+            for (int cb = cb0; cb < cb0 + D / 64; ++cb) {
                 float v[32];
                 ptx::tmem_ld16(tmem + lane_addr + Y_COL + cb * 32, *reinterpret_cast<float(*)[16]>(v));
                 ptx::tmem_ld16(tmem + lane_addr + Y_COL + cb * 32 + 16, *reinterpret_cast<float(*)[16]>(v + 16));
                 ptx::tmem_ld_wait();
-                if (cb == D / 32 - 1) {
+                if (cb == cb0 + D / 64 - 1) {
                     ptx::tc_fence_before();
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(y_empty);  // Y is free for the next tile's GEMM2
                 }
-                {
-                    // 2 KB per warp: row r = lane, 16 B chunk j at (j ^ (r >> 1 & 3)) (conflict-free
-                    // both ways); then 4 lanes per row, 8 rows x 64 B per store instruction
-                    const uint32_t xb = ptx::smem_u32(stg) + static_cast<uint32_t>(slot - 8) * 4096u;
+                // row r = lane, 16 B chunk j at (j ^ (r >> 1 & 3)) (conflict-free both ways);
+                // then 4 lanes per row, 8 rows x 64 B per store instruction
 #pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        ptx::sts128(xb + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4),
-                                    __uint_as_float(pack_bf16((v[8 * j] - mean) * rstd, (v[8 * j + 1] - mean) * rstd)),
-                                    __uint_as_float(pack_bf16((v[8 * j + 2] - mean) * rstd, (v[8 * j + 3] - mean) * rstd)),
-                                    __uint_as_float(pack_bf16((v[8 * j + 4] - mean) * rstd, (v[8 * j + 5] - mean) * rstd)),
-                                    __uint_as_float(pack_bf16((v[8 * j + 6] - mean) * rstd, (v[8 * j + 7] - mean) * rstd)));
-                    __syncwarp();
-                    const int c = lane & 3;
+                for (int j = 0; j < 4; ++j)
+                    ptx::sts128(wst + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4),
+                                __uint_as_float(pack_bf16((v[8 * j] - mean) * rstd, (v[8 * j + 1] - mean) * rstd)),
+                                __uint_as_float(pack_bf16((v[8 * j + 2] - mean) * rstd, (v[8 * j + 3] - mean) * rstd)),
+                                __uint_as_float(pack_bf16((v[8 * j + 4] - mean) * rstd, (v[8 * j + 5] - mean) * rstd)),
+                                __uint_as_float(pack_bf16((v[8 * j + 6] - mean) * rstd, (v[8 * j + 7] - mean) * rstd)));
+                __syncwarp();
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const int rr = 8 * i + (lane >> 2);
-                        const float4 w = ptx::lds128(xb + rr * 64 + ((c ^ ((rr >> 1) & 3)) << 4));
-                        const int mr = m0 + static_cast<int>(q * 32) + rr;
-                        if (mr < src.M) *reinterpret_cast<float4*>(args.xhat + (src.xhat_row0 + mr) * D + cb * 32 + c * 8) = w;
-                    }
-                    __syncwarp();
+                for (int i = 0; i < 4; ++i) {
+                    const int rr = 8 * i + (lane >> 2);
+                    const float4 w = ptx::lds128(wst + rr * 64 + ((c4 ^ ((rr >> 1) & 3)) << 4));
+                    const int mr = m0 + static_cast<int>(q * 32) + rr;
+                    if (mr < src.M)
+                        *reinterpret_cast<float4*>(args.xhat + (src.xhat_row0 + mr) * D + cb * 32 + c4 * 8) = w;
                 }
+                __syncwarp();
             }
         }
     };
@@ -392,10 +406,10 @@ __global__ void __launch_bounds__(512, 1) tok_fused_kernel(const __grid_constant
                 if (lane == 0) ptx::mbar_arrive(&hb_full[g]);
             }
         }
-    } else if (warp < 12) {
-        // ------------------------------------------------ Y epilogue
+    } else if (warp < 12 || warp >= 16) {
+        // ------------------------------------------------ Y epilogue (groups: warps 8..11, 16..19)
         uint32_t n_t = 0;
-        for (int t = blockIdx.x; t < args.n_tiles; t += gridDim.x, ++n_t) drain(n_t, t, warp & 3, static_cast<int>(warp));
+        for (int t = blockIdx.x; t < args.n_tiles; t += gridDim.x, ++n_t) drain(n_t, t, warp & 3, warp >= 16 ? 1u : 0u);
     }
     ptx::tc_fence_before();
     __syncthreads();
