@@ -297,6 +297,15 @@ typedef struct {
 } mtfm_prune_report;
 MTFM_API mtfm_status mtfm_cuda_prune_projections(mtfm_cuda_model* m, mtfm_prune_report* report);
 
+/* 2:4 sparse tensor cores for the projections (the sm_100a counterpart of the
+ * paper's Ampere sparsity): when every f1_w / fuq_w / fkv_w /
+ * f2_w keeps at most two non-zeros per group of 4 input rows (what
+ * prune_projections leaves) the bf16 forward runs those GEMMs as
+ * tcgen05.mma.sp on the compressed weights. mode 2 (default): whenever the
+ * weights are 2:4; 1: required (MTFM_CONTRACT_ERROR if they are not); 0: dense.
+ * active (optional) receives whether the bf16 forward now uses it. */
+MTFM_API mtfm_status mtfm_cuda_set_sparse_mma(mtfm_cuda_model* m, int32_t mode, int32_t* active);
+
 /* ---------------------------------------------------------------- training
  * Trainer::train_step (train.hpp:111-147) on the GPU over every user of a
  * prepared batch: build_loss (model.hpp:323-358: per sample the mean BCE over

@@ -165,6 +165,7 @@ SIGNATURES = [
     ("mtfm_cuda_aggregate_fetch", C.c_int, [C.c_void_p, C.POINTER(PackedBuffers)]),
     ("mtfm_cuda_aggregate_free", C.c_int, [C.c_void_p]),
     ("mtfm_cuda_prune_projections", C.c_int, [C.c_void_p, C.POINTER(PruneReport)]),
+    ("mtfm_cuda_set_sparse_mma", C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_int32)]),
     ("mtfm_cuda_train_step", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(TrainConfig),
                                        C.POINTER(TrainResult)]),
     ("mtfm_cuda_get_param", C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.c_int64, C.c_int64]),

@@ -20,12 +20,14 @@
 #include <map>
 #include <memory>
 #include <stdexcept>
+#include <tuple>
 #include <string>
 #include <vector>
 
 #include "../../include/mtfm_cuda.h"
 #include "attn_tc.cuh"
 #include "common.cuh"
+#include "gemm_sp.cuh"
 #include "gemm_tc.cuh"
 #include "kernels.cuh"
 #include "tok_tc.cuh"
@@ -198,8 +200,55 @@ __global__ void bias_tile_kernel(const float* __restrict__ bias, int N, __nv_bfl
     t[i] = c == 0 ? hi : __float2bfloat16_rn(v);
 }
 
+// 2:4-compressed forms of the pruned projection weights for gemm_sp.cuh, keyed by
+// the K-major bf16 weight slice they are derived from (built on first use).
+struct SparseForms {
+    struct Form {
+        DevBuf comp, meta;
+        int Np = 0, KB = 0;
+    };
+    bool active = false;  // every projection weight is 2:4 along K: f1 / fuq / fkv / f2 run gemm_sp
+    std::vector<std::pair<const char*, const char*>> ranges;  // the eligible bf16 weight buffers
+    std::map<std::tuple<const void*, int, int>, std::unique_ptr<Form>> forms;
+    void clear() {
+        active = false;
+        ranges.clear();
+        forms.clear();
+    }
+    bool eligible(const void* w) const {
+        const char* c = static_cast<const char*>(w);
+        for (const auto& r : ranges)
+            if (c >= r.first && c < r.second) return true;
+        return false;
+    }
+    const Form& get(const __nv_bfloat16* w, long long ldw, int N, int K, cudaStream_t st) {
+        auto& slot = forms[{w, N, K}];
+        if (!slot) {
+            slot = std::make_unique<Form>();
+            slot->Np = static_cast<int>(round_up(N, 128));
+            slot->KB = static_cast<int>(cdiv(K, 128));
+            slot->comp.alloc(static_cast<size_t>(slot->Np) * slot->KB * 64 * 2);
+            slot->meta.alloc(static_cast<size_t>(slot->Np / 128) * slot->KB * 512 * 4);
+            DevBuf bad;
+            bad.alloc(8);
+            ck(cudaMemsetAsync(bad.p, 0, 8, st), "memset");
+            const long long words = static_cast<long long>(slot->Np / 128) * slot->KB * 512;
+            sp_compress_kernel<<<static_cast<int>(std::min<long long>(cdiv(words, 256), 4 * kNumSMs)), 256, 0, st>>>(
+                w, ldw, N, K, slot->Np, slot->KB, slot->comp.as<__nv_bfloat16>(), slot->meta.as<uint32_t>(),
+                bad.as<unsigned long long>());
+            ck(cudaGetLastError(), "sparse compress");
+            unsigned long long nb = 0;
+            ck(cudaMemcpyAsync(&nb, bad.p, 8, cudaMemcpyDeviceToHost, st), "D2H");
+            ck(cudaStreamSynchronize(st), "sparse compress");
+            if (nb) fail(MTFM_CONTRACT_ERROR, "projection weight is not 2:4 sparse along K");
+        }
+        return *slot;
+    }
+};
+
 struct BiasTiles {
     std::map<std::pair<const float*, int>, std::unique_ptr<DevBuf>> tiles;
+    SparseForms sparse;    // compressed projection weights (pruned models)
     bool rebuild = false;  // re-derive on every use (debug entry: caller-owned bias buffers)
     const __nv_bfloat16* get(const float* bias, int N, cudaStream_t st) {
         auto& slot = tiles[{bias, N}];
@@ -326,6 +375,8 @@ struct mtfm_cuda_model {
     // scenario subgraph (subgraph.hpp:25-42): >= 0 -> only the shared parameters and this
     // scenario's are registered; every forward is scoped to it
     int subgraph = -1;
+    // 2:4 sparse tensor-core projections: 0 off, 1 required, 2 when the weights are 2:4
+    int sparse_mode = 2;
     std::vector<size_t> visible;  // registered parameters in registration order
     bool finalized = false;
     int n_ctx_src = 0;  // leading sources of kind hist/rt (context rows) when they precede every scenario source
@@ -492,10 +543,34 @@ std::vector<uint16_t> to_kmajor_bf16(const std::vector<float>& w, long long rows
     return t;
 }
 
+// every hta/.../{f1_w, fuq_w, fkv_w, f2_w} ([K][N], K a multiple of 64) keeps at most two
+// non-zeros in each group of 4 consecutive rows: the 2:4 pattern prune_2_4 leaves
+bool projections_2_4(const mtfm_cuda_model& m) {
+    bool any = false;
+    for (const auto& p : m.params) {
+        const std::string& n = p.name;
+        if (n.rfind("hta/", 0) != 0) continue;
+        const size_t sl = n.rfind('/');
+        const std::string leaf = n.substr(sl + 1);
+        if (leaf != "f1_w" && leaf != "fuq_w" && leaf != "fkv_w" && leaf != "f2_w") continue;
+        any = true;
+        const long long K = p.rows, N = p.cols;
+        if (K % 64 != 0) return false;
+        for (long long r0 = 0; r0 < K; r0 += 4)
+            for (long long c = 0; c < N; ++c) {
+                int nz = 0;
+                for (int e = 0; e < 4; ++e) nz += p.host[(r0 + e) * N + c] != 0.f;
+                if (nz > 2) return false;
+            }
+    }
+    return any;
+}
+
 void finalize(mtfm_cuda_model& m) {
     if (m.finalized) return;
     // bias tiles are keyed by device pointer: rebuilt weights may reuse freed addresses
     m.bias_tiles.tiles.clear();
+    m.bias_tiles.sparse.clear();
     for (auto& p : m.params) {
         if (m.subgraph >= 0 && p.owner >= 0 && p.owner != m.subgraph) {
             // not part of the subgraph: never bound (forwards are scoped to the subgraph scenario)
@@ -604,6 +679,19 @@ void finalize(mtfm_cuda_model& m) {
             upload(L->g2b, g2b, st);
             m.layers.push_back(std::move(L));
         }
+    // pruned projections (prune.hpp:83-90) run on the sparse tensor cores
+    if (m.sparse_mode != 0) {
+        const bool ok = projections_2_4(m);
+        if (!ok && m.sparse_mode == 1)
+            fail(MTFM_CONTRACT_ERROR, "sparse MMA requested but the projection weights are not 2:4 along K");
+        if (ok) {
+            auto& sf = m.bias_tiles.sparse;
+            sf.active = true;
+            for (const auto& L : m.layers)
+                for (const DevBuf* b : {&L->t1, &L->tkv, &L->tf2, &L->tfold})
+                    if (b->p) sf.ranges.push_back({static_cast<const char*>(b->p), static_cast<const char*>(b->p) + b->bytes});
+        }
+    }
     // heads: [d][E*de | n_tasks*E]
     const int E = m.cfg.experts, dx = m.cfg.d_expert;
     m.head_n = E * dx + m.n_tasks_total * E;
@@ -790,10 +878,61 @@ int pick_bn_resident(const std::vector<TcProblem>& ps) {
     return best;
 }
 
+// Pruned projections on the sparse tensor cores (gemm_sp.cuh): same problems, the
+// weight slice replaced by its compressed 2:4 form.
+void run_gemm_sp(const std::vector<TcProblem>& ps, cudaStream_t st, long long& launches, SparseForms& sf) {
+    static bool attr = false;
+    if (!attr) {
+        ck(cudaFuncSetAttribute(gemm_sp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sp_detail::SMEM),
+           "sparse gemm smem attr");
+        attr = true;
+    }
+    for (size_t i0 = 0; i0 < ps.size(); i0 += kMaxProblems) {
+        const size_t i1 = std::min(ps.size(), i0 + kMaxProblems);
+        SpArgs a;
+        std::memset(&a, 0, sizeof(a));
+        int tiles = 0;
+        for (size_t i = i0; i < i1; ++i) {
+            const TcProblem& s = ps[i];
+            const SparseForms::Form& f = sf.get(s.Bt, s.ldb, s.N, s.K, st);
+            SpProblem& p = a.p[a.n_problems++];
+            p.tma_w = tma_2d(f.comp.p, f.Np, static_cast<long long>(f.KB) * 64, static_cast<long long>(f.KB) * 64, 64,
+                             128, 128);
+            p.tma_x = tma_2d(s.A, s.M, s.K, s.lda, 64, 128, 128);
+            p.meta = f.meta.as<uint32_t>();
+            p.M = s.M;
+            p.N = s.N;
+            p.K = s.K;
+            p.kb = f.KB;
+            p.tile_start = tiles;
+            p.tiles_f = f.Np / 128;
+            p.epi = s.epi;
+            p.bias = s.bias;
+            p.out = s.out;
+            p.ldo = s.ldo;
+            p.row_map = s.row_map;
+            p.row_offset = s.row_offset;
+            tiles += static_cast<int>(cdiv(s.M, 128)) * p.tiles_f;
+        }
+        a.n_tiles = tiles;
+        launch_k(gemm_sp_kernel, dim3(std::min(tiles, kNumSMs)), dim3(sp_detail::kThreads), sp_detail::SMEM, st, a);
+        ck(cudaGetLastError(), "gemm_sp launch");
+        ++launches;
+    }
+}
+
 void run_gemm_tc(std::vector<TcProblem> ps, cudaStream_t st, long long& launches, BiasTiles& bias_tiles) {
     ps.erase(std::remove_if(ps.begin(), ps.end(), [](const TcProblem& p) { return p.M == 0 || p.N == 0; }),
              ps.end());
     if (ps.empty()) return;
+    if (bias_tiles.sparse.active &&
+        std::all_of(ps.begin(), ps.end(), [&](const TcProblem& p) {
+            return bias_tiles.sparse.eligible(p.Bt) && p.K % 64 == 0 && p.lda % 8 == 0 &&
+                   (p.epi == EPI_SILU_BF16 || (p.epi == EPI_RESID_F32 && p.resid == p.out));
+        })) {
+        run_gemm_sp(ps, st, launches, bias_tiles.sparse);
+        return;
+    }
     const int bn_res = pick_bn_resident(ps);
     for (size_t i0 = 0; i0 < ps.size(); i0 += kMaxProblems) {
         const size_t i1 = std::min(ps.size(), i0 + kMaxProblems);
@@ -2473,6 +2612,30 @@ mtfm_status mtfm_cuda_prune_projections(mtfm_cuda_model* m, mtfm_prune_report* r
         m->layers.clear();
         m->train.reset();
         if (rep) *rep = r;
+    });
+}
+
+mtfm_status mtfm_cuda_set_sparse_mma(mtfm_cuda_model* m, int32_t mode, int32_t* active) {
+    return guard([&] {
+        if (!m) fail(MTFM_CONTRACT_ERROR, "null argument");
+        if (mode < 0 || mode > 2) fail(MTFM_CONTRACT_ERROR, "sparse MMA mode must be 0, 1 or 2");
+        ck(cudaSetDevice(m->device), "cudaSetDevice");
+        if (m->device_ahead) sync_host_params(*m);
+        const int old = m->sparse_mode;
+        m->sparse_mode = mode;
+        m->finalized = false;
+        m->srcw.clear();
+        m->layers.clear();
+        try {
+            finalize(*m);
+        } catch (...) {
+            m->sparse_mode = old;  // the model stays usable in its previous mode
+            m->finalized = false;
+            m->srcw.clear();
+            m->layers.clear();
+            throw;
+        }
+        if (active) *active = m->bias_tiles.sparse.active && m->precision == MTFM_PRECISION_BF16 ? 1 : 0;
     });
 }
 

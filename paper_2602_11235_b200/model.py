@@ -239,6 +239,13 @@ class Model:
         return dict(groups_covered=rep.groups_covered, zeros_written=rep.zeros_written,
                     exempt_tail_rows=rep.exempt_tail_rows, pruned_params=rep.pruned_params)
 
+    def set_sparse_mma(self, mode=2):
+        """2:4 sparse tensor cores for f1/fuq/fkv/f2 (include/mtfm_cuda.h): mode 2 when the
+        weights are 2:4 (default), 1 required, 0 dense. Returns whether the bf16 forward uses it."""
+        active = C.c_int32(0)
+        abi.check(abi.lib().mtfm_cuda_set_sparse_mma(self._h, int(mode), C.byref(active)))
+        return bool(active.value)
+
     def get_param(self, name, rows, cols):
         out = np.empty((rows, cols), np.float32)
         abi.check(abi.lib().mtfm_cuda_get_param(self._h, name.encode(), abi.ptr(out), rows, cols))
