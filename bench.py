@@ -193,6 +193,12 @@ def workload_inputs(args):
     batch = datagen.generate(wl, n_users=args.users or wl.n_users)
     specs = param_specs(wl.schemas, wl.cfg)
     params = datagen.random_params(specs, seed=7)
+    if getattr(args, "prune", False):
+        # the reference arm's copy of the pruned weights: prune_model_projections restated
+        # (oracle/mtfm_oracle.py, bit-exact with the reference and the device prune)
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import mtfm_oracle as O
+        params = {k: (O.prune_2_4(v)[0] if O.is_projection_param(k) else v) for k, v in params.items()}
     return wl, batch, params, [n for n, _, _ in specs]
 
 
@@ -220,6 +226,7 @@ def run_reference(args, world, rank):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * secs / len(timed),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"MTFM-{args.config}", "users_per_step": users, "threads": threads,
+                   **({"pruned_2_4": True} if args.prune else {}),
                    "cpu_model": cpu_model(), "build": rows[-1].get("build"),
                    "note": "reference Model<float>::forward_sample striped over std::thread workers "
                            "(train.hpp:157-170), compiled from the unmodified reference sources; inputs are "
@@ -245,6 +252,10 @@ def main():
     ap.add_argument("--ref-users", type=int, default=96)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-json", default=None)
+    ap.add_argument("--prune", action="store_true",
+                    help="2:4-prune f1/fuq/fkv/f2 (prune_projections) before timing: the pruned model")
+    ap.add_argument("--sparse-mode", type=int, default=2, choices=[0, 1, 2],
+                    help="with --prune: 2:4 sparse tensor cores 2 auto / 1 required / 0 dense (mtfm_cuda_set_sparse_mma)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_setup()
@@ -276,6 +287,11 @@ def main():
     model = Model(wl.schemas, wl.cfg, precision="bf16", device=local)
     params = datagen.random_params(model.param_specs(), seed=7)
     model.set_params(params)
+    sparse_active = None
+    if args.prune:
+        model.prune_projections()
+        sparse_active = model.set_sparse_mma(args.sparse_mode)
+        params = {n: model.get_param(n, r, c) for n, r, c in model.param_specs()}  # the CPU arm's weights
     n_targets = int(len(batch["exp_ts"]))
     n_tokens = int(len(batch["ev_ts"])) + n_targets
     rank_targets = [n_targets]
@@ -458,6 +474,7 @@ def main():
                    "layers": f"({wl.cfg.hta.target_layers}:{wl.cfg.hta.full_layers})x{wl.cfg.hta.blocks}",
                    "d_model": wl.cfg.hta.d_model, "heads": wl.cfg.hta.heads, "kv_heads": wl.cfg.hta.kv_heads,
                    "parallelism": f"users sharded, {world} GPU(s), no data-path collective",
+                   **({"pruned_2_4": True, "sparse_mma": sparse_active} if args.prune else {}),
                    "l2": "inputs/activations > L2 (X alone is %.0f MB)" % (n_tokens * wl.cfg.hta.d_model * 4 / 1e6)},
         "e2e": {"value": e2e_value, "unit": "targets/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_s * 1000, "api": "batch_update/batch_run/batch_results, two batches in flight",

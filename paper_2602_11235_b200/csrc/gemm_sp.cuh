@@ -8,8 +8,8 @@
 // four in K order) plus metadata (two 2-bit indices per group). The activations X
 // are the dense B operand, N = 128 tokens per tile. D = W X^T lands in TMEM with one
 // feature per lane, so for a token the 32 lanes of a warp hold 32 consecutive
-// features: the epilogue stores 64 B (bf16) / 128 B (fp32) row segments straight
-// from registers, with the row scatter of the dense path.
+// features; the epilogue turns them into one 64 B (bf16) / 128 B (fp32) row segment per lane
+// through a per-warp SMEM transpose, with the row scatter of the dense path.
 //
 // Metadata in TMEM (established on the device by scripts/probe_sparse.cu): one
 // 32-bit column per MMA (M = 128, K = 32); row m, group g (of four logical K) sits
@@ -19,8 +19,8 @@
 // loads and is moved into TMEM by one tcgen05.cp 128x128b (row r -> lane r,
 // checked by scripts/probe_tcgen05_cp.cu) issued ahead of the stage's four MMAs.
 //
-// Roles (352 threads): warps 0..7 epilogue (two groups of four, group g drains
-// accumulator g), warp 8 TMEM allocator, warp 9 TMA producer, warp 10 MMA issuer.
+// Roles (480 threads): warps 0..11 epilogue (three groups of four, group g drains
+// accumulator g), warp 12 TMEM allocator, warp 13 TMA producer, warp 14 MMA issuer.
 #pragma once
 
 #include "common.cuh"
@@ -57,11 +57,15 @@ constexpr int W_BYTES = BM * 64 * 2;        // 128 features x 64 kept values (12
 constexpr int X_BYTES = 2 * BN * 64 * 2;    // 128 tokens x 128 logical K, two SW128 boxes
 constexpr int E_BYTES = 128 * 16;           // metadata: 128 lanes x 4 words
 constexpr int STAGE_BYTES = W_BYTES + X_BYTES + E_BYTES;
-constexpr int kStages = 4;
+constexpr int kStages = 3;
+constexpr int STG_LD = 36;                        // epilogue staging row: 32 fp32 + 16 B pad (conflict-free both ways)
+constexpr int kAcc = 3;                           // TMEM accumulators = epilogue groups of 4 warps
+constexpr int kEpiWarps = 4 * kAcc;
+constexpr int STG_BYTES = kEpiWarps * 32 * STG_LD * 4;  // per epilogue warp: 32 tokens
 constexpr int BAR_BYTES = 256;
-constexpr int SMEM = 1024 + kStages * STAGE_BYTES + BAR_BYTES + kMaxProblems * 4;
-constexpr int kThreads = 352;
-constexpr uint32_t ACC_COL = 0, META_COL = 2 * BN;  // TMEM: two 128-column accumulators, then 4 x 4 metadata columns
+constexpr int SMEM = 1024 + kStages * STAGE_BYTES + STG_BYTES + BAR_BYTES + kMaxProblems * 4;
+constexpr int kThreads = 32 * (kEpiWarps + 3);
+constexpr uint32_t ACC_COL = 0, META_COL = kAcc * BN;  // TMEM: kAcc 128-column accumulators, then 4 metadata columns per stage
 static_assert(SMEM <= 227 * 1024, "sparse GEMM SMEM budget");
 
 __device__ __forceinline__ void decode(const SpArgs& a, const int* ts, int t, int& pi, int& tt, int& ft) {
@@ -100,23 +104,24 @@ __global__ void __launch_bounds__(sp_detail::kThreads, 1) gemm_sp_kernel(const _
     using namespace sp_detail;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* bars = reinterpret_cast<uint64_t*>(base + kStages * STAGE_BYTES);
+    float* stg = reinterpret_cast<float*>(base + kStages * STAGE_BYTES);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(base + kStages * STAGE_BYTES + STG_BYTES);
     uint64_t* full = bars;              // [kStages]
     uint64_t* empty = bars + kStages;   // [kStages]
-    uint64_t* acc_full = bars + 2 * kStages;   // [2]
-    uint64_t* acc_empty = acc_full + 2;        // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
-    int* s_ts = reinterpret_cast<int*>(base + kStages * STAGE_BYTES + BAR_BYTES);
+    uint64_t* acc_full = bars + 2 * kStages;   // [kAcc]
+    uint64_t* acc_empty = acc_full + kAcc;     // [kAcc]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + kAcc);
+    int* s_ts = reinterpret_cast<int*>(base + kStages * STAGE_BYTES + STG_BYTES + BAR_BYTES);
 
     const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
-    constexpr uint32_t kWarpAlloc = 8, kWarpTma = 9, kWarpMma = 10;
+    constexpr uint32_t kWarpAlloc = kEpiWarps, kWarpTma = kEpiWarps + 1, kWarpMma = kEpiWarps + 2;
     for (int i = threadIdx.x; i < args.n_problems; i += blockDim.x) s_ts[i] = args.p[i].tile_start;
     if (warp == kWarpTma && lane == 0) {
         for (int i = 0; i < kStages; ++i) {
             ptx::mbar_init(&full[i], 1);
             ptx::mbar_init(&empty[i], 1);
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kAcc; ++i) {
             ptx::mbar_init(&acc_full[i], 1);
             ptx::mbar_init(&acc_empty[i], 4);
         }
@@ -161,8 +166,8 @@ __global__ void __launch_bounds__(sp_detail::kThreads, 1) gemm_sp_kernel(const _
             int pi, tt, ft;
             decode(args, s_ts, t, pi, tt, ft);
             const SpProblem& p = args.p[pi];
-            const uint32_t acc = n_t & 1;
-            ptx::mbar_wait(&acc_empty[acc], ((n_t >> 1) & 1) ^ 1);
+            const uint32_t acc = n_t % kAcc;
+            ptx::mbar_wait(&acc_empty[acc], ((n_t / kAcc) & 1) ^ 1);
             ptx::tc_fence_after();
             for (int kb = 0; kb < p.kb; ++kb, ++it) {
                 const uint32_t s = it % kStages;
@@ -189,22 +194,40 @@ __global__ void __launch_bounds__(sp_detail::kThreads, 1) gemm_sp_kernel(const _
                 __syncwarp();
             }
         }
-    } else if (warp < 8) {
-        // epilogue group g drains accumulator g (tiles n_t with n_t % 2 == g)
+    } else if (warp < kEpiWarps) {
+        // epilogue group g drains accumulator g (tiles n_t with n_t % kAcc == g); lane = feature.
+        // SiLU -> bf16: per 32-token block through SMEM [token][feature], then lane = token writes
+        // its 32 features (64 B) to its row (scattered through row_map; measured faster than
+        // 4 lanes per row). Residual (contiguous rows): per token the warp's 32 features are one
+        // 128 B segment, read and written straight from registers.
         const uint32_t g = warp >> 2, q = warp & 3;
+        const uint32_t sw = ptx::smem_u32(stg) + warp * (32 * STG_LD * 4);
         uint32_t n_t = 0, k = 0;
         for (int t = blockIdx.x; t < args.n_tiles; t += gridDim.x, ++n_t) {
-            if ((n_t & 1) != g) continue;
+            if (n_t % kAcc != g) continue;
             int pi, tt, ft;
             decode(args, s_ts, t, pi, tt, ft);
             const SpProblem& p = args.p[pi];
-            const int f = ft * BM + static_cast<int>(q * 32 + lane);
-            const bool fv = f < p.N;
-            const float bf = (p.bias && fv) ? __ldg(p.bias + f) : 0.f;
+            const int f0 = ft * BM + static_cast<int>(q * 32);
+            const int nval = min(max(p.N - f0, 0), 32);  // valid features of this warp (a multiple of 8)
+            const bool fv = static_cast<int>(lane) < nval;
+            const float bf = (p.bias && fv) ? __ldg(p.bias + f0 + lane) : 0.f;
+            const bool silu = p.epi == EPI_SILU_BF16;
+            // SiLU store phase: lane = token, its 32 features as 4 x 16 B to its (scattered) row
+            long long rr[BN / 32];
+            if (silu) {
+#pragma unroll
+                for (int cb = 0; cb < BN / 32; ++cb) {
+                    const int tok = tt * BN + cb * 32 + static_cast<int>(lane);
+                    rr[cb] = tok < p.M ? (p.row_map ? static_cast<long long>(__ldg(p.row_map + tok))
+                                                    : p.row_offset + tok)
+                                       : -1;
+                }
+            }
             ptx::mbar_wait(&acc_full[g], k & 1);
             ++k;
             ptx::tc_fence_after();
-#pragma unroll 1
+#pragma unroll
             for (int cb = 0; cb < BN / 32; ++cb) {
                 float v[32];
                 const uint32_t ta = tmem + ((q * 32u) << 16) + ACC_COL + g * BN + cb * 32;
@@ -216,25 +239,36 @@ __global__ void __launch_bounds__(sp_detail::kThreads, 1) gemm_sp_kernel(const _
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(&acc_empty[g]);
                 }
-                // output row of token tok0 + lane, -1 past the end
-                const int tok = tt * BN + cb * 32 + static_cast<int>(lane);
-                long long rr = -1;
-                if (tok < p.M) rr = p.row_map ? static_cast<long long>(__ldg(p.row_map + tok)) : p.row_offset + tok;
-                if (p.epi == EPI_SILU_BF16) {
-                    __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out) + f;
+                const int tok0 = tt * BN + cb * 32;
+                if (silu) {
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const long long r = __shfl_sync(0xffffffffu, rr, j);
-                        const float y = ptx::silu_fast(v[j] + bf);
-                        if (r >= 0 && fv) o[r * p.ldo] = __float2bfloat16_rn(y);
+                    for (int j = 0; j < 32; ++j) ptx::sts32(sw + (j * STG_LD + lane) * 4, ptx::silu_fast(v[j] + bf));
+                    __syncwarp();
+                    float4 w[8];
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) w[c] = ptx::lds128(sw + (lane * STG_LD + 4 * c) * 4);
+                    const long long r = rr[cb];
+                    if (r >= 0) {
+                        __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out) + r * p.ldo + f0;
+#pragma unroll
+                        for (int c = 0; c < 4; ++c)
+                            if (8 * c < nval)
+                                *reinterpret_cast<uint4*>(o + 8 * c) =
+                                    make_uint4(pack_bf16(w[2 * c].x, w[2 * c].y), pack_bf16(w[2 * c].z, w[2 * c].w),
+                                               pack_bf16(w[2 * c + 1].x, w[2 * c + 1].y),
+                                               pack_bf16(w[2 * c + 1].z, w[2 * c + 1].w));
                     }
+                    __syncwarp();
                 } else {
-                    float* o = static_cast<float*>(p.out) + f;
+                    // residual rows first (32 independent 128 B loads in flight), then the stores
+                    const int jn = min(32, p.M - tok0);
+                    float* o = static_cast<float*>(p.out) + (p.row_offset + tok0) * p.ldo + f0 + lane;
+                    float old[32];
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const long long r = __shfl_sync(0xffffffffu, rr, j);
-                        if (r >= 0 && fv) o[r * p.ldo] = (v[j] + bf) + o[r * p.ldo];
-                    }
+                    for (int j = 0; j < 32; ++j) old[j] = (j < jn && fv) ? o[j * p.ldo] : 0.f;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (j < jn && fv) o[j * p.ldo] = (v[j] + bf) + old[j];
                 }
             }
         }

@@ -927,8 +927,10 @@ void run_gemm_tc(std::vector<TcProblem> ps, cudaStream_t st, long long& launches
     if (ps.empty()) return;
     if (bias_tiles.sparse.active &&
         std::all_of(ps.begin(), ps.end(), [&](const TcProblem& p) {
-            return bias_tiles.sparse.eligible(p.Bt) && p.K % 64 == 0 && p.lda % 8 == 0 &&
-                   (p.epi == EPI_SILU_BF16 || (p.epi == EPI_RESID_F32 && p.resid == p.out));
+            // 16 B output vectors: N, ldo multiples of 8 and a 16 B aligned output
+            return bias_tiles.sparse.eligible(p.Bt) && p.K % 64 == 0 && p.lda % 8 == 0 && p.N % 8 == 0 &&
+                   p.ldo % 8 == 0 && reinterpret_cast<uintptr_t>(p.out) % 16 == 0 &&
+                   (p.epi == EPI_SILU_BF16 || (p.epi == EPI_RESID_F32 && p.resid == p.out && !p.row_map));
         })) {
         run_gemm_sp(ps, st, launches, bias_tiles.sparse);
         return;
