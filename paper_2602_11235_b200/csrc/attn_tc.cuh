@@ -94,6 +94,23 @@ __device__ __forceinline__ uint32_t sw128_off(uint32_t row, uint32_t chunk16) {
 
 using ptx::silu2_bf16;
 
+// 16 keys (columns base .. base + 15 of the warp's chunk) -> 8 packed bf16 P words, keys at
+// or past nvalid masked to 0
+__device__ __forceinline__ void silu_half(const float (&v)[16], uint32_t (&p)[8], int nvalid, int base) {
+    if (__all_sync(0xffffffffu, nvalid >= base + 16)) {
+#pragma unroll
+        for (int e = 0; e < 16; e += 2) p[e / 2] = silu2_bf16(v[e], v[e + 1]);
+    } else {
+#pragma unroll
+        for (int e = 0; e < 16; e += 2) {
+            const uint32_t w = silu2_bf16(v[e], v[e + 1]);
+            const int k = base + e;
+            const uint32_t keep = (k + 1 < nvalid) ? 0xffffffffu : (k < nvalid ? 0x0000ffffu : 0u);
+            p[e / 2] = w & keep;
+        }
+    }
+}
+
 }  // namespace attn_detail
 
 // P aliases S: each SiLU warp overwrites the first half of its own S columns
@@ -306,6 +323,26 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
                 ptx::tc_fence_after();
                 const uint32_t col = buf * BKV + cq * CW;
                 const int nvalid = prefix - (j * BKV + static_cast<int>(cq) * CW);  // >= CW: no masking
+                if constexpr (CW == 32) {
+                    // two halves of 16 keys: the second half's TMEM load and the first half's
+                    // P store are in flight while the other half's SiLUs run
+                    uint32_t pa[8], pb[8];
+                    if (__all_sync(0xffffffffu, nvalid <= 0)) {
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) pa[e] = pb[e] = 0u;
+                        ptx::tmem_st8(tmem + lane_addr + col, pa);
+                    } else {
+                        float va[16], vb[16];
+                        ptx::tmem_ld16(tmem + lane_addr + col, va);
+                        ptx::tmem_ld_wait_dep(va);
+                        ptx::tmem_ld16(tmem + lane_addr + col + 16, vb);
+                        attn_detail::silu_half(va, pa, nvalid, 0);
+                        ptx::tmem_st8(tmem + lane_addr + col, pa);
+                        ptx::tmem_ld_wait_dep(vb);
+                        attn_detail::silu_half(vb, pb, nvalid, 16);
+                    }
+                    ptx::tmem_st8(tmem + lane_addr + col + 8, pb);
+                } else {
                 uint32_t pk[CW / 2];
                 if (__all_sync(0xffffffffu, nvalid <= 0)) {
 #pragma unroll
@@ -331,6 +368,7 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
                 }
                 if constexpr (CW / 2 == 16) ptx::tmem_st16(tmem + lane_addr + col, pk);
                 else ptx::tmem_st8(tmem + lane_addr + col, *reinterpret_cast<const uint32_t(*)[8]>(pk));
+                }
                 ptx::tmem_st_wait();
                 ptx::tc_fence_before();
                 __syncwarp();
