@@ -90,6 +90,19 @@ __device__ void bitonic_sort(long long* ts, long long* sec, int npad, Less less)
 }
 
 // number of entries of sorted a[0, n) strictly below v
+// number of a[0..n) <= v (a sorted)
+__device__ __forceinline__ int count_le(const long long* a, int n, long long v) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (a[mid] <= v)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
 __device__ __forceinline__ int count_below(const long long* a, int n, long long v) {
     int lo = 0, hi = n;
     while (lo < hi) {
@@ -161,15 +174,46 @@ __global__ void __launch_bounds__(256, 8) plan_kernel(PlanArgs a) {
     }
 
     // ---------------- context tokens: (kind, ts, pile order)
-    for (int i = tid; i < npad; i += blockDim.x) {
-        if (i < n_ev) {
+    // When every sequence is in time order (the usual input) that order is a stable merge
+    // of the sequences of each kind: an event's rank is its index in its sequence plus, per
+    // other sequence of its kind, the events before it (binary search; the earlier sequence
+    // wins ties, as the pile index does). Otherwise, or with many sequences: bitonic sort.
+    constexpr int kMergeSeqs = 16;
+    int unsorted = s1 - s0 > kMergeSeqs;
+    if (!unsorted)
+        for (int q = s0; q < s1; ++q)
+            for (int e = b.ev_off[q] + tid; e + 1 < b.ev_off[q + 1]; e += blockDim.x)
+                unsorted |= b.ev_ts[e + 1] < b.ev_ts[e];
+    const bool merge = !__syncthreads_or(unsorted);
+    if (merge) {
+        int n_k0 = 0;  // H events precede every R event
+        for (int q = s0; q < s1; ++q)
+            if (!b.seq_kind[q]) n_k0 += b.ev_off[q + 1] - b.ev_off[q];
+        for (int i = tid; i < n_ev; i += blockDim.x) {
             const int e = ev0 + i;
             const int sq = find_seq(b.ev_off, s0, s1, e);
-            s_ts[i] = b.ev_ts[e];
-            s_sec[i] = (static_cast<long long>(b.seq_kind[sq] ? 1 : 0) << 32) | i;
-        } else {
-            s_ts[i] = LLONG_MAX;
-            s_sec[i] = 3ll << 32;
+            const int kind = b.seq_kind[sq] ? 1 : 0;
+            const long long ts = b.ev_ts[e];
+            int rank = (kind ? n_k0 : 0) + (e - b.ev_off[sq]);
+            for (int q = s0; q < s1; ++q) {
+                if (q == sq || (b.seq_kind[q] ? 1 : 0) != kind) continue;
+                const int a0 = b.ev_off[q], n = b.ev_off[q + 1] - a0;
+                rank += q < sq ? count_le(b.ev_ts + a0, n, ts) : count_below(b.ev_ts + a0, n, ts);
+            }
+            s_ts[rank] = ts;
+            s_sec[rank] = (static_cast<long long>(kind) << 32) | i;
+        }
+    } else {
+        for (int i = tid; i < npad; i += blockDim.x) {
+            if (i < n_ev) {
+                const int e = ev0 + i;
+                const int sq = find_seq(b.ev_off, s0, s1, e);
+                s_ts[i] = b.ev_ts[e];
+                s_sec[i] = (static_cast<long long>(b.seq_kind[sq] ? 1 : 0) << 32) | i;
+            } else {
+                s_ts[i] = LLONG_MAX;
+                s_sec[i] = 3ll << 32;
+            }
         }
     }
     __syncthreads();
@@ -178,7 +222,7 @@ __global__ void __launch_bounds__(256, 8) plan_kernel(PlanArgs a) {
     // timestamp below -1 is a dimension_error that precedes every other error of the user
     for (int i = tid; i < n_ev; i += blockDim.x)
         if (b.ev_ts[ev0 + i] < -1) atomicMin(&s_err, err_key(u, 0, 0, 0, ERR_META));
-    if (n_ev > 1) bitonic_sort(s_ts, s_sec, npad, CtxLess{});
+    if (!merge && n_ev > 1) bitonic_sort(s_ts, s_sec, npad, CtxLess{});
     for (int i = tid; i < n_ev; i += blockDim.x)
         if ((s_sec[i] >> 32) == 0 && (i + 1 == n_ev || (s_sec[i + 1] >> 32) != 0)) s_lh = i + 1;
     __syncthreads();

@@ -171,3 +171,53 @@ def test_context_timestamp_below_minus_one_is_dimension_error():
     with pytest.raises(abi.DimensionError) as ei:
         m.forward_batch(b)
     assert "user index 2" in str(ei.value) and "time-sorted" in str(ei.value)
+
+
+def _permute_sequence(b, seq, order):
+    """Reorder the events of packed sequence `seq` (timestamps with their features)."""
+    b = {k: v.copy() for k, v in b.items()}
+    e0, e1 = int(b["ev_off"][seq]), int(b["ev_off"][seq + 1])
+    fo = b["ev_feat_off"]
+    feats = [b["ev_feats"][fo[e]:fo[e + 1]] for e in range(e0, e1)]
+    ts = b["ev_ts"][e0:e1].copy()
+    new_feats = [feats[i] for i in order]
+    b["ev_ts"][e0:e1] = ts[order]
+    pos = int(fo[e0])
+    for k, f in enumerate(new_feats):
+        b["ev_feats"][pos:pos + len(f)] = f
+        pos += len(f)
+        b["ev_feat_off"][e0 + k + 1] = pos
+    return normalize_batch(b)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_unsorted_sequences_and_cross_sequence_ties_vs_oracle(precision):
+    """plan_tokens stable-sorts each kind's context events by time (tokenizer.hpp:117-123):
+    sequences in time order take the merge path of the plan kernel, a shuffled sequence
+    the bitonic sort; equal timestamps across the two H sequences keep pile order."""
+    wl = _wl(hist_len=60, rt_len=12, exp_per_scen=3, seed=51)
+    b = datagen.generate(wl, n_users=4)
+    # user 1: shuffle its first sequence; user 2: copy timestamps of its first H sequence
+    # into its second so that every event ties with one of the other sequence
+    s1 = int(b["seq_off"][1])
+    n1 = int(b["ev_off"][s1 + 1] - b["ev_off"][s1])
+    b = _permute_sequence(b, s1, np.random.default_rng(5).permutation(n1))
+    s2 = int(b["seq_off"][2])
+    a0, a1 = int(b["ev_off"][s2]), int(b["ev_off"][s2 + 1])
+    c0, c1 = int(b["ev_off"][s2 + 1]), int(b["ev_off"][s2 + 2])
+    k = min(a1 - a0, c1 - c0)
+    ts = np.sort(b["ev_ts"][a0:a0 + k])
+    b["ev_ts"][a0:a0 + k] = ts
+    b["ev_ts"][c0:c0 + k] = ts
+    b["ev_ts"][a0 + k:a1] = np.maximum(b["ev_ts"][a0 + k:a1], ts[-1])
+    b["ev_ts"][c0 + k:c1] = np.maximum(b["ev_ts"][c0 + k:c1], ts[-1])
+    assert b["seq_kind"][s2] == 0 and b["seq_kind"][s2 + 1] == 0
+    m, P = _model(wl, precision)
+    osch, ocfg = to_oracle(wl.schemas, wl.cfg)
+    keys, z_ref, _ = oracle_records(osch, ocfg, P, b)
+    ra = m.forward_batch(b)
+    assert np.array_equal(np.stack([ra.user_id, ra.scenario_id, ra.exposure_index, ra.task_index], 1), keys)
+    if precision == "bf16":
+        assert np.max(np.abs(ra.logit - z_ref)) <= 2e-2
+    else:
+        assert rel_err(ra.logit.astype(np.float64), z_ref) <= 1e-4
