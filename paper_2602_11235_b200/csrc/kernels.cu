@@ -429,56 +429,64 @@ __global__ void gather_kernel(DevBatch b, const SourceInfo* __restrict__ srcs, c
                               const long long* __restrict__ src_base, const long long* __restrict__ src_cnt,
                               const long long* __restrict__ emb_base, const T* __restrict__ tables, int d_emb,
                               int n_src, long long total_rows, int max_slots, T* __restrict__ out) {
-    // source tables in SMEM (n_src <= 32); 32-bit item math (n_items < 2^31, checked on the host)
+    // source and slot tables in SMEM (n_src <= 32, slots <= kGatherSlots or read from global)
+    constexpr int kGatherSlots = 128;
     __shared__ long long s_base[33], s_cnt[32], s_emb[32];
     __shared__ SourceInfo s_src[32];
+    __shared__ SlotInfo s_slot[kGatherSlots];
+    int n_slots = 0;
+    for (int i = 0; i < n_src; ++i) n_slots = max(n_slots, srcs[i].slot0 + srcs[i].nslot[0] + srcs[i].nslot[1] + srcs[i].nslot[2]);
     for (int i = threadIdx.x; i < n_src; i += blockDim.x) {
         s_base[i] = src_base[i];
         s_cnt[i] = src_cnt[i];
         s_emb[i] = emb_base[i];
         s_src[i] = srcs[i];
     }
+    for (int i = threadIdx.x; i < n_slots && i < kGatherSlots; i += blockDim.x) s_slot[i] = slots[i];
+    const SlotInfo* sl_tab = n_slots <= kGatherSlots ? s_slot : slots;
     if (threadIdx.x == 0) s_base[n_src] = total_rows;
     MTFM_PDL_ENTRY();
     __syncthreads();
-    const unsigned per = static_cast<unsigned>(max_slots + 1);
-    const unsigned n_items = static_cast<unsigned>(total_rows) * per;
-    for (unsigned w = blockIdx.x * blockDim.x + threadIdx.x; w < n_items; w += gridDim.x * blockDim.x) {
-        const unsigned P = w / per;
-        const int k = static_cast<int>(w - P * per);
+    // one source row per thread: its (row -> item -> feature offset) chain is loaded once,
+    // then every slot's id and table row are independent loads
+    for (long long P = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; P < total_rows;
+         P += static_cast<long long>(gridDim.x) * blockDim.x) {
         int s = 0;
-        while (s + 1 < n_src && static_cast<long long>(P) >= s_base[s + 1]) ++s;
-        const long long p = static_cast<long long>(P) - s_base[s];
+        while (s + 1 < n_src && P >= s_base[s + 1]) ++s;
+        const long long p = P - s_base[s];
         if (p >= s_cnt[s]) continue;
         const SourceInfo& si = s_src[s];
         const int nslots = si.nslot[0] + si.nslot[1] + si.nslot[2];
         T* orow = out + s_emb[s] + p * si.k_pad;
-        if (k == nslots) {  // zero padding columns
-            for (int c = si.k_in; c < si.k_pad; ++c) orow[c] = from_f32<T>(0.f);
-            continue;
-        }
-        if (k > nslots) continue;
-        const int row = __ldg(src_rows + P);
-        const int item = __ldg(row_item + row);
-        int id;
+        for (int c = si.k_in; c < si.k_pad; ++c) orow[c] = from_f32<T>(0.f);  // zero padding columns
+        const int item = __ldg(row_item + __ldg(src_rows + P));
+        const int* fb;
+        int nu = 0, nc = 0;
         if (si.kind < 2) {
-            id = __ldg(b.ev_feats + __ldg(b.ev_feat_off + item) + k);
+            fb = b.ev_feats + __ldg(b.ev_feat_off + item);
         } else {
-            const int nu = __ldg(b.exp_blk + 3 * item), nc = __ldg(b.exp_blk + 3 * item + 1);
-            const int off = k < si.nslot[0] ? k : (k < si.nslot[0] + si.nslot[1] ? nu + (k - si.nslot[0])
-                                                                                  : nu + nc + (k - si.nslot[0] - si.nslot[1]));
-            id = __ldg(b.exp_feats + __ldg(b.exp_feat_off + item) + off);
+            nu = __ldg(b.exp_blk + 3 * item);
+            nc = __ldg(b.exp_blk + 3 * item + 1);
+            fb = b.exp_feats + __ldg(b.exp_feat_off + item);
         }
-        const SlotInfo sl = slots[si.slot0 + k];
-        id = id < 0 ? 0 : (id >= sl.vocab ? sl.vocab - 1 : id);  // invalid ids were reported by the plan
-        const T* trow = tables + sl.emb_off + static_cast<long long>(id) * d_emb;
-        T* dst = orow + k * d_emb;
-        if (sizeof(T) * d_emb % 16 == 0) {
-            const uint4* s4 = reinterpret_cast<const uint4*>(trow);
-            uint4* d4 = reinterpret_cast<uint4*>(dst);
-            for (int c = 0; c < static_cast<int>(sizeof(T) * d_emb / 16); ++c) d4[c] = __ldg(s4 + c);
-        } else {
-            for (int c = 0; c < d_emb; ++c) dst[c] = trow[c];
+#pragma unroll 4
+        for (int k = 0; k < nslots; ++k) {
+            const int off = si.kind < 2 || k < si.nslot[0]
+                                ? k
+                                : (k < si.nslot[0] + si.nslot[1] ? nu + (k - si.nslot[0])
+                                                                 : nu + nc + (k - si.nslot[0] - si.nslot[1]));
+            int id = __ldg(fb + off);
+            const SlotInfo sl = sl_tab[si.slot0 + k];
+            id = id < 0 ? 0 : (id >= sl.vocab ? sl.vocab - 1 : id);  // invalid ids were reported by the plan
+            const T* trow = tables + sl.emb_off + static_cast<long long>(id) * d_emb;
+            T* dst = orow + k * d_emb;
+            if (sizeof(T) * d_emb % 16 == 0) {
+                const uint4* s4 = reinterpret_cast<const uint4*>(trow);
+                uint4* d4 = reinterpret_cast<uint4*>(dst);
+                for (int c = 0; c < static_cast<int>(sizeof(T) * d_emb / 16); ++c) d4[c] = __ldg(s4 + c);
+            } else {
+                for (int c = 0; c < d_emb; ++c) dst[c] = trow[c];
+            }
         }
     }
 }
@@ -489,11 +497,10 @@ bool launch_gather(const DevBatch& b, const SourceInfo* src_dev, const SlotInfo*
                    const T* tables, int d_emb, int n_src, long long total_rows, int max_slots, T* out,
                    cudaStream_t st) {
     if (total_rows == 0) return true;
-    const long long n = total_rows * (max_slots + 1);
-    if (n >= (1ll << 31) || n_src > 32) return false;  // the kernel indexes items in 32 bits
-    // one item per thread where possible: the dependent load chain per item
-    // (row -> item -> feature offset -> id -> table row) is latency-bound
-    const int blocks = static_cast<int>(std::min<long long>(cdiv(n, 256), 148ll * 64));
+    if (n_src > 32) return false;
+    // one source row per thread (the dependent load chain row -> item -> feature
+    // offset -> ids -> table rows is latency-bound): every row in flight at once
+    const int blocks = static_cast<int>(std::min<long long>(cdiv(total_rows, 256), 148ll * 64));
     launch_k(gather_kernel<T>, dim3(blocks), dim3(256), 0, st, b, src_dev, slots_dev, rm.src_rows, rm.item, src_base_dev, src_cnt_dev,
                                              emb_base_dev, tables, d_emb, n_src, total_rows, max_slots, out);
     return true;

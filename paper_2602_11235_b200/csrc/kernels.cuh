@@ -85,7 +85,7 @@ struct PlanArgs {
 void launch_plan(const PlanArgs& a, int smem_elems, cudaStream_t st);
 
 // Embedding gather into the per-source tokenizer input matrices.
-// false when the batch exceeds the kernel's 32-bit item indexing (nothing launched)
+// false when there are more than 32 token sources (nothing launched)
 template <typename T>
 bool launch_gather(const DevBatch& b, const SourceInfo* src_dev, const SlotInfo* slots_dev, const RowMeta& rm,
                    const long long* src_base_dev, const long long* src_cnt_dev, const long long* emb_base_dev,

@@ -1566,14 +1566,14 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
         tok_in += static_cast<double>(B.src_cnt[s]) * m.sources[s].k_pad;
     }
     {
-        if (tok_rows * (max_slots + 1) >= (1ll << 31) || n_src > 32)
-            fail(MTFM_CONTRACT_ERROR, "batch too large for one forward (tokens x slots >= 2^31)");
+        if (tok_rows >= (1ll << 31) || n_src > 32)
+            fail(MTFM_CONTRACT_ERROR, "batch too large for one forward (tokens >= 2^31 or > 32 token sources)");
         StageScope sc(m, "gather", 0, tok_in * el * 2);
         if (!launch_gather<T>(pa.b, pa.src, pa.slots, rm, B.d_src_base.as<long long>(), B.d_src_cnt.as<long long>(),
                               B.d_emb_base.as<long long>(),
                               kTc ? static_cast<const T*>(m.emb_bf16.p) : static_cast<const T*>(m.emb_f32.p),
                               m.cfg.d_emb, n_src, tok_rows, max_slots, E, st))
-            fail(MTFM_CONTRACT_ERROR, "batch too large for one forward (tokens x slots >= 2^31)");
+            fail(MTFM_CONTRACT_ERROR, "more than 32 token sources");
         ck(cudaGetLastError(), "gather launch");
         ++L;
     }
