@@ -21,7 +21,8 @@
 // warp 15 GEMM2 issuer. Two producer and two MMA threads: one thread issues
 // a TMA load only every ~150-300 clk (scripts/ubench_tma.cu), and the
 // per-chunk barrier waits of one MMA thread would serialise both GEMMs.
-// TMEM columns: Y [0, 256), Hacc [256, 384), Hb [384, 448).
+// TMEM columns: Y [0, 256), Hacc [256, 384), Hb [384, 512) (4 chunks: while the Y warps
+// drain a tile, GEMM1 and the SiLU warps prepare half of the next tile's hidden layer).
 // SMEM: 2 x tile stages (E tile 16 KB + b1 tile 16 KB + b2 tile 8 KB),
 // 3 x W1 chunk stages (8 KB), 3 x W2 chunk stages (32 KB), ones tile, Y / x̂ staging.
 #pragma once
@@ -73,6 +74,7 @@ constexpr int BAR_BYTES = 1024;
 constexpr int SMEM = 1024 + kXStages * XS_BYTES + kWStages * (W1_BYTES + W2_BYTES) + ONES_BYTES + STG_BYTES +
                      XCH_BYTES + BAR_BYTES;
 static_assert(SMEM <= 227 * 1024, "tok SMEM budget");
+constexpr int NHB = 4;  // Hb buffers: SiLU runs up to 4 chunks ahead of GEMM2 (through the Y drain)
 constexpr uint32_t Y_COL = 0, HACC_COL = 256, HB_COL = 384;
 
 __device__ __forceinline__ void decode(const TokArgs& a, int t, int& s, int& m0) {
@@ -101,13 +103,13 @@ __global__ void __launch_bounds__(kTokThreads, 1) tok_fused_kernel(const __grid_
     uint64_t* w1_empty = bars + 7;       // [3]
     uint64_t* hacc_full = bars + 10;     // [2]
     uint64_t* hacc_empty = bars + 12;    // [2]
-    uint64_t* hb_full = bars + 14;       // [2]
-    uint64_t* hb_empty = bars + 16;      // [2]
-    uint64_t* y_full = bars + 18;
-    uint64_t* y_empty = bars + 19;
-    uint64_t* w2_full = bars + 20;       // [3]
-    uint64_t* w2_empty = bars + 23;      // [3]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 26);
+    uint64_t* hb_full = bars + 14;       // [NHB]
+    uint64_t* hb_empty = bars + 18;      // [NHB]
+    uint64_t* y_full = bars + 22;
+    uint64_t* y_empty = bars + 23;
+    uint64_t* w2_full = bars + 24;       // [3]
+    uint64_t* w2_empty = bars + 27;      // [3]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 30);
 
     const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
     constexpr uint32_t kWarpMma = 15, kWarpTma = 14, kWarpTmaW2 = 13, kWarpAlloc = 12;
@@ -121,6 +123,8 @@ __global__ void __launch_bounds__(kTokThreads, 1) tok_fused_kernel(const __grid_
             ptx::mbar_init(&x_empty[i], 2);  // GEMM1 warp (E, b1) + GEMM2 warp (b2)
             ptx::mbar_init(&hacc_full[i], 1);
             ptx::mbar_init(&hacc_empty[i], 4);
+        }
+        for (int i = 0; i < NHB; ++i) {
             ptx::mbar_init(&hb_full[i], 4);
             ptx::mbar_init(&hb_empty[i], 1);
         }
@@ -314,8 +318,8 @@ __global__ void __launch_bounds__(kTokThreads, 1) tok_fused_kernel(const __grid_
             ptx::mbar_wait(&x_full[xb], (n_t >> 1) & 1);         // b2 tile
             ptx::mbar_wait(y_empty, (n_t & 1) ^ 1);              // the previous tile's Y has been read out
             for (int c = 0; c < NCH; ++c, ++h) {
-                const uint32_t hb = h & 1, wb = h % kWStages;
-                ptx::mbar_wait(&hb_full[hb], (h >> 1) & 1);
+                const uint32_t hb = h % NHB, wb = h % kWStages;
+                ptx::mbar_wait(&hb_full[hb], (h / NHB) & 1);
                 ptx::mbar_wait(&w2_full[wb], (h / kWStages) & 1);
                 ptx::tc_fence_after();
                 if (ptx::elect_one()) {
@@ -394,16 +398,18 @@ __global__ void __launch_bounds__(kTokThreads, 1) tok_fused_kernel(const __grid_
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&hacc_empty[g]);
-                // Hb[g] must have been consumed by GEMM2 of this group's previous chunk
-                ptx::mbar_wait(&hb_empty[g], (k & 1) ^ 1);
+                // this group's Hb buffers alternate g, g + 2 (chunk c -> c % NHB); the buffer must
+                // have been consumed by GEMM2 of the chunk NHB before
+                const uint32_t hbb = g + 2 * (k & 1);
+                ptx::mbar_wait(&hb_empty[hbb], ((k >> 1) & 1) ^ 1);
                 ptx::tc_fence_after();
-                ptx::tmem_st16(tmem + lane_addr + HB_COL + g * (HC / 2), *reinterpret_cast<uint32_t(*)[16]>(packed));
-                ptx::tmem_st16(tmem + lane_addr + HB_COL + g * (HC / 2) + 16,
+                ptx::tmem_st16(tmem + lane_addr + HB_COL + hbb * (HC / 2), *reinterpret_cast<uint32_t(*)[16]>(packed));
+                ptx::tmem_st16(tmem + lane_addr + HB_COL + hbb * (HC / 2) + 16,
                                *reinterpret_cast<uint32_t(*)[16]>(packed + 16));
                 ptx::tmem_st_wait();
                 ptx::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&hb_full[g]);
+                if (lane == 0) ptx::mbar_arrive(&hb_full[hbb]);
             }
         }
     } else if (warp < 12 || warp >= 16) {
