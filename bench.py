@@ -42,7 +42,7 @@ REF_SRC = os.path.join(ROOT, "baseline", "_ref", "proj")
 # BASELINE.json configs (paper_2602_11235_b200/datagen.py WORKLOADS): small is
 # configs[1] (the 1-GPU headline), base configs[2] (heavy-tailed lengths),
 # large configs[3] (per-GPU shard), paper the north_star's paper-scale shape.
-CONFIGS = ("small", "base", "large", "paper")
+CONFIGS = ("small", "base", "large", "paper", "sweep")
 
 
 def cpu_model():
@@ -189,7 +189,7 @@ def workload_inputs(args):
     """The N=1 batch of the config (the GPU arm's rank-0 input at N=1) and its weights."""
     from paper_2602_11235_b200 import datagen
     from paper_2602_11235_b200.schema import param_specs
-    wl = datagen.WORKLOADS[args.config]()
+    wl = datagen.with_mix(datagen.WORKLOADS[args.config](), args.mix, args.mha)
     batch = datagen.generate(wl, n_users=args.users or wl.n_users)
     specs = param_specs(wl.schemas, wl.cfg)
     params = datagen.random_params(specs, seed=7)
@@ -252,6 +252,8 @@ def main():
     ap.add_argument("--ref-users", type=int, default=96)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-json", default=None)
+    ap.add_argument("--mix", default=None, help='HTA mix "K:P" (target:full layers per block), default the config\'s')
+    ap.add_argument("--mha", action="store_true", help="kv_heads = heads (no GQA), the reference bench's G=H arm")
     ap.add_argument("--prune", action="store_true",
                     help="2:4-prune f1/fuq/fkv/f2 (prune_projections) before timing: the pruned model")
     ap.add_argument("--sparse-mode", type=int, default=2, choices=[0, 1, 2],
@@ -272,7 +274,7 @@ def main():
     from paper_2602_11235_b200 import Model, abi, datagen
     from paper_2602_11235_b200.schema import BATCH_KEYS, batch_nbytes
 
-    wl = datagen.WORKLOADS[args.config]()
+    wl = datagen.with_mix(datagen.WORKLOADS[args.config](), args.mix, args.mha)
     per_gpu = args.users or wl.n_users
     if world == 1:
         batch = datagen.generate(wl, n_users=per_gpu)

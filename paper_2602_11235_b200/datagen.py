@@ -60,7 +60,26 @@ WORKLOADS = {
                              ("lognormal", 16, 0.8, 1, 64), 11),
     "large": lambda: Workload("large", _model(1024, 4, 3, 1, 16, 4), make_schemas(), 1024, 896, 256, 32, 5),
     "paper": lambda: Workload("paper", _model(768, 4, 3, 1, 3, 1), make_schemas(), 256, 896, 256, 32, 7),
+    # multi-scenario aggregation sweep (BASELINE configs[4]): 4 scenarios with distinct token
+    # schemas, 1-256 targets per user (heavy-tailed), d=256 8Q/2KV; the HTA mix and G=H are
+    # varied by the caller (bench.py --mix / --mha)
+    "sweep": lambda: Workload("sweep", _model(256, 1, 3, 1, 8, 2), make_schemas(), 1024,
+                              ("lognormal", 160, 0.8, 8, 448), ("lognormal", 48, 0.8, 2, 128),
+                              ("lognormal", 24, 1.0, 1, 256), 13),
 }
+
+
+def with_mix(wl: Workload, mix=None, mha=False) -> Workload:
+    """The workload with another HTA mix "K:P" and/or G = H (multi-head instead of GQA):
+    the reference's bench matrix (bench.hpp:40-57) over a BASELINE workload."""
+    import dataclasses
+    hta = wl.cfg.hta
+    if mix:
+        k, p = (int(x) for x in mix.split(":"))
+        hta = dataclasses.replace(hta, target_layers=k, full_layers=p)
+    if mha:
+        hta = dataclasses.replace(hta, kv_heads=hta.heads)
+    return dataclasses.replace(wl, cfg=dataclasses.replace(wl.cfg, hta=hta))
 
 
 def _draw_len(rng, spec, n):
