@@ -6,7 +6,7 @@ import sys
 
 d = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out"
 rows = []
-for f in sorted(glob.glob(os.path.join(d, "sweep_*.json"))):
+for f in sorted(glob.glob(os.path.join(d, "sweep_[0-9]*.json"))):
     try:
         line = json.loads(open(f).read().strip().splitlines()[-1])
     except Exception:
