@@ -56,6 +56,7 @@ struct AttnParams {
     long long ldkv;
     __nv_bfloat16* out;          // A rows indexed like Q rows
     long long ldo;
+    int tma_box_kv, tma_chunk;   // host check: the boxes tma_q / tma_kv were built with
 };
 
 namespace attn_detail {

@@ -1123,6 +1123,8 @@ AttnGeom attn_geom(const mtfm_cuda_model& m) {
 template <int D>
 void launch_attn_tc_d(const AttnParams& p, cudaStream_t st) {
     using C = attn_detail::Cfg<D>;
+    // the tensor maps' boxes must be the kernel's K/V tile and swizzle row
+    if (p.tma_box_kv != C::BKV || p.tma_chunk != C::CHUNK) fail(MTFM_CONTRACT_ERROR, "attention tile config mismatch");
     static bool attr = false;
     if (!attr) {
         ck(cudaFuncSetAttribute(attn_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM),
@@ -1139,7 +1141,9 @@ void run_attn_tc(const mtfm_cuda_model& m, AttnParams p, const __nv_bfloat16* q,
     if (p.n_tiles == 0) return;
     const int D = m.dh;
     const int chunk = std::min(D, 64);
-    const int bkv = D <= 128 ? 128 : 64;
+    const int bkv = D <= 64 ? 128 : 64;  // attn_detail::Cfg<D>::BKV
+    p.tma_box_kv = bkv;
+    p.tma_chunk = chunk;
     p.tma_q = tma_2d(q, n_q, q_cols, p.ldq, chunk, p.rt, chunk * 2);
     p.tma_kv = tma_2d(p.kv_ptr, kv_rows, kv_cols, p.ldkv, chunk, bkv, chunk * 2);
     switch (D) {

@@ -59,3 +59,14 @@ def test_targets_per_user(per_scen):
 @pytest.mark.parametrize("norm", ["valid", "seqlen", "none"])
 def test_attn_norm(norm):
     _run(_wl(1, 1, norm=norm), 3, "bf16")
+
+
+@pytest.mark.parametrize("d,H,G", [(256, 4, 2), (256, 2, 1), (512, 4, 4), (128, 8, 2)])
+def test_head_dims(d, H, G):
+    """Every bf16 attention specialisation (head_dim 64, 128, 128 with MHA, 16) against the
+    oracle; head_dim 32 and 256 are the small / paper goldens."""
+    wl = datagen.WORKLOADS["small"]()
+    hta = dataclasses.replace(wl.cfg.hta, d_model=d, heads=H, kv_heads=G, target_layers=1, full_layers=1)
+    cfg = dataclasses.replace(wl.cfg, hta=hta, d_expert=d)
+    wl = dataclasses.replace(wl, cfg=cfg, hist_len=150, rt_len=40, exp_per_scen=3)
+    _run(wl, 4, "bf16")
