@@ -83,6 +83,11 @@ struct Cfg {
     static constexpr uint32_t O_COL = NB * BKV;
     static constexpr int OB = (NB * BKV + 2 * D <= 512) ? 2 : 1;  // O buffers
     static constexpr int kSilu = 16;                        // SiLU warps (4 per TMEM lane quarter)
+    // two groups of 8 SiLU warps take alternate key tiles (a group's warps split a tile's
+    // columns in halves), so one group's SiLUs run while the other's loads, stores and
+    // barrier hand-offs are in flight
+    static constexpr int kSiluGroups = 2;
+    static constexpr int CW = BKV / (kSilu / kSiluGroups / 4);  // key columns per SiLU warp and key tile
     static constexpr int kThreads = (4 + kSilu + 4) * 32;   // + TMA/MMA/alloc/spare + 4 epilogue warps
     static_assert(O_COL + OB * D <= 512, "TMEM budget");
     static_assert(SMEM <= 227 * 1024, "SMEM budget");
@@ -155,7 +160,7 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
         for (int i = 0; i < NB; ++i) {
             ptx::mbar_init(&s_full[i], 1);
             ptx::mbar_init(&s_empty[i], 1);
-            ptx::mbar_init(&p_full[i], C::kSilu);
+            ptx::mbar_init(&p_full[i], C::kSilu / C::kSiluGroups);
         }
         for (int i = 0; i < C::kStages; ++i) {
             ptx::mbar_init(&kv_full[i], 1);
@@ -290,7 +295,7 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
                     for (int kk = 0; kk < BKV / 16; ++kk) {
                         // keys [16kk, 16kk+16) were packed by the SiLU warp owning
                         // S columns [CW*c, CW*(c+1)), c = 16kk / CW, into its first CW/2
-                        constexpr int CW = BKV / 4;
+                        constexpr int CW = C::CW;
                         const uint32_t p_col = buf * BKV + ((16 * kk) / CW) * CW + ((16 * kk) % CW) / 2;
                         const uint64_t db = ptx::smem_desc(sv + kk * 16 * C::ROWB, BKV * C::ROWB, 8 * C::ROWB, C::LAYOUT);
                         ptx::umma_bf16_ts(o_tmem, tmem + p_col, db, idesc_o, (j > 0 || kk > 0));
@@ -305,9 +310,11 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
         }
     } else if (warp >= 4 && warp < 4 + C::kSilu) {
         // ------------------------------------------------ SiLU warps, P aliasing S
-        constexpr int CW = BKV / 4;               // key columns per warp and key tile
+        constexpr int CW = C::CW;                 // key columns per warp and key tile
+        constexpr int NQ = CW / 16;               // 16-key chunks per warp
         const uint32_t q = warp & 3;              // TMEM lane quarter
-        const uint32_t cq = (warp - 4) >> 2;      // column quarter
+        const uint32_t grp = (warp - 4) / (C::kSilu / C::kSiluGroups);  // key tiles s_cnt % 2 == grp
+        const uint32_t cq = ((warp - 4) >> 2) % (BKV / CW);             // column part
         const uint32_t m = q * 32 + lane;         // MMA row == TMEM lane
         const uint32_t lane_addr = (q * 32u) << 16;
         // (announcing P(j) only after issuing the S load of tile j+1 measured 3-5% slower)
@@ -319,56 +326,30 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
             const int i = m - hs * prm.rt;
             const int prefix = i < tile.n_rows ? __ldg(prm.q_prefix + tile.q_row0 + i) : 0;
             for (int j = 0; j < n_kv; ++j, ++s_cnt) {
+                if (s_cnt % C::kSiluGroups != grp) continue;
                 const uint32_t buf = s_cnt % NB;
                 ptx::mbar_wait(&s_full[buf], (s_cnt / NB) & 1);
                 ptx::tc_fence_after();
                 const uint32_t col = buf * BKV + cq * CW;
                 const int nvalid = prefix - (j * BKV + static_cast<int>(cq) * CW);  // >= CW: no masking
-                if constexpr (CW == 32) {
-                    // two halves of 16 keys: the second half's TMEM load and the first half's
-                    // P store are in flight while the other half's SiLUs run
-                    uint32_t pa[8], pb[8];
-                    if (__all_sync(0xffffffffu, nvalid <= 0)) {
-#pragma unroll
-                        for (int e = 0; e < 8; ++e) pa[e] = pb[e] = 0u;
-                        ptx::tmem_st8(tmem + lane_addr + col, pa);
-                    } else {
-                        float va[16], vb[16];
-                        ptx::tmem_ld16(tmem + lane_addr + col, va);
-                        ptx::tmem_ld_wait_dep(va);
-                        ptx::tmem_ld16(tmem + lane_addr + col + 16, vb);
-                        attn_detail::silu_half(va, pa, nvalid, 0);
-                        ptx::tmem_st8(tmem + lane_addr + col, pa);
-                        ptx::tmem_ld_wait_dep(vb);
-                        attn_detail::silu_half(vb, pb, nvalid, 16);
-                    }
-                    ptx::tmem_st8(tmem + lane_addr + col + 8, pb);
-                } else {
-                uint32_t pk[CW / 2];
+                // 16-key chunks: the next chunk's TMEM load and this chunk's P store are in
+                // flight while its SiLUs run; P (packed bf16) overwrites the S columns already read
                 if (__all_sync(0xffffffffu, nvalid <= 0)) {
+                    const uint32_t z[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
 #pragma unroll
-                    for (int e = 0; e < CW / 2; ++e) pk[e] = 0u;
+                    for (int c = 0; c < NQ; ++c) ptx::tmem_st8(tmem + lane_addr + col + 8 * c, z);
                 } else {
-                    float v[CW];
+                    float v[2][16];
+                    ptx::tmem_ld16(tmem + lane_addr + col, v[0]);
+                    ptx::tmem_ld_wait_dep(v[0]);
 #pragma unroll
-                    for (int k = 0; k < CW / 16; ++k)
-                        ptx::tmem_ld16(tmem + lane_addr + col + k * 16, *reinterpret_cast<float(*)[16]>(v + k * 16));
-                    ptx::tmem_ld_wait();
-                    if (__all_sync(0xffffffffu, nvalid >= CW)) {
-#pragma unroll
-                        for (int e = 0; e < CW; e += 2)
-                            pk[e / 2] = attn_detail::silu2_bf16(v[e], v[e + 1]);
-                    } else {
-#pragma unroll
-                        for (int e = 0; e < CW; e += 2) {
-                            const uint32_t w = attn_detail::silu2_bf16(v[e], v[e + 1]);
-                            const uint32_t keep = (e + 1 < nvalid) ? 0xffffffffu : (e < nvalid ? 0x0000ffffu : 0u);
-                            pk[e / 2] = w & keep;
-                        }
+                    for (int c = 0; c < NQ; ++c) {
+                        if (c + 1 < NQ) ptx::tmem_ld16(tmem + lane_addr + col + 16 * (c + 1), v[(c + 1) & 1]);
+                        uint32_t pk[8];
+                        attn_detail::silu_half(v[c & 1], pk, nvalid, 16 * c);
+                        ptx::tmem_st8(tmem + lane_addr + col + 8 * c, pk);
+                        if (c + 1 < NQ) ptx::tmem_ld_wait_dep(v[(c + 1) & 1]);
                     }
-                }
-                if constexpr (CW / 2 == 16) ptx::tmem_st16(tmem + lane_addr + col, pk);
-                else ptx::tmem_st8(tmem + lane_addr + col, *reinterpret_cast<const uint32_t(*)[8]>(pk));
                 }
                 ptx::tmem_st_wait();
                 ptx::tc_fence_before();
