@@ -29,6 +29,7 @@
 #include "common.cuh"
 #include "gemm_sp.cuh"
 #include "gemm_tc.cuh"
+#include "heads_tc.cuh"
 #include "kernels.cuh"
 #include "tok_tc.cuh"
 #include "train_kernels.cuh"
@@ -2030,6 +2031,60 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
             StageScope sc(m, "to_bf16", 0, Td * d * 6);
             launch_to_bf16(X + NE * d, NT, d, XN, d, st);
             ++L;
+        }
+        // fused heads (heads_tc.cuh): the head GEMM's expert columns are reduced to the
+        // per-task logits in its epilogue instead of round-tripping [T][E*de] through HBM
+        int max_nt = 0;
+        for (const auto& sc : m.sources)
+            if (sc.kind == 2) max_nt = std::max(max_nt, sc.ntasks);
+        const int E = m.cfg.experts, dx = m.cfg.d_expert;
+        const int ng_pad = static_cast<int>(round_up(static_cast<long long>(m.n_tasks_total) * E, 16));
+        const size_t hsmem = 1024 + heads_detail::kStages * heads_detail::STAGE_BYTES +
+                             static_cast<size_t>(E * dx + m.n_tasks_total * (dx + 4)) * 4 + heads_detail::XZ_BYTES + 128;
+        if (E <= kHeadsMaxE && max_nt <= kHeadsMaxTasks && dx % heads_detail::CH == 0 && d % 64 == 0 &&
+            ng_pad <= 256 && hsmem <= 227 * 1024) {
+            HeadsTcArgs ha{};
+            ha.tma_x = tma_2d(XN, NT, d, d, 64, 128, 128);
+            ha.tma_w = tma_2d(m.head_t.p, m.head_n, d, d, 64, 128, 128);
+            ha.n_t = static_cast<int>(NT);
+            ha.d = d;
+            ha.E = E;
+            ha.de = dx;
+            ha.n_gate = m.n_tasks_total * E;
+            ha.n_tasks_total = m.n_tasks_total;
+            ha.exp_bias = m.head_eb.as<float>();
+            ha.gate_bias = m.head_gb.as<float>();
+            ha.tower_w = m.tower_w.as<float>();
+            ha.tower_b = m.tower_b.as<float>();
+            ha.src = m.d_src.as<SourceInfo>();
+            ha.n_src = n_src;
+            ha.t_scen = rm.t_scen;
+            ha.t_user = rm.t_user;
+            ha.t_exp_ref = rm.t_exp_ref;
+            ha.t_rec0 = rm.t_rec0;
+            ha.t_rec_stride = rm.t_rec_stride;
+            ha.user_id = B.user_id.as<long long>();
+            ha.rec_user = B.rec_user.as<long long>();
+            ha.rec_scen = B.rec_scen.as<int>();
+            ha.rec_exp = B.rec_exp.as<int>();
+            ha.rec_task = B.rec_task.as<int>();
+            ha.rec_logit = B.rec_logit.as<float>();
+            ha.rec_prob = B.rec_prob.as<double>();
+            StageScope sc(m, "heads", hflops + 2.0 * B.n_records * m.cfg.d_expert, Td * d * 2 + B.n_records * 32.0);
+            if (NT > 0) {
+                static size_t attr = 0;
+                if (hsmem > attr) {
+                    ck(cudaFuncSetAttribute(heads_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(hsmem)),
+                       "heads smem attr");
+                    attr = hsmem;
+                }
+                launch_k(heads_tc_kernel, dim3(static_cast<int>(std::min<long long>(cdiv(NT, 128), kNumSMs))),
+                         dim3(heads_detail::kThreads), hsmem, st, ha);
+                ck(cudaGetLastError(), "heads_tc launch");
+                ++L;
+            }
+            return;
         }
         StageScope sc(m, "heads_gemm", hflops, Td * d * 2 + Td * m.head_n * 4);
         run_gemm_tc({{XN, d, m.head_t.as<__nv_bfloat16>(), d, static_cast<int>(NT), m.head_n, d, EPI_BIAS_F32, nullptr,
