@@ -15,7 +15,7 @@
 // [T][E*de + n_tasks*E] fp32 round trip through HBM and the separate heads pass.
 //
 // Roles (608 threads): warps 0..15 epilogue, warp 16 TMEM allocator, warp 17 TMA
-// producer (A k-block + chunk weight k-block per stage), warp 18 MMA issuer.
+// producer (the tile's X once, then the chunks' weight k-blocks), warp 18 MMA issuer.
 #pragma once
 
 #include "common.cuh"
@@ -33,6 +33,7 @@ struct HeadsTcArgs {
     int n_t, d, E, de;
     int n_gate;             // n_tasks_total * E gate columns, after the E * de expert columns
     int n_tasks_total;
+    int n_wstages;          // weight k-block stages (SMEM left after the resident X tile)
     const float* exp_bias;  // [E * de]
     const float* gate_bias; // [n_tasks_total * E]
     const float* tower_w;   // [n_tasks_total][de]
@@ -55,10 +56,9 @@ struct HeadsTcArgs {
 
 namespace heads_detail {
 constexpr int BM = 128, BK = 64, CH = 128;        // rows, k-block, expert chunk columns
-constexpr int A_BYTES = BM * BK * 2;              // 16 KB
-constexpr int W_BYTES = 256 * BK * 2;             // up to 256 weight rows (the gate block)
-constexpr int STAGE_BYTES = A_BYTES + W_BYTES;    // 48 KB
-constexpr int kStages = 3;
+constexpr int A_BYTES = BM * BK * 2;              // 16 KB per k-block of the resident X tile
+constexpr int W_BYTES = CH * BK * 2;              // 16 KB: 128 weight rows (a chunk, or the gate block) x 64 k
+constexpr int kMaxWStages = 12;
 constexpr int kEpiGroups = 4;                     // epilogue groups: each takes 32 columns of every chunk
 constexpr int kEpiWarps = 4 * kEpiGroups;
 constexpr int kThreads = 32 * (kEpiWarps + 3);
@@ -66,25 +66,33 @@ constexpr int XZ_BYTES = 2 * kEpiGroups * BM * 4 * 4;  // per-group partial logi
 constexpr uint32_t ACC_COL = 0, GATE_COL = 2 * CH;  // two expert-chunk buffers, then the gate block
 }  // namespace heads_detail
 
-// smem_tables: exp_bias [E*de], tower_w [n_tasks_total*de] (fp32), after the stages
+// SMEM: the X tile (d/64 k-blocks, loaded once per tile), n_wstages weight k-blocks,
+// exp_bias [E*de] and tower_w [n_tasks_total][de + 4] (fp32), partial logits, barriers
 __global__ void __launch_bounds__(heads_detail::kThreads, 1) heads_tc_kernel(const __grid_constant__ HeadsTcArgs a) {
     using namespace heads_detail;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    float* s_eb = reinterpret_cast<float*>(base + kStages * STAGE_BYTES);
+    const int n_kb = a.d / BK;
+    const int n_ws = a.n_wstages;
+    uint8_t* sA = base;
+    uint8_t* sW = base + n_kb * A_BYTES;
+    float* s_eb = reinterpret_cast<float*>(sW + n_ws * W_BYTES);
     float* s_tw = s_eb + a.E * a.de;               // rows padded to de + 4 (rows of different tasks in other banks)
     const int tw_ld = a.de + 4;
     float* s_xz = s_tw + a.n_tasks_total * tw_ld;  // [2][group][row][task] partial logits
-    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(s_xz) + XZ_BYTES);
-    uint64_t* full = bars;                   // [kStages]
-    uint64_t* empty = bars + kStages;        // [kStages]
-    uint64_t* acc_full = bars + 2 * kStages;   // [3]: expert buffers 0, 1, gate block
-    uint64_t* acc_empty = acc_full + 3;        // [3]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 3);
+    float* s_gate = s_xz + XZ_BYTES / 4;          // [BM][ng_pad + 1] gate logits of the tile
+    uint64_t* bars = reinterpret_cast<uint64_t*>(
+        (reinterpret_cast<uintptr_t>(s_gate + BM * (((a.n_gate + 15) & ~15) + 1)) + 15) & ~uintptr_t(15));
+    uint64_t* full = bars;                   // [kMaxWStages]
+    uint64_t* empty = bars + kMaxWStages;    // [kMaxWStages]
+    uint64_t* acc_full = bars + 2 * kMaxWStages;  // [3]: expert buffers 0, 1, gate block
+    uint64_t* acc_empty = acc_full + 3;           // [3]
+    uint64_t* a_full = acc_empty + 3;
+    uint64_t* a_empty = a_full + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_empty + 1);
 
     const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
     constexpr uint32_t kWarpAlloc = kEpiWarps, kWarpTma = kEpiWarps + 1, kWarpMma = kEpiWarps + 2;
-    const int n_kb = a.d / BK;
     const int sub = a.de / CH;                         // chunks per expert
     const int n_chunks = 1 + a.E * sub;                // gate block first
     const int ng_pad = (a.n_gate + 15) & ~15;
@@ -94,13 +102,15 @@ __global__ void __launch_bounds__(heads_detail::kThreads, 1) heads_tc_kernel(con
     for (int i = threadIdx.x; i < a.n_tasks_total * a.de; i += blockDim.x)
         s_tw[(i / a.de) * tw_ld + i % a.de] = a.tower_w[i];
     if (warp == kWarpTma && lane == 0) {
-        for (int i = 0; i < kStages; ++i) {
+        for (int i = 0; i < n_ws; ++i) {
             ptx::mbar_init(&full[i], 1);
             ptx::mbar_init(&empty[i], 1);
         }
+        ptx::mbar_init(a_full, 1);
+        ptx::mbar_init(a_empty, 1);
         for (int i = 0; i < 3; ++i) {
             ptx::mbar_init(&acc_full[i], 1);
-            ptx::mbar_init(&acc_empty[i], kEpiWarps);
+            ptx::mbar_init(&acc_empty[i], i == 2 ? 4 : kEpiWarps);  // the gate block is read by group 0
         }
         ptx::fence_mbar_init();
         ptx::tma_prefetch(&a.tma_x);
@@ -115,28 +125,28 @@ __global__ void __launch_bounds__(heads_detail::kThreads, 1) heads_tc_kernel(con
 
     if (warp == kWarpTma) {
         if (ptx::elect_one()) {
-            uint32_t it = 0;
-            for (int t = blockIdx.x; t < n_tiles; t += gridDim.x)
+            uint32_t it = 0, n_t = 0;
+            for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++n_t) {
+                // the X tile: every k-block once per tile (after the previous tile's last MMA)
+                ptx::mbar_wait(a_empty, (n_t & 1) ^ 1);
+                ptx::mbar_arrive_expect_tx(a_full, n_kb * A_BYTES);
+                for (int kb = 0; kb < n_kb; ++kb) ptx::tma_load_2d(sA + kb * A_BYTES, &a.tma_x, a_full, kb * BK, t * BM);
                 for (int c = 0; c < n_chunks; ++c) {
-                    // chunk c: weight rows [r0, r0 + nw)
+                    // chunk c: weight rows [r0, r0 + 128) (the gate block: E*de .. + ng_pad)
                     const int r0 = c == 0 ? a.E * a.de : (c - 1) * CH;
-                    const int nw = c == 0 ? ng_pad : CH;
                     for (int kb = 0; kb < n_kb; ++kb, ++it) {
-                        const uint32_t s = it % kStages;
-                        ptx::mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
-                        uint8_t* st = base + s * STAGE_BYTES;
-                        const int nbox = (nw + 127) / 128;
-                        ptx::mbar_arrive_expect_tx(&full[s], A_BYTES + nbox * (128 * BK * 2));
-                        ptx::tma_load_2d(st, &a.tma_x, &full[s], kb * BK, t * BM);
-                        for (int bx = 0; bx < nbox; ++bx)
-                            ptx::tma_load_2d(st + A_BYTES + bx * (128 * BK * 2), &a.tma_w, &full[s], kb * BK,
-                                             r0 + bx * 128);
+                        const uint32_t s = it % n_ws;
+                        ptx::mbar_wait(&empty[s], ((it / n_ws) & 1) ^ 1);
+                        ptx::mbar_arrive_expect_tx(&full[s], W_BYTES);
+                        ptx::tma_load_2d(sW + s * W_BYTES, &a.tma_w, &full[s], kb * BK, r0);
                     }
                 }
+            }
         }
     } else if (warp == kWarpMma) {
-        uint32_t it = 0, n_exp = 0, n_gate = 0;
-        for (int t = blockIdx.x; t < n_tiles; t += gridDim.x)
+        uint32_t it = 0, n_exp = 0, n_gate = 0, n_t = 0;
+        for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++n_t) {
+            ptx::mbar_wait(a_full, n_t & 1);
             for (int c = 0; c < n_chunks; ++c) {
                 const bool gate = c == 0;
                 const int nw = gate ? ng_pad : CH;
@@ -147,24 +157,26 @@ __global__ void __launch_bounds__(heads_detail::kThreads, 1) heads_tc_kernel(con
                 const uint32_t idesc = ptx::instr_desc_bf16(BM, nw, false, false);
                 const uint32_t d_col = gate ? GATE_COL : ACC_COL + ab * CH;
                 for (int kb = 0; kb < n_kb; ++kb, ++it) {
-                    const uint32_t s = it % kStages;
-                    ptx::mbar_wait(&full[s], (it / kStages) & 1);
+                    const uint32_t s = it % n_ws;
+                    ptx::mbar_wait(&full[s], (it / n_ws) & 1);
                     ptx::tc_fence_after();
                     if (ptx::elect_one()) {
-                        const uint32_t sa = ptx::smem_u32(base + s * STAGE_BYTES);
-                        const uint32_t sw = sa + A_BYTES;
+                        const uint32_t sa = ptx::smem_u32(sA + kb * A_BYTES);
+                        const uint32_t sw = ptx::smem_u32(sW + s * W_BYTES);
 #pragma unroll
                         for (int k = 0; k < BK / 16; ++k)
                             ptx::umma_bf16(tmem + d_col, ptx::smem_desc(sa + k * 32, 16, 1024, 2),
                                            ptx::smem_desc(sw + k * 32, 16, 1024, 2), idesc, (kb > 0 || k > 0) ? 1u : 0u);
                         ptx::umma_commit(&empty[s]);
                         if (kb == n_kb - 1) ptx::umma_commit(&acc_full[ab]);
+                        if (kb == n_kb - 1 && c == n_chunks - 1) ptx::umma_commit(a_empty);
                     }
                     __syncwarp();
                 }
                 if (gate) ++n_gate;
                 else ++n_exp;
             }
+        }
     } else if (warp < kEpiWarps) {
         // epilogue: lane = row of the tile; group gq reduces columns [32 gq, 32 gq + 32) of
         // every expert chunk, the groups' partial logits are summed through SMEM
@@ -192,28 +204,32 @@ __global__ void __launch_bounds__(heads_detail::kThreads, 1) heads_tc_kernel(con
             for (int k = 0; k < kHeadsMaxTasks; ++k)
 #pragma unroll
                 for (int e = 0; e < kHeadsMaxE; ++e) g[k][e] = 0.f;
-            ptx::mbar_wait(&acc_full[2], n_gate & 1);
-            ++n_gate;
-            ptx::tc_fence_after();
-            for (int c0 = 0; c0 < ng_pad; c0 += 16) {
-                float v[16];
-                ptx::tmem_ld16(tmem + lane_addr + GATE_COL + c0, v);
-                ptx::tmem_ld_wait();
+            // group 0 stages the tile's gate block (+ bias) in SMEM ([row][ng_pad + 1]); every
+            // thread then reads its row's task window by index
+            const int gl = ng_pad + 1;
+            const int rl = static_cast<int>(q * 32 + lane);
+            if (gq == 0) {
+                ptx::mbar_wait(&acc_full[2], n_gate & 1);
+                ptx::tc_fence_after();
+                for (int c0 = 0; c0 < ng_pad; c0 += 16) {
+                    float v[16];
+                    ptx::tmem_ld16(tmem + lane_addr + GATE_COL + c0, v);
+                    ptx::tmem_ld_wait();
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const int col = c0 + i;
-                    const int task = col / a.E, e = col - task * a.E;
-                    const int k = task - task0;
-#pragma unroll
-                    for (int kk = 0; kk < kHeadsMaxTasks; ++kk)
-#pragma unroll
-                        for (int ee = 0; ee < kHeadsMaxE; ++ee)
-                            if (kk == k && ee == e && col < a.n_gate) g[kk][ee] = v[i] + __ldg(a.gate_bias + col);
+                    for (int i = 0; i < 16; ++i)
+                        s_gate[rl * gl + c0 + i] = c0 + i < a.n_gate ? v[i] + __ldg(a.gate_bias + c0 + i) : 0.f;
                 }
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&acc_empty[2]);
             }
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&acc_empty[2]);
+            ++n_gate;
+            ptx::named_bar_sync(2, kEpiWarps * 32);
+#pragma unroll
+            for (int k = 0; k < kHeadsMaxTasks; ++k)
+#pragma unroll
+                for (int e = 0; e < kHeadsMaxE; ++e)
+                    g[k][e] = (k < ntasks && e < a.E) ? s_gate[rl * gl + (task0 + k) * a.E + e] : 0.f;
 #pragma unroll
             for (int k = 0; k < kHeadsMaxTasks; ++k) {
                 float mx = -INFINITY;
@@ -284,7 +300,6 @@ __global__ void __launch_bounds__(heads_detail::kThreads, 1) heads_tc_kernel(con
             }
             // ---- the groups' partial logits -> group 0 (fixed order g0 + g1 + g2 + g3)
             float* xz = s_xz + (n_gate & 1) * (kEpiGroups * BM * 4);
-            const int rl = static_cast<int>(q * 32 + lane);
 #pragma unroll
             for (int k = 0; k < kHeadsMaxTasks; ++k) xz[(gq * BM + rl) * 4 + k] = z[k];
             ptx::named_bar_sync(1, kEpiWarps * 32);

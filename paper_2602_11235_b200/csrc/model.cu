@@ -2039,10 +2039,16 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
             if (sc.kind == 2) max_nt = std::max(max_nt, sc.ntasks);
         const int E = m.cfg.experts, dx = m.cfg.d_expert;
         const int ng_pad = static_cast<int>(round_up(static_cast<long long>(m.n_tasks_total) * E, 16));
-        const size_t hsmem = 1024 + heads_detail::kStages * heads_detail::STAGE_BYTES +
-                             static_cast<size_t>(E * dx + m.n_tasks_total * (dx + 4)) * 4 + heads_detail::XZ_BYTES + 128;
+        // SMEM: resident X tile (d/64 x 16 KB), weight stages, tables, partial logits, barriers
+        const size_t fixed = 1024 + static_cast<size_t>(d / 64) * heads_detail::A_BYTES +
+                             static_cast<size_t>(E * dx + m.n_tasks_total * (dx + 4)) * 4 + heads_detail::XZ_BYTES +
+                             static_cast<size_t>(heads_detail::BM * (ng_pad + 1) + 4) * 4 + 512;
+        const int n_ws = fixed < 227 * 1024 ? static_cast<int>(std::min<size_t>(
+                                                  (227 * 1024 - fixed) / heads_detail::W_BYTES, heads_detail::kMaxWStages))
+                                            : 0;
+        const size_t hsmem = fixed + static_cast<size_t>(n_ws) * heads_detail::W_BYTES;
         if (E <= kHeadsMaxE && max_nt <= kHeadsMaxTasks && dx % heads_detail::CH == 0 && d % 64 == 0 &&
-            ng_pad <= 256 && hsmem <= 227 * 1024) {
+            ng_pad <= heads_detail::CH && n_ws >= 3) {
             HeadsTcArgs ha{};
             ha.tma_x = tma_2d(XN, NT, d, d, 64, 128, 128);
             ha.tma_w = tma_2d(m.head_t.p, m.head_n, d, d, 64, 128, 128);
@@ -2052,6 +2058,7 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
             ha.de = dx;
             ha.n_gate = m.n_tasks_total * E;
             ha.n_tasks_total = m.n_tasks_total;
+            ha.n_wstages = n_ws;
             ha.exp_bias = m.head_eb.as<float>();
             ha.gate_bias = m.head_gb.as<float>();
             ha.tower_w = m.tower_w.as<float>();
