@@ -14,8 +14,9 @@
 // per-task dots act_e . tw_k on the fly. This replaces the head GEMM's
 // [T][E*de + n_tasks*E] fp32 round trip through HBM and the separate heads pass.
 //
-// Roles (608 threads): warps 0..15 epilogue, warp 16 TMEM allocator, warp 17 TMA
-// producer (the tile's X once, then the chunks' weight k-blocks), warp 18 MMA issuer.
+// Roles (608 threads): warps 0..15 epilogue (which also convert the tile's fp32 X rows
+// to the bf16 A operand in SMEM), warp 16 TMEM allocator, warp 17 TMA producer (the
+// chunks' weight k-blocks), warp 18 MMA issuer.
 #pragma once
 
 #include "common.cuh"
@@ -28,7 +29,8 @@ constexpr int kHeadsMaxTasks = 4;   // tasks per scenario
 constexpr int kHeadsMaxE = 4;       // experts (E <= 4: the gate weights live in registers)
 
 struct HeadsTcArgs {
-    CUtensorMap tma_x;      // X_T [n_t][d] bf16, box {64, 128}, SW128
+    const float* x;         // X_T [n_t][ldx] fp32 (the residual stream's T rows), converted to bf16 in SMEM
+    long long ldx;
     CUtensorMap tma_w;      // head weights K-major [head_n][d] bf16, box {64, 128}, SW128
     int n_t, d, E, de;
     int n_gate;             // n_tasks_total * E gate columns, after the E * de expert columns
@@ -106,14 +108,13 @@ __global__ void __launch_bounds__(heads_detail::kThreads, 1) heads_tc_kernel(con
             ptx::mbar_init(&full[i], 1);
             ptx::mbar_init(&empty[i], 1);
         }
-        ptx::mbar_init(a_full, 1);
+        ptx::mbar_init(a_full, kEpiWarps);  // the epilogue warps convert the X tile
         ptx::mbar_init(a_empty, 1);
         for (int i = 0; i < 3; ++i) {
             ptx::mbar_init(&acc_full[i], 1);
             ptx::mbar_init(&acc_empty[i], i == 2 ? 4 : kEpiWarps);  // the gate block is read by group 0
         }
         ptx::fence_mbar_init();
-        ptx::tma_prefetch(&a.tma_x);
         ptx::tma_prefetch(&a.tma_w);
     }
     if (warp == kWarpAlloc) ptx::tmem_alloc<512>(tmem_slot);
@@ -127,10 +128,6 @@ __global__ void __launch_bounds__(heads_detail::kThreads, 1) heads_tc_kernel(con
         if (ptx::elect_one()) {
             uint32_t it = 0, n_t = 0;
             for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++n_t) {
-                // the X tile: every k-block once per tile (after the previous tile's last MMA)
-                ptx::mbar_wait(a_empty, (n_t & 1) ^ 1);
-                ptx::mbar_arrive_expect_tx(a_full, n_kb * A_BYTES);
-                for (int kb = 0; kb < n_kb; ++kb) ptx::tma_load_2d(sA + kb * A_BYTES, &a.tma_x, a_full, kb * BK, t * BM);
                 for (int c = 0; c < n_chunks; ++c) {
                     // chunk c: weight rows [r0, r0 + 128) (the gate block: E*de .. + ng_pad)
                     const int r0 = c == 0 ? a.E * a.de : (c - 1) * CH;
@@ -181,11 +178,36 @@ __global__ void __launch_bounds__(heads_detail::kThreads, 1) heads_tc_kernel(con
         // epilogue: lane = row of the tile; group gq reduces columns [32 gq, 32 gq + 32) of
         // every expert chunk, the groups' partial logits are summed through SMEM
         const uint32_t q = warp & 3, gq = warp >> 2;
+        uint32_t n_xt = 0;
         const uint32_t lane_addr = (q * 32u) << 16;
         uint32_t n_exp = 0, n_gate = 0;
         for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
             const long long row = static_cast<long long>(t) * BM + q * 32 + lane;
             const bool valid = row < a.n_t;
+            // the tile's X rows (fp32 residual stream) -> bf16 in the K-major SW128 layout of the
+            // MMA's A operand: 16-byte chunk c of row r of k-block kb at kb*16K + r*128 + ((c ^ r%8) << 4)
+            {
+                ptx::mbar_wait(a_empty, (n_xt & 1) ^ 1);  // the previous tile's MMAs are done with it
+                const int cpr = a.d / 8;                   // 8-element chunks per row
+                for (int i = static_cast<int>(threadIdx.x); i < BM * cpr; i += kEpiWarps * 32) {
+                    const int r = i / cpr, cc = i - r * cpr;
+                    const long long xr = static_cast<long long>(t) * BM + r;
+                    float4 lo = make_float4(0.f, 0.f, 0.f, 0.f), hi = lo;
+                    if (xr < a.n_t) {
+                        const float4* src = reinterpret_cast<const float4*>(a.x + xr * a.ldx + cc * 8);
+                        lo = __ldg(src);
+                        hi = __ldg(src + 1);
+                    }
+                    const int kb = cc >> 3, c = cc & 7;
+                    ptx::sts128(ptx::smem_u32(sA) + kb * A_BYTES + r * 128 + ((c ^ (r & 7)) << 4),
+                                __uint_as_float(pack_bf16(lo.x, lo.y)), __uint_as_float(pack_bf16(lo.z, lo.w)),
+                                __uint_as_float(pack_bf16(hi.x, hi.y)), __uint_as_float(pack_bf16(hi.z, hi.w)));
+                }
+                ptx::fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(a_full);
+                ++n_xt;
+            }
             // the row's scenario: task window [task0, task0 + ntasks)
             int task0 = 0, ntasks = 0, scen = 0;
             if (valid) {

@@ -2027,11 +2027,6 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
     // the GEMM also evaluates the other scenarios' gate columns, which are not counted
     const double hflops = 2.0 * (Td * m.cfg.experts * d * m.cfg.d_expert + static_cast<double>(B.n_records) * d * m.cfg.experts);
     if constexpr (kTc) {
-        {
-            StageScope sc(m, "to_bf16", 0, Td * d * 6);
-            launch_to_bf16(X + NE * d, NT, d, XN, d, st);
-            ++L;
-        }
         // fused heads (heads_tc.cuh): the head GEMM's expert columns are reduced to the
         // per-task logits in its epilogue instead of round-tripping [T][E*de] through HBM
         int max_nt = 0;
@@ -2050,7 +2045,8 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
         if (E <= kHeadsMaxE && max_nt <= kHeadsMaxTasks && dx % heads_detail::CH == 0 && d % 64 == 0 &&
             ng_pad <= heads_detail::CH && n_ws >= 3) {
             HeadsTcArgs ha{};
-            ha.tma_x = tma_2d(XN, NT, d, d, 64, 128, 128);
+            ha.x = X + NE * d;
+            ha.ldx = d;
             ha.tma_w = tma_2d(m.head_t.p, m.head_n, d, d, 64, 128, 128);
             ha.n_t = static_cast<int>(NT);
             ha.d = d;
@@ -2077,7 +2073,7 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
             ha.rec_task = B.rec_task.as<int>();
             ha.rec_logit = B.rec_logit.as<float>();
             ha.rec_prob = B.rec_prob.as<double>();
-            StageScope sc(m, "heads", hflops + 2.0 * B.n_records * m.cfg.d_expert, Td * d * 2 + B.n_records * 32.0);
+            StageScope sc(m, "heads", hflops + 2.0 * B.n_records * m.cfg.d_expert, Td * d * 4 + B.n_records * 32.0);
             if (NT > 0) {
                 static size_t attr = 0;
                 if (hsmem > attr) {
@@ -2092,6 +2088,11 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                 ++L;
             }
             return;
+        }
+        {
+            StageScope sc(m, "to_bf16", 0, Td * d * 6);
+            launch_to_bf16(X + NE * d, NT, d, XN, d, st);
+            ++L;
         }
         StageScope sc(m, "heads_gemm", hflops, Td * d * 2 + Td * m.head_n * 4);
         run_gemm_tc({{XN, d, m.head_t.as<__nv_bfloat16>(), d, static_cast<int>(NT), m.head_n, d, EPI_BIAS_F32, nullptr,
