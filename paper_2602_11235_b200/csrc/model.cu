@@ -378,6 +378,7 @@ struct mtfm_cuda_model {
     int subgraph = -1;
     // 2:4 sparse tensor-core projections: 0 off, 1 required, 2 when the weights are 2:4
     int sparse_mode = 2;
+    int max_run = 1;  // longest run of consecutive target layers (sizes the K|V buffer)
     std::vector<size_t> visible;  // registered parameters in registration order
     bool finalized = false;
     int n_ctx_src = 0;  // leading sources of kind hist/rt (context rows) when they precede every scenario source
@@ -680,6 +681,15 @@ void finalize(mtfm_cuda_model& m) {
             upload(L->g2b, g2b, st);
             m.layers.push_back(std::move(L));
         }
+    // longest run of consecutive target layers: the K|V buffer holds one layer of each
+    // (with no full layers a run spans blocks)
+    m.max_run = 1;
+    for (size_t li = 0; li < m.layers.size();) {
+        size_t lj = li;
+        while (lj < m.layers.size() && m.layers[lj]->target) ++lj;
+        m.max_run = std::max(m.max_run, static_cast<int>(lj - li));
+        li = lj == li ? li + 1 : lj;
+    }
     // pruned projections (prune.hpp:83-90) run on the sparse tensor cores
     if (m.sparse_mode != 0) {
         const bool ok = projections_2_4(m);
@@ -1417,7 +1427,7 @@ void prepare(mtfm_cuda_model& m, const mtfm_packed_batch* hb, int only_scenario,
     need(ACT_X, R * m.d, 4);
     // bf16 path: [0, R) xhat of the context rows (source order) then the T rows' GLN1,
     // [R, 2R) a full layer's GLN1 rows; K|V rows per target layer of a run
-    const long long kt = std::max(1, m.cfg.target_layers);
+    const long long kt = std::max(1, m.max_run);
     need(ACT_XN, 2 * R * m.d, el);
     need(ACT_P, R * pw, el);
     need(ACT_KV, kt * R * 2 * m.gd, el);
