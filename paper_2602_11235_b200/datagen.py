@@ -156,7 +156,7 @@ def generate(wl: Workload, n_users=None) -> dict:
         idx = exp_feat_off[:-1][m]
         for j, v in enumerate(s.user_feature_vocabs + s.cross_feature_vocabs + s.item_feature_vocabs):
             efeats[idx + j] = rng.integers(0, v, int(m.sum()))
-    seq_off = np.arange(0, U * (nh + nr) + 1, nh + nr, dtype=np.int32)
+    seq_off = (np.arange(U + 1, dtype=np.int32) * (nh + nr)).astype(np.int32)
     exp_off = np.zeros(U + 1, np.int64)
     np.cumsum(exp_per_user, out=exp_off[1:])
     return dict(user_id=np.arange(U, dtype=np.int64), seq_off=seq_off, seq_kind=seq_kind,

@@ -70,3 +70,15 @@ def test_head_dims(d, H, G):
     cfg = dataclasses.replace(wl.cfg, hta=hta, d_expert=d)
     wl = dataclasses.replace(wl, cfg=cfg, hist_len=150, rt_len=40, exp_per_scen=3)
     _run(wl, 4, "bf16")
+
+
+@pytest.mark.parametrize("n_hist,n_rt,n_scen", [(1, 0, 4), (0, 1, 2), (3, 2, 1), (2, 1, 6), (0, 0, 3)])
+def test_schema_shapes(n_hist, n_rt, n_scen):
+    """Token-source layouts other than the BASELINE one (2 H + 1 R sequences, 4 scenarios):
+    no realtime or no historical sequence, no context at all (targets attend to themselves),
+    more sequences, one or six scenarios."""
+    wl = datagen.WORKLOADS["small"]()
+    wl = dataclasses.replace(wl, schemas=datagen.make_schemas(n_scenarios=n_scen, n_hist=n_hist, n_rt=n_rt),
+                             hist_len=50, rt_len=15, exp_per_scen=3)
+    for precision in ("bf16", "fp32"):
+        _run(wl, 5, precision)
