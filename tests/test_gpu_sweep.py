@@ -42,7 +42,7 @@ def _wl(K, P, blocks=1, norm="valid", **kw):
 
 
 @pytest.mark.parametrize("precision", ["bf16", "fp32"])
-@pytest.mark.parametrize("K,P,blocks", [(0, 1, 2), (1, 1, 1), (3, 1, 2), (5, 1, 1), (3, 0, 1), (3, 0, 2), (2, 0, 3)])
+@pytest.mark.parametrize("K,P,blocks", [(0, 1, 2), (1, 1, 1), (3, 1, 2), (5, 1, 1), (3, 0, 1), (3, 0, 2), (2, 0, 3), (1, 2, 2), (0, 3, 1), (2, 2, 1)])
 def test_layer_mix(K, P, blocks, precision):
     """Target-layer runs longer than one multi-copy GLN launch (5:1), runs with
     no full layer after them (3:0), full-only stacks (0:1) and repeated blocks."""
