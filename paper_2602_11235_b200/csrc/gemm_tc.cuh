@@ -130,6 +130,13 @@ struct TileSeq {
         t += tstep;
         return true;
     }
+    // advance past one tile without decoding it; false at the end of the sequence
+    __device__ __forceinline__ bool skip() {
+        if (b_res) return i++ < mcount;
+        const bool more = t < n_tiles;
+        t += tstep;
+        return more;
+    }
 };
 
 }  // namespace gemm_detail
@@ -354,8 +361,11 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
         for (int b = 0; b < C::kAcc; ++b)
             if (b % n_groups == group) release(b);
         int pi, mb, nb;
-        for (int j = 0; seq.next(pi, mb, nb); ++j) {
-            if (j % n_groups != group) continue;
+        // this group's tiles are j = group, group + n_groups, ... (the others only skipped)
+        bool more = true;
+        for (int g = 0; g < group && more; ++g) more = seq.skip();
+        for (int j = group; more && seq.next(pi, mb, nb); j += n_groups) {
+            for (int g = 1; g < n_groups && more; ++g) more = seq.skip();
             acc = j % C::kAcc;
             acc_phase = (j / C::kAcc) & 1;
             const GemmProblem& p = args.p[pi];
