@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
     // critical single-thread roles sit at the top: 15 MMA issuer, 14 TMA
     // producer, 13 TMEM allocator; epilogue warps 0..n_epi-1 (warp & 3 = TMEM
     // lane quarter).
-    constexpr uint32_t kWarpMma = 15, kWarpTma = 14, kWarpAlloc = 13;
+    constexpr uint32_t kWarpMma = 15, kWarpTma = 14, kWarpAlloc = 13, kWarpTma2 = 12;
 
     if (warp == kWarpTma && lane == 0) {
         for (int s = 0; s < n_stages; ++s) {
@@ -211,10 +211,14 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
     // prologue done (barriers, TMEM, SMEM tables): wait for the producer of our inputs
     MTFM_PDL_ENTRY();
 
-    if (warp == kWarpTma) {
-        // ------------------------------------------------ TMA producer (A and B)
+    if (warp == kWarpTma || warp == kWarpTma2) {
+        // ------------------------------------------------ TMA producers (A and B)
+        // two issuing warps take alternate stages: one thread issues a TMA load only every
+        // few hundred clocks (scripts/ubench_l2.cu: 8 TB/s aggregate L2 -> SMEM with one
+        // issuer per SM, 16 TB/s with two)
+        const int prod = warp == kWarpTma ? 0 : 1;
         if (ptx::elect_one()) {
-            if (args.b_res && args.cta[blockIdx.x].mcount > 0) {
+            if (prod == 0 && args.b_res && args.cta[blockIdx.x].mcount > 0) {
                 // resident weight slice: every k-block of this CTA's (problem, n-block), once
                 const CtaWork& w = args.cta[blockIdx.x];
                 const GemmProblem& p = args.p[w.pi];
@@ -226,13 +230,21 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
             }
             int stage = 0;
             uint32_t phase = 0;
+            uint32_t it = 0;  // stage iterations (producer prod issues it % 2 == prod)
             gemm_detail::TileSeq seq(args, s_tile_start, s_tiles_n);
             int pi, mb, nb;
             while (seq.next(pi, mb, nb)) {
                 const GemmProblem& p = args.p[pi];
                 const int kblocks = s_kblocks[pi];
                 const bool p_bias = s_has_bias[pi];
-                for (int kb = 0; kb < kblocks; kb += KS) {
+                for (int kb = 0; kb < kblocks; kb += KS, ++it) {
+                    if ((it & 1) != prod) {
+                        if (++stage == n_stages) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
+                        continue;
+                    }
                     ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
                     uint8_t* sa = smem + stage * stage_bytes;
                     uint8_t* sb = sa + KS * C::A_BYTES;
