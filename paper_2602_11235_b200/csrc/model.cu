@@ -1607,7 +1607,10 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
         TokArgs ta{};
         std::vector<int> fused_src;
         double fused_f = 0, fused_in = 0, p_f1 = 0, p_f2 = 0, p_in = 0, p_rows = 0;
-        if (d == 256) {
+        if (d % 256 == 0) {
+            ta.n_pass = d / 256;
+            ta.nch = 2 * d / 64;
+            ta.ldx = d;
             for (int s = 0; s < n_src && ta.n_src < kTokMaxSrc; ++s) {
                 const auto& si = m.sources[s];
                 const int M = static_cast<int>(B.src_cnt[s]);
@@ -1617,14 +1620,14 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
                 ts.tma_e = tma_2d(E + B.emb_base[s], M, si.k_pad, si.k_pad, 64, 128, 128);
                 ts.tma_w1 = tma_2d(w.t1.p, 2 * d, si.k_pad, si.k_pad, 64, 64, 128);
                 ts.tma_w2 = tma_2d(w.t2.p, d, 2 * d, 2 * d, 64, 256, 128);
-                ts.tma_b1 = tma_2d(BT.get(w.b1.as<float>(), 2 * d, st), 2 * d, 16, 16, 16, 256, 32);
+                ts.tma_b1 = tma_2d(BT.get(w.b1.as<float>(), 2 * d, st), 2 * d, 16, 16, 16, 64, 32);
                 ts.tma_b2 = tma_2d(BT.get(w.b2.as<float>(), d, st), d, 16, 16, 16, 256, 32);
                 ts.row_map = rm.src_rows + B.src_base[s];
                 ts.M = M;
                 ts.k_steps = static_cast<int>(cdiv(si.k_pad, 16));
-                ts.tile_start = ta.n_tiles;
-                ts.xhat_row0 = s < m.n_ctx_src ? B.src_base[s] : -1;
-                ta.n_tiles += static_cast<int>(cdiv(M, 128));
+                ts.tile_start = ta.n_tiles / ta.n_pass;  // in tiles (work items are tiles x passes)
+                ts.xhat_row0 = s < m.n_ctx_src && d == 256 ? B.src_base[s] : -1;  // x̂ needs whole rows: one pass
+                ta.n_tiles += static_cast<int>(cdiv(M, 128)) * ta.n_pass;
                 fused_src.push_back(s);
                 fused_f += 2.0 * M * (si.k_in * 2.0 * d + 2.0 * d * d);
                 fused_in += static_cast<double>(M) * si.k_pad;
@@ -1636,6 +1639,7 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
         for (int s = 0; s < m.n_ctx_src; ++s)
             if (B.src_cnt[s] > 0 && std::find(fused_src.begin(), fused_src.end(), s) == fused_src.end())
                 xhat_from_tok = false;
+        if (d != 256) xhat_from_tok = false;
         if (!xhat_from_tok)
             for (int i = 0; i < ta.n_src; ++i) ta.s[i].xhat_row0 = -1;
         for (int s = 0; s < n_src; ++s) {

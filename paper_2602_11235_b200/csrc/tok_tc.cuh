@@ -1,30 +1,32 @@
-// tok_tc.cuh — fused tokenizer MLP on tcgen05 (sm_100a), d_model = 256.
+// tok_tc.cuh — fused tokenizer MLP on tcgen05 (sm_100a), d_model a multiple of 256.
 //
 //   X[row_map[m]] = silu(E[m] W1 + b1) W2 + b2        (tokenizer.hpp:136-149)
 //
 // for every sequence source whose embedding concat fits one 64-wide k-block
-// (k_pad <= 64). The 512-wide hidden layer never leaves the SM: per 128-row
-// tile it is produced in 8 chunks of 64 columns,
+// (k_pad <= 64). The 2d-wide hidden layer never leaves the SM: per 128-row
+// tile and 256-column output pass it is produced in 2d/64 chunks of 64 columns,
 //
 //   GEMM1_c : Hacc[c%2] (TMEM fp32, 128 x 64)  = E_tile . W1[64c:64c+64]^T + b1_c
-//   SiLU    : Hb[c%2]   (TMEM bf16, 128 x 64)  = silu(Hacc[c%2])
-//   GEMM2_c : Y         (TMEM fp32, 128 x 256) += Hb[c%2] . W2[:, 64c:64c+64]^T   (A from TMEM)
+//   SiLU    : Hb[c%4]   (TMEM bf16, 128 x 64)  = silu(Hacc[c%2])
+//   GEMM2_c : Y         (TMEM fp32, 128 x 256) += Hb[c%4] . W2[n0:n0+256, 64c:64c+64]^T   (A from TMEM)
 //
-// and Y (+ b2 through the ones-tile MMA) is scattered to the X rows. Versus
-// the two-GEMM path this removes the 2 x (rows x 512 x 2 B) hidden-layer round
-// trip through HBM.
+// and Y (+ b2 through the ones-tile MMA) is scattered to columns [n0, n0 + 256)
+// of the X rows. Versus the two-GEMM path this removes the 2 x (rows x 2d x 2 B)
+// hidden-layer round trip through HBM; for d > 256 every pass recomputes the
+// hidden layer (Y is half of TMEM, so only 256 output columns fit), and x̂ (which
+// needs whole rows) comes from the separate GLN pass.
 //
 // Roles (640 threads): warps 0..7 SiLU (two groups of 4, group g owns Hacc[g] /
-// Hb[g], i.e. chunks c = g mod 2), warps 8..11 and 16..19 Y epilogue (column
-// halves), warp 12 TMEM
-// allocator + GEMM1 issuer, warp 13 W2 producer, warp 14 tile + W1 producer,
-// warp 15 GEMM2 issuer. Two producer and two MMA threads: one thread issues
-// a TMA load only every ~150-300 clk (scripts/ubench_tma.cu), and the
-// per-chunk barrier waits of one MMA thread would serialise both GEMMs.
+// Hb[g], Hb[g + 2], i.e. chunks c = g mod 2), warps 8..11 and 16..19 Y epilogue
+// (column halves), warp 12 TMEM allocator + GEMM1 issuer, warp 13 W2 producer,
+// warp 14 tile + W1/b1 producer, warp 15 GEMM2 issuer. Two producer and two MMA
+// threads: one thread issues a TMA load only every ~150-300 clk
+// (scripts/ubench_tma.cu), and the per-chunk barrier waits of one MMA thread
+// would serialise both GEMMs.
 // TMEM columns: Y [0, 256), Hacc [256, 384), Hb [384, 512) (4 chunks: while the Y warps
 // drain a tile, GEMM1 and the SiLU warps prepare half of the next tile's hidden layer).
-// SMEM: 2 x tile stages (E tile 16 KB + b1 tile 16 KB + b2 tile 8 KB),
-// 3 x W1 chunk stages (8 KB), 3 x W2 chunk stages (32 KB), ones tile, Y / x̂ staging.
+// SMEM: 2 x tile stages (E tile 16 KB + the pass's b2 rows 8 KB), 3 x W1 chunk stages
+// (8 KB + the chunk's b1 rows 2 KB), 3 x W2 chunk stages (32 KB), ones tile, Y / x̂ staging.
 #pragma once
 
 #include "common.cuh"
@@ -37,10 +39,10 @@ constexpr int kTokThreads = 640;
 
 struct TokSource {
     CUtensorMap tma_e;    // E_s [M][k_pad] bf16, box {64, 128}, SW128 (columns >= k_pad zero-filled)
-    CUtensorMap tma_w1;   // W1^T [512][k_pad] bf16, box {64, 64}, SW128
-    CUtensorMap tma_w2;   // W2^T [256][512] bf16, box {64, 256}, SW128
-    CUtensorMap tma_b1;   // b1 tile [512][16] bf16, box {16, 256}, SW32
-    CUtensorMap tma_b2;   // b2 tile [256][16] bf16, box {16, 256}, SW32
+    CUtensorMap tma_w1;   // W1^T [2d][k_pad] bf16, box {64, 64}, SW128
+    CUtensorMap tma_w2;   // W2^T [d][2d] bf16, box {64, 256}, SW128
+    CUtensorMap tma_b1;   // b1 tile [2d][16] bf16, box {16, 64}, SW32 (one hidden chunk's rows)
+    CUtensorMap tma_b2;   // b2 tile [d][16] bf16, box {16, 256}, SW32 (one output pass's rows)
     const int* row_map;   // X row of source row m
     int M;                // rows
     int k_steps;          // ceil(k_pad / 16)
@@ -51,19 +53,23 @@ struct TokSource {
 struct TokArgs {
     TokSource s[kTokMaxSrc];
     int n_src;
-    int n_tiles;
-    float* X;             // [rows][256] fp32
+    int n_tiles;          // work items: 128-row tiles x output passes
+    int n_pass;           // d_model / 256: output column passes (each recomputes the hidden layer)
+    int nch;              // hidden chunks: 2 d_model / 64
+    int ldx;              // d_model
+    float* X;             // [rows][d_model] fp32
     __nv_bfloat16* xhat;  // [rows][256] bf16, source order: the first target run's normalised context rows
     float eps;
 };
 
 namespace tok_detail {
-constexpr int BM = 128, D = 256, HC = 64, NCH = 8;  // rows per tile, d_model, hidden chunk, chunks
+constexpr int BM = 128, D = 256, HC = 64;          // rows per tile, output columns per pass, hidden chunk
 constexpr int E_BYTES = BM * 64 * 2;                // 16 KB
-constexpr int B1_BYTES = 2 * D * 32;                // 16 KB: b1 tile [512][16]
-constexpr int B2_BYTES = D * 32;                    // 8 KB
-constexpr int XS_BYTES = E_BYTES + B1_BYTES + B2_BYTES;  // tile stage
+constexpr int B2_BYTES = D * 32;                    // 8 KB: the pass's b2 rows [256][16]
+constexpr int XS_BYTES = E_BYTES + B2_BYTES;        // tile stage
 constexpr int W1_BYTES = HC * 64 * 2;               // 8 KB
+constexpr int B1C_BYTES = HC * 32;                  // 2 KB: the chunk's b1 rows [64][16]
+constexpr int W1S_BYTES = W1_BYTES + B1C_BYTES;     // W1 stage (multiple of 1 KB: SW128 alignment)
 constexpr int W2_BYTES = D * 64 * 2;                // 32 KB
 constexpr int kXStages = 2, kWStages = 3;
 constexpr int ONES_BYTES = 4096;
@@ -71,18 +77,21 @@ constexpr int ONES_BYTES = 4096;
 constexpr int STG_BYTES = 8 * 2048;
 constexpr int XCH_BYTES = 2 * 128 * 8;
 constexpr int BAR_BYTES = 1024;
-constexpr int SMEM = 1024 + kXStages * XS_BYTES + kWStages * (W1_BYTES + W2_BYTES) + ONES_BYTES + STG_BYTES +
+constexpr int SMEM = 1024 + kXStages * XS_BYTES + kWStages * (W1S_BYTES + W2_BYTES) + ONES_BYTES + STG_BYTES +
                      XCH_BYTES + BAR_BYTES;
 static_assert(SMEM <= 227 * 1024, "tok SMEM budget");
 constexpr int NHB = 4;  // Hb buffers: SiLU runs up to 4 chunks ahead of GEMM2 (through the Y drain)
 constexpr uint32_t Y_COL = 0, HACC_COL = 256, HB_COL = 384;
 
-__device__ __forceinline__ void decode(const TokArgs& a, int t, int& s, int& m0) {
+// work item t -> source s, first row m0, first output column n_off
+__device__ __forceinline__ void decode(const TokArgs& a, int t, int& s, int& m0, int& n_off) {
+    const int tile = a.n_pass == 1 ? t : t / a.n_pass;
+    n_off = (t - tile * a.n_pass) * D;
     s = 0;
 #pragma unroll 1
     for (int i = 1; i < a.n_src; ++i)
-        if (t >= a.s[i].tile_start) s = i;
-    m0 = (t - a.s[s].tile_start) * BM;
+        if (tile >= a.s[i].tile_start) s = i;
+    m0 = (tile - a.s[s].tile_start) * BM;
 }
 }  // namespace tok_detail
 
@@ -92,7 +101,7 @@ __global__ void __launch_bounds__(kTokThreads, 1) tok_fused_kernel(const __grid_
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* xs = base;                                  // tile stages
     uint8_t* w1s = xs + kXStages * XS_BYTES;             // W1 chunk stages
-    uint8_t* w2s = w1s + kWStages * W1_BYTES;            // W2 chunk stages
+    uint8_t* w2s = w1s + kWStages * W1S_BYTES;           // W2 chunk stages
     uint8_t* ones = w2s + kWStages * W2_BYTES;
     float* stg = reinterpret_cast<float*>(ones + ONES_BYTES);
     float2* xch = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(stg) + STG_BYTES);
@@ -160,8 +169,8 @@ __global__ void __launch_bounds__(kTokThreads, 1) tok_fused_kernel(const __grid_
     // |mean| >> std does not cancel in E[y^2] - mean^2). Y is handed back to the
     // GEMM2 warp as soon as each warp's TMEM reads are done.
     auto drain = [&](uint32_t n_t, int t, uint32_t q, uint32_t grp) {
-        int s, m0;
-        tok_detail::decode(args, t, s, m0);
+        int s, m0, n_off;
+        tok_detail::decode(args, t, s, m0, n_off);
         const TokSource& src = args.s[s];
         const uint32_t slot = grp * 4 + q;
         const uint32_t wst = ptx::smem_u32(stg) + slot * 2048u;
@@ -212,7 +221,7 @@ __global__ void __launch_bounds__(kTokThreads, 1) tok_fused_kernel(const __grid_
                     const int r = 8 * i + (lane >> 2);
                     const float4 w = ptx::lds128(wst + r * 64 + ((c4 ^ ((r >> 1) & 3)) << 4));
                     if (orow[i] >= 0)
-                        __stcs(reinterpret_cast<float4*>(X + static_cast<long long>(orow[i]) * D + cb * 32 + hh * 16 +
+                        __stcs(reinterpret_cast<float4*>(X + static_cast<long long>(orow[i]) * args.ldx + n_off + cb * 32 + hh * 16 +
                                                          c4 * 4),
                                w);
                 }
@@ -272,22 +281,21 @@ __global__ void __launch_bounds__(kTokThreads, 1) tok_fused_kernel(const __grid_
         if (ptx::elect_one()) {
             uint32_t n_t = 0, n_w = 0;
             for (int t = blockIdx.x; t < args.n_tiles; t += gridDim.x, ++n_t) {
-                int s, m0;
-                decode(args, t, s, m0);
+                int s, m0, n_off;
+                decode(args, t, s, m0, n_off);
                 const TokSource& src = args.s[s];
                 const uint32_t xb = n_t & 1;
                 ptx::mbar_wait(&x_empty[xb], ((n_t >> 1) & 1) ^ 1);
                 uint8_t* xst = xs + xb * XS_BYTES;
                 ptx::mbar_arrive_expect_tx(&x_full[xb], XS_BYTES);
                 ptx::tma_load_2d(xst, &src.tma_e, &x_full[xb], 0, m0);
-                ptx::tma_load_2d(xst + E_BYTES, &src.tma_b1, &x_full[xb], 0, 0);
-                ptx::tma_load_2d(xst + E_BYTES + B1_BYTES / 2, &src.tma_b1, &x_full[xb], 0, 256);
-                ptx::tma_load_2d(xst + E_BYTES + B1_BYTES, &src.tma_b2, &x_full[xb], 0, 0);
-                for (int c = 0; c < NCH; ++c, ++n_w) {
+                ptx::tma_load_2d(xst + E_BYTES, &src.tma_b2, &x_full[xb], 0, n_off);
+                for (int c = 0; c < args.nch; ++c, ++n_w) {
                     const uint32_t wb = n_w % kWStages;
                     ptx::mbar_wait(&w1_empty[wb], ((n_w / kWStages) & 1) ^ 1);
-                    ptx::mbar_arrive_expect_tx(&w1_full[wb], W1_BYTES);
-                    ptx::tma_load_2d(w1s + wb * W1_BYTES, &src.tma_w1, &w1_full[wb], 0, c * HC);
+                    ptx::mbar_arrive_expect_tx(&w1_full[wb], W1S_BYTES);
+                    ptx::tma_load_2d(w1s + wb * W1S_BYTES, &src.tma_w1, &w1_full[wb], 0, c * HC);
+                    ptx::tma_load_2d(w1s + wb * W1S_BYTES + W1_BYTES, &src.tma_b1, &w1_full[wb], 0, c * HC);
                 }
             }
         }
@@ -296,14 +304,14 @@ __global__ void __launch_bounds__(kTokThreads, 1) tok_fused_kernel(const __grid_
         if (ptx::elect_one()) {
             uint32_t n_w = 0;
             for (int t = blockIdx.x; t < args.n_tiles; t += gridDim.x) {
-                int s, m0;
-                decode(args, t, s, m0);
+                int s, m0, n_off;
+                decode(args, t, s, m0, n_off);
                 const TokSource& src = args.s[s];
-                for (int c = 0; c < NCH; ++c, ++n_w) {
+                for (int c = 0; c < args.nch; ++c, ++n_w) {
                     const uint32_t wb = n_w % kWStages;
                     ptx::mbar_wait(&w2_empty[wb], ((n_w / kWStages) & 1) ^ 1);
                     ptx::mbar_arrive_expect_tx(&w2_full[wb], W2_BYTES);
-                    ptx::tma_load_2d(w2s + wb * W2_BYTES, &src.tma_w2, &w2_full[wb], c * HC, 0);
+                    ptx::tma_load_2d(w2s + wb * W2_BYTES, &src.tma_w2, &w2_full[wb], c * HC, n_off);
                 }
             }
         }
@@ -317,7 +325,7 @@ __global__ void __launch_bounds__(kTokThreads, 1) tok_fused_kernel(const __grid_
             uint8_t* xst = xs + xb * XS_BYTES;
             ptx::mbar_wait(&x_full[xb], (n_t >> 1) & 1);         // b2 tile
             ptx::mbar_wait(y_empty, (n_t & 1) ^ 1);              // the previous tile's Y has been read out
-            for (int c = 0; c < NCH; ++c, ++h) {
+            for (int c = 0; c < args.nch; ++c, ++h) {
                 const uint32_t hb = h % NHB, wb = h % kWStages;
                 ptx::mbar_wait(&hb_full[hb], (h / NHB) & 1);
                 ptx::mbar_wait(&w2_full[wb], (h / kWStages) & 1);
@@ -328,12 +336,12 @@ __global__ void __launch_bounds__(kTokThreads, 1) tok_fused_kernel(const __grid_
                     for (int k = 0; k < HC / 16; ++k)
                         ptx::umma_bf16_ts(tmem + Y_COL, tmem + HB_COL + hb * (HC / 2) + k * 8,
                                           ptx::smem_desc(w2 + k * 32, 16, 1024, 2), idesc2, (c > 0 || k > 0) ? 1u : 0u);
-                    if (c == NCH - 1)
+                    if (c == args.nch - 1)
                         ptx::umma_bf16(tmem + Y_COL, ones_desc,
-                                       ptx::smem_desc(ptx::smem_u32(xst + E_BYTES + B1_BYTES), 16, 256, 6), idesc2, 1u);
+                                       ptx::smem_desc(ptx::smem_u32(xst + E_BYTES), 16, 256, 6), idesc2, 1u);
                     ptx::umma_commit(&hb_empty[hb]);
                     ptx::umma_commit(&w2_empty[wb]);
-                    if (c == NCH - 1) {
+                    if (c == args.nch - 1) {
                         ptx::umma_commit(&x_empty[xb]);  // b2 tile consumed (the GEMM1 warp releases E)
                         ptx::umma_commit(y_full);
                     }
@@ -349,28 +357,28 @@ __global__ void __launch_bounds__(kTokThreads, 1) tok_fused_kernel(const __grid_
         const uint64_t ones_desc = ptx::smem_desc(ptx::smem_u32(ones), 16, 256, 6);
         uint32_t n_t = 0, h = 0;
         for (int t = blockIdx.x; t < args.n_tiles; t += gridDim.x, ++n_t) {
-            int s, m0;
-            tok_detail::decode(args, t, s, m0);
+            int s, m0, n_off;
+            tok_detail::decode(args, t, s, m0, n_off);
             const int k_steps = args.s[s].k_steps;
             const uint32_t xb = n_t & 1;
             uint8_t* xst = xs + xb * XS_BYTES;
             ptx::mbar_wait(&x_full[xb], (n_t >> 1) & 1);
-            for (int c = 0; c < NCH; ++c, ++h) {
+            for (int c = 0; c < args.nch; ++c, ++h) {
                 const uint32_t wb = h % kWStages, hb = h & 1;
                 ptx::mbar_wait(&w1_full[wb], (h / kWStages) & 1);
                 ptx::mbar_wait(&hacc_empty[hb], ((h >> 1) & 1) ^ 1);
                 ptx::tc_fence_after();
                 if (ptx::elect_one()) {
-                    const uint32_t e = ptx::smem_u32(xst), w1 = ptx::smem_u32(w1s + wb * W1_BYTES);
+                    const uint32_t e = ptx::smem_u32(xst), w1 = ptx::smem_u32(w1s + wb * W1S_BYTES);
                     for (int k = 0; k < k_steps; ++k)
                         ptx::umma_bf16(tmem + HACC_COL + hb * HC, ptx::smem_desc(e + k * 32, 16, 1024, 2),
                                        ptx::smem_desc(w1 + k * 32, 16, 1024, 2), idesc1, k > 0 ? 1u : 0u);
-                    // + b1 rows [64c, 64c + 64) of the tile's b1 tile (SW32, 256 B per 8 rows)
+                    // + b1 rows [64c, 64c + 64), loaded with the W1 chunk (SW32, 256 B per 8 rows)
                     ptx::umma_bf16(tmem + HACC_COL + hb * HC, ones_desc,
-                                   ptx::smem_desc(ptx::smem_u32(xst + E_BYTES) + c * HC * 32, 16, 256, 6), idesc1, 1u);
+                                   ptx::smem_desc(ptx::smem_u32(w1s + wb * W1S_BYTES + W1_BYTES), 16, 256, 6), idesc1, 1u);
                     ptx::umma_commit(&hacc_full[hb]);
                     ptx::umma_commit(&w1_empty[wb]);
-                    if (c == NCH - 1) ptx::umma_commit(&x_empty[xb]);  // E and b1 tiles consumed
+                    if (c == args.nch - 1) ptx::umma_commit(&x_empty[xb]);  // E tile consumed
                 }
                 __syncwarp();
             }
@@ -382,7 +390,7 @@ __global__ void __launch_bounds__(kTokThreads, 1) tok_fused_kernel(const __grid_
         uint32_t k = 0;  // chunks of this group
         uint32_t n_t = 0;
         for (int t = blockIdx.x; t < args.n_tiles; t += gridDim.x, ++n_t) {
-            for (int c = g; c < NCH; c += 2, ++k) {
+            for (int c = g; c < args.nch; c += 2, ++k) {
                 ptx::mbar_wait(&hacc_full[g], k & 1);
                 ptx::tc_fence_after();
                 uint32_t packed[HC / 2];
