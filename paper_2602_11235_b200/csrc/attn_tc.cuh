@@ -318,15 +318,26 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
         const uint32_t m = q * 32 + lane;         // MMA row == TMEM lane
         const uint32_t lane_addr = (q * 32u) << 16;
         // (announcing P(j) only after issuing the S load of tile j+1 measured 3-5% slower)
-        uint32_t s_cnt = 0;
+        uint32_t s_base = 0;  // key tiles of the CTA's earlier tiles (the S/P ring position)
+        const int hs = m / prm.rt;
+        const int i = m - hs * prm.rt;
+        // the row's mask prefix of the next tile is loaded while this tile's keys are processed
+        auto prefix_of = [&](int tt) -> int {
+            if (tt >= prm.n_tiles) return 0;
+            const AttnTile tl = prm.tiles[tt];
+            return i < tl.n_rows ? __ldg(prm.q_prefix + tl.q_row0 + i) : 0;
+        };
+        int prefix_next = prefix_of(blockIdx.x);
         for (int t = blockIdx.x; t < prm.n_tiles; t += gridDim.x) {
             const AttnTile tile = prm.tiles[t];
             const int n_kv = (tile.kmax + BKV - 1) / BKV;
-            const int hs = m / prm.rt;
-            const int i = m - hs * prm.rt;
-            const int prefix = i < tile.n_rows ? __ldg(prm.q_prefix + tile.q_row0 + i) : 0;
-            for (int j = 0; j < n_kv; ++j, ++s_cnt) {
-                if (s_cnt % C::kSiluGroups != grp) continue;
+            const int prefix = prefix_next;
+            prefix_next = prefix_of(t + gridDim.x);
+            // this group's key tiles: s_cnt = s_base + j with s_cnt % kSiluGroups == grp
+            const int j0 = static_cast<int>((grp + C::kSiluGroups - s_base % C::kSiluGroups) % C::kSiluGroups);
+            const uint32_t s_next = s_base + n_kv;
+            for (int j = j0; j < n_kv; j += C::kSiluGroups) {
+                const uint32_t s_cnt = s_base + j;
                 const uint32_t buf = s_cnt % NB;
                 ptx::mbar_wait(&s_full[buf], (s_cnt / NB) & 1);
                 ptx::tc_fence_after();
@@ -356,6 +367,7 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&p_full[buf]);
             }
+            s_base = s_next;
         }
     } else if (warp >= 4 + C::kSilu) {
         // ------------------------------------------------ epilogue warps
