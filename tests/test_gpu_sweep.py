@@ -82,3 +82,34 @@ def test_schema_shapes(n_hist, n_rt, n_scen):
                              hist_len=50, rt_len=15, exp_per_scen=3)
     for precision in ("bf16", "fp32"):
         _run(wl, 5, precision)
+
+
+def _random_case(seed):
+    rng = np.random.default_rng(seed)
+    d = int(rng.choice([128, 256, 512]))
+    dh = int(rng.choice([16, 32, 64, 128]))
+    dh = min(dh, d)
+    H = d // dh
+    G = int(rng.choice([g for g in (1, 2, 4, H) if H % g == 0]))
+    K, P = [(0, 1), (1, 1), (2, 1), (3, 0), (1, 2), (3, 1)][int(rng.integers(6))]
+    blocks = int(rng.integers(1, 3))
+    norm = str(rng.choice(["valid", "none", "seqlen"]))
+    wl = datagen.WORKLOADS["small"]()
+    hta = dataclasses.replace(wl.cfg.hta, d_model=d, heads=H, kv_heads=G, target_layers=K, full_layers=P,
+                              blocks=blocks, norm=norm)
+    cfg = dataclasses.replace(wl.cfg, hta=hta, d_expert=int(rng.choice([64, 128, d])), experts=int(rng.integers(2, 5)))
+    schemas = datagen.make_schemas(n_scenarios=int(rng.integers(1, 5)), n_hist=int(rng.integers(0, 3)),
+                                   n_rt=int(rng.integers(0, 2)))
+    return dataclasses.replace(wl, cfg=cfg, schemas=schemas, seed=seed,
+                               hist_len=("lognormal", 40, 1.0, 0, 300), rt_len=("lognormal", 10, 1.0, 0, 80),
+                               exp_per_scen=("lognormal", 4, 1.0, 1, 24))
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_configs(seed):
+    """Seeded random model geometries (d, head_dim, GQA ratio, layer mix, blocks, row
+    norm, experts, d_expert) and token-source layouts with heavy-tailed ragged users,
+    in bf16 and fp32 check mode, against the oracle."""
+    wl = _random_case(seed)
+    for precision in ("bf16", "fp32"):
+        _run(wl, 6, precision)
