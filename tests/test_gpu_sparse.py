@@ -62,3 +62,26 @@ def test_sparse_matches_dense_and_oracle(name, users):
     print(f"{name}: sparse vs dense max |dz| {d_sd:.3e}; vs oracle: sparse {d_sp:.3e}, dense {d_de:.3e}")
     assert d_sd <= 1e-2
     assert d_sp <= 2e-2 and d_sp <= 2 * d_de + 5e-3
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_sparse_random_geometries(seed):
+    """Seeded random geometries (tests/test_gpu_sweep.py::_random_case): the pruned model on
+    the sparse tensor cores against the dense path on the same weights and the oracle."""
+    from test_gpu_sweep import _random_case
+    wl = _random_case(100 + seed)
+    b = datagen.generate(wl, n_users=6)
+    P = datagen.random_params(param_specs(wl.schemas, wl.cfg), seed=seed)
+    m = Model(wl.schemas, wl.cfg, precision="bf16")
+    m.set_params(P)
+    m.prune_projections()
+    assert m.set_sparse_mma(2)
+    sp = m.forward_batch(b)
+    m.set_sparse_mma(0)
+    de = m.forward_batch(b)
+    Pp = {k: (O.prune_2_4(v)[0] if O.is_projection_param(k) else v) for k, v in P.items()}
+    osch, ocfg = to_oracle(wl.schemas, wl.cfg)
+    keys, z_ref, _ = oracle_records(osch, ocfg, Pp, b)
+    assert np.array_equal(np.stack([sp.user_id, sp.scenario_id, sp.exposure_index, sp.task_index], 1), keys)
+    assert float(np.max(np.abs(sp.logit - de.logit))) <= 1e-2
+    assert float(np.max(np.abs(sp.logit - z_ref))) <= 2e-2
