@@ -377,9 +377,12 @@ def main():
         sfu_ops = tfl / (4.0 * dh)
         sfu_peak = 16.0 * 148 * 1.965e9
         sfu_ach = sfu_ops / (tms / 1000.0)
+        ceiling = sfu_peak * 4.0 * dh / (tflops * 1e12)
         roof["sfu"] = {"achieved_Gops": sfu_ach / 1e9, "peak_Gops": sfu_peak / 1e9, "frac": sfu_ach / sfu_peak,
-                       "tensor_ceiling_frac": sfu_peak * 4.0 * dh / (tflops * 1e12),
-                       "note": "SFU-bound at this head dim: the tensor fraction cannot exceed tensor_ceiling_frac"}
+                       "tensor_ceiling_frac": ceiling,
+                       "note": ("SFU-bound at this head dim: the tensor fraction cannot exceed tensor_ceiling_frac"
+                                if ceiling < 1.0 else "tensor-bound at this head dim (the SFU ceiling is above the "
+                                "tensor peak)")}
     total_flops = sum(v[1] for v in stages.values())
     step_tflops = total_flops / (ms / 1000.0) / 1e12
     traffic_path = os.path.join(ROOT, "profiles", "traffic.json")
