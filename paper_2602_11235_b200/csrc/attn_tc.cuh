@@ -371,49 +371,72 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
         }
     } else if (warp >= 4 + C::kSilu) {
         // ------------------------------------------------ epilogue warps
+        // The row's scale / self index of the next tile are fetched a tile ahead, and the
+        // self term's Q, K (and for D <= 32 V) rows are loaded together before the O wait:
+        // one global round trip per tile on the epilogue's critical path instead of three.
+        constexpr bool kVpre = D <= 32;
         const uint32_t q = warp & 3;
         const uint32_t m = q * 32 + lane;
         const uint32_t lane_addr = (q * 32u) << 16;
+        const int hs = m / prm.rt;
+        const int i = m - hs * prm.rt;
+        auto meta_of = [&](int tt, float& sc, int& sr) {
+            sc = 0.f;
+            sr = -1;
+            if (tt < prm.n_tiles) {
+                const AttnTile tl = prm.tiles[tt];
+                if (i < tl.n_rows) {
+                    sc = __ldg(prm.q_scale + tl.q_row0 + i);
+                    sr = __ldg(prm.q_self + tl.q_row0 + i);
+                }
+            }
+        };
+        float scale_next;
+        int self_next;
+        meta_of(blockIdx.x, scale_next, self_next);
         int it = 0;
         for (int t = blockIdx.x; t < prm.n_tiles; t += gridDim.x, ++it) {
             const AttnTile tile = prm.tiles[t];
             const int n_kv = (tile.kmax + BKV - 1) / BKV;
             const int ob = it % kOB;
-            const int hs = m / prm.rt;
-            const int i = m - hs * prm.rt;
             const bool valid = i < tile.n_rows;
             const int qrow = tile.q_row0 + i;
             const int head = tile.head0 + hs;
             const int g = tile.head0 / r_per_g;
+            const float scale = scale_next;
+            const int self_row = self_next;
+            meta_of(t + gridDim.x, scale_next, self_next);
             // self term inputs (T rows) are independent of O: fetch before waiting
-            float scale = 0.f, wself = 0.f;
-            int self_row = -1;
-            if (valid) {
-                scale = __ldg(prm.q_scale + qrow);
-                self_row = __ldg(prm.q_self + qrow);
-                if (self_row >= 0) {
-                    const __nv_bfloat16* qp = prm.q_ptr + (long long)qrow * prm.ldq + prm.q_col0 + head * D;
-                    const __nv_bfloat16* kp = prm.kv_ptr + (long long)self_row * prm.ldkv + prm.k_col0 + g * D;
-                    float dot = 0.f;
-#pragma unroll 4
-                    for (int e = 0; e < D; e += 8) {
-                        const uint4 a = *reinterpret_cast<const uint4*>(qp + e);
-                        const uint4 b = *reinterpret_cast<const uint4*>(kp + e);
-                        const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
-                        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b);
+            float wself = 0.f;
+            uint4 vpre[kVpre ? D / 8 : 1];
+            if (valid && self_row >= 0) {
+                const __nv_bfloat16* qp = prm.q_ptr + (long long)qrow * prm.ldq + prm.q_col0 + head * D;
+                const __nv_bfloat16* kp = prm.kv_ptr + (long long)self_row * prm.ldkv + prm.k_col0 + g * D;
+                if constexpr (kVpre) {
+                    const __nv_bfloat16* vp = prm.kv_ptr + (long long)self_row * prm.ldkv + prm.v_col0 + g * D;
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            const float2 fa = __bfloat1622float2(a2[k]), fb = __bfloat1622float2(b2[k]);
-                            dot = fmaf(fa.x, fb.x, dot);
-                            dot = fmaf(fa.y, fb.y, dot);
-                        }
-                    }
-                    wself = silu_precise(dot);
+                    for (int e = 0; e < D / 8; ++e) vpre[e] = *reinterpret_cast<const uint4*>(vp + 8 * e);
                 }
+                float dot = 0.f;
+#pragma unroll 4
+                for (int e = 0; e < D; e += 8) {
+                    const uint4 a = *reinterpret_cast<const uint4*>(qp + e);
+                    const uint4 b = *reinterpret_cast<const uint4*>(kp + e);
+                    const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
+                    const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const float2 fa = __bfloat1622float2(a2[k]), fb = __bfloat1622float2(b2[k]);
+                        dot = fmaf(fa.x, fb.x, dot);
+                        dot = fmaf(fa.y, fb.y, dot);
+                    }
+                }
+                wself = silu_precise(dot);
             }
             ptx::mbar_wait(&o_full[ob], (it / kOB) & 1);
             ptx::tc_fence_after();
-#pragma unroll 1
+            // fully unrolled when V was preloaded (register-array indices must be constant)
+#pragma unroll(kVpre ? D / 16 : 1)
             for (int c = 0; c < D; c += 16) {
                 float v[16];
                 ptx::tmem_ld16(tmem + lane_addr + kOCol + ob * D + c, v);
@@ -424,10 +447,16 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
                 }
                 if (valid) {
                     if (self_row >= 0) {
-                        const __nv_bfloat16* vp =
-                            prm.kv_ptr + (long long)self_row * prm.ldkv + prm.v_col0 + g * D + c;
-                        const uint4 a = *reinterpret_cast<const uint4*>(vp);
-                        const uint4 b = *reinterpret_cast<const uint4*>(vp + 8);
+                        uint4 a, b;
+                        if constexpr (kVpre) {
+                            a = vpre[c / 8];
+                            b = vpre[c / 8 + 1];
+                        } else {
+                            const __nv_bfloat16* vp =
+                                prm.kv_ptr + (long long)self_row * prm.ldkv + prm.v_col0 + g * D + c;
+                            a = *reinterpret_cast<const uint4*>(vp);
+                            b = *reinterpret_cast<const uint4*>(vp + 8);
+                        }
                         const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
                         const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b);
 #pragma unroll
