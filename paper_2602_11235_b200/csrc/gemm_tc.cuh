@@ -429,16 +429,24 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                     if (p.use_scatter_c) {
                         // row-mapped rows: 8 lanes per 128-byte row segment, 4 rows per pass
                         __syncwarp();
+                        // all eight shared loads and row shuffles first: the global stores may
+                        // alias the generic staging pointer, so interleaving them would serialise
+                        // every load behind the previous store
                         const uint8_t* s0 = reinterpret_cast<const uint8_t*>(stg);
+                        uint4 vals[8];
+                        int orows[8];
 #pragma unroll
                         for (int it = 0; it < 8; ++it) {
                             const int r = it * 4 + sub;
-                            const uint4 val = *reinterpret_cast<const uint4*>(s0 + r * 128 + ((ch ^ (r & 7)) << 4));
-                            const int orow = __shfl_sync(0xffffffffu, my_orow, r);
-                            if (orow >= 0)
-                                *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) +
-                                                          static_cast<long long>(orow) * p.ldo + n0 + ch * 8) = val;
+                            vals[it] = *reinterpret_cast<const uint4*>(s0 + r * 128 + ((ch ^ (r & 7)) << 4));
+                            orows[it] = __shfl_sync(0xffffffffu, my_orow, r);
                         }
+#pragma unroll
+                        for (int it = 0; it < 8; ++it)
+                            if (orows[it] >= 0)
+                                *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) +
+                                                          static_cast<long long>(orows[it]) * p.ldo + n0 + ch * 8) =
+                                    vals[it];
                         ++nstore;
                         continue;
                     }
