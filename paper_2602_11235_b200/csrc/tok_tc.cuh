@@ -216,15 +216,18 @@ __global__ void __launch_bounds__(kTokThreads, 1) tok_fused_kernel(const __grid_
                     ptx::sts128(wst + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4), v[16 * hh + 4 * j],
                                 v[16 * hh + 4 * j + 1], v[16 * hh + 4 * j + 2], v[16 * hh + 4 * j + 3]);
                 __syncwarp();
+                float4 w[4];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const int r = 8 * i + (lane >> 2);
-                    const float4 w = ptx::lds128(wst + r * 64 + ((c4 ^ ((r >> 1) & 3)) << 4));
+                    w[i] = ptx::lds128(wst + r * 64 + ((c4 ^ ((r >> 1) & 3)) << 4));
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
                     if (orow[i] >= 0)
                         __stcs(reinterpret_cast<float4*>(X + static_cast<long long>(orow[i]) * args.ldx + n_off + cb * 32 + hh * 16 +
                                                          c4 * 4),
-                               w);
-                }
+                               w[i]);
                 __syncwarp();
             }
         }
@@ -263,13 +266,17 @@ __global__ void __launch_bounds__(kTokThreads, 1) tok_fused_kernel(const __grid_
                                 __uint_as_float(pack_bf16((v[8 * j + 4] - mean) * rstd, (v[8 * j + 5] - mean) * rstd)),
                                 __uint_as_float(pack_bf16((v[8 * j + 6] - mean) * rstd, (v[8 * j + 7] - mean) * rstd)));
                 __syncwarp();
+                float4 w[4];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const int rr = 8 * i + (lane >> 2);
-                    const float4 w = ptx::lds128(wst + rr * 64 + ((c4 ^ ((rr >> 1) & 3)) << 4));
-                    const int mr = m0 + static_cast<int>(q * 32) + rr;
+                    w[i] = ptx::lds128(wst + rr * 64 + ((c4 ^ ((rr >> 1) & 3)) << 4));
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int mr = m0 + static_cast<int>(q * 32) + 8 * i + (lane >> 2);
                     if (mr < src.M)
-                        *reinterpret_cast<float4*>(args.xhat + (src.xhat_row0 + mr) * D + cb * 32 + c4 * 8) = w;
+                        *reinterpret_cast<float4*>(args.xhat + (src.xhat_row0 + mr) * D + cb * 32 + c4 * 8) = w[i];
                 }
                 __syncwarp();
             }
