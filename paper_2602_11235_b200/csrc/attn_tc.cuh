@@ -70,14 +70,17 @@ struct Cfg {
     static constexpr uint32_t LAYOUT = ROWB == 128 ? 2 : (ROWB == 64 ? 4 : 6);
     static constexpr int Q_BYTES = 128 * D * 2;
     static constexpr int KV_TILE_BYTES = BKV * D * 2;       // one of K or V
-    static constexpr int STAGE_BYTES = 2 * KV_TILE_BYTES;
     static constexpr int P_BYTES = 128 * BKV * 2;
     static constexpr int QB = D <= 64 ? 2 : 1;              // Q buffers
-    // K|V ring as deep as ~200 KB of SMEM allows: the S warp runs ahead of the
-    // PV warp by a few tiles, and TMA latency must hide behind the rest
-    static constexpr int kStagesRaw = (200 * 1024 - QB * Q_BYTES) / STAGE_BYTES;
-    static constexpr int kStages = kStagesRaw > 12 ? 12 : kStagesRaw;
-    static constexpr int SMEM = QB * Q_BYTES + kStages * STAGE_BYTES + 1024 + 512;
+    // separate K and V rings, as deep as SMEM allows (~200 KB for d_h <= 64, everything
+    // for the wide heads): a K slot is refilled as soon as its S = QK^T completed, not
+    // after the P.V of the same key tile, so the S warp's K loads run further ahead
+    static constexpr int BAR_BYTES = 1024;
+    static constexpr int kRingBudget = (D <= 64 ? 200 * 1024 : 227 * 1024 - 1024 - BAR_BYTES) - QB * Q_BYTES;
+    static constexpr int kSlots = kRingBudget / KV_TILE_BYTES;
+    static constexpr int KS = (kSlots + 1) / 2 > 12 ? 12 : (kSlots + 1) / 2;  // K slots
+    static constexpr int VS = kSlots / 2 > 12 ? 12 : kSlots / 2;              // V slots
+    static constexpr int SMEM = QB * Q_BYTES + (KS + VS) * KV_TILE_BYTES + 1024 + BAR_BYTES;
     static constexpr uint32_t TMEM_COLS = 512;
     static constexpr int NB = 3;                            // S/P TMEM buffers (P aliases S)
     static constexpr uint32_t O_COL = NB * BKV;
@@ -133,8 +136,9 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sQ = smem;
-    uint8_t* sKV = sQ + C::QB * C::Q_BYTES;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + C::kStages * C::STAGE_BYTES);
+    uint8_t* sK = sQ + C::QB * C::Q_BYTES;
+    uint8_t* sV = sK + C::KS * C::KV_TILE_BYTES;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sV + C::VS * C::KV_TILE_BYTES);
     uint64_t* q_full = bars + 0;   // [2]
     uint64_t* q_empty = bars + 2;  // [2]
     uint64_t* o_full = bars + 4;   // [2]
@@ -142,9 +146,12 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
     uint64_t* s_full = bars + 8;            // [NB]
     uint64_t* s_empty = bars + 8 + NB;      // [NB] released by the P.V commit
     uint64_t* p_full = bars + 8 + 2 * NB;   // [NB]
-    uint64_t* kv_full = bars + 8 + 3 * NB;  // [kStages]
-    uint64_t* kv_empty = kv_full + C::kStages;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kv_empty + C::kStages);
+    uint64_t* k_full = bars + 8 + 3 * NB;   // [KS]
+    uint64_t* k_empty = k_full + C::KS;     // [KS] released by the S commit
+    uint64_t* v_full = k_empty + C::KS;     // [VS]
+    uint64_t* v_empty = v_full + C::VS;     // [VS] released by the P.V commit
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(v_empty + C::VS);
+    static_assert((8 + 3 * NB + 2 * C::KS + 2 * C::VS) * 8 + 4 <= C::BAR_BYTES, "barrier area");
 
     const uint32_t warp = ptx::warp_id();
     const uint32_t lane = ptx::lane_id();
@@ -162,9 +169,13 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
             ptx::mbar_init(&s_empty[i], 1);
             ptx::mbar_init(&p_full[i], C::kSilu / C::kSiluGroups);
         }
-        for (int i = 0; i < C::kStages; ++i) {
-            ptx::mbar_init(&kv_full[i], 1);
-            ptx::mbar_init(&kv_empty[i], 2);  // S warp (K) + PV warp (V)
+        for (int i = 0; i < C::KS; ++i) {
+            ptx::mbar_init(&k_full[i], 1);
+            ptx::mbar_init(&k_empty[i], 1);
+        }
+        for (int i = 0; i < C::VS; ++i) {
+            ptx::mbar_init(&v_full[i], 1);
+            ptx::mbar_init(&v_empty[i], 1);
         }
         ptx::fence_mbar_init();
         ptx::tma_prefetch(&prm.tma_q);
@@ -198,18 +209,38 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
                         ptx::tma_load_2d(q_dst + sl * (128 * C::ROWB) + hs * prm.rt * C::ROWB, &prm.tma_q, &q_full[qb],
                                          prm.q_col0 + (tile.head0 + hs) * D + sl * C::CHUNK, tile.q_row0);
                 for (int j = 0; j < n_kv; ++j) {
-                    ptx::mbar_wait(&kv_empty[stage], phase ^ 1);
-                    uint8_t* sk = sKV + stage * C::STAGE_BYTES;
-                    uint8_t* sv = sk + C::KV_TILE_BYTES;
-                    ptx::mbar_arrive_expect_tx(&kv_full[stage], C::STAGE_BYTES);
+                    ptx::mbar_wait(&k_empty[stage], phase ^ 1);
+                    uint8_t* sk = sK + stage * C::KV_TILE_BYTES;
+                    ptx::mbar_arrive_expect_tx(&k_full[stage], C::KV_TILE_BYTES);
                     const int row = tile.key_base + j * BKV;
-                    for (int sl = 0; sl < C::SLABS; ++sl) {
-                        ptx::tma_load_2d(sk + sl * (BKV * C::ROWB), &prm.tma_kv, &kv_full[stage],
+                    for (int sl = 0; sl < C::SLABS; ++sl)
+                        ptx::tma_load_2d(sk + sl * (BKV * C::ROWB), &prm.tma_kv, &k_full[stage],
                                          prm.k_col0 + g * D + sl * C::CHUNK, row);
-                        ptx::tma_load_2d(sv + sl * (BKV * C::ROWB), &prm.tma_kv, &kv_full[stage],
-                                         prm.v_col0 + g * D + sl * C::CHUNK, row);
+                    if (++stage == C::KS) {
+                        stage = 0;
+                        phase ^= 1;
                     }
-                    if (++stage == C::kStages) {
+                }
+            }
+        }
+    } else if (warp == 2) {
+        // ------------------------------------------------ V producer (the TMEM allocator warp)
+        if (ptx::elect_one()) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < prm.n_tiles; t += gridDim.x) {
+                const AttnTile tile = prm.tiles[t];
+                const int g = tile.head0 / r_per_g;
+                const int n_kv = (tile.kmax + BKV - 1) / BKV;
+                for (int j = 0; j < n_kv; ++j) {
+                    ptx::mbar_wait(&v_empty[stage], phase ^ 1);
+                    uint8_t* sv = sV + stage * C::KV_TILE_BYTES;
+                    ptx::mbar_arrive_expect_tx(&v_full[stage], C::KV_TILE_BYTES);
+                    const int row = tile.key_base + j * BKV;
+                    for (int sl = 0; sl < C::SLABS; ++sl)
+                        ptx::tma_load_2d(sv + sl * (BKV * C::ROWB), &prm.tma_kv, &v_full[stage],
+                                         prm.v_col0 + g * D + sl * C::CHUNK, row);
+                    if (++stage == C::VS) {
                         stage = 0;
                         phase ^= 1;
                     }
@@ -238,11 +269,11 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
             const uint32_t sq = ptx::smem_u32(sQ + qb * C::Q_BYTES);
             for (int j = 0; j < n_kv; ++j) {
                 const uint32_t buf = s_cnt % NB;
-                ptx::mbar_wait(&kv_full[stage], phase);
+                ptx::mbar_wait(&k_full[stage], phase);
                 ptx::mbar_wait(&s_empty[buf], ((s_cnt / NB) & 1) ^ 1);
                 ptx::tc_fence_after();
                 if (ptx::elect_one()) {
-                    const uint32_t sk = ptx::smem_u32(sKV + stage * C::STAGE_BYTES);
+                    const uint32_t sk = ptx::smem_u32(sK + stage * C::KV_TILE_BYTES);
 #pragma unroll
                     for (int kk = 0; kk < D / 16; ++kk) {
                         const uint32_t sl = (kk * 16) / C::CHUNK;
@@ -253,11 +284,11 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
                     }
                     if (j == n_kv - 1) ptx::umma_commit(&q_empty[qb]);
                     ptx::umma_commit(&s_full[buf]);
-                    ptx::umma_commit(&kv_empty[stage]);  // K consumed (the PV warp releases V)
+                    ptx::umma_commit(&k_empty[stage]);  // K consumed
                 }
                 __syncwarp();
                 ++s_cnt;
-                if (++stage == C::kStages) {
+                if (++stage == C::KS) {
                     stage = 0;
                     phase ^= 1;
                 }
@@ -269,8 +300,7 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
         // delay the next S, and vice versa.
         const uint32_t idesc_o = ptx::instr_desc_bf16(128, D, false, true);
         int stage = 0;
-        uint32_t phase_unused = 0;
-        (void)phase_unused;
+        uint32_t phase = 0;
         uint32_t cnt = 0;
         int it = 0;
         for (int t = blockIdx.x; t < prm.n_tiles; t += gridDim.x, ++it) {
@@ -287,9 +317,10 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
             for (int j = 0; j < n_kv; ++j, ++cnt) {
                 const uint32_t buf = cnt % NB;
                 ptx::mbar_wait(&p_full[buf], (cnt / NB) & 1);
+                ptx::mbar_wait(&v_full[stage], phase);
                 ptx::tc_fence_after();
                 if (ptx::elect_one()) {
-                    const uint32_t sv = ptx::smem_u32(sKV + stage * C::STAGE_BYTES + C::KV_TILE_BYTES);
+                    const uint32_t sv = ptx::smem_u32(sV + stage * C::KV_TILE_BYTES);
                     const uint32_t o_tmem = tmem + kOCol + ob * D;
 #pragma unroll
                     for (int kk = 0; kk < BKV / 16; ++kk) {
@@ -300,12 +331,15 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
                         const uint64_t db = ptx::smem_desc(sv + kk * 16 * C::ROWB, BKV * C::ROWB, 8 * C::ROWB, C::LAYOUT);
                         ptx::umma_bf16_ts(o_tmem, tmem + p_col, db, idesc_o, (j > 0 || kk > 0));
                     }
-                    ptx::umma_commit(&kv_empty[stage]);
+                    ptx::umma_commit(&v_empty[stage]);
                     ptx::umma_commit(&s_empty[buf]);
                     if (j == n_kv - 1) ptx::umma_commit(&o_full[ob]);
                 }
                 __syncwarp();
-                if (++stage == C::kStages) stage = 0;
+                if (++stage == C::VS) {
+                    stage = 0;
+                    phase ^= 1;
+                }
             }
         }
     } else if (warp >= 4 && warp < 4 + C::kSilu) {
