@@ -73,6 +73,8 @@ struct GemmArgs {
     int n_epi;        // epilogue warps: 8, or 12 when BN < 256 (more accumulators than 2 groups)
     int stg_warp;     // epilogue staging bytes per warp: 8 KB (2 fp32 blocks), 4 KB when every problem is a bf16 bulk store
     int bias_bytes;   // BN x 32 B bias tile: after the resident B slice (b_res) or at the end of every stage
+    int cl;           // 2: CTA pairs (clusters) on m-block pairs share each B k-block by TMA multicast
+                      // (streaming schedule, one k-block per stage; tile_start / n_tiles count pairs)
     GemmProblem p[kMaxProblems];
     CtaWork cta[kNumSMs];
 };
@@ -97,12 +99,12 @@ struct Cfg {
 // streaming: global tile t -> (problem, m, n) through the SMEM tile_start table.
 struct TileSeq {
     int t, i, tstep;
-    int b_res, pi0, nb0, m0, mstep, mcount, n_tiles, n_problems;
+    int b_res, pi0, nb0, m0, mstep, mcount, n_tiles, n_problems, cl, rank;
     const int* tile_start;  // SMEM: first global tile of each problem
     const int* tiles_n;     // SMEM: n-blocks of each problem
     __device__ TileSeq(const GemmArgs& a, const int* ts, const int* tn)
-        : t(blockIdx.x), i(0), tstep(gridDim.x), b_res(a.b_res), n_tiles(a.n_tiles), n_problems(a.n_problems),
-          tile_start(ts), tiles_n(tn) {
+        : t(blockIdx.x / a.cl), i(0), tstep(gridDim.x / a.cl), b_res(a.b_res), n_tiles(a.n_tiles),
+          n_problems(a.n_problems), cl(a.cl), rank(blockIdx.x % a.cl), tile_start(ts), tiles_n(tn) {
         const CtaWork w = a.cta[blockIdx.x];
         pi0 = w.pi;
         nb0 = w.nb;
@@ -127,6 +129,7 @@ struct TileSeq {
         const int local = t - tile_start[pi];
         mb = local / tiles_n[pi];
         nb = local - mb * tiles_n[pi];
+        mb = mb * cl + rank;  // cluster: the pair's m-blocks (the second may lie past M: zero-filled, not stored)
         t += tstep;
         return true;
     }
@@ -189,7 +192,7 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
     if (warp == kWarpTma && lane == 0) {
         for (int s = 0; s < n_stages; ++s) {
             ptx::mbar_init(&full_bar[s], 1);
-            ptx::mbar_init(&empty_bar[s], 1);
+            ptx::mbar_init(&empty_bar[s], args.cl);  // the MMA commit of every CTA of the cluster
         }
         ptx::mbar_init(bres_bar, 1);
         for (int s = 0; s < C::kAcc; ++s) {
@@ -206,8 +209,10 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
     if (warp == kWarpAlloc) ptx::tmem_alloc<C::TMEM_COLS>(tmem_slot);
     ptx::tc_fence_before();
     __syncthreads();
+    if (args.cl > 1) ptx::cluster_sync();  // peers' barriers initialised before any multicast
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    const uint32_t cl_rank = args.cl > 1 ? ptx::cluster_ctarank() : 0;
     // prologue done (barriers, TMEM, SMEM tables): wait for the producer of our inputs
     MTFM_PDL_ENTRY();
 
@@ -254,7 +259,11 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                     // one TMA instruction per operand and stage (each costs ~150 clk of issue)
                     if (KS > 1) ptx::tma_load_3d(sa, &p.tma_a, &full_bar[stage], 0, mb * C::BM, kb);
                     else ptx::tma_load_2d(sa, &p.tma_a, &full_bar[stage], kb * C::BK, mb * C::BM);
-                    if (!args.b_res) {
+                    if (args.cl > 1) {
+                        // this CTA's half of the B k-block (BN / 2 rows, box {64, BN / 2}) to both CTAs
+                        ptx::tma_load_2d_mc(sb + cl_rank * (BN / 2) * 128, &p.tma_b, &full_bar[stage], kb * C::BK,
+                                            nb * BN + static_cast<int>(cl_rank) * (BN / 2), 0x3);
+                    } else if (!args.b_res) {
                         if (KS > 1) ptx::tma_load_3d(sb, &p.tma_b, &full_bar[stage], 0, nb * BN, kb);
                         else ptx::tma_load_2d(sb, &p.tma_b, &full_bar[stage], kb * C::BK, nb * BN);
                     }
@@ -311,7 +320,8 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
                         ptx::umma_bf16(d_tmem, ptx::smem_desc(ptx::smem_u32(ones), 16, 256, 6),
                                        ptx::smem_desc(sbias, 16, 256, 6), idesc, 1u);
                     }
-                    ptx::umma_commit(&empty_bar[stage]);
+                    if (args.cl > 1) ptx::umma_commit_mc(&empty_bar[stage], 0x3);
+                    else ptx::umma_commit(&empty_bar[stage]);
                     if (last) ptx::umma_commit(&tfull_bar[acc]);
                 }
                 __syncwarp();
@@ -615,6 +625,7 @@ __global__ void __launch_bounds__(512, 1) gemm_tc_kernel(const __grid_constant__
     }
     ptx::tc_fence_before();
     __syncthreads();
+    if (args.cl > 1) ptx::cluster_sync();  // no CTA leaves while its peer may still multicast or arrive
     if (warp == kWarpAlloc) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc<C::TMEM_COLS>(tmem_base);

@@ -803,6 +803,55 @@ void finalize(mtfm_cuda_model& m) {
 // ---------------------------------------------------------------- GEMM launch helpers
 
 template <int BN>
+int gemm_smem_bytes(const GemmArgs& a) {
+    return 1024 + a.bres_bytes + 4096 + a.n_stages * a.stage_bytes + a.n_epi * a.stg_warp +
+           gemm_detail::Cfg<BN>::BAR_BYTES;
+}
+
+template <int BN>
+cudaLaunchConfig_t gemm_cluster_cfg(const GemmArgs& a, int grid, cudaStream_t st) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(gemm_detail::Cfg<BN>::kThreads);
+    cfg.dynamicSmemBytes = static_cast<size_t>(gemm_smem_bytes<BN>(a));
+    cfg.stream = st;
+    return cfg;
+}
+
+bool gemm_pairs_enabled() {
+    static const bool on = std::getenv("MTFM_GEMM_PAIRS") == nullptr || std::atoi(std::getenv("MTFM_GEMM_PAIRS")) != 0;
+    return on;
+}
+
+// co-resident CTAs of a pair launch (clusters of two never straddle a GPC)
+template <int BN>
+int gemm_pair_slots(const GemmArgs& a) {
+    using C = gemm_detail::Cfg<BN>;
+    static std::map<int, int> by_smem;  // occupancy depends only on the SMEM size
+    const auto hit = by_smem.find(gemm_smem_bytes<BN>(a));
+    if (hit != by_smem.end()) return hit->second;
+    static bool attr = false;
+    if (!attr) {
+        ck(cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kMaxSmem),
+           "gemm smem attr");
+        attr = true;
+    }
+    cudaLaunchConfig_t cfg = gemm_cluster_cfg<BN>(a, kNumSMs, nullptr);
+    cudaLaunchAttribute la[1];
+    la[0].id = cudaLaunchAttributeClusterDimension;
+    la[0].val.clusterDim.x = 2;
+    la[0].val.clusterDim.y = 1;
+    la[0].val.clusterDim.z = 1;
+    cfg.attrs = la;
+    cfg.numAttrs = 1;
+    int n = 0;
+    ck(cudaOccupancyMaxActiveClusters(&n, gemm_tc_kernel<BN>, &cfg), "gemm cluster occupancy");
+    if (n < 1) fail(MTFM_CUDA_ERROR, "gemm clusters cannot be scheduled");
+    by_smem[gemm_smem_bytes<BN>(a)] = 2 * n;
+    return 2 * n;
+}
+
+template <int BN>
 void launch_gemm_tc_bn(GemmArgs& a, int grid, cudaStream_t st) {
     using C = gemm_detail::Cfg<BN>;
     static bool attr = false;
@@ -811,8 +860,22 @@ void launch_gemm_tc_bn(GemmArgs& a, int grid, cudaStream_t st) {
            "gemm smem attr");
         attr = true;
     }
-    const int smem = 1024 + a.bres_bytes + 4096 + a.n_stages * a.stage_bytes + a.n_epi * a.stg_warp + C::BAR_BYTES;
+    const int smem = gemm_smem_bytes<BN>(a);
     if (smem > C::kMaxSmem) fail(MTFM_CONTRACT_ERROR, "gemm smem plan exceeds 227 KB");
+    if (a.cl > 1) {
+        cudaLaunchConfig_t cfg = gemm_cluster_cfg<BN>(a, grid, st);
+        cudaLaunchAttribute la[2];
+        la[0].id = cudaLaunchAttributeClusterDimension;
+        la[0].val.clusterDim.x = static_cast<unsigned>(a.cl);
+        la[0].val.clusterDim.y = 1;
+        la[0].val.clusterDim.z = 1;
+        la[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        la[1].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = la;
+        cfg.numAttrs = 2;
+        ck(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN>, a), "gemm_tc cluster launch");
+        return;
+    }
     launch_k(gemm_tc_kernel<BN>, dim3(grid), dim3(C::kThreads), smem, st, a);
     ck(cudaGetLastError(), "gemm_tc launch");
 }
@@ -951,6 +1014,7 @@ void run_gemm_tc(std::vector<TcProblem> ps, cudaStream_t st, long long& launches
         const size_t i1 = std::min(ps.size(), i0 + kMaxProblems);
         GemmArgs a;
         std::memset(&a, 0, sizeof(a));
+        a.cl = 1;
         // ---- schedule
         int bn = bn_res;
         int grid = 0;
@@ -1090,6 +1154,21 @@ void run_gemm_tc(std::vector<TcProblem> ps, cudaStream_t st, long long& launches
             if (a.n_stages >= 3) break;
         }
         if (a.n_stages < 2) fail(MTFM_CONTRACT_ERROR, "gemm pipeline does not fit in SMEM");
+        // streamed BN = 256 GEMMs with more tiles than SMs: CTA pairs on m-block pairs load
+        // half of each B k-block each and multicast it (L2 -> SMEM bytes per k-block 48 -> 32 KB)
+        if (!a.b_res && bn == 256 && a.stage_kb == 1 && tiles > 2 * kNumSMs && gemm_pairs_enabled()) {
+            int pt = 0;
+            for (int i = 0; i < a.n_problems; ++i) {
+                GemmProblem& p = a.p[i];
+                const auto& s = ps[i0 + i];
+                p.tile_start = pt;
+                pt += static_cast<int>(cdiv(cdiv(p.M, 128), 2)) * p.tiles_n;
+                p.tma_b = tma_2d(s.Bt, s.N, s.K, s.ldb, 64, bn / 2, 128);
+            }
+            a.n_tiles = pt;
+            a.cl = 2;
+            grid = std::min(2 * pt, gemm_pair_slots<256>(a));
+        }
         if (bn == 256) launch_gemm_tc_bn<256>(a, grid, st);
         else if (bn == 128) launch_gemm_tc_bn<128>(a, grid, st);
         else launch_gemm_tc_bn<64>(a, grid, st);
