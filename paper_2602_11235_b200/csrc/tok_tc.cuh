@@ -73,8 +73,8 @@ constexpr int W1S_BYTES = W1_BYTES + B1C_BYTES;     // W1 stage (multiple of 1 K
 constexpr int W2_BYTES = D * 64 * 2;                // 32 KB
 constexpr int kXStages = 2, kWStages = 3;
 constexpr int ONES_BYTES = 4096;
-// staging: 2 KB per Y warp (32 rows x 64 B of Y or x̂), then the x̂ partial-sum exchange
-constexpr int STG_BYTES = 8 * 2048;
+// staging: 4 KB per Y warp (32 rows x 128 B of Y; 64 B of x̂), then the x̂ partial-sum exchange
+constexpr int STG_BYTES = 8 * 4096;
 constexpr int XCH_BYTES = 2 * 128 * 8;
 constexpr int BAR_BYTES = 1024;
 constexpr int SMEM = 1024 + kXStages * XS_BYTES + kWStages * (W1S_BYTES + W2_BYTES) + ONES_BYTES + STG_BYTES +
@@ -173,12 +173,13 @@ __global__ void __launch_bounds__(kTokThreads, 1) tok_fused_kernel(const __grid_
         tok_detail::decode(args, t, s, m0, n_off);
         const TokSource& src = args.s[s];
         const uint32_t slot = grp * 4 + q;
-        const uint32_t wst = ptx::smem_u32(stg) + slot * 2048u;
-        const int c4 = lane & 3;         // 16 B chunk of a 64 B row segment (store phase)
-        int orow[4];                     // store phase rows 8i + lane / 4 of the warp's 32
+        const uint32_t wst = ptx::smem_u32(stg) + slot * 4096u;
+        const int c4 = lane & 3;         // 16 B chunk of a 64 B x̂ row segment (store phase)
+        const int c8 = lane & 7;         // 16 B chunk of a 128 B X row segment (store phase)
+        int orow[8];                     // X store phase rows 4i + lane / 8 of the warp's 32
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int m = m0 + static_cast<int>(q * 32) + 8 * i + (lane >> 2);
+        for (int i = 0; i < 8; ++i) {
+            const int m = m0 + static_cast<int>(q * 32) + 4 * i + (lane >> 3);
             orow[i] = m < src.M ? __ldg(src.row_map + m) : -1;
         }
         float* const X = args.X;
@@ -209,27 +210,24 @@ __global__ void __launch_bounds__(kTokThreads, 1) tok_fused_kernel(const __grid_
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(y_empty);  // Y is free for the next tile's GEMM2
             }
+            // row r = lane, 16 B chunk j at (j ^ (r & 7)); then 8 lanes per row: four whole
+            // 128 B row segments per store instruction
 #pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
+            for (int j = 0; j < 8; ++j)
+                ptx::sts128(wst + lane * 128 + ((j ^ (lane & 7)) << 4), v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            __syncwarp();
+            float4 w[8];
 #pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    ptx::sts128(wst + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4), v[16 * hh + 4 * j],
-                                v[16 * hh + 4 * j + 1], v[16 * hh + 4 * j + 2], v[16 * hh + 4 * j + 3]);
-                __syncwarp();
-                float4 w[4];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const int r = 8 * i + (lane >> 2);
-                    w[i] = ptx::lds128(wst + r * 64 + ((c4 ^ ((r >> 1) & 3)) << 4));
-                }
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    if (orow[i] >= 0)
-                        __stcs(reinterpret_cast<float4*>(X + static_cast<long long>(orow[i]) * args.ldx + n_off + cb * 32 + hh * 16 +
-                                                         c4 * 4),
-                               w[i]);
-                __syncwarp();
+            for (int i = 0; i < 8; ++i) {
+                const int r = 4 * i + (lane >> 3);
+                w[i] = ptx::lds128(wst + r * 128 + ((c8 ^ (r & 7)) << 4));
             }
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                if (orow[i] >= 0)
+                    __stcs(reinterpret_cast<float4*>(X + static_cast<long long>(orow[i]) * args.ldx + n_off + cb * 32 + c8 * 4),
+                           w[i]);
+            __syncwarp();
         }
         if (xh) {
             // whole-row statistics from the two halves (same summation order in both warps)
