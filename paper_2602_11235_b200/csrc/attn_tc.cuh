@@ -467,14 +467,8 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
                 }
                 wself = silu_precise(dot);
             }
-            ptx::mbar_wait(&o_full[ob], (it / kOB) & 1);
-            ptx::tc_fence_after();
-            // fully unrolled when V was preloaded (register-array indices must be constant)
-#pragma unroll(kVpre ? D / 16 : 1)
-            for (int c = 0; c < D; c += 16) {
-                float v[16];
-                ptx::tmem_ld16(tmem + lane_addr + kOCol + ob * D + c, v);
-                ptx::tmem_ld_wait();
+            // one 16-column chunk of O: x scale (+ the self term), bf16, stored
+            auto emit = [&](float (&v)[16], const int c) {
                 if (n_kv == 0) {
 #pragma unroll
                     for (int e = 0; e < 16; ++e) v[e] = 0.f;
@@ -515,10 +509,34 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
                     reinterpret_cast<uint4*>(o)[0] = w0;
                     reinterpret_cast<uint4*>(o)[1] = w1;
                 }
+            };
+            // O is read out two chunks at a time: the next chunk's TMEM load is in flight while
+            // this one is scaled and stored, and O goes back to the PV warp right after the last
+            // load (before the last chunk's stores)
+            auto release = [&]() {
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&o_empty[ob]);
+            };
+            ptx::mbar_wait(&o_full[ob], (it / kOB) & 1);
+            ptx::tc_fence_after();
+            float v0[16], v1[16];
+            ptx::tmem_ld16(tmem + lane_addr + kOCol + ob * D, v0);
+            // fully unrolled when V was preloaded (register-array indices must be constant)
+#pragma unroll(kVpre ? (D + 31) / 32 : 1)
+            for (int c = 0; c < D; c += 32) {
+                ptx::tmem_ld_wait_dep(v0);
+                const bool two = c + 16 < D;
+                if (two) ptx::tmem_ld16(tmem + lane_addr + kOCol + ob * D + c + 16, v1);
+                else release();
+                emit(v0, c);
+                if (two) {
+                    ptx::tmem_ld_wait_dep(v1);
+                    if (c + 32 < D) ptx::tmem_ld16(tmem + lane_addr + kOCol + ob * D + c + 32, v0);
+                    else release();
+                    emit(v1, c + 16);
+                }
             }
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&o_empty[ob]);
         }
     }
     ptx::tc_fence_before();
