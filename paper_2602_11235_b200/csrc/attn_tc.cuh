@@ -468,23 +468,13 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
                 wself = silu_precise(dot);
             }
             // one 16-column chunk of O: x scale (+ the self term), bf16, stored
-            auto emit = [&](float (&v)[16], const int c) {
+            auto emit = [&](float (&v)[16], const int c, const uint4 a, const uint4 b) {
                 if (n_kv == 0) {
 #pragma unroll
                     for (int e = 0; e < 16; ++e) v[e] = 0.f;
                 }
                 if (valid) {
                     if (self_row >= 0) {
-                        uint4 a, b;
-                        if constexpr (kVpre) {
-                            a = vpre[c / 8];
-                            b = vpre[c / 8 + 1];
-                        } else {
-                            const __nv_bfloat16* vp =
-                                prm.kv_ptr + (long long)self_row * prm.ldkv + prm.v_col0 + g * D + c;
-                            a = *reinterpret_cast<const uint4*>(vp);
-                            b = *reinterpret_cast<const uint4*>(vp + 8);
-                        }
                         const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
                         const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b);
 #pragma unroll
@@ -518,6 +508,19 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&o_empty[ob]);
             };
+            // the self row's V columns of a chunk (T rows), fetched with the chunk's TMEM load
+            auto vload = [&](const int c, uint4& a, uint4& b) {
+                if constexpr (kVpre) {
+                    a = vpre[c / 8];
+                    b = vpre[c / 8 + 1];
+                } else if (valid && self_row >= 0) {
+                    const __nv_bfloat16* vp = prm.kv_ptr + (long long)self_row * prm.ldkv + prm.v_col0 + g * D + c;
+                    a = *reinterpret_cast<const uint4*>(vp);
+                    b = *reinterpret_cast<const uint4*>(vp + 8);
+                }
+            };
+            uint4 a0 = make_uint4(0, 0, 0, 0), b0 = a0, a1 = a0, b1 = a0;
+            vload(0, a0, b0);
             ptx::mbar_wait(&o_full[ob], (it / kOB) & 1);
             ptx::tc_fence_after();
             float v0[16], v1[16];
@@ -527,14 +530,22 @@ __global__ void __launch_bounds__(768, 1) attn_tc_kernel(const __grid_constant__
             for (int c = 0; c < D; c += 32) {
                 ptx::tmem_ld_wait_dep(v0);
                 const bool two = c + 16 < D;
-                if (two) ptx::tmem_ld16(tmem + lane_addr + kOCol + ob * D + c + 16, v1);
-                else release();
-                emit(v0, c);
+                if (two) {
+                    ptx::tmem_ld16(tmem + lane_addr + kOCol + ob * D + c + 16, v1);
+                    vload(c + 16, a1, b1);
+                } else {
+                    release();
+                }
+                emit(v0, c, a0, b0);
                 if (two) {
                     ptx::tmem_ld_wait_dep(v1);
-                    if (c + 32 < D) ptx::tmem_ld16(tmem + lane_addr + kOCol + ob * D + c + 32, v0);
-                    else release();
-                    emit(v1, c + 16);
+                    if (c + 32 < D) {
+                        ptx::tmem_ld16(tmem + lane_addr + kOCol + ob * D + c + 32, v0);
+                        vload(c + 32, a0, b0);
+                    } else {
+                        release();
+                    }
+                    emit(v1, c + 16, a1, b1);
                 }
             }
         }
