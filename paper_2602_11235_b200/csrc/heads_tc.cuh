@@ -302,6 +302,7 @@ __global__ void __launch_bounds__(heads_detail::kThreads, 1) heads_tc_kernel(con
                         for (int i = 0; i < 8; ++i) act[i] = ptx::silu_fast(v[8 * p8 + i] + bv[i]);
 #pragma unroll
                         for (int k = 0; k < kHeadsMaxTasks; ++k) {
+                            if (k >= ntasks) break;  // the row's scenario has fewer towers
                             const float4 w0 = ptx::lds128(tw[k] + static_cast<uint32_t>(j) * 4u);
                             const float4 w1 = ptx::lds128(tw[k] + static_cast<uint32_t>(j + 4) * 4u);
                             const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
