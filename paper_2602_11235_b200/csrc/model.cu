@@ -1187,11 +1187,16 @@ void run_gemm_simt(std::vector<SimtGemm> ps, cudaStream_t st, long long& launche
 }
 
 // ---------------------------------------------------------------- attention helpers
-__global__ void tile_kmax_kernel(AttnTile* tiles, int n, const int* prefix, int rt_unused) {
+// max mask prefix over each tile's rows, for the full-layer table (tiles [0, na)) and the
+// target-layer table (tiles [na, na + nb)) in one launch
+__global__ void tile_kmax_kernel(AttnTile* ta, int na, const int* pa, AttnTile* tb, int nb, const int* pb) {
     MTFM_PDL_ENTRY();
-    const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
-    if (t >= n) return;
+    if (t >= na + nb) return;
+    AttnTile* tiles = t < na ? ta : tb;
+    const int* prefix = t < na ? pa : pb;
+    if (t >= na) t -= na;
     AttnTile tl = tiles[t];
     int mx = 0;
     for (int i = lane; i < tl.n_rows; i += 32) mx = max(mx, prefix[tl.q_row0 + i]);
@@ -1776,16 +1781,11 @@ void run_forward(mtfm_cuda_model& m, mtfm_cuda_batch& B) {
     const int n_tgt = static_cast<int>(B.n_tiles_tgt);
     if (kTc && (n_full || n_tgt)) {
         StageScope sc(m, "tile_kmax", 0, (n_full + n_tgt) * 32.0);
-        if (n_full) {
-            tile_kmax_kernel<<<static_cast<int>(cdiv(n_full, 8)), 256, 0, st>>>(B.tiles_full.as<AttnTile>(), n_full,
-                                                                                rm.prefix, ag.rt);
-            ++L;
-        }
-        if (n_tgt) {
-            tile_kmax_kernel<<<static_cast<int>(cdiv(n_tgt, 8)), 256, 0, st>>>(B.tiles_tgt.as<AttnTile>(), n_tgt,
-                                                                               rm.prefix + NE, ag.rt);
-            ++L;
-        }
+        launch_k(tile_kmax_kernel, dim3(static_cast<unsigned>(cdiv(n_full + n_tgt, 8))), dim3(256), 0, st,
+                 B.tiles_full.as<AttnTile>(), n_full, static_cast<const int*>(rm.prefix), B.tiles_tgt.as<AttnTile>(),
+                 n_tgt, static_cast<const int*>(rm.prefix + NE));
+        ck(cudaGetLastError(), "tile_kmax launch");
+        ++L;
     }
 
     // ---- K2..K4: the HTA stack (hta.hpp:188-212)
