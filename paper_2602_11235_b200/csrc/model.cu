@@ -2587,7 +2587,9 @@ mtfm_status mtfm_cuda_batch_run(mtfm_cuda_model* m, mtfm_cuda_batch* b) {
         if (!m || !b) fail(MTFM_CONTRACT_ERROR, "null argument");
         if (!m->finalized) fail(MTFM_CONTRACT_ERROR, "parameters changed after prepare; prepare the batch again");
         ck(cudaSetDevice(m->device), "cudaSetDevice");
-        ck(cudaStreamWaitEvent(m->stream, b->ev_h2d, 0), "wait uploads");
+        // prepare() returns once its uploads completed: a stream wait is only needed if they
+        // have not (the wait would also cut the programmatic launch overlap with the previous forward)
+        if (cudaEventQuery(b->ev_h2d) != cudaSuccess) ck(cudaStreamWaitEvent(m->stream, b->ev_h2d, 0), "wait uploads");
         if (m->precision == MTFM_PRECISION_BF16)
             run_forward<__nv_bfloat16>(*m, *b);
         else
